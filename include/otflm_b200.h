@@ -1,0 +1,211 @@
+/*
+ * otflm_b200.h -- C-ABI of the B200-native on-the-fly RNNLM rescoring path.
+ *
+ * Drop-in boundary for the reference package ``otflm`` (Python, numba
+ * kernels).  Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/otflm/).  The Python host
+ * mirror ``paper_2007_11794_b200`` binds these with ctypes; INTEGRATION.md
+ * shows the stub the reference side would add.
+ *
+ * Conventions
+ *  - Every function returns an int status: OTFLM_OK (0) or a negative code
+ *    that the host shim maps 1:1 onto the reference's exceptions.
+ *  - "dev" pointers are CUDA device pointers (e.g. torch tensors'
+ *    data_ptr()); "host" pointers are ordinary host memory.  Plain pointers
+ *    and sizes only -- no torch types cross this boundary.
+ *  - ``stream`` is a cudaStream_t passed as void*; all device work is
+ *    enqueued asynchronously on it (functions with host outputs synchronize
+ *    it before returning).
+ *  - A model handle is immutable and may be shared by any number of stream
+ *    sets.  A stream set is single-writer.
+ */
+#ifndef OTFLM_B200_H
+#define OTFLM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OTFLM_OK 0
+#define OTFLM_ERR_VALUE (-1)          /* ValueError (rnnlm.py:173-177, decoder.py:123-124) */
+#define OTFLM_ERR_UNKNOWN_INDEX (-2)  /* context_table.UnknownIndexError (:36-37) */
+#define OTFLM_ERR_TABLE_FULL (-3)     /* context_table.TableFullError (:40-41) */
+#define OTFLM_ERR_NO_PATH (-4)        /* decoder.py:155-156 */
+#define OTFLM_ERR_KEY (-5)            /* ngram.py:179 KeyError */
+#define OTFLM_ERR_NOMEM (-6)
+#define OTFLM_ERR_CYCLE (-7)          /* lattice.LatticeFormatError (lattice.py:86-87) */
+#define OTFLM_ERR_PACK (-8)           /* codec.PackOverflowError (codec.py:31-46) */
+#define OTFLM_ERR_CUDA (-9)
+#define OTFLM_ERR_HASH (-10)          /* 64-bit content-digest collision detected */
+
+/* Precision of the recurrent update h' = sigmoid(U[w] + W h). */
+#define OTFLM_PREC_FP64 0    /* CUDA-core DFMA, reference summation order (exact mode) */
+#define OTFLM_PREC_TF32X3 1  /* tcgen05 kind::tf32, 3-pass split (fp32-faithful) */
+#define OTFLM_PREC_BF16 2    /* tcgen05 kind::f16 with bf16 operands */
+#define OTFLM_PREC_TF32 3    /* tcgen05 kind::tf32, single pass */
+
+typedef struct OtflmModel OtflmModel;
+typedef struct OtflmNgram OtflmNgram;
+typedef struct OtflmStreams OtflmStreams;
+typedef struct OtflmPlan OtflmPlan;
+
+/* ---- model upload (replaces handing numpy arrays to otflm.kernels;
+ *      RnnlmModel rnnlm.py:69-124 + HuffmanTree huffman.py:40-51) ------- */
+/* Any weight pointer may be NULL when only some kernels are needed (the
+ * reference-signature operator table uploads just what a call uses);
+ * decoding streams require a complete model. */
+typedef struct {
+    int32_t hidden_size, vocab_size, maxent_order;
+    uint64_t maxent_size, hash_seed;
+    const float *input_weights;     /* host [V, H] */
+    const float *recurrent_weights; /* host [H, H] */
+    const float *node_vectors;      /* host [V-1, H] */
+    const float *maxent_table;      /* host [maxent_size] */
+    const int32_t *path_nodes;      /* host [n_path] */
+    const float *path_signs;        /* host [n_path] (+1 / -1) */
+    const int64_t *path_offsets;    /* host [V+1] */
+    int64_t n_path;
+} OtflmModelDesc;
+
+int otflm_model_create(const OtflmModelDesc *desc, int32_t device, OtflmModel **out);
+int otflm_model_destroy(OtflmModel *m);
+/* device-resident row pointers of the uploaded weights (read-only) */
+int otflm_model_info(const OtflmModel *m, int64_t *out8);
+
+/* ---- small LM (NgramModel ngram.py:34-46; lookup ngram.py:161-179) ---- */
+typedef struct {
+    int32_t order, vocab_size, bos_id;
+    int64_t n_probs;
+    const int32_t *prob_keys;   /* host [n_probs, order] (row-padded) */
+    const int32_t *prob_lens;   /* host [n_probs] */
+    const double *prob_vals;    /* host [n_probs] natural log */
+    int64_t n_backoffs;
+    const int32_t *bow_keys;    /* host [n_backoffs, order] */
+    const int32_t *bow_lens;
+    const double *bow_vals;
+} OtflmNgramDesc;
+
+int otflm_ngram_create(const OtflmNgramDesc *desc, const OtflmModel *m, OtflmNgram **out);
+int otflm_ngram_destroy(OtflmNgram *g);
+/* ngram_logprob for n (context, word) pairs; ctx dev [n, order-1] padded
+ * with <s> on the left by the caller, out dev double [n]. */
+int otflm_ngram_logprob_batch(const OtflmNgram *g, int64_t n, const int32_t *ctx_dev,
+                              const int32_t *w_dev, double *out_dev, void *stream);
+
+/* ---- kernel table (otflm.kernels, kernels.py:30-36), batched ---------- */
+/* feature_index (_kernels_nb.py:21-33): words dev [n, 8] (first order_k
+ * used), order_k / node dev [n]; out dev uint64 [n]. */
+int otflm_feature_index_batch(uint64_t seed, uint64_t mask, int64_t n, const int32_t *order_k_dev,
+                              const int64_t *words_dev, const int64_t *node_dev,
+                              uint64_t *out_dev, void *stream);
+/* word_logprob (_kernels_nb.py:78-86 via rnnlm.py:195-204): per query the
+ * hidden row h_dev[ctx[i]], history hist_dev[ctx[i], 0:hist_len[ctx[i]]]
+ * (oldest first), word w_dev[i]; out dev double [n]. */
+int otflm_word_logprob_batch(const OtflmModel *m, int64_t n, const int32_t *ctx_dev,
+                             const float *h_dev, const int32_t *hist_dev,
+                             const int32_t *hist_len_dev, const int32_t *w_dev,
+                             double *out_dev, void *stream);
+/* word_logprob with explicit path slices (the reference kernel signature,
+ * _kernels_nb.py:78-79): query i scores path_code[path_off[i]..path_off[i+1])
+ * where code = node | (branch bit << 31). */
+int otflm_word_logprob_paths(const OtflmModel *m, int64_t n, const int32_t *ctx_dev,
+                             const float *h_dev, const int32_t *hist_dev,
+                             const int32_t *hist_len_dev, const int64_t *path_off_dev,
+                             const uint32_t *path_code_dev, double *out_dev, void *stream);
+/* advance_hidden (_kernels_nb.py:51-60 via rnnlm.py:180-188):
+ * h_out[i] = f32(sigmoid(U[w[i]] + W h_in[ctx[i]])). */
+int otflm_advance_hidden_batch(const OtflmModel *m, int64_t n, const int32_t *ctx_dev,
+                               const float *h_in_dev, const int32_t *w_dev, float *h_out_dev,
+                               int32_t precision, void *stream);
+/* advance_hidden with the input rows given explicitly (the reference
+ * signature advance_hidden(input_row, recurrent, hidden)): input_rows dev [n, H]. */
+int otflm_advance_hidden_rows(const OtflmModel *m, int64_t n, const float *input_rows_dev,
+                              const int32_t *ctx_dev, const float *h_in_dev, float *h_out_dev,
+                              int32_t precision, void *stream);
+/* all_word_logprobs (_kernels_nb.py:89-104) for one context; out dev [V]. */
+int otflm_all_word_logprobs(const OtflmModel *m, const float *h_dev, const int32_t *hist_host,
+                            int32_t hist_len, double *out_dev, void *stream);
+
+/* ---- decoding streams: IndexTable + RescoreCache + ledger per stream
+ *      (context_table.py:48-119, cache.py:61-191, codec.py:95-110) ------ */
+typedef struct {
+    int32_t n_streams;
+    int32_t cache_enabled;       /* RescoreCache(enabled=...) cache.py:84-86 */
+    int64_t max_contexts;        /* per stream IndexTable(max_entries) */
+    int64_t cache_slots;         /* per stream (power of two, >= 2x entries) */
+    int64_t arena_rows;          /* total hidden-state rows across streams */
+} OtflmStreamConfig;
+
+int otflm_streams_create(const OtflmModel *m, const OtflmStreamConfig *cfg, OtflmStreams **out);
+int otflm_streams_destroy(OtflmStreams *s);
+/* reset_utterance (cache.py:185-191) for every stream. */
+int otflm_streams_reset(OtflmStreams *s, int32_t retain, void *stream);
+/* per stream 8 counters: lookups, hits, misses, table_len, cum_lookups,
+ * cum_hits, cum_misses, cache_entries.  out host int64 [n_streams * 8]. */
+int otflm_streams_stats(OtflmStreams *s, int64_t *out_host, void *stream);
+/* IndexTable.decode (context_table.py:88-104): hidden host [H], hist host
+ * [order], *len. */
+int otflm_streams_context(OtflmStreams *s, int32_t stream_id, uint32_t idx, float *hidden_host,
+                          int32_t *hist_host, int32_t *len_host, void *stream);
+/* rnnlm_prob (cache.py:165-182) for a batch of n requests with the
+ * semantics of issuing them one by one in array order: a (c, w) repeated
+ * inside the batch is a miss the first time and a hit afterwards; new
+ * context indices are assigned len+1 in array order.  Every c must exist
+ * before the call.  All pointers host; outputs p [n], c_next [n], hit [n]. */
+int otflm_rnnlm_prob_batch(OtflmStreams *s, int64_t n, const int32_t *stream_ids,
+                           const uint32_t *c, const int32_t *w, int32_t precision, double *p,
+                           uint32_t *c_next, uint8_t *hit, void *stream);
+
+/* ---- decoder: rescore_onthefly (decoder.py:114-173) over a batch of
+ *      utterances, one stream each ------------------------------------- */
+typedef struct {
+    int32_t n_utt;
+    const int32_t *n_nodes;      /* [n_utt]; node ids are 0..n_nodes-1 */
+    const int32_t *start;        /* [n_utt] */
+    const int64_t *arc_off;      /* [n_utt+1] into the arc arrays (arc-id order) */
+    const int32_t *arc_src, *arc_dst, *arc_word;
+    const double *arc_ac, *arc_slm;
+    const int64_t *final_off;    /* [n_utt+1] */
+    const int32_t *finals;       /* ascending per utterance */
+    const int32_t *stream_ids;   /* [n_utt] stream of each utterance */
+} OtflmLatticeBatch;
+
+typedef struct {
+    int32_t *path_len;        /* [n_utt] */
+    int32_t *path_arcs;       /* [n_utt * max_path] */
+    int32_t max_path;
+    double *combined, *acoustic, *lm; /* [n_utt] */
+    int64_t *end_ctx, *expansions;    /* [n_utt] */
+    int32_t *status;          /* [n_utt] per utterance OTFLM_* code */
+} OtflmDecodeResult;
+
+/* Host-side compile (topological levels, per-node beam capacities, arrival
+ * slots) and upload of a lattice batch; plan is reusable for repeated runs. */
+int otflm_plan_create(OtflmStreams *s, const OtflmLatticeBatch *lats, int64_t beam,
+                      OtflmPlan **out, void *stream);
+int otflm_plan_destroy(OtflmPlan *p);
+/* plan stats: levels, nodes, arcs, slots, max requests per level, total
+ * request slots, graph nodes (int64 [8]) */
+int otflm_plan_info(const OtflmPlan *p, int64_t *out8);
+/* Device-only decode of a prepared plan (inputs already resident in HBM).
+ * use_graph != 0 replays a captured CUDA graph of the level loop. */
+int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
+                     int32_t use_graph, void *stream);
+/* Copy results of the last run to host (synchronizes). */
+int otflm_decode_fetch(OtflmPlan *p, OtflmDecodeResult *res, void *stream);
+/* End to end: plan_create + decode_run + decode_fetch + plan_destroy. */
+int otflm_decode(OtflmStreams *s, const OtflmNgram *g, const OtflmLatticeBatch *lats,
+                 double lm_weight, int64_t beam, int32_t precision, OtflmDecodeResult *res,
+                 void *stream);
+/* number of kernels the last decode_run enqueued */
+int64_t otflm_last_launch_count(void);
+
+const char *otflm_error_string(int32_t code);
+const char *otflm_last_error_detail(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

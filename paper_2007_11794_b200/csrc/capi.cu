@@ -1,0 +1,1126 @@
+// capi.cu -- C-ABI of libotflm_b200.so (declared in include/otflm_b200.h):
+// model / small-LM upload, per-stream device tables, the host lattice
+// compiler (topological levels, per-node beam capacities, arrival slots) and
+// the level loop (captured once into a CUDA graph and replayed).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "../../include/otflm_b200.h"
+#include "common.cuh"
+#include "decode.cuh"
+#include "hs.cuh"
+#include "tc_advance.cuh"
+
+// --------------------------------------------------------------------------
+static thread_local std::string g_detail;
+static thread_local int64_t g_launches = 0;
+
+#define CK(x)                                                                    \
+    do {                                                                         \
+        cudaError_t _e = (x);                                                    \
+        if (_e != cudaSuccess) {                                                 \
+            g_detail = std::string(#x) + ": " + cudaGetErrorString(_e);          \
+            return OTFLM_ERR_CUDA;                                               \
+        }                                                                        \
+    } while (0)
+#define CKL()                                                                    \
+    do {                                                                         \
+        g_launches++;                                                            \
+        cudaError_t _e = cudaGetLastError();                                     \
+        if (_e != cudaSuccess) {                                                 \
+            g_detail = std::string("launch: ") + cudaGetErrorString(_e);         \
+            return OTFLM_ERR_CUDA;                                               \
+        }                                                                        \
+    } while (0)
+
+static inline uint32_t pow2_at_least(uint64_t x) {
+    uint64_t c = 16;
+    while (c < x) c <<= 1;
+    return (uint32_t)c;
+}
+static inline unsigned cdiv(uint64_t a, uint64_t b) { return (unsigned)((a + b - 1) / b); }
+
+struct Allocs {
+    std::vector<void *> ptrs;
+    template <class T>
+    cudaError_t alloc(T **p, size_t count) {
+        void *q = nullptr;
+        cudaError_t e = cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T));
+        if (e == cudaSuccess) { ptrs.push_back(q); *p = (T *)q; }
+        return e;
+    }
+    void free_all() {
+        for (void *p : ptrs) cudaFree(p);
+        ptrs.clear();
+    }
+};
+
+// ==========================================================================
+// model
+// ==========================================================================
+struct OtflmModel {
+    DevModel d;
+    int device;
+    Allocs mem;
+    int64_t n_path;
+};
+
+__global__ void k_prep_weights(DevModel m, float *WT, float *W_hi, float *W_lo, __nv_bfloat16 *W_bf) {
+    const int64_t HH = (int64_t)m.H * m.H;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < HH; t += (int64_t)gridDim.x * blockDim.x) {
+        int i = (int)(t / m.H), j = (int)(t % m.H);
+        float w = m.W[t];
+        WT[(int64_t)j * m.H + i] = w;
+        // tf32 split: hi = round-to-nearest tf32 (10-bit mantissa), lo = rest
+        uint32_t b = __float_as_uint(w);
+        uint32_t r = (b + 0x1000u) & 0xFFFFE000u;
+        float hi = __uint_as_float(r);
+        float lo = w - hi;
+        uint32_t lb = (__float_as_uint(lo) + 0x1000u) & 0xFFFFE000u;
+        W_hi[t] = hi;
+        W_lo[t] = __uint_as_float(lb);
+        W_bf[t] = __float2bfloat16_rn(w);
+    }
+}
+
+extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, OtflmModel **out) {
+    if (!d || !out) return OTFLM_ERR_VALUE;
+    if (d->hidden_size < 1 || d->vocab_size < 2 || d->maxent_order < 1 ||
+        d->maxent_order > OTF_MAX_ORDER || d->maxent_size < 1 ||
+        (d->maxent_size & (d->maxent_size - 1))) {
+        g_detail = "bad model geometry";
+        return OTFLM_ERR_VALUE;
+    }
+    CK(cudaSetDevice(device));
+    OtflmModel *m = new OtflmModel();
+    m->device = device;
+    const int H = d->hidden_size, V = d->vocab_size;
+    m->n_path = d->n_path;
+    DevModel &dm = m->d;
+    dm.H = H; dm.V = V; dm.order = d->maxent_order;
+    dm.mask = d->maxent_size - 1; dm.seed = d->hash_seed;
+    float *U = nullptr, *W = nullptr, *WT = nullptr, *NV = nullptr, *ME = nullptr, *Whi = nullptr, *Wlo = nullptr;
+    __nv_bfloat16 *Wbf = nullptr;
+    uint32_t *poff = nullptr, *pcode = nullptr;
+    const size_t VH = (size_t)V * H, HH = (size_t)H * H;
+    // every weight block is optional (the reference-signature kernel calls
+    // upload only what they use); the decoder requires all of them
+#define AL(p, n) if (m->mem.alloc(&p, n) != cudaSuccess) { m->mem.free_all(); delete m; g_detail = "cudaMalloc model"; return OTFLM_ERR_NOMEM; }
+    if (d->input_weights) { AL(U, VH); CK(cudaMemcpy(U, d->input_weights, VH * 4, cudaMemcpyHostToDevice)); }
+    if (d->recurrent_weights) {
+        AL(W, HH); AL(WT, HH); AL(Whi, HH); AL(Wlo, HH); AL(Wbf, HH);
+        CK(cudaMemcpy(W, d->recurrent_weights, HH * 4, cudaMemcpyHostToDevice));
+    }
+    if (d->node_vectors) { AL(NV, (size_t)(V - 1) * H); CK(cudaMemcpy(NV, d->node_vectors, (size_t)(V - 1) * H * 4, cudaMemcpyHostToDevice)); }
+    if (d->maxent_table) { AL(ME, d->maxent_size); CK(cudaMemcpy(ME, d->maxent_table, d->maxent_size * 4, cudaMemcpyHostToDevice)); }
+    if (d->path_offsets && d->n_path >= 0) {
+        AL(poff, (size_t)V + 1); AL(pcode, (size_t)std::max<int64_t>(d->n_path, 1));
+        std::vector<uint32_t> off(V + 1), code(std::max<int64_t>(d->n_path, 1));
+        for (int w = 0; w <= V; w++) off[w] = (uint32_t)d->path_offsets[w];
+        if (off[V] != (uint64_t)d->n_path) { m->mem.free_all(); delete m; g_detail = "path_offsets[V] != n_path"; return OTFLM_ERR_VALUE; }
+        for (int64_t p = 0; p < d->n_path; p++) {
+            if (d->path_nodes[p] < 0 || d->path_nodes[p] >= V - 1) { m->mem.free_all(); delete m; g_detail = "bad path node"; return OTFLM_ERR_VALUE; }
+            code[p] = (uint32_t)d->path_nodes[p] | (d->path_signs[p] < 0.f ? 0x80000000u : 0u);
+        }
+        CK(cudaMemcpy(poff, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(pcode, code.data(), (size_t)std::max<int64_t>(d->n_path, 1) * 4, cudaMemcpyHostToDevice));
+    }
+#undef AL
+    if (W) {
+        k_prep_weights<<<256, 256>>>(dm, WT, Whi, Wlo, Wbf);
+        CK(cudaGetLastError());
+    }
+    CK(cudaDeviceSynchronize());
+    *out = m;
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_model_destroy(OtflmModel *m) {
+    if (!m) return OTFLM_OK;
+    cudaSetDevice(m->device);
+    m->mem.free_all();
+    delete m;
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_model_info(const OtflmModel *m, int64_t *o) {
+    if (!m || !o) return OTFLM_ERR_VALUE;
+    o[0] = m->d.H; o[1] = m->d.V; o[2] = m->d.order; o[3] = (int64_t)(m->d.mask + 1);
+    o[4] = (int64_t)(uintptr_t)m->d.U; o[5] = (int64_t)(uintptr_t)m->d.NV;
+    o[6] = (int64_t)(uintptr_t)m->d.ME; o[7] = m->n_path;
+    return OTFLM_OK;
+}
+
+// ==========================================================================
+// small LM
+// ==========================================================================
+struct OtflmNgram {
+    DevNgram d;
+    Allocs mem;
+};
+
+static int build_ng_table(int order, int64_t n, const int32_t *keys, const int32_t *lens,
+                          const double *vals, uint32_t &cap, std::vector<uint64_t> &tag,
+                          std::vector<int32_t> &words, std::vector<double> &val) {
+    const int width = order + 1;
+    cap = pow2_at_least((uint64_t)std::max<int64_t>(n, 1) * 2);
+    tag.assign(cap, 0);
+    words.assign((size_t)cap * width, 0);
+    val.assign(cap, 0.0);
+    for (int64_t r = 0; r < n; r++) {
+        const int len = lens[r];
+        if (len < 0 || len > order) return OTFLM_ERR_VALUE;
+        const int32_t *k = keys + r * order;
+        uint64_t h = otf_tuple_hash(k, len);
+        uint32_t s = (uint32_t)(h >> 7) & (cap - 1);
+        for (;;) {
+            if (tag[s] == 0) break;
+            if (tag[s] == h && words[(size_t)s * width] == len &&
+                std::equal(k, k + len, &words[(size_t)s * width + 1]))
+                break;   // duplicate key: last one wins (dict semantics)
+            s = (s + 1) & (cap - 1);
+        }
+        tag[s] = h;
+        words[(size_t)s * width] = len;
+        for (int i = 0; i < len; i++) words[(size_t)s * width + 1 + i] = k[i];
+        val[s] = vals[r];
+    }
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_ngram_create(const OtflmNgramDesc *d, const OtflmModel *m, OtflmNgram **out) {
+    if (!d || !out) return OTFLM_ERR_VALUE;
+    if (d->order < 1 || d->order > OTF_MAX_ORDER) { g_detail = "small LM order out of range"; return OTFLM_ERR_VALUE; }
+    if (m && d->order - 1 > m->d.order) {
+        g_detail = "small LM order exceeds the stored context history";   // decoder.py:87-90
+        return OTFLM_ERR_VALUE;
+    }
+    OtflmNgram *g = new OtflmNgram();
+    g->d.order = d->order; g->d.V = d->vocab_size; g->d.bos = d->bos_id;
+    std::vector<uint64_t> pt, bt;
+    std::vector<int32_t> pw, bw;
+    std::vector<double> pv, bv;
+    int rc = build_ng_table(d->order, d->n_probs, d->prob_keys, d->prob_lens, d->prob_vals, g->d.p_cap, pt, pw, pv);
+    if (!rc) rc = build_ng_table(d->order, d->n_backoffs, d->bow_keys, d->bow_lens, d->bow_vals, g->d.b_cap, bt, bw, bv);
+    if (rc) { delete g; g_detail = "bad n-gram key length"; return rc; }
+    uint64_t *dpt, *dbt; int32_t *dpw, *dbw; double *dpv, *dbv;
+    if (g->mem.alloc(&dpt, pt.size()) || g->mem.alloc(&dpw, pw.size()) || g->mem.alloc(&dpv, pv.size()) ||
+        g->mem.alloc(&dbt, bt.size()) || g->mem.alloc(&dbw, bw.size()) || g->mem.alloc(&dbv, bv.size())) {
+        g->mem.free_all(); delete g; return OTFLM_ERR_NOMEM;
+    }
+    CK(cudaMemcpy(dpt, pt.data(), pt.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dpw, pw.data(), pw.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dpv, pv.data(), pv.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dbt, bt.data(), bt.size() * 8, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dbw, bw.data(), bw.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dbv, bv.data(), bv.size() * 8, cudaMemcpyHostToDevice));
+    g->d.p_tag = dpt; g->d.p_words = dpw; g->d.p_val = dpv;
+    g->d.b_tag = dbt; g->d.b_words = dbw; g->d.b_val = dbv;
+    *out = g;
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_ngram_destroy(OtflmNgram *g) {
+    if (!g) return OTFLM_OK;
+    g->mem.free_all();
+    delete g;
+    return OTFLM_OK;
+}
+
+__global__ void k_ngram_batch(DevNgram g, int64_t n, const int32_t *ctx, const int32_t *w, double *out,
+                              unsigned int *err) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t hist[OTF_MAX_ORDER];
+    int L = g.order - 1;
+    for (int k = 0; k < L; k++) hist[k] = (uint32_t)ctx[i * (g.order > 1 ? g.order - 1 : 1) + k];
+    double v;
+    if (w[i] < 0 || w[i] >= g.V) { atomicOr(err, OTF_E_VALUE); out[i] = 0; return; }
+    if (!ngram_logprob_dev(g, hist, L, w[i], &v)) { atomicOr(err, OTF_E_KEY); v = 0; }
+    out[i] = v;
+}
+
+static unsigned int *scratch_err() {
+    static unsigned int *p = nullptr;
+    if (!p) cudaMalloc(&p, 4);
+    return p;
+}
+
+extern "C" int otflm_ngram_logprob_batch(const OtflmNgram *g, int64_t n, const int32_t *ctx, const int32_t *w,
+                                         double *out, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned int *err = scratch_err();
+    CK(cudaMemsetAsync(err, 0, 4, s));
+    if (n > 0) { k_ngram_batch<<<cdiv(n, 256), 256, 0, s>>>(g->d, n, ctx, w, out, err); CKL(); }
+    unsigned int he = 0;
+    CK(cudaMemcpyAsync(&he, err, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (he & OTF_E_VALUE) return OTFLM_ERR_VALUE;
+    if (he & OTF_E_KEY) return OTFLM_ERR_KEY;
+    return OTFLM_OK;
+}
+
+// ==========================================================================
+// kernel table
+// ==========================================================================
+extern "C" int otflm_feature_index_batch(uint64_t seed, uint64_t mask, int64_t n, const int32_t *order_k,
+                                         const int64_t *words, const int64_t *node, uint64_t *out, void *stream) {
+    if (n <= 0) return OTFLM_OK;
+    k_feature_index<<<cdiv(n, 256), 256, 0, (cudaStream_t)stream>>>(seed, mask, n, order_k, words, node, out);
+    CKL();
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_word_logprob_batch(const OtflmModel *m, int64_t n, const int32_t *ctx, const float *h,
+                                        const int32_t *hist, const int32_t *hist_len, const int32_t *w,
+                                        double *out, void *stream) {
+    if (n <= 0) return OTFLM_OK;
+    if (!m->d.NV || !m->d.ME || !m->d.path_off) { g_detail = "model has no output layer"; return OTFLM_ERR_VALUE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    const unsigned blocks = cdiv(n, 8);
+#define CALL(VEC, CPL) k_word_logprob_batch<VEC, CPL><<<blocks, 256, 0, s>>>(m->d, n, ctx, h, hist, hist_len, w, out)
+    HS_DISPATCH(m->d.H, CALL);
+#undef CALL
+    CKL();
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_word_logprob_paths(const OtflmModel *m, int64_t n, const int32_t *ctx, const float *h,
+                                        const int32_t *hist, const int32_t *hist_len, const int64_t *path_off,
+                                        const uint32_t *path_code, double *out, void *stream) {
+    if (n <= 0) return OTFLM_OK;
+    if (!m->d.NV || !m->d.ME) { g_detail = "model has no output layer"; return OTFLM_ERR_VALUE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    const unsigned blocks = cdiv(n, 8);
+#define CALL(VEC, CPL) k_word_logprob_paths<VEC, CPL><<<blocks, 256, 0, s>>>(m->d, n, ctx, h, hist, hist_len, path_off, path_code, out)
+    HS_DISPATCH(m->d.H, CALL);
+#undef CALL
+    CKL();
+    return OTFLM_OK;
+}
+
+static int launch_advance(const DevModel &m, int prec, uint32_t n_cap, const uint32_t *n_dev,
+                          const int32_t *in_row, const int32_t *words, const float *h_base, float *out_base,
+                          const uint32_t *out_row0, cudaStream_t s) {
+    if (n_cap == 0) return OTFLM_OK;
+    if (prec == OTFLM_PREC_FP64) {
+        constexpr int QT = 16;
+        const size_t smem = (size_t)QT * m.H * sizeof(float);
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_advance_f64<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dim3 grid(cdiv(n_cap, QT), cdiv(m.H, 256));
+        k_advance_f64<QT><<<grid, 256, smem, s>>>(m, n_cap, n_dev, in_row, words, h_base, out_base, out_row0);
+        CKL();
+        return OTFLM_OK;
+    }
+    int rc = tc_advance_launch(m, prec, n_cap, n_dev, in_row, words, h_base, out_base, out_row0, s);
+    if (rc == OTFLM_OK) g_launches++;
+    else g_detail = "tcgen05 advance launch failed";
+    return rc;
+}
+
+extern "C" int otflm_advance_hidden_batch(const OtflmModel *m, int64_t n, const int32_t *ctx, const float *h_in,
+                                          const int32_t *w, float *h_out, int32_t precision, void *stream) {
+    if (n <= 0) return OTFLM_OK;
+    if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    if (!m->d.U || !m->d.W) { g_detail = "model has no recurrent weights"; return OTFLM_ERR_VALUE; }
+    return launch_advance(m->d, precision, (uint32_t)n, nullptr, ctx, w, h_in, h_out, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int otflm_advance_hidden_rows(const OtflmModel *m, int64_t n, const float *input_rows, const int32_t *ctx,
+                                         const float *h_in, float *h_out, int32_t precision, void *stream) {
+    if (n <= 0) return OTFLM_OK;
+    if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    if (!m->d.W) { g_detail = "model has no recurrent weights"; return OTFLM_ERR_VALUE; }
+    DevModel dm = m->d;
+    dm.U = input_rows;   // row i is the input row of query i
+    return launch_advance(dm, precision, (uint32_t)n, nullptr, ctx, nullptr, h_in, h_out, nullptr, (cudaStream_t)stream);
+}
+
+// all_word_logprobs: activations of every internal node, then path sums
+template <int VEC, int CPL>
+__global__ void k_all_acts(DevModel m, const float *h, const uint32_t *hist, int L, double *acts) {
+    const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (j >= m.V - 1) return;
+    const int H = m.H;
+    const int NCH = VEC == 4 ? H / 4 : H;
+    double a = 0.0;
+    const float *row = m.NV + (size_t)j * H;
+    for (int k = lane; k < NCH; k += 32) {
+        if (VEC == 4) {
+            float4 t = reinterpret_cast<const float4 *>(row)[k];
+            float4 hh = reinterpret_cast<const float4 *>(h)[k];
+            a = fma((double)t.x, (double)hh.x, a); a = fma((double)t.y, (double)hh.y, a);
+            a = fma((double)t.z, (double)hh.z, a); a = fma((double)t.w, (double)hh.w, a);
+        } else {
+            a = fma((double)row[k], (double)h[k], a);
+        }
+    }
+    a = warp_sum_d(a);
+    if (lane == 0) {
+        const int kmax = m.order < L ? m.order : L;
+        for (int k = 1; k <= kmax; k++) {
+            uint64_t x = otf_mix(m.seed, (uint64_t)k);
+            for (int i = L - k; i < L; i++) x = otf_mix(x, (uint64_t)hist[i]);
+            x = otf_mix(x, (uint64_t)j);
+            a += (double)m.ME[x & m.mask];
+        }
+        acts[j] = a;
+    }
+}
+
+__global__ void k_all_paths(DevModel m, const double *acts, double *out) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= m.V) return;
+    double lp = 0.0;
+    for (uint32_t p = m.path_off[w]; p < m.path_off[w + 1]; p++) {
+        uint32_t c = m.path_code[p];
+        double a = acts[c & 0x7FFFFFFFu];
+        lp += otf_log_sigmoid((c & 0x80000000u) ? -a : a);
+    }
+    out[w] = lp;
+}
+
+extern "C" int otflm_all_word_logprobs(const OtflmModel *m, const float *h, const int32_t *hist_host,
+                                       int32_t hist_len, double *out, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    if (hist_len < 0 || hist_len > OTF_MAX_ORDER) return OTFLM_ERR_VALUE;
+    double *acts; uint32_t *dh;
+    CK(cudaMallocAsync(&acts, sizeof(double) * (size_t)(m->d.V - 1 + 1), s));
+    CK(cudaMallocAsync(&dh, sizeof(uint32_t) * OTF_MAX_ORDER, s));
+    uint32_t hh[OTF_MAX_ORDER] = {0};
+    for (int i = 0; i < hist_len; i++) hh[i] = (uint32_t)hist_host[i];
+    CK(cudaMemcpyAsync(dh, hh, sizeof(hh), cudaMemcpyHostToDevice, s));
+    const unsigned blocks = cdiv((uint64_t)m->d.V - 1, 8);
+#define CALL(VEC, CPL) k_all_acts<VEC, CPL><<<blocks, 256, 0, s>>>(m->d, h, dh, hist_len, acts)
+    HS_DISPATCH(m->d.H, CALL);
+#undef CALL
+    CKL();
+    k_all_paths<<<cdiv(m->d.V, 256), 256, 0, s>>>(m->d, acts, out);
+    CKL();
+    CK(cudaFreeAsync(acts, s));
+    CK(cudaFreeAsync(dh, s));
+    CK(cudaStreamSynchronize(s));
+    return OTFLM_OK;
+}
+
+// ==========================================================================
+// streams
+// ==========================================================================
+struct OtflmStreams {
+    const OtflmModel *m;
+    DevStreams d;
+    Allocs mem;
+    OtflmPlan *scratch = nullptr;   // workspace for rnnlm_prob_batch
+};
+
+__global__ void k_streams_reset(DevStreams S, int retain) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < (uint64_t)S.S) {
+        unsigned long long *st = S.stats + t * 8;
+        st[3] += st[0]; st[4] += st[1]; st[5] += st[2];
+        st[0] = st[1] = st[2] = 0;
+        if (!retain) { st[6] = 0; S.table_len[t] = 0; S.novel_cnt[t] = 0; S.ctx_row[t * (S.max_ctx + 1)] = 0; }
+    }
+    if (t == 0 && !retain) {
+        *S.arena_used = 1;
+        for (int i = 0; i < OTF_META; i++) S.arena_meta[i] = 0;
+    }
+    if (!retain && t < (uint64_t)S.H) S.arena_h[t] = 0.f;   // row 0 = zero context
+}
+
+static int streams_clear(OtflmStreams *s, int retain, cudaStream_t st) {
+    DevStreams &d = s->d;
+    if (!retain) {
+        const size_t nct = (size_t)d.S * d.ct_cap, nkc = (size_t)d.S * d.kc_cap;
+        CK(cudaMemsetAsync(d.ct_key, 0, nct * 8, st));
+        CK(cudaMemsetAsync(d.ct_claim, 0xFF, nct * 4, st));
+        CK(cudaMemsetAsync(d.ct_idx, 0xFF, nct * 4, st));
+        CK(cudaMemsetAsync(d.kc_key, 0, nkc * 8, st));
+        CK(cudaMemsetAsync(d.kc_claim, 0xFF, nkc * 4, st));
+        CK(cudaMemsetAsync(d.kc_cnext, 0xFF, nkc * 4, st));
+    }
+    uint64_t n = std::max<uint64_t>((uint64_t)d.S, (uint64_t)d.H);
+    k_streams_reset<<<cdiv(n, 256), 256, 0, st>>>(d, retain);
+    CKL();
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_streams_create(const OtflmModel *m, const OtflmStreamConfig *cfg, OtflmStreams **out) {
+    if (!m || !cfg || !out || cfg->n_streams < 1 || cfg->max_contexts < 1 || cfg->arena_rows < 2)
+        return OTFLM_ERR_VALUE;
+    if (!m->d.U || !m->d.W || !m->d.NV || !m->d.ME || !m->d.path_off) {
+        g_detail = "decoding streams need a complete model";
+        return OTFLM_ERR_VALUE;
+    }
+    if (cfg->max_contexts >= 0xFFFFFFF0ll || cfg->arena_rows >= 0xFFFFFFF0ll) return OTFLM_ERR_VALUE;
+    OtflmStreams *s = new OtflmStreams();
+    s->m = m;
+    DevStreams &d = s->d;
+    d.S = cfg->n_streams; d.enabled = cfg->cache_enabled ? 1 : 0;
+    d.H = m->d.H; d.order = m->d.order;
+    d.max_ctx = (uint32_t)cfg->max_contexts;
+    d.arena_rows = (uint32_t)cfg->arena_rows;
+    d.ct_cap = pow2_at_least((uint64_t)cfg->max_contexts * 2 + 2);
+    d.kc_cap = pow2_at_least((uint64_t)std::max<int64_t>(cfg->cache_slots, 16));
+    const size_t S = d.S;
+    bool bad = false;
+    bad |= s->mem.alloc(&d.ctx_row, S * (d.max_ctx + 1)) != cudaSuccess;
+    bad |= s->mem.alloc(&d.arena_h, (size_t)d.arena_rows * d.H) != cudaSuccess;
+    bad |= s->mem.alloc(&d.arena_meta, (size_t)d.arena_rows * OTF_META) != cudaSuccess;
+    bad |= s->mem.alloc(&d.arena_used, 1) != cudaSuccess;
+    bad |= s->mem.alloc(&d.ct_key, S * d.ct_cap) != cudaSuccess;
+    bad |= s->mem.alloc(&d.ct_claim, S * d.ct_cap) != cudaSuccess;
+    bad |= s->mem.alloc(&d.ct_idx, S * d.ct_cap) != cudaSuccess;
+    bad |= s->mem.alloc(&d.ct_row, S * d.ct_cap) != cudaSuccess;
+    bad |= s->mem.alloc(&d.kc_key, S * d.kc_cap) != cudaSuccess;
+    bad |= s->mem.alloc(&d.kc_claim, S * d.kc_cap) != cudaSuccess;
+    bad |= s->mem.alloc(&d.kc_cnext, S * d.kc_cap) != cudaSuccess;
+    bad |= s->mem.alloc(&d.kc_p, S * d.kc_cap) != cudaSuccess;
+    bad |= s->mem.alloc(&d.table_len, S) != cudaSuccess;
+    bad |= s->mem.alloc(&d.novel_cnt, S) != cudaSuccess;
+    bad |= s->mem.alloc(&d.stats, S * 8) != cudaSuccess;
+    bad |= s->mem.alloc(&d.err, 1) != cudaSuccess;
+    if (bad) { s->mem.free_all(); delete s; g_detail = "cudaMalloc streams"; return OTFLM_ERR_NOMEM; }
+    CK(cudaMemset(d.stats, 0, S * 8 * 8));
+    CK(cudaMemset(d.err, 0, 4));
+    CK(cudaMemset(d.arena_meta, 0, (size_t)OTF_META * 4));
+    int rc = streams_clear(s, 0, 0);
+    if (rc) return rc;
+    CK(cudaDeviceSynchronize());
+    *out = s;
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_plan_destroy(OtflmPlan *p);
+
+extern "C" int otflm_streams_destroy(OtflmStreams *s) {
+    if (!s) return OTFLM_OK;
+    if (s->scratch) otflm_plan_destroy(s->scratch);
+    s->mem.free_all();
+    delete s;
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_streams_reset(OtflmStreams *s, int32_t retain, void *stream) {
+    if (!s) return OTFLM_ERR_VALUE;
+    return streams_clear(s, retain, (cudaStream_t)stream);
+}
+
+static int check_err(OtflmStreams *s, cudaStream_t st) {
+    unsigned int he = 0;
+    CK(cudaMemcpyAsync(&he, s->d.err, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (he) {
+        CK(cudaMemsetAsync(s->d.err, 0, 4, st));
+        CK(cudaStreamSynchronize(st));
+        if (he & OTF_E_HASH) { g_detail = "content digest collision"; return OTFLM_ERR_HASH; }
+        if (he & (OTF_E_TABLE_FULL | OTF_E_ARENA_FULL | OTF_E_CACHE_FULL)) {
+            g_detail = (he & OTF_E_ARENA_FULL) ? "hidden-state arena full"
+                     : (he & OTF_E_CACHE_FULL) ? "cache table full" : "index table full";
+            return OTFLM_ERR_TABLE_FULL;
+        }
+        if (he & OTF_E_KEY) { g_detail = "word missing from unigram table"; return OTFLM_ERR_KEY; }
+        if (he & OTF_E_VALUE) return OTFLM_ERR_VALUE;
+        return OTFLM_ERR_CUDA;
+    }
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_streams_stats(OtflmStreams *s, int64_t *out, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t S = s->d.S;
+    std::vector<unsigned long long> raw(S * 8);
+    std::vector<uint32_t> tl(S);
+    CK(cudaMemcpyAsync(raw.data(), s->d.stats, S * 64, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(tl.data(), s->d.table_len, S * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (size_t i = 0; i < S; i++) {
+        const unsigned long long *r = &raw[i * 8];
+        int64_t *o = out + i * 8;
+        o[0] = r[0]; o[1] = r[1]; o[2] = r[2]; o[3] = tl[i];
+        o[4] = r[3] + r[0]; o[5] = r[4] + r[1]; o[6] = r[5] + r[2]; o[7] = r[6];
+    }
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_streams_context(OtflmStreams *s, int32_t sid, uint32_t idx, float *hidden, int32_t *hist,
+                                     int32_t *len, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (sid < 0 || sid >= s->d.S) return OTFLM_ERR_VALUE;
+    uint32_t tl = 0;
+    CK(cudaMemcpyAsync(&tl, s->d.table_len + sid, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (idx > tl) { g_detail = "index not in table"; return OTFLM_ERR_UNKNOWN_INDEX; }
+    uint32_t row = 0;
+    CK(cudaMemcpyAsync(&row, s->d.ctx_row + (size_t)sid * (s->d.max_ctx + 1) + idx, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    uint32_t meta[OTF_META];
+    CK(cudaMemcpyAsync(hidden, s->d.arena_h + (size_t)row * s->d.H, (size_t)s->d.H * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(meta, s->d.arena_meta + (size_t)row * OTF_META, sizeof(meta), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *len = (int32_t)meta[0];
+    for (uint32_t i = 0; i < meta[0] && i < OTF_MAX_ORDER; i++) hist[i] = (int32_t)meta[1 + i];
+    return OTFLM_OK;
+}
+
+// ==========================================================================
+// plan: compiled lattice batch + level loop
+// ==========================================================================
+struct OtflmPlan {
+    OtflmStreams *st = nullptr;
+    int64_t beam = 0;
+    uint32_t n_utt = 0, n_levels = 0, n_nodes = 0, n_arcs = 0, n_slots = 0, R_max = 0;
+    uint64_t total_req = 0;
+    std::vector<uint32_t> lvl_node_off, lvl_req;   // host copies
+    DevPlan d{};
+    Allocs mem;
+    unsigned long long *scan_status = nullptr;     // [levels][2][nb]
+    uint32_t *scan_ticket = nullptr;               // [levels][2]
+    uint32_t scan_nb = 1;
+    cudaGraphExec_t gexec = nullptr;
+    cudaGraph_t graph = nullptr;
+    double g_lm = 0; int g_prec = -1; const OtflmNgram *g_ng = nullptr; int64_t g_nodes = 0;
+    std::vector<uint32_t> utt_stream_host;
+};
+
+struct HostNode { uint32_t local; };
+
+static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam, int V,
+                         std::vector<NodeInfo> &nodes, std::vector<uint32_t> &level_nodes,
+                         std::vector<uint32_t> &out_list, std::vector<uint32_t> &arc_slot,
+                         std::vector<int32_t> &arc_word, std::vector<double> &arc_ac,
+                         std::vector<double> &arc_slm, std::vector<uint32_t> &start_slot,
+                         std::vector<uint32_t> &final_off, std::vector<uint32_t> &finals,
+                         std::vector<uint32_t> &utt_stream) {
+    const int U = L->n_utt;
+    std::vector<std::vector<std::vector<uint32_t>>> lv(U);   // per utt: levels -> global nodes
+    uint64_t node_base = 0, slot_base = 0;
+    final_off.assign(1, 0);
+    const uint64_t n_arcs_total = (uint64_t)L->arc_off[U];
+    arc_slot.assign(n_arcs_total, 0);
+    arc_word.assign(L->arc_word, L->arc_word + n_arcs_total);
+    arc_ac.assign(L->arc_ac, L->arc_ac + n_arcs_total);
+    arc_slm.assign(L->arc_slm, L->arc_slm + n_arcs_total);
+    out_list.assign(n_arcs_total, 0);
+    std::vector<int> seen_stream(L->stream_ids ? 0 : 0);
+    for (int u = 0; u < U; u++) {
+        const int N = L->n_nodes[u];
+        const int64_t a0 = L->arc_off[u], a1 = L->arc_off[u + 1];
+        const int start = L->start[u];
+        if (N < 1 || start < 0 || start >= N) { g_detail = "bad start node"; return OTFLM_ERR_VALUE; }
+        std::vector<uint32_t> out_cnt(N + 1, 0), indeg(N, 0);
+        for (int64_t a = a0; a < a1; a++) {
+            int s = L->arc_src[a], d = L->arc_dst[a], w = L->arc_word[a];
+            if (s < 0 || s >= N || d < 0 || d >= N) { g_detail = "arc node out of range"; return OTFLM_ERR_VALUE; }
+            if (w < 0 || w >= V) { g_detail = "word id out of range"; return OTFLM_ERR_VALUE; }
+            out_cnt[s + 1]++;
+            indeg[d]++;
+        }
+        for (int n = 0; n < N; n++) out_cnt[n + 1] += out_cnt[n];
+        std::vector<uint32_t> fill(out_cnt.begin(), out_cnt.end() - 1);
+        std::vector<uint32_t> out_loc(std::max<int64_t>(a1 - a0, 1));
+        for (int64_t a = a0; a < a1; a++) out_loc[fill[L->arc_src[a]]++] = (uint32_t)a;
+        for (int64_t k = 0; k < a1 - a0; k++) out_list[a0 + k] = out_loc[k];
+        // Kahn, smallest id first (lattice.py:68-82)
+        std::priority_queue<int, std::vector<int>, std::greater<int>> ready;
+        for (int n = 0; n < N; n++) if (indeg[n] == 0) ready.push(n);
+        std::vector<int> topo;
+        topo.reserve(N);
+        while (!ready.empty()) {
+            int n = ready.top(); ready.pop();
+            topo.push_back(n);
+            for (uint32_t k = out_cnt[n]; k < out_cnt[n + 1]; k++) {
+                int d = L->arc_dst[out_loc[k]];
+                if (--indeg[d] == 0) ready.push(d);
+            }
+        }
+        if ((int)topo.size() != N) { g_detail = "lattice contains a cycle"; return OTFLM_ERR_CYCLE; }
+        // greedy levels: contiguous runs of the topological order with no
+        // internal arc
+        std::vector<int> lvl(N, -1), predmax(N, -1);
+        int cur = 0;
+        for (int n : topo) {
+            if (predmax[n] >= cur) cur++;
+            lvl[n] = cur;
+            for (uint32_t k = out_cnt[n]; k < out_cnt[n + 1]; k++) {
+                int d = L->arc_dst[out_loc[k]];
+                predmax[d] = std::max(predmax[d], cur);
+            }
+        }
+        // capacities: distinct tokens at a node <= arrivals <= sum of the
+        // sources' kept tokens; the start token occupies slot 0 of start.
+        std::vector<uint64_t> cap(N, 0), keep(N, 0);
+        std::vector<uint32_t> arc_off_in(a1 - a0 + 1, 0);
+        cap[start] = 1;
+        for (int n : topo) {
+            keep[n] = std::min<uint64_t>((uint64_t)beam, cap[n]);
+            for (uint32_t k = out_cnt[n]; k < out_cnt[n + 1]; k++) {
+                uint32_t a = out_loc[k];
+                int d = L->arc_dst[a];
+                arc_off_in[a - a0] = (uint32_t)cap[d];
+                cap[d] += keep[n];
+                if (cap[d] > (1ull << 30)) { g_detail = "token capacity explodes (beam too wide for this lattice)"; return OTFLM_ERR_NOMEM; }
+            }
+        }
+        std::vector<uint64_t> sbase(N);
+        for (int n = 0; n < N; n++) { sbase[n] = slot_base; slot_base += cap[n]; }
+        if (slot_base > 0xF0000000ull) { g_detail = "too many arrival slots"; return OTFLM_ERR_NOMEM; }
+        for (int64_t a = a0; a < a1; a++) arc_slot[a] = (uint32_t)(sbase[L->arc_dst[a]] + arc_off_in[a - a0]);
+        start_slot.push_back((uint32_t)sbase[start]);
+        const uint32_t sid = L->stream_ids ? (uint32_t)L->stream_ids[u] : (uint32_t)u;
+        utt_stream.push_back(sid);
+        const uint32_t nb = (uint32_t)node_base;
+        for (int n = 0; n < N; n++) {
+            NodeInfo ni;
+            ni.slot_base = (uint32_t)sbase[n];
+            ni.cap = (uint32_t)cap[n];
+            ni.keep = (uint32_t)keep[n];
+            ni.out_b = (uint32_t)(a0 + out_cnt[n]);
+            ni.out_e = (uint32_t)(a0 + out_cnt[n + 1]);
+            ni.req_base = 0;
+            ni.stream = sid;
+            ni.pad = 0;
+            nodes.push_back(ni);
+        }
+        lv[u].assign(cur + 1, {});
+        for (int n : topo) lv[u][lvl[n]].push_back(nb + n);
+        for (int64_t f = L->final_off[u]; f < L->final_off[u + 1]; f++) {
+            int fn = L->finals[f];
+            if (fn < 0 || fn >= N) { g_detail = "final node out of range"; return OTFLM_ERR_VALUE; }
+            finals.push_back(nb + fn);
+        }
+        final_off.push_back((uint32_t)finals.size());
+        node_base += N;
+    }
+    // merge levels across utterances; static request slots per node
+    size_t nlev = 0;
+    for (int u = 0; u < U; u++) nlev = std::max(nlev, lv[u].size());
+    p->lvl_node_off.assign(1, 0);
+    p->lvl_req.clear();
+    uint64_t rmax = 0, total = 0;
+    for (size_t t = 0; t < nlev; t++) {
+        uint64_t run = 0;
+        for (int u = 0; u < U; u++) {
+            if (t >= lv[u].size()) continue;
+            for (uint32_t g : lv[u][t]) {
+                NodeInfo &ni = nodes[g];
+                ni.req_base = (uint32_t)run;
+                run += (uint64_t)ni.keep * (ni.out_e - ni.out_b);
+                level_nodes.push_back(g);
+            }
+        }
+        if (run > 0xF0000000ull) { g_detail = "too many requests in one level"; return OTFLM_ERR_NOMEM; }
+        p->lvl_node_off.push_back((uint32_t)level_nodes.size());
+        p->lvl_req.push_back((uint32_t)run);
+        rmax = std::max(rmax, run);
+        total += run;
+    }
+    p->n_levels = (uint32_t)nlev;
+    p->n_nodes = (uint32_t)node_base;
+    p->n_arcs = (uint32_t)n_arcs_total;
+    p->n_slots = (uint32_t)slot_base;
+    p->R_max = (uint32_t)std::max<uint64_t>(rmax, 1);
+    p->total_req = total;
+    return OTFLM_OK;
+}
+
+template <class T>
+static int upload(Allocs &mem, T **dst, const std::vector<T> &v, cudaStream_t s) {
+    if (mem.alloc(dst, v.size()) != cudaSuccess) { g_detail = "cudaMalloc plan"; return OTFLM_ERR_NOMEM; }
+    if (!v.empty()) CK(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return OTFLM_OK;
+}
+
+static int plan_alloc_workspace(OtflmPlan *p, uint32_t R, int S) {
+    DevPlan &d = p->d;
+    bool bad = false;
+    bad |= p->mem.alloc(&d.rq_c, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.rq_arc, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.rq_parent, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.rq_stream, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.rq_cslot, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.rq_m, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.rq_dslot, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.rq_w, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.rq_state, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.rq_score, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.pr_req, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.pr_stream, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.pr_ctslot, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.pr_found, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.pr_E, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.pr_cnext, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.pr_inrow, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.pr_w, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.pr_p, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.first_E, (size_t)S) != cudaSuccess;
+    bad |= p->mem.alloc(&d.counters, 4) != cudaSuccess;
+    if (bad) { g_detail = "cudaMalloc workspace"; return OTFLM_ERR_NOMEM; }
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, int64_t beam, OtflmPlan **out,
+                                 void *stream) {
+    if (!st || !L || !out) return OTFLM_ERR_VALUE;
+    if (beam < 1) { g_detail = "beam must be >= 1"; return OTFLM_ERR_VALUE; }
+    if (L->n_utt < 1) return OTFLM_ERR_VALUE;
+    cudaStream_t s = (cudaStream_t)stream;
+    OtflmPlan *p = new OtflmPlan();
+    p->st = st;
+    p->beam = beam;
+    p->n_utt = L->n_utt;
+    std::vector<NodeInfo> nodes;
+    std::vector<uint32_t> level_nodes, out_list, arc_slot, start_slot, final_off, finals, utt_stream;
+    std::vector<int32_t> arc_word;
+    std::vector<double> arc_ac, arc_slm;
+    int rc = compile_batch(p, L, beam, st->m->d.V, nodes, level_nodes, out_list, arc_slot, arc_word, arc_ac,
+                           arc_slm, start_slot, final_off, finals, utt_stream);
+    if (rc) { delete p; return rc; }
+    {
+        std::vector<uint32_t> seen(st->d.S, 0);
+        for (uint32_t sid : utt_stream) {
+            if (sid >= (uint32_t)st->d.S || seen[sid]) { delete p; g_detail = "stream ids must be distinct and < n_streams"; return OTFLM_ERR_VALUE; }
+            seen[sid] = 1;
+        }
+    }
+    p->utt_stream_host = utt_stream;
+    DevPlan &d = p->d;
+    NodeInfo *dn; uint32_t *dln, *dol, *das, *dss, *dus, *dfo, *dfi; int32_t *daw; double *dac, *dsl;
+    if ((rc = upload(p->mem, &dn, nodes, s)) || (rc = upload(p->mem, &dln, level_nodes, s)) ||
+        (rc = upload(p->mem, &dol, out_list, s)) || (rc = upload(p->mem, &das, arc_slot, s)) ||
+        (rc = upload(p->mem, &daw, arc_word, s)) || (rc = upload(p->mem, &dac, arc_ac, s)) ||
+        (rc = upload(p->mem, &dsl, arc_slm, s)) || (rc = upload(p->mem, &dss, start_slot, s)) ||
+        (rc = upload(p->mem, &dus, utt_stream, s)) || (rc = upload(p->mem, &dfo, final_off, s)) ||
+        (rc = upload(p->mem, &dfi, finals, s))) {
+        p->mem.free_all(); delete p; return rc;
+    }
+    d.nodes = dn; d.level_nodes = dln; d.out_list = dol; d.arc_slot = das; d.arc_word = daw;
+    d.arc_ac = dac; d.arc_slm = dsl; d.n_utt = p->n_utt; d.utt_start_slot = dss; d.utt_stream = dus;
+    d.final_off = dfo; d.finals = dfi;
+    bool bad = p->mem.alloc(&d.arr, std::max<uint32_t>(p->n_slots, 1)) != cudaSuccess;
+    bad |= p->mem.alloc(&d.slot_win, std::max<uint32_t>(p->n_slots, 1)) != cudaSuccess;
+    uint32_t max_path = std::max<uint32_t>(p->n_levels, 1);
+    d.max_path = (int32_t)max_path;
+    bad |= p->mem.alloc(&d.out_len, p->n_utt) != cudaSuccess;
+    bad |= p->mem.alloc(&d.out_arcs, (size_t)p->n_utt * max_path) != cudaSuccess;
+    bad |= p->mem.alloc(&d.out_status, p->n_utt) != cudaSuccess;
+    bad |= p->mem.alloc(&d.out_combined, p->n_utt) != cudaSuccess;
+    bad |= p->mem.alloc(&d.out_acoustic, p->n_utt) != cudaSuccess;
+    bad |= p->mem.alloc(&d.out_lm, p->n_utt) != cudaSuccess;
+    bad |= p->mem.alloc(&d.out_end_ctx, p->n_utt) != cudaSuccess;
+    bad |= p->mem.alloc(&d.out_expansions, p->n_utt) != cudaSuccess;
+    p->scan_nb = cdiv(p->R_max, SCAN_BLK);
+    bad |= p->mem.alloc(&p->scan_status, (size_t)std::max<uint32_t>(p->n_levels, 1) * 2 * p->scan_nb) != cudaSuccess;
+    bad |= p->mem.alloc(&p->scan_ticket, (size_t)std::max<uint32_t>(p->n_levels, 1) * 2) != cudaSuccess;
+    if (bad) { p->mem.free_all(); delete p; g_detail = "cudaMalloc plan buffers"; return OTFLM_ERR_NOMEM; }
+    if ((rc = plan_alloc_workspace(p, p->R_max, st->d.S))) { p->mem.free_all(); delete p; return rc; }
+    *out = p;
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_plan_destroy(OtflmPlan *p) {
+    if (!p) return OTFLM_OK;
+    if (p->gexec) cudaGraphExecDestroy(p->gexec);
+    if (p->graph) cudaGraphDestroy(p->graph);
+    p->mem.free_all();
+    delete p;
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_plan_info(const OtflmPlan *p, int64_t *o) {
+    if (!p || !o) return OTFLM_ERR_VALUE;
+    o[0] = p->n_levels; o[1] = p->n_nodes; o[2] = p->n_arcs; o[3] = p->n_slots;
+    o[4] = p->R_max; o[5] = (int64_t)p->total_req; o[6] = p->g_nodes; o[7] = p->n_utt;
+    return OTFLM_OK;
+}
+
+// the per-level pipeline shared by decode and rnnlm_prob_batch (after the
+// requests of the level exist)
+static int enqueue_miss_pipeline(OtflmPlan *p, const DevModel &m, DevStreams &S, uint32_t R, int prec,
+                                 unsigned long long *status, uint32_t *ticket, cudaStream_t s) {
+    DevPlan &d = p->d;
+    const unsigned nb = cdiv(R, SCAN_BLK);
+    k_scan_prim<<<nb, SCAN_BLK, 0, s>>>(d, S, R, status, ticket);
+    CKL();
+    k_level_begin<<<1, 1, 0, s>>>(d, S);
+    CKL();
+#define CALL(VEC, CPL) k_hs_prim<VEC, CPL><<<cdiv(R, 8), 256, 0, s>>>(m, d, S, R)
+    HS_DISPATCH(m.H, CALL);
+#undef CALL
+    CKL();
+    int rc = launch_advance(m, prec, R, &d.counters[0], d.pr_inrow, d.pr_w, S.arena_h, S.arena_h,
+                            &d.counters[2], s);
+    if (rc) return rc;
+    k_dedup<<<cdiv(R, 8), 256, 0, s>>>(d, S);
+    CKL();
+    k_scan_novel<<<nb, SCAN_BLK, 0, s>>>(d, S, status + p->scan_nb, ticket + 1);
+    CKL();
+    k_resolve<<<cdiv(R, 256), 256, 0, s>>>(d, S);
+    CKL();
+    return OTFLM_OK;
+}
+
+static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, cudaStream_t s) {
+    OtflmStreams *st = p->st;
+    const DevModel &m = st->m->d;
+    DevStreams &S = st->d;
+    DevPlan &d = p->d;
+    CK(cudaMemsetAsync(d.arr, 0xFF, (size_t)std::max<uint32_t>(p->n_slots, 1) * sizeof(Arrival), s));
+    CK(cudaMemsetAsync(p->scan_status, 0, (size_t)std::max<uint32_t>(p->n_levels, 1) * 2 * p->scan_nb * 8, s));
+    CK(cudaMemsetAsync(p->scan_ticket, 0, (size_t)std::max<uint32_t>(p->n_levels, 1) * 2 * 4, s));
+    k_init_starts<<<cdiv(p->n_utt, 128), 128, 0, s>>>(d);
+    CKL();
+    k_run_begin<<<cdiv(S.S, 128), 128, 0, s>>>(S);
+    CKL();
+    for (uint32_t t = 0; t < p->n_levels; t++) {
+        const uint32_t nb0 = p->lvl_node_off[t], nn = p->lvl_node_off[t + 1] - nb0;
+        const uint32_t R = p->lvl_req[t];
+        unsigned long long *status = p->scan_status + (size_t)t * 2 * p->scan_nb;
+        uint32_t *ticket = p->scan_ticket + (size_t)t * 2;
+        if (nn == 0) continue;
+        k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, nb0, nn, (long long)p->beam, t);
+        CKL();
+        if (R == 0) continue;
+        int rc = enqueue_miss_pipeline(p, m, S, R, prec, status, ticket, s);
+        if (rc) return rc;
+        k_finish<<<cdiv(std::max<uint64_t>(R, (uint64_t)S.S), 256), 256, 0, s>>>(d, S, g->d, R, t, lm);
+        CKL();
+    }
+    k_final<<<cdiv(p->n_utt, 4), 128, 0, s>>>(d, S, lm);
+    CKL();
+    return OTFLM_OK;
+}
+
+static int64_t g_last_launches = 0;
+
+extern "C" int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
+                                int32_t use_graph, void *stream) {
+    if (!p || !g) return OTFLM_ERR_VALUE;
+    if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    if (g->d.order - 1 > p->st->m->d.order) { g_detail = "small LM order exceeds the stored context history"; return OTFLM_ERR_VALUE; }
+    if (g->d.V < p->st->m->d.V) { g_detail = "small LM vocabulary smaller than model"; return OTFLM_ERR_VALUE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    g_launches = 0;
+    if (!use_graph) {
+        int rc = enqueue_run(p, g, lm_weight, precision, s);
+        g_last_launches = g_launches;
+        return rc;
+    }
+    if (!p->gexec || p->g_lm != lm_weight || p->g_prec != precision || p->g_ng != g) {
+        if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+        if (p->graph) { cudaGraphDestroy(p->graph); p->graph = nullptr; }
+        // capture on a private stream (the caller's may be the legacy default stream)
+        cudaStream_t cs;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_run(p, g, lm_weight, precision, cs);
+        cudaGraph_t graph;
+        cudaError_t e = cudaStreamEndCapture(cs, &graph);
+        cudaStreamDestroy(cs);
+        if (rc) return rc;
+        CK(e);
+        p->graph = graph;
+        CK(cudaGraphInstantiate(&p->gexec, graph, 0));
+        size_t nn = 0;
+        cudaGraphGetNodes(graph, nullptr, &nn);
+        p->g_nodes = (int64_t)nn;
+        p->g_lm = lm_weight; p->g_prec = precision; p->g_ng = g;
+        p->g_nodes = (int64_t)nn;
+        g_last_launches = g_launches;
+    }
+    CK(cudaGraphLaunch(p->gexec, s));
+    return OTFLM_OK;
+}
+
+extern "C" int64_t otflm_last_launch_count(void) { return g_last_launches; }
+
+extern "C" int otflm_decode_fetch(OtflmPlan *p, OtflmDecodeResult *r, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    const uint32_t U = p->n_utt, MP = (uint32_t)p->d.max_path;
+    std::vector<int32_t> len(U), status(U), arcs((size_t)U * MP);
+    std::vector<double> comb(U), ac(U), lm(U);
+    std::vector<long long> endc(U), exps(U);
+    CK(cudaMemcpyAsync(len.data(), p->d.out_len, U * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(status.data(), p->d.out_status, U * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(arcs.data(), p->d.out_arcs, (size_t)U * MP * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(comb.data(), p->d.out_combined, U * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ac.data(), p->d.out_acoustic, U * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(lm.data(), p->d.out_lm, U * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(endc.data(), p->d.out_end_ctx, U * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(exps.data(), p->d.out_expansions, U * 8, cudaMemcpyDeviceToHost, s));
+    int rc = check_err(p->st, s);
+    if (rc) return rc;
+    for (uint32_t u = 0; u < U; u++) {
+        r->path_len[u] = len[u];
+        r->status[u] = status[u];
+        r->combined[u] = comb[u];
+        r->acoustic[u] = ac[u];
+        r->lm[u] = lm[u];
+        r->end_ctx[u] = endc[u];
+        r->expansions[u] = exps[u];
+        int32_t n = std::min<int32_t>(len[u], r->max_path);
+        for (int32_t k = 0; k < n; k++) r->path_arcs[(size_t)u * r->max_path + k] = arcs[(size_t)u * MP + k];
+    }
+    for (uint32_t u = 0; u < U; u++) if (status[u]) return status[u];
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_decode(OtflmStreams *s, const OtflmNgram *g, const OtflmLatticeBatch *lats, double lm_weight,
+                            int64_t beam, int32_t precision, OtflmDecodeResult *res, void *stream) {
+    OtflmPlan *p = nullptr;
+    int rc = otflm_plan_create(s, lats, beam, &p, stream);
+    if (rc) return rc;
+    rc = otflm_decode_run(p, g, lm_weight, precision, 0, stream);
+    if (!rc) rc = otflm_decode_fetch(p, res, stream);
+    cudaStreamSynchronize((cudaStream_t)stream);
+    otflm_plan_destroy(p);
+    return rc;
+}
+
+// ==========================================================================
+// rnnlm_prob_batch: Table-1 lookups in array order (cache.py:165-182)
+// ==========================================================================
+__global__ void k_probe_batch(DevPlan P, DevStreams S, uint32_t n, const uint32_t *c, const int32_t *w,
+                              const uint32_t *sid) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t s = sid[r];
+    P.rq_c[r] = c[r]; P.rq_w[r] = w[r]; P.rq_stream[r] = s; P.rq_m[r] = OTF_UNSET;
+    if (c[r] > S.table_len[s] || w[r] < 0) { atomicOr(S.err, c[r] > S.table_len[s] ? OTF_E_PATH : OTF_E_VALUE); P.rq_state[r] = RQ_INVALID; return; }
+    uint8_t st = RQ_NOCACHE;
+    uint32_t cslot = OTF_UNSET;
+    if (S.enabled) {
+        const uint64_t kb = (uint64_t)s * S.kc_cap;
+        const unsigned long long key = ((((unsigned long long)c[r]) << 32) | (uint32_t)w[r]) + 1ull;
+        const uint32_t mask = S.kc_cap - 1;
+        uint32_t sl = (uint32_t)otf_hash64(key) & mask, probes = 0;
+        for (;;) {
+            unsigned long long k = S.kc_key[kb + sl];
+            if (k == 0ull) { unsigned long long prev = atomicCAS(&S.kc_key[kb + sl], 0ull, key); k = prev == 0ull ? key : prev; }
+            if (k == key) break;
+            sl = (sl + 1) & mask;
+            if (++probes > S.kc_cap) { atomicOr(S.err, OTF_E_CACHE_FULL); sl = OTF_UNSET; break; }
+        }
+        cslot = sl;
+        if (sl != OTF_UNSET) {
+            if (ld_volatile_u32(&S.kc_cnext[kb + sl]) != OTF_UNSET) st = RQ_HIT;
+            else { atomicMin(&S.kc_claim[kb + sl], r); st = RQ_PENDING; }
+        } else st = RQ_INVALID;
+    }
+    P.rq_cslot[r] = cslot;
+    P.rq_state[r] = st;
+}
+
+__global__ void k_batch_out(DevPlan P, DevStreams S, uint32_t n, double *p_out, uint32_t *cn_out, uint8_t *hit_out) {
+    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r == 0) *S.arena_used += P.counters[0];
+    if (r < (uint32_t)S.S) { uint32_t nc = S.novel_cnt[r]; if (nc) { S.table_len[r] += nc; S.novel_cnt[r] = 0; } }
+    if (r >= n) return;
+    if (P.rq_state[r] == RQ_INVALID) return;
+    const uint32_t s = P.rq_stream[r], m = P.rq_m[r];
+    double p; uint32_t cn;
+    if (m != OTF_UNSET) { p = P.pr_p[m]; cn = P.pr_cnext[m]; }
+    else { const uint64_t kb = (uint64_t)s * S.kc_cap + P.rq_cslot[r]; p = S.kc_p[kb]; cn = S.kc_cnext[kb]; }
+    p_out[r] = p; cn_out[r] = cn; hit_out[r] = m == OTF_UNSET ? 1 : 0;
+    unsigned long long *stt = S.stats + (size_t)s * 8;
+    atomicAdd(&stt[0], 1ull);
+    if (m != OTF_UNSET) { atomicAdd(&stt[2], 1ull); if (S.enabled) atomicAdd(&stt[6], 1ull); }
+    else atomicAdd(&stt[1], 1ull);
+}
+
+extern "C" int otflm_rnnlm_prob_batch(OtflmStreams *s, int64_t n, const int32_t *sid_h, const uint32_t *c_h,
+                                      const int32_t *w_h, int32_t precision, double *p_h, uint32_t *cn_h,
+                                      uint8_t *hit_h, void *stream) {
+    if (!s || n < 0) return OTFLM_ERR_VALUE;
+    if (n == 0) return OTFLM_OK;
+    if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    cudaStream_t st = (cudaStream_t)stream;
+    const DevModel &m = s->m->d;
+    for (int64_t i = 0; i < n; i++) {
+        if (w_h[i] < 0 || w_h[i] >= m.V) { g_detail = "word id out of range"; return OTFLM_ERR_VALUE; }
+        if (sid_h[i] < 0 || sid_h[i] >= s->d.S) return OTFLM_ERR_VALUE;
+    }
+    // stable order by stream so each stream's requests are contiguous
+    std::vector<uint32_t> order((size_t)n);
+    for (int64_t i = 0; i < n; i++) order[i] = (uint32_t)i;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return sid_h[a] < sid_h[b]; });
+    std::vector<uint32_t> sc(n), cc(n);
+    std::vector<int32_t> ww(n);
+    for (int64_t i = 0; i < n; i++) { sc[i] = (uint32_t)sid_h[order[i]]; cc[i] = c_h[order[i]]; ww[i] = w_h[order[i]]; }
+    OtflmPlan *p = s->scratch;
+    if (!p || p->R_max < (uint32_t)n) {
+        if (p) otflm_plan_destroy(p);
+        p = new OtflmPlan();
+        p->st = s;
+        p->R_max = (uint32_t)std::max<int64_t>(n, 1024);
+        p->n_levels = 1;
+        p->scan_nb = cdiv(p->R_max, SCAN_BLK);
+        int rc = plan_alloc_workspace(p, p->R_max, s->d.S);
+        bool bad = rc != 0;
+        bad |= p->mem.alloc(&p->scan_status, (size_t)2 * p->scan_nb) != cudaSuccess;
+        bad |= p->mem.alloc(&p->scan_ticket, 2) != cudaSuccess;
+        if (bad) { p->mem.free_all(); delete p; s->scratch = nullptr; return OTFLM_ERR_NOMEM; }
+        s->scratch = p;
+    }
+    uint32_t *dsid, *dc, *dcn; int32_t *dw; double *dp; uint8_t *dh;
+    CK(cudaMallocAsync(&dsid, n * 4, st)); CK(cudaMallocAsync(&dc, n * 4, st)); CK(cudaMallocAsync(&dw, n * 4, st));
+    CK(cudaMallocAsync(&dp, n * 8, st)); CK(cudaMallocAsync(&dcn, n * 4, st)); CK(cudaMallocAsync(&dh, n, st));
+    CK(cudaMemcpyAsync(dsid, sc.data(), n * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dc, cc.data(), n * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dw, ww.data(), n * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(p->scan_status, 0, (size_t)2 * p->scan_nb * 8, st));
+    CK(cudaMemsetAsync(p->scan_ticket, 0, 8, st));
+    const uint32_t R = (uint32_t)n;
+    k_probe_batch<<<cdiv(R, 256), 256, 0, st>>>(p->d, s->d, R, dc, dw, dsid);
+    CKL();
+    int rc = enqueue_miss_pipeline(p, m, s->d, R, precision, p->scan_status, p->scan_ticket, st);
+    if (rc) return rc;
+    k_batch_out<<<cdiv(std::max<uint64_t>(R, (uint64_t)s->d.S), 256), 256, 0, st>>>(p->d, s->d, R, dp, dcn, dh);
+    CKL();
+    std::vector<double> pp(n);
+    std::vector<uint32_t> cn(n);
+    std::vector<uint8_t> hh(n);
+    CK(cudaMemcpyAsync(pp.data(), dp, n * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(cn.data(), dcn, n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hh.data(), dh, n, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(dsid, st)); CK(cudaFreeAsync(dc, st)); CK(cudaFreeAsync(dw, st));
+    CK(cudaFreeAsync(dp, st)); CK(cudaFreeAsync(dcn, st)); CK(cudaFreeAsync(dh, st));
+    unsigned int he = 0;
+    CK(cudaMemcpyAsync(&he, s->d.err, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (he & OTF_E_PATH) {
+        CK(cudaMemset(s->d.err, 0, 4));
+        g_detail = "context index not in table";
+        return OTFLM_ERR_UNKNOWN_INDEX;
+    }
+    rc = check_err(s, st);
+    if (rc) return rc;
+    for (int64_t i = 0; i < n; i++) { p_h[order[i]] = pp[i]; cn_h[order[i]] = cn[i]; hit_h[order[i]] = hh[i]; }
+    return OTFLM_OK;
+}
+
+// ==========================================================================
+extern "C" const char *otflm_error_string(int32_t code) {
+    switch (code) {
+    case OTFLM_OK: return "ok";
+    case OTFLM_ERR_VALUE: return "ValueError";
+    case OTFLM_ERR_UNKNOWN_INDEX: return "UnknownIndexError";
+    case OTFLM_ERR_TABLE_FULL: return "TableFullError";
+    case OTFLM_ERR_NO_PATH: return "no complete path through the lattice";
+    case OTFLM_ERR_KEY: return "word missing from unigram table";
+    case OTFLM_ERR_NOMEM: return "out of device memory";
+    case OTFLM_ERR_CYCLE: return "lattice contains a cycle";
+    case OTFLM_ERR_PACK: return "PackOverflowError";
+    case OTFLM_ERR_CUDA: return "CUDA error";
+    case OTFLM_ERR_HASH: return "context digest collision";
+    }
+    return "unknown error";
+}
+
+extern "C" const char *otflm_last_error_detail(void) { return g_detail.c_str(); }

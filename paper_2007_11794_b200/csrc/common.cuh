@@ -1,0 +1,134 @@
+// common.cuh -- device structures and helpers shared by the sm_100a kernels.
+//
+// Layout in HBM:
+//   model:   U [V,H] f32, W [H,H] f32 (+ WT, tf32 hi/lo and bf16 copies for
+//            the recurrent update), NV [V-1,H] f32, ME [M] f32,
+//            path CSR: off u32 [V+1], code u32 (node | bit<<31).
+//   streams: arena of hidden rows [R,H] f32 + meta [R,8] u32 (len, words),
+//            per-stream ctx_row [max_ctx+1] -> arena row, open-addressing
+//            content table (IndexTable) and (c,w) cache (RescoreCache).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#define OTF_UNSET 0xFFFFFFFFu
+#define OTF_META 8          // u32 words per arena row: len, w0..w6
+#define OTF_MAX_ORDER 7
+
+// error bits (device word, OR-ed)
+#define OTF_E_TABLE_FULL 1u
+#define OTF_E_ARENA_FULL 2u
+#define OTF_E_CACHE_FULL 4u
+#define OTF_E_HASH 8u
+#define OTF_E_KEY 16u
+#define OTF_E_VALUE 32u
+#define OTF_E_PATH 64u
+
+struct DevModel {
+    int H, V, order;
+    uint64_t mask, seed;
+    const float *U, *W, *WT, *NV, *ME;
+    const uint32_t *path_off, *path_code;
+    const float *W_hi, *W_lo;          // tf32-rounded split of W (K-major rows)
+    const __nv_bfloat16 *W_bf;         // bf16 copy of W
+};
+
+struct DevNgram {
+    int order, V, bos;
+    // open addressing, key = tuple hash (nonzero), verified by stored words
+    uint32_t p_cap, b_cap;
+    const uint64_t *p_tag; const int32_t *p_words; const double *p_val;   // [cap], [cap*order]
+    const uint64_t *b_tag; const int32_t *b_words; const double *b_val;
+};
+
+struct DevStreams {
+    int S, enabled, H, order;
+    uint32_t max_ctx;           // per stream contexts (indices 1..max_ctx)
+    uint32_t arena_rows;
+    uint32_t *ctx_row;          // [S][max_ctx+1]
+    float *arena_h;             // [R][H]
+    uint32_t *arena_meta;       // [R][OTF_META]
+    uint32_t *arena_used;       // scalar
+    uint32_t ct_cap;            // per stream content-table slots (pow2)
+    unsigned long long *ct_key; // [S][ct_cap], 0 = empty
+    uint32_t *ct_claim, *ct_idx, *ct_row;
+    uint32_t kc_cap;            // per stream cache slots (pow2)
+    unsigned long long *kc_key; // [S][kc_cap], 0 = empty, else ((c<<32)|w)+1
+    uint32_t *kc_claim, *kc_cnext;
+    double *kc_p;
+    uint32_t *table_len, *novel_cnt;  // [S]
+    unsigned long long *stats;        // [S][8]
+    unsigned int *err;
+};
+
+// per-request state
+#define RQ_INVALID 0
+#define RQ_HIT 1       // value present from an earlier level / call
+#define RQ_PENDING 2   // key inserted this level; claim decides the primary
+#define RQ_NOCACHE 3   // cache disabled: every request computes
+
+struct Arrival {       // 32 B, one per (dst node, in-arc, source rank)
+    double score;
+    uint32_t ctx, parent, arc, lvl, ridx, pad;
+};
+
+struct NodeInfo {      // 32 B
+    uint32_t slot_base, cap, keep, out_b, out_e, req_base, stream, pad;
+};
+
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t otf_mix(uint64_t h, uint64_t x) {
+    h = (h ^ x) * 0x9E3779B97F4A7C15ull;   // _kernels_nb.py:21-24
+    return h ^ (h >> 32);
+}
+
+__device__ __forceinline__ uint64_t otf_hash64(uint64_t x) {
+    x ^= x >> 33; x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+// _kernels_nb.py:36-48 in float64 (CUDA libdevice exp/log1p, <= 1 ulp)
+__device__ __forceinline__ double otf_log_sigmoid(double x) {
+    return x >= 0.0 ? -log1p(exp(-x)) : x - log1p(exp(x));
+}
+__device__ __forceinline__ double otf_sigmoid(double x) {
+    if (x >= 0.0) return 1.0 / (1.0 + exp(-x));
+    double ex = exp(x);
+    return ex / (1.0 + ex);
+}
+
+__device__ __forceinline__ double shfl_xor_d(double v, int m) {
+    return __shfl_xor_sync(0xffffffffu, v, m);
+}
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) v += shfl_xor_d(v, m);
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// tuple hash for the small-LM tables (host mirrors this exactly)
+__host__ __device__ __forceinline__ uint64_t otf_tuple_hash(const int32_t *w, int len) {
+    uint64_t h = 0x243F6A8885A308D3ull ^ (uint64_t)len;
+    for (int i = 0; i < len; i++) {
+        uint64_t x = h ^ (uint64_t)(uint32_t)w[i];
+        x ^= x >> 33; x *= 0xff51afd7ed558ccdull;
+        x ^= x >> 33; x *= 0xc4ceb9fe1a85ec53ull;
+        x ^= x >> 33;
+        h = x + 0x9E37ull * (uint64_t)(i + 1);
+    }
+    return h | 1ull;   // never 0 (0 marks an empty slot)
+}

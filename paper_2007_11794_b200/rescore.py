@@ -1,0 +1,386 @@
+"""Drop-in mirror of the reference decoder/LM API, executed on the B200.
+
+Same names, argument meaning and error behaviour as the reference
+(``otflm.cache``, ``otflm.context_table``, ``otflm.codec``,
+``otflm.decoder``); the numeric work, the IndexTable and the result cache
+live on the device (libotflm_b200.so), never on the host.
+
+* ``IndexTable``      -- context_table.py:48-119 (device content table)
+* ``RescoreCache``    -- cache.py:61-162 (device (c, w) -> (p, c') table;
+                         capacity 0 = unbounded is the device mode)
+* ``rnnlm_prob``      -- cache.py:165-182
+* ``reset_utterance`` -- cache.py:185-191
+* ``RescoreStack``    -- decoder.py:61-70
+* ``rescore_onthefly``-- decoder.py:114-173
+* ``rescore_batch``   -- many utterances, one stream each
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from .device import DeviceModel, DeviceNgram, DeviceStreams, Plan
+from .model import RnnlmContext
+
+ENTRY_BYTES = 32          # cache.py:26
+REQUEST_BYTES = 16        # codec.py:23
+RESPONSE_BYTES = 16
+DEFAULT_RNN_BITS = 32
+DEFAULT_DEVICE_CONTEXTS = 1 << 18
+
+
+@dataclass(frozen=True)
+class CacheValue:
+    p: float
+    c_next: int
+
+
+@dataclass
+class CacheStats:
+    """cache.py:37-58"""
+
+    lookups: int = 0
+    hits: int = 0
+    misses: int = 0
+    evictions: int = 0
+    resident_bytes: int = 0
+
+    @property
+    def hit_ratio(self) -> float:
+        return self.hits / self.lookups if self.lookups else 0.0
+
+    def line(self) -> str:
+        return (f"lookups={self.lookups} hits={self.hits} "
+                f"hit_ratio={self.hit_ratio:.6f} "
+                f"resident_bytes={self.resident_bytes} evictions={self.evictions}")
+
+    def add(self, other: "CacheStats") -> None:
+        self.lookups += other.lookups
+        self.hits += other.hits
+        self.misses += other.misses
+        self.evictions += other.evictions
+
+
+@dataclass
+class TransferLedger:
+    """codec.py:95-110 -- per-stream byte accounting of the (now on-device)
+    request/response exchange; counts are derived from device counters."""
+
+    requests: int = 0
+    bytes_indexed: int = 0
+    bytes_full_baseline: int = 0
+    request_bytes: int = field(default=REQUEST_BYTES, repr=False)
+    response_bytes: int = field(default=RESPONSE_BYTES, repr=False)
+
+    def record(self, context_bytes: int, n: int = 1) -> None:
+        self.requests += n
+        self.bytes_indexed += n * (self.request_bytes + self.response_bytes)
+        self.bytes_full_baseline += n * 2 * context_bytes
+
+
+def reduction_ratio(ledger: TransferLedger, context_bytes: int) -> float:
+    if ledger.requests == 0:
+        raise ValueError("no requests recorded")
+    return ledger.requests * 2 * context_bytes / ledger.bytes_indexed
+
+
+def pack(rnnlm_index: int, smalllm_index: int, rnn_bits: int = DEFAULT_RNN_BITS) -> int:
+    """codec.py:35-46"""
+    if not 1 <= rnn_bits <= 63:
+        raise ValueError(f"rnn_bits must be in 1..63, got {rnn_bits}")
+    small_bits = 64 - rnn_bits
+    if not 0 <= rnnlm_index < (1 << rnn_bits):
+        raise _lib.PackOverflowError(f"rnnlm_index {rnnlm_index} does not fit in {rnn_bits} bits")
+    if not 0 <= smalllm_index < (1 << small_bits):
+        raise _lib.PackOverflowError(
+            f"smalllm_index {smalllm_index} does not fit in {small_bits} bits")
+    return (rnnlm_index << small_bits) | smalllm_index
+
+
+def unpack(value: int, rnn_bits: int = DEFAULT_RNN_BITS) -> tuple:
+    if not 1 <= rnn_bits <= 63:
+        raise ValueError(f"rnn_bits must be in 1..63, got {rnn_bits}")
+    small_bits = 64 - rnn_bits
+    return value >> small_bits, value & ((1 << small_bits) - 1)
+
+
+# --------------------------------------------------------------------------
+class _Binding:
+    """One device stream shared by an (IndexTable, RescoreCache) pair."""
+
+    def __init__(self, model, tree, table: "IndexTable", cache: "RescoreCache"):
+        self.dmodel = DeviceModel.get(model, tree)
+        cap = int(min(table.max_entries, table.device_capacity))
+        self.streams = DeviceStreams(self.dmodel, 1, enabled=cache.enabled, max_contexts=cap,
+                                     cache_slots=2 * cap + 16, arena_rows=cap + 2)
+        self.model, self.tree = model, tree
+
+
+class IndexTable:
+    """Device IndexTable (context_table.py:48-119).  Index 0 is the zero
+    context; fresh contexts get len + 1; dedup is bit-exact on the f32
+    hidden state + history."""
+
+    def __init__(self, hidden_size: int, maxent_order: int, max_entries: int = (1 << 64) - 2,
+                 device_capacity: int = DEFAULT_DEVICE_CONTEXTS):
+        self.hidden_size = hidden_size
+        self.maxent_order = maxent_order
+        self.max_entries = max_entries
+        self.device_capacity = device_capacity
+        self._bind: _Binding | None = None
+
+    @property
+    def element_bytes(self) -> int:
+        return 4 * self.hidden_size + 8 * self.maxent_order + 8
+
+    def __len__(self) -> int:
+        if self._bind is None:
+            return 0
+        return int(self._bind.streams.stats()[0, 3])
+
+    def decode(self, idx: int) -> RnnlmContext:
+        idx = int(idx)
+        if idx == 0:
+            return RnnlmContext(np.zeros(self.hidden_size, np.float32), ())
+        if self._bind is None or not 1 <= idx <= len(self):
+            raise _lib.UnknownIndexError(f"index {idx} not in table (length {len(self)})")
+        h, hist = self._bind.streams.context(0, idx)
+        return RnnlmContext(h, hist)
+
+    def memory_report(self) -> tuple:
+        n = len(self)
+        return n, self.element_bytes, n * self.element_bytes
+
+    def clear(self) -> None:
+        if self._bind is not None:
+            self._bind.streams.reset(retain=False)
+
+
+class RescoreCache:
+    """Device result cache (cache.py:61-162).  capacity_bytes must be 0
+    (unbounded, per-utterance clear via reset_utterance); the LFU bound is
+    a host-side policy not offered on the device path."""
+
+    def __init__(self, capacity_bytes: int = 0, enabled: bool = True):
+        if capacity_bytes < 0:
+            raise ValueError("capacity_bytes must be >= 0")
+        if capacity_bytes > 0:
+            raise NotImplementedError("capacity-bounded LFU eviction is not offered on the device "
+                                      "path (unbounded cache with reset_utterance is)")
+        self.capacity_bytes = capacity_bytes
+        self.enabled = enabled
+        self._bind: _Binding | None = None
+        self._rolled = CacheStats()
+
+    def _raw(self):
+        return self._bind.streams.stats()[0] if self._bind else np.zeros(8, np.int64)
+
+    def __len__(self) -> int:
+        return int(self._raw()[7])
+
+    @property
+    def resident_bytes(self) -> int:
+        return len(self) * ENTRY_BYTES
+
+    def stats(self) -> CacheStats:
+        r = self._raw()
+        return CacheStats(int(r[0]), int(r[1]), int(r[2]), 0, int(r[7]) * ENTRY_BYTES)
+
+    def cumulative_stats(self) -> CacheStats:
+        r = self._raw()
+        return CacheStats(int(r[4]), int(r[5]), int(r[6]), 0, int(r[7]) * ENTRY_BYTES)
+
+
+def _binding(cache: RescoreCache, table: IndexTable, model, tree) -> _Binding:
+    b = table._bind or cache._bind
+    if b is None:
+        b = _Binding(model, tree, table, cache)
+        table._bind = cache._bind = b
+    elif table._bind is not cache._bind:
+        if cache._bind is None:
+            cache._bind = b
+        elif table._bind is None:
+            table._bind = b
+        else:
+            raise ValueError("table and cache are bound to different device streams")
+    if b.model is not model or b.tree is not tree:
+        raise ValueError("stream already bound to a different model")
+    return b
+
+
+def rnnlm_prob(cache: RescoreCache, table: IndexTable, model, tree, w: int, c: int,
+               precision: str = "fp64") -> CacheValue:
+    """cache.py:165-182 -- one Table-1 lookup on the device."""
+    w = int(w)
+    if not 0 <= w < model.vocab_size:
+        raise ValueError(f"word id {w} out of range 0..{model.vocab_size - 1}")
+    b = _binding(cache, table, model, tree)
+    p, cn, _ = b.streams.rnnlm_prob_batch([0], [int(c)], [w], precision)
+    return CacheValue(float(p[0]), int(cn[0]))
+
+
+def rnnlm_prob_trace(cache: RescoreCache, table: IndexTable, model, tree, trace,
+                     precision: str = "fp64"):
+    """Replay a (w, parent_step) trace (reference tests/test_cache.py:60-97)
+    in dependency waves: every request whose parent is resolved goes in one
+    device batch, with the batch's array order equal to trace order, which
+    keeps hit/miss and index numbering identical to one-by-one replay."""
+    b = _binding(cache, table, model, tree)
+    n = len(trace)
+    ws = np.array([t[0] for t in trace], np.int64)
+    par = np.array([t[1] for t in trace], np.int64)
+    if np.any((ws < 0) | (ws >= model.vocab_size)):
+        raise ValueError("word id out of range")
+    depth = np.zeros(n, np.int64)
+    for i in range(n):
+        depth[i] = 0 if par[i] < 0 else depth[par[i]] + 1
+    succ = np.zeros(n, np.int64)
+    p_out = np.zeros(n)
+    hit = np.zeros(n, bool)
+    # waves must also respect order: a request may only run after all
+    # earlier requests (it could hit their entries), so a wave is a maximal
+    # run of consecutive trace entries whose parents lie before the run
+    i = 0
+    while i < n:
+        j = i
+        while j < n and (par[j] < i):
+            j += 1
+        if j == i:
+            raise ValueError("trace parent must precede the request")
+        cs = np.where(par[i:j] < 0, 0, succ[np.maximum(par[i:j], 0)])
+        p, cn, h = b.streams.rnnlm_prob_batch(np.zeros(j - i, np.int32), cs, ws[i:j], precision)
+        succ[i:j] = cn
+        p_out[i:j] = p
+        hit[i:j] = h
+        i = j
+    return p_out, succ, hit
+
+
+def reset_utterance(cache: RescoreCache, table: IndexTable, retain: bool) -> None:
+    """cache.py:185-191"""
+    b = table._bind or cache._bind
+    if b is not None:
+        b.streams.reset(retain)
+
+
+@dataclass
+class RescoreStack:
+    """decoder.py:61-70"""
+
+    model: object
+    tree: object
+    table: IndexTable
+    cache: RescoreCache
+    ledger: TransferLedger = field(default_factory=TransferLedger)
+    rnn_bits: int = 32
+
+
+@dataclass
+class PathHypothesis:
+    """decoder.py:49-58"""
+
+    arcs: tuple
+    words: tuple
+    acoustic_score: float
+    lm_score: float
+    combined_score: float
+    end_context: int = 0
+
+
+@dataclass
+class TraversalReport:
+    """decoder.py:107-111"""
+
+    expansions: int
+    cache_stats: object
+    transfer: TransferLedger
+
+
+def _hyp(out, u, lat) -> PathHypothesis:
+    n = int(out["path_len"][u])
+    arcs = tuple(int(a) for a in out["path_arcs"][u, :n])
+    words = tuple(int(lat.arc_word[a]) for a in arcs)
+    return PathHypothesis(arcs, words, float(out["acoustic"][u]), float(out["lm"][u]),
+                          float(out["combined"][u]), int(out["end_ctx"][u]))
+
+
+def rescore_onthefly(lattice, small_lm, stack: RescoreStack, lm_weight: float = 1.0,
+                     beam: int = 1 << 30, precision: str = "fp64"):
+    """decoder.py:114-173 -- one utterance on the stack's device stream."""
+    if beam < 1:
+        raise ValueError("beam must be >= 1")
+    if small_lm.order - 1 > stack.model.maxent_order:
+        raise ValueError("small LM order exceeds the stored context history; "
+                         f"need maxent_order >= {small_lm.order - 1}")
+    b = _binding(stack.cache, stack.table, stack.model, stack.tree)
+    g = DeviceNgram.get(small_lm, b.dmodel)
+    plan = Plan(b.streams, [lattice], beam)
+    plan.run(g, lm_weight, precision, use_graph=False)
+    out = plan.fetch()
+    hyp = _hyp(out, 0, plan.lats[0])
+    exp = int(out["expansions"][0])
+    stack.ledger.record(stack.table.element_bytes, exp)
+    return hyp, TraversalReport(expansions=exp, cache_stats=stack.cache.stats(),
+                                transfer=stack.ledger)
+
+
+class BatchDecoder:
+    """Decode many utterances at once, one independent stream each
+    (retain=False semantics between batches), on one GPU.
+
+    ``prepare`` compiles and uploads the lattices (host->device), ``run``
+    decodes with the inputs resident in HBM (replaying a CUDA graph of the
+    level loop), ``fetch`` copies the 1-best paths back.
+    """
+
+    def __init__(self, model, tree, small_lm, n_streams: int, max_contexts: int,
+                 enabled: bool = True, precision: str = "fp64"):
+        self.model, self.tree = model, tree
+        self.dmodel = DeviceModel.get(model, tree)
+        self.ngram = DeviceNgram.get(small_lm, self.dmodel)
+        self.precision = precision
+        self.streams = DeviceStreams(self.dmodel, n_streams, enabled=enabled,
+                                     max_contexts=max_contexts,
+                                     cache_slots=2 * max_contexts + 16,
+                                     arena_rows=n_streams * max_contexts + 2)
+        self.plan = None
+
+    @staticmethod
+    def contexts_needed(lattices, beam: int) -> int:
+        """Upper bound on new contexts per utterance: every request may
+        create one (sum over nodes of min(beam, capacity) * out-degree)."""
+        worst = 0
+        for lat in lattices:
+            from .lattice import as_lattice
+            l = as_lattice(lat)
+            worst = max(worst, int(min(beam, 1 << 20)) * l.n_arcs)
+        return worst + 1
+
+    def prepare(self, lattices, beam: int) -> Plan:
+        self.plan = Plan(self.streams, lattices, beam)
+        return self.plan
+
+    def run(self, lm_weight: float = 1.0, use_graph: bool = True) -> None:
+        self.streams.reset(retain=False)
+        self.plan.run(self.ngram, lm_weight, self.precision, use_graph=use_graph)
+
+    def fetch(self):
+        out = self.plan.fetch()
+        return [_hyp(out, u, self.plan.lats[u]) for u in range(self.plan.n_utt)], out
+
+
+def rescore_batch(lattices: Sequence, small_lm, model, tree, lm_weight: float = 1.0,
+                  beam: int = 8, precision: str = "fp64", enabled: bool = True,
+                  max_contexts: int | None = None):
+    """Many utterances, independent fresh streams (retain=False)."""
+    if max_contexts is None:
+        max_contexts = BatchDecoder.contexts_needed(lattices, beam)
+    dec = BatchDecoder(model, tree, small_lm, len(lattices), max_contexts, enabled, precision)
+    dec.prepare(lattices, beam)
+    dec.run(lm_weight, use_graph=False)
+    hyps, out = dec.fetch()
+    return hyps, out

@@ -1,0 +1,237 @@
+"""Decoder / Table-1 parity on the B200 (FP64 mode = exact mode).
+
+Against the reference's own outputs (golden fixtures) and the CPU oracle:
+1-best arc sequence identical, context ids / end context identical, cache
+hit/miss and IndexTable counts bit-exact, combined score within 1e-9
+(float64 path scores; the only source of difference is the f32 rounding of
+a delta whose float64 value differs from the reference's by ~1e-16).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import small_results
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+EXHAUSTIVE = 1 << 30
+
+
+def _stack(gm, enabled=True):
+    from paper_2007_11794_b200 import IndexTable, RescoreCache, RescoreStack
+    m = gm.model
+    return RescoreStack(model=m, tree=gm.tree, table=IndexTable(m.hidden_size, m.maxent_order,
+                                                                device_capacity=1 << 14),
+                        cache=RescoreCache(enabled=enabled))
+
+
+def test_small_decodes_match_reference_golden(small):
+    from paper_2007_11794_b200 import rescore_onthefly
+    d, gm, lats = small
+    beams = [int(b) for b in d["beams"]]
+    for row in small_results(d):
+        li, bi, en = int(row[0]), int(row[1]), int(row[2])
+        st = _stack(gm, enabled=bool(en))
+        lm_w = 1.0 if li % 2 else 0.7
+        hyp, rep = rescore_onthefly(lats[li], gm.lm, st, lm_weight=lm_w, beam=beams[bi])
+        assert hyp.arcs == tuple(d[f"l{li}_b{bi}_e{en}_arcs"]), (li, bi, en)
+        assert abs(hyp.combined_score - row[3]) <= TOL
+        assert abs(hyp.acoustic_score - row[4]) <= TOL
+        assert abs(hyp.lm_score - row[5]) <= TOL
+        assert hyp.end_context == int(row[6])
+        assert rep.expansions == int(row[7])
+        s = st.cache.stats()
+        assert (s.lookups, s.hits, s.misses) == tuple(int(x) for x in row[8:11])
+        assert len(st.table) == int(row[11])
+        # test_decoder.py:100-107 accounting
+        assert st.ledger.requests == rep.expansions == s.lookups
+        assert st.ledger.bytes_indexed == 32 * rep.expansions == int(row[12])
+        assert st.ledger.bytes_full_baseline == int(row[13])
+
+
+def test_config_a_matches_reference_golden(config_a):
+    from paper_2007_11794_b200 import IndexTable, RescoreCache, RescoreStack, rescore_onthefly
+    d, model, tree, lm, lat = config_a
+    st = RescoreStack(model=model, tree=tree, table=IndexTable(64, 3, device_capacity=1 << 16),
+                      cache=RescoreCache())
+    hyp, rep = rescore_onthefly(lat, lm, st, beam=8)
+    res = d["result"]
+    assert hyp.arcs == tuple(d["arcs"])
+    assert abs(hyp.combined_score - res[0]) <= TOL
+    assert hyp.end_context == int(res[3])
+    assert rep.expansions == int(res[4])
+    s = st.cache.stats()
+    assert (s.lookups, s.hits, s.misses) == tuple(int(x) for x in res[5:8])
+    assert len(st.table) == int(res[8])
+
+
+def test_trace_replay_matches_reference_golden(small):
+    """tests/test_cache.py:60-97 and acceptance crit 3: p / c' / hidden."""
+    from paper_2007_11794_b200 import IndexTable, RescoreCache, rnnlm_prob_trace
+    d, gm, _ = small
+    for enabled in (True, False):
+        table = IndexTable(16, 3, device_capacity=1 << 13)
+        cache = RescoreCache(enabled=enabled)
+        p, succ, hit = rnnlm_prob_trace(cache, table, gm.model, gm.tree,
+                                        [tuple(int(x) for x in t) for t in d["trace"]])
+        assert np.max(np.abs(p - d["trace_p"])) <= 1e-12
+        assert np.array_equal(succ, d["trace_c"])
+        for i in range(0, len(succ), 37):
+            assert table.decode(int(succ[i])).hidden.tobytes() == d["trace_h"][i].tobytes()
+        s = cache.stats()
+        if enabled:
+            assert [s.lookups, s.hits, s.misses, len(table)] == list(d["trace_stats"])
+        else:
+            assert s.hits == 0 and s.misses == s.lookups == len(d["trace"])
+            assert len(table) == int(d["trace_stats"][3])
+
+
+def test_single_rnnlm_prob_calls(small):
+    """test_cache.py:32-57 / :100-110 shapes on the device API."""
+    from paper_2007_11794_b200 import IndexTable, RescoreCache, reset_utterance, rnnlm_prob
+    d, gm, _ = small
+    table, cache = IndexTable(16, 3, device_capacity=1024), RescoreCache()
+    v1 = rnnlm_prob(cache, table, gm.model, gm.tree, 5, 0)
+    v2 = rnnlm_prob(cache, table, gm.model, gm.tree, 5, 0)
+    assert v1 == v2 and v1.c_next == 1
+    s = cache.stats()
+    assert (s.lookups, s.hits, s.misses) == (2, 1, 1)
+    st = O.OracleStack(gm.model, gm.tree)
+    p, cn, _ = st.rnnlm_prob(5, 0)
+    assert abs(v1.p - p) <= 1e-12
+    h, hist = st.context(cn)
+    ctx = table.decode(v1.c_next)
+    assert ctx.hidden.tobytes() == h.tobytes() and ctx.history == hist
+    reset_utterance(cache, table, retain=False)
+    assert len(table) == 0 and len(cache) == 0
+    assert cache.stats().lookups == 0 and cache.cumulative_stats().lookups == 2
+    v = rnnlm_prob(cache, table, gm.model, gm.tree, 3, 0)
+    assert v.c_next == 1 and cache.stats().misses == 1
+    with pytest.raises(KeyError):
+        rnnlm_prob(cache, table, gm.model, gm.tree, 3, 99)     # UnknownIndexError
+    with pytest.raises(ValueError):
+        rnnlm_prob(cache, table, gm.model, gm.tree, gm.model.vocab_size, 0)
+
+
+def test_retained_second_pass_computes_nothing(small):
+    """test_decoder.py:110-120."""
+    from paper_2007_11794_b200 import rescore_onthefly, reset_utterance
+    d, gm, lats = small
+    st = _stack(gm)
+    h1, _ = rescore_onthefly(lats[10], gm.lm, st, beam=8)
+    first = st.cache.stats().misses
+    reset_utterance(st.cache, st.table, retain=True)
+    h2, _ = rescore_onthefly(lats[10], gm.lm, st, beam=8)
+    assert st.cache.stats().misses == 0 < first
+    assert h1.arcs == h2.arcs and h1.combined_score == h2.combined_score
+
+
+def test_exhaustive_beam_equals_brute_force(small):
+    """test_decoder.py:40-51 / acceptance crit 6 (oracle path score)."""
+    from paper_2007_11794_b200 import rescore_onthefly
+    d, gm, lats = small
+    for li in (0, 3, 6, 9):
+        lat = lats[li]
+        st = _stack(gm)
+        hyp, _ = rescore_onthefly(lat, gm.lm, st, beam=EXHAUSTIVE)
+        ol = O.OracleLattice(lat)
+        best, best_s = None, -math.inf
+        for path in _paths(lat):
+            s = O.path_score(gm.model, gm.tree, gm.lm, ol, path)
+            if s > best_s:
+                best, best_s = path, s
+        assert hyp.arcs == best
+        assert abs(hyp.combined_score - best_s) <= TOL
+
+
+def _paths(lat, limit=5000):
+    out = []
+    outs = {}
+    for a in lat.arcs:
+        outs.setdefault(a.src, []).append(a)
+
+    def dfs(n, acc):
+        assert len(out) < limit
+        if n in lat.finals:
+            out.append(tuple(acc))
+        for a in outs.get(n, []):
+            dfs(a.dst, acc + [a.id])
+
+    dfs(lat.start, [])
+    return out
+
+
+def test_batch_decode_matches_oracle():
+    """Many utterances, one stream each (the bench path), vs the oracle."""
+    from paper_2007_11794_b200 import synth
+    from paper_2007_11794_b200.rescore import BatchDecoder
+    s = synth.build_setup("a", n_utt=12, T=60, seed=3)
+    ref = O.decode_many(s.model, s.tree, s.small_lm, s.lattices, beam=s.beam, n_threads=4)
+    need = BatchDecoder.contexts_needed(s.lattices, s.beam)
+    dec = BatchDecoder(s.model, s.tree, s.small_lm, len(s.lattices), need)
+    dec.prepare(s.lattices, s.beam)
+    for use_graph in (False, True, True):
+        dec.run(1.0, use_graph=use_graph)
+        hyps, out = dec.fetch()
+        for u, (r, (lk, hi, mi)) in enumerate(ref):
+            assert hyps[u].arcs == r.arcs
+            assert abs(hyps[u].combined_score - r.combined_score) <= TOL
+            assert hyps[u].end_context == r.end_context
+            assert int(out["expansions"][u]) == r.expansions
+        st = dec.streams.stats()
+        assert [int(x) for x in st[:, 0]] == [x[1][0] for x in ref]
+        assert [int(x) for x in st[:, 2]] == [x[1][2] for x in ref]
+
+
+def test_degenerate_zero_model_dedups_contexts(small):
+    """test_decoder.py:61-89: zero recurrent weights -> identical hidden
+    states, so the IndexTable dedups on history alone; every delta is 0 and
+    the best path is the small-LM Viterbi path."""
+    from paper_2007_11794_b200 import RnnlmModel, rescore_onthefly
+    from paper_2007_11794_b200.lattice import generate_lattice
+    from paper_2007_11794_b200.model import log_half_path_unigram
+    d, gm, lats = small
+    V = gm.model.vocab_size
+    model = RnnlmModel.new(V, hidden_size=8, maxent_order=3, maxent_table_bits=6, seed=1)
+    model.input_weights[:] = 0
+    model.recurrent_weights[:] = 0
+    uni = log_half_path_unigram(gm.tree, V, 1, 2)
+    ref = [5, 9, 4, 12, 7]
+    lat = generate_lattice(ref, V, uni, 3, noise_seed=3)
+    from paper_2007_11794_b200 import IndexTable, RescoreCache, RescoreStack
+    st = RescoreStack(model=model, tree=gm.tree, table=IndexTable(8, 3, device_capacity=4096),
+                      cache=RescoreCache())
+    hyp, _ = rescore_onthefly(lat, uni, st, beam=EXHAUSTIVE)
+    ost = O.OracleStack(model, gm.tree)
+    r = ost.rescore_onthefly(lat, uni, beam=EXHAUSTIVE)
+    assert hyp.arcs == r.arcs and hyp.combined_score == r.combined_score
+    assert len(st.table) == ost.stats().table_len
+    assert st.cache.stats().hits == ost.stats().hits
+    best = max(_paths(lat), key=lambda p: sum(lat.arcs[a].acoustic + lat.arcs[a].smalllm for a in p))
+    assert hyp.arcs == best
+
+
+def test_errors_map_to_reference_exceptions(small):
+    from paper_2007_11794_b200 import Lattice, rescore_onthefly
+    d, gm, lats = small
+    st = _stack(gm)
+    with pytest.raises(ValueError):
+        rescore_onthefly(lats[0], gm.lm, st, beam=0)
+    cyc = Lattice(0, [2], src=[0, 1, 1], dst=[1, 0, 2], word=[3, 4, 5], acoustic=[0, 0, 0],
+                  smalllm=[-1.0, -1.0, -1.0])
+    with pytest.raises(ValueError):
+        rescore_onthefly(cyc, gm.lm, st, beam=4)
+    dead = Lattice(0, [3], src=[0, 1], dst=[1, 2], word=[3, 4], acoustic=[0, 0],
+                   smalllm=[-1.0, -1.0])
+    with pytest.raises(ValueError, match="no complete path"):
+        rescore_onthefly(dead, gm.lm, st, beam=4)
+    bad = Lattice(0, [1], src=[0], dst=[1], word=[gm.model.vocab_size + 5], acoustic=[0.0],
+                  smalllm=[-1.0])
+    with pytest.raises(ValueError):
+        rescore_onthefly(bad, gm.lm, st, beam=4)
