@@ -1,0 +1,329 @@
+#!/usr/bin/env python3
+"""On-the-fly RNNLM rescoring benchmark (BASELINE.json metric: decode frames/s
+& RTF; RNNLM (history, word) queries/s per GPU).
+
+Workload at N=1: configs[1] = config (b): synthetic HS+MaxEnt RNNLM
+(V=20,000, H=256, MaxEnt 2^21), 64 utterances x 300 frames (one lattice
+step = one 10 ms frame), breadth 3, beam 8, bigram small LM; one step =
+decoding the whole batch (every frame of every utterance, fresh
+per-utterance streams).  Under torchrun each rank decodes its own 64
+utterances (weak scaling) and NCCL gathers the per-utterance results.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--precision P]
+  python bench.py --impl reference      # CPU arm (oracle port, all host cores)
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FRAME_S = 0.01          # one lattice step = one 10 ms frame
+CONFIG = "b"
+METRIC = "decode frames/sec (RNNLM on-the-fly rescoring, config b: V=20k H=256 HS+MaxEnt 2^21, " \
+         "64 utt x 300 frames, beam 8)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default="tf32x3", choices=["fp64", "tf32x3", "tf32", "bf16"])
+    ap.add_argument("--n-utt", type=int, default=64)
+    ap.add_argument("--frames", type=int, default=300)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--out", default=None, help="also write the JSON line here")
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 4 + i and s[4 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), \
+            "MEASURED_PEAKS.json"
+    return 6650.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_baseline(setup, n_sample: int, threads: int):
+    """The reference algorithm on host cores: the C oracle port
+    (oracle/otflm_oracle.c), fresh stream per utterance, utterance-parallel."""
+    from oracle import oracle as O
+    lats = setup.lattices[:n_sample]
+    om = O.OracleModel(setup.model, setup.tree)
+    og = O.OracleNgram(setup.small_lm)
+    ols = [O.OracleLattice(l) for l in lats]
+    O.decode_many(om, None, og, ols[:1], beam=setup.beam, n_threads=1)   # warm-up
+    t0 = time.perf_counter()
+    res = O.decode_many(om, None, og, ols, beam=setup.beam, n_threads=threads)
+    dt = time.perf_counter() - t0
+    frames = sum(len(r[0].arcs) for r in res)
+    reqs = sum(r[1][0] for r in res)
+    return frames, reqs, dt, res
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2007_11794_b200 import synth
+    threads = len(os.sched_getaffinity(0))
+    n_sample = min(args.n_utt, max(threads, 16))
+    setup = synth.build_setup(CONFIG, n_utt=n_sample, T=args.frames, seed=7)
+    times = []
+    frames = reqs = 0
+    for i in range(args.warmup + args.steps):
+        f, r, dt, _ = cpu_baseline(setup, n_sample, threads)
+        if i >= args.warmup:
+            times.append(dt)
+            frames, reqs = f, r
+    t = float(np.mean(times))
+    v = frames / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config {CONFIG}: V=20000 H=256 MaxEnt 2^21, {n_sample} utt x "
+                               f"{args.frames} frames sample of the 64-utt batch, breadth 3, beam 8",
+                   "n_utt": n_sample, "frames": args.frames},
+        "rtf": (t / (frames * FRAME_S)),
+        "queries_per_s": reqs / t,
+        "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
+                         "sample": f"{n_sample} utterances x {args.frames} frames per step, "
+                                   "oracle/otflm_oracle.c (C restatement of the reference "
+                                   "decoder; numba/Python reference is not shipped)"},
+        "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    if args.out:
+        Path(args.out).write_text(json.dumps(line) + "\n")
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2007_11794_b200 import _lib, synth
+    from paper_2007_11794_b200.device import last_launch_count, profile_start, profile_stop
+    from paper_2007_11794_b200.rescore import BatchDecoder
+
+    setup = synth.build_setup(CONFIG, n_utt=args.n_utt, T=args.frames, seed=7 + 1000 * rank)
+    H = setup.model.hidden_size
+    need = BatchDecoder.contexts_needed(setup.lattices, setup.beam)
+    dec = BatchDecoder(setup.model, setup.tree, setup.small_lm, len(setup.lattices), need,
+                       precision=args.precision)
+    plan = dec.prepare(setup.lattices, setup.beam)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > L2
+    use_graph = not args.no_graph
+
+    for _ in range(args.warmup):
+        dec.run(1.0, use_graph=use_graph)
+    torch.cuda.synchronize()
+    launches_per_step = last_launch_count() + 1          # graph kernels + stream reset kernel
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()                                  # L2 flush between iterations
+            ev[i][0].record(stream)
+            dec.run(1.0, use_graph=use_graph)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    hyps, out = dec.fetch()
+    frames_per_step = int(sum(len(h.arcs) for h in hyps))
+    requests = int(out["expansions"].sum())
+    stats = dec.streams.stats()
+    misses = int(stats[:, 2].sum())
+    ms = total_ms / args.steps
+    value = frames_per_step * world / (ms / 1e3)
+
+    # ---- per-kernel CUDA-event timing (same run, non-graph launches) ----
+    profile_start()
+    dec.run(1.0, use_graph=False)
+    torch.cuda.synchronize()
+    prof = profile_stop()
+    cnt = plan.counters()
+    hbm, tc_peak, peak_src = peaks()
+    # algorithmic bytes: HS per query P(4H + 4k + 8) + 4H + 16;
+    # recurrent update per miss 3 x 4H (h_c read, U row read, h' write) and
+    # 2H^2 flops; W (H^2 x 4 B x passes) is re-read per 128-row tile.
+    hs_bytes = cnt["sum_path"] * (4 * H + 8) + 4 * cnt["sum_path_k"] + cnt["hs_queries"] * (4 * H + 16)
+    adv_flops = 2.0 * H * H * misses
+    kinds = {k: v for k, v in prof.items() if v[1] > 0}
+    dominant = max(kinds, key=lambda k: kinds[k][0])
+    dom_ms, dom_n = kinds[dominant]
+    if dominant == "hs":
+        roof = {"kernel": "k_hs_prim (HS + MaxEnt gather)", "bound": "hbm",
+                "achieved": hs_bytes / (dom_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}
+    elif dominant == "advance":
+        roof = {"kernel": f"recurrent update ({args.precision})", "bound": "tensor",
+                "achieved": adv_flops / (dom_ms / 1e3) / 1e12, "peak": tc_peak, "unit": "TFLOP/s"}
+    else:
+        # control kernels: bytes ~ requests x ~96 B of request/arrival state
+        roof = {"kernel": f"k_{dominant}", "bound": "hbm",
+                "achieved": requests * 96 / (dom_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["peak_source"] = peak_src
+    roof["launches"] = dom_n
+    roof["avg_launch_us"] = dom_ms * 1e3 / max(dom_n, 1)
+    kernel_ms = {k: round(v[0], 4) for k, v in prof.items() if v[1]}
+
+    # ---- end to end through the public API: host lattices in, 1-best out ----
+    e2e_ms = []
+    for i in range(max(2, min(args.steps, 5)) + 1):
+        torch.cuda.synchronize()
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dec.prepare(setup.lattices, setup.beam)          # host compile + H2D
+        dec.run(1.0, use_graph=False)
+        h2, o2 = dec.fetch()                             # D2H (synchronizes)
+        if world > 1:
+            rec = torch.from_numpy(np.concatenate([o2["combined"], o2["path_len"].astype(np.float64)])).cuda()
+            gathered = [torch.empty_like(rec) for _ in range(world)]
+            dist.all_gather(gathered, rec)                # NCCL: results only
+        b.record(stream)
+        torch.cuda.synchronize()
+        if i > 0:
+            e2e_ms.append(a.elapsed_time(b))
+    e2e = float(np.mean(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t.item())
+    d2h = int(sum(v.nbytes for v in o2.values()))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        n_sample = min(args.n_utt, max(threads, 16))
+        f, r, dt, ref = cpu_baseline(setup, n_sample, threads)
+        agree = sum(1 for u in range(n_sample) if hyps[u].arcs == ref[u][0].arcs)
+        cpu = {"value": f / dt, "unit": "frames/s", "cores": threads, "kind": "port",
+               "sample": f"{n_sample} of the {args.n_utt} utterances x {args.frames} frames "
+                         "(oracle/otflm_oracle.c, all host threads)",
+               "one_best_agreement": f"{agree}/{n_sample}"}
+
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 scores / f32 weights / " + args.precision + " recurrent update",
+        "data": "synthetic (seeded: RnnlmModel.new recipe + Zipf Huffman + synthetic bigram)",
+        "config": {"workload": f"config {CONFIG}: V=20000 H=256 MaxEnt 2^21 HS+MaxEnt RNNLM, "
+                               f"{args.n_utt} utterances x {args.frames} frames per GPU, breadth 3, "
+                               "beam 8, per-utterance streams (retain=False)",
+                   "n_utt_per_gpu": args.n_utt, "frames": args.frames, "beam": setup.beam,
+                   "precision": args.precision, "cuda_graph": use_graph,
+                   "l2": "flushed (256 MB write) between timed iterations"},
+        "rtf": (ms / 1e3) / (frames_per_step * FRAME_S) * (1 if world == 1 else 1),
+        "rtf_per_stream": (ms / 1e3) / (args.frames * FRAME_S),
+        "queries_per_s": misses * world / (ms / 1e3),
+        "requests_per_s": requests * world / (ms / 1e3),
+        "kernel_ms_per_step": kernel_ms,
+        "roofline": roof,
+        "e2e": {"value": frames_per_step * world / (e2e / 1e3), "unit": "frames/s",
+                "h2d_bytes_per_step": cnt["h2d_bytes"], "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+        if args.out:
+            Path(args.out).write_text(json.dumps(line) + "\n")
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

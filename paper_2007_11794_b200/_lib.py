@@ -20,6 +20,8 @@ ERR_VALUE, ERR_UNKNOWN_INDEX, ERR_TABLE_FULL, ERR_NO_PATH, ERR_KEY = -1, -2, -3,
 ERR_NOMEM, ERR_CYCLE, ERR_PACK, ERR_CUDA, ERR_HASH = -6, -7, -8, -9, -10
 
 PREC = {"fp64": 0, "tf32x3": 1, "bf16": 2, "tf32": 3}
+PROFILE_CATEGORIES = ("expand", "scan_prim", "level_begin", "hs", "advance", "dedup", "scan_novel",
+                      "resolve", "finish", "final", "misc")
 
 
 class UnknownIndexError(KeyError):
@@ -112,6 +114,8 @@ _SIGS = {
     "otflm_decode_fetch": (C.c_int, [_P, C.POINTER(DecodeResult), _P]),
     "otflm_decode": (C.c_int, [_P, _P, C.POINTER(LatticeBatch), C.c_double, C.c_int64, C.c_int32,
                                C.POINTER(DecodeResult), _P]),
+    "otflm_plan_counters": (C.c_int, [_P, _P, _P]),
+    "otflm_profile": (C.c_int, [C.c_int32, _P, _P]),
     "otflm_last_launch_count": (C.c_int64, []),
     "otflm_error_string": (C.c_char_p, [C.c_int32]),
     "otflm_last_error_detail": (C.c_char_p, []),

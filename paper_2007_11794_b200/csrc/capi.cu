@@ -38,6 +38,23 @@ static thread_local int64_t g_launches = 0;
         }                                                                        \
     } while (0)
 
+// ---- optional per-kernel CUDA-event timing (non-graph runs only) ----
+enum { K_EXPAND, K_SCAN_PRIM, K_LEVEL_BEGIN, K_HS, K_ADVANCE, K_DEDUP, K_SCAN_NOVEL, K_RESOLVE,
+       K_FINISH, K_FINAL, K_MISC, K_NCAT };
+static bool g_prof = false;
+static std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> g_prof_ev;
+static double g_prof_ms[K_NCAT];
+static long long g_prof_n[K_NCAT];
+struct ProfScope {
+    int cat; cudaStream_t s; cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(int c, cudaStream_t st) : cat(c), s(st) {
+        if (g_prof) { cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a, s); }
+    }
+    ~ProfScope() {
+        if (g_prof) { cudaEventRecord(b, s); g_prof_ev.push_back({cat, {a, b}}); }
+    }
+};
+
 static inline uint32_t pow2_at_least(uint64_t x) {
     uint64_t c = 16;
     while (c < x) c <<= 1;
@@ -131,6 +148,9 @@ extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, Otflm
         CK(cudaMemcpy(pcode, code.data(), (size_t)std::max<int64_t>(d->n_path, 1) * 4, cudaMemcpyHostToDevice));
     }
 #undef AL
+    dm.U = U; dm.W = W; dm.WT = WT; dm.NV = NV; dm.ME = ME;
+    dm.path_off = poff; dm.path_code = pcode;
+    dm.W_hi = Whi; dm.W_lo = Wlo; dm.W_bf = Wbf;
     if (W) {
         k_prep_weights<<<256, 256>>>(dm, WT, Whi, Wlo, Wbf);
         CK(cudaGetLastError());
@@ -585,6 +605,7 @@ struct OtflmPlan {
     uint32_t scan_nb = 1;
     cudaGraphExec_t gexec = nullptr;
     cudaGraph_t graph = nullptr;
+    uint64_t h2d_bytes = 0;
     double g_lm = 0; int g_prec = -1; const OtflmNgram *g_ng = nullptr; int64_t g_nodes = 0;
     std::vector<uint32_t> utt_stream_host;
 };
@@ -730,9 +751,11 @@ static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam,
     return OTFLM_OK;
 }
 
+static uint64_t g_upload_bytes = 0;
 template <class T>
 static int upload(Allocs &mem, T **dst, const std::vector<T> &v, cudaStream_t s) {
     if (mem.alloc(dst, v.size()) != cudaSuccess) { g_detail = "cudaMalloc plan"; return OTFLM_ERR_NOMEM; }
+    g_upload_bytes += v.size() * sizeof(T);
     if (!v.empty()) CK(cudaMemcpyAsync(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
     return OTFLM_OK;
 }
@@ -761,6 +784,7 @@ static int plan_alloc_workspace(OtflmPlan *p, uint32_t R, int S) {
     bad |= p->mem.alloc(&d.pr_p, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.first_E, (size_t)S) != cudaSuccess;
     bad |= p->mem.alloc(&d.counters, 4) != cudaSuccess;
+    bad |= p->mem.alloc(&d.alg, 4) != cudaSuccess;
     if (bad) { g_detail = "cudaMalloc workspace"; return OTFLM_ERR_NOMEM; }
     return OTFLM_OK;
 }
@@ -792,6 +816,7 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     p->utt_stream_host = utt_stream;
     DevPlan &d = p->d;
     NodeInfo *dn; uint32_t *dln, *dol, *das, *dss, *dus, *dfo, *dfi; int32_t *daw; double *dac, *dsl;
+    g_upload_bytes = 0;
     if ((rc = upload(p->mem, &dn, nodes, s)) || (rc = upload(p->mem, &dln, level_nodes, s)) ||
         (rc = upload(p->mem, &dol, out_list, s)) || (rc = upload(p->mem, &das, arc_slot, s)) ||
         (rc = upload(p->mem, &daw, arc_word, s)) || (rc = upload(p->mem, &dac, arc_ac, s)) ||
@@ -803,6 +828,7 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     d.nodes = dn; d.level_nodes = dln; d.out_list = dol; d.arc_slot = das; d.arc_word = daw;
     d.arc_ac = dac; d.arc_slm = dsl; d.n_utt = p->n_utt; d.utt_start_slot = dss; d.utt_stream = dus;
     d.final_off = dfo; d.finals = dfi;
+    p->h2d_bytes = g_upload_bytes;
     bool bad = p->mem.alloc(&d.arr, std::max<uint32_t>(p->n_slots, 1)) != cudaSuccess;
     bad |= p->mem.alloc(&d.slot_win, std::max<uint32_t>(p->n_slots, 1)) != cudaSuccess;
     uint32_t max_path = std::max<uint32_t>(p->n_levels, 1);
@@ -840,29 +866,63 @@ extern "C" int otflm_plan_info(const OtflmPlan *p, int64_t *o) {
     return OTFLM_OK;
 }
 
+extern "C" int otflm_plan_counters(const OtflmPlan *p, int64_t *o, void *stream) {
+    if (!p || !o) return OTFLM_ERR_VALUE;
+    unsigned long long a[4] = {0, 0, 0, 0};
+    CK(cudaMemcpyAsync(a, p->d.alg, sizeof(a), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    o[0] = (int64_t)a[0]; o[1] = (int64_t)a[1]; o[2] = (int64_t)a[2];
+    o[3] = (int64_t)p->h2d_bytes;
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_profile(int32_t enable, double *ms_out, int64_t *n_out) {
+    // enable=1 starts collecting per-kernel CUDA-event durations for
+    // non-graph runs; enable=0 synchronizes, reports and clears them.
+    if (enable) {
+        g_prof = true;
+        for (int i = 0; i < K_NCAT; i++) { g_prof_ms[i] = 0; g_prof_n[i] = 0; }
+        return OTFLM_OK;
+    }
+    for (auto &e : g_prof_ev) {
+        CK(cudaEventSynchronize(e.second.second));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
+        g_prof_ms[e.first] += ms;
+        g_prof_n[e.first] += 1;
+        cudaEventDestroy(e.second.first);
+        cudaEventDestroy(e.second.second);
+    }
+    g_prof_ev.clear();
+    g_prof = false;
+    for (int i = 0; i < K_NCAT; i++) { if (ms_out) ms_out[i] = g_prof_ms[i]; if (n_out) n_out[i] = g_prof_n[i]; }
+    return OTFLM_OK;
+}
+
 // the per-level pipeline shared by decode and rnnlm_prob_batch (after the
 // requests of the level exist)
 static int enqueue_miss_pipeline(OtflmPlan *p, const DevModel &m, DevStreams &S, uint32_t R, int prec,
                                  unsigned long long *status, uint32_t *ticket, cudaStream_t s) {
     DevPlan &d = p->d;
     const unsigned nb = cdiv(R, SCAN_BLK);
-    k_scan_prim<<<nb, SCAN_BLK, 0, s>>>(d, S, R, status, ticket);
-    CKL();
-    k_level_begin<<<1, 1, 0, s>>>(d, S);
-    CKL();
+    { ProfScope ps(K_SCAN_PRIM, s); k_scan_prim<<<nb, SCAN_BLK, 0, s>>>(d, S, R, status, ticket); CKL(); }
+    { ProfScope ps(K_LEVEL_BEGIN, s); k_level_begin<<<1, 1, 0, s>>>(d, S); CKL(); }
+    {
+        ProfScope ps(K_HS, s);
 #define CALL(VEC, CPL) k_hs_prim<VEC, CPL><<<cdiv(R, 8), 256, 0, s>>>(m, d, S, R)
-    HS_DISPATCH(m.H, CALL);
+        HS_DISPATCH(m.H, CALL);
 #undef CALL
-    CKL();
-    int rc = launch_advance(m, prec, R, &d.counters[0], d.pr_inrow, d.pr_w, S.arena_h, S.arena_h,
-                            &d.counters[2], s);
-    if (rc) return rc;
-    k_dedup<<<cdiv(R, 8), 256, 0, s>>>(d, S);
-    CKL();
-    k_scan_novel<<<nb, SCAN_BLK, 0, s>>>(d, S, status + p->scan_nb, ticket + 1);
-    CKL();
-    k_resolve<<<cdiv(R, 256), 256, 0, s>>>(d, S);
-    CKL();
+        CKL();
+    }
+    {
+        ProfScope ps(K_ADVANCE, s);
+        int rc = launch_advance(m, prec, R, &d.counters[0], d.pr_inrow, d.pr_w, S.arena_h, S.arena_h,
+                                &d.counters[2], s);
+        if (rc) return rc;
+    }
+    { ProfScope ps(K_DEDUP, s); k_dedup<<<cdiv(R, 8), 256, 0, s>>>(d, S); CKL(); }
+    { ProfScope ps(K_SCAN_NOVEL, s); k_scan_novel<<<nb, SCAN_BLK, 0, s>>>(d, S, status + p->scan_nb, ticket + 1); CKL(); }
+    { ProfScope ps(K_RESOLVE, s); k_resolve<<<cdiv(R, 256), 256, 0, s>>>(d, S); CKL(); }
     return OTFLM_OK;
 }
 
@@ -874,6 +934,7 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
     CK(cudaMemsetAsync(d.arr, 0xFF, (size_t)std::max<uint32_t>(p->n_slots, 1) * sizeof(Arrival), s));
     CK(cudaMemsetAsync(p->scan_status, 0, (size_t)std::max<uint32_t>(p->n_levels, 1) * 2 * p->scan_nb * 8, s));
     CK(cudaMemsetAsync(p->scan_ticket, 0, (size_t)std::max<uint32_t>(p->n_levels, 1) * 2 * 4, s));
+    CK(cudaMemsetAsync(d.alg, 0, 4 * sizeof(unsigned long long), s));
     k_init_starts<<<cdiv(p->n_utt, 128), 128, 0, s>>>(d);
     CKL();
     k_run_begin<<<cdiv(S.S, 128), 128, 0, s>>>(S);
@@ -884,16 +945,13 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
         unsigned long long *status = p->scan_status + (size_t)t * 2 * p->scan_nb;
         uint32_t *ticket = p->scan_ticket + (size_t)t * 2;
         if (nn == 0) continue;
-        k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, nb0, nn, (long long)p->beam, t);
-        CKL();
+        { ProfScope ps(K_EXPAND, s); k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, nb0, nn, (long long)p->beam, t); CKL(); }
         if (R == 0) continue;
         int rc = enqueue_miss_pipeline(p, m, S, R, prec, status, ticket, s);
         if (rc) return rc;
-        k_finish<<<cdiv(std::max<uint64_t>(R, (uint64_t)S.S), 256), 256, 0, s>>>(d, S, g->d, R, t, lm);
-        CKL();
+        { ProfScope ps(K_FINISH, s); k_finish<<<cdiv(std::max<uint64_t>(R, (uint64_t)S.S), 256), 256, 0, s>>>(d, S, g->d, R, t, lm); CKL(); }
     }
-    k_final<<<cdiv(p->n_utt, 4), 128, 0, s>>>(d, S, lm);
-    CKL();
+    { ProfScope ps(K_FINAL, s); k_final<<<cdiv(p->n_utt, 4), 128, 0, s>>>(d, S, lm); CKL(); }
     return OTFLM_OK;
 }
 

@@ -45,6 +45,7 @@ struct DevPlan {
     double *pr_p;
     uint32_t *first_E;            // [S]
     uint32_t *counters;           // [0] n_prim, [1] n_novel, [2] arena_base
+    unsigned long long *alg;      // run totals: [0] sum P, [1] sum P*k, [2] HS queries
     // outputs
     int32_t *out_len, *out_arcs, *out_status;
     double *out_combined, *out_acoustic, *out_lm;
@@ -288,6 +289,12 @@ __global__ void __launch_bounds__(256) k_hs_prim(DevModel m, DevPlan P, DevStrea
                                           m.path_code + o0, o1 - o0, lane);
     const uint32_t base = P.counters[2];
     if (lane == 0) {
+        if (P.alg) {   // algorithmic-work counters for the roofline (bench.py)
+            const int km = m.order < L ? m.order : L;
+            atomicAdd(&P.alg[0], (unsigned long long)(o1 - o0));
+            atomicAdd(&P.alg[1], (unsigned long long)(o1 - o0) * km);
+            atomicAdd(&P.alg[2], 1ull);
+        }
         P.pr_p[q] = lp;
         uint32_t *mo = S.arena_meta + (size_t)(base + q) * OTF_META;
         int nl = L + 1 > m.order ? m.order : L + 1;

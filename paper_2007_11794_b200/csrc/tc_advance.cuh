@@ -1,8 +1,345 @@
-// tc_advance.cuh -- tcgen05 recurrent update (placeholder until the kernel lands)
+// tc_advance.cuh -- the recurrent update h' = sigmoid(U[w] + W h) batched
+// over all new (history, word) queries of a level, as a tcgen05 GEMM
+// (reference _kernels_nb.py:51-60; the only dense contraction of the path).
+//
+//   D[q, i] = sum_j A[q, j] * W[i, j]       A[q] = h of query q's context
+//   M = queries (128-row tiles), N = H outputs, K = H.
+//
+// Both operands are K-major in shared memory in the canonical no-swizzle
+// UMMA layout (8-row x 16-byte core matrices, LBO = 128 B between K-adjacent
+// core matrices, SBO = KC_B/16*128 B between 8-row groups).  A rows are
+// GATHERED (the context arena row of each query) with coalesced 16-byte
+// loads and written to shared memory already converted (tf32 round /
+// hi-lo split / bf16); B (W, pre-split once at model upload) streams through
+// a multi-stage cp.async ring.  One elected thread issues tcgen05.mma with
+// the accumulator in TMEM (128 lanes x N_pad fp32 columns) and commits each
+// stage to an mbarrier that releases the stage for the next loads.  The
+// epilogue (4 warps, one TMEM lane per thread) reads the accumulator with
+// tcgen05.ld, adds U[w] and applies the sigmoid in fp32, and writes h' into
+// its arena row.
+//
+// Precision modes: TF32X3 = hi*hi + hi*lo + lo*hi (fp32-faithful, ~1e-7
+// relative), TF32 = one pass, BF16 = kind::f16 with bf16 operands.
 #pragma once
 #include "common.cuh"
+
+namespace tc {
+
+constexpr int BM = 128;      // rows per CTA tile (UMMA_M)
+constexpr int KC_B = 64;     // bytes of K per row per pipeline stage
+constexpr int NTHREADS = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= 1ull << 46;                 // descriptor version (sm_100)
+    return d;                        // base_offset 0, lbo_mode 0, SWIZZLE_NONE
+}
+
+// instruction descriptor: D fp32, A/B K-major, M = 128, N = n
+__host__ __device__ constexpr uint32_t make_idesc(int ab_fmt, int n) {
+    return (1u << 4) | ((uint32_t)ab_fmt << 7) | ((uint32_t)ab_fmt << 10) |
+           ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONE_%=;\n\t"
+        "bra WAIT_%=;\n\t"
+        "DONE_%=:\n\t}" :: "r"(a), "r"(parity) : "memory");
+}
+
+template <bool BF16>
+__device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if (BF16) {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                     :: "r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    } else {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                     :: "r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    }
+}
+
+__device__ __forceinline__ void commit(uint32_t mbar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 :: "r"(mbar) : "memory");
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g, bool valid) {
+    const int sz = valid ? 16 : 0;   // zero-fill out-of-range chunks
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(saddr), "l"(g), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ float tf32_rn(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int j = 0; j < 32; j++) v[j] = __uint_as_float(r[j]);
+}
+
+// smem offset of (row, 16-byte chunk c) inside a [rows x KC_B] operand tile
+__device__ __forceinline__ uint32_t tile_off(int row, int c) {
+    return (uint32_t)((row >> 3) * (KC_B / 16 * 128) + c * 128 + (row & 7) * 16);
+}
+
+// MODE: 1 = TF32X3, 2 = BF16, 3 = TF32
+template <int MODE>
+__global__ void __launch_bounds__(NTHREADS, 1)
+k_advance_tc(DevModel m, uint32_t n_cap, const uint32_t *n_dev, const int32_t *__restrict__ in_row,
+             const int32_t *__restrict__ words, const float *__restrict__ h_base,
+             float *__restrict__ out_base, const uint32_t *out_row0_dev, int n_pad, int stages,
+             uint32_t tmem_cols) {
+    constexpr bool BF = MODE == 2;
+    constexpr bool X3 = MODE == 1;
+    constexpr int ELT = BF ? 2 : 4;                   // bytes per operand element
+    constexpr int KC = KC_B / ELT;                     // K elements per stage
+    constexpr int CH = KC_B / 16;                      // 16-byte chunks per row per stage
+    const uint32_t n = n_dev ? *n_dev : n_cap;
+    const uint32_t q0 = blockIdx.x * BM;
+    if (q0 >= n) return;
+    const int H = m.H;
+    const int tid = threadIdx.x, warp = tid >> 5;
+
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t a_bytes = BM * KC_B;
+    const uint32_t b_bytes = (uint32_t)n_pad * KC_B;
+    const uint32_t stage_bytes = (X3 ? 2 : 1) * (a_bytes + b_bytes);
+    uint8_t *ring = smem;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + stages * stage_bytes);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + stages + 1);
+    __shared__ int32_t s_row[BM], s_w[BM];
+
+    if (tid < BM) {
+        const uint32_t q = q0 + tid;
+        s_row[tid] = q < n ? in_row[q] : -1;
+        s_w[tid] = q < n ? (words ? words[q] : (int32_t)q) : 0;
+    }
+    if (tid == 0) {
+        for (int s = 0; s <= stages; s++) mbar_init(smem_u32(&bars[s]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                     :: "r"(smem_u32(tmem_slot)), "r"(tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    const int NK = (H * ELT + KC_B - 1) / KC_B;        // pipeline steps over K
+    const uint32_t sbo = CH * 128, lbo = 128;
+    const int nhalf = n_pad > 256 ? 2 : 1;
+    const int nmma = n_pad > 256 ? n_pad / 2 : n_pad;
+    const uint32_t idesc = make_idesc(BF ? 1 : 2, nmma);
+
+    for (int kc = 0; kc < NK; kc++) {
+        const int st = kc % stages;
+        const int use = kc / stages;
+        if (kc >= stages) mbar_wait(smem_u32(&bars[st]), (uint32_t)((use - 1) & 1));
+        uint8_t *sA = ring + st * stage_bytes;
+        uint8_t *sB = sA + a_bytes;
+        uint8_t *sA2 = sB + b_bytes;          // X3: A_lo, B_lo follow
+        uint8_t *sB2 = sA2 + a_bytes;
+        const int k0 = kc * KC;               // first K element of this stage
+        // ---- B (W rows = outputs) via cp.async, zero-filled past H ----
+        for (int idx = tid; idx < n_pad * CH; idx += NTHREADS) {
+            const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
+            const int row = g * 8 + r8;
+            const int kk = k0 + c * (16 / ELT);
+            const bool ok = row < H && kk < H;
+            const uint32_t off = tile_off(row, c);
+            if (BF) {
+                cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_bf + (size_t)row * H + kk) : (const void *)m.W_bf, ok);
+            } else {
+                cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_hi + (size_t)row * H + kk) : (const void *)m.W_hi, ok);
+                if (X3)
+                    cp_async16(smem_u32(sB2 + off), ok ? (const void *)(m.W_lo + (size_t)row * H + kk) : (const void *)m.W_lo, ok);
+            }
+        }
+        cp_async_commit();
+        // ---- A (gathered context rows), converted in registers ----
+        for (int idx = tid; idx < BM * CH; idx += NTHREADS) {
+            const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
+            const int row = g * 8 + r8;
+            const int src = s_row[row];
+            const uint32_t off = tile_off(row, c);
+            if (BF) {
+                const int kk = k0 + c * 8;
+                float v[8];
+#pragma unroll
+                for (int e = 0; e < 8; e++) v[e] = 0.f;
+                if (src >= 0) {
+                    const float *p = h_base + (size_t)src * H + kk;
+                    if (kk + 8 <= H && (H & 3) == 0) {
+                        float4 x0 = __ldg(reinterpret_cast<const float4 *>(p));
+                        float4 x1 = __ldg(reinterpret_cast<const float4 *>(p) + 1);
+                        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+                        v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+                    } else {
+                        for (int e = 0; e < 8; e++) if (kk + e < H) v[e] = __ldg(p + e);
+                    }
+                }
+                __nv_bfloat162 b0 = __floats2bfloat162_rn(v[0], v[1]);
+                __nv_bfloat162 b1 = __floats2bfloat162_rn(v[2], v[3]);
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(v[4], v[5]);
+                __nv_bfloat162 b3 = __floats2bfloat162_rn(v[6], v[7]);
+                uint4 u;
+                u.x = *reinterpret_cast<uint32_t *>(&b0); u.y = *reinterpret_cast<uint32_t *>(&b1);
+                u.z = *reinterpret_cast<uint32_t *>(&b2); u.w = *reinterpret_cast<uint32_t *>(&b3);
+                *reinterpret_cast<uint4 *>(sA + off) = u;
+            } else {
+                const int kk = k0 + c * 4;
+                float v[4] = {0.f, 0.f, 0.f, 0.f};
+                if (src >= 0) {
+                    const float *p = h_base + (size_t)src * H + kk;
+                    if (kk + 4 <= H && (H & 3) == 0) {
+                        float4 x = __ldg(reinterpret_cast<const float4 *>(p));
+                        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+                    } else {
+                        for (int e = 0; e < 4; e++) if (kk + e < H) v[e] = __ldg(p + e);
+                    }
+                }
+                float4 hi, lo;
+                hi.x = tf32_rn(v[0]); hi.y = tf32_rn(v[1]); hi.z = tf32_rn(v[2]); hi.w = tf32_rn(v[3]);
+                *reinterpret_cast<float4 *>(sA + off) = hi;
+                if (X3) {
+                    lo.x = tf32_rn(v[0] - hi.x); lo.y = tf32_rn(v[1] - hi.y);
+                    lo.z = tf32_rn(v[2] - hi.z); lo.w = tf32_rn(v[3] - hi.w);
+                    *reinterpret_cast<float4 *>(sA2 + off) = lo;
+                }
+            }
+        }
+        cp_async_wait_all();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int ks = 0; ks < KC_B / 32; ks++) {          // 32 bytes of K per MMA
+                for (int hh = 0; hh < nhalf; hh++) {
+                    const uint32_t d = tmem + (uint32_t)(hh * nmma);
+                    const uint32_t boff = (uint32_t)(hh * nmma / 8) * sbo + ks * 2 * lbo;
+                    const uint64_t a_hi = make_desc(smem_u32(sA) + ks * 2 * lbo, lbo, sbo);
+                    const uint64_t b_hi = make_desc(smem_u32(sB) + boff, lbo, sbo);
+                    const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+                    mma<BF>(d, a_hi, b_hi, idesc, acc);
+                    if (X3) {
+                        const uint64_t a_lo = make_desc(smem_u32(sA2) + ks * 2 * lbo, lbo, sbo);
+                        const uint64_t b_lo = make_desc(smem_u32(sB2) + boff, lbo, sbo);
+                        mma<false>(d, a_hi, b_lo, idesc, 1u);
+                        mma<false>(d, a_lo, b_hi, idesc, 1u);
+                    }
+                }
+            }
+            commit(smem_u32(&bars[st]));
+        }
+    }
+    // all MMAs done: the last commit's barrier (MMAs complete in order)
+    {
+        const int kl = NK - 1;
+        mbar_wait(smem_u32(&bars[kl % stages]), (uint32_t)((kl / stages) & 1));
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+    // ---- epilogue: TMEM lane = row = tid ----
+    const int row = tid;
+    const uint32_t q = q0 + row;
+    const bool valid = q < n;
+    const uint32_t out0 = out_row0_dev ? *out_row0_dev : 0u;
+    const float *urow = m.U + (size_t)s_w[row] * H;
+    float *orow = out_base + (size_t)(out0 + q) * H;
+    for (int c0 = 0; c0 < n_pad; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        if (valid) {
+            if ((H & 3) == 0 && c0 + 32 <= H) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                    float4 u = __ldg(reinterpret_cast<const float4 *>(urow + c0 + j));
+                    float4 o;
+                    o.x = 1.f / (1.f + expf(-(v[j] + u.x)));
+                    o.y = 1.f / (1.f + expf(-(v[j + 1] + u.y)));
+                    o.z = 1.f / (1.f + expf(-(v[j + 2] + u.z)));
+                    o.w = 1.f / (1.f + expf(-(v[j + 3] + u.w)));
+                    *reinterpret_cast<float4 *>(orow + c0 + j) = o;
+                }
+            } else {
+                for (int j = 0; j < 32; j++)
+                    if (c0 + j < H) orow[c0 + j] = 1.f / (1.f + expf(-(v[j] + urow[c0 + j])));
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(tmem_cols));
+}
+
+}  // namespace tc
+
 static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const uint32_t *n_dev,
                              const int32_t *in_row, const int32_t *words, const float *h_base,
                              float *out_base, const uint32_t *out_row0, cudaStream_t s) {
-    return -1;
+    const int H = m.H;
+    // N per MMA must be a multiple of 16 (M = 128); above 256 the N range is
+    // split into two MMAs, so pad to 32
+    const int n_pad = H > 256 ? (H + 31) / 32 * 32 : (H + 15) / 16 * 16;
+    if (n_pad > 512) return -1;
+    uint32_t cols = 32;
+    while ((int)cols < n_pad) cols <<= 1;
+    const bool x3 = prec == 1;
+    const uint32_t stage_bytes = (x3 ? 2u : 1u) * (uint32_t)(tc::BM + n_pad) * tc::KC_B;
+    const int elt = prec == 2 ? 2 : 4;
+    const int nk = (H * elt + tc::KC_B - 1) / tc::KC_B;
+    int stages = (int)std::min<uint32_t>(4u, (200u * 1024u) / stage_bytes);
+    stages = std::max(1, std::min(stages, nk));
+    const size_t smem = (size_t)stages * stage_bytes + (stages + 1) * 8 + 16 + 1024;
+    const dim3 grid((n_cap + tc::BM - 1) / tc::BM);
+    cudaError_t e;
+#define TC_LAUNCH(MODE)                                                                         \
+    do {                                                                                        \
+        e = cudaFuncSetAttribute(tc::k_advance_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e != cudaSuccess) return -9;                                                        \
+        tc::k_advance_tc<MODE><<<grid, tc::NTHREADS, smem, s>>>(m, n_cap, n_dev, in_row, words, h_base, \
+                                                                 out_base, out_row0, n_pad, stages, cols); \
+    } while (0)
+    if (prec == 1) TC_LAUNCH(1);
+    else if (prec == 2) TC_LAUNCH(2);
+    else if (prec == 3) TC_LAUNCH(3);
+    else return -1;
+#undef TC_LAUNCH
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : -9;
 }

@@ -230,6 +230,13 @@ class Plan:
         _lib.check(_lib.load().otflm_plan_info(self.handle, _p(out)), "plan info")
         return out
 
+    def counters(self) -> dict:
+        out = np.zeros(4, np.int64)
+        _lib.check(_lib.load().otflm_plan_counters(self.handle, _p(out), current_stream_ptr()),
+                   "plan counters")
+        return dict(sum_path=int(out[0]), sum_path_k=int(out[1]), hs_queries=int(out[2]),
+                    h2d_bytes=int(out[3]))
+
     def run(self, ngram: DeviceNgram, lm_weight: float = 1.0, precision: str = "fp64",
             use_graph: bool = True, stream: int | None = None) -> None:
         _lib.check(_lib.load().otflm_decode_run(
@@ -249,6 +256,17 @@ class Plan:
                                                   current_stream_ptr() if stream is None else stream),
                    "decode")
         return out
+
+
+def profile_start() -> None:
+    _lib.check(_lib.load().otflm_profile(1, None, None), "profile")
+
+
+def profile_stop() -> dict:
+    ms = np.zeros(len(_lib.PROFILE_CATEGORIES))
+    n = np.zeros(len(_lib.PROFILE_CATEGORIES), np.int64)
+    _lib.check(_lib.load().otflm_profile(0, _p(ms), _p(n)), "profile")
+    return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(_lib.PROFILE_CATEGORIES)}
 
 
 def last_launch_count() -> int:

@@ -300,9 +300,9 @@ class TraversalReport:
     transfer: TransferLedger
 
 
-def _hyp(out, u, lat) -> PathHypothesis:
+def _hyp(out, u, lat, arc_base: int = 0) -> PathHypothesis:
     n = int(out["path_len"][u])
-    arcs = tuple(int(a) for a in out["path_arcs"][u, :n])
+    arcs = tuple(int(a) - arc_base for a in out["path_arcs"][u, :n])   # batch -> lattice arc ids
     words = tuple(int(lat.arc_word[a]) for a in arcs)
     return PathHypothesis(arcs, words, float(out["acoustic"][u]), float(out["lm"][u]),
                           float(out["combined"][u]), int(out["end_ctx"][u]))
@@ -370,7 +370,8 @@ class BatchDecoder:
 
     def fetch(self):
         out = self.plan.fetch()
-        return [_hyp(out, u, self.plan.lats[u]) for u in range(self.plan.n_utt)], out
+        offs = self.plan.arrays["arc_off"]
+        return [_hyp(out, u, self.plan.lats[u], int(offs[u])) for u in range(self.plan.n_utt)], out
 
 
 def rescore_batch(lattices: Sequence, small_lm, model, tree, lm_weight: float = 1.0,

@@ -27,7 +27,7 @@ def _stack(gm, enabled=True):
     from paper_2007_11794_b200 import IndexTable, RescoreCache, RescoreStack
     m = gm.model
     return RescoreStack(model=m, tree=gm.tree, table=IndexTable(m.hidden_size, m.maxent_order,
-                                                                device_capacity=1 << 14),
+                                                                device_capacity=1 << 17),
                         cache=RescoreCache(enabled=enabled))
 
 
