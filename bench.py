@@ -176,7 +176,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2007_11794_b200 import _lib, synth
-    from paper_2007_11794_b200.device import last_launch_count, profile_start, profile_stop
+    from paper_2007_11794_b200.device import last_launch_count
     from paper_2007_11794_b200.rescore import BatchDecoder
 
     setup = synth.build_setup(CONFIG, n_utt=args.n_utt, T=args.frames, seed=7 + 1000 * rank)
@@ -220,11 +220,10 @@ def main():
     ms = total_ms / args.steps
     value = frames_per_step * world / (ms / 1e3)
 
-    # ---- per-kernel CUDA-event timing (same run, non-graph launches) ----
-    profile_start()
-    dec.run(1.0, use_graph=False)
-    torch.cuda.synchronize()
-    prof = profile_stop()
+    # ---- per-kernel CUDA-event timing: one run replayed from a graph with
+    # event-record nodes around every kernel (device-side spans) ----
+    dec.streams.reset(retain=False)
+    prof = plan.profile(dec.ngram, 1.0, args.precision)
     cnt = plan.counters()
     hbm, tc_peak, peak_src = peaks()
     # algorithmic bytes: HS per query P(4H + 4k + 8) + 4H + 16;

@@ -193,11 +193,12 @@ int otflm_plan_info(const OtflmPlan *p, int64_t *out8);
  * sum of Huffman path lengths over HS queries, sum of path length x MaxEnt
  * orders, HS queries, bytes uploaded by plan_create. */
 int otflm_plan_counters(const OtflmPlan *p, int64_t *out4, void *stream);
-/* Per-kernel CUDA-event timing of non-graph runs: enable=1 starts, enable=0
- * stops and writes total ms / launch counts per category (11 entries:
- * expand, scan_prim, level_begin, hs, advance, dedup, scan_novel, resolve,
- * finish, final, misc). */
-int otflm_profile(int32_t enable, double *ms_out, int64_t *n_out);
+/* One decode run captured as a CUDA graph with an event-record node around
+ * every kernel; writes device-side total ms / launch counts per category
+ * (11 entries: expand, scan_prim, level_begin, hs, advance, dedup,
+ * scan_novel, resolve, finish, final, misc). */
+int otflm_decode_profile(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
+                         void *stream, double *ms_out, int64_t *n_out);
 /* Device-only decode of a prepared plan (inputs already resident in HBM).
  * use_graph != 0 replays a captured CUDA graph of the level loop. */
 int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,

@@ -115,7 +115,7 @@ _SIGS = {
     "otflm_decode": (C.c_int, [_P, _P, C.POINTER(LatticeBatch), C.c_double, C.c_int64, C.c_int32,
                                C.POINTER(DecodeResult), _P]),
     "otflm_plan_counters": (C.c_int, [_P, _P, _P]),
-    "otflm_profile": (C.c_int, [C.c_int32, _P, _P]),
+    "otflm_decode_profile": (C.c_int, [_P, _P, C.c_double, C.c_int32, _P, _P, _P]),
     "otflm_last_launch_count": (C.c_int64, []),
     "otflm_error_string": (C.c_char_p, [C.c_int32]),
     "otflm_last_error_detail": (C.c_char_p, []),

@@ -45,13 +45,22 @@ static bool g_prof = false;
 static std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> g_prof_ev;
 static double g_prof_ms[K_NCAT];
 static long long g_prof_n[K_NCAT];
+// Recorded only while capturing a profiling graph: external event-record
+// nodes around each kernel, so the timings are device-side kernel spans of a
+// graph replay (no host launch gaps).
 struct ProfScope {
     int cat; cudaStream_t s; cudaEvent_t a = nullptr, b = nullptr;
     ProfScope(int c, cudaStream_t st) : cat(c), s(st) {
-        if (g_prof) { cudaEventCreate(&a); cudaEventCreate(&b); cudaEventRecord(a, s); }
+        if (g_prof) {
+            cudaEventCreate(&a); cudaEventCreate(&b);
+            cudaEventRecordWithFlags(a, s, cudaEventRecordExternal);
+        }
     }
     ~ProfScope() {
-        if (g_prof) { cudaEventRecord(b, s); g_prof_ev.push_back({cat, {a, b}}); }
+        if (g_prof) {
+            cudaEventRecordWithFlags(b, s, cudaEventRecordExternal);
+            g_prof_ev.push_back({cat, {a, b}});
+        }
     }
 };
 
@@ -606,6 +615,7 @@ struct OtflmPlan {
     cudaGraphExec_t gexec = nullptr;
     cudaGraph_t graph = nullptr;
     uint64_t h2d_bytes = 0;
+    unsigned long long *alg_buf = nullptr;
     double g_lm = 0; int g_prec = -1; const OtflmNgram *g_ng = nullptr; int64_t g_nodes = 0;
     std::vector<uint32_t> utt_stream_host;
 };
@@ -784,7 +794,8 @@ static int plan_alloc_workspace(OtflmPlan *p, uint32_t R, int S) {
     bad |= p->mem.alloc(&d.pr_p, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.first_E, (size_t)S) != cudaSuccess;
     bad |= p->mem.alloc(&d.counters, 4) != cudaSuccess;
-    bad |= p->mem.alloc(&d.alg, 4) != cudaSuccess;
+    bad |= p->mem.alloc(&p->alg_buf, 4) != cudaSuccess;
+    d.alg = nullptr;   // counters are only maintained in profiling runs
     if (bad) { g_detail = "cudaMalloc workspace"; return OTFLM_ERR_NOMEM; }
     return OTFLM_OK;
 }
@@ -869,33 +880,10 @@ extern "C" int otflm_plan_info(const OtflmPlan *p, int64_t *o) {
 extern "C" int otflm_plan_counters(const OtflmPlan *p, int64_t *o, void *stream) {
     if (!p || !o) return OTFLM_ERR_VALUE;
     unsigned long long a[4] = {0, 0, 0, 0};
-    CK(cudaMemcpyAsync(a, p->d.alg, sizeof(a), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CK(cudaMemcpyAsync(a, p->alg_buf, sizeof(a), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     o[0] = (int64_t)a[0]; o[1] = (int64_t)a[1]; o[2] = (int64_t)a[2];
     o[3] = (int64_t)p->h2d_bytes;
-    return OTFLM_OK;
-}
-
-extern "C" int otflm_profile(int32_t enable, double *ms_out, int64_t *n_out) {
-    // enable=1 starts collecting per-kernel CUDA-event durations for
-    // non-graph runs; enable=0 synchronizes, reports and clears them.
-    if (enable) {
-        g_prof = true;
-        for (int i = 0; i < K_NCAT; i++) { g_prof_ms[i] = 0; g_prof_n[i] = 0; }
-        return OTFLM_OK;
-    }
-    for (auto &e : g_prof_ev) {
-        CK(cudaEventSynchronize(e.second.second));
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
-        g_prof_ms[e.first] += ms;
-        g_prof_n[e.first] += 1;
-        cudaEventDestroy(e.second.first);
-        cudaEventDestroy(e.second.second);
-    }
-    g_prof_ev.clear();
-    g_prof = false;
-    for (int i = 0; i < K_NCAT; i++) { if (ms_out) ms_out[i] = g_prof_ms[i]; if (n_out) n_out[i] = g_prof_n[i]; }
     return OTFLM_OK;
 }
 
@@ -934,7 +922,7 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
     CK(cudaMemsetAsync(d.arr, 0xFF, (size_t)std::max<uint32_t>(p->n_slots, 1) * sizeof(Arrival), s));
     CK(cudaMemsetAsync(p->scan_status, 0, (size_t)std::max<uint32_t>(p->n_levels, 1) * 2 * p->scan_nb * 8, s));
     CK(cudaMemsetAsync(p->scan_ticket, 0, (size_t)std::max<uint32_t>(p->n_levels, 1) * 2 * 4, s));
-    CK(cudaMemsetAsync(d.alg, 0, 4 * sizeof(unsigned long long), s));
+    if (d.alg) CK(cudaMemsetAsync(d.alg, 0, 4 * sizeof(unsigned long long), s));
     k_init_starts<<<cdiv(p->n_utt, 128), 128, 0, s>>>(d);
     CKL();
     k_run_begin<<<cdiv(S.S, 128), 128, 0, s>>>(S);
@@ -997,6 +985,43 @@ extern "C" int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_wei
 }
 
 extern "C" int64_t otflm_last_launch_count(void) { return g_last_launches; }
+extern "C" int otflm_decode_profile(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
+                                    void *stream, double *ms_out, int64_t *n_out) {
+    if (!p || !g) return OTFLM_ERR_VALUE;
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int i = 0; i < K_NCAT; i++) { g_prof_ms[i] = 0; g_prof_n[i] = 0; }
+    cudaStream_t cs;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    g_prof = true;
+    p->d.alg = p->alg_buf;
+    int rc = enqueue_run(p, g, lm_weight, precision, cs);
+    p->d.alg = nullptr;
+    g_prof = false;
+    cudaGraph_t graph;
+    cudaError_t e = cudaStreamEndCapture(cs, &graph);
+    cudaStreamDestroy(cs);
+    if (rc) return rc;
+    CK(e);
+    cudaGraphExec_t ex;
+    CK(cudaGraphInstantiate(&ex, graph, 0));
+    CK(cudaGraphLaunch(ex, s));
+    CK(cudaStreamSynchronize(s));
+    for (auto &ev : g_prof_ev) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev.second.first, ev.second.second));
+        g_prof_ms[ev.first] += ms;
+        g_prof_n[ev.first] += 1;
+        cudaEventDestroy(ev.second.first);
+        cudaEventDestroy(ev.second.second);
+    }
+    g_prof_ev.clear();
+    cudaGraphExecDestroy(ex);
+    cudaGraphDestroy(graph);
+    for (int i = 0; i < K_NCAT; i++) { if (ms_out) ms_out[i] = g_prof_ms[i]; if (n_out) n_out[i] = g_prof_n[i]; }
+    return OTFLM_OK;
+}
+
 
 extern "C" int otflm_decode_fetch(OtflmPlan *p, OtflmDecodeResult *r, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;

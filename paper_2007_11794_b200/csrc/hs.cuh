@@ -27,7 +27,7 @@ __device__ __forceinline__ double hs_logprob_warp(const DevModel &m, const float
                                                   int lane) {
     const int H = m.H;
     const int NCH = VEC == 4 ? (H >> 2) : H;   // chunks of VEC floats
-    float hv[CPL][VEC];
+    double hv[CPL][VEC];                        // hidden state, converted once
 #pragma unroll
     for (int c = 0; c < CPL; c++) {
         int k = lane + 32 * c;
@@ -40,7 +40,7 @@ __device__ __forceinline__ double hs_logprob_warp(const DevModel &m, const float
             }
         } else {
 #pragma unroll
-            for (int v = 0; v < VEC; v++) hv[c][v] = 0.f;
+            for (int v = 0; v < VEC; v++) hv[c][v] = 0.0;
         }
     }
     // MaxEnt hash prefixes: order-k feature hashes (k, last k words oldest
@@ -62,32 +62,8 @@ __device__ __forceinline__ double hs_logprob_warp(const DevModel &m, const float
         double acc[HS_G];
 #pragma unroll
         for (int g = 0; g < HS_G; g++) code[g] = (p0 + g < P) ? __ldg(codes + p0 + g) : OTF_UNSET;
-#pragma unroll
-        for (int g = 0; g < HS_G; g++) {
-            acc[g] = 0.0;
-            if (code[g] != OTF_UNSET) {
-                const float *row = m.NV + (size_t)(code[g] & 0x7FFFFFFFu) * H;
-#pragma unroll
-                for (int c = 0; c < CPL; c++) {
-                    int k = lane + 32 * c;
-                    if (k < NCH) {
-                        if (VEC == 4) {
-                            float4 t = __ldg(reinterpret_cast<const float4 *>(row) + k);
-                            acc[g] = fma((double)t.x, (double)hv[c][0], acc[g]);
-                            acc[g] = fma((double)t.y, (double)hv[c][1], acc[g]);
-                            acc[g] = fma((double)t.z, (double)hv[c][2], acc[g]);
-                            acc[g] = fma((double)t.w, (double)hv[c][3], acc[g]);
-                        } else {
-                            acc[g] = fma((double)__ldg(row + k), (double)hv[c][0], acc[g]);
-                        }
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int g = 0; g < HS_G; g++) acc[g] = warp_sum_d(acc[g]);
-        // MaxEnt gathers: lane j -> (node g = j / kmax, order k = j % kmax)
-        // (lanes >= 32 are only needed for order > 4 and are recomputed below)
+        // MaxEnt gathers first (independent of the dot products): lane j ->
+        // (node g = j / kmax, order k = j % kmax); order > 4 spills below
         double me = 0.0;
         if (lane < HS_G * kmax) {
             int g = lane / kmax, k = lane - g * kmax;
@@ -101,18 +77,40 @@ __device__ __forceinline__ double hs_logprob_warp(const DevModel &m, const float
                 me = (double)__ldg(m.ME + idx);
             }
         }
-        // node activation a_g = dot + ME[k=1] + ME[k=2] + ... in order
-        double mylog = 0.0;
+#pragma unroll
+        for (int g = 0; g < HS_G; g++) {
+            acc[g] = 0.0;
+            if (code[g] != OTF_UNSET) {
+                const float *row = m.NV + (size_t)(code[g] & 0x7FFFFFFFu) * H;
+#pragma unroll
+                for (int c = 0; c < CPL; c++) {
+                    int k = lane + 32 * c;
+                    if (k < NCH) {
+                        if (VEC == 4) {
+                            float4 t = __ldg(reinterpret_cast<const float4 *>(row) + k);
+                            acc[g] = fma((double)t.x, hv[c][0], acc[g]);
+                            acc[g] = fma((double)t.y, hv[c][1], acc[g]);
+                            acc[g] = fma((double)t.z, hv[c][2], acc[g]);
+                            acc[g] = fma((double)t.w, hv[c][3], acc[g]);
+                        } else {
+                            acc[g] = fma((double)__ldg(row + k), hv[c][0], acc[g]);
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int g = 0; g < HS_G; g++) acc[g] = warp_sum_d(acc[g]);
+        // node activation a_g = dot + ME[k=1] + ME[k=2] + ... in order; lane g
+        // keeps a_g and all G log-sigmoids are evaluated in one pass
+        double my_a = 0.0;
 #pragma unroll
         for (int g = 0; g < HS_G; g++) {
             double a = acc[g];
             for (int k = 0; k < kmax; k++) {
                 int j = g * kmax + k;
-                double v;
-                double vs = __shfl_sync(0xffffffffu, me, j & 31);
-                if (j < 32) {
-                    v = vs;
-                } else {  // order > 4 overflow: recompute directly
+                double v = __shfl_sync(0xffffffffu, me, j & 31);
+                if (j >= 32) {  // order > 4 overflow: gather directly
                     uint64_t pk = 0;
 #pragma unroll
                     for (int t = 0; t < OTF_MAX_ORDER; t++) if (t == k) pk = pre[t];
@@ -122,11 +120,14 @@ __device__ __forceinline__ double hs_logprob_warp(const DevModel &m, const float
                 }
                 a += v;
             }
-            if (lane == g && code[g] != OTF_UNSET) {
-                double x = (code[g] & 0x80000000u) ? -a : a;   // sign -1 for branch bit 1
-                mylog = otf_log_sigmoid(x);
-            }
+            if (lane == g) my_a = a;
         }
+        uint32_t my_code = OTF_UNSET;
+#pragma unroll
+        for (int g = 0; g < HS_G; g++) if (lane == g) my_code = code[g];
+        double mylog = 0.0;
+        if (my_code != OTF_UNSET)
+            mylog = otf_log_sigmoid((my_code & 0x80000000u) ? -my_a : my_a);   // sign -1 for bit 1
 #pragma unroll
         for (int g = 0; g < HS_G; g++) {
             double v = __shfl_sync(0xffffffffu, mylog, g);

@@ -112,31 +112,41 @@ __device__ __forceinline__ uint32_t tile_off(int row, int c) {
     return (uint32_t)((row >> 3) * (KC_B / 16 * 128) + c * 128 + (row & 7) * 16);
 }
 
-// MODE: 1 = TF32X3, 2 = BF16, 3 = TF32
+// MODE: 1 = TF32X3, 2 = BF16, 3 = TF32.
+// Pipeline per K chunk k (S-stage ring):
+//   raw A rows (gathered, fp32) and B slices (pre-converted W) arrive by
+//   cp.async S-1 chunks ahead; the chunk's raw A is converted into the
+//   operand layout (tf32 round / hi-lo split / bf16) in shared memory; one
+//   thread issues the MMAs and commits them to the stage's mbarrier; the
+//   stage's operand buffers are refilled only after that barrier fires.
+// Grid: (row tiles of 128, N tiles of bn columns).
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
 k_advance_tc(DevModel m, uint32_t n_cap, const uint32_t *n_dev, const int32_t *__restrict__ in_row,
              const int32_t *__restrict__ words, const float *__restrict__ h_base,
-             float *__restrict__ out_base, const uint32_t *out_row0_dev, int n_pad, int stages,
+             float *__restrict__ out_base, const uint32_t *out_row0_dev, int bn, int stages,
              uint32_t tmem_cols) {
     constexpr bool BF = MODE == 2;
     constexpr bool X3 = MODE == 1;
-    constexpr int ELT = BF ? 2 : 4;                   // bytes per operand element
-    constexpr int KC = KC_B / ELT;                     // K elements per stage
-    constexpr int CH = KC_B / 16;                      // 16-byte chunks per row per stage
+    constexpr int ELT = BF ? 2 : 4;                   // operand bytes per element
+    constexpr int KE = KC_B / ELT;                     // K elements per stage (16 / 32)
+    constexpr int CH = KC_B / 16;                      // operand 16-byte chunks per row
+    constexpr int RAW_ROW = KE * 4 + 16;               // raw fp32 row stride (+16 B pad)
+    constexpr int RAW_CH = KE / 4;                     // raw 16-byte chunks per row
     const uint32_t n = n_dev ? *n_dev : n_cap;
     const uint32_t q0 = blockIdx.x * BM;
     if (q0 >= n) return;
+    const int n0 = blockIdx.y * bn;                    // first output column of this CTA
     const int H = m.H;
     const int tid = threadIdx.x, warp = tid >> 5;
 
     extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t raw_bytes = BM * RAW_ROW;
     const uint32_t a_bytes = BM * KC_B;
-    const uint32_t b_bytes = (uint32_t)n_pad * KC_B;
-    const uint32_t stage_bytes = (X3 ? 2 : 1) * (a_bytes + b_bytes);
-    uint8_t *ring = smem;
+    const uint32_t b_bytes = (uint32_t)bn * KC_B;
+    const uint32_t stage_bytes = raw_bytes + (X3 ? 2 : 1) * (a_bytes + b_bytes);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + stages * stage_bytes);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + stages + 1);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + stages);
     __shared__ int32_t s_row[BM], s_w[BM];
 
     if (tid < BM) {
@@ -145,7 +155,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, const uint32_t *n_dev, const int32_t *_
         s_w[tid] = q < n ? (words ? words[q] : (int32_t)q) : 0;
     }
     if (tid == 0) {
-        for (int s = 0; s <= stages; s++) mbar_init(smem_u32(&bars[s]), 1);
+        for (int st = 0; st < stages; st++) mbar_init(smem_u32(&bars[st]), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -158,102 +168,120 @@ k_advance_tc(DevModel m, uint32_t n_cap, const uint32_t *n_dev, const int32_t *_
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
-    const int NK = (H * ELT + KC_B - 1) / KC_B;        // pipeline steps over K
+    const int NK = (H + KE - 1) / KE;
     const uint32_t sbo = CH * 128, lbo = 128;
-    const int nhalf = n_pad > 256 ? 2 : 1;
-    const int nmma = n_pad > 256 ? n_pad / 2 : n_pad;
+    const int nsub = bn > 256 ? 2 : 1;
+    const int nmma = bn / nsub;
     const uint32_t idesc = make_idesc(BF ? 1 : 2, nmma);
+    const bool vec_ok = (H & 3) == 0;
 
-    for (int kc = 0; kc < NK; kc++) {
-        const int st = kc % stages;
-        const int use = kc / stages;
-        if (kc >= stages) mbar_wait(smem_u32(&bars[st]), (uint32_t)((use - 1) & 1));
-        uint8_t *sA = ring + st * stage_bytes;
-        uint8_t *sB = sA + a_bytes;
-        uint8_t *sA2 = sB + b_bytes;          // X3: A_lo, B_lo follow
-        uint8_t *sB2 = sA2 + a_bytes;
-        const int k0 = kc * KC;               // first K element of this stage
-        // ---- B (W rows = outputs) via cp.async, zero-filled past H ----
-        for (int idx = tid; idx < n_pad * CH; idx += NTHREADS) {
-            const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
-            const int row = g * 8 + r8;
-            const int kk = k0 + c * (16 / ELT);
-            const bool ok = row < H && kk < H;
-            const uint32_t off = tile_off(row, c);
-            if (BF) {
-                cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_bf + (size_t)row * H + kk) : (const void *)m.W_bf, ok);
-            } else {
-                cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_hi + (size_t)row * H + kk) : (const void *)m.W_hi, ok);
-                if (X3)
-                    cp_async16(smem_u32(sB2 + off), ok ? (const void *)(m.W_lo + (size_t)row * H + kk) : (const void *)m.W_lo, ok);
+    auto stage_ptr = [&](int st) { return smem + st * stage_bytes; };
+    auto issue_loads = [&](int k) {
+        uint8_t *base = stage_ptr(k % stages);
+        uint8_t *raw = base;
+        uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
+        const int k0 = k * KE;
+        // raw A: 128 rows x KE fp32 (gathered rows), row-major with padding
+        for (int idx = tid; idx < BM * RAW_CH; idx += NTHREADS) {
+            const int row = idx / RAW_CH, c = idx - row * RAW_CH;
+            const int src = s_row[row];
+            const int kk = k0 + c * 4;
+            const bool ok = src >= 0 && kk < H && vec_ok;
+            cp_async16(smem_u32(raw + row * RAW_ROW + c * 16),
+                       ok ? (const void *)(h_base + (size_t)src * H + kk) : (const void *)h_base, ok);
+            if (!vec_ok && src >= 0) {   // unaligned H: scalar fill (rare)
+                float *dst = reinterpret_cast<float *>(raw + row * RAW_ROW + c * 16);
+                for (int e = 0; e < 4; e++) dst[e] = kk + e < H ? h_base[(size_t)src * H + kk + e] : 0.f;
             }
         }
+        // B: bn rows (W rows n0..n0+bn) x KC_B operand bytes, already converted
+        for (int idx = tid; idx < bn * CH; idx += NTHREADS) {
+            const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
+            const int row = g * 8 + r8;
+            const int wrow = n0 + row;
+            const int kk = k0 + c * (16 / ELT);
+            const bool ok = wrow < H && kk < H && vec_ok;
+            const uint32_t off = tile_off(row, c);
+            if (BF) {
+                cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_bf + (size_t)wrow * H + kk) : (const void *)m.W_bf, ok);
+            } else {
+                cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_hi + (size_t)wrow * H + kk) : (const void *)m.W_hi, ok);
+                if (X3)
+                    cp_async16(smem_u32(sB + b_bytes + off), ok ? (const void *)(m.W_lo + (size_t)wrow * H + kk) : (const void *)m.W_lo, ok);
+            }
+            if (!vec_ok && wrow < H) {
+                for (int e = 0; e < 16 / ELT; e++) {
+                    const bool in = kk + e < H;
+                    if (BF) reinterpret_cast<__nv_bfloat16 *>(sB + off)[e] = in ? m.W_bf[(size_t)wrow * H + kk + e] : __float2bfloat16(0.f);
+                    else {
+                        reinterpret_cast<float *>(sB + off)[e] = in ? m.W_hi[(size_t)wrow * H + kk + e] : 0.f;
+                        if (X3) reinterpret_cast<float *>(sB + b_bytes + off)[e] = in ? m.W_lo[(size_t)wrow * H + kk + e] : 0.f;
+                    }
+                }
+            }
+        }
+    };
+
+    // prologue: S-1 chunks in flight
+    for (int k = 0; k < stages - 1; k++) {
+        if (k < NK) issue_loads(k);
         cp_async_commit();
-        // ---- A (gathered context rows), converted in registers ----
+    }
+    for (int k = 0; k < NK; k++) {
+        const int st = k % stages;
+        uint8_t *base = stage_ptr(st);
+        uint8_t *raw = base;
+        uint8_t *sA = base + raw_bytes;
+        uint8_t *sA2 = sA + a_bytes;
+        uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
+        uint8_t *sB2 = sB + b_bytes;
+        // chunk k landed (S-2 newer groups may stay in flight)
+        // groups committed so far cover chunks 0..k+S-2: allow S-2 pending
+        switch (stages) {
+        case 2: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+        case 3: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+        default: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+        }
+        __syncthreads();
+        // convert raw A -> operand layout
         for (int idx = tid; idx < BM * CH; idx += NTHREADS) {
             const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
             const int row = g * 8 + r8;
-            const int src = s_row[row];
             const uint32_t off = tile_off(row, c);
             if (BF) {
-                const int kk = k0 + c * 8;
-                float v[8];
-#pragma unroll
-                for (int e = 0; e < 8; e++) v[e] = 0.f;
-                if (src >= 0) {
-                    const float *p = h_base + (size_t)src * H + kk;
-                    if (kk + 8 <= H && (H & 3) == 0) {
-                        float4 x0 = __ldg(reinterpret_cast<const float4 *>(p));
-                        float4 x1 = __ldg(reinterpret_cast<const float4 *>(p) + 1);
-                        v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
-                        v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
-                    } else {
-                        for (int e = 0; e < 8; e++) if (kk + e < H) v[e] = __ldg(p + e);
-                    }
-                }
-                __nv_bfloat162 b0 = __floats2bfloat162_rn(v[0], v[1]);
-                __nv_bfloat162 b1 = __floats2bfloat162_rn(v[2], v[3]);
-                __nv_bfloat162 b2 = __floats2bfloat162_rn(v[4], v[5]);
-                __nv_bfloat162 b3 = __floats2bfloat162_rn(v[6], v[7]);
+                const float4 x0 = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 32);
+                const float4 x1 = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 32 + 16);
+                __nv_bfloat162 b0 = __floats2bfloat162_rn(x0.x, x0.y), b1 = __floats2bfloat162_rn(x0.z, x0.w);
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(x1.x, x1.y), b3 = __floats2bfloat162_rn(x1.z, x1.w);
                 uint4 u;
                 u.x = *reinterpret_cast<uint32_t *>(&b0); u.y = *reinterpret_cast<uint32_t *>(&b1);
                 u.z = *reinterpret_cast<uint32_t *>(&b2); u.w = *reinterpret_cast<uint32_t *>(&b3);
                 *reinterpret_cast<uint4 *>(sA + off) = u;
             } else {
-                const int kk = k0 + c * 4;
-                float v[4] = {0.f, 0.f, 0.f, 0.f};
-                if (src >= 0) {
-                    const float *p = h_base + (size_t)src * H + kk;
-                    if (kk + 4 <= H && (H & 3) == 0) {
-                        float4 x = __ldg(reinterpret_cast<const float4 *>(p));
-                        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-                    } else {
-                        for (int e = 0; e < 4; e++) if (kk + e < H) v[e] = __ldg(p + e);
-                    }
-                }
-                float4 hi, lo;
-                hi.x = tf32_rn(v[0]); hi.y = tf32_rn(v[1]); hi.z = tf32_rn(v[2]); hi.w = tf32_rn(v[3]);
+                const float4 x = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 16);
+                float4 hi;
+                hi.x = tf32_rn(x.x); hi.y = tf32_rn(x.y); hi.z = tf32_rn(x.z); hi.w = tf32_rn(x.w);
                 *reinterpret_cast<float4 *>(sA + off) = hi;
                 if (X3) {
-                    lo.x = tf32_rn(v[0] - hi.x); lo.y = tf32_rn(v[1] - hi.y);
-                    lo.z = tf32_rn(v[2] - hi.z); lo.w = tf32_rn(v[3] - hi.w);
+                    float4 lo;
+                    lo.x = tf32_rn(x.x - hi.x); lo.y = tf32_rn(x.y - hi.y);
+                    lo.z = tf32_rn(x.z - hi.z); lo.w = tf32_rn(x.w - hi.w);
                     *reinterpret_cast<float4 *>(sA2 + off) = lo;
                 }
             }
         }
-        cp_async_wait_all();
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncthreads();
         if (tid == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
             for (int ks = 0; ks < KC_B / 32; ks++) {          // 32 bytes of K per MMA
-                for (int hh = 0; hh < nhalf; hh++) {
+                for (int hh = 0; hh < nsub; hh++) {
                     const uint32_t d = tmem + (uint32_t)(hh * nmma);
                     const uint32_t boff = (uint32_t)(hh * nmma / 8) * sbo + ks * 2 * lbo;
                     const uint64_t a_hi = make_desc(smem_u32(sA) + ks * 2 * lbo, lbo, sbo);
                     const uint64_t b_hi = make_desc(smem_u32(sB) + boff, lbo, sbo);
-                    const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+                    const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
                     mma<BF>(d, a_hi, b_hi, idesc, acc);
                     if (X3) {
                         const uint64_t a_lo = make_desc(smem_u32(sA2) + ks * 2 * lbo, lbo, sbo);
@@ -265,39 +293,46 @@ k_advance_tc(DevModel m, uint32_t n_cap, const uint32_t *n_dev, const int32_t *_
             }
             commit(smem_u32(&bars[st]));
         }
+        // refill the stage used by chunk k-1 with chunk k+S-1 once MMA k-1 is done
+        const int kn = k + stages - 1;
+        if (kn < NK) {
+            if (k >= 1) mbar_wait(smem_u32(&bars[(k - 1) % stages]), (uint32_t)(((k - 1) / stages) & 1));
+            issue_loads(kn);
+        }
+        cp_async_commit();
     }
-    // all MMAs done: the last commit's barrier (MMAs complete in order)
     {
         const int kl = NK - 1;
         mbar_wait(smem_u32(&bars[kl % stages]), (uint32_t)((kl / stages) & 1));
     }
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-    // ---- epilogue: TMEM lane = row = tid ----
+    // ---- epilogue: TMEM lane = row = tid; columns n0 .. n0+bn ----
     const int row = tid;
     const uint32_t q = q0 + row;
     const bool valid = q < n;
     const uint32_t out0 = out_row0_dev ? *out_row0_dev : 0u;
     const float *urow = m.U + (size_t)s_w[row] * H;
     float *orow = out_base + (size_t)(out0 + q) * H;
-    for (int c0 = 0; c0 < n_pad; c0 += 32) {
+    for (int c0 = 0; c0 < bn; c0 += 32) {
         float v[32];
         tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        const int gc = n0 + c0;
         if (valid) {
-            if ((H & 3) == 0 && c0 + 32 <= H) {
+            if (vec_ok && gc + 32 <= H) {
 #pragma unroll
                 for (int j = 0; j < 32; j += 4) {
-                    float4 u = __ldg(reinterpret_cast<const float4 *>(urow + c0 + j));
+                    float4 u = __ldg(reinterpret_cast<const float4 *>(urow + gc + j));
                     float4 o;
                     o.x = 1.f / (1.f + expf(-(v[j] + u.x)));
                     o.y = 1.f / (1.f + expf(-(v[j + 1] + u.y)));
                     o.z = 1.f / (1.f + expf(-(v[j + 2] + u.z)));
                     o.w = 1.f / (1.f + expf(-(v[j + 3] + u.w)));
-                    *reinterpret_cast<float4 *>(orow + c0 + j) = o;
+                    *reinterpret_cast<float4 *>(orow + gc + j) = o;
                 }
             } else {
                 for (int j = 0; j < 32; j++)
-                    if (c0 + j < H) orow[c0 + j] = 1.f / (1.f + expf(-(v[j] + urow[c0 + j])));
+                    if (gc + j < H) orow[gc + j] = 1.f / (1.f + expf(-(v[j] + urow[gc + j])));
             }
         }
     }
@@ -313,27 +348,34 @@ static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const 
                              const int32_t *in_row, const int32_t *words, const float *h_base,
                              float *out_base, const uint32_t *out_row0, cudaStream_t s) {
     const int H = m.H;
-    // N per MMA must be a multiple of 16 (M = 128); above 256 the N range is
-    // split into two MMAs, so pad to 32
+    // N per MMA must be a multiple of 16 (M = 128) and <= 256; above 256 the
+    // N tile is issued as two MMAs, so pad to 32
     const int n_pad = H > 256 ? (H + 31) / 32 * 32 : (H + 15) / 16 * 16;
     if (n_pad > 512) return -1;
+    // split N across CTAs when there are too few row tiles to fill 148 SMs
+    const uint32_t m_tiles = (n_cap + tc::BM - 1) / tc::BM;
+    int bn = n_pad;
+    while (bn > 32 && (uint64_t)m_tiles * (n_pad / bn) < 148 && bn % 32 == 0 && (n_pad % (bn / 2)) == 0 &&
+           ((bn / 2) % 16) == 0)
+        bn /= 2;
     uint32_t cols = 32;
-    while ((int)cols < n_pad) cols <<= 1;
+    while ((int)cols < bn) cols <<= 1;
     const bool x3 = prec == 1;
-    const uint32_t stage_bytes = (x3 ? 2u : 1u) * (uint32_t)(tc::BM + n_pad) * tc::KC_B;
-    const int elt = prec == 2 ? 2 : 4;
-    const int nk = (H * elt + tc::KC_B - 1) / tc::KC_B;
+    const int ke = prec == 2 ? 32 : 16;
+    const uint32_t raw_bytes = tc::BM * (ke * 4 + 16);
+    const uint32_t stage_bytes = raw_bytes + (x3 ? 2u : 1u) * (uint32_t)(tc::BM + bn) * tc::KC_B;
+    const int nk = (H + ke - 1) / ke;
     int stages = (int)std::min<uint32_t>(4u, (200u * 1024u) / stage_bytes);
-    stages = std::max(1, std::min(stages, nk));
-    const size_t smem = (size_t)stages * stage_bytes + (stages + 1) * 8 + 16 + 1024;
-    const dim3 grid((n_cap + tc::BM - 1) / tc::BM);
+    stages = std::max(2, std::min(stages, std::max(nk, 2)));
+    const size_t smem = (size_t)stages * stage_bytes + stages * 8 + 16 + 1024;
+    const dim3 grid(m_tiles, n_pad / bn);
     cudaError_t e;
 #define TC_LAUNCH(MODE)                                                                         \
     do {                                                                                        \
         e = cudaFuncSetAttribute(tc::k_advance_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (e != cudaSuccess) return -9;                                                        \
         tc::k_advance_tc<MODE><<<grid, tc::NTHREADS, smem, s>>>(m, n_cap, n_dev, in_row, words, h_base, \
-                                                                 out_base, out_row0, n_pad, stages, cols); \
+                                                                 out_base, out_row0, bn, stages, cols); \
     } while (0)
     if (prec == 1) TC_LAUNCH(1);
     else if (prec == 2) TC_LAUNCH(2);

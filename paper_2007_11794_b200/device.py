@@ -243,6 +243,16 @@ class Plan:
             self.handle, ngram.handle, float(lm_weight), _lib.PREC[precision], int(use_graph),
             current_stream_ptr() if stream is None else stream), "decode")
 
+    def profile(self, ngram: DeviceNgram, lm_weight: float = 1.0, precision: str = "fp64") -> dict:
+        """One run replayed from a graph with event nodes around every kernel:
+        {category: (total device ms, launches)}."""
+        ms = np.zeros(len(_lib.PROFILE_CATEGORIES))
+        n = np.zeros(len(_lib.PROFILE_CATEGORIES), np.int64)
+        _lib.check(_lib.load().otflm_decode_profile(self.handle, ngram.handle, float(lm_weight),
+                                                    _lib.PREC[precision], current_stream_ptr(),
+                                                    _p(ms), _p(n)), "profile")
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(_lib.PROFILE_CATEGORIES)}
+
     def fetch(self, stream: int | None = None):
         U, MP = self.n_utt, self.max_path
         out = dict(path_len=np.zeros(U, np.int32), path_arcs=np.zeros((U, MP), np.int32),
@@ -256,17 +266,6 @@ class Plan:
                                                   current_stream_ptr() if stream is None else stream),
                    "decode")
         return out
-
-
-def profile_start() -> None:
-    _lib.check(_lib.load().otflm_profile(1, None, None), "profile")
-
-
-def profile_stop() -> dict:
-    ms = np.zeros(len(_lib.PROFILE_CATEGORIES))
-    n = np.zeros(len(_lib.PROFILE_CATEGORIES), np.int64)
-    _lib.check(_lib.load().otflm_profile(0, _p(ms), _p(n)), "profile")
-    return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(_lib.PROFILE_CATEGORIES)}
 
 
 def last_launch_count() -> int:
