@@ -195,8 +195,8 @@ int otflm_plan_info(const OtflmPlan *p, int64_t *out8);
 int otflm_plan_counters(const OtflmPlan *p, int64_t *out4, void *stream);
 /* One decode run captured as a CUDA graph with an event-record node around
  * every kernel; writes device-side total ms / launch counts per category
- * (11 entries: expand, scan_prim, level_begin, hs, advance, dedup,
- * scan_novel, resolve, finish, final, misc). */
+ * (6 entries: expand, hs, advance, assign, final, misc).  HS and the
+ * recurrent update run as parallel graph branches, so their spans overlap. */
 int otflm_decode_profile(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
                          void *stream, double *ms_out, int64_t *n_out);
 /* Device-only decode of a prepared plan (inputs already resident in HBM).

@@ -20,8 +20,7 @@ ERR_VALUE, ERR_UNKNOWN_INDEX, ERR_TABLE_FULL, ERR_NO_PATH, ERR_KEY = -1, -2, -3,
 ERR_NOMEM, ERR_CYCLE, ERR_PACK, ERR_CUDA, ERR_HASH = -6, -7, -8, -9, -10
 
 PREC = {"fp64": 0, "tf32x3": 1, "bf16": 2, "tf32": 3}
-PROFILE_CATEGORIES = ("expand", "scan_prim", "level_begin", "hs", "advance", "dedup", "scan_novel",
-                      "resolve", "finish", "final", "misc")
+PROFILE_CATEGORIES = ("expand", "hs", "advance", "assign", "final", "misc")
 
 
 class UnknownIndexError(KeyError):

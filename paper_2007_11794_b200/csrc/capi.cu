@@ -39,8 +39,7 @@ static thread_local int64_t g_launches = 0;
     } while (0)
 
 // ---- optional per-kernel CUDA-event timing (non-graph runs only) ----
-enum { K_EXPAND, K_SCAN_PRIM, K_LEVEL_BEGIN, K_HS, K_ADVANCE, K_DEDUP, K_SCAN_NOVEL, K_RESOLVE,
-       K_FINISH, K_FINAL, K_MISC, K_NCAT };
+enum { K_EXPAND, K_HS, K_ADVANCE, K_ASSIGN, K_FINAL, K_MISC, K_NCAT };
 static bool g_prof = false;
 static std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> g_prof_ev;
 static double g_prof_ms[K_NCAT];
@@ -333,20 +332,20 @@ extern "C" int otflm_word_logprob_paths(const OtflmModel *m, int64_t n, const in
     return OTFLM_OK;
 }
 
-static int launch_advance(const DevModel &m, int prec, uint32_t n_cap, const uint32_t *n_dev,
+static int launch_advance(const DevModel &m, int prec, uint32_t n_cap, const RowSpec &rs,
                           const int32_t *in_row, const int32_t *words, const float *h_base, float *out_base,
-                          const uint32_t *out_row0, cudaStream_t s) {
+                          uint32_t row_limit, cudaStream_t s) {
     if (n_cap == 0) return OTFLM_OK;
     if (prec == OTFLM_PREC_FP64) {
         constexpr int QT = 16;
         const size_t smem = (size_t)QT * m.H * sizeof(float);
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_advance_f64<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         dim3 grid(cdiv(n_cap, QT), cdiv(m.H, 256));
-        k_advance_f64<QT><<<grid, 256, smem, s>>>(m, n_cap, n_dev, in_row, words, h_base, out_base, out_row0);
+        k_advance_f64<QT><<<grid, 256, smem, s>>>(m, n_cap, rs, in_row, words, h_base, out_base, row_limit);
         CKL();
         return OTFLM_OK;
     }
-    int rc = tc_advance_launch(m, prec, n_cap, n_dev, in_row, words, h_base, out_base, out_row0, s);
+    int rc = tc_advance_launch(m, prec, n_cap, rs, in_row, words, h_base, out_base, row_limit, s);
     if (rc == OTFLM_OK) g_launches++;
     else g_detail = "tcgen05 advance launch failed";
     return rc;
@@ -357,7 +356,8 @@ extern "C" int otflm_advance_hidden_batch(const OtflmModel *m, int64_t n, const 
     if (n <= 0) return OTFLM_OK;
     if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
     if (!m->d.U || !m->d.W) { g_detail = "model has no recurrent weights"; return OTFLM_ERR_VALUE; }
-    return launch_advance(m->d, precision, (uint32_t)n, nullptr, ctx, w, h_in, h_out, nullptr, (cudaStream_t)stream);
+    const RowSpec rs{nullptr, nullptr, nullptr, nullptr, nullptr};
+    return launch_advance(m->d, precision, (uint32_t)n, rs, ctx, w, h_in, h_out, 0xFFFFFFFFu, (cudaStream_t)stream);
 }
 
 extern "C" int otflm_advance_hidden_rows(const OtflmModel *m, int64_t n, const float *input_rows, const int32_t *ctx,
@@ -367,7 +367,8 @@ extern "C" int otflm_advance_hidden_rows(const OtflmModel *m, int64_t n, const f
     if (!m->d.W) { g_detail = "model has no recurrent weights"; return OTFLM_ERR_VALUE; }
     DevModel dm = m->d;
     dm.U = input_rows;   // row i is the input row of query i
-    return launch_advance(dm, precision, (uint32_t)n, nullptr, ctx, nullptr, h_in, h_out, nullptr, (cudaStream_t)stream);
+    const RowSpec rs{nullptr, nullptr, nullptr, nullptr, nullptr};
+    return launch_advance(dm, precision, (uint32_t)n, rs, ctx, nullptr, h_in, h_out, 0xFFFFFFFFu, (cudaStream_t)stream);
 }
 
 // all_word_logprobs: activations of every internal node, then path sums
@@ -468,7 +469,6 @@ static int streams_clear(OtflmStreams *s, int retain, cudaStream_t st) {
     if (!retain) {
         const size_t nct = (size_t)d.S * d.ct_cap, nkc = (size_t)d.S * d.kc_cap;
         CK(cudaMemsetAsync(d.ct_key, 0, nct * 8, st));
-        CK(cudaMemsetAsync(d.ct_claim, 0xFF, nct * 4, st));
         CK(cudaMemsetAsync(d.ct_idx, 0xFF, nct * 4, st));
         CK(cudaMemsetAsync(d.kc_key, 0, nkc * 8, st));
         CK(cudaMemsetAsync(d.kc_claim, 0xFF, nkc * 4, st));
@@ -504,7 +504,6 @@ extern "C" int otflm_streams_create(const OtflmModel *m, const OtflmStreamConfig
     bad |= s->mem.alloc(&d.arena_meta, (size_t)d.arena_rows * OTF_META) != cudaSuccess;
     bad |= s->mem.alloc(&d.arena_used, 1) != cudaSuccess;
     bad |= s->mem.alloc(&d.ct_key, S * d.ct_cap) != cudaSuccess;
-    bad |= s->mem.alloc(&d.ct_claim, S * d.ct_cap) != cudaSuccess;
     bad |= s->mem.alloc(&d.ct_idx, S * d.ct_cap) != cudaSuccess;
     bad |= s->mem.alloc(&d.ct_row, S * d.ct_cap) != cudaSuccess;
     bad |= s->mem.alloc(&d.kc_key, S * d.kc_cap) != cudaSuccess;
@@ -606,21 +605,23 @@ struct OtflmPlan {
     int64_t beam = 0;
     uint32_t n_utt = 0, n_levels = 0, n_nodes = 0, n_arcs = 0, n_slots = 0, R_max = 0;
     uint64_t total_req = 0;
-    std::vector<uint32_t> lvl_node_off, lvl_req;   // host copies
+    std::vector<uint32_t> lvl_node_off, lvl_req, lvl_range_off;   // host copies
     DevPlan d{};
     Allocs mem;
-    unsigned long long *scan_status = nullptr;     // [levels][2][nb]
-    uint32_t *scan_ticket = nullptr;               // [levels][2]
-    uint32_t scan_nb = 1;
     cudaGraphExec_t gexec = nullptr;
     cudaGraph_t graph = nullptr;
+    double g_lm = 0; int g_prec = -1; const OtflmNgram *g_ng = nullptr; int64_t g_nodes = 0;
     uint64_t h2d_bytes = 0;
     unsigned long long *alg_buf = nullptr;
-    double g_lm = 0; int g_prec = -1; const OtflmNgram *g_ng = nullptr; int64_t g_nodes = 0;
+    cudaStream_t side = nullptr;               // second branch of each level (HS)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::vector<uint32_t> utt_stream_host;
+    ~OtflmPlan() {
+        if (side) cudaStreamDestroy(side);
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+    }
 };
-
-struct HostNode { uint32_t local; };
 
 static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam, int V,
                          std::vector<NodeInfo> &nodes, std::vector<uint32_t> &level_nodes,
@@ -628,7 +629,7 @@ static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam,
                          std::vector<int32_t> &arc_word, std::vector<double> &arc_ac,
                          std::vector<double> &arc_slm, std::vector<uint32_t> &start_slot,
                          std::vector<uint32_t> &final_off, std::vector<uint32_t> &finals,
-                         std::vector<uint32_t> &utt_stream) {
+                         std::vector<uint32_t> &utt_stream, std::vector<StreamRange> &ranges) {
     const int U = L->n_utt;
     std::vector<std::vector<std::vector<uint32_t>>> lv(U);   // per utt: levels -> global nodes
     uint64_t node_base = 0, slot_base = 0;
@@ -639,7 +640,6 @@ static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam,
     arc_ac.assign(L->arc_ac, L->arc_ac + n_arcs_total);
     arc_slm.assign(L->arc_slm, L->arc_slm + n_arcs_total);
     out_list.assign(n_arcs_total, 0);
-    std::vector<int> seen_stream(L->stream_ids ? 0 : 0);
     for (int u = 0; u < U; u++) {
         const int N = L->n_nodes[u];
         const int64_t a0 = L->arc_off[u], a1 = L->arc_off[u + 1];
@@ -672,8 +672,7 @@ static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam,
             }
         }
         if ((int)topo.size() != N) { g_detail = "lattice contains a cycle"; return OTFLM_ERR_CYCLE; }
-        // greedy levels: contiguous runs of the topological order with no
-        // internal arc
+        // greedy levels: maximal runs of the topological order with no internal arc
         std::vector<int> lvl(N, -1), predmax(N, -1);
         int cur = 0;
         for (int n : topo) {
@@ -729,25 +728,30 @@ static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam,
         final_off.push_back((uint32_t)finals.size());
         node_base += N;
     }
-    // merge levels across utterances; static request slots per node
+    // merge levels across utterances (utterance-major inside a level); static
+    // request slots per node; one request range per (level, stream)
     size_t nlev = 0;
     for (int u = 0; u < U; u++) nlev = std::max(nlev, lv[u].size());
     p->lvl_node_off.assign(1, 0);
+    p->lvl_range_off.assign(1, 0);
     p->lvl_req.clear();
     uint64_t rmax = 0, total = 0;
     for (size_t t = 0; t < nlev; t++) {
         uint64_t run = 0;
         for (int u = 0; u < U; u++) {
-            if (t >= lv[u].size()) continue;
+            if (t >= lv[u].size() || lv[u][t].empty()) continue;
+            const uint64_t rb = run;
             for (uint32_t g : lv[u][t]) {
                 NodeInfo &ni = nodes[g];
                 ni.req_base = (uint32_t)run;
                 run += (uint64_t)ni.keep * (ni.out_e - ni.out_b);
                 level_nodes.push_back(g);
             }
+            if (run > rb) ranges.push_back(StreamRange{utt_stream[u], (uint32_t)rb, (uint32_t)run, 0});
         }
         if (run > 0xF0000000ull) { g_detail = "too many requests in one level"; return OTFLM_ERR_NOMEM; }
         p->lvl_node_off.push_back((uint32_t)level_nodes.size());
+        p->lvl_range_off.push_back((uint32_t)ranges.size());
         p->lvl_req.push_back((uint32_t)run);
         rmax = std::max(rmax, run);
         total += run;
@@ -770,13 +774,12 @@ static int upload(Allocs &mem, T **dst, const std::vector<T> &v, cudaStream_t s)
     return OTFLM_OK;
 }
 
-static int plan_alloc_workspace(OtflmPlan *p, uint32_t R, int S) {
+static int plan_alloc_workspace(OtflmPlan *p, uint32_t R, uint32_t n_lvl_slots) {
     DevPlan &d = p->d;
     bool bad = false;
     bad |= p->mem.alloc(&d.rq_c, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.rq_arc, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.rq_parent, R) != cudaSuccess;
-    bad |= p->mem.alloc(&d.rq_stream, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.rq_cslot, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.rq_m, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.rq_dslot, R) != cudaSuccess;
@@ -784,19 +787,20 @@ static int plan_alloc_workspace(OtflmPlan *p, uint32_t R, int S) {
     bad |= p->mem.alloc(&d.rq_state, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.rq_score, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.pr_req, R) != cudaSuccess;
-    bad |= p->mem.alloc(&d.pr_stream, R) != cudaSuccess;
-    bad |= p->mem.alloc(&d.pr_ctslot, R) != cudaSuccess;
-    bad |= p->mem.alloc(&d.pr_found, R) != cudaSuccess;
-    bad |= p->mem.alloc(&d.pr_E, R) != cudaSuccess;
-    bad |= p->mem.alloc(&d.pr_cnext, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.pr_inrow, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.pr_w, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.pr_p, R) != cudaSuccess;
-    bad |= p->mem.alloc(&d.first_E, (size_t)S) != cudaSuccess;
-    bad |= p->mem.alloc(&d.counters, 4) != cudaSuccess;
+    bad |= p->mem.alloc(&d.pr_dig, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.lvl, n_lvl_slots) != cudaSuccess;
     bad |= p->mem.alloc(&p->alg_buf, 4) != cudaSuccess;
     d.alg = nullptr;   // counters are only maintained in profiling runs
     if (bad) { g_detail = "cudaMalloc workspace"; return OTFLM_ERR_NOMEM; }
+    if (cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        g_detail = "stream/event creation";
+        return OTFLM_ERR_CUDA;
+    }
     return OTFLM_OK;
 }
 
@@ -814,8 +818,9 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     std::vector<uint32_t> level_nodes, out_list, arc_slot, start_slot, final_off, finals, utt_stream;
     std::vector<int32_t> arc_word;
     std::vector<double> arc_ac, arc_slm;
+    std::vector<StreamRange> ranges;
     int rc = compile_batch(p, L, beam, st->m->d.V, nodes, level_nodes, out_list, arc_slot, arc_word, arc_ac,
-                           arc_slm, start_slot, final_off, finals, utt_stream);
+                           arc_slm, start_slot, final_off, finals, utt_stream, ranges);
     if (rc) { delete p; return rc; }
     {
         std::vector<uint32_t> seen(st->d.S, 0);
@@ -824,21 +829,23 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
             seen[sid] = 1;
         }
     }
+    if (ranges.empty()) ranges.push_back(StreamRange{0, 0, 0, 0});
     p->utt_stream_host = utt_stream;
     DevPlan &d = p->d;
     NodeInfo *dn; uint32_t *dln, *dol, *das, *dss, *dus, *dfo, *dfi; int32_t *daw; double *dac, *dsl;
+    StreamRange *drg;
     g_upload_bytes = 0;
     if ((rc = upload(p->mem, &dn, nodes, s)) || (rc = upload(p->mem, &dln, level_nodes, s)) ||
         (rc = upload(p->mem, &dol, out_list, s)) || (rc = upload(p->mem, &das, arc_slot, s)) ||
         (rc = upload(p->mem, &daw, arc_word, s)) || (rc = upload(p->mem, &dac, arc_ac, s)) ||
         (rc = upload(p->mem, &dsl, arc_slm, s)) || (rc = upload(p->mem, &dss, start_slot, s)) ||
         (rc = upload(p->mem, &dus, utt_stream, s)) || (rc = upload(p->mem, &dfo, final_off, s)) ||
-        (rc = upload(p->mem, &dfi, finals, s))) {
+        (rc = upload(p->mem, &dfi, finals, s)) || (rc = upload(p->mem, &drg, ranges, s))) {
         p->mem.free_all(); delete p; return rc;
     }
     d.nodes = dn; d.level_nodes = dln; d.out_list = dol; d.arc_slot = das; d.arc_word = daw;
     d.arc_ac = dac; d.arc_slm = dsl; d.n_utt = p->n_utt; d.utt_start_slot = dss; d.utt_stream = dus;
-    d.final_off = dfo; d.finals = dfi;
+    d.final_off = dfo; d.finals = dfi; d.ranges = drg;
     p->h2d_bytes = g_upload_bytes;
     bool bad = p->mem.alloc(&d.arr, std::max<uint32_t>(p->n_slots, 1)) != cudaSuccess;
     bad |= p->mem.alloc(&d.slot_win, std::max<uint32_t>(p->n_slots, 1)) != cudaSuccess;
@@ -852,11 +859,8 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     bad |= p->mem.alloc(&d.out_lm, p->n_utt) != cudaSuccess;
     bad |= p->mem.alloc(&d.out_end_ctx, p->n_utt) != cudaSuccess;
     bad |= p->mem.alloc(&d.out_expansions, p->n_utt) != cudaSuccess;
-    p->scan_nb = cdiv(p->R_max, SCAN_BLK);
-    bad |= p->mem.alloc(&p->scan_status, (size_t)std::max<uint32_t>(p->n_levels, 1) * 2 * p->scan_nb) != cudaSuccess;
-    bad |= p->mem.alloc(&p->scan_ticket, (size_t)std::max<uint32_t>(p->n_levels, 1) * 2) != cudaSuccess;
     if (bad) { p->mem.free_all(); delete p; g_detail = "cudaMalloc plan buffers"; return OTFLM_ERR_NOMEM; }
-    if ((rc = plan_alloc_workspace(p, p->R_max, st->d.S))) { p->mem.free_all(); delete p; return rc; }
+    if ((rc = plan_alloc_workspace(p, p->R_max, p->n_levels + 1))) { p->mem.free_all(); delete p; return rc; }
     *out = p;
     return OTFLM_OK;
 }
@@ -887,30 +891,26 @@ extern "C" int otflm_plan_counters(const OtflmPlan *p, int64_t *o, void *stream)
     return OTFLM_OK;
 }
 
-// the per-level pipeline shared by decode and rnnlm_prob_batch (after the
-// requests of the level exist)
-static int enqueue_miss_pipeline(OtflmPlan *p, const DevModel &m, DevStreams &S, uint32_t R, int prec,
-                                 unsigned long long *status, uint32_t *ticket, cudaStream_t s) {
+// stage 2 of a level: HS on the side branch || recurrent update on s
+static int enqueue_stage2(OtflmPlan *p, const DevModel &m, DevStreams &S, uint32_t R, int prec,
+                          const RowSpec &rs, cudaStream_t s) {
     DevPlan &d = p->d;
-    const unsigned nb = cdiv(R, SCAN_BLK);
-    { ProfScope ps(K_SCAN_PRIM, s); k_scan_prim<<<nb, SCAN_BLK, 0, s>>>(d, S, R, status, ticket); CKL(); }
-    { ProfScope ps(K_LEVEL_BEGIN, s); k_level_begin<<<1, 1, 0, s>>>(d, S); CKL(); }
+    CK(cudaEventRecord(p->ev_fork, s));
+    CK(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
     {
-        ProfScope ps(K_HS, s);
-#define CALL(VEC, CPL) k_hs_prim<VEC, CPL><<<cdiv(R, 8), 256, 0, s>>>(m, d, S, R)
+        ProfScope ps(K_HS, p->side);
+#define CALL(VEC, CPL) k_hs_prim<VEC, CPL><<<cdiv(R, 8), 256, 0, p->side>>>(m, d, S, rs)
         HS_DISPATCH(m.H, CALL);
 #undef CALL
         CKL();
     }
     {
         ProfScope ps(K_ADVANCE, s);
-        int rc = launch_advance(m, prec, R, &d.counters[0], d.pr_inrow, d.pr_w, S.arena_h, S.arena_h,
-                                &d.counters[2], s);
+        int rc = launch_advance(m, prec, R, rs, d.pr_inrow, d.pr_w, S.arena_h, S.arena_h, S.arena_rows, s);
         if (rc) return rc;
     }
-    { ProfScope ps(K_DEDUP, s); k_dedup<<<cdiv(R, 8), 256, 0, s>>>(d, S); CKL(); }
-    { ProfScope ps(K_SCAN_NOVEL, s); k_scan_novel<<<nb, SCAN_BLK, 0, s>>>(d, S, status + p->scan_nb, ticket + 1); CKL(); }
-    { ProfScope ps(K_RESOLVE, s); k_resolve<<<cdiv(R, 256), 256, 0, s>>>(d, S); CKL(); }
+    CK(cudaEventRecord(p->ev_join, p->side));
+    CK(cudaStreamWaitEvent(s, p->ev_join, 0));
     return OTFLM_OK;
 }
 
@@ -920,26 +920,30 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
     DevStreams &S = st->d;
     DevPlan &d = p->d;
     CK(cudaMemsetAsync(d.arr, 0xFF, (size_t)std::max<uint32_t>(p->n_slots, 1) * sizeof(Arrival), s));
-    CK(cudaMemsetAsync(p->scan_status, 0, (size_t)std::max<uint32_t>(p->n_levels, 1) * 2 * p->scan_nb * 8, s));
-    CK(cudaMemsetAsync(p->scan_ticket, 0, (size_t)std::max<uint32_t>(p->n_levels, 1) * 2 * 4, s));
+    CK(cudaMemsetAsync(d.lvl, 0, (size_t)(p->n_levels + 1) * sizeof(LevelCtr), s));
     if (d.alg) CK(cudaMemsetAsync(d.alg, 0, 4 * sizeof(unsigned long long), s));
-    k_init_starts<<<cdiv(p->n_utt, 128), 128, 0, s>>>(d);
-    CKL();
-    k_run_begin<<<cdiv(S.S, 128), 128, 0, s>>>(S);
-    CKL();
+    { ProfScope ps(K_MISC, s); k_run_begin<<<cdiv(std::max<uint32_t>(p->n_utt, S.S), 128), 128, 0, s>>>(d, S); CKL(); }
+    int prev = -1;
     for (uint32_t t = 0; t < p->n_levels; t++) {
         const uint32_t nb0 = p->lvl_node_off[t], nn = p->lvl_node_off[t + 1] - nb0;
         const uint32_t R = p->lvl_req[t];
-        unsigned long long *status = p->scan_status + (size_t)t * 2 * p->scan_nb;
-        uint32_t *ticket = p->scan_ticket + (size_t)t * 2;
-        if (nn == 0) continue;
+        if (nn == 0 || R == 0) {
+            if (nn) { ProfScope ps(K_EXPAND, s); k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, nb0, nn, (long long)p->beam, t); CKL(); }
+            continue;
+        }
         { ProfScope ps(K_EXPAND, s); k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, nb0, nn, (long long)p->beam, t); CKL(); }
-        if (R == 0) continue;
-        int rc = enqueue_miss_pipeline(p, m, S, R, prec, status, ticket, s);
+        const RowSpec rs{&d.lvl[t].n_prim, &d.lvl[t], prev >= 0 ? &d.lvl[prev] : nullptr, S.arena_used, d.pr_dig};
+        int rc = enqueue_stage2(p, m, S, R, prec, rs, s);
         if (rc) return rc;
-        { ProfScope ps(K_FINISH, s); k_finish<<<cdiv(std::max<uint64_t>(R, (uint64_t)S.S), 256), 256, 0, s>>>(d, S, g->d, R, t, lm); CKL(); }
+        const uint32_t r0 = p->lvl_range_off[t], nr = p->lvl_range_off[t + 1] - r0;
+        {
+            ProfScope ps(K_ASSIGN, s);
+            k_assign<0><<<cdiv(nr, 4), 128, 0, s>>>(d, S, g->d, t, r0, nr, lm, nullptr, nullptr, nullptr);
+            CKL();
+        }
+        prev = (int)t;
     }
-    { ProfScope ps(K_FINAL, s); k_final<<<cdiv(p->n_utt, 4), 128, 0, s>>>(d, S, lm); CKL(); }
+    { ProfScope ps(K_FINAL, s); k_final<<<cdiv(p->n_utt, 4), 128, 0, s>>>(d, S, lm, prev); CKL(); }
     return OTFLM_OK;
 }
 
@@ -977,7 +981,6 @@ extern "C" int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_wei
         cudaGraphGetNodes(graph, nullptr, &nn);
         p->g_nodes = (int64_t)nn;
         p->g_lm = lm_weight; p->g_prec = precision; p->g_ng = g;
-        p->g_nodes = (int64_t)nn;
         g_last_launches = g_launches;
     }
     CK(cudaGraphLaunch(p->gexec, s));
@@ -985,6 +988,7 @@ extern "C" int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_wei
 }
 
 extern "C" int64_t otflm_last_launch_count(void) { return g_last_launches; }
+
 extern "C" int otflm_decode_profile(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
                                     void *stream, double *ms_out, int64_t *n_out) {
     if (!p || !g) return OTFLM_ERR_VALUE;
@@ -1021,7 +1025,6 @@ extern "C" int otflm_decode_profile(OtflmPlan *p, const OtflmNgram *g, double lm
     for (int i = 0; i < K_NCAT; i++) { if (ms_out) ms_out[i] = g_prof_ms[i]; if (n_out) n_out[i] = g_prof_n[i]; }
     return OTFLM_OK;
 }
-
 
 extern "C" int otflm_decode_fetch(OtflmPlan *p, OtflmDecodeResult *r, void *stream) {
     cudaStream_t s = (cudaStream_t)stream;
@@ -1072,49 +1075,25 @@ extern "C" int otflm_decode(OtflmStreams *s, const OtflmNgram *g, const OtflmLat
 __global__ void k_probe_batch(DevPlan P, DevStreams S, uint32_t n, const uint32_t *c, const int32_t *w,
                               const uint32_t *sid) {
     const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    const uint32_t s = sid[r];
-    P.rq_c[r] = c[r]; P.rq_w[r] = w[r]; P.rq_stream[r] = s; P.rq_m[r] = OTF_UNSET;
-    if (c[r] > S.table_len[s] || w[r] < 0) { atomicOr(S.err, c[r] > S.table_len[s] ? OTF_E_PATH : OTF_E_VALUE); P.rq_state[r] = RQ_INVALID; return; }
-    uint8_t st = RQ_NOCACHE;
-    uint32_t cslot = OTF_UNSET;
-    if (S.enabled) {
-        const uint64_t kb = (uint64_t)s * S.kc_cap;
-        const unsigned long long key = ((((unsigned long long)c[r]) << 32) | (uint32_t)w[r]) + 1ull;
-        const uint32_t mask = S.kc_cap - 1;
-        uint32_t sl = (uint32_t)otf_hash64(key) & mask, probes = 0;
-        for (;;) {
-            unsigned long long k = S.kc_key[kb + sl];
-            if (k == 0ull) { unsigned long long prev = atomicCAS(&S.kc_key[kb + sl], 0ull, key); k = prev == 0ull ? key : prev; }
-            if (k == key) break;
-            sl = (sl + 1) & mask;
-            if (++probes > S.kc_cap) { atomicOr(S.err, OTF_E_CACHE_FULL); sl = OTF_UNSET; break; }
+    bool need = false;
+    uint32_t s = 0, cc = 0;
+    int32_t ww = 0;
+    if (r < n) {
+        s = sid[r]; cc = c[r]; ww = w[r];
+        P.rq_c[r] = cc; P.rq_w[r] = ww; P.rq_m[r] = OTF_UNSET;
+        uint8_t st = RQ_NOCACHE;
+        uint32_t cslot = OTF_UNSET;
+        if (cc > S.table_len[s]) {
+            atomicOr(S.err, OTF_E_PATH);
+            st = RQ_INVALID;
+        } else if (S.enabled) {
+            cslot = cache_probe(S, s, cc, ww, r, &st);
         }
-        cslot = sl;
-        if (sl != OTF_UNSET) {
-            if (ld_volatile_u32(&S.kc_cnext[kb + sl]) != OTF_UNSET) st = RQ_HIT;
-            else { atomicMin(&S.kc_claim[kb + sl], r); st = RQ_PENDING; }
-        } else st = RQ_INVALID;
+        P.rq_cslot[r] = cslot;
+        P.rq_state[r] = st;
+        need = st == RQ_PENDING || st == RQ_NOCACHE;
     }
-    P.rq_cslot[r] = cslot;
-    P.rq_state[r] = st;
-}
-
-__global__ void k_batch_out(DevPlan P, DevStreams S, uint32_t n, double *p_out, uint32_t *cn_out, uint8_t *hit_out) {
-    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r == 0) *S.arena_used += P.counters[0];
-    if (r < (uint32_t)S.S) { uint32_t nc = S.novel_cnt[r]; if (nc) { S.table_len[r] += nc; S.novel_cnt[r] = 0; } }
-    if (r >= n) return;
-    if (P.rq_state[r] == RQ_INVALID) return;
-    const uint32_t s = P.rq_stream[r], m = P.rq_m[r];
-    double p; uint32_t cn;
-    if (m != OTF_UNSET) { p = P.pr_p[m]; cn = P.pr_cnext[m]; }
-    else { const uint64_t kb = (uint64_t)s * S.kc_cap + P.rq_cslot[r]; p = S.kc_p[kb]; cn = S.kc_cnext[kb]; }
-    p_out[r] = p; cn_out[r] = cn; hit_out[r] = m == OTF_UNSET ? 1 : 0;
-    unsigned long long *stt = S.stats + (size_t)s * 8;
-    atomicAdd(&stt[0], 1ull);
-    if (m != OTF_UNSET) { atomicAdd(&stt[2], 1ull); if (S.enabled) atomicAdd(&stt[6], 1ull); }
-    else atomicAdd(&stt[1], 1ull);
+    compact_primary(P, S, &P.lvl[0], need, r, cc, ww, s);
 }
 
 extern "C" int otflm_rnnlm_prob_batch(OtflmStreams *s, int64_t n, const int32_t *sid_h, const uint32_t *c_h,
@@ -1129,26 +1108,30 @@ extern "C" int otflm_rnnlm_prob_batch(OtflmStreams *s, int64_t n, const int32_t 
         if (w_h[i] < 0 || w_h[i] >= m.V) { g_detail = "word id out of range"; return OTFLM_ERR_VALUE; }
         if (sid_h[i] < 0 || sid_h[i] >= s->d.S) return OTFLM_ERR_VALUE;
     }
-    // stable order by stream so each stream's requests are contiguous
+    // stable order by stream: each stream's requests contiguous, array order kept
     std::vector<uint32_t> order((size_t)n);
     for (int64_t i = 0; i < n; i++) order[i] = (uint32_t)i;
     std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return sid_h[a] < sid_h[b]; });
     std::vector<uint32_t> sc(n), cc(n);
     std::vector<int32_t> ww(n);
-    for (int64_t i = 0; i < n; i++) { sc[i] = (uint32_t)sid_h[order[i]]; cc[i] = c_h[order[i]]; ww[i] = w_h[order[i]]; }
+    std::vector<StreamRange> ranges;
+    for (int64_t i = 0; i < n; i++) {
+        sc[i] = (uint32_t)sid_h[order[i]]; cc[i] = c_h[order[i]]; ww[i] = w_h[order[i]];
+        if (i == 0 || sc[i] != sc[i - 1]) ranges.push_back(StreamRange{sc[i], (uint32_t)i, (uint32_t)i, 0});
+        ranges.back().re = (uint32_t)i + 1;
+    }
     OtflmPlan *p = s->scratch;
-    if (!p || p->R_max < (uint32_t)n) {
+    if (!p || p->R_max < (uint32_t)n || p->n_utt < ranges.size()) {
         if (p) otflm_plan_destroy(p);
         p = new OtflmPlan();
         p->st = s;
         p->R_max = (uint32_t)std::max<int64_t>(n, 1024);
-        p->n_levels = 1;
-        p->scan_nb = cdiv(p->R_max, SCAN_BLK);
-        int rc = plan_alloc_workspace(p, p->R_max, s->d.S);
-        bool bad = rc != 0;
-        bad |= p->mem.alloc(&p->scan_status, (size_t)2 * p->scan_nb) != cudaSuccess;
-        bad |= p->mem.alloc(&p->scan_ticket, 2) != cudaSuccess;
+        p->n_utt = (uint32_t)std::max<size_t>(ranges.size(), (size_t)s->d.S);
+        int rc = plan_alloc_workspace(p, p->R_max, 2);
+        StreamRange *drg = nullptr;
+        bool bad = rc != 0 || p->mem.alloc(&drg, p->n_utt) != cudaSuccess;
         if (bad) { p->mem.free_all(); delete p; s->scratch = nullptr; return OTFLM_ERR_NOMEM; }
+        p->d.ranges = drg;
         s->scratch = p;
     }
     uint32_t *dsid, *dc, *dcn; int32_t *dw; double *dp; uint8_t *dh;
@@ -1157,14 +1140,16 @@ extern "C" int otflm_rnnlm_prob_batch(OtflmStreams *s, int64_t n, const int32_t 
     CK(cudaMemcpyAsync(dsid, sc.data(), n * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dc, cc.data(), n * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dw, ww.data(), n * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(p->scan_status, 0, (size_t)2 * p->scan_nb * 8, st));
-    CK(cudaMemsetAsync(p->scan_ticket, 0, 8, st));
+    CK(cudaMemcpyAsync((void *)p->d.ranges, ranges.data(), ranges.size() * sizeof(StreamRange), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(p->d.lvl, 0, 2 * sizeof(LevelCtr), st));
     const uint32_t R = (uint32_t)n;
     k_probe_batch<<<cdiv(R, 256), 256, 0, st>>>(p->d, s->d, R, dc, dw, dsid);
     CKL();
-    int rc = enqueue_miss_pipeline(p, m, s->d, R, precision, p->scan_status, p->scan_ticket, st);
+    const RowSpec rs{&p->d.lvl[0].n_prim, &p->d.lvl[0], nullptr, s->d.arena_used, p->d.pr_dig};
+    int rc = enqueue_stage2(p, m, s->d, R, precision, rs, st);
     if (rc) return rc;
-    k_batch_out<<<cdiv(std::max<uint64_t>(R, (uint64_t)s->d.S), 256), 256, 0, st>>>(p->d, s->d, R, dp, dcn, dh);
+    k_assign<1><<<cdiv(ranges.size(), 4), 128, 0, st>>>(p->d, s->d, DevNgram{}, 0, 0, (uint32_t)ranges.size(), 0.0,
+                                                      dp, dcn, dh);
     CKL();
     std::vector<double> pp(n);
     std::vector<uint32_t> cn(n);

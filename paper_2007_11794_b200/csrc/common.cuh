@@ -52,7 +52,7 @@ struct DevStreams {
     uint32_t *arena_used;       // scalar
     uint32_t ct_cap;            // per stream content-table slots (pow2)
     unsigned long long *ct_key; // [S][ct_cap], 0 = empty
-    uint32_t *ct_claim, *ct_idx, *ct_row;
+    uint32_t *ct_idx, *ct_row;
     uint32_t kc_cap;            // per stream cache slots (pow2)
     unsigned long long *kc_key; // [S][kc_cap], 0 = empty, else ((c<<32)|w)+1
     uint32_t *kc_claim, *kc_cnext;
@@ -67,6 +67,28 @@ struct DevStreams {
 #define RQ_HIT 1       // value present from an earlier level / call
 #define RQ_PENDING 2   // key inserted this level; claim decides the primary
 #define RQ_NOCACHE 3   // cache disabled: every request computes
+
+struct LevelCtr {            // one per level (+ spare slots for the Table-1 batch API)
+    uint32_t n_prim;         // requests that run the model this level
+    uint32_t base;           // first arena row of this level's new states
+    uint32_t pad0, pad1;
+};
+
+// Where a recurrent-update / HS launch finds its row count and writes rows:
+// base = prev->base + prev->n_prim (previous level) or *base_dev (first
+// level of a run) -- computed on the device, so CUDA-graph replays need no
+// host round trip.
+struct RowSpec {
+    const uint32_t *n_dev;          // row count (nullptr: n_cap)
+    LevelCtr *cur;                  // this level (its base is recorded here)
+    const LevelCtr *prev;           // previous active level or nullptr
+    const uint32_t *base_dev;       // base when prev == nullptr (nullptr: 0)
+    unsigned long long *dig;        // per-row content digest (nullptr: none)
+};
+__device__ __forceinline__ uint32_t row_base(const RowSpec &rs) {
+    if (rs.prev) return rs.prev->base + rs.prev->n_prim;
+    return rs.base_dev ? *rs.base_dev : 0u;
+}
 
 struct Arrival {       // 32 B, one per (dst node, in-arc, source rank)
     double score;

@@ -4,22 +4,33 @@
 // A "level" is a maximal run of the reference's Kahn topological order
 // (lattice.py:68-82) in which no node feeds another; for generator lattices
 // a level is one frame.  Every node owns a fixed block of arrival slots (one
-// per (in-arc, source rank)), so token recombination needs no atomics: the
-// expand kernel recombines a node's arrivals (max score, earliest arrival on
-// ties = the reference's strict '>' , decoder.py:145-149), ranks the
-// survivors by (-score, ctx) (decoder.py:135) and emits one request per
-// (kept token, out-arc) at a static slot whose index IS the reference's
-// request order (topo node, rank, arc id).  That order is what the cache
-// claim (first occurrence = miss) and the IndexTable's len+1 numbering
-// (context_table.py:83-86) are resolved against, so hit/miss counts and
-// context ids are identical to the sequential reference.
+// per (in-arc, source rank)), so token recombination needs no atomics, and
+// every (kept token, out-arc) request has a static slot whose index IS the
+// reference's request order (topo node, rank, arc id).
 //
-// Per level:  expand(+cache probe) -> scan primaries -> HS+MaxEnt (+history')
-//             -> recurrent update -> content dedup -> scan novel -> resolve
-//             -> finish (n-gram delta, score, arrival write).
+// Per level, three graph stages (the middle two run as parallel branches):
+//   k_expand   warp per node: recombine arrivals (max score, earliest arrival
+//              wins ties = the strict '>' of decoder.py:145-149), rank by
+//              (-score, ctx) (decoder.py:135), keep the beam, emit requests,
+//              probe/claim the stream's (c, w) cache (cache.py:82-96) and
+//              compact the requests that must run the model;
+//   k_hs_prim  HS + MaxEnt score of every computed request (warp each) and the
+//   || advance successor history; the recurrent update h' (tcgen05 GEMM or the
+//              exact FP64 kernel) -- both add their part of the new context's
+//              content digest;
+//   k_assign   warp per stream: walks the stream's requests in reference
+//              order, resolves cache claims (first occurrence = miss),
+//              dedups successor contexts against the IndexTable
+//              (context_table.py:74-86), numbers new ones len+1, fills the
+//              cache, then computes the small-LM delta (decoder.py:99-102),
+//              the new path score (decoder.py:144) and writes the arrival.
 #pragma once
 #include "common.cuh"
 #include "hs.cuh"
+
+struct StreamRange {         // requests of one stream inside one level
+    uint32_t stream, rb, re, pad;
+};
 
 struct DevPlan {
     // compiled lattice batch
@@ -34,92 +45,45 @@ struct DevPlan {
     // per utterance
     uint32_t n_utt;
     const uint32_t *utt_start_slot, *utt_stream, *final_off, *finals;
+    // per level stream ranges
+    const StreamRange *ranges;
+    LevelCtr *lvl;
     // request workspace [R_max]
-    uint32_t *rq_c, *rq_arc, *rq_parent, *rq_stream, *rq_cslot, *rq_m, *rq_dslot;
+    uint32_t *rq_c, *rq_arc, *rq_parent, *rq_cslot, *rq_m, *rq_dslot;
     int32_t *rq_w;
     uint8_t *rq_state;
     double *rq_score;
-    // primary workspace [R_max]
-    uint32_t *pr_req, *pr_stream, *pr_ctslot, *pr_found, *pr_E, *pr_cnext;
+    // primaries [R_max]
+    uint32_t *pr_req;
     int32_t *pr_inrow, *pr_w;
     double *pr_p;
-    uint32_t *first_E;            // [S]
-    uint32_t *counters;           // [0] n_prim, [1] n_novel, [2] arena_base
-    unsigned long long *alg;      // run totals: [0] sum P, [1] sum P*k, [2] HS queries
+    unsigned long long *pr_dig;   // content digest (sum of per-element hashes)
     // outputs
     int32_t *out_len, *out_arcs, *out_status;
     double *out_combined, *out_acoustic, *out_lm;
     long long *out_end_ctx, *out_expansions;
     int32_t max_path;
+    unsigned long long *alg;      // profiling only: [0] sum P, [1] sum P*k, [2] HS queries
 };
 
-// --------------------------------------------------------------------------
-// decoupled look-back scan over a flag predicate (single pass, any n)
-// status word: bits 63:62 = 0 none / 1 aggregate / 2 inclusive, 31:0 value
-// --------------------------------------------------------------------------
-#define SCAN_BLK 512
-template <class FlagF, class OutF>
-__device__ __forceinline__ void chained_scan(uint32_t n, unsigned long long *status,
-                                             uint32_t *ticket, FlagF flagf, OutF outf,
-                                             uint32_t *total_out) {
-    __shared__ uint32_t s_bid, s_prefix, s_warp[SCAN_BLK / 32];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) s_bid = atomicAdd(ticket, 1u);
-    __syncthreads();
-    const uint32_t bid = s_bid;
-    const uint32_t i = bid * SCAN_BLK + tid;
-    const bool f = i < n ? flagf(i) : false;
-    const unsigned bal = __ballot_sync(0xffffffffu, f);
-    const uint32_t lpre = __popc(bal & ((1u << lane) - 1u));
-    if (lane == 0) s_warp[wid] = __popc(bal);
-    __syncthreads();
-    if (wid == 0) {
-        uint32_t v = lane < SCAN_BLK / 32 ? s_warp[lane] : 0u;
-        uint32_t incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        uint32_t block_total = __shfl_sync(0xffffffffu, incl, 31);
-        if (lane < SCAN_BLK / 32) s_warp[lane] = incl - v;
-        if (lane == 0) {
-            uint32_t prefix = 0;
-            if (bid == 0) {
-                __threadfence();
-                atomicExch(&status[0], (2ull << 62) | block_total);
-            } else {
-                atomicExch(&status[bid], (1ull << 62) | block_total);
-                int j = (int)bid - 1;
-                while (j >= 0) {
-                    unsigned long long s = ld_volatile_u64(&status[j]);
-                    unsigned fl = (unsigned)(s >> 62);
-                    if (fl == 0) continue;
-                    prefix += (uint32_t)s;
-                    if (fl == 2) break;
-                    j--;
-                }
-                __threadfence();
-                atomicExch(&status[bid], (2ull << 62) | (uint64_t)(prefix + block_total));
-            }
-            s_prefix = prefix;
-            if (bid == gridDim.x - 1 && total_out) *total_out = prefix + block_total;
-        }
-    }
-    __syncthreads();
-    if (i < n) outf(i, s_prefix + s_warp[wid] + lpre, f);
+// content digest term of element i of a hidden row / word j of the history
+// meta; the digest is their wrapping sum, so partial sums from different CTAs
+// and kernels compose (context_table.py:64-72 serializes the same content)
+__device__ __forceinline__ unsigned long long dig_h(int i, float x) {
+    return otf_hash64(((uint64_t)i << 32) ^ __float_as_uint(x));
+}
+__device__ __forceinline__ unsigned long long dig_meta(int j, uint32_t w) {
+    return otf_hash64(((uint64_t)(0x10000 + j) << 32) ^ w);
 }
 
 // --------------------------------------------------------------------------
-// recombination helpers: arrival j beats i for the same ctx if higher score
-// or equal score and earlier arrival (strict '>' keeps the first, decoder.py:147)
+// recombination: arrival j beats i for the same ctx if higher score or equal
+// score and earlier arrival (strict '>' keeps the first, decoder.py:147)
 // --------------------------------------------------------------------------
 __device__ __forceinline__ uint64_t arr_key(const Arrival &a) {
     return ((uint64_t)a.lvl << 32) | a.ridx;
 }
 
-// Returns, for the calling lane's slot i (or invalid), whether it is the
-// recombined winner of its ctx; all lanes of the warp must call it.
 __device__ __forceinline__ void recombine_node(const Arrival *__restrict__ arr, uint8_t *win,
                                                uint32_t base, uint32_t cap, int lane) {
     for (uint32_t i0 = 0; i0 < cap; i0 += 32) {
@@ -147,21 +111,68 @@ __device__ __forceinline__ void recombine_node(const Arrival *__restrict__ arr, 
     __syncwarp();
 }
 
+// probe/insert (c, w) in the stream's cache table; returns the slot and
+// whether a value from an earlier level/call is present; a new or pending
+// key is claimed by the lowest request index (atomicMin)
+__device__ __forceinline__ uint32_t cache_probe(const DevStreams &S, uint32_t s, uint32_t c, int32_t w,
+                                                uint32_t r, uint8_t *state) {
+    const uint64_t kb = (uint64_t)s * S.kc_cap;
+    const unsigned long long key = ((((unsigned long long)c) << 32) | (uint32_t)w) + 1ull;
+    const uint32_t mask = S.kc_cap - 1;
+    uint32_t sl = (uint32_t)otf_hash64(key) & mask;
+    for (uint32_t probes = 0;; probes++) {
+        unsigned long long k = S.kc_key[kb + sl];
+        if (k == 0ull) {
+            unsigned long long prev = atomicCAS(&S.kc_key[kb + sl], 0ull, key);
+            k = prev == 0ull ? key : prev;
+        }
+        if (k == key) break;
+        sl = (sl + 1) & mask;
+        if (probes > S.kc_cap) { atomicOr(S.err, OTF_E_CACHE_FULL); *state = RQ_INVALID; return OTF_UNSET; }
+    }
+    if (ld_volatile_u32(&S.kc_cnext[kb + sl]) != OTF_UNSET) {
+        *state = RQ_HIT;
+    } else {
+        atomicMin(&S.kc_claim[kb + sl], r);
+        *state = RQ_PENDING;
+    }
+    return sl;
+}
+
+// warp-aggregated compaction of the requests that run the model this level
+// (all lanes of the warp call it)
+__device__ __forceinline__ void compact_primary(DevPlan &P, const DevStreams &S, LevelCtr *lc, bool need,
+                                                uint32_t r, uint32_t c, int32_t w, uint32_t s) {
+    const unsigned bal = __ballot_sync(0xffffffffu, need);
+    if (!bal) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(bal) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&lc->n_prim, (uint32_t)__popc(bal));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (need) {
+        const uint32_t m = base + __popc(bal & ((1u << lane) - 1u));
+        P.rq_m[r] = m;
+        P.pr_req[m] = r;
+        P.pr_w[m] = w;
+        P.pr_inrow[m] = (int32_t)S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + c];
+        P.pr_dig[m] = 0ull;
+    }
+}
+
 // --------------------------------------------------------------------------
-// kernel 1: expand one level (warp per node) + cache probe/claim per request
+// stage 1: expand one level (warp per node)
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, uint32_t node_begin,
                                                 uint32_t n_nodes, long long beam, uint32_t lvl) {
     const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (gw >= n_nodes) return;
+    LevelCtr *lc = &P.lvl[lvl];
     const NodeInfo nd = P.nodes[P.level_nodes[node_begin + gw]];
     const uint32_t outdeg = nd.out_e - nd.out_b;
     if (nd.cap == 0 || outdeg == 0) {
-        for (uint32_t r = lane; r < nd.keep * outdeg; r += 32) {
-            P.rq_w[nd.req_base + r] = -1;
-            P.rq_state[nd.req_base + r] = RQ_INVALID;
-        }
+        for (uint32_t r = lane; r < nd.keep * outdeg; r += 32) P.rq_state[nd.req_base + r] = RQ_INVALID;
         return;
     }
     recombine_node(P.arr, P.slot_win, nd.slot_base, nd.cap, lane);
@@ -172,7 +183,6 @@ __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, uint32_
         n_win += __popc(__ballot_sync(0xffffffffu, wi));
     }
     const uint32_t n_kept = (uint32_t)min((long long)n_win, beam);
-    const uint64_t kc_base = (uint64_t)nd.stream * S.kc_cap;
     for (uint32_t i0 = 0; i0 < nd.cap; i0 += 32) {
         uint32_t i = i0 + lane;
         bool wi = i < nd.cap && P.slot_win[nd.slot_base + i];
@@ -187,98 +197,56 @@ __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, uint32_
             unsigned bal = __ballot_sync(0xffffffffu, wj);
             uint32_t lim = min(32u, nd.cap - j0);
             for (uint32_t t = 0; t < lim; t++) {
-                double s = __shfl_sync(0xffffffffu, sj, t);
+                double sc = __shfl_sync(0xffffffffu, sj, t);
                 uint32_t c = __shfl_sync(0xffffffffu, cj, t);
-                if (wi && ((bal >> t) & 1u) && (s > ai.score || (s == ai.score && c < ai.ctx))) rank++;
+                if (wi && ((bal >> t) & 1u) && (sc > ai.score || (sc == ai.score && c < ai.ctx))) rank++;
             }
         }
-        if (wi && rank < n_kept) {
-            for (uint32_t q = 0; q < outdeg; q++) {
+        const bool emit = wi && rank < n_kept;
+        for (uint32_t q = 0; q < outdeg; q++) {      // uniform trip count across the warp
+            uint32_t r = 0;
+            int32_t w = 0;
+            uint8_t st = RQ_INVALID;
+            if (emit) {
                 const uint32_t a = P.out_list[nd.out_b + q];
-                const uint32_t r = nd.req_base + rank * outdeg + q;
-                const int32_t w = P.arc_word[a];
+                r = nd.req_base + rank * outdeg + q;
+                w = P.arc_word[a];
                 P.rq_c[r] = ai.ctx;
                 P.rq_w[r] = w;
                 P.rq_arc[r] = a;
                 P.rq_parent[r] = nd.slot_base + i;
                 P.rq_score[r] = ai.score;
-                P.rq_stream[r] = nd.stream;
                 P.rq_dslot[r] = P.arc_slot[a] + rank;
                 P.rq_m[r] = OTF_UNSET;
-                uint8_t st = RQ_NOCACHE;
+                st = RQ_NOCACHE;
                 uint32_t cslot = OTF_UNSET;
-                if (S.enabled) {
-                    const unsigned long long key =
-                        ((((unsigned long long)ai.ctx) << 32) | (uint32_t)w) + 1ull;
-                    const uint32_t mask = S.kc_cap - 1;
-                    uint32_t s = (uint32_t)otf_hash64(key) & mask;
-                    uint32_t probes = 0;
-                    for (;;) {
-                        unsigned long long k = S.kc_key[kc_base + s];
-                        if (k == 0ull) {
-                            unsigned long long prev = atomicCAS(&S.kc_key[kc_base + s], 0ull, key);
-                            k = prev == 0ull ? key : prev;
-                        }
-                        if (k == key) break;
-                        s = (s + 1) & mask;
-                        if (++probes > S.kc_cap) { atomicOr(S.err, OTF_E_CACHE_FULL); s = OTF_UNSET; break; }
-                    }
-                    cslot = s;
-                    if (s != OTF_UNSET) {
-                        if (ld_volatile_u32(&S.kc_cnext[kc_base + s]) != OTF_UNSET) {
-                            st = RQ_HIT;
-                        } else {
-                            atomicMin(&S.kc_claim[kc_base + s], r);
-                            st = RQ_PENDING;
-                        }
-                    }
-                }
+                if (S.enabled) cslot = cache_probe(S, nd.stream, ai.ctx, w, r, &st);
                 P.rq_cslot[r] = cslot;
                 P.rq_state[r] = st;
             }
+            compact_primary(P, S, lc, emit && (st == RQ_PENDING || st == RQ_NOCACHE), r,
+                            emit ? ai.ctx : 0u, w, nd.stream);
         }
     }
-    // invalidate unused request slots of this node
-    for (uint32_t r = n_kept * outdeg + lane; r < nd.keep * outdeg; r += 32) {
-        P.rq_w[nd.req_base + r] = -1;
+    for (uint32_t r = n_kept * outdeg + lane; r < nd.keep * outdeg; r += 32)
         P.rq_state[nd.req_base + r] = RQ_INVALID;
-    }
 }
 
 // --------------------------------------------------------------------------
-// kernel 2: primaries = requests that must run the model (cache miss, first
-// claimant).  Ordered compaction keeps request order.
-// --------------------------------------------------------------------------
-__global__ void __launch_bounds__(SCAN_BLK) k_scan_prim(DevPlan P, DevStreams S, uint32_t n_req,
-                                                        unsigned long long *status, uint32_t *ticket) {
-    auto flag = [&](uint32_t r) -> bool {
-        uint8_t st = P.rq_state[r];
-        if (st == RQ_NOCACHE) return true;
-        if (st != RQ_PENDING) return false;
-        uint64_t kb = (uint64_t)P.rq_stream[r] * S.kc_cap;
-        return S.kc_claim[kb + P.rq_cslot[r]] == r;
-    };
-    auto out = [&](uint32_t r, uint32_t m, bool f) {
-        if (!f) return;
-        const uint32_t s = P.rq_stream[r];
-        P.rq_m[r] = m;
-        P.pr_req[m] = r;
-        P.pr_w[m] = P.rq_w[r];
-        P.pr_stream[m] = s;
-        P.pr_inrow[m] = (int32_t)S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + P.rq_c[r]];
-    };
-    chained_scan(n_req, status, ticket, flag, out, &P.counters[0]);
-}
-
-// --------------------------------------------------------------------------
-// kernel 3: HS + MaxEnt score of the primaries (warp per primary) and the
-// successor history (history + (w,))[-order:] (rnnlm.py:187) of new rows
+// stage 2a: HS + MaxEnt score of the computed requests (warp per request),
+// successor history (history + (w,))[-order:] (rnnlm.py:187) and its digest
 // --------------------------------------------------------------------------
 template <int VEC, int CPL>
-__global__ void __launch_bounds__(256) k_hs_prim(DevModel m, DevPlan P, DevStreams S, uint32_t cap) {
-    const uint32_t n = P.counters[0];
+__global__ void __launch_bounds__(256) k_hs_prim(DevModel m, DevPlan P, DevStreams S, RowSpec rs) {
+    const uint32_t n = *rs.n_dev;
+    const uint32_t base = row_base(rs);
     const uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
+    if (q == 0 && lane == 0) rs.cur->base = base;   // also written by the update kernel (same value)
+    if ((uint64_t)base + n > S.arena_rows) {
+        if (q == 0 && lane == 0) atomicOr(S.err, OTF_E_ARENA_FULL);
+        return;
+    }
     if (q >= n) return;
     const uint32_t row = (uint32_t)P.pr_inrow[q];
     const uint32_t *meta = S.arena_meta + (size_t)row * OTF_META;
@@ -287,177 +255,31 @@ __global__ void __launch_bounds__(256) k_hs_prim(DevModel m, DevPlan P, DevStrea
     const uint32_t o0 = __ldg(m.path_off + w), o1 = __ldg(m.path_off + w + 1);
     double lp = hs_logprob_warp<VEC, CPL>(m, S.arena_h + (size_t)row * m.H, meta + 1, L,
                                           m.path_code + o0, o1 - o0, lane);
-    const uint32_t base = P.counters[2];
+    // new history: drop the oldest word once `order` are stored
+    const int nl = L + 1 > m.order ? m.order : L + 1;
+    const int drop = L + 1 - nl;
+    uint32_t v = 0;
+    if (lane == 0) v = (uint32_t)nl;
+    else if (lane < nl) v = meta[lane + drop];
+    else if (lane == nl) v = (uint32_t)w;
+    unsigned long long d = lane < OTF_META ? dig_meta(lane, v) : 0ull;
+    if (lane < OTF_META) S.arena_meta[(size_t)(base + q) * OTF_META + lane] = v;
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
     if (lane == 0) {
-        if (P.alg) {   // algorithmic-work counters for the roofline (bench.py)
+        atomicAdd(&P.pr_dig[q], d);
+        if (P.alg) {   // algorithmic-work counters for the roofline (profiling runs)
             const int km = m.order < L ? m.order : L;
             atomicAdd(&P.alg[0], (unsigned long long)(o1 - o0));
             atomicAdd(&P.alg[1], (unsigned long long)(o1 - o0) * km);
             atomicAdd(&P.alg[2], 1ull);
         }
         P.pr_p[q] = lp;
-        uint32_t *mo = S.arena_meta + (size_t)(base + q) * OTF_META;
-        int nl = L + 1 > m.order ? m.order : L + 1;
-        int drop = L + 1 - nl;
-        uint32_t nm[OTF_META];
-#pragma unroll
-        for (int k = 0; k < OTF_META; k++) nm[k] = 0;
-        for (int k = 0; k < nl - 1; k++) nm[1 + k] = meta[1 + drop + k];
-        nm[nl] = (uint32_t)w;
-        nm[0] = (uint32_t)nl;
-#pragma unroll
-        for (int k = 0; k < OTF_META; k++) mo[k] = nm[k];
-    }
-}
-
-// arena capacity check + base row for this level (1 thread)
-__global__ void k_level_begin(DevPlan P, DevStreams S) {
-    const uint32_t base = *S.arena_used;
-    P.counters[2] = base;
-    if ((uint64_t)base + P.counters[0] > S.arena_rows) {
-        atomicOr(S.err, OTF_E_ARENA_FULL);
-        P.counters[0] = 0;   // drop the level: the run is failed and reported
     }
 }
 
 // --------------------------------------------------------------------------
-// kernel 5: content dedup (IndexTable.encode, context_table.py:74-86):
-// digest of (h' bytes, history) -> probe the stream's content table; a
-// pre-existing entry is confirmed by full comparison; a slot created in
-// this level is claimed by the lowest primary index.
-// --------------------------------------------------------------------------
-__device__ __forceinline__ bool rows_equal(const DevStreams &S, uint32_t ra, uint32_t rb, int lane) {
-    const float *a = S.arena_h + (size_t)ra * S.H, *b = S.arena_h + (size_t)rb * S.H;
-    bool eq = true;
-    for (int i = lane; i < S.H; i += 32) eq &= (__float_as_uint(a[i]) == __float_as_uint(b[i]));
-    if (lane < OTF_META) eq &= S.arena_meta[(size_t)ra * OTF_META + lane] == S.arena_meta[(size_t)rb * OTF_META + lane];
-    return __all_sync(0xffffffffu, eq);
-}
-
-__global__ void __launch_bounds__(256) k_dedup(DevPlan P, DevStreams S) {
-    const uint32_t n = P.counters[0];
-    const uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (q >= n) return;
-    const uint32_t row = P.counters[2] + q;
-    const uint32_t s = P.pr_stream[q];
-    // content digest: per-element mixes summed (order-independent reduction
-    // of position-tagged words; deterministic for identical content)
-    const float *h = S.arena_h + (size_t)row * S.H;
-    unsigned long long acc = 0;
-    for (int i = lane; i < S.H; i += 32)
-        acc += otf_hash64(((uint64_t)i << 32) ^ __float_as_uint(h[i]));
-    if (lane < OTF_META)
-        acc += otf_hash64(((uint64_t)(0x10000 + lane) << 32) ^ S.arena_meta[(size_t)row * OTF_META + lane]);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    const unsigned long long key = otf_hash64(acc) | 1ull;
-    const uint64_t base = (uint64_t)s * S.ct_cap;
-    const uint32_t mask = S.ct_cap - 1;
-    uint32_t slot = (uint32_t)(key >> 20) & mask;
-    for (uint32_t probes = 0;; probes++) {
-        if (probes > S.ct_cap) {
-            if (lane == 0) { atomicOr(S.err, OTF_E_TABLE_FULL); P.pr_ctslot[q] = OTF_UNSET; P.pr_found[q] = 0; }
-            return;
-        }
-        unsigned long long k = 0;
-        if (lane == 0) {
-            k = S.ct_key[base + slot];
-            if (k == 0ull) {
-                unsigned long long prev = atomicCAS(&S.ct_key[base + slot], 0ull, key);
-                k = prev == 0ull ? key : prev;
-            }
-        }
-        k = __shfl_sync(0xffffffffu, k, 0);
-        if (k == key) {
-            uint32_t idx = lane == 0 ? ld_volatile_u32(&S.ct_idx[base + slot]) : 0;
-            idx = __shfl_sync(0xffffffffu, idx, 0);
-            if (idx != OTF_UNSET) {   // stored by an earlier level / call
-                uint32_t srow = S.ct_row[base + slot];
-                if (rows_equal(S, srow, row, lane)) {
-                    if (lane == 0) { P.pr_ctslot[q] = OTF_UNSET; P.pr_found[q] = idx; }
-                    return;
-                }
-            } else {
-                if (lane == 0) { atomicMin(&S.ct_claim[base + slot], q); P.pr_ctslot[q] = slot; }
-                return;
-            }
-        }
-        slot = (slot + 1) & mask;
-    }
-}
-
-// kernel 6: ordered numbering of novel contexts (new index = len + 1 in
-// request order per stream)
-__global__ void __launch_bounds__(SCAN_BLK) k_scan_novel(DevPlan P, DevStreams S, unsigned long long *status,
-                                                         uint32_t *ticket) {
-    const uint32_t n = P.counters[0];
-    auto flag = [&](uint32_t q) -> bool {
-        uint32_t slot = P.pr_ctslot[q];
-        if (slot == OTF_UNSET) return false;
-        return S.ct_claim[(uint64_t)P.pr_stream[q] * S.ct_cap + slot] == q;
-    };
-    // pr_E[q] = novel primaries before q (all q); the stream's first primary
-    // also records the stream's base so numbering restarts per stream
-    auto out = [&](uint32_t q, uint32_t e, bool) {
-        P.pr_E[q] = e;
-        const uint32_t s = P.pr_stream[q];
-        if (q == 0 || P.pr_stream[q - 1] != s) P.first_E[s] = e;
-    };
-    chained_scan(n, status, ticket, flag, out, &P.counters[1]);
-}
-
-// --------------------------------------------------------------------------
-// kernel 7: assign indices, fill the IndexTable / cache values
-// --------------------------------------------------------------------------
-__global__ void k_resolve(DevPlan P, DevStreams S) {
-    const uint32_t n = P.counters[0];
-    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= n) return;
-    const uint32_t s = P.pr_stream[q];
-    const uint32_t slot = P.pr_ctslot[q];
-    const uint32_t base_row = P.counters[2];
-    uint32_t cn;
-    if (slot == OTF_UNSET) {
-        cn = P.pr_found[q];
-    } else {
-        const uint64_t cb = (uint64_t)s * S.ct_cap;
-        const uint32_t win = S.ct_claim[cb + slot];
-        const uint32_t idx = S.table_len[s] + (P.pr_E[win] - P.first_E[s]) + 1u;
-        cn = idx;
-        if (win == q) {
-            if (idx > S.max_ctx) {
-                atomicOr(S.err, OTF_E_TABLE_FULL);
-            } else {
-                S.ct_idx[cb + slot] = idx;
-                S.ct_row[cb + slot] = base_row + q;
-                S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + idx] = base_row + q;
-                atomicAdd(&S.novel_cnt[s], 1u);
-            }
-        } else {
-            // same digest claimed by another primary: must be identical content
-            const float *a = S.arena_h + (size_t)(base_row + q) * S.H;
-            const float *b = S.arena_h + (size_t)(base_row + win) * S.H;
-            bool eq = true;
-            for (int i = 0; i < S.H; i++) eq &= __float_as_uint(a[i]) == __float_as_uint(b[i]);
-            for (int i = 0; i < OTF_META; i++)
-                eq &= S.arena_meta[(size_t)(base_row + q) * OTF_META + i] ==
-                      S.arena_meta[(size_t)(base_row + win) * OTF_META + i];
-            if (!eq) atomicOr(S.err, OTF_E_HASH);
-        }
-    }
-    P.pr_cnext[q] = cn;
-    const uint32_t r = P.pr_req[q];
-    if (S.enabled) {
-        const uint64_t kb = (uint64_t)s * S.kc_cap + P.rq_cslot[r];
-        S.kc_p[kb] = P.pr_p[q];
-        __threadfence();
-        S.kc_cnext[kb] = cn;
-    }
-}
-
-// --------------------------------------------------------------------------
-// kernel 8: finish requests: small-LM delta, score, arrival write, counters
+// stage 3: per-stream ordered resolution + finish
 // --------------------------------------------------------------------------
 __device__ __forceinline__ bool ng_get(const uint64_t *tag, const int32_t *words, const double *val,
                                        uint32_t cap, int width, const int32_t *key, int len,
@@ -511,65 +333,146 @@ __device__ __forceinline__ bool ngram_logprob_dev(const DevNgram &g, const uint3
     return false;
 }
 
-__global__ void __launch_bounds__(256) k_finish(DevPlan P, DevStreams S, DevNgram g, uint32_t n_req,
-                                                uint32_t lvl, double lm_weight) {
-    const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r == 0) *S.arena_used += P.counters[0];
-    if (r < (uint32_t)S.S) {
-        uint32_t nc = S.novel_cnt[r];
-        if (nc) { S.table_len[r] += nc; S.novel_cnt[r] = 0; }
+__device__ __forceinline__ bool rows_equal_lane(const DevStreams &S, uint32_t ra, uint32_t rb) {
+    const float *a = S.arena_h + (size_t)ra * S.H, *b = S.arena_h + (size_t)rb * S.H;
+    for (int i = 0; i < S.H; i++)
+        if (__float_as_uint(a[i]) != __float_as_uint(b[i])) return false;
+    for (int i = 0; i < OTF_META; i++)
+        if (S.arena_meta[(size_t)ra * OTF_META + i] != S.arena_meta[(size_t)rb * OTF_META + i]) return false;
+    return true;
+}
+
+// MODE 0: decode (finish requests into arrival slots)
+// MODE 1: Table-1 batch API (write p / c' / hit per request)
+template <int MODE>
+__global__ void __launch_bounds__(256) k_assign(DevPlan P, DevStreams S, DevNgram g, uint32_t lvl,
+                                                uint32_t range_begin, uint32_t n_ranges, double lm_weight,
+                                                double *out_p, uint32_t *out_cn, uint8_t *out_hit) {
+    const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    const LevelCtr lc = P.lvl[lvl];
+    if (MODE == 1 && wid == 0 && lane == 0) *S.arena_used = lc.base + lc.n_prim;
+    if (wid >= n_ranges) return;
+    if ((uint64_t)lc.base + lc.n_prim > S.arena_rows) return;   // flagged by stage 2
+    const StreamRange rg = P.ranges[range_begin + wid];
+    const uint32_t s = rg.stream;
+    const uint64_t kb = (uint64_t)s * S.kc_cap, cb = (uint64_t)s * S.ct_cap;
+    const uint32_t cmask = S.ct_cap - 1;
+    uint32_t tlen = S.table_len[s];
+    unsigned long long n_look = 0, n_hit = 0, n_miss = 0, n_ins = 0;
+    bool full = false;
+    for (uint32_t r0 = rg.rb; r0 < rg.re; r0 += 32) {
+        const uint32_t r = r0 + lane;
+        const bool in = r < rg.re;
+        const uint8_t st = in ? P.rq_state[r] : (uint8_t)RQ_INVALID;
+        const bool valid = st != RQ_INVALID;
+        const uint32_t cslot = (st == RQ_HIT || st == RQ_PENDING) ? P.rq_cslot[r] : OTF_UNSET;
+        bool prim = st == RQ_NOCACHE;
+        if (st == RQ_PENDING) prim = S.kc_claim[kb + cslot] == r;
+        const uint32_t m = prim ? P.rq_m[r] : OTF_UNSET;
+        // --- successor context of primaries: dedup + ordered numbering ---
+        unsigned long long key = 0;
+        uint32_t row = 0, cn = OTF_UNSET;
+        if (prim) {
+            key = otf_hash64(P.pr_dig[m]) | 1ull;
+            row = lc.base + m;
+            uint32_t slot = (uint32_t)(key >> 20) & cmask;   // entries from earlier levels / chunks
+            for (uint32_t probes = 0; probes <= S.ct_cap; probes++) {
+                const unsigned long long k = S.ct_key[cb + slot];
+                if (k == 0ull) break;
+                if (k == key && rows_equal_lane(S, S.ct_row[cb + slot], row)) { cn = S.ct_idx[cb + slot]; break; }
+                slot = (slot + 1) & cmask;
+            }
+        }
+        // duplicates inside this chunk: the earliest lane with equal content
+        const bool novel = prim && cn == OTF_UNSET;
+        int dup_of = -1;
+        const unsigned nov_bal = __ballot_sync(0xffffffffu, novel);
+        if (nov_bal & (nov_bal - 1)) {          // at least two novel lanes: compare digests
+            for (int t = 0; t < 32; t++) {
+                const unsigned long long kt = __shfl_sync(0xffffffffu, key, t);
+                const uint32_t rowt = __shfl_sync(0xffffffffu, row, t);
+                if (novel && dup_of < 0 && t < lane && ((nov_bal >> t) & 1u) && kt == key) {
+                    if (rows_equal_lane(S, rowt, row)) dup_of = t;
+                    else atomicOr(S.err, OTF_E_HASH);
+                }
+            }
+        }
+        const bool first = novel && dup_of < 0;
+        const unsigned fb = __ballot_sync(0xffffffffu, first);
+        if (first) {
+            const uint32_t idx = tlen + __popc(fb & ((1u << lane) - 1u)) + 1u;   // len + 1 (context_table.py:83-86)
+            if (idx > S.max_ctx) {
+                full = true;
+            } else {
+                cn = idx;
+                uint32_t slot = (uint32_t)(key >> 20) & cmask;
+                for (uint32_t probes = 0; probes <= S.ct_cap; probes++, slot = (slot + 1) & cmask)
+                    if (atomicCAS(&S.ct_key[cb + slot], 0ull, key) == 0ull) break;
+                S.ct_idx[cb + slot] = idx;
+                S.ct_row[cb + slot] = row;
+                S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + idx] = row;
+            }
+        }
+        tlen += __popc(fb);
+        const uint32_t dup_cn = __shfl_sync(0xffffffffu, cn, dup_of < 0 ? lane : dup_of);
+        if (dup_of >= 0) cn = dup_cn;
+        // cache fill by the claim winner, then the value for every request
+        double p = 0.0;
+        if (prim) {
+            p = P.pr_p[m];
+            if (st == RQ_PENDING) { S.kc_p[kb + cslot] = p; S.kc_cnext[kb + cslot] = cn; }
+        }
+        __syncwarp();
+        if (valid && !prim) {   // hit: earlier level, or an earlier request of this level
+            p = S.kc_p[kb + cslot];
+            cn = S.kc_cnext[kb + cslot];
+        }
+        n_look += __popc(__ballot_sync(0xffffffffu, valid));
+        n_miss += __popc(__ballot_sync(0xffffffffu, prim));
+        n_hit += __popc(__ballot_sync(0xffffffffu, valid && !prim));
+        if (S.enabled) n_ins += __popc(__ballot_sync(0xffffffffu, prim));
+        if (!valid) continue;
+        if (MODE == 1) {
+            out_p[r] = p; out_cn[r] = cn; out_hit[r] = prim ? 0 : 1;
+            continue;
+        }
+        // --- finish: small-LM delta, score, arrival ---
+        const uint32_t c = P.rq_c[r];
+        const int w = P.rq_w[r];
+        const uint32_t crow = S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + c];
+        const uint32_t *meta = S.arena_meta + (size_t)crow * OTF_META;
+        double ps;
+        if (!ngram_logprob_dev(g, meta + 1, (int)meta[0], w, &ps)) { atomicOr(S.err, OTF_E_KEY); ps = 0.0; }
+        const float delta = __double2float_rn(__dsub_rn(p, ps));    // codec.py:57-59
+        const uint32_t a = P.rq_arc[r];
+        // decoder.py:144: (score + acoustic) + lm_weight * (smalllm + delta)
+        const double ns = __dadd_rn(__dadd_rn(P.rq_score[r], P.arc_ac[a]),
+                                    __dmul_rn(lm_weight, __dadd_rn(P.arc_slm[a], (double)delta)));
+        Arrival out;
+        out.score = ns; out.ctx = cn; out.parent = P.rq_parent[r]; out.arc = a;
+        out.lvl = lvl; out.ridx = r; out.pad = 0;
+        P.arr[P.rq_dslot[r]] = out;
     }
-    if (r >= n_req) return;
-    const uint8_t st = P.rq_state[r];
-    if (st == RQ_INVALID) return;
-    const uint32_t s = P.rq_stream[r];
-    double p;
-    uint32_t cn;
-    const uint32_t m = P.rq_m[r];
-    if (m != OTF_UNSET) {
-        p = P.pr_p[m];
-        cn = P.pr_cnext[m];
-    } else {
-        const uint64_t kb = (uint64_t)s * S.kc_cap + P.rq_cslot[r];
-        p = S.kc_p[kb];
-        cn = S.kc_cnext[kb];
+    if (lane == 0) {
+        if (full) atomicOr(S.err, OTF_E_TABLE_FULL);
+        S.table_len[s] = full ? S.max_ctx : tlen;
+        unsigned long long *stt = S.stats + (size_t)s * 8;
+        stt[0] += n_look; stt[1] += n_hit; stt[2] += n_miss; stt[6] += n_ins; stt[7] += n_look;
     }
-    const uint32_t c = P.rq_c[r];
-    const int w = P.rq_w[r];
-    const uint32_t row = S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + c];
-    const uint32_t *meta = S.arena_meta + (size_t)row * OTF_META;
-    double ps;
-    if (!ngram_logprob_dev(g, meta + 1, (int)meta[0], w, &ps)) {
-        atomicOr(S.err, OTF_E_KEY);
-        ps = 0.0;
-    }
-    const float delta = __double2float_rn(__dsub_rn(p, ps));    // codec.py:57-59
-    const uint32_t a = P.rq_arc[r];
-    // decoder.py:144: (score + acoustic) + lm_weight * (smalllm + delta)
-    const double ns = __dadd_rn(__dadd_rn(P.rq_score[r], P.arc_ac[a]),
-                                __dmul_rn(lm_weight, __dadd_rn(P.arc_slm[a], (double)delta)));
-    Arrival out;
-    out.score = ns; out.ctx = cn; out.parent = P.rq_parent[r]; out.arc = a;
-    out.lvl = lvl; out.ridx = r; out.pad = 0;
-    P.arr[P.rq_dslot[r]] = out;
-    unsigned long long *stt = S.stats + (size_t)s * 8;
-    atomicAdd(&stt[0], 1ull);                        // lookups
-    if (m != OTF_UNSET) {                            // misses (model runs)
-        atomicAdd(&stt[2], 1ull);
-        if (S.enabled) atomicAdd(&stt[6], 1ull);     // cache entries
-    } else {
-        atomicAdd(&stt[1], 1ull);                    // hits
-    }
-    atomicAdd(&stt[7], 1ull);                        // expansions this run
 }
 
 // --------------------------------------------------------------------------
 // final: best token over sorted finals x sorted ctx (decoder.py:150-156),
 // backtrace (decoder.py:157-162), score breakdown (decoder.py:163-169)
 // --------------------------------------------------------------------------
-__global__ void k_final(DevPlan P, DevStreams S, double lm_weight) {
+__global__ void k_final(DevPlan P, DevStreams S, double lm_weight, int last_lvl) {
     const uint32_t u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
+    if (u == 0 && lane == 0 && last_lvl >= 0) {   // arena rows in use after the run
+        const uint32_t end = P.lvl[last_lvl].base + P.lvl[last_lvl].n_prim;
+        if (end <= S.arena_rows) *S.arena_used = end;
+    }
     if (u >= P.n_utt) return;
     bool have = false;
     double best = 0.0;
@@ -578,7 +481,6 @@ __global__ void k_final(DevPlan P, DevStreams S, double lm_weight) {
         const NodeInfo nd = P.nodes[P.finals[f]];
         if (nd.cap == 0) continue;
         recombine_node(P.arr, P.slot_win, nd.slot_base, nd.cap, lane);
-        // best winner of this node: max score, ties -> smallest ctx
         double bs = 0.0; uint32_t bc = OTF_UNSET, bslot = OTF_UNSET; bool bh = false;
         for (uint32_t i0 = 0; i0 < nd.cap; i0 += 32) {
             uint32_t i = i0 + lane;
@@ -619,16 +521,12 @@ __global__ void k_final(DevPlan P, DevStreams S, double lm_weight) {
     P.out_status[u] = 0;
 }
 
-__global__ void k_init_starts(DevPlan P) {
-    const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= P.n_utt) return;
-    Arrival a;
-    a.score = 0.0; a.ctx = 0; a.parent = OTF_UNSET; a.arc = OTF_UNSET; a.lvl = 0; a.ridx = 0; a.pad = 0;
-    P.arr[P.utt_start_slot[u]] = a;
-}
-
-__global__ void k_run_begin(DevStreams S) {
-    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= (uint32_t)S.S) return;
-    S.stats[(size_t)s * 8 + 7] = 0;
+__global__ void k_run_begin(DevPlan P, DevStreams S) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < P.n_utt) {
+        Arrival a;
+        a.score = 0.0; a.ctx = 0; a.parent = OTF_UNSET; a.arc = OTF_UNSET; a.lvl = 0; a.ridx = 0; a.pad = 0;
+        P.arr[P.utt_start_slot[t]] = a;
+    }
+    if (t < (uint32_t)S.S) S.stats[(size_t)t * 8 + 7] = 0;
 }

@@ -20,6 +20,53 @@
 
 #define HS_G 8
 
+// f32 -> f64 with integer ops (rebias the exponent, shift the mantissa):
+// the F2F conversion unit was the top stall reason of the first version.
+// Exact for normal numbers and zero; f32 denormals (|x| < 1.2e-38) flush to
+// signed zero, a change far below one f64 ulp of any activation sum.
+__device__ __forceinline__ double widen(float x) {
+    const uint32_t u = __float_as_uint(x);
+    const uint32_t hi = (u & 0x80000000u) | (((u >> 3) & 0x0FFFFFFFu) + (896u << 20));
+    const uint32_t lo = u << 29;
+    return (u & 0x7F800000u) ? __hiloint2double((int)hi, (int)lo)
+                             : __hiloint2double((int)(u & 0x80000000u), 0);
+}
+
+// Reduce 8 per-lane partial sums across the warp with 9 exchanges (instead of
+// 8 x 5 butterflies): each step halves the vector, lanes keep one half and
+// receive the partner's other half.  Afterwards the full sum of node g is in
+// the 4 lanes whose bits (4,3,2) spell g; lane_of(g) names the first of them.
+__device__ __forceinline__ double reduce8(double (&v)[8], int lane) {
+    const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        double send = u16 ? v[i] : v[i + 4];
+        double keep = u16 ? v[i + 4] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+        double send = u8 ? v[i] : v[i + 2];
+        double keep = u8 ? v[i + 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    {
+        double send = u4 ? v[0] : v[1];
+        double keep = u4 ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    double x = v[0];
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    return x;
+}
+__device__ __forceinline__ int node_of_lane(int lane) {
+    return ((lane >> 4) & 1) << 2 | ((lane >> 3) & 1) << 1 | ((lane >> 2) & 1);
+}
+__device__ __forceinline__ int lane_of_node(int g) {
+    return ((g >> 2) & 1) << 4 | ((g >> 1) & 1) << 3 | (g & 1) << 2;
+}
+
 template <int VEC, int CPL>
 __device__ __forceinline__ double hs_logprob_warp(const DevModel &m, const float *__restrict__ h,
                                                   const uint32_t *__restrict__ hist, int L,
@@ -27,24 +74,24 @@ __device__ __forceinline__ double hs_logprob_warp(const DevModel &m, const float
                                                   int lane) {
     const int H = m.H;
     const int NCH = VEC == 4 ? (H >> 2) : H;   // chunks of VEC floats
-    double hv[CPL][VEC];                        // hidden state, converted once
+    double hv[CPL][VEC];                        // hidden state, widened once
 #pragma unroll
     for (int c = 0; c < CPL; c++) {
         int k = lane + 32 * c;
         if (k < NCH) {
             if (VEC == 4) {
                 float4 t = __ldg(reinterpret_cast<const float4 *>(h) + k);
-                hv[c][0] = t.x; hv[c][1] = t.y; hv[c][2] = t.z; hv[c][3] = t.w;
+                hv[c][0] = widen(t.x); hv[c][1] = widen(t.y); hv[c][2] = widen(t.z); hv[c][3] = widen(t.w);
             } else {
-                hv[c][0] = __ldg(h + k);
+                hv[c][0] = widen(__ldg(h + k));
             }
         } else {
 #pragma unroll
             for (int v = 0; v < VEC; v++) hv[c][v] = 0.0;
         }
     }
-    // MaxEnt hash prefixes: order-k feature hashes (k, last k words oldest
-    // first) and then the node id (_kernels_nb.py:27-33, :72-74).
+    // MaxEnt hash prefixes: order-k feature hash of (k, last k words oldest
+    // first), finished per node (_kernels_nb.py:27-33, :72-74)
     const int kmax = m.order < L ? m.order : L;
     uint64_t pre[OTF_MAX_ORDER];
 #pragma unroll
@@ -56,82 +103,54 @@ __device__ __forceinline__ double hs_logprob_warp(const DevModel &m, const float
             pre[k] = x;
         }
     }
+    const int my_g = node_of_lane(lane);
+    const bool leader = (lane & 3) == 0;
     double lp = 0.0;
     for (uint32_t p0 = 0; p0 < P; p0 += HS_G) {
-        uint32_t code[HS_G];
-        double acc[HS_G];
+        // this lane's node (for the MaxEnt / log-sigmoid part)
+        const uint32_t my_code = (p0 + my_g < P) ? __ldg(codes + p0 + my_g) : OTF_UNSET;
+        double me[OTF_MAX_ORDER];
 #pragma unroll
-        for (int g = 0; g < HS_G; g++) code[g] = (p0 + g < P) ? __ldg(codes + p0 + g) : OTF_UNSET;
-        // MaxEnt gathers first (independent of the dot products): lane j ->
-        // (node g = j / kmax, order k = j % kmax); order > 4 spills below
-        double me = 0.0;
-        if (lane < HS_G * kmax) {
-            int g = lane / kmax, k = lane - g * kmax;
-            uint32_t cg = 0; uint64_t pk = 0;
-#pragma unroll
-            for (int t = 0; t < HS_G; t++) if (t == g) cg = code[t];
-#pragma unroll
-            for (int t = 0; t < OTF_MAX_ORDER; t++) if (t == k) pk = pre[t];
-            if (cg != OTF_UNSET) {
-                uint64_t idx = otf_mix(pk, (uint64_t)(cg & 0x7FFFFFFFu)) & m.mask;
-                me = (double)__ldg(m.ME + idx);
-            }
+        for (int k = 0; k < OTF_MAX_ORDER; k++) {
+            me[k] = 0.0;
+            if (leader && k < kmax && my_code != OTF_UNSET)
+                me[k] = (double)__ldg(m.ME + (otf_mix(pre[k], (uint64_t)(my_code & 0x7FFFFFFFu)) & m.mask));
         }
+        double acc[HS_G];
 #pragma unroll
         for (int g = 0; g < HS_G; g++) {
             acc[g] = 0.0;
-            if (code[g] != OTF_UNSET) {
-                const float *row = m.NV + (size_t)(code[g] & 0x7FFFFFFFu) * H;
+            const uint32_t cg = (p0 + g < P) ? __ldg(codes + p0 + g) : OTF_UNSET;
+            if (cg != OTF_UNSET) {
+                const float *row = m.NV + (size_t)(cg & 0x7FFFFFFFu) * H;
 #pragma unroll
                 for (int c = 0; c < CPL; c++) {
                     int k = lane + 32 * c;
                     if (k < NCH) {
                         if (VEC == 4) {
                             float4 t = __ldg(reinterpret_cast<const float4 *>(row) + k);
-                            acc[g] = fma((double)t.x, hv[c][0], acc[g]);
-                            acc[g] = fma((double)t.y, hv[c][1], acc[g]);
-                            acc[g] = fma((double)t.z, hv[c][2], acc[g]);
-                            acc[g] = fma((double)t.w, hv[c][3], acc[g]);
+                            acc[g] = fma(widen(t.x), hv[c][0], acc[g]);
+                            acc[g] = fma(widen(t.y), hv[c][1], acc[g]);
+                            acc[g] = fma(widen(t.z), hv[c][2], acc[g]);
+                            acc[g] = fma(widen(t.w), hv[c][3], acc[g]);
                         } else {
-                            acc[g] = fma((double)__ldg(row + k), hv[c][0], acc[g]);
+                            acc[g] = fma(widen(__ldg(row + k)), hv[c][0], acc[g]);
                         }
                     }
                 }
             }
         }
+        // a_g = dot + ME[k=1] + ME[k=2] + ... (reference order, :72-74)
+        double a = reduce8(acc, lane);
 #pragma unroll
-        for (int g = 0; g < HS_G; g++) acc[g] = warp_sum_d(acc[g]);
-        // node activation a_g = dot + ME[k=1] + ME[k=2] + ... in order; lane g
-        // keeps a_g and all G log-sigmoids are evaluated in one pass
-        double my_a = 0.0;
-#pragma unroll
-        for (int g = 0; g < HS_G; g++) {
-            double a = acc[g];
-            for (int k = 0; k < kmax; k++) {
-                int j = g * kmax + k;
-                double v = __shfl_sync(0xffffffffu, me, j & 31);
-                if (j >= 32) {  // order > 4 overflow: gather directly
-                    uint64_t pk = 0;
-#pragma unroll
-                    for (int t = 0; t < OTF_MAX_ORDER; t++) if (t == k) pk = pre[t];
-                    v = code[g] != OTF_UNSET
-                            ? (double)__ldg(m.ME + (otf_mix(pk, (uint64_t)(code[g] & 0x7FFFFFFFu)) & m.mask))
-                            : 0.0;
-                }
-                a += v;
-            }
-            if (lane == g) my_a = a;
-        }
-        uint32_t my_code = OTF_UNSET;
-#pragma unroll
-        for (int g = 0; g < HS_G; g++) if (lane == g) my_code = code[g];
+        for (int k = 0; k < OTF_MAX_ORDER; k++) if (k < kmax) a += me[k];
         double mylog = 0.0;
-        if (my_code != OTF_UNSET)
-            mylog = otf_log_sigmoid((my_code & 0x80000000u) ? -my_a : my_a);   // sign -1 for bit 1
+        if (leader && my_code != OTF_UNSET)
+            mylog = otf_log_sigmoid((my_code & 0x80000000u) ? -a : a);   // sign -1 for bit 1
 #pragma unroll
         for (int g = 0; g < HS_G; g++) {
-            double v = __shfl_sync(0xffffffffu, mylog, g);
-            if (code[g] != OTF_UNSET) lp += v;
+            const double v = __shfl_sync(0xffffffffu, mylog, lane_of_node(g));
+            if (p0 + g < P) lp += v;
         }
     }
     return lp;
@@ -219,15 +238,18 @@ __global__ void k_feature_index(uint64_t seed, uint64_t mask, int64_t n, const i
 // columns i (coalesced reads of W^T rows), QT queries share each W^T load.
 // --------------------------------------------------------------------------
 template <int QT>
-__global__ void __launch_bounds__(256) k_advance_f64(DevModel m, uint32_t n_cap, const uint32_t *n_dev,
+__global__ void __launch_bounds__(256) k_advance_f64(DevModel m, uint32_t n_cap, RowSpec rs,
                                                      const int32_t *__restrict__ in_row,
                                                      const int32_t *__restrict__ words,
                                                      const float *__restrict__ h_base,
-                                                     float *__restrict__ out_base,
-                                                     const uint32_t *out_row0_dev) {
+                                                     float *__restrict__ out_base, uint32_t row_limit) {
     extern __shared__ float4 smem4[];
     float *hs = reinterpret_cast<float *>(smem4);
-    const uint32_t n = n_dev ? *n_dev : n_cap;
+    __shared__ unsigned long long s_dig[QT];
+    const uint32_t n = rs.n_dev ? *rs.n_dev : n_cap;
+    const uint32_t out0 = row_base(rs);
+    if (rs.cur && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) rs.cur->base = out0;
+    if ((uint64_t)out0 + n > row_limit) return;     // arena overflow (flagged by the HS stage)
     const uint32_t q0 = blockIdx.x * QT;
     if (q0 >= n) return;
     const int H = m.H;
@@ -236,8 +258,11 @@ __global__ void __launch_bounds__(256) k_advance_f64(DevModel m, uint32_t n_cap,
         int q = t / H, j = t - q * H;
         hs[t] = q < nq ? h_base[(size_t)in_row[q0 + q] * H + j] : 0.f;
     }
+    if (threadIdx.x < QT) s_dig[threadIdx.x] = 0ull;
     __syncthreads();
-    const uint32_t out0 = out_row0_dev ? *out_row0_dev : 0u;
+    unsigned long long dg[QT];
+#pragma unroll
+    for (int q = 0; q < QT; q++) dg[q] = 0ull;
     for (int i = threadIdx.x + blockIdx.y * blockDim.x; i < H; i += blockDim.x * gridDim.y) {
         double acc[QT];
 #pragma unroll
@@ -251,6 +276,21 @@ __global__ void __launch_bounds__(256) k_advance_f64(DevModel m, uint32_t n_cap,
         }
 #pragma unroll
         for (int q = 0; q < QT; q++)
-            if (q < nq) out_base[(size_t)(out0 + q0 + q) * H + i] = (float)otf_sigmoid(acc[q]);
+            if (q < nq) {
+                const float o = (float)otf_sigmoid(acc[q]);
+                out_base[(size_t)(out0 + q0 + q) * H + i] = o;
+                dg[q] += otf_hash64(((uint64_t)i << 32) ^ __float_as_uint(o));
+            }
+    }
+    if (rs.dig) {
+#pragma unroll
+        for (int q = 0; q < QT; q++) {
+            unsigned long long d = dg[q];
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+            if ((threadIdx.x & 31) == 0 && q < nq) atomicAdd(&s_dig[q], d);
+        }
+        __syncthreads();
+        if (threadIdx.x < nq) atomicAdd(&rs.dig[q0 + threadIdx.x], s_dig[threadIdx.x]);
     }
 }

@@ -122,9 +122,9 @@ __device__ __forceinline__ uint32_t tile_off(int row, int c) {
 // Grid: (row tiles of 128, N tiles of bn columns).
 template <int MODE>
 __global__ void __launch_bounds__(NTHREADS, 1)
-k_advance_tc(DevModel m, uint32_t n_cap, const uint32_t *n_dev, const int32_t *__restrict__ in_row,
+k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__ in_row,
              const int32_t *__restrict__ words, const float *__restrict__ h_base,
-             float *__restrict__ out_base, const uint32_t *out_row0_dev, int bn, int stages,
+             float *__restrict__ out_base, uint32_t row_limit, int bn, int stages,
              uint32_t tmem_cols) {
     constexpr bool BF = MODE == 2;
     constexpr bool X3 = MODE == 1;
@@ -133,7 +133,10 @@ k_advance_tc(DevModel m, uint32_t n_cap, const uint32_t *n_dev, const int32_t *_
     constexpr int CH = KC_B / 16;                      // operand 16-byte chunks per row
     constexpr int RAW_ROW = KE * 4 + 16;               // raw fp32 row stride (+16 B pad)
     constexpr int RAW_CH = KE / 4;                     // raw 16-byte chunks per row
-    const uint32_t n = n_dev ? *n_dev : n_cap;
+    const uint32_t n = rs.n_dev ? *rs.n_dev : n_cap;
+    const uint32_t out0 = row_base(rs);
+    if (rs.cur && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) rs.cur->base = out0;
+    if ((uint64_t)out0 + n > row_limit) return;     // arena overflow (flagged by the HS stage)
     const uint32_t q0 = blockIdx.x * BM;
     if (q0 >= n) return;
     const int n0 = blockIdx.y * bn;                    // first output column of this CTA
@@ -311,7 +314,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, const uint32_t *n_dev, const int32_t *_
     const int row = tid;
     const uint32_t q = q0 + row;
     const bool valid = q < n;
-    const uint32_t out0 = out_row0_dev ? *out_row0_dev : 0u;
+    unsigned long long dig = 0ull;
     const float *urow = m.U + (size_t)s_w[row] * H;
     float *orow = out_base + (size_t)(out0 + q) * H;
     for (int c0 = 0; c0 < bn; c0 += 32) {
@@ -329,13 +332,22 @@ k_advance_tc(DevModel m, uint32_t n_cap, const uint32_t *n_dev, const int32_t *_
                     o.z = 1.f / (1.f + expf(-(v[j + 2] + u.z)));
                     o.w = 1.f / (1.f + expf(-(v[j + 3] + u.w)));
                     *reinterpret_cast<float4 *>(orow + gc + j) = o;
+                    dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o.x));
+                    dig += otf_hash64(((uint64_t)(gc + j + 1) << 32) ^ __float_as_uint(o.y));
+                    dig += otf_hash64(((uint64_t)(gc + j + 2) << 32) ^ __float_as_uint(o.z));
+                    dig += otf_hash64(((uint64_t)(gc + j + 3) << 32) ^ __float_as_uint(o.w));
                 }
             } else {
                 for (int j = 0; j < 32; j++)
-                    if (gc + j < H) orow[gc + j] = 1.f / (1.f + expf(-(v[j] + urow[gc + j])));
+                    if (gc + j < H) {
+                        const float o = 1.f / (1.f + expf(-(v[j] + urow[gc + j])));
+                        orow[gc + j] = o;
+                        dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o));
+                    }
             }
         }
     }
+    if (rs.dig && valid) atomicAdd(&rs.dig[q], dig);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
@@ -344,9 +356,9 @@ k_advance_tc(DevModel m, uint32_t n_cap, const uint32_t *n_dev, const int32_t *_
 
 }  // namespace tc
 
-static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const uint32_t *n_dev,
+static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const RowSpec &rs,
                              const int32_t *in_row, const int32_t *words, const float *h_base,
-                             float *out_base, const uint32_t *out_row0, cudaStream_t s) {
+                             float *out_base, uint32_t row_limit, cudaStream_t s) {
     const int H = m.H;
     // N per MMA must be a multiple of 16 (M = 128) and <= 256; above 256 the
     // N tile is issued as two MMAs, so pad to 32
@@ -374,8 +386,8 @@ static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const 
     do {                                                                                        \
         e = cudaFuncSetAttribute(tc::k_advance_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (e != cudaSuccess) return -9;                                                        \
-        tc::k_advance_tc<MODE><<<grid, tc::NTHREADS, smem, s>>>(m, n_cap, n_dev, in_row, words, h_base, \
-                                                                 out_base, out_row0, bn, stages, cols); \
+        tc::k_advance_tc<MODE><<<grid, tc::NTHREADS, smem, s>>>(m, n_cap, rs, in_row, words, h_base, \
+                                                                 out_base, row_limit, bn, stages, cols); \
     } while (0)
     if (prec == 1) TC_LAUNCH(1);
     else if (prec == 2) TC_LAUNCH(2);
