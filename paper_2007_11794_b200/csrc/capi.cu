@@ -786,6 +786,8 @@ static int plan_alloc_workspace(OtflmPlan *p, uint32_t R, uint32_t n_lvl_slots) 
     bad |= p->mem.alloc(&d.rq_w, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.rq_state, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.rq_score, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.rq_slm, R) != cudaSuccess;
+    bad |= p->mem.alloc(&d.rq_ps, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.pr_req, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.pr_inrow, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.pr_w, R) != cudaSuccess;
@@ -928,17 +930,17 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
         const uint32_t nb0 = p->lvl_node_off[t], nn = p->lvl_node_off[t + 1] - nb0;
         const uint32_t R = p->lvl_req[t];
         if (nn == 0 || R == 0) {
-            if (nn) { ProfScope ps(K_EXPAND, s); k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, nb0, nn, (long long)p->beam, t); CKL(); }
+            if (nn) { ProfScope ps(K_EXPAND, s); k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, g->d, nb0, nn, (long long)p->beam, t); CKL(); }
             continue;
         }
-        { ProfScope ps(K_EXPAND, s); k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, nb0, nn, (long long)p->beam, t); CKL(); }
+        { ProfScope ps(K_EXPAND, s); k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, g->d, nb0, nn, (long long)p->beam, t); CKL(); }
         const RowSpec rs{&d.lvl[t].n_prim, &d.lvl[t], prev >= 0 ? &d.lvl[prev] : nullptr, S.arena_used, d.pr_dig};
         int rc = enqueue_stage2(p, m, S, R, prec, rs, s);
         if (rc) return rc;
         const uint32_t r0 = p->lvl_range_off[t], nr = p->lvl_range_off[t + 1] - r0;
         {
             ProfScope ps(K_ASSIGN, s);
-            k_assign<0><<<cdiv(nr, 4), 128, 0, s>>>(d, S, g->d, t, r0, nr, lm, nullptr, nullptr, nullptr);
+            k_assign<0><<<nr, ASSIGN_T, 0, s>>>(d, S, t, r0, lm, nullptr, nullptr, nullptr);
             CKL();
         }
         prev = (int)t;
@@ -1148,8 +1150,7 @@ extern "C" int otflm_rnnlm_prob_batch(OtflmStreams *s, int64_t n, const int32_t 
     const RowSpec rs{&p->d.lvl[0].n_prim, &p->d.lvl[0], nullptr, s->d.arena_used, p->d.pr_dig};
     int rc = enqueue_stage2(p, m, s->d, R, precision, rs, st);
     if (rc) return rc;
-    k_assign<1><<<cdiv(ranges.size(), 4), 128, 0, st>>>(p->d, s->d, DevNgram{}, 0, 0, (uint32_t)ranges.size(), 0.0,
-                                                      dp, dcn, dh);
+    k_assign<1><<<(unsigned)ranges.size(), ASSIGN_T, 0, st>>>(p->d, s->d, 0, 0, 0.0, dp, dcn, dh);
     CKL();
     std::vector<double> pp(n);
     std::vector<uint32_t> cn(n);

@@ -52,7 +52,8 @@ struct DevPlan {
     uint32_t *rq_c, *rq_arc, *rq_parent, *rq_cslot, *rq_m, *rq_dslot;
     int32_t *rq_w;
     uint8_t *rq_state;
-    double *rq_score;
+    double *rq_score;             // token score + arc acoustic (decoder.py:144 first sum)
+    double *rq_slm, *rq_ps;       // arc small-LM score; ngram_logprob(small_context(c), w)
     // primaries [R_max]
     uint32_t *pr_req;
     int32_t *pr_inrow, *pr_w;
@@ -160,12 +161,75 @@ __device__ __forceinline__ void compact_primary(DevPlan &P, const DevStreams &S,
     }
 }
 
+__device__ __forceinline__ bool ng_get(const uint64_t *tag, const int32_t *words, const double *val,
+                                       uint32_t cap, int width, const int32_t *key, int len,
+                                       double *out) {
+    const uint64_t h = otf_tuple_hash(key, len);
+    uint32_t s = (uint32_t)(h >> 7) & (cap - 1);
+    for (uint32_t probes = 0; probes <= cap; probes++) {
+        uint64_t t = tag[s];
+        if (t == 0) return false;
+        if (t == h) {
+            const int32_t *wk = words + (size_t)s * width;
+            if (wk[0] == len) {
+                bool eq = true;
+                for (int i = 0; i < len; i++) eq &= wk[1 + i] == key[i];
+                if (eq) { *out = val[s]; return true; }
+            }
+        }
+        s = (s + 1) & (cap - 1);
+    }
+    return false;
+}
+
+// ngram_logprob(small_context(history), w) (ngram.py:161-179, decoder.py:73-80)
+__device__ __forceinline__ bool ngram_logprob_dev(const DevNgram &g, const uint32_t *hist, int L,
+                                                  int w, double *out) {
+    int32_t ctx[OTF_MAX_ORDER + 1];
+    const int need = g.order - 1;
+    int n = 0;
+    for (int i = L; i < need; i++) ctx[n++] = g.bos;
+    for (int i = 0; i < L; i++) ctx[n++] = (int32_t)hist[i];
+    int keep = g.order > 1 ? g.order - 1 : 0;
+    if (keep > n) keep = n;
+    const int32_t *c = ctx + (n - keep);
+    int32_t buf[OTF_MAX_ORDER + 1];
+    const int width = g.order + 1;
+    for (int depth = 0; depth <= keep; depth++) {
+        int sl = keep - depth;
+        for (int i = 0; i < sl; i++) buf[i] = c[depth + i];
+        buf[sl] = w;
+        double v;
+        if (ng_get(g.p_tag, g.p_words, g.p_val, g.p_cap, width, buf, sl + 1, &v)) {
+            for (int sh = depth - 1; sh >= 0; sh--) {
+                double b;
+                if (!ng_get(g.b_tag, g.b_words, g.b_val, g.b_cap, width, c + sh, keep - sh, &b)) b = 0.0;
+                v = __dadd_rn(b, v);
+            }
+            *out = v;
+            return true;
+        }
+    }
+    return false;
+}
+
 // --------------------------------------------------------------------------
 // stage 1: expand one level (warp per node)
 // --------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, uint32_t node_begin,
+// Fast path: a node's arrivals fit one warp (cap <= 32, e.g. 24 at beam 8 /
+// breadth 3): arrivals live in registers, recombination and ranking are
+// shuffle sweeps, the kept tokens go to a per-warp shared table by rank, and
+// the (rank, arc) requests are spread over lanes so their cache probes and
+// small-LM lookups overlap.  Larger nodes (wide beams) take the general path
+// through the slot_win scratch.
+constexpr int EXP_WARPS = 8;
+__global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, DevNgram g, uint32_t node_begin,
                                                 uint32_t n_nodes, long long beam, uint32_t lvl) {
-    const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    __shared__ uint32_t s_ctx[EXP_WARPS][32], s_slot[EXP_WARPS][32];
+    __shared__ double s_score[EXP_WARPS][32];
+    __shared__ uint32_t s_arc[EXP_WARPS][32];
+    const uint32_t wib = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * EXP_WARPS + wib;
     const int lane = threadIdx.x & 31;
     if (gw >= n_nodes) return;
     LevelCtr *lc = &P.lvl[lvl];
@@ -175,58 +239,99 @@ __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, uint32_
         for (uint32_t r = lane; r < nd.keep * outdeg; r += 32) P.rq_state[nd.req_base + r] = RQ_INVALID;
         return;
     }
-    recombine_node(P.arr, P.slot_win, nd.slot_base, nd.cap, lane);
-    uint32_t n_win = 0;
-    for (uint32_t i0 = 0; i0 < nd.cap; i0 += 32) {
-        uint32_t i = i0 + lane;
-        bool wi = i < nd.cap && P.slot_win[nd.slot_base + i];
-        n_win += __popc(__ballot_sync(0xffffffffu, wi));
-    }
-    const uint32_t n_kept = (uint32_t)min((long long)n_win, beam);
-    for (uint32_t i0 = 0; i0 < nd.cap; i0 += 32) {
-        uint32_t i = i0 + lane;
-        bool wi = i < nd.cap && P.slot_win[nd.slot_base + i];
-        uint32_t rank = 0;
+    // out-arcs of the node (arc-id order), staged once
+    for (uint32_t q = lane; q < outdeg && q < 32; q += 32) s_arc[wib][q] = P.out_list[nd.out_b + q];
+    uint32_t n_kept = 0;
+    if (nd.cap <= 32) {
         Arrival ai;
-        if (wi) ai = P.arr[nd.slot_base + i];
-        for (uint32_t j0 = 0; j0 < nd.cap; j0 += 32) {
-            uint32_t j = j0 + lane;
-            bool wj = j < nd.cap && P.slot_win[nd.slot_base + j];
-            double sj = 0.0; uint32_t cj = 0;
-            if (wj) { Arrival aj = P.arr[nd.slot_base + j]; sj = aj.score; cj = aj.ctx; }
-            unsigned bal = __ballot_sync(0xffffffffu, wj);
-            uint32_t lim = min(32u, nd.cap - j0);
-            for (uint32_t t = 0; t < lim; t++) {
-                double sc = __shfl_sync(0xffffffffu, sj, t);
-                uint32_t c = __shfl_sync(0xffffffffu, cj, t);
-                if (wi && ((bal >> t) & 1u) && (sc > ai.score || (sc == ai.score && c < ai.ctx))) rank++;
-            }
+        bool vi = false;
+        if ((uint32_t)lane < nd.cap) { ai = P.arr[nd.slot_base + lane]; vi = ai.ctx != OTF_UNSET; }
+        const double si = vi ? ai.score : 0.0;
+        const uint32_t ci = vi ? ai.ctx : OTF_UNSET;
+        const uint64_t ki = vi ? arr_key(ai) : 0;
+        bool win = vi;
+        for (uint32_t t = 0; t < nd.cap; t++) {
+            const double st = __shfl_sync(0xffffffffu, si, t);
+            const uint32_t ct = __shfl_sync(0xffffffffu, ci, t);
+            const uint64_t kt = __shfl_sync(0xffffffffu, ki, t);
+            if (win && ct == ci && t != (uint32_t)lane && (st > si || (st == si && kt < ki))) win = false;
         }
-        const bool emit = wi && rank < n_kept;
-        for (uint32_t q = 0; q < outdeg; q++) {      // uniform trip count across the warp
-            uint32_t r = 0;
-            int32_t w = 0;
-            uint8_t st = RQ_INVALID;
-            if (emit) {
-                const uint32_t a = P.out_list[nd.out_b + q];
-                r = nd.req_base + rank * outdeg + q;
-                w = P.arc_word[a];
-                P.rq_c[r] = ai.ctx;
-                P.rq_w[r] = w;
-                P.rq_arc[r] = a;
-                P.rq_parent[r] = nd.slot_base + i;
-                P.rq_score[r] = ai.score;
-                P.rq_dslot[r] = P.arc_slot[a] + rank;
-                P.rq_m[r] = OTF_UNSET;
-                st = RQ_NOCACHE;
-                uint32_t cslot = OTF_UNSET;
-                if (S.enabled) cslot = cache_probe(S, nd.stream, ai.ctx, w, r, &st);
-                P.rq_cslot[r] = cslot;
-                P.rq_state[r] = st;
-            }
-            compact_primary(P, S, lc, emit && (st == RQ_PENDING || st == RQ_NOCACHE), r,
-                            emit ? ai.ctx : 0u, w, nd.stream);
+        const unsigned wb = __ballot_sync(0xffffffffu, win);
+        uint32_t rank = 0;
+        for (uint32_t t = 0; t < nd.cap; t++) {
+            const double st = __shfl_sync(0xffffffffu, si, t);
+            const uint32_t ct = __shfl_sync(0xffffffffu, ci, t);
+            if (win && ((wb >> t) & 1u) && (st > si || (st == si && ct < ci))) rank++;
         }
+        n_kept = (uint32_t)min((long long)__popc(wb), beam);
+        if (win && rank < n_kept) {
+            s_ctx[wib][rank] = ci;
+            s_score[wib][rank] = si;
+            s_slot[wib][rank] = nd.slot_base + lane;
+        }
+    } else {
+        // general path: O(cap^2) sweeps through the slot_win scratch
+        recombine_node(P.arr, P.slot_win, nd.slot_base, nd.cap, lane);
+        uint32_t n_win = 0;
+        for (uint32_t i0 = 0; i0 < nd.cap; i0 += 32) {
+            uint32_t i = i0 + lane;
+            n_win += __popc(__ballot_sync(0xffffffffu, i < nd.cap && P.slot_win[nd.slot_base + i]));
+        }
+        n_kept = (uint32_t)min((long long)n_win, beam);
+    }
+    __syncwarp();
+    const bool fast = nd.cap <= 32;   // token table by rank is in shared memory
+    // one lane per (rank, arc) request; the trip count is uniform per warp
+    for (uint32_t j0 = 0; j0 < n_kept * outdeg; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const bool emit = j < n_kept * outdeg;
+        uint32_t r = 0, c = 0, s_tok = 0;
+        int32_t w = 0;
+        double sc = 0.0;
+        uint8_t st = RQ_INVALID;
+        if (emit) {
+            const uint32_t rank = j / outdeg, q = j - rank * outdeg;
+            if (fast) {
+                c = s_ctx[wib][rank]; sc = s_score[wib][rank]; s_tok = s_slot[wib][rank];
+            } else {
+                // find the token of this rank among the winners (general path)
+                for (uint32_t i = 0; i < nd.cap; i++) {
+                    if (!P.slot_win[nd.slot_base + i]) continue;
+                    const Arrival ai = P.arr[nd.slot_base + i];
+                    uint32_t rk = 0;
+                    for (uint32_t t = 0; t < nd.cap; t++) {
+                        if (!P.slot_win[nd.slot_base + t]) continue;
+                        const Arrival at = P.arr[nd.slot_base + t];
+                        if (at.score > ai.score || (at.score == ai.score && at.ctx < ai.ctx)) rk++;
+                    }
+                    if (rk == rank) { c = ai.ctx; sc = ai.score; s_tok = nd.slot_base + i; break; }
+                }
+            }
+            const uint32_t a = (outdeg <= 32) ? s_arc[wib][q] : P.out_list[nd.out_b + q];
+            r = nd.req_base + j;
+            w = P.arc_word[a];
+            st = RQ_NOCACHE;
+            uint32_t cslot = OTF_UNSET;
+            if (S.enabled) cslot = cache_probe(S, nd.stream, c, w, r, &st);
+            // small-LM score of the same transition from the context's
+            // stored history (decoder.py:99-100), independent of the model
+            const uint32_t crow = S.ctx_row[(uint64_t)nd.stream * (S.max_ctx + 1) + c];
+            const uint32_t *meta = S.arena_meta + (size_t)crow * OTF_META;
+            double ps;
+            if (!ngram_logprob_dev(g, meta + 1, (int)meta[0], w, &ps)) { atomicOr(S.err, OTF_E_KEY); ps = 0.0; }
+            P.rq_c[r] = c;
+            P.rq_w[r] = w;
+            P.rq_arc[r] = a;
+            P.rq_parent[r] = s_tok;
+            P.rq_score[r] = __dadd_rn(sc, P.arc_ac[a]);
+            P.rq_slm[r] = P.arc_slm[a];
+            P.rq_ps[r] = ps;
+            P.rq_dslot[r] = P.arc_slot[a] + rank;
+            P.rq_m[r] = OTF_UNSET;
+            P.rq_cslot[r] = cslot;
+            P.rq_state[r] = st;
+        }
+        compact_primary(P, S, lc, emit && (st == RQ_PENDING || st == RQ_NOCACHE), r, c, w, nd.stream);
     }
     for (uint32_t r = n_kept * outdeg + lane; r < nd.keep * outdeg; r += 32)
         P.rq_state[nd.req_base + r] = RQ_INVALID;
@@ -281,58 +386,6 @@ __global__ void __launch_bounds__(256) k_hs_prim(DevModel m, DevPlan P, DevStrea
 // --------------------------------------------------------------------------
 // stage 3: per-stream ordered resolution + finish
 // --------------------------------------------------------------------------
-__device__ __forceinline__ bool ng_get(const uint64_t *tag, const int32_t *words, const double *val,
-                                       uint32_t cap, int width, const int32_t *key, int len,
-                                       double *out) {
-    const uint64_t h = otf_tuple_hash(key, len);
-    uint32_t s = (uint32_t)(h >> 7) & (cap - 1);
-    for (uint32_t probes = 0; probes <= cap; probes++) {
-        uint64_t t = tag[s];
-        if (t == 0) return false;
-        if (t == h) {
-            const int32_t *wk = words + (size_t)s * width;
-            if (wk[0] == len) {
-                bool eq = true;
-                for (int i = 0; i < len; i++) eq &= wk[1 + i] == key[i];
-                if (eq) { *out = val[s]; return true; }
-            }
-        }
-        s = (s + 1) & (cap - 1);
-    }
-    return false;
-}
-
-// ngram_logprob(small_context(history), w) (ngram.py:161-179, decoder.py:73-80)
-__device__ __forceinline__ bool ngram_logprob_dev(const DevNgram &g, const uint32_t *hist, int L,
-                                                  int w, double *out) {
-    int32_t ctx[OTF_MAX_ORDER + 1];
-    const int need = g.order - 1;
-    int n = 0;
-    for (int i = L; i < need; i++) ctx[n++] = g.bos;
-    for (int i = 0; i < L; i++) ctx[n++] = (int32_t)hist[i];
-    int keep = g.order > 1 ? g.order - 1 : 0;
-    if (keep > n) keep = n;
-    const int32_t *c = ctx + (n - keep);
-    int32_t buf[OTF_MAX_ORDER + 1];
-    const int width = g.order + 1;
-    for (int depth = 0; depth <= keep; depth++) {
-        int sl = keep - depth;
-        for (int i = 0; i < sl; i++) buf[i] = c[depth + i];
-        buf[sl] = w;
-        double v;
-        if (ng_get(g.p_tag, g.p_words, g.p_val, g.p_cap, width, buf, sl + 1, &v)) {
-            for (int sh = depth - 1; sh >= 0; sh--) {
-                double b;
-                if (!ng_get(g.b_tag, g.b_words, g.b_val, g.b_cap, width, c + sh, keep - sh, &b)) b = 0.0;
-                v = __dadd_rn(b, v);
-            }
-            *out = v;
-            return true;
-        }
-    }
-    return false;
-}
-
 __device__ __forceinline__ bool rows_equal_lane(const DevStreams &S, uint32_t ra, uint32_t rb) {
     const float *a = S.arena_h + (size_t)ra * S.H, *b = S.arena_h + (size_t)rb * S.H;
     for (int i = 0; i < S.H; i++)
@@ -344,25 +397,31 @@ __device__ __forceinline__ bool rows_equal_lane(const DevStreams &S, uint32_t ra
 
 // MODE 0: decode (finish requests into arrival slots)
 // MODE 1: Table-1 batch API (write p / c' / hit per request)
+// One CTA per (level, stream) range, one thread per request (chunks of
+// ASSIGN_T): the reference order is the thread order, so the ordered steps
+// (cache claim = first occurrence, len+1 numbering of new contexts, dedup of
+// equal contexts created in the same level) are block-wide scans.
+constexpr int ASSIGN_T = 128;
 template <int MODE>
-__global__ void __launch_bounds__(256) k_assign(DevPlan P, DevStreams S, DevNgram g, uint32_t lvl,
-                                                uint32_t range_begin, uint32_t n_ranges, double lm_weight,
-                                                double *out_p, uint32_t *out_cn, uint8_t *out_hit) {
-    const uint32_t wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
+__global__ void __launch_bounds__(ASSIGN_T) k_assign(DevPlan P, DevStreams S, uint32_t lvl, uint32_t range_begin,
+                                                     double lm_weight, double *out_p, uint32_t *out_cn,
+                                                     uint8_t *out_hit) {
+    __shared__ unsigned long long s_key[ASSIGN_T];
+    __shared__ uint32_t s_row[ASSIGN_T], s_cn[ASSIGN_T], s_wsum[ASSIGN_T / 32];
+    __shared__ uint32_t s_cnt[4];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const LevelCtr lc = P.lvl[lvl];
-    if (MODE == 1 && wid == 0 && lane == 0) *S.arena_used = lc.base + lc.n_prim;
-    if (wid >= n_ranges) return;
+    if (MODE == 1 && blockIdx.x == 0 && tid == 0) *S.arena_used = lc.base + lc.n_prim;
     if ((uint64_t)lc.base + lc.n_prim > S.arena_rows) return;   // flagged by stage 2
-    const StreamRange rg = P.ranges[range_begin + wid];
+    const StreamRange rg = P.ranges[range_begin + blockIdx.x];
     const uint32_t s = rg.stream;
     const uint64_t kb = (uint64_t)s * S.kc_cap, cb = (uint64_t)s * S.ct_cap;
     const uint32_t cmask = S.ct_cap - 1;
     uint32_t tlen = S.table_len[s];
-    unsigned long long n_look = 0, n_hit = 0, n_miss = 0, n_ins = 0;
+    if (tid < 4) s_cnt[tid] = 0;
     bool full = false;
-    for (uint32_t r0 = rg.rb; r0 < rg.re; r0 += 32) {
-        const uint32_t r = r0 + lane;
+    for (uint32_t r0 = rg.rb; r0 < rg.re; r0 += ASSIGN_T) {
+        const uint32_t r = r0 + tid;
         const bool in = r < rg.re;
         const uint8_t st = in ? P.rq_state[r] : (uint8_t)RQ_INVALID;
         const bool valid = st != RQ_INVALID;
@@ -370,13 +429,12 @@ __global__ void __launch_bounds__(256) k_assign(DevPlan P, DevStreams S, DevNgra
         bool prim = st == RQ_NOCACHE;
         if (st == RQ_PENDING) prim = S.kc_claim[kb + cslot] == r;
         const uint32_t m = prim ? P.rq_m[r] : OTF_UNSET;
-        // --- successor context of primaries: dedup + ordered numbering ---
         unsigned long long key = 0;
         uint32_t row = 0, cn = OTF_UNSET;
         if (prim) {
             key = otf_hash64(P.pr_dig[m]) | 1ull;
             row = lc.base + m;
-            uint32_t slot = (uint32_t)(key >> 20) & cmask;   // entries from earlier levels / chunks
+            uint32_t slot = (uint32_t)(key >> 20) & cmask;   // contexts of earlier levels / chunks
             for (uint32_t probes = 0; probes <= S.ct_cap; probes++) {
                 const unsigned long long k = S.ct_key[cb + slot];
                 if (k == 0ull) break;
@@ -384,24 +442,30 @@ __global__ void __launch_bounds__(256) k_assign(DevPlan P, DevStreams S, DevNgra
                 slot = (slot + 1) & cmask;
             }
         }
-        // duplicates inside this chunk: the earliest lane with equal content
         const bool novel = prim && cn == OTF_UNSET;
+        s_key[tid] = novel ? key : 0ull;
+        s_row[tid] = row;
+        __syncthreads();
+        // equal contexts created by earlier requests of this chunk
         int dup_of = -1;
-        const unsigned nov_bal = __ballot_sync(0xffffffffu, novel);
-        if (nov_bal & (nov_bal - 1)) {          // at least two novel lanes: compare digests
-            for (int t = 0; t < 32; t++) {
-                const unsigned long long kt = __shfl_sync(0xffffffffu, key, t);
-                const uint32_t rowt = __shfl_sync(0xffffffffu, row, t);
-                if (novel && dup_of < 0 && t < lane && ((nov_bal >> t) & 1u) && kt == key) {
-                    if (rows_equal_lane(S, rowt, row)) dup_of = t;
-                    else atomicOr(S.err, OTF_E_HASH);
+        if (novel)
+            for (int t = 0; t < tid; t++)
+                if (s_key[t] == key) {
+                    if (rows_equal_lane(S, s_row[t], row)) { dup_of = t; break; }
+                    atomicOr(S.err, OTF_E_HASH);
                 }
-            }
-        }
         const bool first = novel && dup_of < 0;
+        // block-wide exclusive scan of `first` in thread (= request) order
         const unsigned fb = __ballot_sync(0xffffffffu, first);
+        if (lane == 0) s_wsum[wid] = __popc(fb);
+        __syncthreads();
+        uint32_t before = __popc(fb & ((1u << lane) - 1u)), total = 0;
+        for (int w2 = 0; w2 < ASSIGN_T / 32; w2++) {
+            if (w2 < wid) before += s_wsum[w2];
+            total += s_wsum[w2];
+        }
         if (first) {
-            const uint32_t idx = tlen + __popc(fb & ((1u << lane) - 1u)) + 1u;   // len + 1 (context_table.py:83-86)
+            const uint32_t idx = tlen + before + 1u;            // len + 1 (context_table.py:83-86)
             if (idx > S.max_ctx) {
                 full = true;
             } else {
@@ -414,51 +478,49 @@ __global__ void __launch_bounds__(256) k_assign(DevPlan P, DevStreams S, DevNgra
                 S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + idx] = row;
             }
         }
-        tlen += __popc(fb);
-        const uint32_t dup_cn = __shfl_sync(0xffffffffu, cn, dup_of < 0 ? lane : dup_of);
-        if (dup_of >= 0) cn = dup_cn;
-        // cache fill by the claim winner, then the value for every request
+        tlen += total;
+        s_cn[tid] = cn;
+        __syncthreads();
+        if (dup_of >= 0) cn = s_cn[dup_of];
         double p = 0.0;
         if (prim) {
             p = P.pr_p[m];
             if (st == RQ_PENDING) { S.kc_p[kb + cslot] = p; S.kc_cnext[kb + cslot] = cn; }
         }
-        __syncwarp();
+        __syncthreads();
         if (valid && !prim) {   // hit: earlier level, or an earlier request of this level
             p = S.kc_p[kb + cslot];
-            cn = S.kc_cnext[kb + cslot];
+            cn = ld_volatile_u32(&S.kc_cnext[kb + cslot]);
         }
-        n_look += __popc(__ballot_sync(0xffffffffu, valid));
-        n_miss += __popc(__ballot_sync(0xffffffffu, prim));
-        n_hit += __popc(__ballot_sync(0xffffffffu, valid && !prim));
-        if (S.enabled) n_ins += __popc(__ballot_sync(0xffffffffu, prim));
-        if (!valid) continue;
-        if (MODE == 1) {
-            out_p[r] = p; out_cn[r] = cn; out_hit[r] = prim ? 0 : 1;
-            continue;
+        {
+            const unsigned bv = __ballot_sync(0xffffffffu, valid), bp = __ballot_sync(0xffffffffu, prim);
+            if (lane == 0) {
+                atomicAdd(&s_cnt[0], __popc(bv));
+                atomicAdd(&s_cnt[1], __popc(bp));
+            }
         }
-        // --- finish: small-LM delta, score, arrival ---
-        const uint32_t c = P.rq_c[r];
-        const int w = P.rq_w[r];
-        const uint32_t crow = S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + c];
-        const uint32_t *meta = S.arena_meta + (size_t)crow * OTF_META;
-        double ps;
-        if (!ngram_logprob_dev(g, meta + 1, (int)meta[0], w, &ps)) { atomicOr(S.err, OTF_E_KEY); ps = 0.0; }
-        const float delta = __double2float_rn(__dsub_rn(p, ps));    // codec.py:57-59
-        const uint32_t a = P.rq_arc[r];
-        // decoder.py:144: (score + acoustic) + lm_weight * (smalllm + delta)
-        const double ns = __dadd_rn(__dadd_rn(P.rq_score[r], P.arc_ac[a]),
-                                    __dmul_rn(lm_weight, __dadd_rn(P.arc_slm[a], (double)delta)));
-        Arrival out;
-        out.score = ns; out.ctx = cn; out.parent = P.rq_parent[r]; out.arc = a;
-        out.lvl = lvl; out.ridx = r; out.pad = 0;
-        P.arr[P.rq_dslot[r]] = out;
+        if (valid) {
+            if (MODE == 1) {
+                out_p[r] = p; out_cn[r] = cn; out_hit[r] = prim ? 0 : 1;
+            } else {
+                // delta rounded to f32 (codec.py:57-59); score (decoder.py:144)
+                const float delta = __double2float_rn(__dsub_rn(p, P.rq_ps[r]));
+                const double ns = __dadd_rn(P.rq_score[r], __dmul_rn(lm_weight, __dadd_rn(P.rq_slm[r], (double)delta)));
+                Arrival out;
+                out.score = ns; out.ctx = cn; out.parent = P.rq_parent[r]; out.arc = P.rq_arc[r];
+                out.lvl = lvl; out.ridx = r; out.pad = 0;
+                P.arr[P.rq_dslot[r]] = out;
+            }
+        }
+        __syncthreads();
     }
-    if (lane == 0) {
-        if (full) atomicOr(S.err, OTF_E_TABLE_FULL);
-        S.table_len[s] = full ? S.max_ctx : tlen;
+    if (full) atomicOr(S.err, OTF_E_TABLE_FULL);
+    if (tid == 0) {
+        S.table_len[s] = tlen > S.max_ctx ? S.max_ctx : tlen;
         unsigned long long *stt = S.stats + (size_t)s * 8;
-        stt[0] += n_look; stt[1] += n_hit; stt[2] += n_miss; stt[6] += n_ins; stt[7] += n_look;
+        const unsigned long long look = s_cnt[0], miss = s_cnt[1];
+        stt[0] += look; stt[1] += look - miss; stt[2] += miss; stt[7] += look;
+        if (S.enabled) stt[6] += miss;
     }
 }
 
