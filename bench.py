@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--frames", type=int, default=300)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-queries", action="store_true", help="skip the config-d query microbench")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     return ap.parse_args()
 
@@ -104,6 +105,59 @@ def peaks():
         return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), \
             "MEASURED_PEAKS.json"
     return 6650.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+def query_microbench(precision: str, n_queries: int = 1 << 20, n_ctx: int = 1 << 18, reps: int = 5):
+    """Config (d): isolated LM queries -- n (history, word) pairs through the
+    HS + MaxEnt kernel and the recurrent update, inputs resident in HBM, L2
+    flushed before every timed launch.  Algorithmic HS bytes per query:
+    P(4H + 4k + 8) + 4H + 16."""
+    import torch
+    from paper_2007_11794_b200 import kernels, synth
+    from paper_2007_11794_b200.device import DeviceModel
+    from paper_2007_11794_b200.model import build_huffman_from_counts
+    cfg = synth.CONFIGS["d"]
+    V, H, bits = cfg["V"], cfg["H"], cfg["bits"]
+    model = synth.synth_model(V, H, bits)
+    tree = build_huffman_from_counts(synth.zipf_counts(V))
+    dm = DeviceModel(model, tree)
+    words, hidden, hist, hlen, ctx = synth.query_set(model, n_queries, n_ctx)
+    d = lambda x: torch.from_numpy(x).cuda()
+    tw, th, thist, thl, tctx = d(words), d(hidden), d(hist), d(hlen), d(ctx)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    out = torch.empty(n_queries, dtype=torch.float64, device="cuda")
+    hout = torch.empty((n_queries, H), dtype=torch.float32, device="cuda")
+
+    def timed(fn):
+        fn()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return float(np.median(ts))
+
+    hs_ms = timed(lambda: kernels.word_logprob_batch(dm, tctx, th, thist, thl, tw))
+    adv_ms = timed(lambda: kernels.advance_hidden_batch(dm, tctx, th, tw, precision, out=hout))
+    P = (tree.path_offsets[1:] - tree.path_offsets[:-1])[words]
+    k = np.minimum(hlen[ctx], model.maxent_order)
+    hs_bytes = float(np.sum(P * (4 * H + 4 * k + 8)) + n_queries * (4 * H + 16))
+    hbm, tc_peak, src = peaks()
+    gbs = hs_bytes / (hs_ms / 1e3) / 1e9
+    flops = 2.0 * H * H * n_queries
+    tfs = flops / (adv_ms / 1e3) / 1e12
+    return {"workload": f"config d: {n_queries} queries, {n_ctx} contexts, V={V} H={H} MaxEnt 2^{bits}, "
+                        "words ~ Zipf(1.05); L2 flushed before each launch",
+            "hs_ms": hs_ms, "hs_gbs": gbs, "hs_frac_of_hbm": gbs / hbm, "hs_bytes": hs_bytes,
+            "mean_path": float(P.mean()),
+            "advance_ms": adv_ms, "advance_tflops": tfs, "advance_frac_of_bf16_peak": tfs / tc_peak,
+            "advance_precision": precision,
+            "queries_per_s": n_queries / ((hs_ms + adv_ms) / 1e3), "peak_source": src}
 
 
 def cpu_baseline(setup, n_sample: int, threads: int):
@@ -289,6 +343,9 @@ def main():
                "one_best_agreement": f"{agree}/{n_sample}"}
 
     clocks = clk.summary()
+    extras = {}
+    if rank == 0 and not args.no_queries:
+        extras["config_d_queries"] = query_microbench(args.precision)
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -312,6 +369,7 @@ def main():
                 "ms_per_step": e2e},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
+        "extras": extras,
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu

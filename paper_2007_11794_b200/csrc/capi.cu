@@ -851,6 +851,7 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     p->h2d_bytes = g_upload_bytes;
     bool bad = p->mem.alloc(&d.arr, std::max<uint32_t>(p->n_slots, 1)) != cudaSuccess;
     bad |= p->mem.alloc(&d.slot_win, std::max<uint32_t>(p->n_slots, 1)) != cudaSuccess;
+    bad |= p->mem.alloc(&d.tok, std::max<uint32_t>(p->n_slots, 1)) != cudaSuccess;
     uint32_t max_path = std::max<uint32_t>(p->n_levels, 1);
     d.max_path = (int32_t)max_path;
     bad |= p->mem.alloc(&d.out_len, p->n_utt) != cudaSuccess;

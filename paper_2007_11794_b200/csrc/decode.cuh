@@ -42,6 +42,7 @@ struct DevPlan {
     const double *arc_ac, *arc_slm;
     Arrival *arr;
     uint8_t *slot_win;
+    uint4 *tok;                   // general path: kept token by (node slot base + rank)
     // per utterance
     uint32_t n_utt;
     const uint32_t *utt_start_slot, *utt_stream, *final_off, *finals;
@@ -270,7 +271,8 @@ __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, DevNgra
             s_slot[wib][rank] = nd.slot_base + lane;
         }
     } else {
-        // general path: O(cap^2) sweeps through the slot_win scratch
+        // general path: O(cap^2 / 32) sweeps through the slot_win scratch;
+        // kept tokens are written to P.tok by rank
         recombine_node(P.arr, P.slot_win, nd.slot_base, nd.cap, lane);
         uint32_t n_win = 0;
         for (uint32_t i0 = 0; i0 < nd.cap; i0 += 32) {
@@ -278,6 +280,31 @@ __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, DevNgra
             n_win += __popc(__ballot_sync(0xffffffffu, i < nd.cap && P.slot_win[nd.slot_base + i]));
         }
         n_kept = (uint32_t)min((long long)n_win, beam);
+        for (uint32_t i0 = 0; i0 < nd.cap; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const bool wi = i < nd.cap && P.slot_win[nd.slot_base + i];
+            Arrival ai;
+            if (wi) ai = P.arr[nd.slot_base + i];
+            uint32_t rank = 0;
+            for (uint32_t j0 = 0; j0 < nd.cap; j0 += 32) {
+                const uint32_t j = j0 + lane;
+                const bool wj = j < nd.cap && P.slot_win[nd.slot_base + j];
+                double sj = 0.0; uint32_t cj = 0;
+                if (wj) { const Arrival aj = P.arr[nd.slot_base + j]; sj = aj.score; cj = aj.ctx; }
+                const unsigned bal = __ballot_sync(0xffffffffu, wj);
+                const uint32_t lim = min(32u, nd.cap - j0);
+                for (uint32_t t = 0; t < lim; t++) {
+                    const double st = __shfl_sync(0xffffffffu, sj, t);
+                    const uint32_t ct = __shfl_sync(0xffffffffu, cj, t);
+                    if (wi && ((bal >> t) & 1u) && (st > ai.score || (st == ai.score && ct < ai.ctx))) rank++;
+                }
+            }
+            if (wi && rank < n_kept) {
+                const unsigned long long sb = (unsigned long long)__double_as_longlong(ai.score);
+                P.tok[nd.slot_base + rank] = make_uint4(ai.ctx, nd.slot_base + i, (uint32_t)sb, (uint32_t)(sb >> 32));
+            }
+        }
+        __threadfence_block();
     }
     __syncwarp();
     const bool fast = nd.cap <= 32;   // token table by rank is in shared memory
@@ -294,18 +321,9 @@ __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, DevNgra
             if (fast) {
                 c = s_ctx[wib][rank]; sc = s_score[wib][rank]; s_tok = s_slot[wib][rank];
             } else {
-                // find the token of this rank among the winners (general path)
-                for (uint32_t i = 0; i < nd.cap; i++) {
-                    if (!P.slot_win[nd.slot_base + i]) continue;
-                    const Arrival ai = P.arr[nd.slot_base + i];
-                    uint32_t rk = 0;
-                    for (uint32_t t = 0; t < nd.cap; t++) {
-                        if (!P.slot_win[nd.slot_base + t]) continue;
-                        const Arrival at = P.arr[nd.slot_base + t];
-                        if (at.score > ai.score || (at.score == ai.score && at.ctx < ai.ctx)) rk++;
-                    }
-                    if (rk == rank) { c = ai.ctx; sc = ai.score; s_tok = nd.slot_base + i; break; }
-                }
+                const uint4 tk = P.tok[nd.slot_base + rank];
+                c = tk.x; s_tok = tk.y;
+                sc = __longlong_as_double((long long)(((unsigned long long)tk.w << 32) | tk.z));
             }
             const uint32_t a = (outdeg <= 32) ? s_arc[wib][q] : P.out_list[nd.out_b + q];
             r = nd.req_base + j;

@@ -26,7 +26,7 @@
 namespace tc {
 
 constexpr int BM = 128;      // rows per CTA tile (UMMA_M)
-constexpr int KC_B = 64;     // bytes of K per row per pipeline stage
+constexpr int KC_B = 128;    // bytes of K per row per pipeline stage
 constexpr int NTHREADS = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -113,15 +113,19 @@ __device__ __forceinline__ uint32_t tile_off(int row, int c) {
 }
 
 // MODE: 1 = TF32X3, 2 = BF16, 3 = TF32.
-// Pipeline per K chunk k (S-stage ring):
-//   raw A rows (gathered, fp32) and B slices (pre-converted W) arrive by
-//   cp.async S-1 chunks ahead; the chunk's raw A is converted into the
-//   operand layout (tf32 round / hi-lo split / bf16) in shared memory; one
-//   thread issues the MMAs and commits them to the stage's mbarrier; the
-//   stage's operand buffers are refilled only after that barrier fires.
+// Warp-specialized S-stage ring (no block barrier inside the K loop):
+//   warp 0      producer: cp.async of the gathered fp32 A rows (raw) and the
+//               pre-converted W slice (B, operand layout) for chunk k, then
+//               cp.async.mbarrier.arrive on full_raw[s];
+//   warps 2..5  converters: raw A -> operand layout (tf32 round / hi-lo split
+//               / bf16), fence.proxy.async, arrive on full_op[s]; afterwards
+//               they are the epilogue (TMEM lane quadrant = warp % 4);
+//   warp 1      MMA issuer (one lane): tcgen05.mma for chunk k, commit to
+//               empty[s] (stage reusable) and finally to done.
 // Grid: (row tiles of 128, N tiles of bn columns).
+constexpr int WS_THREADS = 192;
 template <int MODE>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __launch_bounds__(WS_THREADS, 1)
 k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__ in_row,
              const int32_t *__restrict__ words, const float *__restrict__ h_base,
              float *__restrict__ out_base, uint32_t row_limit, int bn, int stages,
@@ -129,7 +133,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     constexpr bool BF = MODE == 2;
     constexpr bool X3 = MODE == 1;
     constexpr int ELT = BF ? 2 : 4;                   // operand bytes per element
-    constexpr int KE = KC_B / ELT;                     // K elements per stage (16 / 32)
+    constexpr int KE = KC_B / ELT;                     // K elements per stage
     constexpr int CH = KC_B / 16;                      // operand 16-byte chunks per row
     constexpr int RAW_ROW = KE * 4 + 16;               // raw fp32 row stride (+16 B pad)
     constexpr int RAW_CH = KE / 4;                     // raw 16-byte chunks per row
@@ -139,29 +143,37 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     if ((uint64_t)out0 + n > row_limit) return;     // arena overflow (flagged by the HS stage)
     const uint32_t q0 = blockIdx.x * BM;
     if (q0 >= n) return;
-    const int n0 = blockIdx.y * bn;                    // first output column of this CTA
+    const int n0 = blockIdx.y * bn;
     const int H = m.H;
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t raw_bytes = BM * RAW_ROW;
     const uint32_t a_bytes = BM * KC_B;
     const uint32_t b_bytes = (uint32_t)bn * KC_B;
     const uint32_t stage_bytes = raw_bytes + (X3 ? 2 : 1) * (a_bytes + b_bytes);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + stages * stage_bytes);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + stages);
+    uint64_t *full_raw = reinterpret_cast<uint64_t *>(smem + stages * stage_bytes);
+    uint64_t *full_op = full_raw + stages;
+    uint64_t *empty = full_op + stages;
+    uint64_t *done = empty + stages;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
     __shared__ int32_t s_row[BM], s_w[BM];
 
-    if (tid < BM) {
-        const uint32_t q = q0 + tid;
-        s_row[tid] = q < n ? in_row[q] : -1;
-        s_w[tid] = q < n ? (words ? words[q] : (int32_t)q) : 0;
+    for (int t = tid; t < BM; t += WS_THREADS) {
+        const uint32_t q = q0 + t;
+        s_row[t] = q < n ? in_row[q] : -1;
+        s_w[t] = q < n ? (words ? words[q] : (int32_t)q) : 0;
     }
     if (tid == 0) {
-        for (int st = 0; st < stages; st++) mbar_init(smem_u32(&bars[st]), 1);
+        for (int st = 0; st < stages; st++) {
+            mbar_init(smem_u32(&full_raw[st]), 32);
+            mbar_init(smem_u32(&full_op[st]), 128);
+            mbar_init(smem_u32(&empty[st]), 1);
+        }
+        mbar_init(smem_u32(done), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0) {
+    if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      :: "r"(smem_u32(tmem_slot)), "r"(tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -175,182 +187,176 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     const uint32_t sbo = CH * 128, lbo = 128;
     const int nsub = bn > 256 ? 2 : 1;
     const int nmma = bn / nsub;
-    const uint32_t idesc = make_idesc(BF ? 1 : 2, nmma);
     const bool vec_ok = (H & 3) == 0;
 
-    auto stage_ptr = [&](int st) { return smem + st * stage_bytes; };
-    auto issue_loads = [&](int k) {
-        uint8_t *base = stage_ptr(k % stages);
-        uint8_t *raw = base;
-        uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
-        const int k0 = k * KE;
-        // raw A: 128 rows x KE fp32 (gathered rows), row-major with padding
-        for (int idx = tid; idx < BM * RAW_CH; idx += NTHREADS) {
-            const int row = idx / RAW_CH, c = idx - row * RAW_CH;
-            const int src = s_row[row];
-            const int kk = k0 + c * 4;
-            const bool ok = src >= 0 && kk < H && vec_ok;
-            cp_async16(smem_u32(raw + row * RAW_ROW + c * 16),
-                       ok ? (const void *)(h_base + (size_t)src * H + kk) : (const void *)h_base, ok);
-            if (!vec_ok && src >= 0) {   // unaligned H: scalar fill (rare)
-                float *dst = reinterpret_cast<float *>(raw + row * RAW_ROW + c * 16);
-                for (int e = 0; e < 4; e++) dst[e] = kk + e < H ? h_base[(size_t)src * H + kk + e] : 0.f;
+    if (warp == 0) {
+        // ------------------------------ producer ------------------------------
+        for (int k = 0; k < NK; k++) {
+            const int st = k % stages;
+            if (k >= stages) mbar_wait(smem_u32(&empty[st]), (uint32_t)(((k / stages) - 1) & 1));
+            uint8_t *base = smem + st * stage_bytes;
+            uint8_t *raw = base;
+            uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
+            const int k0 = k * KE;
+            for (int idx = lane; idx < BM * RAW_CH; idx += 32) {
+                const int row = idx / RAW_CH, c = idx - row * RAW_CH;
+                const int src = s_row[row];
+                const int kk = k0 + c * 4;
+                const bool ok = src >= 0 && kk < H && vec_ok;
+                cp_async16(smem_u32(raw + row * RAW_ROW + c * 16),
+                           ok ? (const void *)(h_base + (size_t)src * H + kk) : (const void *)h_base, ok);
+                if (!vec_ok && src >= 0) {   // unaligned H: synchronous scalar fill (rare)
+                    float *dst = reinterpret_cast<float *>(raw + row * RAW_ROW + c * 16);
+                    for (int e = 0; e < 4; e++) dst[e] = kk + e < H ? h_base[(size_t)src * H + kk + e] : 0.f;
+                }
             }
-        }
-        // B: bn rows (W rows n0..n0+bn) x KC_B operand bytes, already converted
-        for (int idx = tid; idx < bn * CH; idx += NTHREADS) {
-            const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
-            const int row = g * 8 + r8;
-            const int wrow = n0 + row;
-            const int kk = k0 + c * (16 / ELT);
-            const bool ok = wrow < H && kk < H && vec_ok;
-            const uint32_t off = tile_off(row, c);
-            if (BF) {
-                cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_bf + (size_t)wrow * H + kk) : (const void *)m.W_bf, ok);
-            } else {
-                cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_hi + (size_t)wrow * H + kk) : (const void *)m.W_hi, ok);
-                if (X3)
-                    cp_async16(smem_u32(sB + b_bytes + off), ok ? (const void *)(m.W_lo + (size_t)wrow * H + kk) : (const void *)m.W_lo, ok);
-            }
-            if (!vec_ok && wrow < H) {
-                for (int e = 0; e < 16 / ELT; e++) {
-                    const bool in = kk + e < H;
-                    if (BF) reinterpret_cast<__nv_bfloat16 *>(sB + off)[e] = in ? m.W_bf[(size_t)wrow * H + kk + e] : __float2bfloat16(0.f);
-                    else {
-                        reinterpret_cast<float *>(sB + off)[e] = in ? m.W_hi[(size_t)wrow * H + kk + e] : 0.f;
-                        if (X3) reinterpret_cast<float *>(sB + b_bytes + off)[e] = in ? m.W_lo[(size_t)wrow * H + kk + e] : 0.f;
+            for (int idx = lane; idx < bn * CH; idx += 32) {
+                const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
+                const int row = g * 8 + r8;
+                const int wrow = n0 + row;
+                const int kk = k0 + c * (16 / ELT);
+                const bool ok = wrow < H && kk < H && vec_ok;
+                const uint32_t off = tile_off(row, c);
+                if (BF) {
+                    cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_bf + (size_t)wrow * H + kk) : (const void *)m.W_bf, ok);
+                } else {
+                    cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_hi + (size_t)wrow * H + kk) : (const void *)m.W_hi, ok);
+                    if (X3)
+                        cp_async16(smem_u32(sB + b_bytes + off), ok ? (const void *)(m.W_lo + (size_t)wrow * H + kk) : (const void *)m.W_lo, ok);
+                }
+                if (!vec_ok && wrow < H) {
+                    for (int e = 0; e < 16 / ELT; e++) {
+                        const bool in = kk + e < H;
+                        if (BF) reinterpret_cast<__nv_bfloat16 *>(sB + off)[e] = in ? m.W_bf[(size_t)wrow * H + kk + e] : __float2bfloat16(0.f);
+                        else {
+                            reinterpret_cast<float *>(sB + off)[e] = in ? m.W_hi[(size_t)wrow * H + kk + e] : 0.f;
+                            if (X3) reinterpret_cast<float *>(sB + b_bytes + off)[e] = in ? m.W_lo[(size_t)wrow * H + kk + e] : 0.f;
+                        }
                     }
                 }
             }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(smem_u32(&full_raw[st])) : "memory");
         }
-    };
-
-    // prologue: S-1 chunks in flight
-    for (int k = 0; k < stages - 1; k++) {
-        if (k < NK) issue_loads(k);
-        cp_async_commit();
-    }
-    for (int k = 0; k < NK; k++) {
-        const int st = k % stages;
-        uint8_t *base = stage_ptr(st);
-        uint8_t *raw = base;
-        uint8_t *sA = base + raw_bytes;
-        uint8_t *sA2 = sA + a_bytes;
-        uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
-        uint8_t *sB2 = sB + b_bytes;
-        // chunk k landed (S-2 newer groups may stay in flight)
-        // groups committed so far cover chunks 0..k+S-2: allow S-2 pending
-        switch (stages) {
-        case 2: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
-        case 3: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
-        default: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
-        }
-        __syncthreads();
-        // convert raw A -> operand layout
-        for (int idx = tid; idx < BM * CH; idx += NTHREADS) {
-            const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
-            const int row = g * 8 + r8;
-            const uint32_t off = tile_off(row, c);
-            if (BF) {
-                const float4 x0 = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 32);
-                const float4 x1 = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 32 + 16);
-                __nv_bfloat162 b0 = __floats2bfloat162_rn(x0.x, x0.y), b1 = __floats2bfloat162_rn(x0.z, x0.w);
-                __nv_bfloat162 b2 = __floats2bfloat162_rn(x1.x, x1.y), b3 = __floats2bfloat162_rn(x1.z, x1.w);
-                uint4 u;
-                u.x = *reinterpret_cast<uint32_t *>(&b0); u.y = *reinterpret_cast<uint32_t *>(&b1);
-                u.z = *reinterpret_cast<uint32_t *>(&b2); u.w = *reinterpret_cast<uint32_t *>(&b3);
-                *reinterpret_cast<uint4 *>(sA + off) = u;
-            } else {
-                const float4 x = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 16);
-                float4 hi;
-                hi.x = tf32_rn(x.x); hi.y = tf32_rn(x.y); hi.z = tf32_rn(x.z); hi.w = tf32_rn(x.w);
-                *reinterpret_cast<float4 *>(sA + off) = hi;
-                if (X3) {
-                    float4 lo;
-                    lo.x = tf32_rn(x.x - hi.x); lo.y = tf32_rn(x.y - hi.y);
-                    lo.z = tf32_rn(x.z - hi.z); lo.w = tf32_rn(x.w - hi.w);
-                    *reinterpret_cast<float4 *>(sA2 + off) = lo;
-                }
-            }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
-        if (tid == 0) {
+    } else if (warp == 1) {
+        // ------------------------------ MMA issuer ----------------------------
+        const uint32_t idesc = make_idesc(BF ? 1 : 2, nmma);
+        for (int k = 0; k < NK; k++) {
+            const int st = k % stages;
+            mbar_wait(smem_u32(&full_op[st]), (uint32_t)((k / stages) & 1));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (lane == 0) {
+                uint8_t *base = smem + st * stage_bytes;
+                uint8_t *sA = base + raw_bytes;
+                uint8_t *sA2 = sA + a_bytes;
+                uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
+                uint8_t *sB2 = sB + b_bytes;
 #pragma unroll
-            for (int ks = 0; ks < KC_B / 32; ks++) {          // 32 bytes of K per MMA
-                for (int hh = 0; hh < nsub; hh++) {
-                    const uint32_t d = tmem + (uint32_t)(hh * nmma);
-                    const uint32_t boff = (uint32_t)(hh * nmma / 8) * sbo + ks * 2 * lbo;
-                    const uint64_t a_hi = make_desc(smem_u32(sA) + ks * 2 * lbo, lbo, sbo);
-                    const uint64_t b_hi = make_desc(smem_u32(sB) + boff, lbo, sbo);
-                    const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
-                    mma<BF>(d, a_hi, b_hi, idesc, acc);
+                for (int ks = 0; ks < KC_B / 32; ks++) {
+                    for (int hh = 0; hh < nsub; hh++) {
+                        const uint32_t d = tmem + (uint32_t)(hh * nmma);
+                        const uint32_t boff = (uint32_t)(hh * nmma / 8) * sbo + ks * 2 * lbo;
+                        const uint64_t a_hi = make_desc(smem_u32(sA) + ks * 2 * lbo, lbo, sbo);
+                        const uint64_t b_hi = make_desc(smem_u32(sB) + boff, lbo, sbo);
+                        const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
+                        mma<BF>(d, a_hi, b_hi, idesc, acc);
+                        if (X3) {
+                            const uint64_t a_lo = make_desc(smem_u32(sA2) + ks * 2 * lbo, lbo, sbo);
+                            const uint64_t b_lo = make_desc(smem_u32(sB2) + boff, lbo, sbo);
+                            mma<false>(d, a_hi, b_lo, idesc, 1u);
+                            mma<false>(d, a_lo, b_hi, idesc, 1u);
+                        }
+                    }
+                }
+                commit(smem_u32(&empty[st]));
+                if (k == NK - 1) commit(smem_u32(done));
+            }
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------ converters ----------------------------
+        const int ct = tid - 64;                          // 0..127
+        for (int k = 0; k < NK; k++) {
+            const int st = k % stages;
+            mbar_wait(smem_u32(&full_raw[st]), (uint32_t)((k / stages) & 1));
+            uint8_t *base = smem + st * stage_bytes;
+            uint8_t *raw = base;
+            uint8_t *sA = base + raw_bytes;
+            uint8_t *sA2 = sA + a_bytes;
+            for (int idx = ct; idx < BM * CH; idx += 128) {
+                const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
+                const int row = g * 8 + r8;
+                const uint32_t off = tile_off(row, c);
+                if (BF) {
+                    const float4 x0 = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 32);
+                    const float4 x1 = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 32 + 16);
+                    __nv_bfloat162 b0 = __floats2bfloat162_rn(x0.x, x0.y), b1 = __floats2bfloat162_rn(x0.z, x0.w);
+                    __nv_bfloat162 b2 = __floats2bfloat162_rn(x1.x, x1.y), b3 = __floats2bfloat162_rn(x1.z, x1.w);
+                    uint4 u;
+                    u.x = *reinterpret_cast<uint32_t *>(&b0); u.y = *reinterpret_cast<uint32_t *>(&b1);
+                    u.z = *reinterpret_cast<uint32_t *>(&b2); u.w = *reinterpret_cast<uint32_t *>(&b3);
+                    *reinterpret_cast<uint4 *>(sA + off) = u;
+                } else {
+                    const float4 x = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 16);
+                    float4 hi;
+                    hi.x = tf32_rn(x.x); hi.y = tf32_rn(x.y); hi.z = tf32_rn(x.z); hi.w = tf32_rn(x.w);
+                    *reinterpret_cast<float4 *>(sA + off) = hi;
                     if (X3) {
-                        const uint64_t a_lo = make_desc(smem_u32(sA2) + ks * 2 * lbo, lbo, sbo);
-                        const uint64_t b_lo = make_desc(smem_u32(sB2) + boff, lbo, sbo);
-                        mma<false>(d, a_hi, b_lo, idesc, 1u);
-                        mma<false>(d, a_lo, b_hi, idesc, 1u);
+                        float4 lo;
+                        lo.x = tf32_rn(x.x - hi.x); lo.y = tf32_rn(x.y - hi.y);
+                        lo.z = tf32_rn(x.z - hi.z); lo.w = tf32_rn(x.w - hi.w);
+                        *reinterpret_cast<float4 *>(sA2 + off) = lo;
                     }
                 }
             }
-            commit(smem_u32(&bars[st]));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&full_op[st])) : "memory");
         }
-        // refill the stage used by chunk k-1 with chunk k+S-1 once MMA k-1 is done
-        const int kn = k + stages - 1;
-        if (kn < NK) {
-            if (k >= 1) mbar_wait(smem_u32(&bars[(k - 1) % stages]), (uint32_t)(((k - 1) / stages) & 1));
-            issue_loads(kn);
-        }
-        cp_async_commit();
-    }
-    {
-        const int kl = NK - 1;
-        mbar_wait(smem_u32(&bars[kl % stages]), (uint32_t)((kl / stages) & 1));
-    }
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
-    // ---- epilogue: TMEM lane = row = tid; columns n0 .. n0+bn ----
-    const int row = tid;
-    const uint32_t q = q0 + row;
-    const bool valid = q < n;
-    unsigned long long dig = 0ull;
-    const float *urow = m.U + (size_t)s_w[row] * H;
-    float *orow = out_base + (size_t)(out0 + q) * H;
-    for (int c0 = 0; c0 < bn; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-        const int gc = n0 + c0;
-        if (valid) {
-            if (vec_ok && gc + 32 <= H) {
+        // ------------------------------ epilogue ------------------------------
+        mbar_wait(smem_u32(done), 0u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int quad = warp & 3;                        // TMEM lanes 32*quad .. +31
+        const int row = quad * 32 + lane;
+        const uint32_t q = q0 + row;
+        const bool valid = q < n;
+        unsigned long long dig = 0ull;
+        const float *urow = m.U + (size_t)s_w[row] * H;
+        float *orow = out_base + (size_t)(out0 + q) * H;
+        for (int c0 = 0; c0 < bn; c0 += 32) {
+            float v[32];
+            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, v);
+            const int gc = n0 + c0;
+            if (valid) {
+                if (vec_ok && gc + 32 <= H) {
 #pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                    float4 u = __ldg(reinterpret_cast<const float4 *>(urow + gc + j));
-                    float4 o;
-                    o.x = 1.f / (1.f + expf(-(v[j] + u.x)));
-                    o.y = 1.f / (1.f + expf(-(v[j + 1] + u.y)));
-                    o.z = 1.f / (1.f + expf(-(v[j + 2] + u.z)));
-                    o.w = 1.f / (1.f + expf(-(v[j + 3] + u.w)));
-                    *reinterpret_cast<float4 *>(orow + gc + j) = o;
-                    dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o.x));
-                    dig += otf_hash64(((uint64_t)(gc + j + 1) << 32) ^ __float_as_uint(o.y));
-                    dig += otf_hash64(((uint64_t)(gc + j + 2) << 32) ^ __float_as_uint(o.z));
-                    dig += otf_hash64(((uint64_t)(gc + j + 3) << 32) ^ __float_as_uint(o.w));
-                }
-            } else {
-                for (int j = 0; j < 32; j++)
-                    if (gc + j < H) {
-                        const float o = 1.f / (1.f + expf(-(v[j] + urow[gc + j])));
-                        orow[gc + j] = o;
-                        dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o));
+                    for (int j = 0; j < 32; j += 4) {
+                        float4 u = __ldg(reinterpret_cast<const float4 *>(urow + gc + j));
+                        float4 o;
+                        o.x = 1.f / (1.f + expf(-(v[j] + u.x)));
+                        o.y = 1.f / (1.f + expf(-(v[j + 1] + u.y)));
+                        o.z = 1.f / (1.f + expf(-(v[j + 2] + u.z)));
+                        o.w = 1.f / (1.f + expf(-(v[j + 3] + u.w)));
+                        *reinterpret_cast<float4 *>(orow + gc + j) = o;
+                        dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o.x));
+                        dig += otf_hash64(((uint64_t)(gc + j + 1) << 32) ^ __float_as_uint(o.y));
+                        dig += otf_hash64(((uint64_t)(gc + j + 2) << 32) ^ __float_as_uint(o.z));
+                        dig += otf_hash64(((uint64_t)(gc + j + 3) << 32) ^ __float_as_uint(o.w));
                     }
+                } else {
+                    for (int j = 0; j < 32; j++)
+                        if (gc + j < H) {
+                            const float o = 1.f / (1.f + expf(-(v[j] + urow[gc + j])));
+                            orow[gc + j] = o;
+                            dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o));
+                        }
+                }
             }
         }
+        if (rs.dig && valid) atomicAdd(&rs.dig[q], dig);
     }
-    if (rs.dig && valid) atomicAdd(&rs.dig[q], dig);
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 0)
+    if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(tmem_cols));
 }
 
@@ -364,29 +370,30 @@ static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const 
     // N tile is issued as two MMAs, so pad to 32
     const int n_pad = H > 256 ? (H + 31) / 32 * 32 : (H + 15) / 16 * 16;
     if (n_pad > 512) return -1;
-    // split N across CTAs when there are too few row tiles to fill 148 SMs
+    // N tile per CTA: capped so that >= 2 pipeline stages fit in shared
+    // memory, halved while there are too few row tiles to fill 148 SMs; a
+    // partial last N tile is zero-filled (rows >= H) and masked on store
     const uint32_t m_tiles = (n_cap + tc::BM - 1) / tc::BM;
-    int bn = n_pad;
-    while (bn > 32 && (uint64_t)m_tiles * (n_pad / bn) < 148 && bn % 32 == 0 && (n_pad % (bn / 2)) == 0 &&
-           ((bn / 2) % 16) == 0)
-        bn /= 2;
+    int bn = std::min(n_pad, prec == 1 ? 128 : 256);
+    while (bn > 32 && (uint64_t)m_tiles * ((n_pad + bn - 1) / bn) < 148) bn /= 2;
+    bn = (bn + 15) / 16 * 16;
     uint32_t cols = 32;
     while ((int)cols < bn) cols <<= 1;
     const bool x3 = prec == 1;
-    const int ke = prec == 2 ? 32 : 16;
+    const int ke = prec == 2 ? tc::KC_B / 2 : tc::KC_B / 4;
     const uint32_t raw_bytes = tc::BM * (ke * 4 + 16);
     const uint32_t stage_bytes = raw_bytes + (x3 ? 2u : 1u) * (uint32_t)(tc::BM + bn) * tc::KC_B;
     const int nk = (H + ke - 1) / ke;
     int stages = (int)std::min<uint32_t>(4u, (200u * 1024u) / stage_bytes);
     stages = std::max(2, std::min(stages, std::max(nk, 2)));
-    const size_t smem = (size_t)stages * stage_bytes + stages * 8 + 16 + 1024;
-    const dim3 grid(m_tiles, n_pad / bn);
+    const size_t smem = (size_t)stages * stage_bytes + (3 * stages + 1) * 8 + 16 + 1024;
+    const dim3 grid(m_tiles, (n_pad + bn - 1) / bn);
     cudaError_t e;
 #define TC_LAUNCH(MODE)                                                                         \
     do {                                                                                        \
         e = cudaFuncSetAttribute(tc::k_advance_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (e != cudaSuccess) return -9;                                                        \
-        tc::k_advance_tc<MODE><<<grid, tc::NTHREADS, smem, s>>>(m, n_cap, rs, in_row, words, h_base, \
+        tc::k_advance_tc<MODE><<<grid, tc::WS_THREADS, smem, s>>>(m, n_cap, rs, in_row, words, h_base, \
                                                                  out_base, row_limit, bn, stages, cols); \
     } while (0)
     if (prec == 1) TC_LAUNCH(1);
