@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--n-utt", type=int, default=64)
     ap.add_argument("--frames", type=int, default=300)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--groups", type=int, default=4, help="concurrent level chains per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-queries", action="store_true", help="skip the config-d query microbench")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
@@ -237,8 +238,8 @@ def main():
     H = setup.model.hidden_size
     need = BatchDecoder.contexts_needed(setup.lattices, setup.beam)
     dec = BatchDecoder(setup.model, setup.tree, setup.small_lm, len(setup.lattices), need,
-                       precision=args.precision)
-    plan = dec.prepare(setup.lattices, setup.beam)
+                       precision=args.precision, n_groups=args.groups)
+    dec.prepare(setup.lattices, setup.beam)
     stream = torch.cuda.current_stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > L2
     use_graph = not args.no_graph
@@ -276,9 +277,8 @@ def main():
 
     # ---- per-kernel CUDA-event timing: one run replayed from a graph with
     # event-record nodes around every kernel (device-side spans) ----
-    dec.streams.reset(retain=False)
-    prof = plan.profile(dec.ngram, 1.0, args.precision)
-    cnt = plan.counters()
+    prof = dec.profile(1.0)
+    cnt = dec.counters()
     hbm, tc_peak, peak_src = peaks()
     # algorithmic bytes: HS per query P(4H + 4k + 8) + 4H + 16;
     # recurrent update per miss 3 x 4H (h_c read, U row read, h' write) and
@@ -357,6 +357,7 @@ def main():
                                "beam 8, per-utterance streams (retain=False)",
                    "n_utt_per_gpu": args.n_utt, "frames": args.frames, "beam": setup.beam,
                    "precision": args.precision, "cuda_graph": use_graph,
+                   "concurrent_groups": dec.n_groups,
                    "l2": "flushed (256 MB write) between timed iterations"},
         "rtf": (ms / 1e3) / (frames_per_step * FRAME_S) * (1 if world == 1 else 1),
         "rtf_per_stream": (ms / 1e3) / (args.frames * FRAME_S),

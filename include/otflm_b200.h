@@ -50,6 +50,7 @@ typedef struct OtflmModel OtflmModel;
 typedef struct OtflmNgram OtflmNgram;
 typedef struct OtflmStreams OtflmStreams;
 typedef struct OtflmPlan OtflmPlan;
+typedef struct OtflmGroup OtflmGroup;
 
 /* ---- model upload (replaces handing numpy arrays to otflm.kernels;
  *      RnnlmModel rnnlm.py:69-124 + HuffmanTree huffman.py:40-51) ------- */
@@ -203,6 +204,16 @@ int otflm_decode_profile(OtflmPlan *p, const OtflmNgram *g, double lm_weight, in
  * use_graph != 0 replays a captured CUDA graph of the level loop. */
 int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
                      int32_t use_graph, void *stream);
+/* Concurrent groups: plans over disjoint utterances get disjoint arena row
+ * partitions [start, end) and are replayed as parallel chains of one CUDA
+ * graph (the per-frame stages of different groups overlap on the GPU). */
+int otflm_plan_set_arena(OtflmPlan *p, uint32_t start, uint32_t end);
+int otflm_group_create(OtflmPlan **plans, int32_t n, OtflmGroup **out);
+int otflm_group_destroy(OtflmGroup *g);
+int otflm_group_run(OtflmGroup *g, const OtflmNgram *ng, double lm_weight, int32_t precision,
+                    void *stream);
+int otflm_group_profile(OtflmGroup *g, const OtflmNgram *ng, double lm_weight, int32_t precision,
+                        void *stream, double *ms_out, int64_t *n_out);
 /* Copy results of the last run to host (synchronizes). */
 int otflm_decode_fetch(OtflmPlan *p, OtflmDecodeResult *res, void *stream);
 /* End to end: plan_create + decode_run + decode_fetch + plan_destroy. */

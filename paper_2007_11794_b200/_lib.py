@@ -115,6 +115,11 @@ _SIGS = {
                                C.POINTER(DecodeResult), _P]),
     "otflm_plan_counters": (C.c_int, [_P, _P, _P]),
     "otflm_decode_profile": (C.c_int, [_P, _P, C.c_double, C.c_int32, _P, _P, _P]),
+    "otflm_plan_set_arena": (C.c_int, [_P, C.c_uint32, C.c_uint32]),
+    "otflm_group_create": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_void_p)]),
+    "otflm_group_destroy": (C.c_int, [_P]),
+    "otflm_group_run": (C.c_int, [_P, _P, C.c_double, C.c_int32, _P]),
+    "otflm_group_profile": (C.c_int, [_P, _P, C.c_double, C.c_int32, _P, _P, _P]),
     "otflm_last_launch_count": (C.c_int64, []),
     "otflm_error_string": (C.c_char_p, [C.c_int32]),
     "otflm_last_error_detail": (C.c_char_p, []),

@@ -356,7 +356,7 @@ extern "C" int otflm_advance_hidden_batch(const OtflmModel *m, int64_t n, const 
     if (n <= 0) return OTFLM_OK;
     if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
     if (!m->d.U || !m->d.W) { g_detail = "model has no recurrent weights"; return OTFLM_ERR_VALUE; }
-    const RowSpec rs{nullptr, nullptr, nullptr, nullptr, nullptr};
+    const RowSpec rs{nullptr, nullptr, nullptr, nullptr, nullptr, 0xFFFFFFFFu};
     return launch_advance(m->d, precision, (uint32_t)n, rs, ctx, w, h_in, h_out, 0xFFFFFFFFu, (cudaStream_t)stream);
 }
 
@@ -367,7 +367,7 @@ extern "C" int otflm_advance_hidden_rows(const OtflmModel *m, int64_t n, const f
     if (!m->d.W) { g_detail = "model has no recurrent weights"; return OTFLM_ERR_VALUE; }
     DevModel dm = m->d;
     dm.U = input_rows;   // row i is the input row of query i
-    const RowSpec rs{nullptr, nullptr, nullptr, nullptr, nullptr};
+    const RowSpec rs{nullptr, nullptr, nullptr, nullptr, nullptr, 0xFFFFFFFFu};
     return launch_advance(dm, precision, (uint32_t)n, rs, ctx, nullptr, h_in, h_out, 0xFFFFFFFFu, (cudaStream_t)stream);
 }
 
@@ -614,12 +614,15 @@ struct OtflmPlan {
     uint64_t h2d_bytes = 0;
     unsigned long long *alg_buf = nullptr;
     cudaStream_t side = nullptr;               // second branch of each level (HS)
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t chain = nullptr;              // this plan's chain inside a group graph
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_done = nullptr;
     std::vector<uint32_t> utt_stream_host;
     ~OtflmPlan() {
         if (side) cudaStreamDestroy(side);
+        if (chain) cudaStreamDestroy(chain);
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
+        if (ev_done) cudaEventDestroy(ev_done);
     }
 };
 
@@ -795,11 +798,16 @@ static int plan_alloc_workspace(OtflmPlan *p, uint32_t R, uint32_t n_lvl_slots) 
     bad |= p->mem.alloc(&d.pr_dig, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.lvl, n_lvl_slots) != cudaSuccess;
     bad |= p->mem.alloc(&p->alg_buf, 4) != cudaSuccess;
+    bad |= p->mem.alloc(&d.cursor, 1) != cudaSuccess;
     d.alg = nullptr;   // counters are only maintained in profiling runs
+    d.arena_start = OTF_UNSET;
+    d.arena_end = 0;
     if (bad) { g_detail = "cudaMalloc workspace"; return OTFLM_ERR_NOMEM; }
     if (cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&p->chain, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming) != cudaSuccess) {
         g_detail = "stream/event creation";
         return OTFLM_ERR_CUDA;
     }
@@ -909,7 +917,7 @@ static int enqueue_stage2(OtflmPlan *p, const DevModel &m, DevStreams &S, uint32
     }
     {
         ProfScope ps(K_ADVANCE, s);
-        int rc = launch_advance(m, prec, R, rs, d.pr_inrow, d.pr_w, S.arena_h, S.arena_h, S.arena_rows, s);
+        int rc = launch_advance(m, prec, R, rs, d.pr_inrow, d.pr_w, S.arena_h, S.arena_h, rs.row_limit, s);
         if (rc) return rc;
     }
     CK(cudaEventRecord(p->ev_join, p->side));
@@ -925,7 +933,7 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
     CK(cudaMemsetAsync(d.arr, 0xFF, (size_t)std::max<uint32_t>(p->n_slots, 1) * sizeof(Arrival), s));
     CK(cudaMemsetAsync(d.lvl, 0, (size_t)(p->n_levels + 1) * sizeof(LevelCtr), s));
     if (d.alg) CK(cudaMemsetAsync(d.alg, 0, 4 * sizeof(unsigned long long), s));
-    { ProfScope ps(K_MISC, s); k_run_begin<<<cdiv(std::max<uint32_t>(p->n_utt, S.S), 128), 128, 0, s>>>(d, S); CKL(); }
+    { ProfScope ps(K_MISC, s); k_run_begin<<<cdiv(p->n_utt, 128), 128, 0, s>>>(d, S); CKL(); }
     int prev = -1;
     for (uint32_t t = 0; t < p->n_levels; t++) {
         const uint32_t nb0 = p->lvl_node_off[t], nn = p->lvl_node_off[t + 1] - nb0;
@@ -935,7 +943,9 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
             continue;
         }
         { ProfScope ps(K_EXPAND, s); k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, g->d, nb0, nn, (long long)p->beam, t); CKL(); }
-        const RowSpec rs{&d.lvl[t].n_prim, &d.lvl[t], prev >= 0 ? &d.lvl[prev] : nullptr, S.arena_used, d.pr_dig};
+        const bool part = d.arena_start != OTF_UNSET;
+        const RowSpec rs{&d.lvl[t].n_prim, &d.lvl[t], prev >= 0 ? &d.lvl[prev] : nullptr,
+                         part ? d.cursor : S.arena_used, d.pr_dig, part ? d.arena_end : S.arena_rows};
         int rc = enqueue_stage2(p, m, S, R, prec, rs, s);
         if (rc) return rc;
         const uint32_t r0 = p->lvl_range_off[t], nr = p->lvl_range_off[t + 1] - r0;
@@ -1073,6 +1083,130 @@ extern "C" int otflm_decode(OtflmStreams *s, const OtflmNgram *g, const OtflmLat
 }
 
 // ==========================================================================
+// plan groups: several plans over disjoint utterances (and disjoint arena
+// partitions) captured as parallel dependency chains of one CUDA graph, so
+// the latency-bound level stages of different groups overlap on the GPU
+// ==========================================================================
+extern "C" int otflm_plan_set_arena(OtflmPlan *p, uint32_t start, uint32_t end) {
+    if (!p || end <= start || end > p->st->d.arena_rows || start == 0) return OTFLM_ERR_VALUE;
+    p->d.arena_start = start;
+    p->d.arena_end = end;
+    if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+    if (p->graph) { cudaGraphDestroy(p->graph); p->graph = nullptr; }
+    return OTFLM_OK;
+}
+
+struct OtflmGroup {
+    std::vector<OtflmPlan *> plans;
+    cudaGraphExec_t gexec = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaEvent_t ev0 = nullptr;
+    double g_lm = 0; int g_prec = -1; const OtflmNgram *g_ng = nullptr;
+    int64_t launches = 0;
+    ~OtflmGroup() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (graph) cudaGraphDestroy(graph);
+        if (ev0) cudaEventDestroy(ev0);
+    }
+};
+
+extern "C" int otflm_group_create(OtflmPlan **plans, int32_t n, OtflmGroup **out) {
+    if (!plans || n < 1 || !out) return OTFLM_ERR_VALUE;
+    OtflmGroup *g = new OtflmGroup();
+    for (int i = 0; i < n; i++) {
+        if (!plans[i] || plans[i]->st != plans[0]->st) { delete g; return OTFLM_ERR_VALUE; }
+        if (n > 1 && plans[i]->d.arena_start == OTF_UNSET) {
+            delete g; g_detail = "grouped plans need disjoint arena partitions"; return OTFLM_ERR_VALUE;
+        }
+        g->plans.push_back(plans[i]);
+    }
+    CK(cudaEventCreateWithFlags(&g->ev0, cudaEventDisableTiming));
+    *out = g;
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_group_destroy(OtflmGroup *g) {
+    delete g;
+    return OTFLM_OK;
+}
+
+static int enqueue_group(OtflmGroup *g, const OtflmNgram *ng, double lm, int prec, cudaStream_t cs) {
+    CK(cudaEventRecord(g->ev0, cs));
+    for (OtflmPlan *p : g->plans) {
+        CK(cudaStreamWaitEvent(p->chain, g->ev0, 0));
+        int rc = enqueue_run(p, ng, lm, prec, p->chain);
+        if (rc) return rc;
+        CK(cudaEventRecord(p->ev_done, p->chain));
+        CK(cudaStreamWaitEvent(cs, p->ev_done, 0));
+    }
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_group_run(OtflmGroup *g, const OtflmNgram *ng, double lm_weight, int32_t precision,
+                               void *stream) {
+    if (!g || !ng || precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!g->gexec || g->g_lm != lm_weight || g->g_prec != precision || g->g_ng != ng) {
+        if (g->gexec) { cudaGraphExecDestroy(g->gexec); g->gexec = nullptr; }
+        if (g->graph) { cudaGraphDestroy(g->graph); g->graph = nullptr; }
+        g_launches = 0;
+        cudaStream_t cs;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_group(g, ng, lm_weight, precision, cs);
+        cudaGraph_t graph;
+        cudaError_t e = cudaStreamEndCapture(cs, &graph);
+        cudaStreamDestroy(cs);
+        if (rc) return rc;
+        CK(e);
+        g->graph = graph;
+        CK(cudaGraphInstantiate(&g->gexec, graph, 0));
+        g->g_lm = lm_weight; g->g_prec = precision; g->g_ng = ng;
+        g->launches = g_launches;
+    }
+    g_last_launches = g->launches;
+    CK(cudaGraphLaunch(g->gexec, s));
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_group_profile(OtflmGroup *g, const OtflmNgram *ng, double lm_weight, int32_t precision,
+                                   void *stream, double *ms_out, int64_t *n_out) {
+    if (!g || !ng) return OTFLM_ERR_VALUE;
+    cudaStream_t s = (cudaStream_t)stream;
+    for (int i = 0; i < K_NCAT; i++) { g_prof_ms[i] = 0; g_prof_n[i] = 0; }
+    cudaStream_t cs;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    g_prof = true;
+    for (OtflmPlan *p : g->plans) p->d.alg = p->alg_buf;
+    int rc = enqueue_group(g, ng, lm_weight, precision, cs);
+    for (OtflmPlan *p : g->plans) p->d.alg = nullptr;
+    g_prof = false;
+    cudaGraph_t graph;
+    cudaError_t e = cudaStreamEndCapture(cs, &graph);
+    cudaStreamDestroy(cs);
+    if (rc) return rc;
+    CK(e);
+    cudaGraphExec_t ex;
+    CK(cudaGraphInstantiate(&ex, graph, 0));
+    CK(cudaGraphLaunch(ex, s));
+    CK(cudaStreamSynchronize(s));
+    for (auto &ev : g_prof_ev) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev.second.first, ev.second.second));
+        g_prof_ms[ev.first] += ms;
+        g_prof_n[ev.first] += 1;
+        cudaEventDestroy(ev.second.first);
+        cudaEventDestroy(ev.second.second);
+    }
+    g_prof_ev.clear();
+    cudaGraphExecDestroy(ex);
+    cudaGraphDestroy(graph);
+    for (int i = 0; i < K_NCAT; i++) { if (ms_out) ms_out[i] = g_prof_ms[i]; if (n_out) n_out[i] = g_prof_n[i]; }
+    return OTFLM_OK;
+}
+
+// ==========================================================================
 // rnnlm_prob_batch: Table-1 lookups in array order (cache.py:165-182)
 // ==========================================================================
 __global__ void k_probe_batch(DevPlan P, DevStreams S, uint32_t n, const uint32_t *c, const int32_t *w,
@@ -1148,7 +1282,7 @@ extern "C" int otflm_rnnlm_prob_batch(OtflmStreams *s, int64_t n, const int32_t 
     const uint32_t R = (uint32_t)n;
     k_probe_batch<<<cdiv(R, 256), 256, 0, st>>>(p->d, s->d, R, dc, dw, dsid);
     CKL();
-    const RowSpec rs{&p->d.lvl[0].n_prim, &p->d.lvl[0], nullptr, s->d.arena_used, p->d.pr_dig};
+    const RowSpec rs{&p->d.lvl[0].n_prim, &p->d.lvl[0], nullptr, s->d.arena_used, p->d.pr_dig, s->d.arena_rows};
     int rc = enqueue_stage2(p, m, s->d, R, precision, rs, st);
     if (rc) return rc;
     k_assign<1><<<(unsigned)ranges.size(), ASSIGN_T, 0, st>>>(p->d, s->d, 0, 0, 0.0, dp, dcn, dh);

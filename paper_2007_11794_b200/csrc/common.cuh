@@ -84,6 +84,7 @@ struct RowSpec {
     const LevelCtr *prev;           // previous active level or nullptr
     const uint32_t *base_dev;       // base when prev == nullptr (nullptr: 0)
     unsigned long long *dig;        // per-row content digest (nullptr: none)
+    uint32_t row_limit;             // rows >= row_limit are out of this plan's arena
 };
 __device__ __forceinline__ uint32_t row_base(const RowSpec &rs) {
     if (rs.prev) return rs.prev->base + rs.prev->n_prim;

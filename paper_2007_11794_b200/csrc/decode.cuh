@@ -65,6 +65,8 @@ struct DevPlan {
     double *out_combined, *out_acoustic, *out_lm;
     long long *out_end_ctx, *out_expansions;
     int32_t max_path;
+    uint32_t *cursor;             // arena cursor of a partitioned plan (concurrent groups)
+    uint32_t arena_start, arena_end;   // partition [start, end), or start == OTF_UNSET
     unsigned long long *alg;      // profiling only: [0] sum P, [1] sum P*k, [2] HS queries
 };
 
@@ -366,7 +368,7 @@ __global__ void __launch_bounds__(256) k_hs_prim(DevModel m, DevPlan P, DevStrea
     const uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (q == 0 && lane == 0) rs.cur->base = base;   // also written by the update kernel (same value)
-    if ((uint64_t)base + n > S.arena_rows) {
+    if ((uint64_t)base + n > rs.row_limit) {
         if (q == 0 && lane == 0) atomicOr(S.err, OTF_E_ARENA_FULL);
         return;
     }
@@ -430,7 +432,8 @@ __global__ void __launch_bounds__(ASSIGN_T) k_assign(DevPlan P, DevStreams S, ui
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const LevelCtr lc = P.lvl[lvl];
     if (MODE == 1 && blockIdx.x == 0 && tid == 0) *S.arena_used = lc.base + lc.n_prim;
-    if ((uint64_t)lc.base + lc.n_prim > S.arena_rows) return;   // flagged by stage 2
+    const uint32_t limit = P.arena_start == OTF_UNSET ? S.arena_rows : P.arena_end;
+    if ((uint64_t)lc.base + lc.n_prim > limit) return;   // flagged by stage 2
     const StreamRange rg = P.ranges[range_begin + blockIdx.x];
     const uint32_t s = rg.stream;
     const uint64_t kb = (uint64_t)s * S.kc_cap, cb = (uint64_t)s * S.ct_cap;
@@ -551,7 +554,8 @@ __global__ void k_final(DevPlan P, DevStreams S, double lm_weight, int last_lvl)
     const int lane = threadIdx.x & 31;
     if (u == 0 && lane == 0 && last_lvl >= 0) {   // arena rows in use after the run
         const uint32_t end = P.lvl[last_lvl].base + P.lvl[last_lvl].n_prim;
-        if (end <= S.arena_rows) *S.arena_used = end;
+        if (P.arena_start == OTF_UNSET) { if (end <= S.arena_rows) *S.arena_used = end; }
+        else *P.cursor = end;
     }
     if (u >= P.n_utt) return;
     bool have = false;
@@ -608,5 +612,6 @@ __global__ void k_run_begin(DevPlan P, DevStreams S) {
         a.score = 0.0; a.ctx = 0; a.parent = OTF_UNSET; a.arc = OTF_UNSET; a.lvl = 0; a.ridx = 0; a.pad = 0;
         P.arr[P.utt_start_slot[t]] = a;
     }
-    if (t < (uint32_t)S.S) S.stats[(size_t)t * 8 + 7] = 0;
+    if (t < P.n_utt) S.stats[(size_t)P.utt_stream[t] * 8 + 7] = 0;
+    if (t == 0 && P.arena_start != OTF_UNSET) *P.cursor = P.arena_start;
 }

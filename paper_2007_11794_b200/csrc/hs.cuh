@@ -242,7 +242,8 @@ __global__ void __launch_bounds__(256) k_advance_f64(DevModel m, uint32_t n_cap,
                                                      const int32_t *__restrict__ in_row,
                                                      const int32_t *__restrict__ words,
                                                      const float *__restrict__ h_base,
-                                                     float *__restrict__ out_base, uint32_t row_limit) {
+                                                     float *__restrict__ out_base, uint32_t row_limit_unused) {
+    const uint32_t row_limit = rs.row_limit;
     extern __shared__ float4 smem4[];
     float *hs = reinterpret_cast<float *>(smem4);
     __shared__ unsigned long long s_dig[QT];

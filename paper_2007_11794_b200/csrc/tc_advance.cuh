@@ -128,8 +128,9 @@ template <int MODE>
 __global__ void __launch_bounds__(WS_THREADS, 1)
 k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__ in_row,
              const int32_t *__restrict__ words, const float *__restrict__ h_base,
-             float *__restrict__ out_base, uint32_t row_limit, int bn, int stages,
+             float *__restrict__ out_base, uint32_t row_limit_unused, int bn, int stages,
              uint32_t tmem_cols) {
+    const uint32_t row_limit = rs.row_limit;
     constexpr bool BF = MODE == 2;
     constexpr bool X3 = MODE == 1;
     constexpr int ELT = BF ? 2 : 4;                   // operand bytes per element

@@ -230,6 +230,9 @@ class Plan:
         _lib.check(_lib.load().otflm_plan_info(self.handle, _p(out)), "plan info")
         return out
 
+    def set_arena(self, start: int, end: int) -> None:
+        _lib.check(_lib.load().otflm_plan_set_arena(self.handle, int(start), int(end)), "arena")
+
     def counters(self) -> dict:
         out = np.zeros(4, np.int64)
         _lib.check(_lib.load().otflm_plan_counters(self.handle, _p(out), current_stream_ptr()),
@@ -266,6 +269,32 @@ class Plan:
                                                   current_stream_ptr() if stream is None else stream),
                    "decode")
         return out
+
+
+class PlanGroup:
+    """Plans over disjoint utterance subsets replayed as parallel chains of
+    one CUDA graph; each plan owns an arena partition."""
+
+    def __init__(self, plans):
+        L = _lib.load()
+        self.plans = plans
+        arr = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
+        h = C.c_void_p()
+        _lib.check(L.otflm_group_create(arr, len(plans), C.byref(h)), "group")
+        self.handle = h
+        self._fin = weakref.finalize(self, L.otflm_group_destroy, h)
+
+    def run(self, ngram: DeviceNgram, lm_weight: float = 1.0, precision: str = "fp64") -> None:
+        _lib.check(_lib.load().otflm_group_run(self.handle, ngram.handle, float(lm_weight),
+                                               _lib.PREC[precision], current_stream_ptr()), "decode")
+
+    def profile(self, ngram: DeviceNgram, lm_weight: float = 1.0, precision: str = "fp64") -> dict:
+        ms = np.zeros(len(_lib.PROFILE_CATEGORIES))
+        n = np.zeros(len(_lib.PROFILE_CATEGORIES), np.int64)
+        _lib.check(_lib.load().otflm_group_profile(self.handle, ngram.handle, float(lm_weight),
+                                                   _lib.PREC[precision], current_stream_ptr(),
+                                                   _p(ms), _p(n)), "profile")
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(_lib.PROFILE_CATEGORIES)}
 
 
 def last_launch_count() -> int:

@@ -334,44 +334,92 @@ class BatchDecoder:
 
     ``prepare`` compiles and uploads the lattices (host->device), ``run``
     decodes with the inputs resident in HBM (replaying a CUDA graph of the
-    level loop), ``fetch`` copies the 1-best paths back.
+    level loop), ``fetch`` copies the 1-best paths back.  With ``n_groups``
+    > 1 the utterances are split into groups whose level loops run as
+    parallel chains of the same graph (each with its own arena partition).
     """
 
     def __init__(self, model, tree, small_lm, n_streams: int, max_contexts: int,
-                 enabled: bool = True, precision: str = "fp64"):
+                 enabled: bool = True, precision: str = "fp64", n_groups: int = 1):
         self.model, self.tree = model, tree
         self.dmodel = DeviceModel.get(model, tree)
         self.ngram = DeviceNgram.get(small_lm, self.dmodel)
         self.precision = precision
+        self.n_groups = max(1, min(int(n_groups), n_streams))
+        self.arena_rows = n_streams * max_contexts + 2
         self.streams = DeviceStreams(self.dmodel, n_streams, enabled=enabled,
                                      max_contexts=max_contexts,
                                      cache_slots=2 * max_contexts + 16,
-                                     arena_rows=n_streams * max_contexts + 2)
+                                     arena_rows=self.arena_rows)
+        self.plans = []
+        self.group = None
         self.plan = None
 
     @staticmethod
     def contexts_needed(lattices, beam: int) -> int:
         """Upper bound on new contexts per utterance: every request may
         create one (sum over nodes of min(beam, capacity) * out-degree)."""
+        from .lattice import as_lattice
         worst = 0
         for lat in lattices:
-            from .lattice import as_lattice
             l = as_lattice(lat)
             worst = max(worst, int(min(beam, 1 << 20)) * l.n_arcs)
         return worst + 1
 
-    def prepare(self, lattices, beam: int) -> Plan:
-        self.plan = Plan(self.streams, lattices, beam)
-        return self.plan
+    def prepare(self, lattices, beam: int):
+        lattices = list(lattices)
+        G = min(self.n_groups, len(lattices))
+        bounds = np.linspace(0, len(lattices), G + 1).astype(int)
+        self.plans = []
+        self.spans = []
+        rows = (self.arena_rows - 1) // G
+        for g in range(G):
+            ids = np.arange(bounds[g], bounds[g + 1])
+            p = Plan(self.streams, [lattices[i] for i in ids], beam, stream_ids=ids)
+            if G > 1:
+                p.set_arena(1 + g * rows, 1 + (g + 1) * rows)
+            self.plans.append(p)
+            self.spans.append(ids)
+        self.group = PlanGroup(self.plans) if G > 1 else None
+        self.plan = self.plans[0]
+        return self.plans
 
     def run(self, lm_weight: float = 1.0, use_graph: bool = True) -> None:
         self.streams.reset(retain=False)
-        self.plan.run(self.ngram, lm_weight, self.precision, use_graph=use_graph)
+        if self.group is not None:
+            self.group.run(self.ngram, lm_weight, self.precision)
+        else:
+            self.plan.run(self.ngram, lm_weight, self.precision, use_graph=use_graph)
+
+    def profile(self, lm_weight: float = 1.0) -> dict:
+        self.streams.reset(retain=False)
+        if self.group is not None:
+            return self.group.profile(self.ngram, lm_weight, self.precision)
+        return self.plan.profile(self.ngram, lm_weight, self.precision)
+
+    def counters(self) -> dict:
+        tot = {}
+        for p in self.plans:
+            for k, v in p.counters().items():
+                tot[k] = tot.get(k, 0) + v
+        return tot
 
     def fetch(self):
-        out = self.plan.fetch()
-        offs = self.plan.arrays["arc_off"]
-        return [_hyp(out, u, self.plan.lats[u], int(offs[u])) for u in range(self.plan.n_utt)], out
+        hyps, outs = [], []
+        for p in self.plans:
+            out = p.fetch()
+            offs = p.arrays["arc_off"]
+            hyps += [_hyp(out, u, p.lats[u], int(offs[u])) for u in range(p.n_utt)]
+            outs.append(out)
+        merged = {}
+        for k in outs[0]:
+            if k == "path_arcs":
+                w = max(o[k].shape[1] for o in outs)
+                merged[k] = np.concatenate([np.pad(o[k], ((0, 0), (0, w - o[k].shape[1])))
+                                            for o in outs])
+            else:
+                merged[k] = np.concatenate([o[k] for o in outs])
+        return hyps, merged
 
 
 def rescore_batch(lattices: Sequence, small_lm, model, tree, lm_weight: float = 1.0,

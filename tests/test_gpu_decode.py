@@ -167,14 +167,16 @@ def _paths(lat, limit=5000):
     return out
 
 
-def test_batch_decode_matches_oracle():
-    """Many utterances, one stream each (the bench path), vs the oracle."""
+@pytest.mark.parametrize("groups", [1, 3])
+def test_batch_decode_matches_oracle(groups):
+    """Many utterances, one stream each (the bench path), vs the oracle;
+    groups > 1 replays the utterance groups as parallel graph chains."""
     from paper_2007_11794_b200 import synth
     from paper_2007_11794_b200.rescore import BatchDecoder
     s = synth.build_setup("a", n_utt=12, T=60, seed=3)
     ref = O.decode_many(s.model, s.tree, s.small_lm, s.lattices, beam=s.beam, n_threads=4)
     need = BatchDecoder.contexts_needed(s.lattices, s.beam)
-    dec = BatchDecoder(s.model, s.tree, s.small_lm, len(s.lattices), need)
+    dec = BatchDecoder(s.model, s.tree, s.small_lm, len(s.lattices), need, n_groups=groups)
     dec.prepare(s.lattices, s.beam)
     for use_graph in (False, True, True):
         dec.run(1.0, use_graph=use_graph)
