@@ -310,6 +310,22 @@ extern "C" int otflm_word_logprob_batch(const OtflmModel *m, int64_t n, const in
     if (n <= 0) return OTFLM_OK;
     if (!m->d.NV || !m->d.ME || !m->d.path_off) { g_detail = "model has no output layer"; return OTFLM_ERR_VALUE; }
     cudaStream_t s = (cudaStream_t)stream;
+    if (m->d.H % 4 == 0 && m->d.H <= 1024) {
+        // TMA-fed ring: 4 warps per CTA, grid sized to the SMs' resident CTAs
+        const size_t smem = 4 * ring_bytes_per_warp(m->d.H);
+        int per_sm = 1;
+#define RING(CPL)                                                                                        \
+        do {                                                                                             \
+            CK(cudaFuncSetAttribute(k_word_logprob_ring<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_word_logprob_ring<CPL>, 128, smem)); \
+            const unsigned grid = (unsigned)std::min<int64_t>(cdiv(n, 4), (int64_t)148 * std::max(per_sm, 1)); \
+            k_word_logprob_ring<CPL><<<grid, 128, smem, s>>>(m->d, n, ctx, h, hist, hist_len, w, out);   \
+        } while (0)
+        if (m->d.H <= 128) RING(1); else if (m->d.H <= 256) RING(2); else if (m->d.H <= 512) RING(4); else RING(8);
+#undef RING
+        CKL();
+        return OTFLM_OK;
+    }
     const unsigned blocks = cdiv(n, 8);
 #define CALL(VEC, CPL) k_word_logprob_batch<VEC, CPL><<<blocks, 256, 0, s>>>(m->d, n, ctx, h, hist, hist_len, w, out)
     HS_DISPATCH(m->d.H, CALL);

@@ -156,6 +156,165 @@ __device__ __forceinline__ double hs_logprob_warp(const DevModel &m, const float
     return lp;
 }
 
+// --------------------------------------------------------------------------
+// HS v3: node rows streamed into a per-warp shared-memory ring by the TMA
+// bulk-copy engine (cp.async.bulk + mbarrier complete_tx), NS rows in flight
+// per warp without holding registers; lanes read the landed row with
+// conflict-free 16-byte shared loads.  Same arithmetic as hs_logprob_warp
+// (float64 accumulation, reduce8, reference node / MaxEnt order).
+// --------------------------------------------------------------------------
+#define HS_NS 8
+struct HsRing {
+    uint8_t *buf;            // HS_NS rows of 4H bytes
+    uint32_t bar0;           // shared address of HS_NS mbarriers (8 B apart)
+    uint32_t phase;          // bit s = parity to wait for on slot s
+};
+
+__device__ __forceinline__ void ring_issue(HsRing &r, int slot, const float *src, uint32_t bytes) {
+    const uint32_t bar = r.bar0 + slot * 8;
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(r.buf + (size_t)slot * bytes);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void ring_wait(HsRing &r, int slot) {
+    const uint32_t bar = r.bar0 + slot * 8;
+    const uint32_t par = (r.phase >> slot) & 1u;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAITR_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@P1 bra DONER_%=;\n\t"
+        "bra WAITR_%=;\n\t"
+        "DONER_%=:\n\t}" :: "r"(bar), "r"(par) : "memory");
+    r.phase ^= 1u << slot;
+}
+
+template <int CPL>
+__device__ __forceinline__ double hs_logprob_ring(const DevModel &m, HsRing &ring, const float *__restrict__ h,
+                                                  const uint32_t *__restrict__ hist, int L,
+                                                  const uint32_t *__restrict__ codes, uint32_t P, int lane) {
+    const int H = m.H;
+    const int NCH = H >> 2;
+    const uint32_t bytes = (uint32_t)H * 4u;
+    // first HS_NS rows in flight before anything else
+    if (lane == 0)
+        for (uint32_t p = 0; p < P && p < HS_NS; p++)
+            ring_issue(ring, (int)p, m.NV + (size_t)(__ldg(codes + p) & 0x7FFFFFFFu) * H, bytes);
+    double hv[CPL][4];
+#pragma unroll
+    for (int c = 0; c < CPL; c++) {
+        const int k = lane + 32 * c;
+        if (k < NCH) {
+            const float4 t = __ldg(reinterpret_cast<const float4 *>(h) + k);
+            hv[c][0] = widen(t.x); hv[c][1] = widen(t.y); hv[c][2] = widen(t.z); hv[c][3] = widen(t.w);
+        } else {
+            hv[c][0] = hv[c][1] = hv[c][2] = hv[c][3] = 0.0;
+        }
+    }
+    const int kmax = m.order < L ? m.order : L;
+    uint64_t pre[OTF_MAX_ORDER];
+#pragma unroll
+    for (int k = 0; k < OTF_MAX_ORDER; k++) {
+        pre[k] = 0;
+        if (k < kmax) {
+            uint64_t x = otf_mix(m.seed, (uint64_t)(k + 1));
+            for (int i = L - (k + 1); i < L; i++) x = otf_mix(x, (uint64_t)hist[i]);
+            pre[k] = x;
+        }
+    }
+    const int my_g = node_of_lane(lane);
+    const bool leader = (lane & 3) == 0;
+    double lp = 0.0;
+    for (uint32_t p0 = 0; p0 < P; p0 += HS_G) {
+        const uint32_t my_code = (p0 + my_g < P) ? __ldg(codes + p0 + my_g) : OTF_UNSET;
+        double me[OTF_MAX_ORDER];
+#pragma unroll
+        for (int k = 0; k < OTF_MAX_ORDER; k++) {
+            me[k] = 0.0;
+            if (leader && k < kmax && my_code != OTF_UNSET)
+                me[k] = (double)__ldg(m.ME + (otf_mix(pre[k], (uint64_t)(my_code & 0x7FFFFFFFu)) & m.mask));
+        }
+        double acc[HS_G];
+#pragma unroll
+        for (int g = 0; g < HS_G; g++) {
+            acc[g] = 0.0;
+            const uint32_t p = p0 + g;
+            if (p < P) {
+                const int slot = (int)(p % HS_NS);
+                ring_wait(ring, slot);
+                const float4 *row = reinterpret_cast<const float4 *>(ring.buf + (size_t)slot * bytes);
+#pragma unroll
+                for (int c = 0; c < CPL; c++) {
+                    const int k = lane + 32 * c;
+                    if (k < NCH) {
+                        const float4 t = row[k];
+                        acc[g] = fma(widen(t.x), hv[c][0], acc[g]);
+                        acc[g] = fma(widen(t.y), hv[c][1], acc[g]);
+                        acc[g] = fma(widen(t.z), hv[c][2], acc[g]);
+                        acc[g] = fma(widen(t.w), hv[c][3], acc[g]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0 && p + HS_NS < P)
+                    ring_issue(ring, slot, m.NV + (size_t)(__ldg(codes + p + HS_NS) & 0x7FFFFFFFu) * H, bytes);
+            }
+        }
+        double a = reduce8(acc, lane);
+#pragma unroll
+        for (int k = 0; k < OTF_MAX_ORDER; k++) if (k < kmax) a += me[k];
+        double mylog = 0.0;
+        if (leader && my_code != OTF_UNSET)
+            mylog = otf_log_sigmoid((my_code & 0x80000000u) ? -a : a);
+#pragma unroll
+        for (int g = 0; g < HS_G; g++) {
+            const double v = __shfl_sync(0xffffffffu, mylog, lane_of_node(g));
+            if (p0 + g < P) lp += v;
+        }
+    }
+    return lp;
+}
+
+// warp-ring setup: HS_NS row slots + barriers per warp in dynamic smem
+__device__ __forceinline__ HsRing ring_setup(uint8_t *smem, int warp_in_block, int H, int lane) {
+    const uint32_t bytes = (uint32_t)H * 4u;
+    HsRing r;
+    uint8_t *wbase = smem + (size_t)warp_in_block * (HS_NS * bytes + HS_NS * 8);
+    r.buf = wbase;
+    r.bar0 = (uint32_t)__cvta_generic_to_shared(wbase + HS_NS * bytes);
+    r.phase = 0;
+    if (lane < HS_NS)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(r.bar0 + lane * 8) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    return r;
+}
+__host__ __device__ constexpr size_t ring_bytes_per_warp(int H) { return (size_t)HS_NS * (4 * H + 8); }
+
+// batch API (config d): warps stride over queries, ring reused across queries
+template <int CPL>
+__global__ void __launch_bounds__(128) k_word_logprob_ring(DevModel m, int64_t n, const int32_t *__restrict__ ctx,
+                                                           const float *__restrict__ h,
+                                                           const int32_t *__restrict__ hist,
+                                                           const int32_t *__restrict__ hist_len,
+                                                           const int32_t *__restrict__ w,
+                                                           double *__restrict__ out) {
+    extern __shared__ __align__(128) uint8_t smem_ring[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    HsRing ring = ring_setup(smem_ring, wib, m.H, lane);
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib; q < n; q += nw) {
+        const int c = ctx[q];
+        uint32_t hw[OTF_MAX_ORDER];
+        const int L = hist_len[c];
+        for (int i = 0; i < L; i++) hw[i] = (uint32_t)hist[(int64_t)c * m.order + i];
+        const uint32_t o0 = __ldg(m.path_off + w[q]), o1 = __ldg(m.path_off + w[q] + 1);
+        const double lp = hs_logprob_ring<CPL>(m, ring, h + (int64_t)c * m.H, hw, L, m.path_code + o0, o1 - o0, lane);
+        if (lane == 0) out[q] = lp;
+    }
+}
+
 // dispatch on H: VEC=4 needs H % 4 == 0 (16-byte aligned rows)
 #define HS_DISPATCH(H, CALL)                                                   \
     do {                                                                       \

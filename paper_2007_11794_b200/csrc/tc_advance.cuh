@@ -114,23 +114,24 @@ __device__ __forceinline__ uint32_t tile_off(int row, int c) {
 
 // MODE: 1 = TF32X3, 2 = BF16, 3 = TF32.
 // Warp-specialized S-stage ring (no block barrier inside the K loop):
-//   warp 0      producer: cp.async of the gathered fp32 A rows (raw) and the
-//               pre-converted W slice (B, operand layout) for chunk k, then
-//               cp.async.mbarrier.arrive on full_raw[s];
-//   warps 2..5  converters: raw A -> operand layout (tf32 round / hi-lo split
-//               / bf16), fence.proxy.async, arrive on full_op[s]; afterwards
-//               they are the epilogue (TMEM lane quadrant = warp % 4);
-//   warp 1      MMA issuer (one lane): tcgen05.mma for chunk k, commit to
-//               empty[s] (stage reusable) and finally to done.
+//   warps 0..3  loaders/converters: each thread cp.asyncs its share of the
+//               gathered fp32 A rows (raw) and of the pre-converted W slice
+//               (B, operand layout) for chunk k+S-1 (after empty[] says the
+//               stage's MMAs are done), cp.async.mbarrier.arrive on
+//               full_raw[]; then waits full_raw[k], converts its share of
+//               raw A to the operand layout (tf32 round / hi-lo split /
+//               bf16), fence.proxy.async, arrives on full_op[k]; at the end
+//               they are the epilogue (TMEM lane quadrant = warp);
+//   warp 4      MMA issuer (one lane): tcgen05.mma for chunk k, commit to
+//               empty[k % S] and, after the last chunk, to done.
 // Grid: (row tiles of 128, N tiles of bn columns).
-constexpr int WS_THREADS = 192;
+constexpr int WS_THREADS = 160;
 template <int MODE>
 __global__ void __launch_bounds__(WS_THREADS, 1)
 k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__ in_row,
              const int32_t *__restrict__ words, const float *__restrict__ h_base,
              float *__restrict__ out_base, uint32_t row_limit_unused, int bn, int stages,
              uint32_t tmem_cols) {
-    const uint32_t row_limit = rs.row_limit;
     constexpr bool BF = MODE == 2;
     constexpr bool X3 = MODE == 1;
     constexpr int ELT = BF ? 2 : 4;                   // operand bytes per element
@@ -138,6 +139,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     constexpr int CH = KC_B / 16;                      // operand 16-byte chunks per row
     constexpr int RAW_ROW = KE * 4 + 16;               // raw fp32 row stride (+16 B pad)
     constexpr int RAW_CH = KE / 4;                     // raw 16-byte chunks per row
+    const uint32_t row_limit = rs.row_limit;
     const uint32_t n = rs.n_dev ? *rs.n_dev : n_cap;
     const uint32_t out0 = row_base(rs);
     if (rs.cur && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) rs.cur->base = out0;
@@ -167,14 +169,14 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     }
     if (tid == 0) {
         for (int st = 0; st < stages; st++) {
-            mbar_init(smem_u32(&full_raw[st]), 32);
+            mbar_init(smem_u32(&full_raw[st]), 128);
             mbar_init(smem_u32(&full_op[st]), 128);
             mbar_init(smem_u32(&empty[st]), 1);
         }
         mbar_init(smem_u32(done), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) {
+    if (warp == 4) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      :: "r"(smem_u32(tmem_slot)), "r"(tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -186,20 +188,49 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
 
     const int NK = (H + KE - 1) / KE;
     const uint32_t sbo = CH * 128, lbo = 128;
-    const int nsub = bn > 256 ? 2 : 1;
-    const int nmma = bn / nsub;
     const bool vec_ok = (H & 3) == 0;
 
-    if (warp == 0) {
-        // ------------------------------ producer ------------------------------
+    if (warp == 4) {
+        // ------------------------------ MMA issuer ----------------------------
+        const uint32_t idesc = make_idesc(BF ? 1 : 2, bn);
         for (int k = 0; k < NK; k++) {
             const int st = k % stages;
-            if (k >= stages) mbar_wait(smem_u32(&empty[st]), (uint32_t)(((k / stages) - 1) & 1));
+            mbar_wait(smem_u32(&full_op[st]), (uint32_t)((k / stages) & 1));
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (lane == 0) {
+                uint8_t *base = smem + st * stage_bytes;
+                uint8_t *sA = base + raw_bytes;
+                uint8_t *sA2 = sA + a_bytes;
+                uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
+                uint8_t *sB2 = sB + b_bytes;
+#pragma unroll
+                for (int ks = 0; ks < KC_B / 32; ks++) {     // 32 bytes of K per MMA
+                    const uint64_t a_hi = make_desc(smem_u32(sA) + ks * 2 * lbo, lbo, sbo);
+                    const uint64_t b_hi = make_desc(smem_u32(sB) + ks * 2 * lbo, lbo, sbo);
+                    const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
+                    mma<BF>(tmem, a_hi, b_hi, idesc, acc);
+                    if (X3) {
+                        const uint64_t a_lo = make_desc(smem_u32(sA2) + ks * 2 * lbo, lbo, sbo);
+                        const uint64_t b_lo = make_desc(smem_u32(sB2) + ks * 2 * lbo, lbo, sbo);
+                        mma<false>(tmem, a_hi, b_lo, idesc, 1u);
+                        mma<false>(tmem, a_lo, b_hi, idesc, 1u);
+                    }
+                }
+                commit(smem_u32(&empty[st]));
+                if (k == NK - 1) commit(smem_u32(done));
+            }
+            __syncwarp();
+        }
+    } else {
+        // ----------------------- loaders / converters -------------------------
+        auto issue = [&](int k) {
+            const int st = k % stages;
             uint8_t *base = smem + st * stage_bytes;
             uint8_t *raw = base;
             uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
             const int k0 = k * KE;
-            for (int idx = lane; idx < BM * RAW_CH; idx += 32) {
+            for (int idx = tid; idx < BM * RAW_CH; idx += 128) {
                 const int row = idx / RAW_CH, c = idx - row * RAW_CH;
                 const int src = s_row[row];
                 const int kk = k0 + c * 4;
@@ -211,7 +242,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                     for (int e = 0; e < 4; e++) dst[e] = kk + e < H ? h_base[(size_t)src * H + kk + e] : 0.f;
                 }
             }
-            for (int idx = lane; idx < bn * CH; idx += 32) {
+            for (int idx = tid; idx < bn * CH; idx += 128) {
                 const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
                 const int row = g * 8 + r8;
                 const int wrow = n0 + row;
@@ -237,54 +268,22 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                 }
             }
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(smem_u32(&full_raw[st])) : "memory");
-        }
-    } else if (warp == 1) {
-        // ------------------------------ MMA issuer ----------------------------
-        const uint32_t idesc = make_idesc(BF ? 1 : 2, nmma);
+        };
+        for (int k = 0; k < stages - 1 && k < NK; k++) issue(k);
         for (int k = 0; k < NK; k++) {
             const int st = k % stages;
-            mbar_wait(smem_u32(&full_op[st]), (uint32_t)((k / stages) & 1));
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (lane == 0) {
-                uint8_t *base = smem + st * stage_bytes;
-                uint8_t *sA = base + raw_bytes;
-                uint8_t *sA2 = sA + a_bytes;
-                uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
-                uint8_t *sB2 = sB + b_bytes;
-#pragma unroll
-                for (int ks = 0; ks < KC_B / 32; ks++) {
-                    for (int hh = 0; hh < nsub; hh++) {
-                        const uint32_t d = tmem + (uint32_t)(hh * nmma);
-                        const uint32_t boff = (uint32_t)(hh * nmma / 8) * sbo + ks * 2 * lbo;
-                        const uint64_t a_hi = make_desc(smem_u32(sA) + ks * 2 * lbo, lbo, sbo);
-                        const uint64_t b_hi = make_desc(smem_u32(sB) + boff, lbo, sbo);
-                        const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
-                        mma<BF>(d, a_hi, b_hi, idesc, acc);
-                        if (X3) {
-                            const uint64_t a_lo = make_desc(smem_u32(sA2) + ks * 2 * lbo, lbo, sbo);
-                            const uint64_t b_lo = make_desc(smem_u32(sB2) + boff, lbo, sbo);
-                            mma<false>(d, a_hi, b_lo, idesc, 1u);
-                            mma<false>(d, a_lo, b_hi, idesc, 1u);
-                        }
-                    }
-                }
-                commit(smem_u32(&empty[st]));
-                if (k == NK - 1) commit(smem_u32(done));
+            const int kn = k + stages - 1;
+            if (kn < NK) {
+                // stage (kn % S) was last used by chunk k-1: wait for its MMAs
+                if (k >= 1) mbar_wait(smem_u32(&empty[(k - 1) % stages]), (uint32_t)(((k - 1) / stages) & 1));
+                issue(kn);
             }
-            __syncwarp();
-        }
-    } else {
-        // ------------------------------ converters ----------------------------
-        const int ct = tid - 64;                          // 0..127
-        for (int k = 0; k < NK; k++) {
-            const int st = k % stages;
             mbar_wait(smem_u32(&full_raw[st]), (uint32_t)((k / stages) & 1));
             uint8_t *base = smem + st * stage_bytes;
             uint8_t *raw = base;
             uint8_t *sA = base + raw_bytes;
             uint8_t *sA2 = sA + a_bytes;
-            for (int idx = ct; idx < BM * CH; idx += 128) {
+            for (int idx = tid; idx < BM * CH; idx += 128) {
                 const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
                 const int row = g * 8 + r8;
                 const uint32_t off = tile_off(row, c);
@@ -316,8 +315,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
         // ------------------------------ epilogue ------------------------------
         mbar_wait(smem_u32(done), 0u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int quad = warp & 3;                        // TMEM lanes 32*quad .. +31
-        const int row = quad * 32 + lane;
+        const int row = warp * 32 + lane;                 // TMEM lane = row
         const uint32_t q = q0 + row;
         const bool valid = q < n;
         unsigned long long dig = 0ull;
@@ -325,7 +323,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
         float *orow = out_base + (size_t)(out0 + q) * H;
         for (int c0 = 0; c0 < bn; c0 += 32) {
             float v[32];
-            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, v);
+            tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
             const int gc = n0 + c0;
             if (valid) {
                 if (vec_ok && gc + 32 <= H) {
@@ -338,10 +336,12 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                         o.z = 1.f / (1.f + expf(-(v[j + 2] + u.z)));
                         o.w = 1.f / (1.f + expf(-(v[j + 3] + u.w)));
                         *reinterpret_cast<float4 *>(orow + gc + j) = o;
-                        dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o.x));
-                        dig += otf_hash64(((uint64_t)(gc + j + 1) << 32) ^ __float_as_uint(o.y));
-                        dig += otf_hash64(((uint64_t)(gc + j + 2) << 32) ^ __float_as_uint(o.z));
-                        dig += otf_hash64(((uint64_t)(gc + j + 3) << 32) ^ __float_as_uint(o.w));
+                        if (rs.dig) {
+                            dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o.x));
+                            dig += otf_hash64(((uint64_t)(gc + j + 1) << 32) ^ __float_as_uint(o.y));
+                            dig += otf_hash64(((uint64_t)(gc + j + 2) << 32) ^ __float_as_uint(o.z));
+                            dig += otf_hash64(((uint64_t)(gc + j + 3) << 32) ^ __float_as_uint(o.w));
+                        }
                     }
                 } else {
                     for (int j = 0; j < 32; j++)
@@ -357,7 +357,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 1)
+    if (warp == 4)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(tmem_cols));
 }
 
@@ -375,7 +375,7 @@ static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const 
     // memory, halved while there are too few row tiles to fill 148 SMs; a
     // partial last N tile is zero-filled (rows >= H) and masked on store
     const uint32_t m_tiles = (n_cap + tc::BM - 1) / tc::BM;
-    int bn = std::min(n_pad, prec == 1 ? 128 : 256);
+    int bn = std::min(std::min(n_pad, 256), prec == 1 ? 128 : 256);
     while (bn > 32 && (uint64_t)m_tiles * ((n_pad + bn - 1) / bn) < 148) bn /= 2;
     bn = (bn + 15) / 16 * 16;
     uint32_t cols = 32;

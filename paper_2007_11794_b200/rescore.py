@@ -23,7 +23,7 @@ from typing import Sequence
 import numpy as np
 
 from . import _lib
-from .device import DeviceModel, DeviceNgram, DeviceStreams, Plan
+from .device import DeviceModel, DeviceNgram, DeviceStreams, Plan, PlanGroup
 from .model import RnnlmContext
 
 ENTRY_BYTES = 32          # cache.py:26
