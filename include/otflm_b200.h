@@ -187,6 +187,11 @@ typedef struct {
 int otflm_plan_create(OtflmStreams *s, const OtflmLatticeBatch *lats, int64_t beam,
                       OtflmPlan **out, void *stream);
 int otflm_plan_destroy(OtflmPlan *p);
+/* Load another lattice batch into an existing plan.  When its compiled
+ * structure matches, the arrays are re-uploaded into the same buffers and
+ * captured graphs stay valid (*same = 1); otherwise nothing changes and
+ * OTFLM_ERR_VALUE is returned with *same = 0. */
+int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *lats, int32_t *same, void *stream);
 /* plan stats: levels, nodes, arcs, slots, max requests per level, total
  * request slots, graph nodes (int64 [8]) */
 int otflm_plan_info(const OtflmPlan *p, int64_t *out8);

@@ -108,6 +108,7 @@ _SIGS = {
     "otflm_rnnlm_prob_batch": (C.c_int, [_P, C.c_int64, _P, _P, _P, C.c_int32, _P, _P, _P, _P]),
     "otflm_plan_create": (C.c_int, [_P, C.POINTER(LatticeBatch), C.c_int64, C.POINTER(C.c_void_p), _P]),
     "otflm_plan_destroy": (C.c_int, [_P]),
+    "otflm_plan_refresh": (C.c_int, [_P, C.POINTER(LatticeBatch), C.POINTER(C.c_int32), _P]),
     "otflm_plan_info": (C.c_int, [_P, _P]),
     "otflm_decode_run": (C.c_int, [_P, _P, C.c_double, C.c_int32, C.c_int32, _P]),
     "otflm_decode_fetch": (C.c_int, [_P, C.POINTER(DecodeResult), _P]),

@@ -892,6 +892,50 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     return OTFLM_OK;
 }
 
+// Load a new lattice batch into an existing plan.  If the compiled
+// structure (levels, per-level node / request / range counts, slots, arcs,
+// utterances, stream ids) is identical, the arrays are copied into the same
+// device buffers and every captured CUDA graph stays valid: the next run is
+// a graph replay.  Returns OTFLM_ERR_VALUE with *same == 0 otherwise (the
+// caller creates a new plan).
+extern "C" int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *L, int32_t *same, void *stream) {
+    if (!p || !L || !same) return OTFLM_ERR_VALUE;
+    *same = 0;
+    if ((uint32_t)L->n_utt != p->n_utt) return OTFLM_ERR_VALUE;
+    cudaStream_t s = (cudaStream_t)stream;
+    OtflmPlan tmp;
+    std::vector<NodeInfo> nodes;
+    std::vector<uint32_t> level_nodes, out_list, arc_slot, start_slot, final_off, finals, utt_stream;
+    std::vector<int32_t> arc_word;
+    std::vector<double> arc_ac, arc_slm;
+    std::vector<StreamRange> ranges;
+    int rc = compile_batch(&tmp, L, p->beam, p->st->m->d.V, nodes, level_nodes, out_list, arc_slot, arc_word,
+                           arc_ac, arc_slm, start_slot, final_off, finals, utt_stream, ranges);
+    if (rc) return rc;
+    if (ranges.empty()) ranges.push_back(StreamRange{0, 0, 0, 0});
+    if (tmp.n_levels != p->n_levels || tmp.n_nodes != p->n_nodes || tmp.n_arcs != p->n_arcs ||
+        tmp.n_slots != p->n_slots || tmp.R_max != p->R_max || tmp.lvl_node_off != p->lvl_node_off ||
+        tmp.lvl_req != p->lvl_req || tmp.lvl_range_off != p->lvl_range_off || utt_stream != p->utt_stream_host)
+        return OTFLM_ERR_VALUE;
+    DevPlan &d = p->d;
+    auto put = [&](const void *dst, const void *src, size_t bytes) -> cudaError_t {
+        return bytes ? cudaMemcpyAsync((void *)dst, src, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
+    };
+    CK(put(d.nodes, nodes.data(), nodes.size() * sizeof(NodeInfo)));
+    CK(put(d.level_nodes, level_nodes.data(), level_nodes.size() * 4));
+    CK(put(d.out_list, out_list.data(), out_list.size() * 4));
+    CK(put(d.arc_slot, arc_slot.data(), arc_slot.size() * 4));
+    CK(put(d.arc_word, arc_word.data(), arc_word.size() * 4));
+    CK(put(d.arc_ac, arc_ac.data(), arc_ac.size() * 8));
+    CK(put(d.arc_slm, arc_slm.data(), arc_slm.size() * 8));
+    CK(put(d.utt_start_slot, start_slot.data(), start_slot.size() * 4));
+    CK(put(d.final_off, final_off.data(), final_off.size() * 4));
+    CK(put(d.finals, finals.data(), finals.size() * 4));
+    CK(put(d.ranges, ranges.data(), ranges.size() * sizeof(StreamRange)));
+    *same = 1;
+    return OTFLM_OK;
+}
+
 extern "C" int otflm_plan_destroy(OtflmPlan *p) {
     if (!p) return OTFLM_OK;
     if (p->gexec) cudaGraphExecDestroy(p->gexec);

@@ -230,6 +230,19 @@ class Plan:
         _lib.check(_lib.load().otflm_plan_info(self.handle, _p(out)), "plan info")
         return out
 
+    def refresh(self, lattices, stream_ids=None) -> bool:
+        """Load another batch with the same compiled structure into this plan
+        (same buffers, captured graphs stay valid).  False: structure differs."""
+        batch, arrays, lats = pack_lattices(lattices, stream_ids)
+        same = C.c_int32(0)
+        rc = _lib.load().otflm_plan_refresh(self.handle, C.byref(batch), C.byref(same),
+                                            current_stream_ptr())
+        if not same.value:
+            return False
+        _lib.check(rc, "plan refresh")
+        self.batch, self.arrays, self.lats = batch, arrays, lats
+        return True
+
     def set_arena(self, start: int, end: int) -> None:
         _lib.check(_lib.load().otflm_plan_set_arena(self.handle, int(start), int(end)), "arena")
 

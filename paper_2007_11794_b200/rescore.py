@@ -367,9 +367,19 @@ class BatchDecoder:
         return worst + 1
 
     def prepare(self, lattices, beam: int):
+        """Compile + upload a batch.  A batch with the same compiled
+        structure as the previous one (same beam, same level/node/arc
+        counts) is loaded into the existing plans so the captured graph is
+        replayed; otherwise new plans are built."""
         lattices = list(lattices)
         G = min(self.n_groups, len(lattices))
         bounds = np.linspace(0, len(lattices), G + 1).astype(int)
+        if self.plans and getattr(self, "beam", None) == beam and len(self.plans) == G and \
+                all(len(ids) == b1 - b0 for ids, b0, b1 in zip(self.spans, bounds[:-1], bounds[1:])):
+            if all(p.refresh([lattices[i] for i in ids], stream_ids=ids)
+                   for p, ids in zip(self.plans, self.spans)):
+                return self.plans
+        self.beam = beam
         self.plans = []
         self.spans = []
         rows = (self.arena_rows - 1) // G

@@ -108,6 +108,15 @@ def build_setup(name: str, n_utt: int | None = None, T: int | None = None,
     return Setup(name, model, tree, lm, lats, cfg["beam"], cfg["breadth"])
 
 
+def more_lattices(setup: Setup, n_utt: int, T: int, seed: int) -> list:
+    """Another batch of lattices over the same model / small LM."""
+    V = setup.model.vocab_size
+    index = _BigramIndex(setup.small_lm)
+    refs = reference_sentences(V, n_utt, T, seed)
+    return [generate_lattice(refs[i], V, setup.small_lm, setup.breadth, noise_seed=seed * 100003 + i,
+                             index=index) for i in range(n_utt)]
+
+
 def query_set(model: RnnlmModel, n_queries: int, n_ctx: int, seed_w: int = 4, seed_c: int = 5):
     """Config (d): words ~ Zipf(1.05) over V, distinct contexts with
     h ~ U(0.001, 0.999) and 3-word histories ~ U[0, V)."""
