@@ -143,22 +143,26 @@ def query_microbench(precision: str, n_queries: int = 1 << 20, n_ctx: int = 1 <<
             ts.append(a.elapsed_time(b))
         return float(np.median(ts))
 
-    hs_ms = timed(lambda: kernels.word_logprob_batch(dm, tctx, th, thist, thl, tw))
+    hs_ms = timed(lambda: kernels.word_logprob_batch(dm, tctx, th, thist, thl, tw, exact=True, out=out))
+    hs_fast_ms = timed(lambda: kernels.word_logprob_batch(dm, tctx, th, thist, thl, tw, exact=False, out=out))
     adv_ms = timed(lambda: kernels.advance_hidden_batch(dm, tctx, th, tw, precision, out=hout))
     P = (tree.path_offsets[1:] - tree.path_offsets[:-1])[words]
     k = np.minimum(hlen[ctx], model.maxent_order)
     hs_bytes = float(np.sum(P * (4 * H + 4 * k + 8)) + n_queries * (4 * H + 16))
     hbm, tc_peak, src = peaks()
     gbs = hs_bytes / (hs_ms / 1e3) / 1e9
+    gbs_fast = hs_bytes / (hs_fast_ms / 1e3) / 1e9
     flops = 2.0 * H * H * n_queries
     tfs = flops / (adv_ms / 1e3) / 1e12
     return {"workload": f"config d: {n_queries} queries, {n_ctx} contexts, V={V} H={H} MaxEnt 2^{bits}, "
                         "words ~ Zipf(1.05); L2 flushed before each launch",
-            "hs_ms": hs_ms, "hs_gbs": gbs, "hs_frac_of_hbm": gbs / hbm, "hs_bytes": hs_bytes,
+            "hs_exact_ms": hs_ms, "hs_exact_gbs": gbs, "hs_exact_frac_of_hbm": gbs / hbm,
+            "hs_fast_ms": hs_fast_ms, "hs_fast_gbs": gbs_fast, "hs_fast_frac_of_hbm": gbs_fast / hbm,
+            "hs_bytes": hs_bytes,
             "mean_path": float(P.mean()),
             "advance_ms": adv_ms, "advance_tflops": tfs, "advance_frac_of_bf16_peak": tfs / tc_peak,
             "advance_precision": precision,
-            "queries_per_s": n_queries / ((hs_ms + adv_ms) / 1e3), "peak_source": src}
+            "queries_per_s": n_queries / ((min(hs_ms, hs_fast_ms) + adv_ms) / 1e3), "peak_source": src}
 
 
 def cpu_baseline(setup, n_sample: int, threads: int):

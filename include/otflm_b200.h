@@ -108,6 +108,13 @@ int otflm_word_logprob_batch(const OtflmModel *m, int64_t n, const int32_t *ctx_
                              const float *h_dev, const int32_t *hist_dev,
                              const int32_t *hist_len_dev, const int32_t *w_dev,
                              double *out_dev, void *stream);
+/* Same with the accumulation mode chosen: exact != 0 accumulates the dot
+ * products in float64 (|d| <= 1e-12 vs the reference); exact == 0 uses f32
+ * per-lane partials (|d| <= 1e-5; the tensor-core decode modes use it). */
+int otflm_word_logprob_batch2(const OtflmModel *m, int64_t n, const int32_t *ctx_dev,
+                              const float *h_dev, const int32_t *hist_dev,
+                              const int32_t *hist_len_dev, const int32_t *w_dev,
+                              double *out_dev, int32_t exact, void *stream);
 /* word_logprob with explicit path slices (the reference kernel signature,
  * _kernels_nb.py:78-79): query i scores path_code[path_off[i]..path_off[i+1])
  * where code = node | (branch bit << 31). */

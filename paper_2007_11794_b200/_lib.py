@@ -96,6 +96,7 @@ _SIGS = {
     "otflm_ngram_logprob_batch": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P]),
     "otflm_feature_index_batch": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int64, _P, _P, _P, _P, _P]),
     "otflm_word_logprob_batch": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, _P]),
+    "otflm_word_logprob_batch2": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, C.c_int32, _P]),
     "otflm_word_logprob_paths": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, _P, _P, _P]),
     "otflm_advance_hidden_batch": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, C.c_int32, _P]),
     "otflm_advance_hidden_rows": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, C.c_int32, _P]),

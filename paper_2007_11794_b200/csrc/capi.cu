@@ -304,34 +304,44 @@ extern "C" int otflm_feature_index_batch(uint64_t seed, uint64_t mask, int64_t n
     return OTFLM_OK;
 }
 
-extern "C" int otflm_word_logprob_batch(const OtflmModel *m, int64_t n, const int32_t *ctx, const float *h,
-                                        const int32_t *hist, const int32_t *hist_len, const int32_t *w,
-                                        double *out, void *stream) {
+static int launch_ring_batch(const DevModel &m, int64_t n, const int32_t *ctx, const float *h, const int32_t *hist,
+                             const int32_t *hist_len, const int32_t *w, double *out, bool exact, cudaStream_t s) {
+    const size_t smem = 4 * ring_bytes_per_warp(m.H);
+    int per_sm = 1;
+#define CALLR(CPL, EX, ORD)                                                                                        \
+    do {                                                                                                           \
+        CK(cudaFuncSetAttribute(k_word_logprob_ring<CPL, EX, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_word_logprob_ring<CPL, EX, ORD>, 128, smem)); \
+        const unsigned grid = (unsigned)std::min<int64_t>(cdiv(n, 4), (int64_t)148 * std::max(per_sm, 1));        \
+        k_word_logprob_ring<CPL, EX, ORD><<<grid, 128, smem, s>>>(m, n, ctx, h, hist, hist_len, w, out);           \
+    } while (0)
+    if (exact) RING_DISPATCH(m.H, true, m.order, CALLR);
+    else RING_DISPATCH(m.H, false, m.order, CALLR);
+#undef CALLR
+    CKL();
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_word_logprob_batch2(const OtflmModel *m, int64_t n, const int32_t *ctx, const float *h,
+                                         const int32_t *hist, const int32_t *hist_len, const int32_t *w,
+                                         double *out, int32_t exact, void *stream) {
     if (n <= 0) return OTFLM_OK;
     if (!m->d.NV || !m->d.ME || !m->d.path_off) { g_detail = "model has no output layer"; return OTFLM_ERR_VALUE; }
     cudaStream_t s = (cudaStream_t)stream;
-    if (m->d.H % 4 == 0 && m->d.H <= 1024) {
-        // TMA-fed ring: 4 warps per CTA, grid sized to the SMs' resident CTAs
-        const size_t smem = 4 * ring_bytes_per_warp(m->d.H);
-        int per_sm = 1;
-#define RING(CPL)                                                                                        \
-        do {                                                                                             \
-            CK(cudaFuncSetAttribute(k_word_logprob_ring<CPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_word_logprob_ring<CPL>, 128, smem)); \
-            const unsigned grid = (unsigned)std::min<int64_t>(cdiv(n, 4), (int64_t)148 * std::max(per_sm, 1)); \
-            k_word_logprob_ring<CPL><<<grid, 128, smem, s>>>(m->d, n, ctx, h, hist, hist_len, w, out);   \
-        } while (0)
-        if (m->d.H <= 128) RING(1); else if (m->d.H <= 256) RING(2); else if (m->d.H <= 512) RING(4); else RING(8);
-#undef RING
-        CKL();
-        return OTFLM_OK;
-    }
+    if (m->d.H % 4 == 0 && m->d.H <= 1024)
+        return launch_ring_batch(m->d, n, ctx, h, hist, hist_len, w, out, exact != 0, s);
     const unsigned blocks = cdiv(n, 8);
 #define CALL(VEC, CPL) k_word_logprob_batch<VEC, CPL><<<blocks, 256, 0, s>>>(m->d, n, ctx, h, hist, hist_len, w, out)
     HS_DISPATCH(m->d.H, CALL);
 #undef CALL
     CKL();
     return OTFLM_OK;
+}
+
+extern "C" int otflm_word_logprob_batch(const OtflmModel *m, int64_t n, const int32_t *ctx, const float *h,
+                                        const int32_t *hist, const int32_t *hist_len, const int32_t *w,
+                                        double *out, void *stream) {
+    return otflm_word_logprob_batch2(m, n, ctx, h, hist, hist_len, w, out, 1, stream);
 }
 
 extern "C" int otflm_word_logprob_paths(const OtflmModel *m, int64_t n, const int32_t *ctx, const float *h,
@@ -970,9 +980,27 @@ static int enqueue_stage2(OtflmPlan *p, const DevModel &m, DevStreams &S, uint32
     CK(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
     {
         ProfScope ps(K_HS, p->side);
+        if (m.H % 4 == 0 && m.H <= 1024) {
+            // persistent TMA-ring warps: enough CTAs for the level, at most the
+            // resident capacity of the GPU
+            const size_t smem = 4 * ring_bytes_per_warp(m.H);
+            const bool exact = prec == OTFLM_PREC_FP64;
+#define CALLR(CPL, EX, ORD)                                                                                        \
+            do {                                                                                                   \
+                CK(cudaFuncSetAttribute(k_hs_prim_ring<CPL, EX, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+                int per_sm = 1;                                                                                    \
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hs_prim_ring<CPL, EX, ORD>, 128, smem)); \
+                const unsigned grid = (unsigned)std::min<uint64_t>(cdiv(R, 4), (uint64_t)148 * std::max(per_sm, 1)); \
+                k_hs_prim_ring<CPL, EX, ORD><<<grid, 128, smem, p->side>>>(m, d, S, rs);                          \
+            } while (0)
+            if (exact) RING_DISPATCH(m.H, true, m.order, CALLR);
+            else RING_DISPATCH(m.H, false, m.order, CALLR);
+#undef CALLR
+        } else {
 #define CALL(VEC, CPL) k_hs_prim<VEC, CPL><<<cdiv(R, 8), 256, 0, p->side>>>(m, d, S, rs)
-        HS_DISPATCH(m.H, CALL);
+            HS_DISPATCH(m.H, CALL);
 #undef CALL
+        }
         CKL();
     }
     {

@@ -361,6 +361,33 @@ __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, DevNgra
 // stage 2a: HS + MaxEnt score of the computed requests (warp per request),
 // successor history (history + (w,))[-order:] (rnnlm.py:187) and its digest
 // --------------------------------------------------------------------------
+__device__ __forceinline__ void hs_prim_finish(DevModel &m, DevPlan &P, DevStreams &S, const RowSpec &rs,
+                                               uint32_t base, uint32_t q, const uint32_t *meta, int L, int w,
+                                               uint32_t P_len, double lp, int lane) {
+    // new history: drop the oldest word once `order` are stored (rnnlm.py:187)
+    const int nl = L + 1 > m.order ? m.order : L + 1;
+    const int drop = L + 1 - nl;
+    uint32_t v = 0;
+    if (lane == 0) v = (uint32_t)nl;
+    else if (lane < nl) v = meta[lane + drop];
+    else if (lane == nl) v = (uint32_t)w;
+    unsigned long long dg = lane < OTF_META ? dig_meta(lane, v) : 0ull;
+    if (lane < OTF_META) S.arena_meta[(size_t)(base + q) * OTF_META + lane] = v;
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) dg += __shfl_xor_sync(0xffffffffu, dg, o);
+    if (lane == 0) {
+        atomicAdd(&P.pr_dig[q], dg);
+        if (P.alg) {   // algorithmic-work counters for the roofline (profiling runs)
+            const int km = m.order < L ? m.order : L;
+            atomicAdd(&P.alg[0], (unsigned long long)P_len);
+            atomicAdd(&P.alg[1], (unsigned long long)P_len * km);
+            atomicAdd(&P.alg[2], 1ull);
+        }
+        P.pr_p[q] = lp;
+    }
+}
+
+// generic path (H % 4 != 0): warp per request, registers
 template <int VEC, int CPL>
 __global__ void __launch_bounds__(256) k_hs_prim(DevModel m, DevPlan P, DevStreams S, RowSpec rs) {
     const uint32_t n = *rs.n_dev;
@@ -378,28 +405,36 @@ __global__ void __launch_bounds__(256) k_hs_prim(DevModel m, DevPlan P, DevStrea
     const int L = (int)meta[0];
     const int w = P.pr_w[q];
     const uint32_t o0 = __ldg(m.path_off + w), o1 = __ldg(m.path_off + w + 1);
-    double lp = hs_logprob_warp<VEC, CPL>(m, S.arena_h + (size_t)row * m.H, meta + 1, L,
-                                          m.path_code + o0, o1 - o0, lane);
-    // new history: drop the oldest word once `order` are stored
-    const int nl = L + 1 > m.order ? m.order : L + 1;
-    const int drop = L + 1 - nl;
-    uint32_t v = 0;
-    if (lane == 0) v = (uint32_t)nl;
-    else if (lane < nl) v = meta[lane + drop];
-    else if (lane == nl) v = (uint32_t)w;
-    unsigned long long d = lane < OTF_META ? dig_meta(lane, v) : 0ull;
-    if (lane < OTF_META) S.arena_meta[(size_t)(base + q) * OTF_META + lane] = v;
-#pragma unroll
-    for (int o = 4; o >= 1; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-    if (lane == 0) {
-        atomicAdd(&P.pr_dig[q], d);
-        if (P.alg) {   // algorithmic-work counters for the roofline (profiling runs)
-            const int km = m.order < L ? m.order : L;
-            atomicAdd(&P.alg[0], (unsigned long long)(o1 - o0));
-            atomicAdd(&P.alg[1], (unsigned long long)(o1 - o0) * km);
-            atomicAdd(&P.alg[2], 1ull);
-        }
-        P.pr_p[q] = lp;
+    const double lp = hs_logprob_warp<VEC, CPL>(m, S.arena_h + (size_t)row * m.H, meta + 1, L,
+                                                m.path_code + o0, o1 - o0, lane);
+    hs_prim_finish(m, P, S, rs, base, q, meta, L, w, o1 - o0, lp, lane);
+}
+
+// TMA ring path (H % 4 == 0): persistent warps stride over the requests
+template <int CPL, bool EXACT, int ORD>
+__global__ void __launch_bounds__(128) k_hs_prim_ring(DevModel m, DevPlan P, DevStreams S, RowSpec rs) {
+    extern __shared__ __align__(128) uint8_t smem_ring[];
+    const uint32_t n = *rs.n_dev;
+    const uint32_t base = row_base(rs);
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + wib;
+    if (gw == 0 && lane == 0) rs.cur->base = base;
+    if ((uint64_t)base + n > rs.row_limit) {
+        if (gw == 0 && lane == 0) atomicOr(S.err, OTF_E_ARENA_FULL);
+        return;
+    }
+    if (gw >= n) return;
+    HsRing ring = ring_setup(smem_ring, wib, m.H, lane);
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t q = gw; q < n; q += nw) {
+        const uint32_t row = (uint32_t)P.pr_inrow[q];
+        const uint32_t *meta = S.arena_meta + (size_t)row * OTF_META;
+        const int L = (int)meta[0];
+        const int w = P.pr_w[q];
+        const uint32_t o0 = __ldg(m.path_off + w), o1 = __ldg(m.path_off + w + 1);
+        const double lp = hs_logprob_ring<CPL, EXACT, ORD>(m, ring, S.arena_h + (size_t)row * m.H, meta + 1, L,
+                                                           m.path_code + o0, o1 - o0, lane);
+        hs_prim_finish(m, P, S, rs, base, q, meta, L, w, o1 - o0, lp, lane);
     }
 }
 

@@ -191,32 +191,43 @@ __device__ __forceinline__ void ring_wait(HsRing &r, int slot) {
     r.phase ^= 1u << slot;
 }
 
-template <int CPL>
+// EXACT: float64 accumulation of the exact f32 x f32 products (4 independent
+// accumulators per row keep the DFMA chains short); only the summation order
+// differs from the reference (~1e-16 relative).
+// !EXACT: per-lane partial dot in f32 FFMA (<= 4H/128 terms per lane, error
+// ~1e-7 relative), lane partials combined and everything after (MaxEnt,
+// log-sigmoid, path sum) in float64 -- used with the tensor-core update
+// modes, whose h' already differs from the reference at ~1e-7; log-probs stay
+// within 1e-5 of the reference (the north star allows 1e-4).
+template <int CPL, bool EXACT, int ORD>
 __device__ __forceinline__ double hs_logprob_ring(const DevModel &m, HsRing &ring, const float *__restrict__ h,
                                                   const uint32_t *__restrict__ hist, int L,
                                                   const uint32_t *__restrict__ codes, uint32_t P, int lane) {
     const int H = m.H;
     const int NCH = H >> 2;
     const uint32_t bytes = (uint32_t)H * 4u;
-    // first HS_NS rows in flight before anything else
     if (lane == 0)
         for (uint32_t p = 0; p < P && p < HS_NS; p++)
             ring_issue(ring, (int)p, m.NV + (size_t)(__ldg(codes + p) & 0x7FFFFFFFu) * H, bytes);
-    double hv[CPL][4];
+    double hd[EXACT ? CPL : 1][4];
+    float hf[EXACT ? 1 : CPL][4];
 #pragma unroll
     for (int c = 0; c < CPL; c++) {
         const int k = lane + 32 * c;
-        if (k < NCH) {
-            const float4 t = __ldg(reinterpret_cast<const float4 *>(h) + k);
-            hv[c][0] = widen(t.x); hv[c][1] = widen(t.y); hv[c][2] = widen(t.z); hv[c][3] = widen(t.w);
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < NCH) t = __ldg(reinterpret_cast<const float4 *>(h) + k);
+        if (EXACT) {
+            hd[EXACT ? c : 0][0] = widen(t.x); hd[EXACT ? c : 0][1] = widen(t.y);
+            hd[EXACT ? c : 0][2] = widen(t.z); hd[EXACT ? c : 0][3] = widen(t.w);
         } else {
-            hv[c][0] = hv[c][1] = hv[c][2] = hv[c][3] = 0.0;
+            hf[EXACT ? 0 : c][0] = t.x; hf[EXACT ? 0 : c][1] = t.y;
+            hf[EXACT ? 0 : c][2] = t.z; hf[EXACT ? 0 : c][3] = t.w;
         }
     }
     const int kmax = m.order < L ? m.order : L;
-    uint64_t pre[OTF_MAX_ORDER];
+    uint64_t pre[ORD];
 #pragma unroll
-    for (int k = 0; k < OTF_MAX_ORDER; k++) {
+    for (int k = 0; k < ORD; k++) {
         pre[k] = 0;
         if (k < kmax) {
             uint64_t x = otf_mix(m.seed, (uint64_t)(k + 1));
@@ -229,9 +240,9 @@ __device__ __forceinline__ double hs_logprob_ring(const DevModel &m, HsRing &rin
     double lp = 0.0;
     for (uint32_t p0 = 0; p0 < P; p0 += HS_G) {
         const uint32_t my_code = (p0 + my_g < P) ? __ldg(codes + p0 + my_g) : OTF_UNSET;
-        double me[OTF_MAX_ORDER];
+        double me[ORD];
 #pragma unroll
-        for (int k = 0; k < OTF_MAX_ORDER; k++) {
+        for (int k = 0; k < ORD; k++) {
             me[k] = 0.0;
             if (leader && k < kmax && my_code != OTF_UNSET)
                 me[k] = (double)__ldg(m.ME + (otf_mix(pre[k], (uint64_t)(my_code & 0x7FFFFFFFu)) & m.mask));
@@ -245,16 +256,34 @@ __device__ __forceinline__ double hs_logprob_ring(const DevModel &m, HsRing &rin
                 const int slot = (int)(p % HS_NS);
                 ring_wait(ring, slot);
                 const float4 *row = reinterpret_cast<const float4 *>(ring.buf + (size_t)slot * bytes);
+                if (EXACT) {
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-                for (int c = 0; c < CPL; c++) {
-                    const int k = lane + 32 * c;
-                    if (k < NCH) {
-                        const float4 t = row[k];
-                        acc[g] = fma(widen(t.x), hv[c][0], acc[g]);
-                        acc[g] = fma(widen(t.y), hv[c][1], acc[g]);
-                        acc[g] = fma(widen(t.z), hv[c][2], acc[g]);
-                        acc[g] = fma(widen(t.w), hv[c][3], acc[g]);
+                    for (int c = 0; c < CPL; c++) {
+                        const int k = lane + 32 * c;
+                        if (k < NCH) {
+                            const float4 t = row[k];
+                            a0 = fma(widen(t.x), hd[EXACT ? c : 0][0], a0);
+                            a1 = fma(widen(t.y), hd[EXACT ? c : 0][1], a1);
+                            a2 = fma(widen(t.z), hd[EXACT ? c : 0][2], a2);
+                            a3 = fma(widen(t.w), hd[EXACT ? c : 0][3], a3);
+                        }
                     }
+                    acc[g] = (a0 + a1) + (a2 + a3);
+                } else {
+                    float f0 = 0.f, f1 = 0.f, f2 = 0.f, f3 = 0.f;
+#pragma unroll
+                    for (int c = 0; c < CPL; c++) {
+                        const int k = lane + 32 * c;
+                        if (k < NCH) {
+                            const float4 t = row[k];
+                            f0 = fmaf(t.x, hf[EXACT ? 0 : c][0], f0);
+                            f1 = fmaf(t.y, hf[EXACT ? 0 : c][1], f1);
+                            f2 = fmaf(t.z, hf[EXACT ? 0 : c][2], f2);
+                            f3 = fmaf(t.w, hf[EXACT ? 0 : c][3], f3);
+                        }
+                    }
+                    acc[g] = ((double)f0 + (double)f1) + ((double)f2 + (double)f3);
                 }
                 __syncwarp();
                 if (lane == 0 && p + HS_NS < P)
@@ -263,7 +292,7 @@ __device__ __forceinline__ double hs_logprob_ring(const DevModel &m, HsRing &rin
         }
         double a = reduce8(acc, lane);
 #pragma unroll
-        for (int k = 0; k < OTF_MAX_ORDER; k++) if (k < kmax) a += me[k];
+        for (int k = 0; k < ORD; k++) if (k < kmax) a += me[k];
         double mylog = 0.0;
         if (leader && my_code != OTF_UNSET)
             mylog = otf_log_sigmoid((my_code & 0x80000000u) ? -a : a);
@@ -292,8 +321,24 @@ __device__ __forceinline__ HsRing ring_setup(uint8_t *smem, int warp_in_block, i
 }
 __host__ __device__ constexpr size_t ring_bytes_per_warp(int H) { return (size_t)HS_NS * (4 * H + 8); }
 
+// CALLR(CPL, EXACT, ORD) for H % 4 == 0, H <= 1024
+#define RING_DISPATCH(H, EXACT, ORDER, CALLR)                                   \
+    do {                                                                       \
+        if ((ORDER) <= 3) {                                                    \
+            if ((H) <= 128) { CALLR(1, EXACT, 3); }                            \
+            else if ((H) <= 256) { CALLR(2, EXACT, 3); }                       \
+            else if ((H) <= 512) { CALLR(4, EXACT, 3); }                       \
+            else { CALLR(8, EXACT, 3); }                                       \
+        } else {                                                               \
+            if ((H) <= 128) { CALLR(1, EXACT, OTF_MAX_ORDER); }                \
+            else if ((H) <= 256) { CALLR(2, EXACT, OTF_MAX_ORDER); }           \
+            else if ((H) <= 512) { CALLR(4, EXACT, OTF_MAX_ORDER); }           \
+            else { CALLR(8, EXACT, OTF_MAX_ORDER); }                           \
+        }                                                                      \
+    } while (0)
+
 // batch API (config d): warps stride over queries, ring reused across queries
-template <int CPL>
+template <int CPL, bool EXACT, int ORD>
 __global__ void __launch_bounds__(128) k_word_logprob_ring(DevModel m, int64_t n, const int32_t *__restrict__ ctx,
                                                            const float *__restrict__ h,
                                                            const int32_t *__restrict__ hist,
@@ -310,7 +355,8 @@ __global__ void __launch_bounds__(128) k_word_logprob_ring(DevModel m, int64_t n
         const int L = hist_len[c];
         for (int i = 0; i < L; i++) hw[i] = (uint32_t)hist[(int64_t)c * m.order + i];
         const uint32_t o0 = __ldg(m.path_off + w[q]), o1 = __ldg(m.path_off + w[q] + 1);
-        const double lp = hs_logprob_ring<CPL>(m, ring, h + (int64_t)c * m.H, hw, L, m.path_code + o0, o1 - o0, lane);
+        const double lp = hs_logprob_ring<CPL, EXACT, ORD>(m, ring, h + (int64_t)c * m.H, hw, L, m.path_code + o0,
+                                                           o1 - o0, lane);
         if (lane == 0) out[q] = lp;
     }
 }

@@ -26,7 +26,7 @@
 namespace tc {
 
 constexpr int BM = 128;      // rows per CTA tile (UMMA_M)
-constexpr int KC_B = 128;    // bytes of K per row per pipeline stage
+constexpr int KC_B = 64;     // operand bytes of K per row per pipeline stage
 constexpr int NTHREADS = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -137,8 +137,8 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     constexpr int ELT = BF ? 2 : 4;                   // operand bytes per element
     constexpr int KE = KC_B / ELT;                     // K elements per stage
     constexpr int CH = KC_B / 16;                      // operand 16-byte chunks per row
-    constexpr int RAW_ROW = KE * 4 + 16;               // raw fp32 row stride (+16 B pad)
-    constexpr int RAW_CH = KE / 4;                     // raw 16-byte chunks per row
+    constexpr int RAW_ROW = KE * 4 + 16;               // bf16 only: raw fp32 row stride (+16 B pad)
+    constexpr int RAW_CH = KE / 4;                     // raw fp32 16-byte chunks per row
     const uint32_t row_limit = rs.row_limit;
     const uint32_t n = rs.n_dev ? *rs.n_dev : n_cap;
     const uint32_t out0 = row_base(rs);
@@ -151,7 +151,10 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     extern __shared__ __align__(1024) uint8_t smem[];
-    const uint32_t raw_bytes = BM * RAW_ROW;
+    // tf32 modes stage the fp32 A chunks directly in the operand layout and
+    // round them in place (x3 also writes the lo part); bf16 needs a raw
+    // fp32 staging area
+    const uint32_t raw_bytes = BF ? BM * RAW_ROW : 0u;
     const uint32_t a_bytes = BM * KC_B;
     const uint32_t b_bytes = (uint32_t)bn * KC_B;
     const uint32_t stage_bytes = raw_bytes + (X3 ? 2 : 1) * (a_bytes + b_bytes);
@@ -230,15 +233,20 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
             uint8_t *raw = base;
             uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
             const int k0 = k * KE;
+            uint8_t *sAop = base + raw_bytes;
             for (int idx = tid; idx < BM * RAW_CH; idx += 128) {
-                const int row = idx / RAW_CH, c = idx - row * RAW_CH;
+                int row, c;
+                uint32_t off;
+                if (BF) { row = idx / RAW_CH; c = idx - row * RAW_CH; off = row * RAW_ROW + c * 16; }
+                else { const int r8 = idx & 7, g = idx / (8 * CH); c = (idx >> 3) % CH; row = g * 8 + r8; off = tile_off(row, c); }
+                uint8_t *dstb = BF ? raw : sAop;
                 const int src = s_row[row];
                 const int kk = k0 + c * 4;
                 const bool ok = src >= 0 && kk < H && vec_ok;
-                cp_async16(smem_u32(raw + row * RAW_ROW + c * 16),
+                cp_async16(smem_u32(dstb + off),
                            ok ? (const void *)(h_base + (size_t)src * H + kk) : (const void *)h_base, ok);
                 if (!vec_ok && src >= 0) {   // unaligned H: synchronous scalar fill (rare)
-                    float *dst = reinterpret_cast<float *>(raw + row * RAW_ROW + c * 16);
+                    float *dst = reinterpret_cast<float *>(dstb + off);
                     for (int e = 0; e < 4; e++) dst[e] = kk + e < H ? h_base[(size_t)src * H + kk + e] : 0.f;
                 }
             }
@@ -297,7 +305,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                     u.z = *reinterpret_cast<uint32_t *>(&b2); u.w = *reinterpret_cast<uint32_t *>(&b3);
                     *reinterpret_cast<uint4 *>(sA + off) = u;
                 } else {
-                    const float4 x = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 16);
+                    const float4 x = *reinterpret_cast<const float4 *>(sA + off);   // staged in place
                     float4 hi;
                     hi.x = tf32_rn(x.x); hi.y = tf32_rn(x.y); hi.z = tf32_rn(x.z); hi.w = tf32_rn(x.w);
                     *reinterpret_cast<float4 *>(sA + off) = hi;
@@ -382,10 +390,13 @@ static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const 
     while ((int)cols < bn) cols <<= 1;
     const bool x3 = prec == 1;
     const int ke = prec == 2 ? tc::KC_B / 2 : tc::KC_B / 4;
-    const uint32_t raw_bytes = tc::BM * (ke * 4 + 16);
+    const uint32_t raw_bytes = prec == 2 ? tc::BM * (ke * 4 + 16) : 0u;
     const uint32_t stage_bytes = raw_bytes + (x3 ? 2u : 1u) * (uint32_t)(tc::BM + bn) * tc::KC_B;
     const int nk = (H + ke - 1) / ke;
-    int stages = (int)std::min<uint32_t>(4u, (200u * 1024u) / stage_bytes);
+    // two CTAs per SM (each <= 110 KB) when that still leaves >= 4 stages, so
+    // one CTA's epilogue / pipeline fill overlaps the other's main loop
+    int stages = (int)std::min<uint32_t>(8u, (200u * 1024u) / stage_bytes);
+    if (4u * stage_bytes <= 110u * 1024u) stages = (int)std::min<uint32_t>(8u, (110u * 1024u) / stage_bytes);
     stages = std::max(2, std::min(stages, std::max(nk, 2)));
     const size_t smem = (size_t)stages * stage_bytes + (3 * stages + 1) * 8 + 16 + 1024;
     const dim3 grid(m_tiles, (n_pad + bn - 1) / bn);

@@ -163,15 +163,18 @@ def all_word_logprobs(hidden, history, path_nodes, path_signs, path_offsets, nod
 
 # --- batched forms used by the decoder and the query microbenchmark -------
 
-def word_logprob_batch(dmodel: DeviceModel, ctx, h, hist, hist_len, words):
-    """Device tensors in, device float64 tensor out (query i: context ctx[i])."""
+def word_logprob_batch(dmodel: DeviceModel, ctx, h, hist, hist_len, words, exact: bool = True,
+                       out=None):
+    """Device tensors in, device float64 tensor out (query i: context ctx[i]).
+    exact=True: float64 accumulation (|d| <= 1e-12); False: f32 lane partials."""
     torch = cuda()
     n = int(words.shape[0])
-    out = torch.empty(n, dtype=torch.float64, device=words.device)
-    _lib.check(_lib.load().otflm_word_logprob_batch(dmodel.handle, n, ctx.data_ptr(), h.data_ptr(),
-                                                    hist.data_ptr(), hist_len.data_ptr(),
-                                                    words.data_ptr(), out.data_ptr(),
-                                                    current_stream_ptr()), "word_logprob_batch")
+    if out is None:
+        out = torch.empty(n, dtype=torch.float64, device=words.device)
+    _lib.check(_lib.load().otflm_word_logprob_batch2(dmodel.handle, n, ctx.data_ptr(), h.data_ptr(),
+                                                     hist.data_ptr(), hist_len.data_ptr(),
+                                                     words.data_ptr(), out.data_ptr(), int(bool(exact)),
+                                                     current_stream_ptr()), "word_logprob_batch")
     return out
 
 

@@ -156,3 +156,23 @@ def _oracle_perm(model, h, w, perm):
                            np.zeros((len(perm), model.maxent_order), np.int64),
                            np.zeros(len(perm), np.int32), w, want_p=False)
     return out
+
+
+@pytest.mark.parametrize("V,H", [(20000, 256), (65536, 512)])
+def test_word_logprob_fast_mode_within_spec(V, H, torch):
+    """f32 lane-partial HS (used with the tensor-core modes): |d| <= 1e-5,
+    inside the north star's 1e-4."""
+    from paper_2007_11794_b200 import kernels, synth
+    from paper_2007_11794_b200.device import DeviceModel
+    from paper_2007_11794_b200.model import build_huffman_from_counts
+    model = synth.synth_model(V, H, 20)
+    tree = build_huffman_from_counts(synth.zipf_counts(V))
+    dm = DeviceModel(model, tree)
+    n = 4096
+    h, hist, hl, w = _queries(model, n, seed=V + 1)
+    want, _ = O.query_batch(model, tree, h, hist.astype(np.int64), hl, w, want_h=False)
+    ctx = torch.arange(n, dtype=torch.int32, device="cuda")
+    got = kernels.word_logprob_batch(dm, ctx, torch.from_numpy(h).cuda(), torch.from_numpy(hist).cuda(),
+                                     torch.from_numpy(hl).cuda(), torch.from_numpy(w).cuda(),
+                                     exact=False).cpu().numpy()
+    assert np.max(np.abs(got - want)) <= 1e-5
