@@ -113,19 +113,23 @@ __device__ __forceinline__ uint32_t tile_off(int row, int c) {
 }
 
 // MODE: 1 = TF32X3, 2 = BF16, 3 = TF32.
-// Warp-specialized S-stage ring (no block barrier inside the K loop):
-//   warps 0..3  loaders/converters: each thread cp.asyncs its share of the
-//               gathered fp32 A rows (raw) and of the pre-converted W slice
-//               (B, operand layout) for chunk k+S-1 (after empty[] says the
-//               stage's MMAs are done), cp.async.mbarrier.arrive on
-//               full_raw[]; then waits full_raw[k], converts its share of
-//               raw A to the operand layout (tf32 round / hi-lo split /
-//               bf16), fence.proxy.async, arrives on full_op[k]; at the end
-//               they are the epilogue (TMEM lane quadrant = warp);
-//   warp 4      MMA issuer (one lane): tcgen05.mma for chunk k, commit to
-//               empty[k % S] and, after the last chunk, to done.
-// Grid: (row tiles of 128, N tiles of bn columns).
-constexpr int WS_THREADS = 160;
+// Persistent, warp-specialized (the canonical sm_100 GEMM shape):
+//   warps 0..3  loaders/converters: stream K chunks of consecutive tiles
+//               through an S-stage ring without stopping at tile borders --
+//               cp.async of the gathered fp32 A rows (staged in the operand
+//               layout for tf32, raw for bf16) and of the pre-converted W
+//               slice, cp.async.mbarrier.arrive on full_raw[]; then convert
+//               in place (tf32 round, hi/lo split) or raw->bf16, arrive on
+//               full_op[];
+//   warp 4      MMA issuer: tcgen05.mma into one of two TMEM accumulators
+//               (tile parity), commit empty[stage] per chunk and tmem_full[]
+//               per tile;
+//   warps 5..8  epilogue: tcgen05.ld the finished accumulator (lane quadrant
+//               = warp % 4), + U[w], sigmoid, store h', content digest;
+//               release the accumulator (tmem_empty[]) so tile i+2 can start
+//               while tile i+1 is still in the MMA pipe.
+// Grid: persistent CTAs over tiles = (row tile of 128) x (N tile of bn).
+constexpr int WS_THREADS = 288;
 template <int MODE>
 __global__ void __launch_bounds__(WS_THREADS, 1)
 k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__ in_row,
@@ -142,18 +146,17 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     const uint32_t row_limit = rs.row_limit;
     const uint32_t n = rs.n_dev ? *rs.n_dev : n_cap;
     const uint32_t out0 = row_base(rs);
-    if (rs.cur && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) rs.cur->base = out0;
+    if (rs.cur && blockIdx.x == 0 && threadIdx.x == 0) rs.cur->base = out0;
     if ((uint64_t)out0 + n > row_limit) return;     // arena overflow (flagged by the HS stage)
-    const uint32_t q0 = blockIdx.x * BM;
-    if (q0 >= n) return;
-    const int n0 = blockIdx.y * bn;
     const int H = m.H;
+    const int n_pad = H > 256 ? (H + 31) / 32 * 32 : (H + 15) / 16 * 16;
+    const int n_tiles = (n_pad + bn - 1) / bn;
+    const uint32_t m_tiles = (n + BM - 1) / BM;
+    const uint32_t tiles = m_tiles * (uint32_t)n_tiles;
+    if (blockIdx.x >= tiles) return;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     extern __shared__ __align__(1024) uint8_t smem[];
-    // tf32 modes stage the fp32 A chunks directly in the operand layout and
-    // round them in place (x3 also writes the lo part); bf16 needs a raw
-    // fp32 staging area
     const uint32_t raw_bytes = BF ? BM * RAW_ROW : 0u;
     const uint32_t a_bytes = BM * KC_B;
     const uint32_t b_bytes = (uint32_t)bn * KC_B;
@@ -161,22 +164,20 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     uint64_t *full_raw = reinterpret_cast<uint64_t *>(smem + stages * stage_bytes);
     uint64_t *full_op = full_raw + stages;
     uint64_t *empty = full_op + stages;
-    uint64_t *done = empty + stages;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
-    __shared__ int32_t s_row[BM], s_w[BM];
+    uint64_t *tfull = empty + stages;                  // [2]
+    uint64_t *tempty = tfull + 2;                      // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
 
-    for (int t = tid; t < BM; t += WS_THREADS) {
-        const uint32_t q = q0 + t;
-        s_row[t] = q < n ? in_row[q] : -1;
-        s_w[t] = q < n ? (words ? words[q] : (int32_t)q) : 0;
-    }
     if (tid == 0) {
         for (int st = 0; st < stages; st++) {
             mbar_init(smem_u32(&full_raw[st]), 128);
             mbar_init(smem_u32(&full_op[st]), 128);
             mbar_init(smem_u32(&empty[st]), 1);
         }
-        mbar_init(smem_u32(done), 1);
+        for (int b2 = 0; b2 < 2; b2++) {
+            mbar_init(smem_u32(&tfull[b2]), 1);
+            mbar_init(smem_u32(&tempty[b2]), 128);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 4) {
@@ -192,55 +193,70 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     const int NK = (H + KE - 1) / KE;
     const uint32_t sbo = CH * 128, lbo = 128;
     const bool vec_ok = (H & 3) == 0;
+    const uint32_t my_tiles = (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const uint32_t total_chunks = my_tiles * (uint32_t)NK;
 
     if (warp == 4) {
         // ------------------------------ MMA issuer ----------------------------
         const uint32_t idesc = make_idesc(BF ? 1 : 2, bn);
-        for (int k = 0; k < NK; k++) {
-            const int st = k % stages;
-            mbar_wait(smem_u32(&full_op[st]), (uint32_t)((k / stages) & 1));
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        uint32_t g = 0;
+        for (uint32_t it = 0; it < my_tiles; it++) {
+            const uint32_t buf = it & 1;
+            if (it >= 2) mbar_wait(smem_u32(&tempty[buf]), (uint32_t)(((it >> 1) - 1) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if (lane == 0) {
-                uint8_t *base = smem + st * stage_bytes;
-                uint8_t *sA = base + raw_bytes;
-                uint8_t *sA2 = sA + a_bytes;
-                uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
-                uint8_t *sB2 = sB + b_bytes;
+            const uint32_t dacc = tmem + buf * (uint32_t)bn;
+            for (int k = 0; k < NK; k++, g++) {
+                const int st = (int)(g % stages);
+                mbar_wait(smem_u32(&full_op[st]), (uint32_t)((g / stages) & 1));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                if (lane == 0) {
+                    uint8_t *base = smem + st * stage_bytes;
+                    uint8_t *sA = base + raw_bytes;
+                    uint8_t *sA2 = sA + a_bytes;
+                    uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
+                    uint8_t *sB2 = sB + b_bytes;
 #pragma unroll
-                for (int ks = 0; ks < KC_B / 32; ks++) {     // 32 bytes of K per MMA
-                    const uint64_t a_hi = make_desc(smem_u32(sA) + ks * 2 * lbo, lbo, sbo);
-                    const uint64_t b_hi = make_desc(smem_u32(sB) + ks * 2 * lbo, lbo, sbo);
-                    const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
-                    mma<BF>(tmem, a_hi, b_hi, idesc, acc);
-                    if (X3) {
-                        const uint64_t a_lo = make_desc(smem_u32(sA2) + ks * 2 * lbo, lbo, sbo);
-                        const uint64_t b_lo = make_desc(smem_u32(sB2) + ks * 2 * lbo, lbo, sbo);
-                        mma<false>(tmem, a_hi, b_lo, idesc, 1u);
-                        mma<false>(tmem, a_lo, b_hi, idesc, 1u);
+                    for (int ks = 0; ks < KC_B / 32; ks++) {     // 32 bytes of K per MMA
+                        const uint64_t a_hi = make_desc(smem_u32(sA) + ks * 2 * lbo, lbo, sbo);
+                        const uint64_t b_hi = make_desc(smem_u32(sB) + ks * 2 * lbo, lbo, sbo);
+                        const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
+                        mma<BF>(dacc, a_hi, b_hi, idesc, acc);
+                        if (X3) {
+                            const uint64_t a_lo = make_desc(smem_u32(sA2) + ks * 2 * lbo, lbo, sbo);
+                            const uint64_t b_lo = make_desc(smem_u32(sB2) + ks * 2 * lbo, lbo, sbo);
+                            mma<false>(dacc, a_hi, b_lo, idesc, 1u);
+                            mma<false>(dacc, a_lo, b_hi, idesc, 1u);
+                        }
                     }
+                    commit(smem_u32(&empty[st]));
+                    if (k == NK - 1) commit(smem_u32(&tfull[buf]));
                 }
-                commit(smem_u32(&empty[st]));
-                if (k == NK - 1) commit(smem_u32(done));
+                __syncwarp();
             }
-            __syncwarp();
         }
-    } else {
+    } else if (warp < 4) {
         // ----------------------- loaders / converters -------------------------
-        auto issue = [&](int k) {
-            const int st = k % stages;
+        auto issue = [&](uint32_t gc) {
+            const uint32_t it = gc / NK;
+            const int k = (int)(gc - it * NK);
+            const uint32_t tile = blockIdx.x + it * gridDim.x;
+            const uint32_t q0 = (tile / n_tiles) * BM;
+            const int n0 = (int)(tile % n_tiles) * bn;
+            const int st = (int)(gc % stages);
             uint8_t *base = smem + st * stage_bytes;
             uint8_t *raw = base;
+            uint8_t *sAop = base + raw_bytes;
             uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
             const int k0 = k * KE;
-            uint8_t *sAop = base + raw_bytes;
             for (int idx = tid; idx < BM * RAW_CH; idx += 128) {
                 int row, c;
                 uint32_t off;
                 if (BF) { row = idx / RAW_CH; c = idx - row * RAW_CH; off = row * RAW_ROW + c * 16; }
-                else { const int r8 = idx & 7, g = idx / (8 * CH); c = (idx >> 3) % CH; row = g * 8 + r8; off = tile_off(row, c); }
+                else { const int r8 = idx & 7, g8 = idx / (8 * CH); c = (idx >> 3) % CH; row = g8 * 8 + r8; off = tile_off(row, c); }
                 uint8_t *dstb = BF ? raw : sAop;
-                const int src = s_row[row];
+                const uint32_t q = q0 + row;
+                const int src = q < n ? __ldg(in_row + q) : -1;
                 const int kk = k0 + c * 4;
                 const bool ok = src >= 0 && kk < H && vec_ok;
                 cp_async16(smem_u32(dstb + off),
@@ -251,8 +267,8 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                 }
             }
             for (int idx = tid; idx < bn * CH; idx += 128) {
-                const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
-                const int row = g * 8 + r8;
+                const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
+                const int row = g8 * 8 + r8;
                 const int wrow = n0 + row;
                 const int kk = k0 + c * (16 / ELT);
                 const bool ok = wrow < H && kk < H && vec_ok;
@@ -277,23 +293,23 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
             }
             asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" :: "r"(smem_u32(&full_raw[st])) : "memory");
         };
-        for (int k = 0; k < stages - 1 && k < NK; k++) issue(k);
-        for (int k = 0; k < NK; k++) {
-            const int st = k % stages;
-            const int kn = k + stages - 1;
-            if (kn < NK) {
-                // stage (kn % S) was last used by chunk k-1: wait for its MMAs
-                if (k >= 1) mbar_wait(smem_u32(&empty[(k - 1) % stages]), (uint32_t)(((k - 1) / stages) & 1));
-                issue(kn);
+        for (uint32_t gc = 0; gc < (uint32_t)(stages - 1) && gc < total_chunks; gc++) issue(gc);
+        for (uint32_t gc = 0; gc < total_chunks; gc++) {
+            const int st = (int)(gc % stages);
+            const uint32_t gn = gc + stages - 1;
+            if (gn < total_chunks) {
+                // stage (gn % S) was last used by chunk gc-1: wait for its MMAs
+                if (gc >= 1) mbar_wait(smem_u32(&empty[(gc - 1) % stages]), (uint32_t)(((gc - 1) / stages) & 1));
+                issue(gn);
             }
-            mbar_wait(smem_u32(&full_raw[st]), (uint32_t)((k / stages) & 1));
+            mbar_wait(smem_u32(&full_raw[st]), (uint32_t)((gc / stages) & 1));
             uint8_t *base = smem + st * stage_bytes;
             uint8_t *raw = base;
             uint8_t *sA = base + raw_bytes;
             uint8_t *sA2 = sA + a_bytes;
             for (int idx = tid; idx < BM * CH; idx += 128) {
-                const int r8 = idx & 7, c = (idx >> 3) % CH, g = idx / (8 * CH);
-                const int row = g * 8 + r8;
+                const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
+                const int row = g8 * 8 + r8;
                 const uint32_t off = tile_off(row, c);
                 if (BF) {
                     const float4 x0 = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 32);
@@ -320,48 +336,59 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&full_op[st])) : "memory");
         }
+    } else {
         // ------------------------------ epilogue ------------------------------
-        mbar_wait(smem_u32(done), 0u);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int row = warp * 32 + lane;                 // TMEM lane = row
-        const uint32_t q = q0 + row;
-        const bool valid = q < n;
-        unsigned long long dig = 0ull;
-        const float *urow = m.U + (size_t)s_w[row] * H;
-        float *orow = out_base + (size_t)(out0 + q) * H;
-        for (int c0 = 0; c0 < bn; c0 += 32) {
-            float v[32];
-            tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-            const int gc = n0 + c0;
-            if (valid) {
-                if (vec_ok && gc + 32 <= H) {
+        const int quad = warp & 3;                        // TMEM lanes 32*quad .. +31
+        const int row = quad * 32 + lane;
+        for (uint32_t it = 0; it < my_tiles; it++) {
+            const uint32_t buf = it & 1;
+            const uint32_t tile = blockIdx.x + it * gridDim.x;
+            const uint32_t q0 = (tile / n_tiles) * BM;
+            const int n0 = (int)(tile % n_tiles) * bn;
+            mbar_wait(smem_u32(&tfull[buf]), (uint32_t)((it >> 1) & 1));
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t q = q0 + row;
+            const bool valid = q < n;
+            const int wq = valid ? (words ? __ldg(words + q) : (int32_t)q) : 0;
+            unsigned long long dig = 0ull;
+            const float *urow = m.U + (size_t)wq * H;
+            float *orow = out_base + (size_t)(out0 + q) * H;
+            for (int c0 = 0; c0 < bn; c0 += 32) {
+                float v[32];
+                tmem_ld32(tmem + buf * (uint32_t)bn + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, v);
+                const int gc = n0 + c0;
+                if (valid) {
+                    if (vec_ok && gc + 32 <= H) {
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        float4 u = __ldg(reinterpret_cast<const float4 *>(urow + gc + j));
-                        float4 o;
-                        o.x = 1.f / (1.f + expf(-(v[j] + u.x)));
-                        o.y = 1.f / (1.f + expf(-(v[j + 1] + u.y)));
-                        o.z = 1.f / (1.f + expf(-(v[j + 2] + u.z)));
-                        o.w = 1.f / (1.f + expf(-(v[j + 3] + u.w)));
-                        *reinterpret_cast<float4 *>(orow + gc + j) = o;
-                        if (rs.dig) {
-                            dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o.x));
-                            dig += otf_hash64(((uint64_t)(gc + j + 1) << 32) ^ __float_as_uint(o.y));
-                            dig += otf_hash64(((uint64_t)(gc + j + 2) << 32) ^ __float_as_uint(o.z));
-                            dig += otf_hash64(((uint64_t)(gc + j + 3) << 32) ^ __float_as_uint(o.w));
+                        for (int j = 0; j < 32; j += 4) {
+                            float4 u = __ldg(reinterpret_cast<const float4 *>(urow + gc + j));
+                            float4 o;
+                            o.x = 1.f / (1.f + expf(-(v[j] + u.x)));
+                            o.y = 1.f / (1.f + expf(-(v[j + 1] + u.y)));
+                            o.z = 1.f / (1.f + expf(-(v[j + 2] + u.z)));
+                            o.w = 1.f / (1.f + expf(-(v[j + 3] + u.w)));
+                            *reinterpret_cast<float4 *>(orow + gc + j) = o;
+                            if (rs.dig) {
+                                dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o.x));
+                                dig += otf_hash64(((uint64_t)(gc + j + 1) << 32) ^ __float_as_uint(o.y));
+                                dig += otf_hash64(((uint64_t)(gc + j + 2) << 32) ^ __float_as_uint(o.z));
+                                dig += otf_hash64(((uint64_t)(gc + j + 3) << 32) ^ __float_as_uint(o.w));
+                            }
                         }
+                    } else {
+                        for (int j = 0; j < 32; j++)
+                            if (gc + j < H) {
+                                const float o = 1.f / (1.f + expf(-(v[j] + urow[gc + j])));
+                                orow[gc + j] = o;
+                                dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o));
+                            }
                     }
-                } else {
-                    for (int j = 0; j < 32; j++)
-                        if (gc + j < H) {
-                            const float o = 1.f / (1.f + expf(-(v[j] + urow[gc + j])));
-                            orow[gc + j] = o;
-                            dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o));
-                        }
                 }
             }
+            if (rs.dig && valid) atomicAdd(&rs.dig[q], dig);
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tempty[buf])) : "memory");
         }
-        if (rs.dig && valid) atomicAdd(&rs.dig[q], dig);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -387,7 +414,8 @@ static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const 
     while (bn > 32 && (uint64_t)m_tiles * ((n_pad + bn - 1) / bn) < 148) bn /= 2;
     bn = (bn + 15) / 16 * 16;
     uint32_t cols = 32;
-    while ((int)cols < bn) cols <<= 1;
+    while ((int)cols < 2 * bn) cols <<= 1;             // two accumulators
+    if (cols > 512) return -1;
     const bool x3 = prec == 1;
     const int ke = prec == 2 ? tc::KC_B / 2 : tc::KC_B / 4;
     const uint32_t raw_bytes = prec == 2 ? tc::BM * (ke * 4 + 16) : 0u;
@@ -398,13 +426,17 @@ static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const 
     int stages = (int)std::min<uint32_t>(8u, (200u * 1024u) / stage_bytes);
     if (4u * stage_bytes <= 110u * 1024u) stages = (int)std::min<uint32_t>(8u, (110u * 1024u) / stage_bytes);
     stages = std::max(2, std::min(stages, std::max(nk, 2)));
-    const size_t smem = (size_t)stages * stage_bytes + (3 * stages + 1) * 8 + 16 + 1024;
-    const dim3 grid(m_tiles, (n_pad + bn - 1) / bn);
+    const size_t smem = (size_t)stages * stage_bytes + (3 * stages + 4) * 8 + 16 + 1024;
+    const uint64_t tiles = (uint64_t)m_tiles * ((n_pad + bn - 1) / bn);
     cudaError_t e;
 #define TC_LAUNCH(MODE)                                                                         \
     do {                                                                                        \
         e = cudaFuncSetAttribute(tc::k_advance_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (e != cudaSuccess) return -9;                                                        \
+        int per_sm = 1;                                                                         \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc::k_advance_tc<MODE>, tc::WS_THREADS, smem); \
+        per_sm = std::max(1, std::min(per_sm, (int)(512 / cols)));                              \
+        const dim3 grid((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)148 * per_sm))); \
         tc::k_advance_tc<MODE><<<grid, tc::WS_THREADS, smem, s>>>(m, n_cap, rs, in_row, words, h_base, \
                                                                  out_base, row_limit, bn, stages, cols); \
     } while (0)
