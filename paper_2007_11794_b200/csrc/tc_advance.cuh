@@ -297,11 +297,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
         for (uint32_t gc = 0; gc < total_chunks; gc++) {
             const int st = (int)(gc % stages);
             const uint32_t gn = gc + stages - 1;
-            if (gn < total_chunks) {
-                // stage (gn % S) was last used by chunk gc-1: wait for its MMAs
-                if (gc >= 1) mbar_wait(smem_u32(&empty[(gc - 1) % stages]), (uint32_t)(((gc - 1) / stages) & 1));
-                issue(gn);
-            }
+            // convert chunk gc first, so its conversion overlaps MMA gc-1 ...
             mbar_wait(smem_u32(&full_raw[st]), (uint32_t)((gc / stages) & 1));
             uint8_t *base = smem + st * stage_bytes;
             uint8_t *raw = base;
@@ -335,6 +331,11 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&full_op[st])) : "memory");
+            // ... then refill the stage chunk gc-1 used, once its MMAs retired
+            if (gn < total_chunks) {
+                if (gc >= 1) mbar_wait(smem_u32(&empty[(gc - 1) % stages]), (uint32_t)(((gc - 1) / stages) & 1));
+                issue(gn);
+            }
         }
     } else {
         // ------------------------------ epilogue ------------------------------
