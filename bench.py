@@ -45,7 +45,9 @@ def parse():
     ap.add_argument("--n-utt", type=int, default=64)
     ap.add_argument("--frames", type=int, default=300)
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--groups", type=int, default=4, help="concurrent level chains per GPU")
+    ap.add_argument("--groups", type=int, default=4, help="concurrent level chains per GPU (level schedule)")
+    ap.add_argument("--schedule", default="auto", choices=["auto", "level", "stream"],
+                    help="decode schedule: persistent per-stream kernel or level-synchronous graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-queries", action="store_true", help="skip the config-d query microbench")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
@@ -242,7 +244,7 @@ def main():
     H = setup.model.hidden_size
     need = BatchDecoder.contexts_needed(setup.lattices, setup.beam)
     dec = BatchDecoder(setup.model, setup.tree, setup.small_lm, len(setup.lattices), need,
-                       precision=args.precision, n_groups=args.groups)
+                       precision=args.precision, n_groups=args.groups, schedule=args.schedule)
     dec.prepare(setup.lattices, setup.beam)
     stream = torch.cuda.current_stream()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > L2
@@ -292,7 +294,14 @@ def main():
     kinds = {k: v for k, v in prof.items() if v[1] > 0}
     dominant = max(kinds, key=lambda k: kinds[k][0])
     dom_ms, dom_n = kinds[dominant]
-    if dominant == "hs":
+    if dominant == "stream":
+        # persistent kernel: all algorithmic bytes of the path (HS rows +
+        # update rows 3 x 4H per miss + ~96 B of request / arrival state)
+        byt = hs_bytes + 12.0 * H * misses + 96.0 * requests
+        roof = {"kernel": "k_decode_streams (persistent: expand + tcgen05 update + HS + assign)",
+                "bound": "hbm", "achieved": byt / (dom_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                "tensor_tflops": adv_flops * (3 if args.precision == "tf32x3" else 1) / (dom_ms / 1e3) / 1e12}
+    elif dominant == "hs":
         roof = {"kernel": "k_hs_prim (HS + MaxEnt gather)", "bound": "hbm",
                 "achieved": hs_bytes / (dom_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}
     elif dominant == "advance":
@@ -308,6 +317,12 @@ def main():
     roof["launches"] = dom_n
     roof["avg_launch_us"] = dom_ms * 1e3 / max(dom_n, 1)
     kernel_ms = {k: round(v[0], 4) for k, v in prof.items() if v[1]}
+    phases = None
+    if dec.schedule == "stream":
+        ph = dec.plan.phase_ns()
+        n_lv = max(1, args.frames)
+        phases = {k: round(ph[k] / max(ph["ctas"], 1) / n_lv / 1e3, 3)
+                  for k in ("expand", "update_mma", "update_epilogue", "hs", "assign", "wait_full", "wait_empty")}
 
     # ---- end to end through the public API: host lattices in, 1-best out;
     # two different batches alternate (same compiled structure -> the plans
@@ -363,7 +378,8 @@ def main():
                                f"{args.n_utt} utterances x {args.frames} frames per GPU, breadth 3, "
                                "beam 8, per-utterance streams (retain=False)",
                    "n_utt_per_gpu": args.n_utt, "frames": args.frames, "beam": setup.beam,
-                   "precision": args.precision, "cuda_graph": use_graph,
+                   "precision": args.precision, "schedule": dec.schedule,
+                   "cuda_graph": use_graph and dec.schedule == "level",
                    "concurrent_groups": dec.n_groups,
                    "l2": "flushed (256 MB write) between timed iterations"},
         "rtf": (ms / 1e3) / (frames_per_step * FRAME_S) * (1 if world == 1 else 1),
@@ -371,6 +387,7 @@ def main():
         "queries_per_s": misses * world / (ms / 1e3),
         "requests_per_s": requests * world / (ms / 1e3),
         "kernel_ms_per_step": kernel_ms,
+        "stream_phase_us_per_level": phases,
         "roofline": roof,
         "e2e": {"value": frames_per_step * world / (e2e / 1e3), "unit": "frames/s",
                 "h2d_bytes_per_step": cnt["h2d_bytes"], "d2h_bytes_per_step": d2h,

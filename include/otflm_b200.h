@@ -46,6 +46,12 @@ extern "C" {
 #define OTFLM_PREC_BF16 2    /* tcgen05 kind::f16 with bf16 operands */
 #define OTFLM_PREC_TF32 3    /* tcgen05 kind::tf32, single pass */
 
+/* decode schedules (otflm_plan_set_schedule) */
+#define OTFLM_SCHED_LEVEL 0   /* level-synchronous: expand / HS || update / assign kernels per level
+                                 for the whole batch (CUDA graph); every precision */
+#define OTFLM_SCHED_STREAM 1  /* persistent: one CTA per utterance stream runs all of its levels in
+                                 one launch (TF32X3 / TF32, H % 4 == 0, H <= 512) */
+
 typedef struct OtflmModel OtflmModel;
 typedef struct OtflmNgram OtflmNgram;
 typedef struct OtflmStreams OtflmStreams;
@@ -208,18 +214,31 @@ int otflm_plan_info(const OtflmPlan *p, int64_t *out8);
 int otflm_plan_counters(const OtflmPlan *p, int64_t *out4, void *stream);
 /* One decode run captured as a CUDA graph with an event-record node around
  * every kernel; writes device-side total ms / launch counts per category
- * (6 entries: expand, hs, advance, assign, final, misc).  HS and the
- * recurrent update run as parallel graph branches, so their spans overlap. */
+ * (7 entries: expand, hs, advance, assign, final, misc, stream).  HS and the
+ * recurrent update run as parallel graph branches, so their spans overlap;
+ * the stream schedule reports its persistent kernel under "stream". */
 int otflm_decode_profile(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
                          void *stream, double *ms_out, int64_t *n_out);
 /* Device-only decode of a prepared plan (inputs already resident in HBM).
- * use_graph != 0 replays a captured CUDA graph of the level loop. */
+ * use_graph != 0 replays a captured CUDA graph of the level loop (level
+ * schedule; the stream schedule is three launches and ignores it). */
 int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
                      int32_t use_graph, void *stream);
 /* Concurrent groups: plans over disjoint utterances get disjoint arena row
  * partitions [start, end) and are replayed as parallel chains of one CUDA
  * graph (the per-frame stages of different groups overlap on the GPU). */
 int otflm_plan_set_arena(OtflmPlan *p, uint32_t start, uint32_t end);
+/* Select the decode schedule of a plan (OTFLM_SCHED_*); both produce the
+ * reference's results (rescore_onthefly, decoder.py:114-173) for every
+ * utterance.  otflm_schedule_supported returns 1 if the model / precision can
+ * run the schedule. */
+int otflm_plan_set_schedule(OtflmPlan *p, int32_t schedule);
+/* Stream schedule, after otflm_decode_profile: device time per phase summed
+ * over CTAs (ns) -- o[0] expand, o[1] recurrent-update K loop (loads + MMAs),
+ * o[2] update epilogue, o[3] HS, o[4] assign, o[5..6] 0, o[7] CTAs that
+ * reported (8 entries). */
+int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream);
+int otflm_schedule_supported(const OtflmModel *m, int32_t schedule, int32_t precision);
 int otflm_group_create(OtflmPlan **plans, int32_t n, OtflmGroup **out);
 int otflm_group_destroy(OtflmGroup *g);
 int otflm_group_run(OtflmGroup *g, const OtflmNgram *ng, double lm_weight, int32_t precision,

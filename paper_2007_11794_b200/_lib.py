@@ -20,7 +20,8 @@ ERR_VALUE, ERR_UNKNOWN_INDEX, ERR_TABLE_FULL, ERR_NO_PATH, ERR_KEY = -1, -2, -3,
 ERR_NOMEM, ERR_CYCLE, ERR_PACK, ERR_CUDA, ERR_HASH = -6, -7, -8, -9, -10
 
 PREC = {"fp64": 0, "tf32x3": 1, "bf16": 2, "tf32": 3}
-PROFILE_CATEGORIES = ("expand", "hs", "advance", "assign", "final", "misc")
+PROFILE_CATEGORIES = ("expand", "hs", "advance", "assign", "final", "misc", "stream")
+SCHED = {"level": 0, "stream": 1}
 
 
 class UnknownIndexError(KeyError):
@@ -118,6 +119,9 @@ _SIGS = {
     "otflm_plan_counters": (C.c_int, [_P, _P, _P]),
     "otflm_decode_profile": (C.c_int, [_P, _P, C.c_double, C.c_int32, _P, _P, _P]),
     "otflm_plan_set_arena": (C.c_int, [_P, C.c_uint32, C.c_uint32]),
+    "otflm_plan_set_schedule": (C.c_int, [_P, C.c_int32]),
+    "otflm_plan_phase_ns": (C.c_int, [_P, _P, _P]),
+    "otflm_schedule_supported": (C.c_int, [_P, C.c_int32, C.c_int32]),
     "otflm_group_create": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_void_p)]),
     "otflm_group_destroy": (C.c_int, [_P]),
     "otflm_group_run": (C.c_int, [_P, _P, C.c_double, C.c_int32, _P]),

@@ -15,6 +15,7 @@
 #include "decode.cuh"
 #include "hs.cuh"
 #include "tc_advance.cuh"
+#include "stream_decode.cuh"
 
 // --------------------------------------------------------------------------
 static thread_local std::string g_detail;
@@ -39,7 +40,7 @@ static thread_local int64_t g_launches = 0;
     } while (0)
 
 // ---- optional per-kernel CUDA-event timing (non-graph runs only) ----
-enum { K_EXPAND, K_HS, K_ADVANCE, K_ASSIGN, K_FINAL, K_MISC, K_NCAT };
+enum { K_EXPAND, K_HS, K_ADVANCE, K_ASSIGN, K_FINAL, K_MISC, K_STREAM, K_NCAT };
 static bool g_prof = false;
 static std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> g_prof_ev;
 static double g_prof_ms[K_NCAT];
@@ -113,6 +114,28 @@ __global__ void k_prep_weights(DevModel m, float *WT, float *W_hi, float *W_lo, 
     }
 }
 
+// W_hi / W_lo into the persistent kernel's chunked canonical tiles (see DevModel::W_t)
+__global__ void k_prep_wtiles(DevModel m, float *wt) {
+    const int H = m.H, np = m.wt_npad, kcb = m.wt_kcb, KE = kcb / 4;
+    const int NK = (H + KE - 1) / KE;
+    const int64_t total = (int64_t)NK * 2 * np * KE;
+    const int64_t blk = (int64_t)np * KE;                  // floats per [hi] or [lo] block
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int kk = (int)(t % KE);
+        const int row = (int)((t / KE) % np);
+        const int part = (int)((t / ((int64_t)KE * np)) % 2);
+        const int kc = (int)(t / ((int64_t)KE * np * 2));
+        const int k = kc * KE + kk;
+        float v = 0.f;
+        if (row < H && k < H) v = (part ? m.W_lo : m.W_hi)[(int64_t)row * H + k];
+        const int sh = kcb == 128 ? 0 : kcb == 64 ? 1 : 2;      // swizzled K-major (tc::swz_off)
+        const int64_t off = (int64_t)(kc * 2 + part) * blk +
+                            ((row >> 3) * (8 * kcb) + (row & 7) * kcb + ((((kk >> 2) ^ ((row & 7) >> sh))) << 4)) / 4 +
+                            (kk & 3);
+        wt[off] = v;
+    }
+}
+
 extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, OtflmModel **out) {
     if (!d || !out) return OTFLM_ERR_VALUE;
     if (d->hidden_size < 1 || d->vocab_size < 2 || d->maxent_order < 1 ||
@@ -159,9 +182,20 @@ extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, Otflm
     dm.U = U; dm.W = W; dm.WT = WT; dm.NV = NV; dm.ME = ME;
     dm.path_off = poff; dm.path_code = pcode;
     dm.W_hi = Whi; dm.W_lo = Wlo; dm.W_bf = Wbf;
+    dm.W_t = nullptr; dm.wt_kcb = 0; dm.wt_npad = 0;
     if (W) {
         k_prep_weights<<<256, 256>>>(dm, WT, Whi, Wlo, Wbf);
         CK(cudaGetLastError());
+        const int np = (H + 127) / 128 * 128;             // whole 128-row M tiles
+        if (np <= 512) {
+            const int kcb = np <= 256 ? 64 : 32, KE = kcb / 4, NK = (H + KE - 1) / KE;
+            float *Wt = nullptr;
+            const size_t nwt = (size_t)NK * 2 * np * KE;
+            if (m->mem.alloc(&Wt, nwt) != cudaSuccess) { m->mem.free_all(); delete m; g_detail = "cudaMalloc model"; return OTFLM_ERR_NOMEM; }
+            dm.W_t = Wt; dm.wt_kcb = kcb; dm.wt_npad = np;
+            k_prep_wtiles<<<256, 256>>>(dm, Wt);
+            CK(cudaGetLastError());
+        }
     }
     CK(cudaDeviceSynchronize());
     *out = m;
@@ -643,6 +677,9 @@ struct OtflmPlan {
     cudaStream_t chain = nullptr;              // this plan's chain inside a group graph
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_done = nullptr;
     std::vector<uint32_t> utt_stream_host;
+    int32_t schedule = OTFLM_SCHED_LEVEL;      // level-synchronous or persistent per-stream
+    uint32_t ws_cap = 0;                       // request / primary workspace entries
+    uint32_t ul_cap = 0;                       // UttLevel entries
     ~OtflmPlan() {
         if (side) cudaStreamDestroy(side);
         if (chain) cudaStreamDestroy(chain);
@@ -658,7 +695,8 @@ static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam,
                          std::vector<int32_t> &arc_word, std::vector<double> &arc_ac,
                          std::vector<double> &arc_slm, std::vector<uint32_t> &start_slot,
                          std::vector<uint32_t> &final_off, std::vector<uint32_t> &finals,
-                         std::vector<uint32_t> &utt_stream, std::vector<StreamRange> &ranges) {
+                         std::vector<uint32_t> &utt_stream, std::vector<StreamRange> &ranges,
+                         std::vector<UttLevel> &ul, std::vector<uint32_t> &ul_off, std::vector<uint32_t> &rq_off) {
     const int U = L->n_utt;
     std::vector<std::vector<std::vector<uint32_t>>> lv(U);   // per utt: levels -> global nodes
     uint64_t node_base = 0, slot_base = 0;
@@ -761,6 +799,7 @@ static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam,
     // request slots per node; one request range per (level, stream)
     size_t nlev = 0;
     for (int u = 0; u < U; u++) nlev = std::max(nlev, lv[u].size());
+    std::vector<std::vector<UttLevel>> ulv(U);
     p->lvl_node_off.assign(1, 0);
     p->lvl_range_off.assign(1, 0);
     p->lvl_req.clear();
@@ -770,13 +809,17 @@ static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam,
         for (int u = 0; u < U; u++) {
             if (t >= lv[u].size() || lv[u][t].empty()) continue;
             const uint64_t rb = run;
+            const uint32_t nb = (uint32_t)level_nodes.size();
             for (uint32_t g : lv[u][t]) {
                 NodeInfo &ni = nodes[g];
                 ni.req_base = (uint32_t)run;
                 run += (uint64_t)ni.keep * (ni.out_e - ni.out_b);
                 level_nodes.push_back(g);
             }
-            if (run > rb) ranges.push_back(StreamRange{utt_stream[u], (uint32_t)rb, (uint32_t)run, 0});
+            if (run > rb) {
+                ranges.push_back(StreamRange{utt_stream[u], (uint32_t)rb, (uint32_t)run, 0});
+                ulv[u].push_back(UttLevel{(uint32_t)t, nb, (uint32_t)level_nodes.size(), (uint32_t)rb, (uint32_t)run, 0, 0, 0});
+            }
         }
         if (run > 0xF0000000ull) { g_detail = "too many requests in one level"; return OTFLM_ERR_NOMEM; }
         p->lvl_node_off.push_back((uint32_t)level_nodes.size());
@@ -784,6 +827,17 @@ static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam,
         p->lvl_req.push_back((uint32_t)run);
         rmax = std::max(rmax, run);
         total += run;
+    }
+    // persistent schedule: levels per utterance, private workspace offsets
+    ul.clear(); ul_off.assign(1, 0); rq_off.assign(1, 0);
+    uint64_t ws = 0;
+    for (int u = 0; u < U; u++) {
+        uint32_t mx = 0;
+        for (const UttLevel &e : ulv[u]) { ul.push_back(e); mx = std::max(mx, e.re - e.rb); }
+        ul_off.push_back((uint32_t)ul.size());
+        ws += mx;
+        if (ws > 0xF0000000ull) { g_detail = "too many requests"; return OTFLM_ERR_NOMEM; }
+        rq_off.push_back((uint32_t)ws);
     }
     p->n_levels = (uint32_t)nlev;
     p->n_nodes = (uint32_t)node_base;
@@ -823,9 +877,10 @@ static int plan_alloc_workspace(OtflmPlan *p, uint32_t R, uint32_t n_lvl_slots) 
     bad |= p->mem.alloc(&d.pr_p, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.pr_dig, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.lvl, n_lvl_slots) != cudaSuccess;
-    bad |= p->mem.alloc(&p->alg_buf, 4) != cudaSuccess;
+    bad |= p->mem.alloc(&p->alg_buf, 16) != cudaSuccess;   // [0..3] work counters, [8..15] phase ns
     bad |= p->mem.alloc(&d.cursor, 1) != cudaSuccess;
     d.alg = nullptr;   // counters are only maintained in profiling runs
+    d.phase_ns = nullptr;
     d.arena_start = OTF_UNSET;
     d.arena_end = 0;
     if (bad) { g_detail = "cudaMalloc workspace"; return OTFLM_ERR_NOMEM; }
@@ -855,8 +910,10 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     std::vector<int32_t> arc_word;
     std::vector<double> arc_ac, arc_slm;
     std::vector<StreamRange> ranges;
+    std::vector<UttLevel> ul;
+    std::vector<uint32_t> ul_off, rq_off;
     int rc = compile_batch(p, L, beam, st->m->d.V, nodes, level_nodes, out_list, arc_slot, arc_word, arc_ac,
-                           arc_slm, start_slot, final_off, finals, utt_stream, ranges);
+                           arc_slm, start_slot, final_off, finals, utt_stream, ranges, ul, ul_off, rq_off);
     if (rc) { delete p; return rc; }
     {
         std::vector<uint32_t> seen(st->d.S, 0);
@@ -870,15 +927,22 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     DevPlan &d = p->d;
     NodeInfo *dn; uint32_t *dln, *dol, *das, *dss, *dus, *dfo, *dfi; int32_t *daw; double *dac, *dsl;
     StreamRange *drg;
+    UttLevel *dul; uint32_t *dulo, *drqo;
+    if (ul.empty()) ul.push_back(UttLevel{0, 0, 0, 0, 0, 0, 0, 0});   // keep the buffer non-empty
     g_upload_bytes = 0;
     if ((rc = upload(p->mem, &dn, nodes, s)) || (rc = upload(p->mem, &dln, level_nodes, s)) ||
         (rc = upload(p->mem, &dol, out_list, s)) || (rc = upload(p->mem, &das, arc_slot, s)) ||
         (rc = upload(p->mem, &daw, arc_word, s)) || (rc = upload(p->mem, &dac, arc_ac, s)) ||
         (rc = upload(p->mem, &dsl, arc_slm, s)) || (rc = upload(p->mem, &dss, start_slot, s)) ||
         (rc = upload(p->mem, &dus, utt_stream, s)) || (rc = upload(p->mem, &dfo, final_off, s)) ||
-        (rc = upload(p->mem, &dfi, finals, s)) || (rc = upload(p->mem, &drg, ranges, s))) {
+        (rc = upload(p->mem, &dfi, finals, s)) || (rc = upload(p->mem, &drg, ranges, s)) ||
+        (rc = upload(p->mem, &dul, ul, s)) || (rc = upload(p->mem, &dulo, ul_off, s)) ||
+        (rc = upload(p->mem, &drqo, rq_off, s))) {
         p->mem.free_all(); delete p; return rc;
     }
+    d.ul = dul; d.ul_off = dulo; d.rq_off = drqo;
+    p->ul_cap = (uint32_t)ul.size();
+    p->ws_cap = std::max(p->R_max, rq_off.back());
     d.nodes = dn; d.level_nodes = dln; d.out_list = dol; d.arc_slot = das; d.arc_word = daw;
     d.arc_ac = dac; d.arc_slm = dsl; d.n_utt = p->n_utt; d.utt_start_slot = dss; d.utt_stream = dus;
     d.final_off = dfo; d.finals = dfi; d.ranges = drg;
@@ -897,7 +961,7 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     bad |= p->mem.alloc(&d.out_end_ctx, p->n_utt) != cudaSuccess;
     bad |= p->mem.alloc(&d.out_expansions, p->n_utt) != cudaSuccess;
     if (bad) { p->mem.free_all(); delete p; g_detail = "cudaMalloc plan buffers"; return OTFLM_ERR_NOMEM; }
-    if ((rc = plan_alloc_workspace(p, p->R_max, p->n_levels + 1))) { p->mem.free_all(); delete p; return rc; }
+    if ((rc = plan_alloc_workspace(p, std::max<uint32_t>(p->ws_cap, 1), p->n_levels + 1))) { p->mem.free_all(); delete p; return rc; }
     *out = p;
     return OTFLM_OK;
 }
@@ -919,10 +983,14 @@ extern "C" int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *L, int3
     std::vector<int32_t> arc_word;
     std::vector<double> arc_ac, arc_slm;
     std::vector<StreamRange> ranges;
+    std::vector<UttLevel> ul;
+    std::vector<uint32_t> ul_off, rq_off;
     int rc = compile_batch(&tmp, L, p->beam, p->st->m->d.V, nodes, level_nodes, out_list, arc_slot, arc_word,
-                           arc_ac, arc_slm, start_slot, final_off, finals, utt_stream, ranges);
+                           arc_ac, arc_slm, start_slot, final_off, finals, utt_stream, ranges, ul, ul_off, rq_off);
     if (rc) return rc;
     if (ranges.empty()) ranges.push_back(StreamRange{0, 0, 0, 0});
+    if (ul.empty()) ul.push_back(UttLevel{0, 0, 0, 0, 0, 0, 0, 0});
+    if (ul.size() > p->ul_cap || rq_off.back() > p->ws_cap) return OTFLM_ERR_VALUE;
     if (tmp.n_levels != p->n_levels || tmp.n_nodes != p->n_nodes || tmp.n_arcs != p->n_arcs ||
         tmp.n_slots != p->n_slots || tmp.R_max != p->R_max || tmp.lvl_node_off != p->lvl_node_off ||
         tmp.lvl_req != p->lvl_req || tmp.lvl_range_off != p->lvl_range_off || utt_stream != p->utt_stream_host)
@@ -942,6 +1010,9 @@ extern "C" int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *L, int3
     CK(put(d.final_off, final_off.data(), final_off.size() * 4));
     CK(put(d.finals, finals.data(), finals.size() * 4));
     CK(put(d.ranges, ranges.data(), ranges.size() * sizeof(StreamRange)));
+    CK(put(d.ul, ul.data(), ul.size() * sizeof(UttLevel)));
+    CK(put(d.ul_off, ul_off.data(), ul_off.size() * 4));
+    CK(put(d.rq_off, rq_off.data(), rq_off.size() * 4));
     *same = 1;
     return OTFLM_OK;
 }
@@ -959,6 +1030,15 @@ extern "C" int otflm_plan_info(const OtflmPlan *p, int64_t *o) {
     if (!p || !o) return OTFLM_ERR_VALUE;
     o[0] = p->n_levels; o[1] = p->n_nodes; o[2] = p->n_arcs; o[3] = p->n_slots;
     o[4] = p->R_max; o[5] = (int64_t)p->total_req; o[6] = p->g_nodes; o[7] = p->n_utt;
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream) {
+    if (!p || !o) return OTFLM_ERR_VALUE;
+    unsigned long long a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    CK(cudaMemcpyAsync(a, p->alg_buf + 8, sizeof(a), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    for (int i = 0; i < 8; i++) o[i] = (int64_t)a[i];
     return OTFLM_OK;
 }
 
@@ -1048,6 +1128,84 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
     return OTFLM_OK;
 }
 
+// ---- persistent per-stream schedule (stream_decode.cuh) ----
+struct SdConfig { int stages, hs_warps; size_t smem; uint32_t tmem_cols; };
+static bool sd_config(const DevModel &m, int prec, SdConfig *c) {
+    if (!(prec == OTFLM_PREC_TF32X3 || prec == OTFLM_PREC_TF32)) return false;
+    if (!m.W_t || m.H % 4 != 0 || m.wt_npad > 512 || !m.U || !m.NV || !m.path_off) return false;
+    const bool x3 = prec == OTFLM_PREC_TF32X3;
+    const size_t stage = (x3 ? 2u : 1u) * ((size_t)m.wt_npad * m.wt_kcb + (size_t)tc::BM * m.wt_kcb);
+    const size_t budget = 200u * 1024u;
+    c->stages = (int)std::min<size_t>(4, budget / stage);
+    if (c->stages < 2) return false;
+    const size_t rb = (size_t)HS_NS * 4 * m.H;         // ring slots only (barriers are static)
+    c->hs_warps = (int)std::min<size_t>(sd::NW, budget / rb);
+    if (c->hs_warps < 1) return false;
+    c->smem = std::max((size_t)c->stages * stage, (size_t)c->hs_warps * rb);
+    c->tmem_cols = 128;
+    while ((int)c->tmem_cols < m.wt_npad) c->tmem_cols <<= 1;
+    return true;
+}
+
+static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, cudaStream_t s) {
+    const DevModel &m = p->st->m->d;
+    DevStreams &S = p->st->d;
+    DevPlan &d = p->d;
+    SdConfig c;
+    if (!sd_config(m, prec, &c)) { g_detail = "persistent schedule needs a TF32X3/TF32 precision and H % 4 == 0, H <= 512"; return OTFLM_ERR_VALUE; }
+    const bool part = d.arena_start != OTF_UNSET;
+    uint32_t *cursor = part ? d.cursor : S.arena_used;
+    const uint32_t limit = part ? d.arena_end : S.arena_rows;
+#define SD_LAUNCH(MODE, KCB, CPL, ORD)                                                                          \
+    do {                                                                                                        \
+        CK(cudaFuncSetAttribute(k_decode_streams<MODE, KCB, CPL, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem)); \
+        k_decode_streams<MODE, KCB, CPL, ORD><<<p->n_utt, sd::NT, c.smem, s>>>(m, d, S, g->d, (long long)p->beam, lm, \
+                                                                              c.stages, c.hs_warps, cursor, limit, c.tmem_cols); \
+    } while (0)
+#define SD_ORD(MODE, KCB, CPL) do { if (m.order <= 3) SD_LAUNCH(MODE, KCB, CPL, 3); else SD_LAUNCH(MODE, KCB, CPL, OTF_MAX_ORDER); } while (0)
+#define SD_H(MODE)                                                                                              \
+    do {                                                                                                        \
+        if (m.H <= 128) SD_ORD(MODE, 64, 1);                                                                    \
+        else if (m.H <= 256) SD_ORD(MODE, 64, 2);                                                               \
+        else SD_ORD(MODE, 32, 4);                                                                               \
+    } while (0)
+    if ((m.H <= 256 ? 64 : 32) != m.wt_kcb) { g_detail = "W tile layout mismatch"; return OTFLM_ERR_VALUE; }
+    if (prec == OTFLM_PREC_TF32X3) SD_H(1); else SD_H(3);
+#undef SD_H
+#undef SD_ORD
+#undef SD_LAUNCH
+    CKL();
+    return OTFLM_OK;
+}
+
+static int enqueue_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, cudaStream_t s) {
+    DevStreams &S = p->st->d;
+    DevPlan &d = p->d;
+    CK(cudaMemsetAsync(d.arr, 0xFF, (size_t)std::max<uint32_t>(p->n_slots, 1) * sizeof(Arrival), s));
+    if (d.alg) CK(cudaMemsetAsync(d.alg, 0, 16 * sizeof(unsigned long long), s));
+    { ProfScope ps(K_MISC, s); k_run_begin<<<cdiv(p->n_utt, 128), 128, 0, s>>>(d, S); CKL(); }
+    { ProfScope ps(K_STREAM, s); int rc = launch_streams(p, g, lm, prec, s); if (rc) return rc; }
+    { ProfScope ps(K_FINAL, s); k_final<<<cdiv(p->n_utt, 4), 128, 0, s>>>(d, S, lm, -1); CKL(); }
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_plan_set_schedule(OtflmPlan *p, int32_t schedule) {
+    if (!p || (schedule != OTFLM_SCHED_LEVEL && schedule != OTFLM_SCHED_STREAM)) return OTFLM_ERR_VALUE;
+    p->schedule = schedule;
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_schedule_supported(const OtflmModel *m, int32_t schedule, int32_t precision) {
+    if (!m) return 0;
+    if (schedule == OTFLM_SCHED_LEVEL) return precision >= 0 && precision <= 3;
+    SdConfig c;
+    return schedule == OTFLM_SCHED_STREAM && sd_config(m->d, precision, &c) ? 1 : 0;
+}
+
+static int enqueue_any(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, cudaStream_t s) {
+    return p->schedule == OTFLM_SCHED_STREAM ? enqueue_streams(p, g, lm, prec, s) : enqueue_run(p, g, lm, prec, s);
+}
+
 static int64_t g_last_launches = 0;
 
 extern "C" int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
@@ -1058,8 +1216,8 @@ extern "C" int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_wei
     if (g->d.V < p->st->m->d.V) { g_detail = "small LM vocabulary smaller than model"; return OTFLM_ERR_VALUE; }
     cudaStream_t s = (cudaStream_t)stream;
     g_launches = 0;
-    if (!use_graph) {
-        int rc = enqueue_run(p, g, lm_weight, precision, s);
+    if (!use_graph || p->schedule == OTFLM_SCHED_STREAM) {   // the persistent schedule is 3 launches
+        int rc = enqueue_any(p, g, lm_weight, precision, s);
         g_last_launches = g_launches;
         return rc;
     }
@@ -1100,8 +1258,10 @@ extern "C" int otflm_decode_profile(OtflmPlan *p, const OtflmNgram *g, double lm
     CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
     g_prof = true;
     p->d.alg = p->alg_buf;
-    int rc = enqueue_run(p, g, lm_weight, precision, cs);
+    p->d.phase_ns = p->alg_buf + 8;
+    int rc = enqueue_any(p, g, lm_weight, precision, cs);
     p->d.alg = nullptr;
+    p->d.phase_ns = nullptr;
     g_prof = false;
     cudaGraph_t graph;
     cudaError_t e = cudaStreamEndCapture(cs, &graph);
@@ -1318,7 +1478,7 @@ __global__ void k_probe_batch(DevPlan P, DevStreams S, uint32_t n, const uint32_
         P.rq_state[r] = st;
         need = st == RQ_PENDING || st == RQ_NOCACHE;
     }
-    compact_primary(P, S, &P.lvl[0], need, r, cc, ww, s);
+    compact_primary(P, S, &P.lvl[0].n_prim, need, r, cc, ww, s);
 }
 
 extern "C" int otflm_rnnlm_prob_batch(OtflmStreams *s, int64_t n, const int32_t *sid_h, const uint32_t *c_h,

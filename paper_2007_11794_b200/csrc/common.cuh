@@ -32,6 +32,12 @@ struct DevModel {
     const uint32_t *path_off, *path_code;
     const float *W_hi, *W_lo;          // tf32-rounded split of W (K-major rows)
     const __nv_bfloat16 *W_bf;         // bf16 copy of W
+    // W_hi / W_lo pre-tiled for the persistent stream kernel: per K chunk of
+    // wt_kcb bytes, [hi | lo] blocks of wt_npad rows (H rounded up to whole
+    // 128-row M tiles, zero padded) in the canonical no-swizzle K-major UMMA
+    // layout, so one bulk copy moves a whole chunk
+    const float *W_t;
+    int wt_kcb, wt_npad;
 };
 
 struct DevNgram {

@@ -32,6 +32,13 @@ struct StreamRange {         // requests of one stream inside one level
     uint32_t stream, rb, re, pad;
 };
 
+struct UttLevel {             // one (utterance, level) with requests (persistent schedule)
+    uint32_t t;               // level index (arrival ordering key)
+    uint32_t nb, ne;          // nodes: level_nodes[nb .. ne)
+    uint32_t rb, re;          // level-global request range of the utterance
+    uint32_t pad0, pad1, pad2;
+};
+
 struct DevPlan {
     // compiled lattice batch
     const NodeInfo *nodes;
@@ -68,6 +75,11 @@ struct DevPlan {
     uint32_t *cursor;             // arena cursor of a partitioned plan (concurrent groups)
     uint32_t arena_start, arena_end;   // partition [start, end), or start == OTF_UNSET
     unsigned long long *alg;      // profiling only: [0] sum P, [1] sum P*k, [2] HS queries
+    // persistent schedule: per utterance its levels ul[ul_off[u] .. ul_off[u+1])
+    // and the offset of its private request / primary workspace
+    const UttLevel *ul;
+    const uint32_t *ul_off, *rq_off;
+    unsigned long long *phase_ns;  // profiling only: [expand, update, hs, assign, CTAs]
 };
 
 // content digest term of element i of a hidden row / word j of the history
@@ -145,14 +157,14 @@ __device__ __forceinline__ uint32_t cache_probe(const DevStreams &S, uint32_t s,
 
 // warp-aggregated compaction of the requests that run the model this level
 // (all lanes of the warp call it)
-__device__ __forceinline__ void compact_primary(DevPlan &P, const DevStreams &S, LevelCtr *lc, bool need,
+__device__ __forceinline__ void compact_primary(DevPlan &P, const DevStreams &S, uint32_t *n_prim, bool need,
                                                 uint32_t r, uint32_t c, int32_t w, uint32_t s) {
     const unsigned bal = __ballot_sync(0xffffffffu, need);
     if (!bal) return;
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(bal) - 1;
     uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(&lc->n_prim, (uint32_t)__popc(bal));
+    if (lane == leader) base = atomicAdd(n_prim, (uint32_t)__popc(bal));
     base = __shfl_sync(0xffffffffu, base, leader);
     if (need) {
         const uint32_t m = base + __popc(bal & ((1u << lane) - 1u));
@@ -225,25 +237,22 @@ __device__ __forceinline__ bool ngram_logprob_dev(const DevNgram &g, const uint3
 // the (rank, arc) requests are spread over lanes so their cache probes and
 // small-LM lookups overlap.  Larger nodes (wide beams) take the general path
 // through the slot_win scratch.
-constexpr int EXP_WARPS = 8;
-__global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, DevNgram g, uint32_t node_begin,
-                                                uint32_t n_nodes, long long beam, uint32_t lvl) {
-    __shared__ uint32_t s_ctx[EXP_WARPS][32], s_slot[EXP_WARPS][32];
-    __shared__ double s_score[EXP_WARPS][32];
-    __shared__ uint32_t s_arc[EXP_WARPS][32];
-    const uint32_t wib = threadIdx.x >> 5;
-    const uint32_t gw = blockIdx.x * EXP_WARPS + wib;
-    const int lane = threadIdx.x & 31;
-    if (gw >= n_nodes) return;
-    LevelCtr *lc = &P.lvl[lvl];
-    const NodeInfo nd = P.nodes[P.level_nodes[node_begin + gw]];
+// One warp expands one node.  Request slots are nd.req_base + r_shift + j
+// (r_shift = 0: level-global indices; the persistent stream kernel passes
+// -rb so indices are local to its utterance's workspace).  s_* are this
+// warp's 32-entry token / arc tables in shared memory.
+__device__ __forceinline__ void expand_node(DevPlan &P, const DevStreams &S, const DevNgram &g,
+                                            const NodeInfo &nd, long long beam, uint32_t lvl, int64_t r_shift,
+                                            uint32_t *n_prim, uint32_t *s_ctx, uint32_t *s_slot, double *s_score,
+                                            uint32_t *s_arc, int lane) {
     const uint32_t outdeg = nd.out_e - nd.out_b;
+    const uint32_t rq0 = (uint32_t)((int64_t)nd.req_base + r_shift);
     if (nd.cap == 0 || outdeg == 0) {
-        for (uint32_t r = lane; r < nd.keep * outdeg; r += 32) P.rq_state[nd.req_base + r] = RQ_INVALID;
+        for (uint32_t r = lane; r < nd.keep * outdeg; r += 32) P.rq_state[rq0 + r] = RQ_INVALID;
         return;
     }
     // out-arcs of the node (arc-id order), staged once
-    for (uint32_t q = lane; q < outdeg && q < 32; q += 32) s_arc[wib][q] = P.out_list[nd.out_b + q];
+    for (uint32_t q = lane; q < outdeg && q < 32; q += 32) s_arc[q] = P.out_list[nd.out_b + q];
     uint32_t n_kept = 0;
     if (nd.cap <= 32) {
         Arrival ai;
@@ -268,9 +277,9 @@ __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, DevNgra
         }
         n_kept = (uint32_t)min((long long)__popc(wb), beam);
         if (win && rank < n_kept) {
-            s_ctx[wib][rank] = ci;
-            s_score[wib][rank] = si;
-            s_slot[wib][rank] = nd.slot_base + lane;
+            s_ctx[rank] = ci;
+            s_score[rank] = si;
+            s_slot[rank] = nd.slot_base + lane;
         }
     } else {
         // general path: O(cap^2 / 32) sweeps through the slot_win scratch;
@@ -321,14 +330,14 @@ __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, DevNgra
         if (emit) {
             const uint32_t rank = j / outdeg, q = j - rank * outdeg;
             if (fast) {
-                c = s_ctx[wib][rank]; sc = s_score[wib][rank]; s_tok = s_slot[wib][rank];
+                c = s_ctx[rank]; sc = s_score[rank]; s_tok = s_slot[rank];
             } else {
                 const uint4 tk = P.tok[nd.slot_base + rank];
                 c = tk.x; s_tok = tk.y;
                 sc = __longlong_as_double((long long)(((unsigned long long)tk.w << 32) | tk.z));
             }
-            const uint32_t a = (outdeg <= 32) ? s_arc[wib][q] : P.out_list[nd.out_b + q];
-            r = nd.req_base + j;
+            const uint32_t a = (outdeg <= 32) ? s_arc[q] : P.out_list[nd.out_b + q];
+            r = rq0 + j;
             w = P.arc_word[a];
             st = RQ_NOCACHE;
             uint32_t cslot = OTF_UNSET;
@@ -351,10 +360,24 @@ __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, DevNgra
             P.rq_cslot[r] = cslot;
             P.rq_state[r] = st;
         }
-        compact_primary(P, S, lc, emit && (st == RQ_PENDING || st == RQ_NOCACHE), r, c, w, nd.stream);
+        compact_primary(P, S, n_prim, emit && (st == RQ_PENDING || st == RQ_NOCACHE), r, c, w, nd.stream);
     }
     for (uint32_t r = n_kept * outdeg + lane; r < nd.keep * outdeg; r += 32)
-        P.rq_state[nd.req_base + r] = RQ_INVALID;
+        P.rq_state[rq0 + r] = RQ_INVALID;
+}
+
+constexpr int EXP_WARPS = 8;
+__global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, DevNgram g, uint32_t node_begin,
+                                                uint32_t n_nodes, long long beam, uint32_t lvl) {
+    __shared__ uint32_t s_ctx[EXP_WARPS][32], s_slot[EXP_WARPS][32];
+    __shared__ double s_score[EXP_WARPS][32];
+    __shared__ uint32_t s_arc[EXP_WARPS][32];
+    const uint32_t wib = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * EXP_WARPS + wib;
+    if (gw >= n_nodes) return;
+    const NodeInfo nd = P.nodes[P.level_nodes[node_begin + gw]];
+    expand_node(P, S, g, nd, beam, lvl, 0, &P.lvl[lvl].n_prim, s_ctx[wib], s_slot[wib], s_score[wib], s_arc[wib],
+                threadIdx.x & 31);
 }
 
 // --------------------------------------------------------------------------
@@ -457,26 +480,27 @@ __device__ __forceinline__ bool rows_equal_lane(const DevStreams &S, uint32_t ra
 // (cache claim = first occurrence, len+1 numbering of new contexts, dedup of
 // equal contexts created in the same level) are block-wide scans.
 constexpr int ASSIGN_T = 128;
-template <int MODE>
-__global__ void __launch_bounds__(ASSIGN_T) k_assign(DevPlan P, DevStreams S, uint32_t lvl, uint32_t range_begin,
-                                                     double lm_weight, double *out_p, uint32_t *out_cn,
-                                                     uint8_t *out_hit) {
-    __shared__ unsigned long long s_key[ASSIGN_T];
-    __shared__ uint32_t s_row[ASSIGN_T], s_cn[ASSIGN_T], s_wsum[ASSIGN_T / 32];
-    __shared__ uint32_t s_cnt[4];
+struct AssignSmem {           // per-thread scratch of assign_range (NTH entries)
+    unsigned long long *key;
+    uint32_t *row, *cn, *wsum, *cnt;
+};
+// Requests [rg.rb, rg.re) of one stream in one level, NTH threads of the CTA
+// (the reference order is the thread order inside each chunk of NTH).
+template <int MODE, int NTH>
+__device__ __forceinline__ void assign_range(DevPlan &P, const DevStreams &S, uint32_t lvl, const StreamRange &rg,
+                                             const LevelCtr &lc, uint32_t limit, double lm_weight, double *out_p,
+                                             uint32_t *out_cn, uint8_t *out_hit, const AssignSmem &sm) {
+    unsigned long long *s_key = sm.key;
+    uint32_t *s_row = sm.row, *s_cn = sm.cn, *s_wsum = sm.wsum, *s_cnt = sm.cnt;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const LevelCtr lc = P.lvl[lvl];
-    if (MODE == 1 && blockIdx.x == 0 && tid == 0) *S.arena_used = lc.base + lc.n_prim;
-    const uint32_t limit = P.arena_start == OTF_UNSET ? S.arena_rows : P.arena_end;
     if ((uint64_t)lc.base + lc.n_prim > limit) return;   // flagged by stage 2
-    const StreamRange rg = P.ranges[range_begin + blockIdx.x];
     const uint32_t s = rg.stream;
     const uint64_t kb = (uint64_t)s * S.kc_cap, cb = (uint64_t)s * S.ct_cap;
     const uint32_t cmask = S.ct_cap - 1;
     uint32_t tlen = S.table_len[s];
     if (tid < 4) s_cnt[tid] = 0;
     bool full = false;
-    for (uint32_t r0 = rg.rb; r0 < rg.re; r0 += ASSIGN_T) {
+    for (uint32_t r0 = rg.rb; r0 < rg.re; r0 += NTH) {
         const uint32_t r = r0 + tid;
         const bool in = r < rg.re;
         const uint8_t st = in ? P.rq_state[r] : (uint8_t)RQ_INVALID;
@@ -516,7 +540,7 @@ __global__ void __launch_bounds__(ASSIGN_T) k_assign(DevPlan P, DevStreams S, ui
         if (lane == 0) s_wsum[wid] = __popc(fb);
         __syncthreads();
         uint32_t before = __popc(fb & ((1u << lane) - 1u)), total = 0;
-        for (int w2 = 0; w2 < ASSIGN_T / 32; w2++) {
+        for (int w2 = 0; w2 < NTH / 32; w2++) {
             if (w2 < wid) before += s_wsum[w2];
             total += s_wsum[w2];
         }
@@ -578,6 +602,21 @@ __global__ void __launch_bounds__(ASSIGN_T) k_assign(DevPlan P, DevStreams S, ui
         stt[0] += look; stt[1] += look - miss; stt[2] += miss; stt[7] += look;
         if (S.enabled) stt[6] += miss;
     }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(ASSIGN_T) k_assign(DevPlan P, DevStreams S, uint32_t lvl, uint32_t range_begin,
+                                                     double lm_weight, double *out_p, uint32_t *out_cn,
+                                                     uint8_t *out_hit) {
+    __shared__ unsigned long long s_key[ASSIGN_T];
+    __shared__ uint32_t s_row[ASSIGN_T], s_cn[ASSIGN_T], s_wsum[ASSIGN_T / 32];
+    __shared__ uint32_t s_cnt[4];
+    const LevelCtr lc = P.lvl[lvl];
+    if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) *S.arena_used = lc.base + lc.n_prim;
+    const uint32_t limit = P.arena_start == OTF_UNSET ? S.arena_rows : P.arena_end;
+    const StreamRange rg = P.ranges[range_begin + blockIdx.x];
+    assign_range<MODE, ASSIGN_T>(P, S, lvl, rg, lc, limit, lm_weight, out_p, out_cn, out_hit,
+                                 AssignSmem{s_key, s_row, s_cn, s_wsum, s_cnt});
 }
 
 // --------------------------------------------------------------------------

@@ -17,6 +17,7 @@
 // in path order like the reference.
 #pragma once
 #include "common.cuh"
+#include <cstdio>
 
 #define HS_G 8
 
@@ -170,24 +171,31 @@ struct HsRing {
     uint32_t phase;          // bit s = parity to wait for on slot s
 };
 
+// Warp-collective: all lanes pass the same operands, one lane is elected
+// inside the asm (issuing under `if (lane == 0)` costs a per-lane R2UR loop).
+// The slot's previous contents were only read by this warp (ordered by the
+// __syncwarp before the refill), so no proxy fence is needed.
 __device__ __forceinline__ void ring_issue(HsRing &r, int slot, const float *src, uint32_t bytes) {
     const uint32_t bar = r.bar0 + slot * 8;
     const uint32_t dst = (uint32_t)__cvta_generic_to_shared(r.buf + (size_t)slot * bytes);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+    asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 t;\n\telect.sync t|e, 0xffffffff;\n\t"
+                 "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %3;\n\t"
+                 "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %3, [%1];\n\t}"
+                 :: "r"(dst), "r"(bar), "l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void ring_wait(HsRing &r, int slot) {
     const uint32_t bar = r.bar0 + slot * 8;
     const uint32_t par = (r.phase >> slot) & 1u;
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "WAITR_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONER_%=;\n\t"
-        "bra WAITR_%=;\n\t"
-        "DONER_%=:\n\t}" :: "r"(bar), "r"(par) : "memory");
+    for (uint32_t it = 0;; it++) {     // bounded: a lost copy traps instead of hanging
+        uint32_t ok;
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(bar), "r"(par) : "memory");
+        if (ok) break;
+        if (it == (1u << 22)) {
+            printf("hs ring: wait timeout block %d thread %d slot %d\n", (int)blockIdx.x, (int)threadIdx.x, slot);
+            __trap();
+        }
+    }
     r.phase ^= 1u << slot;
 }
 
@@ -206,16 +214,16 @@ __device__ __forceinline__ double hs_logprob_ring(const DevModel &m, HsRing &rin
     const int H = m.H;
     const int NCH = H >> 2;
     const uint32_t bytes = (uint32_t)H * 4u;
-    if (lane == 0)
-        for (uint32_t p = 0; p < P && p < HS_NS; p++)
-            ring_issue(ring, (int)p, m.NV + (size_t)(__ldg(codes + p) & 0x7FFFFFFFu) * H, bytes);
+    for (uint32_t p = 0; p < P && p < HS_NS; p++)
+        ring_issue(ring, (int)p, m.NV + (size_t)(__ldg(codes + p) & 0x7FFFFFFFu) * H, bytes);
     double hd[EXACT ? CPL : 1][4];
     float hf[EXACT ? 1 : CPL][4];
 #pragma unroll
     for (int c = 0; c < CPL; c++) {
         const int k = lane + 32 * c;
         float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (k < NCH) t = __ldg(reinterpret_cast<const float4 *>(h) + k);
+        // L2 load: h may have been written earlier in the same (persistent) kernel
+        if (k < NCH) t = __ldcg(reinterpret_cast<const float4 *>(h) + k);
         if (EXACT) {
             hd[EXACT ? c : 0][0] = widen(t.x); hd[EXACT ? c : 0][1] = widen(t.y);
             hd[EXACT ? c : 0][2] = widen(t.z); hd[EXACT ? c : 0][3] = widen(t.w);
@@ -286,7 +294,7 @@ __device__ __forceinline__ double hs_logprob_ring(const DevModel &m, HsRing &rin
                     acc[g] = ((double)f0 + (double)f1) + ((double)f2 + (double)f3);
                 }
                 __syncwarp();
-                if (lane == 0 && p + HS_NS < P)
+                if (p + HS_NS < P)
                     ring_issue(ring, slot, m.NV + (size_t)(__ldg(codes + p + HS_NS) & 0x7FFFFFFFu) * H, bytes);
             }
         }

@@ -26,7 +26,6 @@
 namespace tc {
 
 constexpr int BM = 128;      // rows per CTA tile (UMMA_M)
-constexpr int KC_B = 64;     // operand bytes of K per row per pipeline stage
 constexpr int NTHREADS = 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -40,6 +39,28 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
     d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
     d |= 1ull << 46;                 // descriptor version (sm_100)
     return d;                        // base_offset 0, lbo_mode 0, SWIZZLE_NONE
+}
+
+// Swizzled K-major operand tiles (rows of KC_B bytes, 8-row atoms of
+// 8*KC_B bytes, 16-byte chunk c of row r stored at chunk c ^ f(r)): the
+// tensor core reads 8-row core-matrix groups in parallel, and with the
+// unswizzled layout (groups SBO apart) those reads collide in the same banks.
+// KC_B = 128 / 64 / 32 -> SWIZZLE_128B / 64B / 32B.
+template <int KC_B>
+__host__ __device__ __forceinline__ uint32_t swz_off(int row, int c) {
+    constexpr int SH = KC_B == 128 ? 0 : KC_B == 64 ? 1 : 2;
+    return (uint32_t)((row >> 3) * (8 * KC_B) + (row & 7) * KC_B + ((c ^ ((row & 7) >> SH)) << 4));
+}
+template <int KC_B>
+__device__ __forceinline__ uint64_t make_desc_sw(uint32_t saddr) {
+    constexpr uint64_t LAYOUT = KC_B == 128 ? 2 : KC_B == 64 ? 4 : 6;
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+    d |= (uint64_t)1 << 16;                          // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(((8 * KC_B) >> 4) & 0x3FFFu) << 32;   // SBO: 8-row atom stride
+    d |= 1ull << 46;                                 // descriptor version (sm_100)
+    d |= LAYOUT << 61;
+    return d;
 }
 
 // instruction descriptor: D fp32, A/B K-major, M = 128, N = n
@@ -72,6 +93,31 @@ __device__ __forceinline__ void mma(uint32_t d_tmem, uint64_t a, uint64_t b, uin
                      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
                      :: "r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
     }
+}
+
+// Issue from a converged warp: every lane computes the (warp-uniform)
+// descriptors, one lane is elected inside the asm.  Issuing under
+// `if (lane == 0)` instead makes ptxas move the operands into uniform
+// registers through a per-lane R2UR loop -- ~176 cycles per MMA against ~70
+// (measured, tools/mma_micro.cu).
+template <bool BF16>
+__device__ __forceinline__ void mma_elect(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if (BF16) {
+        asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+                     "setp.ne.b32 p, %4, 0;\n\t"
+                     "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                     :: "r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    } else {
+        asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+                     "setp.ne.b32 p, %4, 0;\n\t"
+                     "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                     :: "r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+    }
+}
+__device__ __forceinline__ void commit_elect(uint32_t mbar) {
+    asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
+                 "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}"
+                 :: "r"(mbar) : "memory");
 }
 
 __device__ __forceinline__ void commit(uint32_t mbar) {
@@ -108,6 +154,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 }
 
 // smem offset of (row, 16-byte chunk c) inside a [rows x KC_B] operand tile
+template <int KC_B>
 __device__ __forceinline__ uint32_t tile_off(int row, int c) {
     return (uint32_t)((row >> 3) * (KC_B / 16 * 128) + c * 128 + (row & 7) * 16);
 }
@@ -130,11 +177,11 @@ __device__ __forceinline__ uint32_t tile_off(int row, int c) {
 //               while tile i+1 is still in the MMA pipe.
 // Grid: persistent CTAs over tiles = (row tile of 128) x (N tile of bn).
 constexpr int WS_THREADS = 288;
-template <int MODE>
+template <int MODE, int KC_B>
 __global__ void __launch_bounds__(WS_THREADS, 1)
 k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__ in_row,
              const int32_t *__restrict__ words, const float *__restrict__ h_base,
-             float *__restrict__ out_base, uint32_t row_limit_unused, int bn, int stages,
+             float *__restrict__ out_base, uint32_t row_limit_unused, int bn_max, int stages,
              uint32_t tmem_cols) {
     constexpr bool BF = MODE == 2;
     constexpr bool X3 = MODE == 1;
@@ -150,11 +197,16 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     if ((uint64_t)out0 + n > row_limit) return;     // arena overflow (flagged by the HS stage)
     const int H = m.H;
     const int n_pad = H > 256 ? (H + 31) / 32 * 32 : (H + 15) / 16 * 16;
-    const int n_tiles = (n_pad + bn - 1) / bn;
     const uint32_t m_tiles = (n + BM - 1) / BM;
+    // the row count is only known on the device: narrow the N tile while the
+    // tiles still fit one per CTA (smem ring and TMEM are sized for bn_max)
+    int bn = bn_max;
+    while (bn > 32 && (bn / 2) % 16 == 0 && m_tiles * (uint32_t)((n_pad + bn / 2 - 1) / (bn / 2)) <= gridDim.x) bn /= 2;
+    const int n_tiles = (n_pad + bn - 1) / bn;
     const uint32_t tiles = m_tiles * (uint32_t)n_tiles;
     if (blockIdx.x >= tiles) return;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);   // provably warp-uniform
 
     extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t raw_bytes = BF ? BM * RAW_ROW : 0u;
@@ -171,12 +223,12 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     if (tid == 0) {
         for (int st = 0; st < stages; st++) {
             mbar_init(smem_u32(&full_raw[st]), 128);
-            mbar_init(smem_u32(&full_op[st]), 128);
+            mbar_init(smem_u32(&full_op[st]), 4);          // one arrival per converter warp
             mbar_init(smem_u32(&empty[st]), 1);
         }
         for (int b2 = 0; b2 < 2; b2++) {
             mbar_init(smem_u32(&tfull[b2]), 1);
-            mbar_init(smem_u32(&tempty[b2]), 128);
+            mbar_init(smem_u32(&tempty[b2]), 4);           // one arrival per epilogue warp
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -210,7 +262,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                 mbar_wait(smem_u32(&full_op[st]), (uint32_t)((g / stages) & 1));
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                if (lane == 0) {
+                {
                     uint8_t *base = smem + st * stage_bytes;
                     uint8_t *sA = base + raw_bytes;
                     uint8_t *sA2 = sA + a_bytes;
@@ -221,16 +273,16 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                         const uint64_t a_hi = make_desc(smem_u32(sA) + ks * 2 * lbo, lbo, sbo);
                         const uint64_t b_hi = make_desc(smem_u32(sB) + ks * 2 * lbo, lbo, sbo);
                         const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
-                        mma<BF>(dacc, a_hi, b_hi, idesc, acc);
+                        mma_elect<BF>(dacc, a_hi, b_hi, idesc, acc);
                         if (X3) {
                             const uint64_t a_lo = make_desc(smem_u32(sA2) + ks * 2 * lbo, lbo, sbo);
                             const uint64_t b_lo = make_desc(smem_u32(sB2) + ks * 2 * lbo, lbo, sbo);
-                            mma<false>(dacc, a_hi, b_lo, idesc, 1u);
-                            mma<false>(dacc, a_lo, b_hi, idesc, 1u);
+                            mma_elect<false>(dacc, a_hi, b_lo, idesc, 1u);
+                            mma_elect<false>(dacc, a_lo, b_hi, idesc, 1u);
                         }
                     }
-                    commit(smem_u32(&empty[st]));
-                    if (k == NK - 1) commit(smem_u32(&tfull[buf]));
+                    commit_elect(smem_u32(&empty[st]));
+                    if (k == NK - 1) commit_elect(smem_u32(&tfull[buf]));
                 }
                 __syncwarp();
             }
@@ -253,7 +305,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                 int row, c;
                 uint32_t off;
                 if (BF) { row = idx / RAW_CH; c = idx - row * RAW_CH; off = row * RAW_ROW + c * 16; }
-                else { const int r8 = idx & 7, g8 = idx / (8 * CH); c = (idx >> 3) % CH; row = g8 * 8 + r8; off = tile_off(row, c); }
+                else { const int r8 = idx & 7, g8 = idx / (8 * CH); c = (idx >> 3) % CH; row = g8 * 8 + r8; off = tile_off<KC_B>(row, c); }
                 uint8_t *dstb = BF ? raw : sAop;
                 const uint32_t q = q0 + row;
                 const int src = q < n ? __ldg(in_row + q) : -1;
@@ -272,7 +324,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                 const int wrow = n0 + row;
                 const int kk = k0 + c * (16 / ELT);
                 const bool ok = wrow < H && kk < H && vec_ok;
-                const uint32_t off = tile_off(row, c);
+                const uint32_t off = tile_off<KC_B>(row, c);
                 if (BF) {
                     cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_bf + (size_t)wrow * H + kk) : (const void *)m.W_bf, ok);
                 } else {
@@ -306,7 +358,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
             for (int idx = tid; idx < BM * CH; idx += 128) {
                 const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
                 const int row = g8 * 8 + r8;
-                const uint32_t off = tile_off(row, c);
+                const uint32_t off = tile_off<KC_B>(row, c);
                 if (BF) {
                     const float4 x0 = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 32);
                     const float4 x1 = *reinterpret_cast<const float4 *>(raw + row * RAW_ROW + c * 32 + 16);
@@ -330,7 +382,9 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&full_op[st])) : "memory");
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&full_op[st])) : "memory");
             // ... then refill the stage chunk gc-1 used, once its MMAs retired
             if (gn < total_chunks) {
                 if (gc >= 1) mbar_wait(smem_u32(&empty[(gc - 1) % stages]), (uint32_t)(((gc - 1) / stages) & 1));
@@ -388,7 +442,9 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
             }
             if (rs.dig && valid) atomicAdd(&rs.dig[q], dig);
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tempty[buf])) : "memory");
+            __syncwarp();
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tempty[buf])) : "memory");
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -403,48 +459,47 @@ static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const 
                              const int32_t *in_row, const int32_t *words, const float *h_base,
                              float *out_base, uint32_t row_limit, cudaStream_t s) {
     const int H = m.H;
-    // N per MMA must be a multiple of 16 (M = 128) and <= 256; above 256 the
-    // N tile is issued as two MMAs, so pad to 32
     const int n_pad = H > 256 ? (H + 31) / 32 * 32 : (H + 15) / 16 * 16;
     if (n_pad > 512) return -1;
-    // N tile per CTA: capped so that >= 2 pipeline stages fit in shared
-    // memory, halved while there are too few row tiles to fill 148 SMs; a
-    // partial last N tile is zero-filled (rows >= H) and masked on store
     const uint32_t m_tiles = (n_cap + tc::BM - 1) / tc::BM;
-    int bn = std::min(std::min(n_pad, 256), prec == 1 ? 128 : 256);
-    while (bn > 32 && (uint64_t)m_tiles * ((n_pad + bn - 1) / bn) < 148) bn /= 2;
+    // Small problems (one decode level) are latency-bound: one tile per CTA,
+    // 128-byte K chunks (half the pipeline steps).  Large ones stream tiles
+    // through persistent CTAs with 64-byte chunks and deeper rings.
+    const bool small = m_tiles < 148;
+    int bn = std::min(std::min(n_pad, 256), prec == 1 ? 128 : 256);   // bn_max; the kernel narrows it
     bn = (bn + 15) / 16 * 16;
     uint32_t cols = 32;
     while ((int)cols < 2 * bn) cols <<= 1;             // two accumulators
     if (cols > 512) return -1;
     const bool x3 = prec == 1;
-    const int ke = prec == 2 ? tc::KC_B / 2 : tc::KC_B / 4;
+    const int kcb = small ? 128 : 64;
+    const int ke = prec == 2 ? kcb / 2 : kcb / 4;
     const uint32_t raw_bytes = prec == 2 ? tc::BM * (ke * 4 + 16) : 0u;
-    const uint32_t stage_bytes = raw_bytes + (x3 ? 2u : 1u) * (uint32_t)(tc::BM + bn) * tc::KC_B;
+    const uint32_t stage_bytes = raw_bytes + (x3 ? 2u : 1u) * (uint32_t)(tc::BM + bn) * kcb;
     const int nk = (H + ke - 1) / ke;
-    // two CTAs per SM (each <= 110 KB) when that still leaves >= 4 stages, so
-    // one CTA's epilogue / pipeline fill overlaps the other's main loop
     int stages = (int)std::min<uint32_t>(8u, (200u * 1024u) / stage_bytes);
-    if (4u * stage_bytes <= 110u * 1024u) stages = (int)std::min<uint32_t>(8u, (110u * 1024u) / stage_bytes);
+    if (!small && 4u * stage_bytes <= 110u * 1024u) stages = (int)std::min<uint32_t>(8u, (110u * 1024u) / stage_bytes);
     stages = std::max(2, std::min(stages, std::max(nk, 2)));
     const size_t smem = (size_t)stages * stage_bytes + (3 * stages + 4) * 8 + 16 + 1024;
-    const uint64_t tiles = (uint64_t)m_tiles * ((n_pad + bn - 1) / bn);
+    const uint64_t tiles = small ? (uint64_t)m_tiles * ((n_pad + 31) / 32)      // finest split
+                                 : (uint64_t)m_tiles * ((n_pad + bn - 1) / bn);
     cudaError_t e;
-#define TC_LAUNCH(MODE)                                                                         \
+#define TC_LAUNCH(MODE, KCB)                                                                    \
     do {                                                                                        \
-        e = cudaFuncSetAttribute(tc::k_advance_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        e = cudaFuncSetAttribute(tc::k_advance_tc<MODE, KCB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (e != cudaSuccess) return -9;                                                        \
         int per_sm = 1;                                                                         \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc::k_advance_tc<MODE>, tc::WS_THREADS, smem); \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc::k_advance_tc<MODE, KCB>, tc::WS_THREADS, smem); \
         per_sm = std::max(1, std::min(per_sm, (int)(512 / cols)));                              \
         const dim3 grid((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)148 * per_sm))); \
-        tc::k_advance_tc<MODE><<<grid, tc::WS_THREADS, smem, s>>>(m, n_cap, rs, in_row, words, h_base, \
-                                                                 out_base, row_limit, bn, stages, cols); \
+        tc::k_advance_tc<MODE, KCB><<<grid, tc::WS_THREADS, smem, s>>>(m, n_cap, rs, in_row, words, h_base, \
+                                                                        out_base, row_limit, bn, stages, cols); \
     } while (0)
-    if (prec == 1) TC_LAUNCH(1);
-    else if (prec == 2) TC_LAUNCH(2);
-    else if (prec == 3) TC_LAUNCH(3);
-    else return -1;
+    if (kcb == 128) {
+        if (prec == 1) TC_LAUNCH(1, 128); else if (prec == 2) TC_LAUNCH(2, 128); else if (prec == 3) TC_LAUNCH(3, 128); else return -1;
+    } else {
+        if (prec == 1) TC_LAUNCH(1, 64); else if (prec == 2) TC_LAUNCH(2, 64); else if (prec == 3) TC_LAUNCH(3, 64); else return -1;
+    }
 #undef TC_LAUNCH
     e = cudaGetLastError();
     return e == cudaSuccess ? 0 : -9;

@@ -246,6 +246,22 @@ class Plan:
     def set_arena(self, start: int, end: int) -> None:
         _lib.check(_lib.load().otflm_plan_set_arena(self.handle, int(start), int(end)), "arena")
 
+    def phase_ns(self) -> dict:
+        """Stream schedule, after ``profile``: device ns per phase summed over
+        CTAs (utterance streams)."""
+        o = np.zeros(8, np.int64)
+        _lib.check(_lib.load().otflm_plan_phase_ns(self.handle, o.ctypes.data, current_stream_ptr()),
+                   "phase_ns")
+        return {"expand": int(o[0]), "update_mma": int(o[1]), "update_epilogue": int(o[2]),
+                "hs": int(o[3]), "assign": int(o[4]), "wait_full": int(o[5]), "wait_empty": int(o[6]),
+                "ctas": int(o[7])}
+
+    def set_schedule(self, schedule: str) -> None:
+        """"level" (level-synchronous kernels, CUDA graph) or "stream"
+        (persistent kernel, one CTA per utterance stream)."""
+        _lib.check(_lib.load().otflm_plan_set_schedule(self.handle, _lib.SCHED[schedule]), "schedule")
+        self.schedule = schedule
+
     def counters(self) -> dict:
         out = np.zeros(4, np.int64)
         _lib.check(_lib.load().otflm_plan_counters(self.handle, _p(out), current_stream_ptr()),

@@ -340,12 +340,21 @@ class BatchDecoder:
     """
 
     def __init__(self, model, tree, small_lm, n_streams: int, max_contexts: int,
-                 enabled: bool = True, precision: str = "fp64", n_groups: int = 1):
+                 enabled: bool = True, precision: str = "fp64", n_groups: int = 1,
+                 schedule: str = "auto"):
         self.model, self.tree = model, tree
         self.dmodel = DeviceModel.get(model, tree)
         self.ngram = DeviceNgram.get(small_lm, self.dmodel)
         self.precision = precision
-        self.n_groups = max(1, min(int(n_groups), n_streams))
+        if schedule == "auto":
+            schedule = "stream" if schedule_supported(self.dmodel, "stream", precision) else "level"
+        if schedule not in _lib.SCHED:
+            raise ValueError(f"unknown schedule {schedule!r}")
+        if schedule == "stream" and not schedule_supported(self.dmodel, "stream", precision):
+            raise ValueError(f"the stream schedule does not support precision {precision!r} / this model")
+        self.schedule = schedule
+        # concurrent groups only help the level-synchronous schedule
+        self.n_groups = 1 if schedule == "stream" else max(1, min(int(n_groups), n_streams))
         self.arena_rows = n_streams * max_contexts + 2
         self.streams = DeviceStreams(self.dmodel, n_streams, enabled=enabled,
                                      max_contexts=max_contexts,
@@ -386,6 +395,7 @@ class BatchDecoder:
         for g in range(G):
             ids = np.arange(bounds[g], bounds[g + 1])
             p = Plan(self.streams, [lattices[i] for i in ids], beam, stream_ids=ids)
+            p.set_schedule(self.schedule)
             if G > 1:
                 p.set_arena(1 + g * rows, 1 + (g + 1) * rows)
             self.plans.append(p)
@@ -432,13 +442,19 @@ class BatchDecoder:
         return hyps, merged
 
 
+def schedule_supported(dmodel, schedule: str, precision: str) -> bool:
+    return bool(_lib.load().otflm_schedule_supported(dmodel.handle, _lib.SCHED[schedule],
+                                                     _lib.PREC[precision]))
+
+
 def rescore_batch(lattices: Sequence, small_lm, model, tree, lm_weight: float = 1.0,
                   beam: int = 8, precision: str = "fp64", enabled: bool = True,
-                  max_contexts: int | None = None):
+                  max_contexts: int | None = None, schedule: str = "auto"):
     """Many utterances, independent fresh streams (retain=False)."""
     if max_contexts is None:
         max_contexts = BatchDecoder.contexts_needed(lattices, beam)
-    dec = BatchDecoder(model, tree, small_lm, len(lattices), max_contexts, enabled, precision)
+    dec = BatchDecoder(model, tree, small_lm, len(lattices), max_contexts, enabled, precision,
+                       schedule=schedule)
     dec.prepare(lattices, beam)
     dec.run(lm_weight, use_graph=False)
     hyps, out = dec.fetch()

@@ -237,3 +237,69 @@ def test_errors_map_to_reference_exceptions(small):
                   smalllm=[-1.0])
     with pytest.raises(ValueError):
         rescore_onthefly(bad, gm.lm, st, beam=4)
+
+
+def _decode(s, precision, schedule, beam, enabled=True):
+    from paper_2007_11794_b200.rescore import BatchDecoder
+    need = BatchDecoder.contexts_needed(s.lattices, beam)
+    dec = BatchDecoder(s.model, s.tree, s.small_lm, len(s.lattices), need, enabled=enabled,
+                       precision=precision, schedule=schedule)
+    assert dec.schedule == schedule
+    dec.prepare(s.lattices, beam)
+    dec.run(1.0)
+    hyps, out = dec.fetch()
+    return hyps, out, dec.streams.stats()
+
+
+# (config, n_utt, frames, beam, cache): H = 64 and 256; cache off and a wide
+# beam push a level past one 128-row tile and one 512-request assign chunk
+STREAM_CASES = [("a", 12, 60, 8, True), ("a", 6, 30, 32, False), ("b", 4, 40, 8, True)]
+
+
+@pytest.mark.parametrize("case", STREAM_CASES)
+def test_stream_schedule_matches_level_schedule(case):
+    """The persistent per-stream kernel and the level-synchronous kernels in
+    TF32X3: same 1-best paths, expansions and cache lookups; scores within
+    the fp32 bound.  (The stream kernel puts W in the MMA A operand, so h'
+    can differ in the last f32 bit and the byte-exact content dedup may
+    merge a few contexts differently: table lengths agree to 0.5 %.)"""
+    from paper_2007_11794_b200 import synth
+    name, n_utt, T, beam, enabled = case
+    s = synth.build_setup(name, n_utt=n_utt, T=T, seed=5)
+    hl, ol, sl = _decode(s, "tf32x3", "level", beam, enabled)
+    hs, os_, ss = _decode(s, "tf32x3", "stream", beam, enabled)
+    assert np.array_equal(ol["expansions"], os_["expansions"])
+    assert np.array_equal(sl[:, 0], ss[:, 0])                      # lookups
+    assert np.all(np.abs(sl[:, 3] - ss[:, 3]) <= 0.005 * sl[:, 3] + 1)
+    for a, b in zip(hl, hs):
+        assert a.arcs == b.arcs
+        assert abs(a.combined_score - b.combined_score) <= 1e-4 * T
+
+
+@pytest.mark.parametrize("case", STREAM_CASES)
+def test_stream_schedule_tf32x3_matches_oracle(case):
+    """TF32X3 (fp32-faithful) stream decode vs the exact CPU oracle: same
+    1-best arcs, expansions and lookups; combined score within 1e-4 per
+    frame (north star: per-query log-probs within 1e-4)."""
+    from paper_2007_11794_b200 import synth
+    name, n_utt, T, beam, enabled = case
+    s = synth.build_setup(name, n_utt=n_utt, T=T, seed=5)
+    ref = O.decode_many(s.model, s.tree, s.small_lm, s.lattices, beam=beam, enabled=enabled, n_threads=4)
+    hyps, out, st = _decode(s, "tf32x3", "stream", beam, enabled)
+    for u, (r, (lk, hi, mi)) in enumerate(ref):
+        assert hyps[u].arcs == r.arcs
+        assert abs(hyps[u].combined_score - r.combined_score) <= 1e-4 * T
+        assert int(out["expansions"][u]) == r.expansions
+    assert [int(x) for x in st[:, 0]] == [x[1][0] for x in ref]
+
+
+def test_stream_schedule_tf32_single_pass():
+    """Single-pass TF32 (the looser mode): runs the same traversal; scores
+    within 2e-3 per frame of the oracle."""
+    from paper_2007_11794_b200 import synth
+    s = synth.build_setup("a", n_utt=6, T=40, seed=5)
+    ref = O.decode_many(s.model, s.tree, s.small_lm, s.lattices, beam=8, n_threads=4)
+    hyps, out, st = _decode(s, "tf32", "stream", 8)
+    for u, (r, _) in enumerate(ref):
+        assert abs(hyps[u].combined_score - r.combined_score) <= 2e-3 * 40
+        assert int(out["expansions"][u]) == r.expansions

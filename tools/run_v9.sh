@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 300 python bench.py --steps 5 --warmup 3 --schedule stream --no-cpu-baseline --no-queries > gpurun_out/bench_v9_stream.jsonl 2>gpurun_out/bench_v9_stream.err; echo bs=$?
+tail -3 gpurun_out/bench_v9_stream.err
