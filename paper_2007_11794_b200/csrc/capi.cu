@@ -1129,7 +1129,7 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
 }
 
 // ---- persistent per-stream schedule (stream_decode.cuh) ----
-struct SdConfig { int stages, hs_warps; size_t smem; uint32_t tmem_cols; };
+struct SdConfig { int stages, qb_max; size_t smem; uint32_t tmem_cols; };
 static bool sd_config(const DevModel &m, int prec, SdConfig *c) {
     if (!(prec == OTFLM_PREC_TF32X3 || prec == OTFLM_PREC_TF32)) return false;
     if (!m.W_t || m.H % 4 != 0 || m.wt_npad > 512 || !m.U || !m.NV || !m.path_off) return false;
@@ -1138,10 +1138,11 @@ static bool sd_config(const DevModel &m, int prec, SdConfig *c) {
     const size_t budget = 200u * 1024u;
     c->stages = (int)std::min<size_t>(4, budget / stage);
     if (c->stages < 2) return false;
-    const size_t rb = (size_t)HS_NS * 4 * m.H;         // ring slots only (barriers are static)
-    c->hs_warps = (int)std::min<size_t>(sd::NW, budget / rb);
-    if (c->hs_warps < 1) return false;
-    c->smem = std::max((size_t)c->stages * stage, (size_t)c->hs_warps * rb);
+    // node-parallel HS scratch beyond the context rows (hs_level_nodepar)
+    const size_t hs_fixed = (size_t)sd::PAIRCAP * 13 + (size_t)sd::QMAX * (OTF_MAX_ORDER * 8 + 7 * 4) + (sd::NW + 2) * 4 + 64;
+    c->smem = std::max((size_t)c->stages * stage, hs_fixed + 32 * 4 * (size_t)m.H);
+    c->qb_max = (int)std::min<size_t>(sd::QMAX, (c->smem - hs_fixed) / (4 * (size_t)m.H));
+    if (c->qb_max < 1 || c->smem > budget) return false;
     c->tmem_cols = 128;
     while ((int)c->tmem_cols < m.wt_npad) c->tmem_cols <<= 1;
     return true;
@@ -1160,7 +1161,7 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
     do {                                                                                                        \
         CK(cudaFuncSetAttribute(k_decode_streams<MODE, KCB, CPL, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem)); \
         k_decode_streams<MODE, KCB, CPL, ORD><<<p->n_utt, sd::NT, c.smem, s>>>(m, d, S, g->d, (long long)p->beam, lm, \
-                                                                              c.stages, c.hs_warps, cursor, limit, c.tmem_cols); \
+                                                                              c.stages, c.qb_max, cursor, limit, c.tmem_cols); \
     } while (0)
 #define SD_ORD(MODE, KCB, CPL) do { if (m.order <= 3) SD_LAUNCH(MODE, KCB, CPL, 3); else SD_LAUNCH(MODE, KCB, CPL, OTF_MAX_ORDER); } while (0)
 #define SD_H(MODE)                                                                                              \

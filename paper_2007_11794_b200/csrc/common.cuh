@@ -119,9 +119,11 @@ __device__ __forceinline__ uint64_t otf_hash64(uint64_t x) {
     return x;
 }
 
-// _kernels_nb.py:36-48 in float64 (CUDA libdevice exp/log1p, <= 1 ulp)
+// _kernels_nb.py:36-48 in float64 (CUDA libdevice exp/log1p, <= 1 ulp).
+// Branch-free form of x >= 0 ? -log1p(exp(-x)) : x - log1p(exp(x)): the same
+// value for every x (up to the sign of a zero result), without divergence.
 __device__ __forceinline__ double otf_log_sigmoid(double x) {
-    return x >= 0.0 ? -log1p(exp(-x)) : x - log1p(exp(x));
+    return fmin(x, 0.0) - log1p(exp(-fabs(x)));
 }
 __device__ __forceinline__ double otf_sigmoid(double x) {
     if (x >= 0.0) return 1.0 / (1.0 + exp(-x));

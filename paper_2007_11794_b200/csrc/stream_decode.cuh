@@ -21,9 +21,9 @@
 //            cp.async and are split into tf32 hi/lo in place; an S-stage ring
 //            overlaps loads, conversion and MMAs; accumulators in TMEM
 //            (lane = output unit, column = row), epilogue by all 16 warps;
-//   HS       warp per computed request over the TMA bulk-copy ring
-//            (hs_logprob_ring, shared with k_hs_prim_ring), in the same shared
-//            memory the update's ring used;
+//   HS       node-parallel over the level's (query, path node) pairs
+//            (hs_level_nodepar): context rows staged in the shared memory the
+//            update's ring used, 8 pairs per warp round, path-order sums;
 //   assign   assign_range (shared with k_assign) over the stream's requests
 //            in reference order with the whole CTA.
 // Tensor-core precisions only (TF32X3 / TF32); FP64 exact mode and BF16 use
@@ -49,18 +49,28 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
 }
 
 // Bounded mbarrier wait: a protocol error traps (and reports where) instead
-// of hanging the GPU.  2^22 polls is well over a second, orders of magnitude above any
+// of hanging the GPU after 2 s of wall time, orders of magnitude above any
 // legitimate wait in this kernel.
+__device__ __forceinline__ unsigned long long gtimer_() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ void wait_bounded(uint32_t bar, uint32_t parity, int tag) {
+    unsigned long long t0 = 0;
     for (uint32_t it = 0;; it++) {
         uint32_t ok;
         asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                      "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
         if (ok) return;
-        if (it == (1u << 22)) {
-            printf("k_decode_streams: wait timeout block %d thread %d tag %d parity %u\n", (int)blockIdx.x,
-                   (int)threadIdx.x, tag, parity);
-            __trap();
+        if ((it & 1023u) == 0) {                   // wall-clock bound: 2 s
+            const unsigned long long t = gtimer_();
+            if (it == 0) t0 = t;
+            else if (t - t0 > 2000000000ull) {
+                printf("k_decode_streams: wait timeout block %d thread %d tag %d parity %u\n", (int)blockIdx.x,
+                       (int)threadIdx.x, tag, parity);
+                __trap();
+            }
         }
     }
 }
@@ -87,11 +97,201 @@ __device__ __forceinline__ unsigned long long transpose_sum32(unsigned long long
 }
 }  // namespace sd
 
+// --------------------------------------------------------------------------
+// Node-parallel HS + MaxEnt for one level of one stream (fast mode: f32 lane
+// partials, float64 from the lane combine on -- the same arithmetic, in the
+// same order, as hs_logprob_ring<CPL, false, ORD>, so both schedules agree
+// bit for bit).  Queries are few per stream-level (~70) and each is a
+// dependent chain of ~10 node rows, so instead of a warp per query the
+// (query, path node) pairs of a batch are spread over all warps, 8 per warp
+// round with all row loads in flight; the context rows live in shared memory
+// and each pair's log-sigmoid goes to a per-pair slot, summed per query in
+// path order afterwards.
+// --------------------------------------------------------------------------
+namespace sd {
+constexpr int PAIRCAP = 4096;      // (query, node) pairs per batch
+constexpr int QMAX = 128;          // queries per batch (upper bound)
+struct HsLevelSmem {
+    float *h;                      // [qb][H] context rows
+    double *lsig;                  // [PAIRCAP] activation, then log-sigmoid, per pair
+    uint32_t *pcode;               // [PAIRCAP] path code of each pair
+    uint8_t *pq;                   // [PAIRCAP] batch query of each pair
+    unsigned long long *pre;       // [QMAX][ORD] MaxEnt hash prefixes
+    uint32_t *row, *cb, *off, *P;  // [QMAX] arena row, path code base, pair offset, path length
+    int32_t *w, *kmax, *L;         // [QMAX]
+    uint32_t *scan;                // [NW + 2]
+};
+}  // namespace sd
+
+template <int CPL, int ORD>
+__device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, DevStreams &S, uint32_t base,
+                                                 uint32_t n, const sd::HsLevelSmem &hs, int qb_max, int tid,
+                                                 int wid, int lane) {
+    constexpr int NT = sd::NT, NW = sd::NW;
+    const int H = m.H, NCH = H >> 2;
+    for (uint32_t q0 = 0; q0 < n;) {
+        const int nq = (int)min((uint32_t)qb_max, n - q0);
+        // ---- A: per-query setup (thread per query), pair offsets ----
+        uint32_t Pt = 0;
+        if (tid < nq) {
+            const uint32_t q = q0 + tid;
+            const uint32_t row = (uint32_t)Q.pr_inrow[q];
+            const uint32_t *meta = S.arena_meta + (size_t)row * OTF_META;
+            const int L = (int)meta[0];
+            const int w = Q.pr_w[q];
+            const uint32_t o0 = __ldg(m.path_off + w), o1 = __ldg(m.path_off + w + 1);
+            const int kmax = m.order < L ? m.order : L;
+#pragma unroll
+            for (int k = 0; k < ORD; k++) {
+                uint64_t x = 0;
+                if (k < kmax) {
+                    x = otf_mix(m.seed, (uint64_t)(k + 1));
+                    for (int i = L - (k + 1); i < L; i++) x = otf_mix(x, (uint64_t)meta[1 + i]);
+                }
+                hs.pre[tid * ORD + k] = x;
+            }
+            Pt = o1 - o0;
+            hs.row[tid] = row; hs.cb[tid] = o0; hs.P[tid] = Pt; hs.w[tid] = w; hs.kmax[tid] = kmax; hs.L[tid] = L;
+        }
+        // exclusive scan of P over the batch (threads 0..nq-1 live in warps 0..3)
+        uint32_t inc = Pt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+        }
+        if (lane == 31) hs.scan[wid] = inc;
+        __syncthreads();
+        uint32_t before = 0;
+        for (int w2 = 0; w2 < wid; w2++) before += hs.scan[w2];
+        const uint32_t excl = before + inc - Pt;
+        if (tid < nq) hs.off[tid] = excl;
+        __syncthreads();
+        // batch = the leading queries whose pairs fit PAIRCAP (offsets are monotone)
+        if (tid == 0) {
+            int lo = 0, hi = nq;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (hs.off[mid - 1] + hs.P[mid - 1] <= (uint32_t)sd::PAIRCAP) lo = mid; else hi = mid - 1;
+            }
+            if (lo == 0) { atomicOr(S.err, OTF_E_VALUE); lo = 1; }   // one path longer than PAIRCAP
+            hs.scan[NW] = (uint32_t)lo;
+        }
+        __syncthreads();
+        const int nb = (int)hs.scan[NW];
+        const uint32_t T = min(hs.off[nb - 1] + hs.P[nb - 1], (uint32_t)sd::PAIRCAP);
+        // pair -> query map and the context rows
+        for (int t = wid; t < nb; t += NW) {
+            const uint32_t o = hs.off[t], p = hs.P[t], cb = hs.cb[t];
+            for (uint32_t i = lane; i < p && o + i < (uint32_t)sd::PAIRCAP; i += 32) {
+                hs.pq[o + i] = (uint8_t)t;
+                hs.pcode[o + i] = __ldg(m.path_code + cb + i);
+            }
+        }
+        for (int i = tid; i < nb * NCH; i += NT) {
+            const int t = i / NCH, c = i - t * NCH;
+            reinterpret_cast<float4 *>(hs.h)[(size_t)t * NCH + c] =
+                __ldcg(reinterpret_cast<const float4 *>(S.arena_h + (size_t)hs.row[t] * H) + c);
+        }
+        __syncthreads();
+        // ---- B: 8 pairs per warp round ----
+        const int my_g = node_of_lane(lane);
+        const bool leader = (lane & 3) == 0;
+        for (uint32_t j0 = (uint32_t)wid * HS_G; j0 < T; j0 += (uint32_t)NW * HS_G) {
+            uint32_t code[HS_G];
+            int qt[HS_G];
+#pragma unroll
+            for (int g = 0; g < HS_G; g++) {
+                const uint32_t j = j0 + g;
+                qt[g] = j < T ? (int)hs.pq[j] : 0;
+                code[g] = j < T ? hs.pcode[j] : OTF_UNSET;
+            }
+            // MaxEnt terms of this lane's node (leaders), issued before the rows
+            const uint32_t mycode = code[my_g];
+            const int myq = qt[my_g];
+            const int kmax = hs.kmax[myq];
+            double me[ORD];
+#pragma unroll
+            for (int k = 0; k < ORD; k++) {
+                me[k] = 0.0;
+                if (leader && k < kmax && mycode != OTF_UNSET)
+                    me[k] = (double)__ldg(m.ME + (otf_mix(hs.pre[myq * ORD + k], (uint64_t)(mycode & 0x7FFFFFFFu)) & m.mask));
+            }
+            double acc[HS_G];
+#pragma unroll
+            for (int g = 0; g < HS_G; g++) {
+                acc[g] = 0.0;
+                if (code[g] != OTF_UNSET) {
+                    const float4 *row = reinterpret_cast<const float4 *>(m.NV + (size_t)(code[g] & 0x7FFFFFFFu) * H);
+                    const float4 *hv = reinterpret_cast<const float4 *>(hs.h + (size_t)qt[g] * H);
+                    float f0 = 0.f, f1 = 0.f, f2 = 0.f, f3 = 0.f;
+#pragma unroll
+                    for (int c = 0; c < CPL; c++) {
+                        const int k = lane + 32 * c;
+                        if (k < NCH) {
+                            const float4 t = __ldg(row + k);
+                            const float4 h4 = hv[k];
+                            f0 = fmaf(t.x, h4.x, f0);
+                            f1 = fmaf(t.y, h4.y, f1);
+                            f2 = fmaf(t.z, h4.z, f2);
+                            f3 = fmaf(t.w, h4.w, f3);
+                        }
+                    }
+                    acc[g] = ((double)f0 + (double)f1) + ((double)f2 + (double)f3);
+                }
+            }
+            double a = reduce8(acc, lane);
+#pragma unroll
+            for (int k = 0; k < ORD; k++) if (k < kmax) a += me[k];
+            if (leader && mycode != OTF_UNSET) hs.lsig[j0 + my_g] = (mycode & 0x80000000u) ? -a : a;
+        }
+        __syncthreads();
+        // log-sigmoid once per pair with every lane busy (f64, libdevice)
+        for (uint32_t j = (uint32_t)tid; j < T; j += NT) hs.lsig[j] = otf_log_sigmoid(hs.lsig[j]);
+        __syncthreads();
+        // ---- C: per query: path-order sum, successor history, digest ----
+        // thread per query: path-order sum, successor history (rnnlm.py:187),
+        // its digest terms (same values as hs_prim_finish)
+        if (tid < nb) {
+            const int t = tid;
+            const uint32_t q = q0 + (uint32_t)t;
+            const uint32_t o = hs.off[t], p = hs.P[t];
+            double lp = 0.0;
+            for (uint32_t i = 0; i < p; i++) lp += hs.lsig[o + i];
+            const uint32_t *meta = S.arena_meta + (size_t)hs.row[t] * OTF_META;
+            const int L = hs.L[t];
+            const int nl = L + 1 > m.order ? m.order : L + 1;
+            const int drop = L + 1 - nl;
+            uint32_t *dst = S.arena_meta + (size_t)(base + q) * OTF_META;
+            unsigned long long dg = 0ull;
+#pragma unroll
+            for (int k = 0; k < OTF_META; k++) {
+                uint32_t v = 0;
+                if (k == 0) v = (uint32_t)nl;
+                else if (k < nl) v = meta[k + drop];
+                else if (k == nl) v = (uint32_t)hs.w[t];
+                dst[k] = v;
+                dg += dig_meta(k, v);
+            }
+            atomicAdd(&Q.pr_dig[q], dg);
+            Q.pr_p[q] = lp;
+            if (Q.alg) {
+                const int km = m.order < L ? m.order : L;
+                atomicAdd(&Q.alg[0], (unsigned long long)p);
+                atomicAdd(&Q.alg[1], (unsigned long long)p * km);
+                atomicAdd(&Q.alg[2], 1ull);
+            }
+        }
+        __syncthreads();
+        q0 += (uint32_t)nb;
+    }
+}
+
 // MODE 1 = TF32X3, 3 = TF32; KC_B = m.wt_kcb; CPL/ORD as RING_DISPATCH.
 template <int MODE, int KC_B, int CPL, int ORD>
 __global__ void __launch_bounds__(sd::NT, 1)
 k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, double lm_weight, int stages,
-                 int hs_warps, uint32_t *cursor, uint32_t row_limit, uint32_t tmem_cols) {
+                 int qb_max, uint32_t *cursor, uint32_t row_limit, uint32_t tmem_cols) {
     using namespace tc;
     constexpr bool X3 = MODE == 1;
     constexpr int NT = sd::NT, NW = sd::NW;
@@ -104,7 +304,6 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     __shared__ uint32_t a_row[NT], a_cn[NT], a_wsum[NW], a_cnt[4];
     __shared__ __align__(8) uint64_t bar_full[4], bar_empty[4], bar_done;
     __shared__ uint32_t s_tmem, s_nprim, s_base, s_abort;
-    __shared__ __align__(8) uint64_t hs_bar[NW][HS_NS];   // HS ring barriers (initialised once)
 
     const int tid = threadIdx.x, lane = tid & 31;
     const int wid = __shfl_sync(0xffffffffu, tid >> 5, 0);     // provably warp-uniform
@@ -123,7 +322,6 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
             mbar_init(smem_u32(&bar_empty[st]), 1);
         }
         mbar_init(smem_u32(&bar_done), 1);
-        for (int i = 0; i < NW * HS_NS; i++) mbar_init(smem_u32(&hs_bar[i / HS_NS][i % HS_NS]), 1);
         s_abort = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -149,12 +347,24 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     const AssignSmem asmem{a_key, a_row, a_cn, a_wsum, a_cnt};
     uint32_t gctr = 0;          // K chunks through the ring so far (uniform)
     uint32_t tiles_done = 0;
-    // HS ring of this warp: row slots in the shared union (free while HS
-    // runs), barriers in static shared memory with phases kept across levels
-    HsRing ring;
-    ring.buf = smem + (size_t)wid * HS_NS * 4 * H;
-    ring.bar0 = smem_u32(&hs_bar[wid][0]);
-    ring.phase = 0;
+    // node-parallel HS scratch, in the shared union (free while HS runs)
+    sd::HsLevelSmem hsm;
+    {
+        uint8_t *p = smem + (size_t)qb_max * 4 * H;
+        hsm.h = reinterpret_cast<float *>(smem);
+        hsm.lsig = reinterpret_cast<double *>(p); p += sd::PAIRCAP * 8;
+        hsm.pcode = reinterpret_cast<uint32_t *>(p); p += sd::PAIRCAP * 4;
+        hsm.pre = reinterpret_cast<unsigned long long *>(p); p += sd::QMAX * ORD * 8;
+        hsm.row = reinterpret_cast<uint32_t *>(p); p += sd::QMAX * 4;
+        hsm.cb = reinterpret_cast<uint32_t *>(p); p += sd::QMAX * 4;
+        hsm.off = reinterpret_cast<uint32_t *>(p); p += sd::QMAX * 4;
+        hsm.P = reinterpret_cast<uint32_t *>(p); p += sd::QMAX * 4;
+        hsm.w = reinterpret_cast<int32_t *>(p); p += sd::QMAX * 4;
+        hsm.kmax = reinterpret_cast<int32_t *>(p); p += sd::QMAX * 4;
+        hsm.L = reinterpret_cast<int32_t *>(p); p += sd::QMAX * 4;
+        hsm.scan = reinterpret_cast<uint32_t *>(p); p += (NW + 2) * 4;
+        hsm.pq = p;
+    }
 
     // profiling runs only: per-phase device time (ns), summed over CTAs
     unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
@@ -197,10 +407,9 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
                 // warp would sit behind its siblings' suspended mbarrier waits.
                 constexpr int LT = NT - 32;                        // loader threads
                 const int ltid = tid - 32;
-                auto issue = [&](uint32_t gc, int kc) {
-                    const int st = (int)(gc % stages);
-                    const uint32_t use = gc / stages;
+                auto issue = [&](int st, uint32_t use, int kc) {
                     if (use >= 1) sd::wait_bounded(smem_u32(&bar_empty[st]), (use - 1) & 1, 1);
+                    __syncwarp();                                // lanes leave the wait independently
                     uint8_t *sW = smem + st * stage_bytes;
                     uint8_t *sH = sW + (X3 ? 2 : 1) * wa_bytes;
                     if (wid == 1) {                              // W chunk: one bulk copy, elected lane
@@ -225,8 +434,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
                     }
                     cp_async_commit();
                 };
-                auto consume = [&](uint32_t gc, int pending) {
-                    const int st = (int)(gc % stages);
+                auto consume = [&](int st, int pending) {
                     sd::cp_wait_n(pending);
                     uint8_t *sH = smem + st * stage_bytes + (X3 ? 2 : 1) * wa_bytes;
                     for (int idx = ltid; idx < nitems; idx += LT) {
@@ -253,10 +461,11 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
                 if (wid == 0) {
                     const uint32_t idesc = make_idesc(2, nn);
                     for (int kc = 0; kc < NK; kc++) {
-                        const uint32_t gc = gctr + kc;
-                        const int st = (int)(gc % stages);
+                        const int st = (int)((gctr + kc) % (uint32_t)stages);
+                        const uint32_t use = (gctr + kc) / (uint32_t)stages;
                         const unsigned long long w0 = prof ? sd::gtimer() : 0ull;
-                        sd::wait_bounded(smem_u32(&bar_full[st]), (gc / stages) & 1, 2);
+                        sd::wait_bounded(smem_u32(&bar_full[st]), use & 1, 2);
+                        __syncwarp();                            // elect.sync below needs a converged warp
                         if (prof) ph[5] += sd::gtimer() - w0;
                         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                         {
@@ -287,11 +496,17 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
                     }
                 } else {
                     const int pre = min(stages - 1, NK);
-                    for (int j = 0; j < pre; j++) issue(gctr + j, j);
+                    for (int j = 0; j < pre; j++) {
+                        const uint32_t gc = gctr + j;
+                        issue((int)(gc % (uint32_t)stages), gc / (uint32_t)stages, j);
+                    }
                     for (int kc = 0; kc < NK; kc++) {
                         const uint32_t gc = gctr + kc;
-                        consume(gc, min(stages - 2, NK - 1 - kc));
-                        if (kc + stages - 1 < NK) issue(gctr + kc + stages - 1, kc + stages - 1);
+                        consume((int)(gc % (uint32_t)stages), min(stages - 2, NK - 1 - kc));
+                        if (kc + stages - 1 < NK) {
+                            const uint32_t gi = gc + stages - 1;
+                            issue((int)(gi % (uint32_t)stages), gi / (uint32_t)stages, kc + stages - 1);
+                        }
                     }
                 }
                 gctr += NK;
@@ -310,15 +525,17 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
                         float v[32];
                         tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(mt * BM + ch * 32), v);
                         unsigned long long dg[32];
+                        // lane j fetches row j's word once; rows are broadcast below
+                        const int wl = ch * 32 + lane < nr ? Q.pr_w[q0 + ch * 32 + lane] : 0;
+                        const float *ucol = m.U + unit;
+                        float *ocol = S.arena_h + (size_t)(base + q0 + ch * 32) * H + unit;
 #pragma unroll
                         for (int j = 0; j < 32; j++) {
                             dg[j] = 0ull;
-                            const int row = ch * 32 + j;
-                            if (row < nr && unit < H) {
-                                const uint32_t q = q0 + (uint32_t)row;
-                                const int wq = Q.pr_w[q];
-                                const float o = 1.f / (1.f + expf(-(v[j] + __ldg(m.U + (size_t)wq * H + unit))));
-                                S.arena_h[(size_t)(base + q) * H + unit] = o;
+                            const int wq = __shfl_sync(0xffffffffu, wl, j);
+                            if (ch * 32 + j < nr && unit < H) {
+                                const float o = 1.f / (1.f + expf(-(v[j] + __ldg(ucol + (size_t)wq * H))));
+                                ocol[(size_t)j * H] = o;
                                 dg[j] = otf_hash64(((uint64_t)unit << 32) ^ __float_as_uint(o));
                             }
                         }
@@ -332,25 +549,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
                 SD_MARK(2);
             }
             // ------------- HS + MaxEnt of the computed requests -------------
-            if (wid < hs_warps) {
-                const RowSpec rs0{nullptr, nullptr, nullptr, nullptr, nullptr, row_limit};
-                for (uint32_t q = wid; q < n; q += hs_warps) {
-                    const uint32_t row = (uint32_t)Q.pr_inrow[q];
-                    const uint32_t *meta = S.arena_meta + (size_t)row * OTF_META;
-                    const int Lh = (int)meta[0];
-                    const int w = Q.pr_w[q];
-#ifdef SD_CHECK
-                    if (row >= S.arena_rows || w < 0 || w >= m.V || Lh > m.order) {
-                        printf("SD_CHECK hs: blk %d q %u n %u row %u w %d L %d base %u lvl %u\n", (int)blockIdx.x, q, n, row, w, Lh, base, L.t);
-                        __trap();
-                    }
-#endif
-                    const uint32_t o0 = __ldg(m.path_off + w), o1 = __ldg(m.path_off + w + 1);
-                    const double lp = hs_logprob_ring<CPL, false, ORD>(m, ring, S.arena_h + (size_t)row * H, meta + 1,
-                                                                       Lh, m.path_code + o0, o1 - o0, lane);
-                    hs_prim_finish(m, Q, S, rs0, base, q, meta, Lh, w, o1 - o0, lp, lane);
-                }
-            }
+            hs_level_nodepar<CPL, ORD>(m, Q, S, base, n, hsm, qb_max, tid, wid, lane);
             __syncthreads();
             SD_MARK(3);
         }
