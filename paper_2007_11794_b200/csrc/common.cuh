@@ -131,6 +131,16 @@ __device__ __forceinline__ double otf_sigmoid(double x) {
     return ex / (1.0 + ex);
 }
 
+// Content-digest term of element i of a hidden row (the digest is the
+// wrapping sum over elements; every digest match is confirmed by a full row
+// comparison, so the term only needs to spread well): one 64-bit multiply of
+// a 32-bit mix of (i, bits).
+__device__ __forceinline__ unsigned long long otf_dig_h(uint32_t i, float x) {
+    const uint32_t k = (__float_as_uint(x) ^ (i * 0x9E3779B9u)) * 0x85EBCA6Bu;
+    const uint64_t v = ((uint64_t)k << 32 | (uint64_t)(i + 0x27D4EB2Fu)) * 0xff51afd7ed558ccdull;
+    return v ^ (v >> 29);
+}
+
 __device__ __forceinline__ double shfl_xor_d(double v, int m) {
     return __shfl_xor_sync(0xffffffffu, v, m);
 }

@@ -85,9 +85,7 @@ struct DevPlan {
 // content digest term of element i of a hidden row / word j of the history
 // meta; the digest is their wrapping sum, so partial sums from different CTAs
 // and kernels compose (context_table.py:64-72 serializes the same content)
-__device__ __forceinline__ unsigned long long dig_h(int i, float x) {
-    return otf_hash64(((uint64_t)i << 32) ^ __float_as_uint(x));
-}
+__device__ __forceinline__ unsigned long long dig_h(int i, float x) { return otf_dig_h((uint32_t)i, x); }
 __device__ __forceinline__ unsigned long long dig_meta(int j, uint32_t w) {
     return otf_hash64(((uint64_t)(0x10000 + j) << 32) ^ w);
 }

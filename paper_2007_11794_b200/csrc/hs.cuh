@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(256) k_advance_f64(DevModel m, uint32_t n_cap,
             if (q < nq) {
                 const float o = (float)otf_sigmoid(acc[q]);
                 out_base[(size_t)(out0 + q0 + q) * H + i] = o;
-                dg[q] += otf_hash64(((uint64_t)i << 32) ^ __float_as_uint(o));
+                dg[q] += otf_dig_h((uint32_t)i, o);
             }
     }
     if (rs.dig) {

@@ -60,8 +60,10 @@ __device__ __forceinline__ void wait_bounded(uint32_t bar, uint32_t parity, int 
     unsigned long long t0 = 0;
     for (uint32_t it = 0;; it++) {
         uint32_t ok;
-        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+        // suspend-time hint (ns): the warp is parked until the phase completes
+        // instead of re-polling (polls cost issue slots of the working warps)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(bar), "r"(parity), "r"(1000000u) : "memory");
         if (ok) return;
         if ((it & 1023u) == 0) {                   // wall-clock bound: 2 s
             const unsigned long long t = gtimer_();
@@ -194,56 +196,49 @@ __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, 
                 __ldcg(reinterpret_cast<const float4 *>(S.arena_h + (size_t)hs.row[t] * H) + c);
         }
         __syncthreads();
-        // ---- B: 8 pairs per warp round ----
-        const int my_g = node_of_lane(lane);
-        const bool leader = (lane & 3) == 0;
-        for (uint32_t j0 = (uint32_t)wid * HS_G; j0 < T; j0 += (uint32_t)NW * HS_G) {
-            uint32_t code[HS_G];
-            int qt[HS_G];
-#pragma unroll
-            for (int g = 0; g < HS_G; g++) {
-                const uint32_t j = j0 + g;
-                qt[g] = j < T ? (int)hs.pq[j] : 0;
-                code[g] = j < T ? hs.pcode[j] : OTF_UNSET;
-            }
-            // MaxEnt terms of this lane's node (leaders), issued before the rows
-            const uint32_t mycode = code[my_g];
-            const int myq = qt[my_g];
-            const int kmax = hs.kmax[myq];
-            double me[ORD];
-#pragma unroll
-            for (int k = 0; k < ORD; k++) {
-                me[k] = 0.0;
-                if (leader && k < kmax && mycode != OTF_UNSET)
-                    me[k] = (double)__ldg(m.ME + (otf_mix(hs.pre[myq * ORD + k], (uint64_t)(mycode & 0x7FFFFFFFu)) & m.mask));
-            }
-            double acc[HS_G];
-#pragma unroll
-            for (int g = 0; g < HS_G; g++) {
-                acc[g] = 0.0;
-                if (code[g] != OTF_UNSET) {
-                    const float4 *row = reinterpret_cast<const float4 *>(m.NV + (size_t)(code[g] & 0x7FFFFFFFu) * H);
-                    const float4 *hv = reinterpret_cast<const float4 *>(hs.h + (size_t)qt[g] * H);
-                    float f0 = 0.f, f1 = 0.f, f2 = 0.f, f3 = 0.f;
-#pragma unroll
-                    for (int c = 0; c < CPL; c++) {
-                        const int k = lane + 32 * c;
-                        if (k < NCH) {
-                            const float4 t = __ldg(row + k);
-                            const float4 h4 = hv[k];
-                            f0 = fmaf(t.x, h4.x, f0);
-                            f1 = fmaf(t.y, h4.y, f1);
-                            f2 = fmaf(t.z, h4.z, f2);
-                            f3 = fmaf(t.w, h4.w, f3);
-                        }
+        // ---- B: 8 pairs per warp round, 4 lanes per pair ----
+        // lane = 4 * pair + sub; sub covers float4 chunks sub, sub+4, ... of H
+        {
+            const int pg = lane >> 2, sub = lane & 3;
+            for (uint32_t j0 = (uint32_t)wid * HS_G; j0 < T; j0 += (uint32_t)NW * HS_G) {
+                const uint32_t j = j0 + (uint32_t)pg;
+                const bool live = j < T;
+                const int t = live ? (int)hs.pq[j] : 0;
+                const uint32_t code = live ? hs.pcode[j] : 0u;
+                const int kmax = hs.kmax[t];
+                // MaxEnt terms: lane sub < kmax gathers order sub+1 (issued first)
+                double me = 0.0;
+                if (live && sub < kmax)
+                    me = (double)__ldg(m.ME + (otf_mix(hs.pre[t * ORD + sub], (uint64_t)(code & 0x7FFFFFFFu)) & m.mask));
+                float f0 = 0.f, f1 = 0.f, f2 = 0.f, f3 = 0.f;
+                if (live) {
+                    const float4 *row = reinterpret_cast<const float4 *>(m.NV + (size_t)(code & 0x7FFFFFFFu) * H);
+                    const float4 *hv = reinterpret_cast<const float4 *>(hs.h + (size_t)t * H);
+#pragma unroll 8
+                    for (int k = sub; k < NCH; k += 4) {
+                        const float4 x = __ldg(row + k);
+                        const float4 h4 = hv[k];
+                        f0 = fmaf(x.x, h4.x, f0);
+                        f1 = fmaf(x.y, h4.y, f1);
+                        f2 = fmaf(x.z, h4.z, f2);
+                        f3 = fmaf(x.w, h4.w, f3);
                     }
-                    acc[g] = ((double)f0 + (double)f1) + ((double)f2 + (double)f3);
                 }
-            }
-            double a = reduce8(acc, lane);
+                double a = ((double)f0 + (double)f1) + ((double)f2 + (double)f3);
+                a += __shfl_xor_sync(0xffffffffu, a, 1);
+                a += __shfl_xor_sync(0xffffffffu, a, 2);
+                // MaxEnt orders added in reference order (k = 1, 2, ...)
 #pragma unroll
-            for (int k = 0; k < ORD; k++) if (k < kmax) a += me[k];
-            if (leader && mycode != OTF_UNSET) hs.lsig[j0 + my_g] = (mycode & 0x80000000u) ? -a : a;
+                for (int k = 0; k < (ORD < 4 ? ORD : 4); k++) {
+                    const double mk = __shfl_sync(0xffffffffu, me, (lane & ~3) | k);
+                    if (k < kmax) a += mk;
+                }
+                if (ORD > 4) {                       // orders 5..7 (rare): leader gathers them
+                    for (int k = 4; k < kmax; k++)
+                        a += (double)__ldg(m.ME + (otf_mix(hs.pre[t * ORD + k], (uint64_t)(code & 0x7FFFFFFFu)) & m.mask));
+                }
+                if (live && sub == 0) hs.lsig[j] = (code & 0x80000000u) ? -a : a;
+            }
         }
         __syncthreads();
         // log-sigmoid once per pair with every lane busy (f64, libdevice)
@@ -534,9 +529,9 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
                             dg[j] = 0ull;
                             const int wq = __shfl_sync(0xffffffffu, wl, j);
                             if (ch * 32 + j < nr && unit < H) {
-                                const float o = 1.f / (1.f + expf(-(v[j] + __ldg(ucol + (size_t)wq * H))));
+                                const float o = __frcp_rn(1.f + expf(-(v[j] + __ldg(ucol + (size_t)wq * H))));   // == 1/x, IEEE
                                 ocol[(size_t)j * H] = o;
-                                dg[j] = otf_hash64(((uint64_t)unit << 32) ^ __float_as_uint(o));
+                                dg[j] = otf_dig_h((uint32_t)unit, o);
                             }
                         }
                         const unsigned long long tot = sd::transpose_sum32(dg, lane);

@@ -418,24 +418,24 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                         for (int j = 0; j < 32; j += 4) {
                             float4 u = __ldg(reinterpret_cast<const float4 *>(urow + gc + j));
                             float4 o;
-                            o.x = 1.f / (1.f + expf(-(v[j] + u.x)));
-                            o.y = 1.f / (1.f + expf(-(v[j + 1] + u.y)));
-                            o.z = 1.f / (1.f + expf(-(v[j + 2] + u.z)));
-                            o.w = 1.f / (1.f + expf(-(v[j + 3] + u.w)));
+                            o.x = __frcp_rn(1.f + expf(-(v[j] + u.x)));
+                            o.y = __frcp_rn(1.f + expf(-(v[j + 1] + u.y)));
+                            o.z = __frcp_rn(1.f + expf(-(v[j + 2] + u.z)));
+                            o.w = __frcp_rn(1.f + expf(-(v[j + 3] + u.w)));
                             *reinterpret_cast<float4 *>(orow + gc + j) = o;
                             if (rs.dig) {
-                                dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o.x));
-                                dig += otf_hash64(((uint64_t)(gc + j + 1) << 32) ^ __float_as_uint(o.y));
-                                dig += otf_hash64(((uint64_t)(gc + j + 2) << 32) ^ __float_as_uint(o.z));
-                                dig += otf_hash64(((uint64_t)(gc + j + 3) << 32) ^ __float_as_uint(o.w));
+                                dig += otf_dig_h((uint32_t)(gc + j), o.x);
+                                dig += otf_dig_h((uint32_t)(gc + j + 1), o.y);
+                                dig += otf_dig_h((uint32_t)(gc + j + 2), o.z);
+                                dig += otf_dig_h((uint32_t)(gc + j + 3), o.w);
                             }
                         }
                     } else {
                         for (int j = 0; j < 32; j++)
                             if (gc + j < H) {
-                                const float o = 1.f / (1.f + expf(-(v[j] + urow[gc + j])));
+                                const float o = __frcp_rn(1.f + expf(-(v[j] + urow[gc + j])));
                                 orow[gc + j] = o;
-                                dig += otf_hash64(((uint64_t)(gc + j) << 32) ^ __float_as_uint(o));
+                                dig += otf_dig_h((uint32_t)(gc + j), o);
                             }
                     }
                 }
