@@ -185,9 +185,14 @@ def pack_lattices(lattices, stream_ids=None):
     for i, lat in enumerate(lats):
         ids = lat.node_ids
         n_nodes[i] = len(ids)
-        start[i] = np.searchsorted(ids, lat.start)
-        src.append(np.searchsorted(ids, lat.arc_src).astype(np.int32))
-        dst.append(np.searchsorted(ids, lat.arc_dst).astype(np.int32))
+        if len(ids) and ids[0] == 0 and ids[-1] == len(ids) - 1:     # already 0..n-1 (sorted unique)
+            start[i] = lat.start
+            src.append(lat.arc_src.astype(np.int32, copy=False))
+            dst.append(lat.arc_dst.astype(np.int32, copy=False))
+        else:
+            start[i] = np.searchsorted(ids, lat.start)
+            src.append(np.searchsorted(ids, lat.arc_src).astype(np.int32))
+            dst.append(np.searchsorted(ids, lat.arc_dst).astype(np.int32))
         word.append(lat.arc_word.astype(np.int32))
         ac.append(lat.arc_acoustic)
         slm.append(lat.arc_smalllm)
