@@ -312,7 +312,18 @@ def main():
         roof = {"kernel": f"k_{dominant}", "bound": "hbm",
                 "achieved": requests * 96 / (dom_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    # DRAM bytes per launch of the dominant kernel from the committed ncu
+    # capture of this same command (profiles/traffic.json), else null
     roof["traffic"] = None
+    tfile = Path(__file__).resolve().parent / "profiles" / "traffic.json"
+    if dominant == "stream" and tfile.exists():
+        try:
+            t = json.loads(tfile.read_text())["k_decode_streams"]
+            roof["traffic"] = t["dram_bytes_per_launch"]
+            roof["traffic_source"] = t["source"]
+            roof["algorithmic_bytes"] = roof["achieved"] * 1e9 * (dom_ms / 1e3)
+        except (KeyError, ValueError):
+            pass
     roof["peak_source"] = peak_src
     roof["launches"] = dom_n
     roof["avg_launch_us"] = dom_ms * 1e3 / max(dom_n, 1)
