@@ -234,9 +234,11 @@ int otflm_plan_set_arena(OtflmPlan *p, uint32_t start, uint32_t end);
  * run the schedule. */
 int otflm_plan_set_schedule(OtflmPlan *p, int32_t schedule);
 /* Stream schedule, after otflm_decode_profile: device time per phase summed
- * over CTAs (ns) -- o[0] expand, o[1] recurrent-update K loop (loads + MMAs),
- * o[2] update epilogue, o[3] HS, o[4] assign, o[5..6] 0, o[7] CTAs that
- * reported (8 entries). */
+ * over CTAs (ns), 12 entries -- o[0] expand, o[1] recurrent-update K loop,
+ * o[2] MMA drain, o[3] update epilogue, o[4] HS setup + row staging,
+ * o[5] HS pair rounds, o[6] whole HS group (small-LM scores + HS; runs
+ * concurrently with o[1..3]), o[7] assign, o[8] wait of the update group for
+ * the HS group, o[9] MMA-warp wait for operands, o[10] 0, o[11] CTAs. */
 int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream);
 int otflm_schedule_supported(const OtflmModel *m, int32_t schedule, int32_t precision);
 int otflm_group_create(OtflmPlan **plans, int32_t n, OtflmGroup **out);

@@ -877,7 +877,7 @@ static int plan_alloc_workspace(OtflmPlan *p, uint32_t R, uint32_t n_lvl_slots) 
     bad |= p->mem.alloc(&d.pr_p, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.pr_dig, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.lvl, n_lvl_slots) != cudaSuccess;
-    bad |= p->mem.alloc(&p->alg_buf, 16) != cudaSuccess;   // [0..3] work counters, [8..15] phase ns
+    bad |= p->mem.alloc(&p->alg_buf, 24) != cudaSuccess;   // [0..3] work counters, [8..19] phase ns
     bad |= p->mem.alloc(&d.cursor, 1) != cudaSuccess;
     d.alg = nullptr;   // counters are only maintained in profiling runs
     d.phase_ns = nullptr;
@@ -1035,10 +1035,10 @@ extern "C" int otflm_plan_info(const OtflmPlan *p, int64_t *o) {
 
 extern "C" int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream) {
     if (!p || !o) return OTFLM_ERR_VALUE;
-    unsigned long long a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long a[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(a, p->alg_buf + 8, sizeof(a), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     CK(cudaStreamSynchronize((cudaStream_t)stream));
-    for (int i = 0; i < 8; i++) o[i] = (int64_t)a[i];
+    for (int i = 0; i < 12; i++) o[i] = (int64_t)a[i];
     return OTFLM_OK;
 }
 
@@ -1135,14 +1135,16 @@ static bool sd_config(const DevModel &m, int prec, SdConfig *c) {
     if (!m.W_t || m.H % 4 != 0 || m.wt_npad > 512 || !m.U || !m.NV || !m.path_off) return false;
     const bool x3 = prec == OTFLM_PREC_TF32X3;
     const size_t stage = (x3 ? 2u : 1u) * ((size_t)m.wt_npad * m.wt_kcb + (size_t)tc::BM * m.wt_kcb);
-    const size_t budget = 200u * 1024u;
-    c->stages = (int)std::min<size_t>(4, budget / stage);
-    if (c->stages < 2) return false;
-    // node-parallel HS scratch beyond the context rows (hs_level_nodepar)
-    const size_t hs_fixed = (size_t)sd::PAIRCAP * 13 + (size_t)sd::QMAX * (OTF_MAX_ORDER * 8 + 7 * 4) + (sd::NW + 2) * 4 + 64;
-    c->smem = std::max((size_t)c->stages * stage, hs_fixed + 32 * 4 * (size_t)m.H);
-    c->qb_max = (int)std::min<size_t>(sd::QMAX, (c->smem - hs_fixed) / (4 * (size_t)m.H));
-    if (c->qb_max < 1 || c->smem > budget) return false;
+    const size_t budget = 204u * 1024u;                   // + ~21 KB static shared memory
+    // the update's ring and the HS scratch are live at the same time (the
+    // two warp groups run concurrently): 2 ring stages, the rest for HS
+    const int ord = m.order <= 3 ? 3 : OTF_MAX_ORDER;
+    const size_t hs_fixed = (size_t)sd::PAIRCAP * 13 + (size_t)sd::QMAX * (ord * 8 + 7 * 4) + (sd::NW + 2) * 4 + 64;
+    c->stages = 2;
+    const size_t ring = (size_t)c->stages * stage;
+    if (ring + hs_fixed + 8 * 4 * (size_t)m.H > budget) return false;
+    c->qb_max = (int)std::min<size_t>(sd::QMAX, (budget - ring - hs_fixed) / (4 * (size_t)m.H));
+    c->smem = ring + hs_fixed + (size_t)c->qb_max * 4 * m.H;
     c->tmem_cols = 128;
     while ((int)c->tmem_cols < m.wt_npad) c->tmem_cols <<= 1;
     return true;
@@ -1183,7 +1185,7 @@ static int enqueue_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int pre
     DevStreams &S = p->st->d;
     DevPlan &d = p->d;
     CK(cudaMemsetAsync(d.arr, 0xFF, (size_t)std::max<uint32_t>(p->n_slots, 1) * sizeof(Arrival), s));
-    if (d.alg) CK(cudaMemsetAsync(d.alg, 0, 16 * sizeof(unsigned long long), s));
+    if (d.alg) CK(cudaMemsetAsync(d.alg, 0, 24 * sizeof(unsigned long long), s));
     { ProfScope ps(K_MISC, s); k_run_begin<<<cdiv(p->n_utt, 128), 128, 0, s>>>(d, S); CKL(); }
     { ProfScope ps(K_STREAM, s); int rc = launch_streams(p, g, lm, prec, s); if (rc) return rc; }
     { ProfScope ps(K_FINAL, s); k_final<<<cdiv(p->n_utt, 4), 128, 0, s>>>(d, S, lm, -1); CKL(); }

@@ -242,7 +242,7 @@ __device__ __forceinline__ bool ngram_logprob_dev(const DevNgram &g, const uint3
 __device__ __forceinline__ void expand_node(DevPlan &P, const DevStreams &S, const DevNgram &g,
                                             const NodeInfo &nd, long long beam, uint32_t lvl, int64_t r_shift,
                                             uint32_t *n_prim, uint32_t *s_ctx, uint32_t *s_slot, double *s_score,
-                                            uint32_t *s_arc, int lane) {
+                                            uint32_t *s_arc, int lane, bool defer_ps = false) {
     const uint32_t outdeg = nd.out_e - nd.out_b;
     const uint32_t rq0 = (uint32_t)((int64_t)nd.req_base + r_shift);
     if (nd.cap == 0 || outdeg == 0) {
@@ -342,10 +342,12 @@ __device__ __forceinline__ void expand_node(DevPlan &P, const DevStreams &S, con
             if (S.enabled) cslot = cache_probe(S, nd.stream, c, w, r, &st);
             // small-LM score of the same transition from the context's
             // stored history (decoder.py:99-100), independent of the model
-            const uint32_t crow = S.ctx_row[(uint64_t)nd.stream * (S.max_ctx + 1) + c];
-            const uint32_t *meta = S.arena_meta + (size_t)crow * OTF_META;
-            double ps;
-            if (!ngram_logprob_dev(g, meta + 1, (int)meta[0], w, &ps)) { atomicOr(S.err, OTF_E_KEY); ps = 0.0; }
+            double ps = 0.0;
+            if (!defer_ps) {
+                const uint32_t crow = S.ctx_row[(uint64_t)nd.stream * (S.max_ctx + 1) + c];
+                const uint32_t *meta = S.arena_meta + (size_t)crow * OTF_META;
+                if (!ngram_logprob_dev(g, meta + 1, (int)meta[0], w, &ps)) { atomicOr(S.err, OTF_E_KEY); ps = 0.0; }
+            }
             P.rq_c[r] = c;
             P.rq_w[r] = w;
             P.rq_arc[r] = a;
@@ -362,6 +364,24 @@ __device__ __forceinline__ void expand_node(DevPlan &P, const DevStreams &S, con
     }
     for (uint32_t r = n_kept * outdeg + lane; r < nd.keep * outdeg; r += 32)
         P.rq_state[rq0 + r] = RQ_INVALID;
+}
+
+// Small-LM scores of requests [0, nreq) of one stream (decoder.py:99-100),
+// when expand_node ran with defer_ps: thread per request over `nthr` threads
+// starting at thread `t0` (they only feed assign, so they can run alongside
+// the recurrent update and HS).
+__device__ __forceinline__ void small_lm_scores(DevPlan &P, const DevStreams &S, const DevNgram &g, uint32_t s,
+                                                uint32_t nreq, int t, int nthr) {
+    for (uint32_t r = (uint32_t)t; r < nreq; r += (uint32_t)nthr) {
+        if (P.rq_state[r] == RQ_INVALID) continue;
+        const uint32_t c = P.rq_c[r];
+        const int32_t w = P.rq_w[r];
+        const uint32_t crow = S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + c];
+        const uint32_t *meta = S.arena_meta + (size_t)crow * OTF_META;
+        double ps;
+        if (!ngram_logprob_dev(g, meta + 1, (int)meta[0], w, &ps)) { atomicOr(S.err, OTF_E_KEY); ps = 0.0; }
+        P.rq_ps[r] = ps;
+    }
 }
 
 constexpr int EXP_WARPS = 8;

@@ -35,6 +35,8 @@
 namespace sd {
 constexpr int NT = 512;
 constexpr int NW = NT / 32;
+constexpr int GW = 8;              // warps of the recurrent-update group (warp 0 issues MMAs)
+constexpr int GT = GW * 32;
 
 __device__ __forceinline__ void cp_wait_n(int n) {
     if (n <= 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -83,6 +85,35 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
+// named barrier over a warp group (id 0 is __syncthreads)
+__device__ __forceinline__ void group_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
+}
+
+// reduce8 (hs.cuh) for wrapping 64-bit sums: 8 values per lane -> the sum
+// over lanes of value g on the lanes whose bits (4,3,2) spell g
+__device__ __forceinline__ unsigned long long reduce8_u64(unsigned long long (&v)[8], int lane) {
+    const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        const unsigned long long send = u16 ? v[i] : v[i + 4], keep = u16 ? v[i + 4] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+        const unsigned long long send = u8 ? v[i] : v[i + 2], keep = u8 ? v[i + 2] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+    {
+        const unsigned long long send = u4 ? v[0] : v[1], keep = u4 ? v[1] : v[0];
+        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    unsigned long long x = v[0];
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    return x;
+}
+
 // v[j] (j = 0..31) per lane -> lane j returns sum over lanes of v[j]
 __device__ __forceinline__ unsigned long long transpose_sum32(unsigned long long (&v)[32], int lane) {
 #pragma unroll
@@ -111,7 +142,7 @@ __device__ __forceinline__ unsigned long long transpose_sum32(unsigned long long
 // path order afterwards.
 // --------------------------------------------------------------------------
 namespace sd {
-constexpr int PAIRCAP = 4096;      // (query, node) pairs per batch
+constexpr int PAIRCAP = 2048;      // (query, node) pairs per batch
 constexpr int QMAX = 128;          // queries per batch (upper bound)
 struct HsLevelSmem {
     float *h;                      // [qb][H] context rows
@@ -125,11 +156,18 @@ struct HsLevelSmem {
 };
 }  // namespace sd
 
-template <int CPL, int ORD>
+// Run by a group of NT threads (NW warps) synchronising on named barrier
+// BAR; tid / wid are group-relative.
+template <int CPL, int ORD, int NT, int BAR>
 __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, DevStreams &S, uint32_t base,
                                                  uint32_t n, const sd::HsLevelSmem &hs, int qb_max, int tid,
-                                                 int wid, int lane) {
-    constexpr int NT = sd::NT, NW = sd::NW;
+                                                 int wid, int lane, unsigned long long *ph) {
+    constexpr int NW = NT / 32;
+#define HS_SYNC() sd::group_sync(BAR, NT)
+    // ph (profiling, thread 0 only): [4] setup + staging, [5] pair rounds; the
+    // caller's mark after HS then covers log-sigmoid + per-query finish
+    unsigned long long tm = ph ? sd::gtimer() : 0ull;
+#define HS_MARK(i) do { if (ph) { const unsigned long long t2 = sd::gtimer(); ph[i] += t2 - tm; tm = t2; } } while (0)
     const int H = m.H, NCH = H >> 2;
     for (uint32_t q0 = 0; q0 < n;) {
         const int nq = (int)min((uint32_t)qb_max, n - q0);
@@ -163,12 +201,12 @@ __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, 
             if (lane >= o) inc += v;
         }
         if (lane == 31) hs.scan[wid] = inc;
-        __syncthreads();
+        HS_SYNC();
         uint32_t before = 0;
         for (int w2 = 0; w2 < wid; w2++) before += hs.scan[w2];
         const uint32_t excl = before + inc - Pt;
         if (tid < nq) hs.off[tid] = excl;
-        __syncthreads();
+        HS_SYNC();
         // batch = the leading queries whose pairs fit PAIRCAP (offsets are monotone)
         if (tid == 0) {
             int lo = 0, hi = nq;
@@ -179,7 +217,7 @@ __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, 
             if (lo == 0) { atomicOr(S.err, OTF_E_VALUE); lo = 1; }   // one path longer than PAIRCAP
             hs.scan[NW] = (uint32_t)lo;
         }
-        __syncthreads();
+        HS_SYNC();
         const int nb = (int)hs.scan[NW];
         const uint32_t T = min(hs.off[nb - 1] + hs.P[nb - 1], (uint32_t)sd::PAIRCAP);
         // pair -> query map and the context rows
@@ -195,7 +233,8 @@ __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, 
             reinterpret_cast<float4 *>(hs.h)[(size_t)t * NCH + c] =
                 __ldcg(reinterpret_cast<const float4 *>(S.arena_h + (size_t)hs.row[t] * H) + c);
         }
-        __syncthreads();
+        HS_SYNC();
+        HS_MARK(4);
         // ---- B: 8 pairs per warp round, 4 lanes per pair ----
         // lane = 4 * pair + sub; sub covers float4 chunks sub, sub+4, ... of H
         {
@@ -240,10 +279,11 @@ __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, 
                 if (live && sub == 0) hs.lsig[j] = (code & 0x80000000u) ? -a : a;
             }
         }
-        __syncthreads();
+        HS_SYNC();
+        HS_MARK(5);
         // log-sigmoid once per pair with every lane busy (f64, libdevice)
         for (uint32_t j = (uint32_t)tid; j < T; j += NT) hs.lsig[j] = otf_log_sigmoid(hs.lsig[j]);
-        __syncthreads();
+        HS_SYNC();
         // ---- C: per query: path-order sum, successor history, digest ----
         // thread per query: path-order sum, successor history (rnnlm.py:187),
         // its digest terms (same values as hs_prim_finish)
@@ -277,9 +317,11 @@ __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, 
                 atomicAdd(&Q.alg[2], 1ull);
             }
         }
-        __syncthreads();
+        HS_SYNC();
         q0 += (uint32_t)nb;
     }
+#undef HS_MARK
+#undef HS_SYNC
 }
 
 // MODE 1 = TF32X3, 3 = TF32; KC_B = m.wt_kcb; CPL/ORD as RING_DISPATCH.
@@ -313,7 +355,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
 
     if (tid == 0) {
         for (int st = 0; st < stages; st++) {
-            mbar_init(smem_u32(&bar_full[st]), NW);   // one per loader warp + the W copy
+            mbar_init(smem_u32(&bar_full[st]), sd::GW);   // one per loader warp + the W copy
             mbar_init(smem_u32(&bar_empty[st]), 1);
         }
         mbar_init(smem_u32(&bar_done), 1);
@@ -345,8 +387,9 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     // node-parallel HS scratch, in the shared union (free while HS runs)
     sd::HsLevelSmem hsm;
     {
-        uint8_t *p = smem + (size_t)qb_max * 4 * H;
-        hsm.h = reinterpret_cast<float *>(smem);
+        uint8_t *hb = smem + (size_t)stages * stage_bytes;           // after the update's ring
+        uint8_t *p = hb + (size_t)qb_max * 4 * H;
+        hsm.h = reinterpret_cast<float *>(hb);
         hsm.lsig = reinterpret_cast<double *>(p); p += sd::PAIRCAP * 8;
         hsm.pcode = reinterpret_cast<uint32_t *>(p); p += sd::PAIRCAP * 4;
         hsm.pre = reinterpret_cast<unsigned long long *>(p); p += sd::QMAX * ORD * 8;
@@ -361,9 +404,11 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
         hsm.pq = p;
     }
 
-    // profiling runs only: per-phase device time (ns), summed over CTAs
-    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
-    const bool prof = P.phase_ns != nullptr && tid == 0;
+    // profiling runs only: per-phase device time (ns), summed over CTAs;
+    // thread 0 times the shared phases and the update group, thread GT the
+    // HS group (they run concurrently)
+    unsigned long long ph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
+    const bool prof = P.phase_ns != nullptr && (tid == 0 || tid == sd::GT);
 #define SD_MARK(i) do { if (prof) { t1 = sd::gtimer(); ph[i] += t1 - t0; t0 = t1; } } while (0)
     if (prof) t0 = sd::gtimer();
     for (uint32_t li = P.ul_off[u]; li < P.ul_off[u + 1]; li++) {
@@ -374,10 +419,10 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
         for (uint32_t k = L.nb + wid; k < L.ne; k += NW) {
             const NodeInfo nd = P.nodes[P.level_nodes[k]];
             expand_node(Q, S, g, nd, beam, L.t, -(int64_t)L.rb, &s_nprim, e_ctx[wid], e_slot[wid], e_score[wid],
-                        e_arc[wid], lane);
+                        e_arc[wid], lane, /*defer_ps=*/true);
         }
         __syncthreads();
-        SD_MARK(0);
+        if (tid == 0) SD_MARK(0);
         const uint32_t n = s_nprim;
 #ifdef SD_CHECK
         if (tid == 0 && n > L.re - L.rb) { printf("SD_CHECK n %u > requests %u blk %d\n", n, L.re - L.rb, (int)blockIdx.x); __trap(); }
@@ -392,172 +437,200 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
         if (s_abort) break;
         const uint32_t base = s_base;
         if (n) {
-            // ------------- recurrent update (tcgen05) -------------
-            for (uint32_t q0 = 0; q0 < n; q0 += BM) {
-                const int nr = (int)min((uint32_t)BM, n - q0);
-                const int nn = (nr + 15) & ~15;                   // MMA N
-                const int nitems = ((nr + 7) & ~7) * CH;          // row pieces per chunk
-                // warp 0: MMA issuer (converged; lane 0 issues).  Warps 1..NW-1:
-                // loaders / converters -- a divergent issuer inside a loader
-                // warp would sit behind its siblings' suspended mbarrier waits.
-                constexpr int LT = NT - 32;                        // loader threads
-                const int ltid = tid - 32;
-                auto issue = [&](int st, uint32_t use, int kc) {
-                    if (use >= 1) sd::wait_bounded(smem_u32(&bar_empty[st]), (use - 1) & 1, 1);
-                    __syncwarp();                                // lanes leave the wait independently
-                    uint8_t *sW = smem + st * stage_bytes;
-                    uint8_t *sH = sW + (X3 ? 2 : 1) * wa_bytes;
-                    if (wid == 1) {                              // W chunk: one bulk copy, elected lane
-                        const uint32_t bytes = (X3 ? 2u : 1u) * wa_bytes;
-                        const void *src = reinterpret_cast<const uint8_t *>(m.W_t) + (size_t)kc * 2 * wa_bytes;
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 t;\n\telect.sync t|e, 0xffffffff;\n\t"
-                                     "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %3;\n\t"
-                                     "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %3, [%1];\n\t}"
-                                     :: "r"(smem_u32(sW)), "r"(smem_u32(&bar_full[st])), "l"(src), "r"(bytes) : "memory");
-                    }
-                    const int k0 = kc * KE;
-                    for (int idx = ltid; idx < nitems; idx += LT) {
-                        const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
-                        const int row = g8 * 8 + r8;
-                        if (row >= nr) continue;
-                        const int kk = k0 + c * 4;
-                        const bool ok = kk < H;
-                        const int src = Q.pr_inrow[q0 + row];
-                        cp_async16(smem_u32(sH + swz_off<KC_B>(row, c)),
-                                   ok ? (const void *)(S.arena_h + (size_t)src * H + kk) : (const void *)S.arena_h, ok);
-                    }
-                    cp_async_commit();
-                };
-                auto consume = [&](int st, int pending) {
-                    sd::cp_wait_n(pending);
-                    uint8_t *sH = smem + st * stage_bytes + (X3 ? 2 : 1) * wa_bytes;
-                    for (int idx = ltid; idx < nitems; idx += LT) {
-                        const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
-                        const int row = g8 * 8 + r8;
-                        if (row >= nr) continue;
-                        const uint32_t off = swz_off<KC_B>(row, c);
-                        const float4 x = *reinterpret_cast<const float4 *>(sH + off);
-                        float4 hi;
-                        hi.x = tf32_rn(x.x); hi.y = tf32_rn(x.y); hi.z = tf32_rn(x.z); hi.w = tf32_rn(x.w);
-                        *reinterpret_cast<float4 *>(sH + off) = hi;
-                        if (X3) {
-                            float4 lo;
-                            lo.x = tf32_rn(x.x - hi.x); lo.y = tf32_rn(x.y - hi.y);
-                            lo.z = tf32_rn(x.z - hi.z); lo.w = tf32_rn(x.w - hi.w);
-                            *reinterpret_cast<float4 *>(sH + hb_bytes + off) = lo;
+            // The recurrent update (warps 0..GW-1) and the HS + deferred
+            // small-LM scores (warps GW..NW-1) only depend on expand: the two
+            // groups run concurrently on disjoint shared memory, each
+            // synchronising on its own named barrier.
+            if (wid < sd::GW) {
+                // ------------- recurrent update (tcgen05) -------------
+                for (uint32_t q0 = 0; q0 < n; q0 += BM) {
+                    const int nr = (int)min((uint32_t)BM, n - q0);
+                    const int nn = (nr + 15) & ~15;                   // MMA N
+                    const int nitems = ((nr + 7) & ~7) * CH;          // row pieces per chunk
+                    // warp 0: MMA issuer (converged; lane 0 issues).  Warps 1..NW-1:
+                    // loaders / converters -- a divergent issuer inside a loader
+                    // warp would sit behind its siblings' suspended mbarrier waits.
+                    constexpr int LT = sd::GT - 32;                    // loader threads (warps 1..GW-1)
+                    const int ltid = tid - 32;
+                    auto issue = [&](int st, uint32_t use, int kc) {
+                        if (use >= 1) sd::wait_bounded(smem_u32(&bar_empty[st]), (use - 1) & 1, 1);
+                        __syncwarp();                                // lanes leave the wait independently
+                        uint8_t *sW = smem + st * stage_bytes;
+                        uint8_t *sH = sW + (X3 ? 2 : 1) * wa_bytes;
+                        if (wid == 1) {                              // W chunk: one bulk copy, elected lane
+                            const uint32_t bytes = (X3 ? 2u : 1u) * wa_bytes;
+                            const void *src = reinterpret_cast<const uint8_t *>(m.W_t) + (size_t)kc * 2 * wa_bytes;
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 t;\n\telect.sync t|e, 0xffffffff;\n\t"
+                                         "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %3;\n\t"
+                                         "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %3, [%1];\n\t}"
+                                         :: "r"(smem_u32(sW)), "r"(smem_u32(&bar_full[st])), "l"(src), "r"(bytes) : "memory");
                         }
-                    }
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    __syncwarp();
-                    if (lane == 0)
-                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&bar_full[st])) : "memory");
-                };
-                if (wid == 0) {
-                    const uint32_t idesc = make_idesc(2, nn);
-                    for (int kc = 0; kc < NK; kc++) {
-                        const int st = (int)((gctr + kc) % (uint32_t)stages);
-                        const uint32_t use = (gctr + kc) / (uint32_t)stages;
-                        const unsigned long long w0 = prof ? sd::gtimer() : 0ull;
-                        sd::wait_bounded(smem_u32(&bar_full[st]), use & 1, 2);
-                        __syncwarp();                            // elect.sync below needs a converged warp
-                        if (prof) ph[5] += sd::gtimer() - w0;
-                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                        {
-                            const uint32_t sW = smem_u32(smem + st * stage_bytes);
-                            const uint32_t sWlo = sW + wa_bytes;
-                            const uint32_t sH = sW + (X3 ? 2 : 1) * wa_bytes;
-                            const uint32_t sHlo = sH + hb_bytes;
-#pragma unroll
-                            for (int ks = 0; ks < KC_B / 32; ks++) {     // 8 tf32 (32 B) of K per MMA
-                                const uint64_t b_hi = make_desc_sw<KC_B>(sH + ks * 32);
-                                const uint64_t b_lo = make_desc_sw<KC_B>(sHlo + ks * 32);
-                                for (int mt = 0; mt < nmt; mt++) {
-                                    const uint32_t d = tmem + (uint32_t)(mt * BM);
-                                    const uint32_t mo = (uint32_t)mt * BM * KC_B;
-                                    const uint64_t a_hi = make_desc_sw<KC_B>(sW + mo + ks * 32);
-                                    mma_elect<false>(d, a_hi, b_hi, idesc, (kc > 0 || ks > 0) ? 1u : 0u);
-                                    if (X3) {
-                                        const uint64_t a_lo = make_desc_sw<KC_B>(sWlo + mo + ks * 32);
-                                        mma_elect<false>(d, a_hi, b_lo, idesc, 1u);
-                                        mma_elect<false>(d, a_lo, b_hi, idesc, 1u);
+                        const int k0 = kc * KE;
+                        for (int idx = ltid; idx < nitems; idx += LT) {
+                            const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
+                            const int row = g8 * 8 + r8;
+                            if (row >= nr) continue;
+                            const int kk = k0 + c * 4;
+                            const bool ok = kk < H;
+                            const int src = Q.pr_inrow[q0 + row];
+                            cp_async16(smem_u32(sH + swz_off<KC_B>(row, c)),
+                                       ok ? (const void *)(S.arena_h + (size_t)src * H + kk) : (const void *)S.arena_h, ok);
+                        }
+                        cp_async_commit();
+                    };
+                    auto consume = [&](int st, int pending) {
+                        sd::cp_wait_n(pending);
+                        uint8_t *sH = smem + st * stage_bytes + (X3 ? 2 : 1) * wa_bytes;
+                        for (int idx = ltid; idx < nitems; idx += LT) {
+                            const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
+                            const int row = g8 * 8 + r8;
+                            if (row >= nr) continue;
+                            const uint32_t off = swz_off<KC_B>(row, c);
+                            const float4 x = *reinterpret_cast<const float4 *>(sH + off);
+                            float4 hi;
+                            hi.x = tf32_rn(x.x); hi.y = tf32_rn(x.y); hi.z = tf32_rn(x.z); hi.w = tf32_rn(x.w);
+                            *reinterpret_cast<float4 *>(sH + off) = hi;
+                            if (X3) {
+                                float4 lo;
+                                lo.x = tf32_rn(x.x - hi.x); lo.y = tf32_rn(x.y - hi.y);
+                                lo.z = tf32_rn(x.z - hi.z); lo.w = tf32_rn(x.w - hi.w);
+                                *reinterpret_cast<float4 *>(sH + hb_bytes + off) = lo;
+                            }
+                        }
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0)
+                            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&bar_full[st])) : "memory");
+                    };
+                    if (wid == 0) {
+                        const uint32_t idesc = make_idesc(2, nn);
+                        for (int kc = 0; kc < NK; kc++) {
+                            const int st = (int)((gctr + kc) % (uint32_t)stages);
+                            const uint32_t use = (gctr + kc) / (uint32_t)stages;
+                            const unsigned long long w0 = prof ? sd::gtimer() : 0ull;
+                            sd::wait_bounded(smem_u32(&bar_full[st]), use & 1, 2);
+                            __syncwarp();                            // elect.sync below needs a converged warp
+                            if (prof) ph[9] += sd::gtimer() - w0;
+                            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                            {
+                                const uint32_t sW = smem_u32(smem + st * stage_bytes);
+                                const uint32_t sWlo = sW + wa_bytes;
+                                const uint32_t sH = sW + (X3 ? 2 : 1) * wa_bytes;
+                                const uint32_t sHlo = sH + hb_bytes;
+    #pragma unroll
+                                for (int ks = 0; ks < KC_B / 32; ks++) {     // 8 tf32 (32 B) of K per MMA
+                                    const uint64_t b_hi = make_desc_sw<KC_B>(sH + ks * 32);
+                                    const uint64_t b_lo = make_desc_sw<KC_B>(sHlo + ks * 32);
+                                    for (int mt = 0; mt < nmt; mt++) {
+                                        const uint32_t d = tmem + (uint32_t)(mt * BM);
+                                        const uint32_t mo = (uint32_t)mt * BM * KC_B;
+                                        const uint64_t a_hi = make_desc_sw<KC_B>(sW + mo + ks * 32);
+                                        mma_elect<false>(d, a_hi, b_hi, idesc, (kc > 0 || ks > 0) ? 1u : 0u);
+                                        if (X3) {
+                                            const uint64_t a_lo = make_desc_sw<KC_B>(sWlo + mo + ks * 32);
+                                            mma_elect<false>(d, a_hi, b_lo, idesc, 1u);
+                                            mma_elect<false>(d, a_lo, b_hi, idesc, 1u);
+                                        }
                                     }
                                 }
+                                commit_elect(smem_u32(&bar_empty[st]));
+                                if (kc == NK - 1) commit_elect(smem_u32(&bar_done));
                             }
-                            commit_elect(smem_u32(&bar_empty[st]));
-                            if (kc == NK - 1) commit_elect(smem_u32(&bar_done));
+                            __syncwarp();
                         }
-                        __syncwarp();
-                    }
-                } else {
-                    const int pre = min(stages - 1, NK);
-                    for (int j = 0; j < pre; j++) {
-                        const uint32_t gc = gctr + j;
-                        issue((int)(gc % (uint32_t)stages), gc / (uint32_t)stages, j);
-                    }
-                    for (int kc = 0; kc < NK; kc++) {
-                        const uint32_t gc = gctr + kc;
-                        consume((int)(gc % (uint32_t)stages), min(stages - 2, NK - 1 - kc));
-                        if (kc + stages - 1 < NK) {
-                            const uint32_t gi = gc + stages - 1;
-                            issue((int)(gi % (uint32_t)stages), gi / (uint32_t)stages, kc + stages - 1);
+                    } else {
+                        const int pre = min(stages - 1, NK);
+                        for (int j = 0; j < pre; j++) {
+                            const uint32_t gc = gctr + j;
+                            issue((int)(gc % (uint32_t)stages), gc / (uint32_t)stages, j);
                         }
-                    }
-                }
-                gctr += NK;
-                SD_MARK(1);
-                // epilogue: TMEM lane = output unit, column = row of the tile
-                sd::wait_bounded(smem_u32(&bar_done), tiles_done & 1, 3);
-                tiles_done++;
-                __syncwarp();
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                {
-                    const int quad = wid & 3;
-                    const int nch = (nr + 31) / 32;
-                    for (int it = wid >> 2; it < nmt * nch; it += NW / 4) {
-                        const int mt = it / nch, ch = it - mt * nch;
-                        const int unit = mt * BM + quad * 32 + lane;
-                        float v[32];
-                        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(mt * BM + ch * 32), v);
-                        unsigned long long dg[32];
-                        // lane j fetches row j's word once; rows are broadcast below
-                        const int wl = ch * 32 + lane < nr ? Q.pr_w[q0 + ch * 32 + lane] : 0;
-                        const float *ucol = m.U + unit;
-                        float *ocol = S.arena_h + (size_t)(base + q0 + ch * 32) * H + unit;
-#pragma unroll
-                        for (int j = 0; j < 32; j++) {
-                            dg[j] = 0ull;
-                            const int wq = __shfl_sync(0xffffffffu, wl, j);
-                            if (ch * 32 + j < nr && unit < H) {
-                                const float o = __frcp_rn(1.f + expf(-(v[j] + __ldg(ucol + (size_t)wq * H))));   // == 1/x, IEEE
-                                ocol[(size_t)j * H] = o;
-                                dg[j] = otf_dig_h((uint32_t)unit, o);
+                        for (int kc = 0; kc < NK; kc++) {
+                            const uint32_t gc = gctr + kc;
+                            consume((int)(gc % (uint32_t)stages), min(stages - 2, NK - 1 - kc));
+                            if (kc + stages - 1 < NK) {
+                                const uint32_t gi = gc + stages - 1;
+                                issue((int)(gi % (uint32_t)stages), gi / (uint32_t)stages, kc + stages - 1);
                             }
                         }
-                        const unsigned long long tot = sd::transpose_sum32(dg, lane);
-                        const int row = ch * 32 + lane;
-                        if (row < nr) atomicAdd(&Q.pr_dig[q0 + row], tot);
                     }
+                    gctr += NK;
+                    if (tid == 0) SD_MARK(1);
+                    // epilogue: TMEM lane = output unit, column = row of the tile
+                    sd::wait_bounded(smem_u32(&bar_done), tiles_done & 1, 3);
+                    if (tid == 0) SD_MARK(2);
+                    tiles_done++;
+                    __syncwarp();
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    {
+                        const int quad = wid & 3;
+                        const int nch = (nr + 31) / 32;
+                        for (int it = wid >> 2; it < nmt * nch; it += sd::GW / 4) {
+                            const int mt = it / nch, ch = it - mt * nch;
+                            const int unit = mt * BM + quad * 32 + lane;
+                            float v[32];
+                            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(mt * BM + ch * 32), v);
+                            // lane j fetches row j's word once; rows are broadcast below.
+                            // Rows go in groups of 8: the 8 U loads of a group are in
+                            // flight together, and the group's digest terms are reduced
+                            // with the 9-exchange reduce8 pattern (the sum for row g of
+                            // the group lands on the lanes whose bits 4,3,2 spell g).
+                            const int wl = ch * 32 + lane < nr ? Q.pr_w[q0 + ch * 32 + lane] : 0;
+                            const float *ucol = m.U + unit;
+                            float *ocol = S.arena_h + (size_t)(base + q0 + ch * 32) * H + unit;
+    #pragma unroll
+                            for (int jg = 0; jg < 32; jg += 8) {
+                                float uv[8];
+    #pragma unroll
+                                for (int g = 0; g < 8; g++) {
+                                    const int wq = __shfl_sync(0xffffffffu, wl, jg + g);
+                                    uv[g] = (ch * 32 + jg + g < nr && unit < H) ? __ldg(ucol + (size_t)wq * H) : 0.f;
+                                }
+                                unsigned long long dg[8];
+    #pragma unroll
+                                for (int g = 0; g < 8; g++) {
+                                    dg[g] = 0ull;
+                                    const int j = jg + g;
+                                    if (ch * 32 + j < nr && unit < H) {
+                                        const float o = __frcp_rn(1.f + expf(-(v[j] + uv[g])));   // == 1/x, IEEE
+                                        ocol[(size_t)j * H] = o;
+                                        dg[g] = otf_dig_h((uint32_t)unit, o);
+                                    }
+                                }
+                                const unsigned long long tot = sd::reduce8_u64(dg, lane);
+                                const int row = ch * 32 + jg + node_of_lane(lane);
+                                if ((lane & 3) == 0 && row < nr) atomicAdd(&Q.pr_dig[q0 + row], tot);
+                            }
+                        }
+                    }
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    sd::group_sync(1, sd::GT);
+                    if (tid == 0) SD_MARK(3);
                 }
-                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                __syncthreads();
-                SD_MARK(2);
+            } else {
+                if (tid == sd::GT && prof) t0 = sd::gtimer();
+                small_lm_scores(Q, S, g, sid, L.re - L.rb, tid - sd::GT, sd::NT - sd::GT);
+                // ------------- HS + MaxEnt of the computed requests -------------
+                hs_level_nodepar<CPL, ORD, sd::NT - sd::GT, 2>(m, Q, S, base, n, hsm, qb_max, tid - sd::GT,
+                                                               wid - sd::GW, lane, prof ? ph : nullptr);
+                if (tid == sd::GT) SD_MARK(6);
             }
-            // ------------- HS + MaxEnt of the computed requests -------------
-            hs_level_nodepar<CPL, ORD>(m, Q, S, base, n, hsm, qb_max, tid, wid, lane);
             __syncthreads();
-            SD_MARK(3);
+            if (tid == 0) SD_MARK(8);       // wait of the update group for the HS group
+        } else {
+            small_lm_scores(Q, S, g, sid, L.re - L.rb, tid, NT);
+            __syncthreads();
         }
         // ---------------- assign ----------------
         const StreamRange rg{sid, 0u, L.re - L.rb, 0u};
         const LevelCtr lc{n, base, 0u, 0u};
         assign_range<0, NT>(Q, S, L.t, rg, lc, row_limit, lm_weight, nullptr, nullptr, nullptr, asmem);
         __syncthreads();
-        SD_MARK(4);
+        if (tid == 0) SD_MARK(7);
     }
     if (prof) {
-        ph[7] = 1;
-        for (int i = 0; i < 8; i++) atomicAdd(&P.phase_ns[i], ph[i]);
+        ph[11] = tid == 0 ? 1 : 0;
+        for (int i = 0; i < 12; i++) atomicAdd(&P.phase_ns[i], ph[i]);
     }
 #undef SD_MARK
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

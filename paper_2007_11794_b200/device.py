@@ -254,12 +254,14 @@ class Plan:
     def phase_ns(self) -> dict:
         """Stream schedule, after ``profile``: device ns per phase summed over
         CTAs (utterance streams)."""
-        o = np.zeros(8, np.int64)
+        o = np.zeros(12, np.int64)
         _lib.check(_lib.load().otflm_plan_phase_ns(self.handle, o.ctypes.data, current_stream_ptr()),
                    "phase_ns")
-        return {"expand": int(o[0]), "update_mma": int(o[1]), "update_epilogue": int(o[2]),
-                "hs": int(o[3]), "assign": int(o[4]), "wait_full": int(o[5]), "wait_empty": int(o[6]),
-                "ctas": int(o[7])}
+        names = ("expand", "update_kloop", "update_drain", "update_epilogue", "hs_setup", "hs_pairs",
+                 "hs_group_total", "assign", "update_group_waits_for_hs", "mma_wait_operands")
+        out = {k: int(o[i]) for i, k in enumerate(names)}
+        out["ctas"] = int(o[11])
+        return out
 
     def set_schedule(self, schedule: str) -> None:
         """"level" (level-synchronous kernels, CUDA graph) or "stream"
