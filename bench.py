@@ -333,7 +333,7 @@ def main():
         ph = dec.plan.phase_ns()
         n_lv = max(1, args.frames)
         phases = {k: round(ph[k] / max(ph["ctas"], 1) / n_lv / 1e3, 3)
-                  for k in ("expand", "update_mma", "update_epilogue", "hs", "assign", "wait_full", "wait_empty")}
+                  for k in ph if k != "ctas"}
 
     # ---- end to end through the public API: host lattices in, 1-best out;
     # two different batches alternate (same compiled structure -> the plans
