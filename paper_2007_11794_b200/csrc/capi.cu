@@ -680,7 +680,15 @@ struct OtflmPlan {
     int32_t schedule = OTFLM_SCHED_LEVEL;      // level-synchronous or persistent per-stream
     uint32_t ws_cap = 0;                       // request / primary workspace entries
     uint32_t ul_cap = 0;                       // UttLevel entries
+    // pinned staging for otflm_plan_refresh: the uploads are truly
+    // asynchronous, so compiling the next batch on the host overlaps the
+    // decode of the current one; ev_staged guards reuse of the buffer
+    uint8_t *staging = nullptr;
+    size_t staging_cap = 0;
+    cudaEvent_t ev_staged = nullptr;
     ~OtflmPlan() {
+        if (staging) cudaFreeHost(staging);
+        if (ev_staged) cudaEventDestroy(ev_staged);
         if (side) cudaStreamDestroy(side);
         if (chain) cudaStreamDestroy(chain);
         if (ev_fork) cudaEventDestroy(ev_fork);
@@ -996,8 +1004,30 @@ extern "C" int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *L, int3
         tmp.lvl_req != p->lvl_req || tmp.lvl_range_off != p->lvl_range_off || utt_stream != p->utt_stream_host)
         return OTFLM_ERR_VALUE;
     DevPlan &d = p->d;
+    // stage every array in one pinned buffer, then issue async copies
+    size_t need = 0;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    need += al(nodes.size() * sizeof(NodeInfo)) + al(level_nodes.size() * 4) + al(out_list.size() * 4) +
+            al(arc_slot.size() * 4) + al(arc_word.size() * 4) + al(arc_ac.size() * 8) + al(arc_slm.size() * 8) +
+            al(start_slot.size() * 4) + al(final_off.size() * 4) + al(finals.size() * 4) +
+            al(ranges.size() * sizeof(StreamRange)) + al(ul.size() * sizeof(UttLevel)) + al(ul_off.size() * 4) +
+            al(rq_off.size() * 4);
+    if (p->ev_staged) CK(cudaEventSynchronize(p->ev_staged));     // previous uploads left the buffer
+    if (need > p->staging_cap) {
+        if (p->staging) cudaFreeHost(p->staging);
+        p->staging = nullptr;
+        p->staging_cap = 0;
+        CK(cudaMallocHost((void **)&p->staging, need));
+        p->staging_cap = need;
+    }
+    if (!p->ev_staged) CK(cudaEventCreateWithFlags(&p->ev_staged, cudaEventDisableTiming));
+    size_t pos = 0;
     auto put = [&](const void *dst, const void *src, size_t bytes) -> cudaError_t {
-        return bytes ? cudaMemcpyAsync((void *)dst, src, bytes, cudaMemcpyHostToDevice, s) : cudaSuccess;
+        if (!bytes) return cudaSuccess;
+        std::memcpy(p->staging + pos, src, bytes);
+        cudaError_t e = cudaMemcpyAsync((void *)dst, p->staging + pos, bytes, cudaMemcpyHostToDevice, s);
+        pos += al(bytes);
+        return e;
     };
     CK(put(d.nodes, nodes.data(), nodes.size() * sizeof(NodeInfo)));
     CK(put(d.level_nodes, level_nodes.data(), level_nodes.size() * 4));
@@ -1013,6 +1043,7 @@ extern "C" int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *L, int3
     CK(put(d.ul, ul.data(), ul.size() * sizeof(UttLevel)));
     CK(put(d.ul_off, ul_off.data(), ul_off.size() * 4));
     CK(put(d.rq_off, rq_off.data(), rq_off.size() * 4));
+    CK(cudaEventRecord(p->ev_staged, s));
     *same = 1;
     return OTFLM_OK;
 }

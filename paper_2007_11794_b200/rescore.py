@@ -341,7 +341,7 @@ class BatchDecoder:
 
     def __init__(self, model, tree, small_lm, n_streams: int, max_contexts: int,
                  enabled: bool = True, precision: str = "fp64", n_groups: int = 1,
-                 schedule: str = "auto"):
+                 schedule: str = "auto", n_buffers: int = 1):
         self.model, self.tree = model, tree
         self.dmodel = DeviceModel.get(model, tree)
         self.ngram = DeviceNgram.get(small_lm, self.dmodel)
@@ -363,6 +363,23 @@ class BatchDecoder:
         self.plans = []
         self.group = None
         self.plan = None
+        # n_buffers = 2: two plan sets used alternately, so the host compile +
+        # upload of batch i+1 (prepare) overlaps the decode of batch i
+        self.n_buffers = max(1, int(n_buffers))
+        self._slots = [dict(plans=[], spans=[], group=None, plan=None, beam=None)
+                       for _ in range(self.n_buffers)]
+        self._cur = 0
+        self._next = 0
+
+    def _activate(self, slot: int) -> None:
+        st = self._slots[slot]
+        self.plans, self.spans, self.group, self.plan = st["plans"], st["spans"], st["group"], st["plan"]
+        self.beam = st["beam"]
+        self._cur = slot
+
+    def _store(self, slot: int) -> None:
+        self._slots[slot].update(plans=self.plans, spans=self.spans, group=self.group, plan=self.plan,
+                                 beam=getattr(self, "beam", None))
 
     @staticmethod
     def contexts_needed(lattices, beam: int) -> int:
@@ -376,10 +393,19 @@ class BatchDecoder:
         return worst + 1
 
     def prepare(self, lattices, beam: int):
-        """Compile + upload a batch.  A batch with the same compiled
-        structure as the previous one (same beam, same level/node/arc
-        counts) is loaded into the existing plans so the captured graph is
-        replayed; otherwise new plans are built."""
+        """Compile + upload a batch into the next plan buffer and make it the
+        current one (returns the buffer index for run / fetch).  A batch with
+        the same compiled structure as the buffer's previous one is loaded
+        into the existing plans (captured graphs are replayed); otherwise new
+        plans are built."""
+        slot = self._next
+        self._next = (self._next + 1) % self.n_buffers
+        self._activate(slot)
+        self._prepare(lattices, beam)
+        self._store(slot)
+        return slot
+
+    def _prepare(self, lattices, beam: int):
         lattices = list(lattices)
         G = min(self.n_groups, len(lattices))
         bounds = np.linspace(0, len(lattices), G + 1).astype(int)
@@ -404,7 +430,9 @@ class BatchDecoder:
         self.plan = self.plans[0]
         return self.plans
 
-    def run(self, lm_weight: float = 1.0, use_graph: bool = True) -> None:
+    def run(self, lm_weight: float = 1.0, use_graph: bool = True, slot: int | None = None) -> None:
+        if slot is not None:
+            self._activate(slot)
         self.streams.reset(retain=False)
         if self.group is not None:
             self.group.run(self.ngram, lm_weight, self.precision)
@@ -424,7 +452,9 @@ class BatchDecoder:
                 tot[k] = tot.get(k, 0) + v
         return tot
 
-    def fetch(self):
+    def fetch(self, slot: int | None = None):
+        if slot is not None:
+            self._activate(slot)
         hyps, outs = [], []
         for p in self.plans:
             out = p.fetch()
