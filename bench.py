@@ -348,8 +348,8 @@ def main():
     dec.run(1.0, use_graph=True, slot=s_prev)
     for i in range(1, 3):                                 # both buffers built and warm
         s_cur = dec.prepare(batches[i % 2], setup.beam)
-        dec.fetch(slot=s_prev)
         dec.run(1.0, use_graph=True, slot=s_cur)
+        dec.fetch(slot=s_prev)
         s_prev = s_cur
     torch.cuda.synchronize()
     if world > 1:
@@ -360,12 +360,12 @@ def main():
     a.record(stream)
     for i in range(1, n_e2e + 1):
         s_cur = dec.prepare(batches[i % 2], setup.beam)   # host compile + H2D, overlaps the decode of s_prev
-        h2, o2 = dec.fetch(slot=s_prev)                   # D2H of the previous batch's 1-best
+        dec.run(1.0, use_graph=True, slot=s_cur)          # queued behind s_prev on the GPU
+        h2, o2 = dec.fetch(slot=s_prev)                   # D2H of s_prev's 1-best (copy stream) while s_cur decodes
         if world > 1:
             rec = torch.from_numpy(np.concatenate([o2["combined"], o2["path_len"].astype(np.float64)])).cuda()
             gathered = [torch.empty_like(rec) for _ in range(world)]
             dist.all_gather(gathered, rec)                # NCCL: results only
-        dec.run(1.0, use_graph=True, slot=s_cur)
         s_prev = s_cur
     h2, o2 = dec.fetch(slot=s_prev)
     b.record(stream)

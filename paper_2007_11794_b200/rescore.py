@@ -23,7 +23,7 @@ from typing import Sequence
 import numpy as np
 
 from . import _lib
-from .device import DeviceModel, DeviceNgram, DeviceStreams, Plan, PlanGroup
+from .device import DeviceModel, DeviceNgram, DeviceStreams, Plan, PlanGroup, cuda
 from .model import RnnlmContext
 
 ENTRY_BYTES = 32          # cache.py:26
@@ -366,8 +366,9 @@ class BatchDecoder:
         # n_buffers = 2: two plan sets used alternately, so the host compile +
         # upload of batch i+1 (prepare) overlaps the decode of batch i
         self.n_buffers = max(1, int(n_buffers))
-        self._slots = [dict(plans=[], spans=[], group=None, plan=None, beam=None)
+        self._slots = [dict(plans=[], spans=[], group=None, plan=None, beam=None, done=None)
                        for _ in range(self.n_buffers)]
+        self._side = None            # copy stream for fetch (waits only for its own batch)
         self._cur = 0
         self._next = 0
 
@@ -438,6 +439,11 @@ class BatchDecoder:
             self.group.run(self.ngram, lm_weight, self.precision)
         else:
             self.plan.run(self.ngram, lm_weight, self.precision, use_graph=use_graph)
+        if self.n_buffers > 1:           # completion of this batch, for fetch on the copy stream
+            torch = cuda()
+            ev = torch.cuda.Event()
+            ev.record()
+            self._slots[self._cur]["done"] = ev
 
     def profile(self, lm_weight: float = 1.0) -> dict:
         self.streams.reset(retain=False)
@@ -455,9 +461,19 @@ class BatchDecoder:
     def fetch(self, slot: int | None = None):
         if slot is not None:
             self._activate(slot)
+        stream = None
+        done = self._slots[self._cur].get("done") if self.n_buffers > 1 else None
+        if done is not None:
+            # read this batch's results on a copy stream that waits only for
+            # its own decode, not for a later batch already queued behind it
+            torch = cuda()
+            if self._side is None:
+                self._side = torch.cuda.Stream()
+            self._side.wait_event(done)
+            stream = self._side.cuda_stream
         hyps, outs = [], []
         for p in self.plans:
-            out = p.fetch()
+            out = p.fetch(stream=stream)
             offs = p.arrays["arc_off"]
             hyps += [_hyp(out, u, p.lats[u], int(offs[u])) for u in range(p.n_utt)]
             outs.append(out)

@@ -303,3 +303,33 @@ def test_stream_schedule_tf32_single_pass():
     for u, (r, _) in enumerate(ref):
         assert abs(hyps[u].combined_score - r.combined_score) <= 2e-3 * 40
         assert int(out["expansions"][u]) == r.expansions
+
+
+def test_double_buffered_pipeline_matches_single_batches():
+    """BatchDecoder(n_buffers=2): prepare(i+1) / run(i+1) are queued while
+    batch i is fetched on the copy stream; every batch's results equal a
+    fresh single-buffer decode of the same batch."""
+    from paper_2007_11794_b200 import synth
+    from paper_2007_11794_b200.rescore import BatchDecoder
+    s = synth.build_setup("a", n_utt=6, T=40, seed=5)
+    batches = [s.lattices] + [synth.more_lattices(s, 6, 40, seed=20 + i) for i in range(3)]
+    need = max(BatchDecoder.contexts_needed(b, 8) for b in batches)
+    ref = []
+    for b in batches:
+        d1 = BatchDecoder(s.model, s.tree, s.small_lm, 6, need, precision="tf32x3")
+        d1.prepare(b, 8)
+        d1.run(1.0)
+        ref.append(d1.fetch()[0])
+    dec = BatchDecoder(s.model, s.tree, s.small_lm, 6, need, precision="tf32x3", n_buffers=2)
+    prev = dec.prepare(batches[0], 8)
+    dec.run(1.0, slot=prev)
+    got = []
+    for b in batches[1:]:
+        cur = dec.prepare(b, 8)
+        dec.run(1.0, slot=cur)
+        got.append(dec.fetch(slot=prev)[0])
+        prev = cur
+    got.append(dec.fetch(slot=prev)[0])
+    for r, g in zip(ref, got):
+        assert [h.arcs for h in r] == [h.arcs for h in g]
+        assert [h.combined_score for h in r] == [h.combined_score for h in g]
