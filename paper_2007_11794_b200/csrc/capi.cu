@@ -1166,16 +1166,16 @@ static bool sd_config(const DevModel &m, int prec, SdConfig *c) {
     if (!m.W_t || m.H % 4 != 0 || m.wt_npad > 512 || !m.U || !m.NV || !m.path_off) return false;
     const bool x3 = prec == OTFLM_PREC_TF32X3;
     const size_t stage = (x3 ? 2u : 1u) * ((size_t)m.wt_npad * m.wt_kcb + (size_t)tc::BM * m.wt_kcb);
-    const size_t budget = 204u * 1024u;                   // + ~21 KB static shared memory
-    // the update's ring and the HS scratch are live at the same time (the
-    // two warp groups run concurrently): 2 ring stages, the rest for HS
+    const size_t budget = 200u * 1024u;                   // + ~21 KB static shared memory
+    // rank 1 (update) uses the dynamic shared memory as its ring, rank 0
+    // (control) as the HS scratch: one size serves both
+    c->stages = (int)std::min<size_t>(4, budget / stage);
+    if (c->stages < 2) return false;
     const int ord = m.order <= 3 ? 3 : OTF_MAX_ORDER;
     const size_t hs_fixed = (size_t)sd::PAIRCAP * 13 + (size_t)sd::QMAX * (ord * 8 + 7 * 4) + (sd::NW + 2) * 4 + 64;
-    c->stages = 2;
-    const size_t ring = (size_t)c->stages * stage;
-    if (ring + hs_fixed + 8 * 4 * (size_t)m.H > budget) return false;
-    c->qb_max = (int)std::min<size_t>(sd::QMAX, (budget - ring - hs_fixed) / (4 * (size_t)m.H));
-    c->smem = ring + hs_fixed + (size_t)c->qb_max * 4 * m.H;
+    if (hs_fixed + 8 * 4 * (size_t)m.H > budget) return false;
+    c->qb_max = (int)std::min<size_t>(sd::QMAX, (budget - hs_fixed) / (4 * (size_t)m.H));
+    c->smem = std::max((size_t)c->stages * stage, hs_fixed + (size_t)c->qb_max * 4 * m.H);
     c->tmem_cols = 128;
     while ((int)c->tmem_cols < m.wt_npad) c->tmem_cols <<= 1;
     return true;
@@ -1193,7 +1193,7 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
 #define SD_LAUNCH(MODE, KCB, CPL, ORD)                                                                          \
     do {                                                                                                        \
         CK(cudaFuncSetAttribute(k_decode_streams<MODE, KCB, CPL, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem)); \
-        k_decode_streams<MODE, KCB, CPL, ORD><<<p->n_utt, sd::NT, c.smem, s>>>(m, d, S, g->d, (long long)p->beam, lm, \
+        k_decode_streams<MODE, KCB, CPL, ORD><<<2 * p->n_utt, sd::NT, c.smem, s>>>(m, d, S, g->d, (long long)p->beam, lm, \
                                                                               c.stages, c.qb_max, cursor, limit, c.tmem_cols); \
     } while (0)
 #define SD_ORD(MODE, KCB, CPL) do { if (m.order <= 3) SD_LAUNCH(MODE, KCB, CPL, 3); else SD_LAUNCH(MODE, KCB, CPL, OTF_MAX_ORDER); } while (0)

@@ -31,6 +31,7 @@
 #pragma once
 #include "decode.cuh"
 #include "tc_advance.cuh"
+#include <cooperative_groups.h>
 
 namespace sd {
 constexpr int NT = 512;
@@ -325,11 +326,21 @@ __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, 
 }
 
 // MODE 1 = TF32X3, 3 = TF32; KC_B = m.wt_kcb; CPL/ORD as RING_DISPATCH.
+// A cluster of two CTAs per stream: rank 0 (control) runs expand, the
+// small-LM scores + HS and assign; rank 1 (update) runs the tcgen05 recurrent
+// update and its epilogue.  Per level:
+//   rank 0: expand -> rows -> [cluster barrier A] -> small-LM + HS -> [B] -> assign
+//   rank 1:                   [A] -> update + epilogue                 -> [B]
+// The row count / arena base / abort flag cross over DSMEM after A; every
+// global write before a barrier is visible after it (release / acquire at
+// cluster scope).  Each role has a whole SM: 16 warps and the full shared
+// memory (4-stage update ring on rank 1, single-batch HS staging on rank 0).
 template <int MODE, int KC_B, int CPL, int ORD>
-__global__ void __launch_bounds__(sd::NT, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sd::NT, 1)
 k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, double lm_weight, int stages,
                  int qb_max, uint32_t *cursor, uint32_t row_limit, uint32_t tmem_cols) {
     using namespace tc;
+    namespace cg = cooperative_groups;
     constexpr bool X3 = MODE == 1;
     constexpr int NT = sd::NT, NW = sd::NW;
     constexpr int KE = KC_B / 4;            // tf32 elements of K per chunk
@@ -342,27 +353,29 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     __shared__ __align__(8) uint64_t bar_full[4], bar_empty[4], bar_done;
     __shared__ uint32_t s_tmem, s_nprim, s_base, s_abort;
 
+    cg::cluster_group cluster = cg::this_cluster();
+    const unsigned rank = cluster.block_rank();
     const int tid = threadIdx.x, lane = tid & 31;
     const int wid = __shfl_sync(0xffffffffu, tid >> 5, 0);     // provably warp-uniform
-    const uint32_t u = blockIdx.x;
-    if (u >= P.n_utt) return;
+    const uint32_t u = blockIdx.x >> 1;                        // stream of this cluster
     const int H = m.H;
-    const int nmt = m.wt_npad / BM;                      // M tiles of output units
-    const uint32_t wa_bytes = (uint32_t)m.wt_npad * KC_B;  // one W block (hi or lo)
-    const uint32_t hb_bytes = BM * KC_B;                 // one row block (hi or lo)
+    const int nmt = m.wt_npad / BM;                            // M tiles of output units
+    const uint32_t wa_bytes = (uint32_t)m.wt_npad * KC_B;      // one W block (hi or lo)
+    const uint32_t hb_bytes = BM * KC_B;                       // one row block (hi or lo)
     const uint32_t stage_bytes = (X3 ? 2u : 1u) * (wa_bytes + hb_bytes);
     const int NK = (H + KE - 1) / KE;
 
     if (tid == 0) {
         for (int st = 0; st < stages; st++) {
-            mbar_init(smem_u32(&bar_full[st]), sd::GW);   // one per loader warp + the W copy
+            mbar_init(smem_u32(&bar_full[st]), NW);           // one per loader warp + the W copy
             mbar_init(smem_u32(&bar_empty[st]), 1);
         }
         mbar_init(smem_u32(&bar_done), 1);
         s_abort = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (wid == 0) {
+    uint32_t tmem = 0;
+    if (rank == 1 && wid == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      :: "r"(smem_u32(&s_tmem)), "r"(tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -370,26 +383,29 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = s_tmem;
+    if (rank == 1) tmem = s_tmem;
+    // rank 0's row count / base / abort flag, read by rank 1 over DSMEM
+    const uint32_t *r0_nprim = cluster.map_shared_rank(&s_nprim, 0);
+    const uint32_t *r0_base = cluster.map_shared_rank(&s_base, 0);
+    const uint32_t *r0_abort = cluster.map_shared_rank(&s_abort, 0);
 
     // this utterance's request / primary workspace
     DevPlan Q = P;
-    {
+    if (u < P.n_utt) {
         const uint32_t o = P.rq_off[u];
         Q.rq_c += o; Q.rq_arc += o; Q.rq_parent += o; Q.rq_cslot += o; Q.rq_m += o; Q.rq_dslot += o;
         Q.rq_w += o; Q.rq_state += o; Q.rq_score += o; Q.rq_slm += o; Q.rq_ps += o;
         Q.pr_req += o; Q.pr_inrow += o; Q.pr_w += o; Q.pr_p += o; Q.pr_dig += o;
     }
-    const uint32_t sid = P.utt_stream[u];
+    const uint32_t sid = u < P.n_utt ? P.utt_stream[u] : 0u;
     const AssignSmem asmem{a_key, a_row, a_cn, a_wsum, a_cnt};
-    uint32_t gctr = 0;          // K chunks through the ring so far (uniform)
+    uint32_t gctr = 0;          // K chunks through the ring so far (rank 1, uniform)
     uint32_t tiles_done = 0;
-    // node-parallel HS scratch, in the shared union (free while HS runs)
+    // node-parallel HS scratch (rank 0): the whole dynamic shared memory
     sd::HsLevelSmem hsm;
     {
-        uint8_t *hb = smem + (size_t)stages * stage_bytes;           // after the update's ring
-        uint8_t *p = hb + (size_t)qb_max * 4 * H;
-        hsm.h = reinterpret_cast<float *>(hb);
+        uint8_t *p = smem + (size_t)qb_max * 4 * H;
+        hsm.h = reinterpret_cast<float *>(smem);
         hsm.lsig = reinterpret_cast<double *>(p); p += sd::PAIRCAP * 8;
         hsm.pcode = reinterpret_cast<uint32_t *>(p); p += sd::PAIRCAP * 4;
         hsm.pre = reinterpret_cast<unsigned long long *>(p); p += sd::QMAX * ORD * 8;
@@ -404,237 +420,229 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
         hsm.pq = p;
     }
 
-    // profiling runs only: per-phase device time (ns), summed over CTAs;
-    // thread 0 times the shared phases and the update group, thread GT the
-    // HS group (they run concurrently)
+    // profiling runs only: per-phase device time (ns), summed over streams
+    // (thread 0 of each rank marks its own phases)
     unsigned long long ph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
-    const bool prof = P.phase_ns != nullptr && (tid == 0 || tid == sd::GT);
+    const bool prof = P.phase_ns != nullptr && tid == 0;
 #define SD_MARK(i) do { if (prof) { t1 = sd::gtimer(); ph[i] += t1 - t0; t0 = t1; } } while (0)
     if (prof) t0 = sd::gtimer();
-    for (uint32_t li = P.ul_off[u]; li < P.ul_off[u + 1]; li++) {
+    const uint32_t l_begin = u < P.n_utt ? P.ul_off[u] : 0u, l_end = u < P.n_utt ? P.ul_off[u + 1] : 0u;
+    for (uint32_t li = l_begin; li < l_end; li++) {
         const UttLevel L = P.ul[li];
-        if (tid == 0) s_nprim = 0;
-        __syncthreads();
-        // ---------------- expand ----------------
-        for (uint32_t k = L.nb + wid; k < L.ne; k += NW) {
-            const NodeInfo nd = P.nodes[P.level_nodes[k]];
-            expand_node(Q, S, g, nd, beam, L.t, -(int64_t)L.rb, &s_nprim, e_ctx[wid], e_slot[wid], e_score[wid],
-                        e_arc[wid], lane, /*defer_ps=*/true);
-        }
-        __syncthreads();
-        if (tid == 0) SD_MARK(0);
-        const uint32_t n = s_nprim;
-#ifdef SD_CHECK
-        if (tid == 0 && n > L.re - L.rb) { printf("SD_CHECK n %u > requests %u blk %d\n", n, L.re - L.rb, (int)blockIdx.x); __trap(); }
-#endif
-        if (tid == 0) {
-            uint32_t b = 0;
-            if (n) b = atomicAdd(cursor, n);
-            if ((uint64_t)b + n > row_limit) { atomicOr(S.err, OTF_E_ARENA_FULL); s_abort = 1; }
-            s_base = b;
-        }
-        __syncthreads();
-        if (s_abort) break;
-        const uint32_t base = s_base;
-        if (n) {
-            // The recurrent update (warps 0..GW-1) and the HS + deferred
-            // small-LM scores (warps GW..NW-1) only depend on expand: the two
-            // groups run concurrently on disjoint shared memory, each
-            // synchronising on its own named barrier.
-            if (wid < sd::GW) {
-                // ------------- recurrent update (tcgen05) -------------
-                for (uint32_t q0 = 0; q0 < n; q0 += BM) {
-                    const int nr = (int)min((uint32_t)BM, n - q0);
-                    const int nn = (nr + 15) & ~15;                   // MMA N
-                    const int nitems = ((nr + 7) & ~7) * CH;          // row pieces per chunk
-                    // warp 0: MMA issuer (converged; lane 0 issues).  Warps 1..NW-1:
-                    // loaders / converters -- a divergent issuer inside a loader
-                    // warp would sit behind its siblings' suspended mbarrier waits.
-                    constexpr int LT = sd::GT - 32;                    // loader threads (warps 1..GW-1)
-                    const int ltid = tid - 32;
-                    auto issue = [&](int st, uint32_t use, int kc) {
-                        if (use >= 1) sd::wait_bounded(smem_u32(&bar_empty[st]), (use - 1) & 1, 1);
-                        __syncwarp();                                // lanes leave the wait independently
-                        uint8_t *sW = smem + st * stage_bytes;
-                        uint8_t *sH = sW + (X3 ? 2 : 1) * wa_bytes;
-                        if (wid == 1) {                              // W chunk: one bulk copy, elected lane
-                            const uint32_t bytes = (X3 ? 2u : 1u) * wa_bytes;
-                            const void *src = reinterpret_cast<const uint8_t *>(m.W_t) + (size_t)kc * 2 * wa_bytes;
-                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                            asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 t;\n\telect.sync t|e, 0xffffffff;\n\t"
-                                         "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %3;\n\t"
-                                         "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %3, [%1];\n\t}"
-                                         :: "r"(smem_u32(sW)), "r"(smem_u32(&bar_full[st])), "l"(src), "r"(bytes) : "memory");
-                        }
-                        const int k0 = kc * KE;
-                        for (int idx = ltid; idx < nitems; idx += LT) {
-                            const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
-                            const int row = g8 * 8 + r8;
-                            if (row >= nr) continue;
-                            const int kk = k0 + c * 4;
-                            const bool ok = kk < H;
-                            const int src = Q.pr_inrow[q0 + row];
-                            cp_async16(smem_u32(sH + swz_off<KC_B>(row, c)),
-                                       ok ? (const void *)(S.arena_h + (size_t)src * H + kk) : (const void *)S.arena_h, ok);
-                        }
-                        cp_async_commit();
-                    };
-                    auto consume = [&](int st, int pending) {
-                        sd::cp_wait_n(pending);
-                        uint8_t *sH = smem + st * stage_bytes + (X3 ? 2 : 1) * wa_bytes;
-                        for (int idx = ltid; idx < nitems; idx += LT) {
-                            const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
-                            const int row = g8 * 8 + r8;
-                            if (row >= nr) continue;
-                            const uint32_t off = swz_off<KC_B>(row, c);
-                            const float4 x = *reinterpret_cast<const float4 *>(sH + off);
-                            float4 hi;
-                            hi.x = tf32_rn(x.x); hi.y = tf32_rn(x.y); hi.z = tf32_rn(x.z); hi.w = tf32_rn(x.w);
-                            *reinterpret_cast<float4 *>(sH + off) = hi;
-                            if (X3) {
-                                float4 lo;
-                                lo.x = tf32_rn(x.x - hi.x); lo.y = tf32_rn(x.y - hi.y);
-                                lo.z = tf32_rn(x.z - hi.z); lo.w = tf32_rn(x.w - hi.w);
-                                *reinterpret_cast<float4 *>(sH + hb_bytes + off) = lo;
-                            }
-                        }
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        __syncwarp();
-                        if (lane == 0)
-                            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&bar_full[st])) : "memory");
-                    };
-                    if (wid == 0) {
-                        const uint32_t idesc = make_idesc(2, nn);
-                        for (int kc = 0; kc < NK; kc++) {
-                            const int st = (int)((gctr + kc) % (uint32_t)stages);
-                            const uint32_t use = (gctr + kc) / (uint32_t)stages;
-                            const unsigned long long w0 = prof ? sd::gtimer() : 0ull;
-                            sd::wait_bounded(smem_u32(&bar_full[st]), use & 1, 2);
-                            __syncwarp();                            // elect.sync below needs a converged warp
-                            if (prof) ph[9] += sd::gtimer() - w0;
-                            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                            {
-                                const uint32_t sW = smem_u32(smem + st * stage_bytes);
-                                const uint32_t sWlo = sW + wa_bytes;
-                                const uint32_t sH = sW + (X3 ? 2 : 1) * wa_bytes;
-                                const uint32_t sHlo = sH + hb_bytes;
-    #pragma unroll
-                                for (int ks = 0; ks < KC_B / 32; ks++) {     // 8 tf32 (32 B) of K per MMA
-                                    const uint64_t b_hi = make_desc_sw<KC_B>(sH + ks * 32);
-                                    const uint64_t b_lo = make_desc_sw<KC_B>(sHlo + ks * 32);
-                                    for (int mt = 0; mt < nmt; mt++) {
-                                        const uint32_t d = tmem + (uint32_t)(mt * BM);
-                                        const uint32_t mo = (uint32_t)mt * BM * KC_B;
-                                        const uint64_t a_hi = make_desc_sw<KC_B>(sW + mo + ks * 32);
-                                        mma_elect<false>(d, a_hi, b_hi, idesc, (kc > 0 || ks > 0) ? 1u : 0u);
-                                        if (X3) {
-                                            const uint64_t a_lo = make_desc_sw<KC_B>(sWlo + mo + ks * 32);
-                                            mma_elect<false>(d, a_hi, b_lo, idesc, 1u);
-                                            mma_elect<false>(d, a_lo, b_hi, idesc, 1u);
-                                        }
-                                    }
-                                }
-                                commit_elect(smem_u32(&bar_empty[st]));
-                                if (kc == NK - 1) commit_elect(smem_u32(&bar_done));
-                            }
-                            __syncwarp();
-                        }
-                    } else {
-                        const int pre = min(stages - 1, NK);
-                        for (int j = 0; j < pre; j++) {
-                            const uint32_t gc = gctr + j;
-                            issue((int)(gc % (uint32_t)stages), gc / (uint32_t)stages, j);
-                        }
-                        for (int kc = 0; kc < NK; kc++) {
-                            const uint32_t gc = gctr + kc;
-                            consume((int)(gc % (uint32_t)stages), min(stages - 2, NK - 1 - kc));
-                            if (kc + stages - 1 < NK) {
-                                const uint32_t gi = gc + stages - 1;
-                                issue((int)(gi % (uint32_t)stages), gi / (uint32_t)stages, kc + stages - 1);
-                            }
-                        }
-                    }
-                    gctr += NK;
-                    if (tid == 0) SD_MARK(1);
-                    // epilogue: TMEM lane = output unit, column = row of the tile
-                    sd::wait_bounded(smem_u32(&bar_done), tiles_done & 1, 3);
-                    if (tid == 0) SD_MARK(2);
-                    tiles_done++;
-                    __syncwarp();
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    {
-                        const int quad = wid & 3;
-                        const int nch = (nr + 31) / 32;
-                        for (int it = wid >> 2; it < nmt * nch; it += sd::GW / 4) {
-                            const int mt = it / nch, ch = it - mt * nch;
-                            const int unit = mt * BM + quad * 32 + lane;
-                            float v[32];
-                            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(mt * BM + ch * 32), v);
-                            // lane j fetches row j's word once; rows are broadcast below.
-                            // Rows go in groups of 8: the 8 U loads of a group are in
-                            // flight together, and the group's digest terms are reduced
-                            // with the 9-exchange reduce8 pattern (the sum for row g of
-                            // the group lands on the lanes whose bits 4,3,2 spell g).
-                            const int wl = ch * 32 + lane < nr ? Q.pr_w[q0 + ch * 32 + lane] : 0;
-                            const float *ucol = m.U + unit;
-                            float *ocol = S.arena_h + (size_t)(base + q0 + ch * 32) * H + unit;
-    #pragma unroll
-                            for (int jg = 0; jg < 32; jg += 8) {
-                                float uv[8];
-    #pragma unroll
-                                for (int g = 0; g < 8; g++) {
-                                    const int wq = __shfl_sync(0xffffffffu, wl, jg + g);
-                                    uv[g] = (ch * 32 + jg + g < nr && unit < H) ? __ldg(ucol + (size_t)wq * H) : 0.f;
-                                }
-                                unsigned long long dg[8];
-    #pragma unroll
-                                for (int g = 0; g < 8; g++) {
-                                    dg[g] = 0ull;
-                                    const int j = jg + g;
-                                    if (ch * 32 + j < nr && unit < H) {
-                                        const float o = __frcp_rn(1.f + expf(-(v[j] + uv[g])));   // == 1/x, IEEE
-                                        ocol[(size_t)j * H] = o;
-                                        dg[g] = otf_dig_h((uint32_t)unit, o);
-                                    }
-                                }
-                                const unsigned long long tot = sd::reduce8_u64(dg, lane);
-                                const int row = ch * 32 + jg + node_of_lane(lane);
-                                if ((lane & 3) == 0 && row < nr) atomicAdd(&Q.pr_dig[q0 + row], tot);
-                            }
-                        }
-                    }
-                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-                    sd::group_sync(1, sd::GT);
-                    if (tid == 0) SD_MARK(3);
-                }
-            } else {
-                if (tid == sd::GT && prof) t0 = sd::gtimer();
-                small_lm_scores(Q, S, g, sid, L.re - L.rb, tid - sd::GT, sd::NT - sd::GT);
-                // ------------- HS + MaxEnt of the computed requests -------------
-                hs_level_nodepar<CPL, ORD, sd::NT - sd::GT, 2>(m, Q, S, base, n, hsm, qb_max, tid - sd::GT,
-                                                               wid - sd::GW, lane, prof ? ph : nullptr);
-                if (tid == sd::GT) SD_MARK(6);
+        uint32_t n = 0, base = 0;
+        bool abort = false;
+        if (rank == 0) {
+            if (tid == 0) s_nprim = 0;
+            __syncthreads();
+            // ---------------- expand ----------------
+            for (uint32_t k = L.nb + wid; k < L.ne; k += NW) {
+                const NodeInfo nd = P.nodes[P.level_nodes[k]];
+                expand_node(Q, S, g, nd, beam, L.t, -(int64_t)L.rb, &s_nprim, e_ctx[wid], e_slot[wid], e_score[wid],
+                            e_arc[wid], lane, /*defer_ps=*/true);
             }
             __syncthreads();
-            if (tid == 0) SD_MARK(8);       // wait of the update group for the HS group
-        } else {
-            small_lm_scores(Q, S, g, sid, L.re - L.rb, tid, NT);
-            __syncthreads();
+            n = s_nprim;
+            if (tid == 0) {
+                uint32_t b = 0;
+                if (n) b = atomicAdd(cursor, n);
+                if ((uint64_t)b + n > row_limit) { atomicOr(S.err, OTF_E_ARENA_FULL); s_abort = 1; }
+                s_base = b;
+            }
+            SD_MARK(0);
         }
-        // ---------------- assign ----------------
+        cluster.sync();                                      // A: rows reserved, requests compacted
+        if (rank == 0) { n = s_nprim; base = s_base; abort = s_abort != 0; }
+        else { n = *r0_nprim; base = *r0_base; abort = *r0_abort != 0; if (prof) t0 = sd::gtimer(); }
+        if (abort) break;
+        if (rank == 0) {
+            small_lm_scores(Q, S, g, sid, L.re - L.rb, tid, NT);
+            if (n) hs_level_nodepar<CPL, ORD, NT, 0>(m, Q, S, base, n, hsm, qb_max, tid, wid, lane, prof ? ph : nullptr);
+            SD_MARK(6);
+        } else if (n) {
+            // ------------- recurrent update (tcgen05) -------------
+            for (uint32_t q0 = 0; q0 < n; q0 += BM) {
+                const int nr = (int)min((uint32_t)BM, n - q0);
+                const int nn = (nr + 15) & ~15;                   // MMA N
+                const int nitems = ((nr + 7) & ~7) * CH;          // row pieces per chunk
+                // warp 0: MMA issuer (converged; lane 0 issues).  Warps 1..NW-1:
+                // loaders / converters -- a divergent issuer inside a loader
+                // warp would sit behind its siblings' suspended mbarrier waits.
+                constexpr int LT = NT - 32;                        // loader threads (warps 1..NW-1)
+                const int ltid = tid - 32;
+                auto issue = [&](int st, uint32_t use, int kc) {
+                    if (use >= 1) sd::wait_bounded(smem_u32(&bar_empty[st]), (use - 1) & 1, 1);
+                    __syncwarp();                                // lanes leave the wait independently
+                    uint8_t *sW = smem + st * stage_bytes;
+                    uint8_t *sH = sW + (X3 ? 2 : 1) * wa_bytes;
+                    if (wid == 1) {                              // W chunk: one bulk copy, elected lane
+                        const uint32_t bytes = (X3 ? 2u : 1u) * wa_bytes;
+                        const void *src = reinterpret_cast<const uint8_t *>(m.W_t) + (size_t)kc * 2 * wa_bytes;
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 t;\n\telect.sync t|e, 0xffffffff;\n\t"
+                                     "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %3;\n\t"
+                                     "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %3, [%1];\n\t}"
+                                     :: "r"(smem_u32(sW)), "r"(smem_u32(&bar_full[st])), "l"(src), "r"(bytes) : "memory");
+                    }
+                    const int k0 = kc * KE;
+                    for (int idx = ltid; idx < nitems; idx += LT) {
+                        const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
+                        const int row = g8 * 8 + r8;
+                        if (row >= nr) continue;
+                        const int kk = k0 + c * 4;
+                        const bool ok = kk < H;
+                        const int src = Q.pr_inrow[q0 + row];
+                        cp_async16(smem_u32(sH + swz_off<KC_B>(row, c)),
+                                   ok ? (const void *)(S.arena_h + (size_t)src * H + kk) : (const void *)S.arena_h, ok);
+                    }
+                    cp_async_commit();
+                };
+                auto consume = [&](int st, int pending) {
+                    sd::cp_wait_n(pending);
+                    uint8_t *sH = smem + st * stage_bytes + (X3 ? 2 : 1) * wa_bytes;
+                    for (int idx = ltid; idx < nitems; idx += LT) {
+                        const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
+                        const int row = g8 * 8 + r8;
+                        if (row >= nr) continue;
+                        const uint32_t off = swz_off<KC_B>(row, c);
+                        const float4 x = *reinterpret_cast<const float4 *>(sH + off);
+                        float4 hi;
+                        hi.x = tf32_rn(x.x); hi.y = tf32_rn(x.y); hi.z = tf32_rn(x.z); hi.w = tf32_rn(x.w);
+                        *reinterpret_cast<float4 *>(sH + off) = hi;
+                        if (X3) {
+                            float4 lo;
+                            lo.x = tf32_rn(x.x - hi.x); lo.y = tf32_rn(x.y - hi.y);
+                            lo.z = tf32_rn(x.z - hi.z); lo.w = tf32_rn(x.w - hi.w);
+                            *reinterpret_cast<float4 *>(sH + hb_bytes + off) = lo;
+                        }
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0)
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&bar_full[st])) : "memory");
+                };
+                if (wid == 0) {
+                    const uint32_t idesc = make_idesc(2, nn);
+                    for (int kc = 0; kc < NK; kc++) {
+                        const int st = (int)((gctr + kc) % (uint32_t)stages);
+                        const uint32_t use = (gctr + kc) / (uint32_t)stages;
+                        const unsigned long long w0 = prof ? sd::gtimer() : 0ull;
+                        sd::wait_bounded(smem_u32(&bar_full[st]), use & 1, 2);
+                        __syncwarp();                            // elect.sync below needs a converged warp
+                        if (prof) ph[9] += sd::gtimer() - w0;
+                        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        {
+                            const uint32_t sW = smem_u32(smem + st * stage_bytes);
+                            const uint32_t sWlo = sW + wa_bytes;
+                            const uint32_t sH = sW + (X3 ? 2 : 1) * wa_bytes;
+                            const uint32_t sHlo = sH + hb_bytes;
+#pragma unroll
+                            for (int ks = 0; ks < KC_B / 32; ks++) {     // 8 tf32 (32 B) of K per MMA
+                                const uint64_t b_hi = make_desc_sw<KC_B>(sH + ks * 32);
+                                const uint64_t b_lo = make_desc_sw<KC_B>(sHlo + ks * 32);
+                                for (int mt = 0; mt < nmt; mt++) {
+                                    const uint32_t d = tmem + (uint32_t)(mt * BM);
+                                    const uint32_t mo = (uint32_t)mt * BM * KC_B;
+                                    const uint64_t a_hi = make_desc_sw<KC_B>(sW + mo + ks * 32);
+                                    mma_elect<false>(d, a_hi, b_hi, idesc, (kc > 0 || ks > 0) ? 1u : 0u);
+                                    if (X3) {
+                                        const uint64_t a_lo = make_desc_sw<KC_B>(sWlo + mo + ks * 32);
+                                        mma_elect<false>(d, a_hi, b_lo, idesc, 1u);
+                                        mma_elect<false>(d, a_lo, b_hi, idesc, 1u);
+                                    }
+                                }
+                            }
+                            commit_elect(smem_u32(&bar_empty[st]));
+                            if (kc == NK - 1) commit_elect(smem_u32(&bar_done));
+                        }
+                        __syncwarp();
+                    }
+                } else {
+                    const int pre = min(stages - 1, NK);
+                    for (int j = 0; j < pre; j++) {
+                        const uint32_t gc = gctr + j;
+                        issue((int)(gc % (uint32_t)stages), gc / (uint32_t)stages, j);
+                    }
+                    for (int kc = 0; kc < NK; kc++) {
+                        const uint32_t gc = gctr + kc;
+                        consume((int)(gc % (uint32_t)stages), min(stages - 2, NK - 1 - kc));
+                        if (kc + stages - 1 < NK) {
+                            const uint32_t gi = gc + stages - 1;
+                            issue((int)(gi % (uint32_t)stages), gi / (uint32_t)stages, kc + stages - 1);
+                        }
+                    }
+                }
+                gctr += NK;
+                if (tid == 0) SD_MARK(1);
+                // epilogue: TMEM lane = output unit, column = row of the tile
+                sd::wait_bounded(smem_u32(&bar_done), tiles_done & 1, 3);
+                if (tid == 0) SD_MARK(2);
+                tiles_done++;
+                __syncwarp();
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                {
+                    const int quad = wid & 3;
+                    const int nch = (nr + 31) / 32;
+                    for (int it = wid >> 2; it < nmt * nch; it += NW / 4) {
+                        const int mt = it / nch, ch = it - mt * nch;
+                        const int unit = mt * BM + quad * 32 + lane;
+                        float v[32];
+                        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(mt * BM + ch * 32), v);
+                        // lane j fetches row j's word once; rows are broadcast below.
+                        // Rows go in groups of 8: the 8 U loads of a group are in
+                        // flight together, and the group's digest terms are reduced
+                        // with the 9-exchange reduce8 pattern (the sum for row g of
+                        // the group lands on the lanes whose bits 4,3,2 spell g).
+                        const int wl = ch * 32 + lane < nr ? Q.pr_w[q0 + ch * 32 + lane] : 0;
+                        const float *ucol = m.U + unit;
+                        float *ocol = S.arena_h + (size_t)(base + q0 + ch * 32) * H + unit;
+#pragma unroll
+                        for (int jg = 0; jg < 32; jg += 8) {
+                            float uv[8];
+#pragma unroll
+                            for (int g = 0; g < 8; g++) {
+                                const int wq = __shfl_sync(0xffffffffu, wl, jg + g);
+                                uv[g] = (ch * 32 + jg + g < nr && unit < H) ? __ldg(ucol + (size_t)wq * H) : 0.f;
+                            }
+                            unsigned long long dg[8];
+#pragma unroll
+                            for (int g = 0; g < 8; g++) {
+                                dg[g] = 0ull;
+                                const int j = jg + g;
+                                if (ch * 32 + j < nr && unit < H) {
+                                    const float o = __frcp_rn(1.f + expf(-(v[j] + uv[g])));   // == 1/x, IEEE
+                                    ocol[(size_t)j * H] = o;
+                                    dg[g] = otf_dig_h((uint32_t)unit, o);
+                                }
+                            }
+                            const unsigned long long tot = sd::reduce8_u64(dg, lane);
+                            const int row = ch * 32 + jg + node_of_lane(lane);
+                            if ((lane & 3) == 0 && row < nr) atomicAdd(&Q.pr_dig[q0 + row], tot);
+                        }
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncthreads();
+                if (tid == 0) SD_MARK(3);
+            }
+        }
+        cluster.sync();                                      // B: h', p and digests complete
+        if (rank == 1) continue;
+        SD_MARK(8);                                          // control waits for the update
+        // ---------------- assign (rank 0) ----------------
         const StreamRange rg{sid, 0u, L.re - L.rb, 0u};
         const LevelCtr lc{n, base, 0u, 0u};
         assign_range<0, NT>(Q, S, L.t, rg, lc, row_limit, lm_weight, nullptr, nullptr, nullptr, asmem);
         __syncthreads();
-        if (tid == 0) SD_MARK(7);
+        SD_MARK(7);
     }
     if (prof) {
-        ph[11] = tid == 0 ? 1 : 0;
+        ph[11] = rank == 0 ? 1 : 0;
         for (int i = 0; i < 12; i++) atomicAdd(&P.phase_ns[i], ph[i]);
     }
 #undef SD_MARK
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (wid == 0)
+    if (rank == 1 && wid == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(tmem_cols));
+    cluster.sync();                                          // rank 0's shared memory outlives rank 1's reads
 }

@@ -258,7 +258,7 @@ class Plan:
         _lib.check(_lib.load().otflm_plan_phase_ns(self.handle, o.ctypes.data, current_stream_ptr()),
                    "phase_ns")
         names = ("expand", "update_kloop", "update_drain", "update_epilogue", "hs_setup", "hs_pairs",
-                 "hs_group_total", "assign", "update_group_waits_for_hs", "mma_wait_operands")
+                 "hs_group_total", "assign", "control_waits_for_update", "mma_wait_operands")
         out = {k: int(o[i]) for i, k in enumerate(names)}
         out["ctas"] = int(o[11])
         return out
