@@ -91,6 +91,10 @@ def lib():
         L.orc_decode_many.argtypes = [p, p, p, i32, f64, i64, i32, i32, p, p, p, p, p]
         L.orc_query_batch.restype = None
         L.orc_query_batch.argtypes = [p, i64, p, p, p, p, p, p, i32]
+        L.orc_nbest.restype = C.c_int
+        L.orc_nbest.argtypes = [p, i32, f64, p, p, p, i64, p, p]
+        L.orc_twopass.restype = C.c_int
+        L.orc_twopass.argtypes = [p, p, i32, p, p, p, i32, f64, f64, p, p, p]
         _lib = L
     return _lib
 
@@ -423,3 +427,63 @@ def query_batch(model, tree, h, hist, hlen, words, want_p=True, want_h=True, n_t
                           _ptr(p) if p is not None else None,
                           _ptr(ho) if ho is not None else None, int(n_threads))
     return p, ho
+
+
+# --------------------------------------------------------------------------
+# two-pass rescoring (decoder.py:180-274)
+# --------------------------------------------------------------------------
+
+def nbest(lattice, n: int, lm_weight: float = 1.0) -> list:
+    """decoder.py:180-230: top-n distinct word sequences by first-pass score.
+    Returns OraclePath records (end_context / expansions = 0)."""
+    ol = lattice if isinstance(lattice, OracleLattice) else OracleLattice(lattice)
+    n = int(n)
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    n_out = np.zeros(1, np.int32)
+    hl = np.zeros(n, np.int32)
+    sc = np.zeros((n, 3), np.float64)
+    need = np.zeros(1, np.int64)
+    cap = max(16, n * 64)
+    while True:
+        arcs = np.zeros(cap, np.int32)
+        rc = lib().orc_nbest(C.byref(ol.struct), n, float(lm_weight), _ptr(n_out), _ptr(hl),
+                             _ptr(arcs), cap, _ptr(sc), _ptr(need))
+        if rc == -6 and int(need[0]) > cap:
+            cap = int(need[0])
+            continue
+        _check(rc, "nbest")
+        break
+    word = ol.arrs[2]
+    out, o = [], 0
+    for k in range(int(n_out[0])):
+        a = tuple(int(x) for x in arcs[o:o + hl[k]])
+        o += int(hl[k])
+        out.append(OraclePath(a, tuple(int(word[x]) for x in a), float(sc[k, 1]),
+                              float(sc[k, 2]), float(sc[k, 0]), 0, 0))
+    return out
+
+
+def twopass(om: "OracleModel", ngram, word_seqs, acoustic, mode: str, interp_weight: float = 0.5,
+            lm_weight: float = 1.0):
+    """decoder.py:243-274 over one n-best list: (lm [n], combined [n], best)."""
+    if mode not in ("rnnlm", "hybrid"):
+        raise ValueError(f"unknown two-pass mode {mode!r}")
+    if len(word_seqs) == 0:
+        raise ValueError("empty hypothesis list")
+    og = None
+    if ngram is not None:
+        og = ngram if isinstance(ngram, OracleNgram) else OracleNgram(ngram)
+    off = np.zeros(len(word_seqs) + 1, np.int64)
+    off[1:] = np.cumsum([len(w) for w in word_seqs])
+    words = np.ascontiguousarray(np.concatenate([np.asarray(w, np.int32) for w in word_seqs])
+                                 if off[-1] else np.zeros(1, np.int32), dtype=np.int32)
+    ac = np.ascontiguousarray(np.asarray(acoustic, np.float64))
+    lm = np.zeros(len(word_seqs))
+    comb = np.zeros(len(word_seqs))
+    best = np.zeros(1, np.int32)
+    _check(lib().orc_twopass(om.ref, og.handle if og else None, len(word_seqs), _ptr(off),
+                             _ptr(words), _ptr(ac), 0 if mode == "rnnlm" else 1,
+                             float(interp_weight), float(lm_weight), _ptr(lm), _ptr(comb),
+                             _ptr(best)), "twopass")
+    return lm, comb, int(best[0])

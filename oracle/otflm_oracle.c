@@ -894,3 +894,234 @@ void orc_query_batch(const OrcModel *m, int64_t n, const float *h, const int64_t
     for (int32_t t = 0; t < n_threads; t++) pthread_join(th[t], NULL);
     free(th); free(jobs);
 }
+
+/* ------------------------------------------------------------------ */
+/* Two-pass rescoring: nbest (decoder.py:180-230) and rescore_twopass   */
+/* (decoder.py:243-274).                                                */
+/* ------------------------------------------------------------------ */
+static double orc_pysum(const double *x, const int32_t *idx, int32_t n);
+typedef struct { double key; uint64_t counter; int32_t done, node; double g; int64_t path; } OrcNbEnt;
+typedef struct { int32_t arc; int64_t parent; } OrcNbLink;
+
+/* heap order of the reference tuples (-f, counter, ...): counter is unique */
+static int orc_nb_less(const OrcNbEnt *a, const OrcNbEnt *b) {
+    if (a->key < b->key) return 1;
+    if (a->key > b->key) return 0;
+    return a->counter < b->counter;
+}
+
+static uint64_t orc_words_hash(const int32_t *w, int32_t n) {
+    uint64_t h = 0xcbf29ce484222325ULL ^ (uint64_t)n;
+    for (int32_t i = 0; i < n; i++) h = orc_mix(h, (uint64_t)(uint32_t)w[i]);
+    return h;
+}
+
+/* nbest: exact best-first search with the backward-Viterbi completion as
+ * heuristic; the first complete path of each distinct word sequence is
+ * kept (decoder.py:180-230).  Outputs: *n_out hypotheses, hyp_len [n],
+ * arcs (concatenated, capacity arcs_cap), scores [n, 3] = (combined,
+ * acoustic, lm).  Returns ORC_ERR_NOMEM with *arcs_needed set when
+ * arcs_cap is too small. */
+int orc_nbest(const OrcLattice *lat, int32_t n, double lm_weight, int32_t *n_out,
+              int32_t *hyp_len, int32_t *arcs, int64_t arcs_cap, double *scores,
+              int64_t *arcs_needed) {
+    if (n < 1) return ORC_ERR_VALUE;
+    int32_t N = lat->n_nodes;
+    int32_t *order = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N > 0 ? N : 1));
+    int32_t *out_off = (int32_t *)calloc((size_t)N + 1, sizeof(int32_t));
+    int32_t *out_arc = (int32_t *)malloc(sizeof(int32_t) * (size_t)(lat->n_arcs > 0 ? lat->n_arcs : 1));
+    int rc = orc_topo(lat, order, out_off, out_arc);
+    if (rc) { free(order); free(out_off); free(out_arc); return rc; }
+    uint8_t *is_final = (uint8_t *)calloc((size_t)N + 1, 1);
+    for (int32_t i = 0; i < lat->n_finals; i++) is_final[lat->finals[i]] = 1;
+    double *comp = (double *)malloc(sizeof(double) * (size_t)(N > 0 ? N : 1));
+    for (int32_t k = N - 1; k >= 0; k--) {            /* decoder.py:191-198 */
+        int32_t v = order[k];
+        double best = is_final[v] ? 0.0 : -INFINITY;
+        for (int32_t e = out_off[v]; e < out_off[v + 1]; e++) {
+            int32_t a = out_arc[e];
+            double cand = (lat->ac[a] + lm_weight * lat->slm[a]) + comp[lat->dst[a]];
+            if (cand > best) best = cand;
+        }
+        comp[v] = best;
+    }
+    *n_out = 0;
+    *arcs_needed = 0;
+    if (comp[lat->start] == -INFINITY) {
+        free(order); free(out_off); free(out_arc); free(is_final); free(comp);
+        return ORC_ERR_NO_PATH;
+    }
+    size_t hcap = 1024, hn = 0, lcap = 1024, ln = 0;
+    OrcNbEnt *heap = (OrcNbEnt *)malloc(sizeof(OrcNbEnt) * hcap);
+    OrcNbLink *links = (OrcNbLink *)malloc(sizeof(OrcNbLink) * lcap);
+    /* seen word sequences: open addressing over (hash, offset, len) */
+    size_t scap = 1024;
+    uint64_t *s_hash = (uint64_t *)calloc(scap, sizeof(uint64_t));
+    int64_t *s_off = (int64_t *)malloc(sizeof(int64_t) * scap);
+    int32_t *s_len = (int32_t *)malloc(sizeof(int32_t) * scap);
+    uint8_t *s_used = (uint8_t *)calloc(scap, 1);
+    size_t s_n = 0, wcap = 4096, wn = 0;
+    int32_t *warena = (int32_t *)malloc(sizeof(int32_t) * wcap);
+    int32_t *tmp = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N + 1));
+    int32_t *tmpw = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N + 1));
+    uint64_t counter = 0;
+    int64_t arcs_used = 0;
+
+#define NB_PUSH(E) do {                                                                  \
+        if (hn == hcap) { hcap *= 2; heap = (OrcNbEnt *)realloc(heap, sizeof(OrcNbEnt) * hcap); } \
+        size_t _i = hn++; heap[_i] = (E);                                                \
+        while (_i > 0) { size_t _p = (_i - 1) / 2;                                       \
+            if (!orc_nb_less(&heap[_i], &heap[_p])) break;                               \
+            OrcNbEnt _t = heap[_p]; heap[_p] = heap[_i]; heap[_i] = _t; _i = _p; }       \
+    } while (0)
+
+    OrcNbEnt e0 = {-comp[lat->start], counter, 0, lat->start, 0.0, -1};
+    NB_PUSH(e0);
+    while (hn > 0 && *n_out < n) {
+        OrcNbEnt cur = heap[0];
+        heap[0] = heap[--hn];
+        for (size_t i = 0;;) {
+            size_t l = 2 * i + 1, r = l + 1, m = i;
+            if (l < hn && orc_nb_less(&heap[l], &heap[m])) m = l;
+            if (r < hn && orc_nb_less(&heap[r], &heap[m])) m = r;
+            if (m == i) break;
+            OrcNbEnt t = heap[m]; heap[m] = heap[i]; heap[i] = t; i = m;
+        }
+        if (cur.done) {                                  /* decoder.py:207-218 */
+            int32_t L = 0;
+            for (int64_t p = cur.path; p >= 0; p = links[p].parent) tmp[L++] = links[p].arc;
+            for (int32_t i = 0; i < L / 2; i++) { int32_t t = tmp[i]; tmp[i] = tmp[L - 1 - i]; tmp[L - 1 - i] = t; }
+            for (int32_t i = 0; i < L; i++) tmpw[i] = lat->word[tmp[i]];
+            uint64_t hh = orc_words_hash(tmpw, L);
+            size_t slot = (size_t)(hh & (scap - 1));
+            int dup = 0;
+            while (s_used[slot]) {
+                if (s_hash[slot] == hh && s_len[slot] == L &&
+                    memcmp(warena + s_off[slot], tmpw, sizeof(int32_t) * (size_t)L) == 0) { dup = 1; break; }
+                slot = (slot + 1) & (scap - 1);
+            }
+            if (dup) continue;
+            if (wn + (size_t)L > wcap) { while (wn + (size_t)L > wcap) wcap *= 2; warena = (int32_t *)realloc(warena, sizeof(int32_t) * wcap); }
+            memcpy(warena + wn, tmpw, sizeof(int32_t) * (size_t)L);
+            s_used[slot] = 1; s_hash[slot] = hh; s_off[slot] = (int64_t)wn; s_len[slot] = L;
+            wn += (size_t)L;
+            if (++s_n * 2 > scap) {                      /* rehash */
+                size_t ncap = scap * 2;
+                uint64_t *nh = (uint64_t *)calloc(ncap, sizeof(uint64_t));
+                int64_t *no = (int64_t *)malloc(sizeof(int64_t) * ncap);
+                int32_t *nl = (int32_t *)malloc(sizeof(int32_t) * ncap);
+                uint8_t *nu = (uint8_t *)calloc(ncap, 1);
+                for (size_t i = 0; i < scap; i++) if (s_used[i]) {
+                    size_t q = (size_t)(s_hash[i] & (ncap - 1));
+                    while (nu[q]) q = (q + 1) & (ncap - 1);
+                    nu[q] = 1; nh[q] = s_hash[i]; no[q] = s_off[i]; nl[q] = s_len[i];
+                }
+                free(s_hash); free(s_off); free(s_len); free(s_used);
+                s_hash = nh; s_off = no; s_len = nl; s_used = nu; scap = ncap;
+            }
+            double ac = orc_pysum(lat->ac, tmp, L), lm = orc_pysum(lat->slm, tmp, L);
+            int32_t k = (*n_out)++;
+            hyp_len[k] = L;
+            scores[3 * k] = cur.g; scores[3 * k + 1] = ac; scores[3 * k + 2] = lm;
+            if (arcs_used + L <= arcs_cap) memcpy(arcs + arcs_used, tmp, sizeof(int32_t) * (size_t)L);
+            arcs_used += L;
+            continue;
+        }
+        if (is_final[cur.node]) {                        /* decoder.py:220-222 */
+            OrcNbEnt e = {-cur.g, ++counter, 1, cur.node, cur.g, cur.path};
+            NB_PUSH(e);
+        }
+        for (int32_t x = out_off[cur.node]; x < out_off[cur.node + 1]; x++) {
+            int32_t a = out_arc[x];
+            double tail = comp[lat->dst[a]];
+            if (tail == -INFINITY) continue;
+            double g2 = cur.g + (lat->ac[a] + lm_weight * lat->slm[a]);
+            if (ln == lcap) { lcap *= 2; links = (OrcNbLink *)realloc(links, sizeof(OrcNbLink) * lcap); }
+            links[ln].arc = a; links[ln].parent = cur.path;
+            OrcNbEnt e = {-(g2 + tail), ++counter, 0, lat->dst[a], g2, (int64_t)ln};
+            ln++;
+            NB_PUSH(e);
+        }
+    }
+#undef NB_PUSH
+    *arcs_needed = arcs_used;
+    free(order); free(out_off); free(out_arc); free(is_final); free(comp); free(heap); free(links);
+    free(s_hash); free(s_off); free(s_len); free(s_used); free(warena); free(tmp); free(tmpw);
+    return arcs_used > arcs_cap ? ORC_ERR_NOMEM : ORC_OK;
+}
+
+/* CPython >= 3.12 builtin sum() over floats starting from int 0: the first
+ * item is taken exactly, the rest use Neumaier-compensated summation, and the
+ * compensation is added once at the end (Python/bltinmodule.c builtin_sum_impl). */
+static double orc_pysum(const double *x, const int32_t *idx, int32_t n) {
+    if (n == 0) return 0.0;
+    double f = 0.0 + x[idx[0]], c = 0.0;
+    for (int32_t i = 1; i < n; i++) {
+        double v = x[idx[i]], t = f + v;
+        if (fabs(f) >= fabs(v)) c += (f - t) + v;
+        else c += (v - t) + f;
+        f = t;
+    }
+    if (c != 0.0 && isfinite(c)) f += c;
+    return f;
+}
+
+/* _hybrid_logprob: decoder.py:233-240 */
+static double orc_hybrid(double lp_ng, double lp_rnn, double lam) {
+    if (lam >= 1.0) return lp_ng;
+    if (lam <= 0.0) return lp_rnn;
+    double hi = lp_ng > lp_rnn ? lp_ng : lp_rnn;
+    return hi + log(lam * exp(lp_ng - hi) + (1.0 - lam) * exp(lp_rnn - hi));
+}
+
+/* rescore_twopass (decoder.py:243-274) for one n-best list: per hypothesis
+ * a fresh zero context, word-by-word score then advance; mode 0 = rnnlm,
+ * 1 = hybrid.  lm_out / combined_out [n_hyp]; *best = index of the first
+ * maximum (strict >).  g may be NULL in rnnlm mode. */
+int orc_twopass(const OrcModel *m, const OrcNgram *g, int32_t n_hyp, const int64_t *hyp_off,
+                const int32_t *words, const double *acoustic, int32_t mode, double lam,
+                double lm_weight, double *lm_out, double *combined_out, int32_t *best) {
+    if (n_hyp < 1 || mode < 0 || mode > 1 || (mode == 1 && !g)) return ORC_ERR_VALUE;
+    float *h = (float *)calloc((size_t)m->H, sizeof(float));
+    float *h2 = (float *)calloc((size_t)m->H, sizeof(float));
+    int rc = ORC_OK;
+    *best = -1;
+    double best_s = 0.0;
+    for (int32_t j = 0; j < n_hyp && rc == ORC_OK; j++) {
+        memset(h, 0, sizeof(float) * (size_t)m->H);
+        int64_t hist[16]; int32_t L = 0;
+        double lm = 0.0;
+        const int32_t *ws = words + hyp_off[j];
+        int64_t len = hyp_off[j + 1] - hyp_off[j];
+        for (int64_t i = 0; i < len; i++) {
+            int32_t w = ws[i];
+            if (w < 0 || w >= m->V) { rc = ORC_ERR_VALUE; break; }
+            int64_t o0 = m->path_offsets[w], o1 = m->path_offsets[w + 1];
+            double lp_rnn = orc_word_logprob(h, m->H, hist, L, m->path_nodes + o0, m->path_signs + o0,
+                                             o1 - o0, m->NV, m->ME, m->order, m->seed, m->maxent_size - 1);
+            if (mode == 0) {
+                lm += lp_rnn;
+            } else {
+                int32_t need = g->order - 1, ctx[ORC_MAX_NGRAM], nc = 0;
+                if (need > 0) {
+                    if (i < need) for (int64_t k = 0; k < need - i; k++) ctx[nc++] = g->bos;
+                    for (int64_t k = (i < need ? 0 : i - need); k < i; k++) ctx[nc++] = ws[k];
+                }
+                double lp_ng;
+                rc = orc_ngram_logprob(g, ctx, nc, w, &lp_ng);
+                if (rc) break;
+                lm += orc_hybrid(lp_ng, lp_rnn, lam);
+            }
+            orc_advance_hidden(m->U + (size_t)w * m->H, m->W, h, m->H, h2);
+            memcpy(h, h2, sizeof(float) * (size_t)m->H);
+            if (L < m->order) hist[L++] = w;
+            else { for (int32_t k = 1; k < L; k++) hist[k - 1] = hist[k]; hist[L - 1] = w; }
+        }
+        double combined = acoustic[j] + lm_weight * lm;
+        lm_out[j] = lm;
+        combined_out[j] = combined;
+        if (*best < 0 || combined > best_s) { *best = j; best_s = combined; }
+    }
+    free(h); free(h2);
+    return rc;
+}

@@ -22,6 +22,11 @@ decode_small.npz  the reference small_setup stack (tests/conftest.py:86-99):
                (lattice, beam): rescore_onthefly 1-best, scores, end context,
                expansions, cache/table counters; plus a 2000-step
                rnnlm_prob trace replay (tests/test_cache.py:60-97).
+twopass.npz    nbest (decoder.py:180-230) and rescore_twopass (decoder.py:243-274)
+               on the decode_small lattices (model regenerated and checked
+               against decode_small.npz) and on the config (a) lattice:
+               n-best arcs and scores, two-pass winners, per-hypothesis LM
+               scores (rnnlm and hybrid modes).
 decode_a.npz   config (a) geometry (V=1000, H=64, MaxEnt 2^20; one 300-step
                breadth-3 lattice, beam 8): model regenerated from seeds at
                test time (sha256-checked), lattice arcs and the bigram
@@ -46,7 +51,7 @@ from otflm import rnnlm as rnnlm_mod  # noqa: E402
 from otflm.cache import RescoreCache, rnnlm_prob  # noqa: E402
 from otflm.codec import TransferLedger  # noqa: E402
 from otflm.context_table import IndexTable  # noqa: E402
-from otflm.decoder import RescoreStack, rescore_onthefly  # noqa: E402
+from otflm.decoder import RescoreStack, nbest, rescore_onthefly, rescore_twopass  # noqa: E402
 from otflm.huffman import build_huffman, build_huffman_from_counts  # noqa: E402
 from otflm.lattice import generate_lattice  # noqa: E402
 from otflm.ngram import ngram_logprob, train_ngram  # noqa: E402
@@ -290,10 +295,79 @@ def make_decode_a():
     print(f"decode_a: {rep.expansions} requests in {dt:.2f}s on the reference")
 
 
+def _twopass_block(d, key, lat, model, tree, bigram, n, lm_w, n_score):
+    hyps = nbest(lat, n, lm_weight=lm_w)
+    d[f"{key}_n"] = np.int32(n)
+    d[f"{key}_lmw"] = np.float64(lm_w)
+    d[f"{key}_hyp_len"] = np.array([len(h.arcs) for h in hyps], np.int32)
+    d[f"{key}_hyp_arcs"] = np.array([a for h in hyps for a in h.arcs], np.int32)
+    d[f"{key}_hyp_scores"] = np.array([[h.combined_score, h.acoustic_score, h.lm_score]
+                                       for h in hyps], np.float64)
+    modes = [("rnnlm", 0.5), ("hybrid", 0.0), ("hybrid", 0.3), ("hybrid", 1.0)]
+    best = []
+    for mode, lam in modes:
+        b = rescore_twopass(hyps[:n_score], mode, model, tree, bigram, interp_weight=lam,
+                            lm_weight=lm_w)
+        idx = [h.arcs for h in hyps].index(b.arcs)
+        best.append((idx, b.lm_score, b.combined_score))
+    d[f"{key}_best"] = np.array(best, np.float64)
+    per = np.zeros((min(n_score, len(hyps)), 2))
+    for j, h in enumerate(hyps[:n_score]):
+        per[j, 0] = rescore_twopass([h], "rnnlm", model, tree, bigram, lm_weight=lm_w).lm_score
+        per[j, 1] = rescore_twopass([h], "hybrid", model, tree, bigram, interp_weight=0.3,
+                                    lm_weight=lm_w).lm_score
+    d[f"{key}_per_hyp_lm"] = per
+
+
+def make_twopass():
+    lines = zipfian_corpus(400, 60, seed=91)
+    vocab = build_vocabulary(lines)
+    tree = build_huffman(vocab)
+    bigram = train_ngram(lines, vocab, 2, smoothing="kneser-ney")
+    model = RnnlmModel.new(vocab.size, hidden_size=16, maxent_order=3, maxent_table_bits=12, seed=17)
+    rnnlm_mod.train(model, lines[:150], vocab, tree, epochs=1, learn_rate=0.1)
+    small = np.load(OUT / "decode_small.npz")
+    assert np.array_equal(small["U"], model.input_weights), "small setup drifted"
+    assert np.array_equal(small["W"], model.recurrent_weights)
+    d = {}
+    for li in range(12):
+        line = lines[li]
+        breadth = 2 if li % 3 == 0 else 3
+        lat = generate_lattice(vocab.tokenize(line), vocab, bigram, breadth,
+                               zlib.crc32(line.encode()))
+        assert np.array_equal(small[f"l{li}_word"],
+                              np.array([a.word for a in sorted(lat.arcs, key=lambda a: a.id)]))
+        _twopass_block(d, f"l{li}", lat, model, tree, bigram, n=60 if li % 2 else 25,
+                       lm_w=1.0 if li % 2 else 0.7, n_score=20)
+    # config (a) lattice: 300 frames, V=1000, H=64
+    a = np.load(OUT / "decode_a.npz")
+    V, H, bits = 1000, 64, 20
+    words = ["<unk>", "<s>", "</s>"] + [f"w{i}" for i in range(3, V)]
+    vocab = Vocabulary(words, zipf_counts(V))
+    tree = build_huffman(vocab)
+    model = synth_model(V, H, bits)
+    corpus = [" ".join(f"w{int(x) + 3}" for x in s.replace("w", "").split())
+              for s in zipfian_corpus(20000, V - 3, seed=1)]
+    bigram = train_ngram(corpus, vocab, 2, smoothing="kneser-ney")
+    rng = np.random.RandomState(21)
+    ref = [int(x) for x in rng.randint(3, V, size=300)]
+    lat = generate_lattice(ref, vocab, bigram, 3, noise_seed=5)
+    assert np.array_equal(a["lat_word"], np.array([x.word for x in sorted(lat.arcs, key=lambda x: x.id)]))
+    t0 = time.time()
+    _twopass_block(d, "a", lat, model, tree, bigram, n=100, lm_w=1.0, n_score=40)
+    print(f"twopass config a: {time.time() - t0:.1f}s")
+    d["produced_by"] = np.array("otflm.decoder.nbest; otflm.decoder.rescore_twopass")
+    np.savez_compressed(OUT / "twopass.npz", **d)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["twopass"]:
+        make_twopass()
+        sys.exit(0)
     make_kernels()
     make_huffman()
     make_decode_small()
     make_decode_a()
+    make_twopass()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)
