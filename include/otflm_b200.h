@@ -256,6 +256,53 @@ int otflm_decode(OtflmStreams *s, const OtflmNgram *g, const OtflmLatticeBatch *
 /* number of kernels the last decode_run enqueued */
 int64_t otflm_last_launch_count(void);
 
+/* ---- two-pass rescoring ------------------------ */
+/* nbest (decoder.py:180-230) for every utterance of a lattice batch:
+ * exact best-first search over first-pass weights (acoustic + lm_weight *
+ * smalllm) with the backward-Viterbi completion as heuristic; distinct word
+ * sequences, best path of each.  Host-side (a sequential priority-queue
+ * walk that never touches the RNNLM), utterance-parallel on n_threads
+ * threads (<= 0: all).  Per-utterance failures (no complete path, cycle) are
+ * reported in the status array of otflm_nbest_copy. */
+typedef struct OtflmNbest OtflmNbest;
+int otflm_nbest_create(const OtflmLatticeBatch *lats, int32_t n, double lm_weight, int32_t n_threads,
+                       OtflmNbest **out);
+/* n_hyp host [n_utt]; out2 = {total hypotheses, total arcs} */
+int otflm_nbest_sizes(const OtflmNbest *r, int32_t *n_hyp_host, int64_t *out2);
+/* hyp_len [total hyps], arcs [total arcs] (lattice-local arc ids, path
+ * order), scores [total hyps, 3] = (combined, acoustic, lm), status [n_utt] */
+int otflm_nbest_copy(const OtflmNbest *r, int32_t *hyp_len, int32_t *arcs, double *scores,
+                     int32_t *status);
+int otflm_nbest_destroy(OtflmNbest *r);
+
+/* rescore_twopass (decoder.py:243-274) for a batch of n-best lists.  The
+ * hypotheses are merged into per-list prefix tries on the host; the device
+ * scores each trie node once (HS + MaxEnt, recurrent update, running LM
+ * sum), level by level over all lists. */
+typedef struct OtflmTwopass OtflmTwopass;
+typedef struct {
+    int32_t n_lists;
+    const int64_t *list_off;    /* host [n_lists+1] into the hypotheses; lists non-empty */
+    const int64_t *hyp_off;     /* host [n_hyp+1] into words */
+    const int32_t *words;       /* host word ids, hypothesis order */
+    const double *acoustic;     /* host [n_hyp] */
+} OtflmHypBatch;
+#define OTFLM_TWOPASS_RNNLM 0   /* words scored by the recurrent model alone */
+#define OTFLM_TWOPASS_HYBRID 1  /* lambda * ngram + (1 - lambda) * rnnlm in probability space */
+int otflm_twopass_create(const OtflmModel *m, const OtflmNgram *g /* may be NULL in rnnlm mode */,
+                         const OtflmHypBatch *hyps, int32_t n_threads, OtflmTwopass **out,
+                         void *stream);
+/* int64 [6]: trie nodes, levels, words, recurrent updates, widest level, hypotheses */
+int otflm_twopass_info(const OtflmTwopass *p, int64_t *out6);
+/* precision: OTFLM_PREC_FP64 (exact HS + f64 update) or a tensor-core mode;
+ * use_graph != 0 replays a captured CUDA graph of the level loop. */
+int otflm_twopass_run(OtflmTwopass *p, int32_t mode, double interp_weight, double lm_weight,
+                      int32_t precision, int32_t use_graph, void *stream);
+/* host outputs (any may be NULL): lm [n_hyp], combined [n_hyp], best [n_lists]
+ * (index within the list of the first maximum of combined); synchronizes. */
+int otflm_twopass_fetch(OtflmTwopass *p, double *lm, double *combined, int32_t *best, void *stream);
+int otflm_twopass_destroy(OtflmTwopass *p);
+
 const char *otflm_error_string(int32_t code);
 const char *otflm_last_error_detail(void);
 

@@ -40,6 +40,13 @@ from .rescore import (  # noqa: F401
     rnnlm_prob_trace,
     unpack,
 )
+from .twopass import (  # noqa: F401
+    TwopassPlan,
+    nbest,
+    nbest_batch,
+    rescore_twopass,
+    rescore_twopass_batch,
+)
 from ._lib import PackOverflowError, TableFullError, UnknownIndexError  # noqa: F401
 
 

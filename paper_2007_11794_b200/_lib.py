@@ -80,6 +80,11 @@ class LatticeBatch(C.Structure):
                 ("final_off", C.c_void_p), ("finals", C.c_void_p), ("stream_ids", C.c_void_p)]
 
 
+class HypBatch(C.Structure):
+    _fields_ = [("n_lists", C.c_int32), ("list_off", C.c_void_p), ("hyp_off", C.c_void_p),
+                ("words", C.c_void_p), ("acoustic", C.c_void_p)]
+
+
 class DecodeResult(C.Structure):
     _fields_ = [("path_len", C.c_void_p), ("path_arcs", C.c_void_p), ("max_path", C.c_int32),
                 ("combined", C.c_void_p), ("acoustic", C.c_void_p), ("lm", C.c_void_p),
@@ -127,6 +132,18 @@ _SIGS = {
     "otflm_group_run": (C.c_int, [_P, _P, C.c_double, C.c_int32, _P]),
     "otflm_group_profile": (C.c_int, [_P, _P, C.c_double, C.c_int32, _P, _P, _P]),
     "otflm_last_launch_count": (C.c_int64, []),
+    "otflm_nbest_create": (C.c_int, [C.POINTER(LatticeBatch), C.c_int32, C.c_double, C.c_int32,
+                                     C.POINTER(C.c_void_p)]),
+    "otflm_nbest_sizes": (C.c_int, [_P, _P, _P]),
+    "otflm_nbest_copy": (C.c_int, [_P, _P, _P, _P, _P]),
+    "otflm_nbest_destroy": (C.c_int, [_P]),
+    "otflm_twopass_create": (C.c_int, [_P, _P, C.POINTER(HypBatch), C.c_int32,
+                                       C.POINTER(C.c_void_p), _P]),
+    "otflm_twopass_info": (C.c_int, [_P, _P]),
+    "otflm_twopass_run": (C.c_int, [_P, C.c_int32, C.c_double, C.c_double, C.c_int32, C.c_int32,
+                                    _P]),
+    "otflm_twopass_fetch": (C.c_int, [_P, _P, _P, _P, _P]),
+    "otflm_twopass_destroy": (C.c_int, [_P]),
     "otflm_error_string": (C.c_char_p, [C.c_int32]),
     "otflm_last_error_detail": (C.c_char_p, []),
 }

@@ -1610,3 +1610,8 @@ extern "C" const char *otflm_error_string(int32_t code) {
 }
 
 extern "C" const char *otflm_last_error_detail(void) { return g_detail.c_str(); }
+
+// ==========================================================================
+// two-pass rescoring (uses the launchers above)
+// ==========================================================================
+#include "twopass.cuh"

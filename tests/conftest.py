@@ -88,6 +88,12 @@ def config_a(golden):
     return d, model, tree, lm, golden_lattice(d, "lat_")
 
 
+@pytest.fixture(scope="session")
+def tp(golden):
+    """tests/golden/twopass.npz: reference nbest / rescore_twopass outputs."""
+    return golden("twopass")
+
+
 def small_results(d):
     """rows: (li, bi, enabled, combined, acoustic, lm, end_ctx, expansions,
     lookups, hits, misses, table_len, bytes_indexed, bytes_full)"""

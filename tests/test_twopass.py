@@ -19,11 +19,6 @@ from oracle import oracle as O
 MODES = [("rnnlm", 0.5), ("hybrid", 0.0), ("hybrid", 0.3), ("hybrid", 1.0)]
 
 
-@pytest.fixture(scope="session")
-def tp(golden):
-    return golden("twopass")
-
-
 def _blocks(tp, small, config_a):
     d, gm, lats = small
     for li in range(12):
@@ -71,3 +66,28 @@ def test_oracle_nbest_errors(small):
     _, _, lats = small
     with pytest.raises(ValueError):
         O.nbest(lats[0], 0)
+
+
+def test_product_nbest_matches_reference(tp, small, config_a):
+    """The product n-best search (host C++ in libotflm_b200.so; no GPU needed)."""
+    from paper_2007_11794_b200 import nbest, nbest_batch
+    blocks = list(_blocks(tp, small, config_a))
+    for key, lat, *_ in blocks:
+        _check_nbest(tp, key, nbest(lat, int(tp[f"{key}_n"]), float(tp[f"{key}_lmw"])))
+    # batch form: utterance-parallel threads, same lists
+    small_blocks = [b for b in blocks if b[0] != "a" and float(tp[f"{b[0]}_lmw"]) == 1.0]
+    lists = nbest_batch([b[1] for b in small_blocks], 60, 1.0, n_threads=4)
+    for (key, *_), hyps in zip(small_blocks, lists):
+        _check_nbest(tp, key, hyps)
+
+
+def test_product_nbest_errors(small):
+    from paper_2007_11794_b200 import nbest
+    from paper_2007_11794_b200.lattice import Lattice
+    _, _, lats = small
+    with pytest.raises(ValueError):
+        nbest(lats[0], 0)
+    dead = Lattice(0, [5], src=np.array([0, 1]), dst=np.array([1, 2]), word=np.array([3, 4]),
+                   acoustic=np.array([-1.0, -1.0]), smalllm=np.array([-1.0, -1.0]))
+    with pytest.raises(ValueError):
+        nbest(dead, 3)
