@@ -50,6 +50,7 @@ def parse():
                     help="decode schedule: persistent per-stream kernel or level-synchronous graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-queries", action="store_true", help="skip the config-d query microbench")
+    ap.add_argument("--twopass-n", type=int, default=1000, help="n-best size of the two-pass extra (0: skip)")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     return ap.parse_args()
 
@@ -165,6 +166,73 @@ def query_microbench(precision: str, n_queries: int = 1 << 20, n_ctx: int = 1 <<
             "advance_ms": adv_ms, "advance_tflops": tfs, "advance_frac_of_bf16_peak": tfs / tc_peak,
             "advance_precision": precision,
             "queries_per_s": n_queries / ((min(hs_ms, hs_fast_ms) + adv_ms) / 1e3), "peak_source": src}
+
+
+def twopass_microbench(setup, precision: str, n: int, reps: int = 5):
+    """Two-pass rescoring (decoder.py:180-274) on the
+    config-(b) batch: n-best lists of every utterance (host search in
+    libotflm_b200.so), merged prefix tries, device scoring (rnnlm mode).
+    Device time has the tries resident in HBM (L2 flushed before each run);
+    e2e = n-best search + trie build + H2D + device scoring + D2H."""
+    import torch
+    from oracle import oracle as O
+    from paper_2007_11794_b200.twopass import TwopassPlan, nbest_arrays
+    m = setup.model
+    H = m.hidden_size
+    t0 = time.perf_counter()
+    nb = nbest_arrays(setup.lattices, n, 1.0)
+    t_nbest = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    plan = TwopassPlan(m, setup.tree, None, nb)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    info = plan.info()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    plan.run("rnnlm", 0.5, 1.0, precision)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        plan.run("rnnlm", 0.5, 1.0, precision)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    dev_ms = float(np.median(ts))
+    t0 = time.perf_counter()
+    lm, comb, best = plan.fetch()
+    t_fetch = time.perf_counter() - t0
+    e2e_s = t_nbest + t_build + dev_ms / 1e3 + t_fetch
+    # algorithmic bytes: every trie node is one HS query (mean path P over its
+    # words) + every internal node one update (h, U row in, h' out)
+    pl = (setup.tree.path_offsets[1:] - setup.tree.path_offsets[:-1])
+    P = float(pl[nb.words].mean())
+    byt = info["trie_nodes"] * (P * (4 * H + 20) + 4 * H + 16) + info["updates"] * 12 * H
+    hbm, tc_peak, _ = peaks()
+    # CPU: the oracle restatement of rescore_twopass on a bounded sample
+    om = O.OracleModel(m, setup.tree)
+    k = max(1, min(int(nb.n_hyp[0]), 24))
+    ws = [nb.words[nb.hyp_off[j]:nb.hyp_off[j + 1]] for j in range(k)]
+    t0 = time.perf_counter()
+    O.twopass(om, None, ws, nb.scores[:k, 1], "rnnlm")
+    cpu_s = time.perf_counter() - t0
+    cpu_wps = sum(len(w) for w in ws) / cpu_s
+    return {"workload": f"config b: {len(setup.lattices)} utterances x {n}-best lists "
+                        f"({info['hypotheses']} hypotheses, {info['words']} words), rnnlm mode, "
+                        f"{precision} update; tries resident, L2 flushed before each run",
+            "device_ms": dev_ms, "words_per_s": info["words"] / (dev_ms / 1e3),
+            "hyps_per_s": info["hypotheses"] / (dev_ms / 1e3),
+            "trie_nodes": info["trie_nodes"], "updates": info["updates"], "levels": info["levels"],
+            "prefix_sharing": info["words"] / max(info["trie_nodes"], 1),
+            "algorithmic_gbs": byt / (dev_ms / 1e3) / 1e9, "frac_of_hbm": byt / (dev_ms / 1e3) / 1e9 / hbm,
+            "update_tflops": 2.0 * H * H * info["updates"] / (dev_ms / 1e3) / 1e12,
+            "e2e": {"words_per_s": info["words"] / e2e_s, "nbest_s": t_nbest, "trie_build_h2d_s": t_build,
+                    "fetch_s": t_fetch, "host_threads": len(os.sched_getaffinity(0))},
+            "cpu_baseline": {"words_per_s": cpu_wps, "cores": 1, "kind": "port",
+                             "sample": f"oracle rescore_twopass on the first {k} hypotheses of utterance 0 "
+                                       "(every word scored and advanced, no prefix sharing)"}}
 
 
 def cpu_baseline(setup, n_sample: int, threads: int):
@@ -393,6 +461,8 @@ def main():
     extras = {}
     if rank == 0 and not args.no_queries:
         extras["config_d_queries"] = query_microbench(args.precision)
+    if rank == 0 and args.twopass_n > 0:
+        extras["twopass"] = twopass_microbench(setup, args.precision, args.twopass_n)
     line = {
         "metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

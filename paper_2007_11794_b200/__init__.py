@@ -41,8 +41,10 @@ from .rescore import (  # noqa: F401
     unpack,
 )
 from .twopass import (  # noqa: F401
+    NbestArrays,
     TwopassPlan,
     nbest,
+    nbest_arrays,
     nbest_batch,
     rescore_twopass,
     rescore_twopass_batch,

@@ -69,14 +69,27 @@ struct List {
     int status = OTFLM_OK;
 };
 
+// Per-thread search state, reused across utterances: the heap and path links
+// reach ~10^5-10^6 entries at n = 1000, and regrowing them per utterance
+// serialises the threads on page faults.
+struct Work {
+    std::vector<Ent> heap;
+    std::vector<std::pair<int32_t, int64_t>> links;     // (arc, parent link)
+    std::unordered_map<uint64_t, std::vector<std::pair<int64_t, int32_t>>> seen;   // hash -> (offset, len)
+    std::vector<int32_t> seen_words, tmp, tmpw, out_off, out_arc, indeg, order;
+    std::vector<uint8_t> is_final;
+    std::vector<double> comp;
+};
+
 // one utterance of the batch; node ids 0..N-1, arcs [a0, a1) of the batch arrays
-static int search(const OtflmLatticeBatch *L, int u, int32_t n, double lmw, List *out) {
+static int search(const OtflmLatticeBatch *L, int u, int32_t n, double lmw, List *out, Work &W) {
     const int32_t N = L->n_nodes[u];
     const int64_t a0 = L->arc_off[u], a1 = L->arc_off[u + 1];
     const int32_t A = (int32_t)(a1 - a0);
     const int32_t *src = L->arc_src + a0, *dst = L->arc_dst + a0, *word = L->arc_word + a0;
     const double *ac = L->arc_ac + a0, *slm = L->arc_slm + a0;
-    std::vector<int32_t> out_off(N + 1, 0), out_arc(A), indeg(N, 0), order;
+    std::vector<int32_t> &out_off = W.out_off, &out_arc = W.out_arc, &indeg = W.indeg, &order = W.order;
+    out_off.assign(N + 1, 0); out_arc.resize(A); indeg.assign(N, 0); order.clear();
     for (int32_t a = 0; a < A; a++) {
         if (src[a] < 0 || src[a] >= N || dst[a] < 0 || dst[a] >= N) return OTFLM_ERR_VALUE;
         out_off[src[a] + 1]++; indeg[dst[a]]++;
@@ -97,10 +110,12 @@ static int search(const OtflmLatticeBatch *L, int u, int32_t n, double lmw, List
             if (--indeg[dst[out_arc[e]]] == 0) ready.push(dst[out_arc[e]]);
     }
     if ((int32_t)order.size() != N) return OTFLM_ERR_CYCLE;
-    std::vector<uint8_t> is_final(N, 0);
+    std::vector<uint8_t> &is_final = W.is_final;
+    is_final.assign(N, 0);
     for (int64_t f = L->final_off[u]; f < L->final_off[u + 1]; f++) is_final[L->finals[f]] = 1;
     // backward Viterbi completion (decoder.py:191-198)
-    std::vector<double> comp(N);
+    std::vector<double> &comp = W.comp;
+    comp.resize(N);
     for (int32_t k = N - 1; k >= 0; k--) {
         const int32_t v = order[k];
         double best = is_final[v] ? 0.0 : -INFINITY;
@@ -114,15 +129,21 @@ static int search(const OtflmLatticeBatch *L, int u, int32_t n, double lmw, List
     const int32_t start = L->start[u];
     if (start < 0 || start >= N || comp[start] == -INFINITY) return OTFLM_ERR_NO_PATH;
     // best-first search (decoder.py:200-229); paths are parent-linked lists
-    std::priority_queue<Ent, std::vector<Ent>, EntGreater> heap;
-    std::vector<std::pair<int32_t, int64_t>> links;     // (arc, parent link)
-    std::unordered_map<uint64_t, std::vector<std::pair<int64_t, int32_t>>> seen;   // hash -> (offset, len)
-    std::vector<int32_t> seen_words, tmp, tmpw;
+    // (a binary heap on a reused vector; (key, counter) is a total order, so
+    // the pop sequence is the reference's heapq sequence)
+    std::vector<Ent> &heap = W.heap;
+    auto &links = W.links;
+    auto &seen = W.seen;
+    std::vector<int32_t> &seen_words = W.seen_words, &tmp = W.tmp, &tmpw = W.tmpw;
+    heap.clear(); links.clear(); seen.clear(); seen_words.clear();
+    const EntGreater cmp;
+    auto push = [&](const Ent &e) { heap.push_back(e); std::push_heap(heap.begin(), heap.end(), cmp); };
     uint64_t counter = 0;
-    heap.push(Ent{-comp[start], counter, 0, start, 0.0, -1});
+    push(Ent{-comp[start], counter, 0, start, 0.0, -1});
     int32_t got = 0;
     while (!heap.empty() && got < n) {
-        const Ent cur = heap.top(); heap.pop();
+        std::pop_heap(heap.begin(), heap.end(), cmp);
+        const Ent cur = heap.back(); heap.pop_back();
         if (cur.done) {
             tmp.clear();
             for (int64_t p = cur.path; p >= 0; p = links[p].second) tmp.push_back(links[p].first);
@@ -145,27 +166,28 @@ static int search(const OtflmLatticeBatch *L, int u, int32_t n, double lmw, List
             got++;
             continue;
         }
-        if (is_final[cur.node]) heap.push(Ent{-cur.g, ++counter, 1, cur.node, cur.g, cur.path});
+        if (is_final[cur.node]) push(Ent{-cur.g, ++counter, 1, cur.node, cur.g, cur.path});
         for (int32_t e = out_off[cur.node]; e < out_off[cur.node + 1]; e++) {
             const int32_t a = out_arc[e];
             const double tail = comp[dst[a]];
             if (tail == -INFINITY) continue;
             const double g2 = cur.g + (ac[a] + lmw * slm[a]);
             links.push_back({a, cur.path});
-            heap.push(Ent{-(g2 + tail), ++counter, 0, dst[a], g2, (int64_t)links.size() - 1});
+            push(Ent{-(g2 + tail), ++counter, 0, dst[a], g2, (int64_t)links.size() - 1});
         }
     }
     return OTFLM_OK;
 }
 
+// f(item, thread index) over items 0..n-1, dynamic scheduling
 template <class F>
 static void parallel_for(int n, int threads, F f) {
     threads = std::max(1, std::min(threads, n));
-    if (threads == 1) { for (int i = 0; i < n; i++) f(i); return; }
+    if (threads == 1) { for (int i = 0; i < n; i++) f(i, 0); return; }
     std::atomic<int> next{0};
     std::vector<std::thread> th;
     for (int t = 0; t < threads; t++)
-        th.emplace_back([&] { for (int i; (i = next.fetch_add(1)) < n;) f(i); });
+        th.emplace_back([&, t] { for (int i; (i = next.fetch_add(1)) < n;) f(i, t); });
     for (auto &x : th) x.join();
 }
 
@@ -186,8 +208,10 @@ extern "C" int otflm_nbest_create(const OtflmLatticeBatch *L, int32_t n, double 
     if (n < 1) { g_detail = "n must be >= 1"; return OTFLM_ERR_VALUE; }
     auto *r = new OtflmNbest();
     r->lists.resize(L->n_utt);
-    nb::parallel_for(L->n_utt, n_threads > 0 ? n_threads : nb::default_threads(), [&](int u) {
-        r->lists[u].status = nb::search(L, u, n, lm_weight, &r->lists[u]);
+    const int nt = std::max(1, std::min(n_threads > 0 ? n_threads : nb::default_threads(), L->n_utt));
+    std::vector<nb::Work> work(nt);
+    nb::parallel_for(L->n_utt, nt, [&](int u, int t) {
+        r->lists[u].status = nb::search(L, u, n, lm_weight, &r->lists[u], work[t]);
     });
     *out = r;
     return OTFLM_OK;
@@ -354,7 +378,7 @@ static int twopass_build(OtflmTwopass *p, const OtflmHypBatch *B, int n_threads,
     std::atomic<int> bad{0};
     const int V = p->m->d.V;
     // 1. per-list tries (local ids, root = 0)
-    nb::parallel_for(NL, n_threads, [&](int l) {
+    nb::parallel_for(NL, n_threads, [&](int l, int) {
         TrieBuild::Local &T = loc[l];
         T.par.push_back(0); T.depth.push_back(0); T.word.push_back(-1); T.internal.push_back(0);
         std::unordered_map<uint64_t, uint32_t> child;
@@ -388,7 +412,7 @@ static int twopass_build(OtflmTwopass *p, const OtflmHypBatch *B, int n_threads,
     uint32_t D = 0;
     for (auto &T : loc) for (uint32_t d : T.depth) D = std::max(D, d);
     std::vector<std::vector<uint32_t>> cnt_int(NL, std::vector<uint32_t>(D + 1, 0)), cnt_leaf = cnt_int;
-    nb::parallel_for(NL, n_threads, [&](int l) {
+    nb::parallel_for(NL, n_threads, [&](int l, int) {
         TrieBuild::Local &T = loc[l];
         T.rank.resize(T.par.size());
         for (size_t v = 1; v < T.par.size(); v++)
@@ -412,7 +436,7 @@ static int twopass_build(OtflmTwopass *p, const OtflmHypBatch *B, int n_threads,
     // 3. global arrays
     std::vector<uint32_t> par_row(node, 0), par_node(node, 0), own_row(node, 0xFFFFFFFFu), leaf(B->list_off[NL]);
     std::vector<int32_t> word(node, 0);
-    nb::parallel_for(NL, n_threads, [&](int l) {
+    nb::parallel_for(NL, n_threads, [&](int l, int) {
         TrieBuild::Local &T = loc[l];
         T.gid.assign(T.par.size(), 0);
         for (size_t v = 1; v < T.par.size(); v++) {   // parents precede children (creation order)

@@ -26,8 +26,38 @@ from .rescore import PathHypothesis
 MODES = {"rnnlm": 0, "hybrid": 1}
 
 
-def nbest_batch(lattices: Sequence, n: int, lm_weight: float = 1.0, n_threads: int = 0):
-    """nbest for every lattice; returns one list of PathHypothesis per lattice."""
+class NbestArrays:
+    """n-best lists of a lattice batch as flat arrays (hypothesis order =
+    search order within each utterance)."""
+
+    def __init__(self, lats, n_hyp, hyp_len, arcs, scores, arc_word, arc_off):
+        self.lats = lats
+        self.n_hyp = n_hyp                        # [U]
+        self.list_off = np.zeros(len(n_hyp) + 1, np.int64)
+        self.list_off[1:] = np.cumsum(n_hyp)
+        self.hyp_len = hyp_len                    # [n_hyp total]
+        self.hyp_off = np.zeros(len(hyp_len) + 1, np.int64)
+        self.hyp_off[1:] = np.cumsum(hyp_len)
+        self.arcs = arcs                          # lattice-local arc ids
+        self.scores = scores                      # [n, 3] combined, acoustic, lm
+        # words of every hypothesis, gathered through the batch arc table
+        utt_of_arc = np.repeat(np.repeat(np.arange(len(n_hyp)), n_hyp), hyp_len)
+        self.words = np.ascontiguousarray(arc_word[arc_off[utt_of_arc] + arcs], np.int32)
+
+    def hypothesis(self, u: int, k: int) -> PathHypothesis:
+        j = int(self.list_off[u]) + int(k)
+        a0, a1 = int(self.hyp_off[j]), int(self.hyp_off[j + 1])
+        return PathHypothesis(tuple(self.arcs[a0:a1].tolist()), tuple(self.words[a0:a1].tolist()),
+                              float(self.scores[j, 1]), float(self.scores[j, 2]),
+                              float(self.scores[j, 0]))
+
+    def hypotheses(self, u: int) -> list:
+        return [self.hypothesis(u, k) for k in range(int(self.n_hyp[u]))]
+
+
+def nbest_arrays(lattices: Sequence, n: int, lm_weight: float = 1.0, n_threads: int = 0) -> NbestArrays:
+    """nbest (decoder.py:180-230) for every lattice, utterance-parallel on
+    host threads, returned as flat arrays."""
     n = int(n)
     if n < 1:
         raise ValueError("n must be >= 1")
@@ -52,18 +82,14 @@ def nbest_batch(lattices: Sequence, n: int, lm_weight: float = 1.0, n_threads: i
         if status[u] == _lib.ERR_NO_PATH:
             raise ValueError("no complete path through the lattice")
         _lib.check(int(status[u]), f"nbest (utterance {u})")
-    out, hi, ai = [], 0, 0
-    for u, lat in enumerate(lats):
-        lst = []
-        for _ in range(int(n_hyp[u])):
-            k = int(hl[hi])
-            a = tuple(int(x) for x in arcs[ai:ai + k])
-            lst.append(PathHypothesis(a, tuple(int(lat.arc_word[x]) for x in a), float(sc[hi, 1]),
-                                      float(sc[hi, 2]), float(sc[hi, 0])))
-            hi += 1
-            ai += k
-        out.append(lst)
-    return out
+    H, A = int(tot[0]), int(tot[1])
+    return NbestArrays(lats, n_hyp, hl[:H], arcs[:A], sc[:H], arrays["arc_word"], arrays["arc_off"])
+
+
+def nbest_batch(lattices: Sequence, n: int, lm_weight: float = 1.0, n_threads: int = 0):
+    """nbest for every lattice; returns one list of PathHypothesis per lattice."""
+    r = nbest_arrays(lattices, n, lm_weight, n_threads)
+    return [r.hypotheses(u) for u in range(len(r.lats))]
 
 
 def nbest(lattice, n: int, lm_weight: float = 1.0) -> list:
@@ -72,29 +98,45 @@ def nbest(lattice, n: int, lm_weight: float = 1.0) -> list:
 
 
 class TwopassPlan:
-    """Prefix tries of a batch of n-best lists, uploaded; reusable runs."""
+    """Prefix tries of a batch of n-best lists, uploaded; reusable runs.
+
+    ``hyp_lists``: lists of PathHypothesis, or an ``NbestArrays``."""
 
     def __init__(self, model, tree, small_lm, hyp_lists, n_threads: int = 0):
         L = _lib.load()
-        if not hyp_lists or any(len(l) == 0 for l in hyp_lists):
-            raise ValueError("empty hypothesis list")
         self.dmodel = DeviceModel.get(model, tree)
         self.ngram = DeviceNgram.get(small_lm, self.dmodel) if small_lm is not None else None
-        self.lists = [list(l) for l in hyp_lists]
-        counts = [len(l) for l in self.lists]
-        self.list_off = np.zeros(len(counts) + 1, np.int64)
-        self.list_off[1:] = np.cumsum(counts)
-        flat = [h for l in self.lists for h in l]
-        lens = np.array([len(h.words) for h in flat], np.int64)
-        self.hyp_off = np.zeros(len(flat) + 1, np.int64)
-        self.hyp_off[1:] = np.cumsum(lens)
-        self.words = np.ascontiguousarray(
-            np.fromiter((w for h in flat for w in h.words), np.int32, int(self.hyp_off[-1])))
+        if isinstance(hyp_lists, NbestArrays):
+            r = hyp_lists
+            if len(r.n_hyp) == 0 or np.any(r.n_hyp == 0):
+                raise ValueError("empty hypothesis list")
+            self.lists = None
+            self.nb = r
+            self.list_off = r.list_off
+            self.hyp_off = r.hyp_off
+            self.words = r.words
+            self.acoustic = np.ascontiguousarray(r.scores[:, 1])
+        else:
+            if not hyp_lists or any(len(l) == 0 for l in hyp_lists):
+                raise ValueError("empty hypothesis list")
+            self.nb = None
+            self.lists = [list(l) for l in hyp_lists]
+            counts = [len(l) for l in self.lists]
+            self.list_off = np.zeros(len(counts) + 1, np.int64)
+            self.list_off[1:] = np.cumsum(counts)
+            flat = [h for l in self.lists for h in l]
+            lens = np.array([len(h.words) for h in flat], np.int64)
+            self.hyp_off = np.zeros(len(flat) + 1, np.int64)
+            self.hyp_off[1:] = np.cumsum(lens)
+            self.words = np.ascontiguousarray(
+                np.fromiter((w for h in flat for w in h.words), np.int32, int(self.hyp_off[-1])))
+            self.acoustic = np.ascontiguousarray([h.acoustic_score for h in flat], np.float64)
         if len(self.words) and (self.words.min() < 0 or self.words.max() >= model.vocab_size):
             raise ValueError("word id out of range")
-        self.acoustic = np.ascontiguousarray([h.acoustic_score for h in flat], np.float64)
-        self._batch = _lib.HypBatch(len(counts), _p(self.list_off), _p(self.hyp_off), _p(self.words),
-                                    _p(self.acoustic))
+        self.n_lists = len(self.list_off) - 1
+        self.n_hyp = int(self.list_off[-1])
+        self._batch = _lib.HypBatch(self.n_lists, _p(self.list_off), _p(self.hyp_off),
+                                    _p(self.words), _p(self.acoustic))
         h = C.c_void_p()
         _lib.check(L.otflm_twopass_create(self.dmodel.handle,
                                           self.ngram.handle if self.ngram is not None else None,
@@ -102,7 +144,6 @@ class TwopassPlan:
                                           current_stream_ptr()), "rescore_twopass")
         self.handle = h
         self._fin = weakref.finalize(self, L.otflm_twopass_destroy, h)
-        self.n_hyp = len(flat)
 
     def info(self) -> dict:
         o = np.zeros(6, np.int64)
@@ -124,7 +165,7 @@ class TwopassPlan:
     def fetch(self):
         lm = np.zeros(self.n_hyp)
         comb = np.zeros(self.n_hyp)
-        best = np.zeros(len(self.lists), np.int32)
+        best = np.zeros(self.n_lists, np.int32)
         _lib.check(_lib.load().otflm_twopass_fetch(self.handle, _p(lm), _p(comb), _p(best),
                                                    current_stream_ptr()), "rescore_twopass")
         return lm, comb, best
@@ -133,9 +174,10 @@ class TwopassPlan:
         """The winning PathHypothesis of every list (decoder.py:264-274)."""
         lm, comb, best = self.fetch()
         out = []
-        for l, lst in enumerate(self.lists):
+        for l in range(self.n_lists):
             j = int(self.list_off[l]) + int(best[l])
-            h = lst[int(best[l])]
+            h = self.lists[l][int(best[l])] if self.lists is not None else \
+                self.nb.hypothesis(l, int(best[l]))
             out.append(PathHypothesis(h.arcs, h.words, h.acoustic_score, float(lm[j]),
                                       float(comb[j])))
         return out
