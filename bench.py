@@ -50,6 +50,8 @@ def parse():
                     help="decode schedule: persistent per-stream kernel or level-synchronous graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-queries", action="store_true", help="skip the config-d query microbench")
+    ap.add_argument("--beam-sweep", action="store_true", help="add the config-c beam sweep extra")
+    ap.add_argument("--all-word", action="store_true", help="add the all_word_logprobs extra")
     ap.add_argument("--twopass-n", type=int, default=1000, help="n-best size of the two-pass extra (0: skip)")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
     return ap.parse_args()
@@ -233,6 +235,86 @@ def twopass_microbench(setup, precision: str, n: int, reps: int = 5):
             "cpu_baseline": {"words_per_s": cpu_wps, "cores": 1, "kind": "port",
                              "sample": f"oracle rescore_twopass on the first {k} hypotheses of utterance 0 "
                                        "(every word scored and advanced, no prefix sharing)"}}
+
+
+def all_word_microbench(precision: str, n_ctx: int = 256, reps: int = 5):
+    """all_word_logprobs for n contexts at config c/d size (V=65,536, H=512):
+    the [n x (V-1)] node activations as one tcgen05 GEMM, then float64
+    MaxEnt + log-sigmoids per node and path sums per word."""
+    import torch
+    from paper_2007_11794_b200 import kernels, synth
+    from paper_2007_11794_b200.device import DeviceModel
+    from paper_2007_11794_b200.model import build_huffman_from_counts
+    cfg = synth.CONFIGS["d"]
+    V, H, bits = cfg["V"], cfg["H"], cfg["bits"]
+    model = synth.synth_model(V, H, bits)
+    tree = build_huffman_from_counts(synth.zipf_counts(V))
+    dm = DeviceModel(model, tree)
+    _, hidden, hist, hlen, _ = synth.query_set(model, 16, n_ctx)
+    d = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    ctx = d(np.arange(n_ctx, dtype=np.int32))
+    th, thist, thl = d(hidden), d(hist), d(hlen)
+    out = torch.empty((n_ctx, V), dtype=torch.float64, device="cuda")
+    res = {"workload": f"{n_ctx} contexts x V={V} (H={H}, MaxEnt 2^{bits}); L2 flushed before each run"}
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    for prec in ("fp64", precision):
+        kernels.all_word_logprobs_batch(dm, ctx, th, thist, thl, prec, out=out)
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            kernels.all_word_logprobs_batch(dm, ctx, th, thist, thl, prec, out=out)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ms = float(np.median(ts))
+        res[prec] = {"ms": ms, "contexts_per_s": n_ctx / (ms / 1e3),
+                     "word_logprobs_per_s": n_ctx * V / (ms / 1e3),
+                     "gemm_tflops_equiv": 2.0 * H * (V - 1) * n_ctx / (ms / 1e3) / 1e12}
+    return res
+
+
+def beam_sweep(precision: str, beams=(1, 2, 4, 8, 16, 32, 64), n_utt: int = 8, frames: int = 300,
+               reps: int = 3):
+    """Config (c): V=65,536 H=512 MaxEnt 2^22, 8 utterances x 300 frames,
+    decode throughput and RTF per beam (device time, lattices resident, L2
+    flushed before each run)."""
+    import torch
+    from paper_2007_11794_b200 import synth
+    from paper_2007_11794_b200.rescore import BatchDecoder
+    setup = synth.build_setup("c", n_utt=n_utt, T=frames, seed=17)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    rows = []
+    for beam in beams:
+        need = BatchDecoder.contexts_needed(setup.lattices, beam)
+        dec = BatchDecoder(setup.model, setup.tree, setup.small_lm, n_utt, need, precision=precision)
+        dec.prepare(setup.lattices, beam)
+        dec.run(1.0)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            dec.run(1.0)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ms = float(np.median(ts))
+        hyps, out = dec.fetch()
+        fr = sum(len(h.arcs) for h in hyps)
+        st = dec.streams.stats()
+        rows.append({"beam": beam, "ms": ms, "frames_per_s": fr / (ms / 1e3),
+                     "rtf_per_stream": (ms / 1e3) / (frames * FRAME_S),
+                     "requests": int(out["expansions"].sum()), "misses": int(st[:, 2].sum()),
+                     "queries_per_s": int(st[:, 2].sum()) / (ms / 1e3), "schedule": dec.schedule})
+        del dec
+        torch.cuda.empty_cache()
+    return {"workload": f"config c: V=65536 H=512 MaxEnt 2^22, {n_utt} utterances x {frames} frames, "
+                        f"breadth 3, {precision} update; L2 flushed before each run", "sweep": rows}
 
 
 def cpu_baseline(setup, n_sample: int, threads: int):
@@ -461,6 +543,10 @@ def main():
     extras = {}
     if rank == 0 and not args.no_queries:
         extras["config_d_queries"] = query_microbench(args.precision)
+    if rank == 0 and args.all_word:
+        extras["all_word_logprobs"] = all_word_microbench(args.precision)
+    if rank == 0 and args.beam_sweep:
+        extras["config_c_beam_sweep"] = beam_sweep(args.precision)
     if rank == 0 and args.twopass_n > 0:
         extras["twopass"] = twopass_microbench(setup, args.precision, args.twopass_n)
     line = {

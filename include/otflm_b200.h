@@ -142,6 +142,18 @@ int otflm_advance_hidden_rows(const OtflmModel *m, int64_t n, const float *input
 int otflm_all_word_logprobs(const OtflmModel *m, const float *h_dev, const int32_t *hist_host,
                             int32_t hist_len, double *out_dev, void *stream);
 
+/* all_word_logprobs for n contexts at once: query i uses h_dev[ctx[i]] and
+ * hist_dev[ctx[i], 0:hist_len[ctx[i]]] (row stride maxent_order); out dev
+ * double [n, V].  precision OTFLM_PREC_FP64: float64 CUDA-core dot products
+ * (the reference's arithmetic up to summation order); a tensor-core mode:
+ * the node activations [n x (V-1)] are one tcgen05 GEMM of the contexts
+ * against the node vectors (fp32 accumulate), MaxEnt terms and log-sigmoids
+ * in float64 once per node, path sums per word. */
+int otflm_all_word_logprobs_batch(const OtflmModel *m, int64_t n, const int32_t *ctx_dev,
+                                  const float *h_dev, const int32_t *hist_dev,
+                                  const int32_t *hist_len_dev, double *out_dev, int32_t precision,
+                                  void *stream);
+
 /* ---- decoding streams: IndexTable + RescoreCache + ledger per stream
  *      (context_table.py:48-119, cache.py:61-191, codec.py:95-110) ------ */
 typedef struct {

@@ -107,6 +107,7 @@ _SIGS = {
     "otflm_advance_hidden_batch": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, C.c_int32, _P]),
     "otflm_advance_hidden_rows": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, C.c_int32, _P]),
     "otflm_all_word_logprobs": (C.c_int, [_P, _P, _P, C.c_int32, _P, _P]),
+    "otflm_all_word_logprobs_batch": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, C.c_int32, _P]),
     "otflm_streams_create": (C.c_int, [_P, C.POINTER(StreamConfig), C.POINTER(C.c_void_p)]),
     "otflm_streams_destroy": (C.c_int, [_P]),
     "otflm_streams_reset": (C.c_int, [_P, C.c_int32, _P]),

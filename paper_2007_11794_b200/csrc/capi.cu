@@ -94,6 +94,10 @@ struct OtflmModel {
     int device;
     Allocs mem;
     int64_t n_path;
+    // tensor-core copies of the node vectors (all_word_logprobs), made on first use
+    mutable std::mutex nv_mu;
+    mutable float *NV_hi = nullptr, *NV_lo = nullptr;
+    mutable __nv_bfloat16 *NV_bf = nullptr;
 };
 
 __global__ void k_prep_weights(DevModel m, float *WT, float *W_hi, float *W_lo, __nv_bfloat16 *W_bf) {
@@ -137,6 +141,13 @@ __global__ void k_prep_wtiles(DevModel m, float *wt) {
 }
 
 extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, OtflmModel **out) {
+    {   // stream-ordered scratch (cudaMallocAsync) stays pooled across calls
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     if (!d || !out) return OTFLM_ERR_VALUE;
     if (d->hidden_size < 1 || d->vocab_size < 2 || d->maxent_order < 1 ||
         d->maxent_order > OTF_MAX_ORDER || d->maxent_size < 1 ||
@@ -497,6 +508,167 @@ extern "C" int otflm_all_word_logprobs(const OtflmModel *m, const float *h, cons
     CK(cudaFreeAsync(dh, s));
     CK(cudaStreamSynchronize(s));
     return OTFLM_OK;
+}
+
+// ---- batched all_word_logprobs: every word's log-prob for n contexts ----
+// node activations a[q, j] = v_j . h_q (tcgen05 GEMM, or float64 CUDA cores in
+// exact mode), + MaxEnt terms in the reference's order (_kernels_nb.py:63-75),
+// then per node both log-sigmoids once, then per word the path-order sum
+// (_kernels_nb.py:89-104).
+__global__ void k_split_nv(DevModel m, float *hi, float *lo, __nv_bfloat16 *bf) {
+    const int64_t n = (int64_t)(m.V - 1) * m.H;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float x = m.NV[i];
+        const float h = tc::tf32_rn(x);
+        hi[i] = h; lo[i] = tc::tf32_rn(x - h); bf[i] = __float2bfloat16(x);
+    }
+}
+
+// exact mode: warp per node, AW_QT contexts per block (their rows staged in
+// shared memory), the node row read once per block into registers; float64
+// FMA over H, lane-strided, then a warp reduction per context
+constexpr int AW_QT = 8;
+template <int VEC>
+__global__ void __launch_bounds__(256) k_all_acts_f64(DevModel m, int64_t n, const int32_t *ctx, const float *h,
+                                                      double *act, int64_t ld) {
+    extern __shared__ float4 aw_h4[];
+    float *hs = reinterpret_cast<float *>(aw_h4);
+    const int H = m.H;
+    const int64_t q0 = (int64_t)blockIdx.y * AW_QT;
+    const int nq = (int)min((int64_t)AW_QT, n - q0);
+    for (int t = threadIdx.x; t < AW_QT * H; t += blockDim.x) {
+        const int q = t / H, k = t - q * H;
+        hs[t] = q < nq ? h[(size_t)ctx[q0 + q] * H + k] : 0.f;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); j < m.V - 1; j += nw) {
+        const float *row = m.NV + (size_t)j * H;
+        double a[AW_QT];
+#pragma unroll
+        for (int q = 0; q < AW_QT; q++) a[q] = 0.0;
+        if (VEC == 4) {
+            for (int k = lane; k < H / 4; k += 32) {
+                const float4 t = __ldg(reinterpret_cast<const float4 *>(row) + k);
+#pragma unroll
+                for (int q = 0; q < AW_QT; q++) {
+                    const float4 hh = reinterpret_cast<const float4 *>(hs + q * H)[k];
+                    a[q] = fma((double)t.x, (double)hh.x, a[q]); a[q] = fma((double)t.y, (double)hh.y, a[q]);
+                    a[q] = fma((double)t.z, (double)hh.z, a[q]); a[q] = fma((double)t.w, (double)hh.w, a[q]);
+                }
+            }
+        } else {
+            for (int k = lane; k < H; k += 32) {
+                const double t = (double)__ldg(row + k);
+#pragma unroll
+                for (int q = 0; q < AW_QT; q++) a[q] = fma(t, (double)hs[q * H + k], a[q]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < AW_QT; q++) {
+            const double v = warp_sum_d(a[q]);
+            if (lane == q && q < nq) act[(q0 + q) * ld + j] = v;
+        }
+    }
+}
+
+// per (context, node): + MaxEnt, then log-sigmoid of +a and -a
+template <typename T>
+__global__ void k_all_node_lsig(DevModel m, int64_t n, const int32_t *ctx, const int32_t *hist,
+                                const int32_t *hist_len, const T *act, int64_t ld, double2 *ls) {
+    const int64_t q = blockIdx.y;
+    if (q >= n) return;
+    const int c = ctx[q];
+    const int L = hist_len[c];
+    const int kmax = m.order < L ? m.order : L;
+    uint64_t pre[OTF_MAX_ORDER];
+    for (int k = 0; k < kmax; k++) {
+        uint64_t x = otf_mix(m.seed, (uint64_t)(k + 1));
+        for (int i = L - (k + 1); i < L; i++) x = otf_mix(x, (uint64_t)hist[(size_t)c * m.order + i]);
+        pre[k] = x;
+    }
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < m.V - 1; j += (int64_t)gridDim.x * blockDim.x) {
+        double a = (double)act[q * ld + j];
+        for (int k = 0; k < kmax; k++) a += (double)__ldg(m.ME + (otf_mix(pre[k], (uint64_t)j) & m.mask));
+        ls[q * (int64_t)(m.V - 1) + j] = make_double2(otf_log_sigmoid(a), otf_log_sigmoid(-a));
+    }
+}
+
+__global__ void k_all_word_paths(DevModel m, int64_t n, const double2 *ls, double *out) {
+    const int64_t q = blockIdx.y;
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n || w >= m.V) return;
+    const double2 *l = ls + q * (int64_t)(m.V - 1);
+    double lp = 0.0;
+    for (uint32_t p = m.path_off[w]; p < m.path_off[w + 1]; p++) {
+        const uint32_t c = m.path_code[p];
+        const double2 v = l[c & 0x7FFFFFFFu];
+        lp += (c & 0x80000000u) ? v.y : v.x;
+    }
+    out[q * (int64_t)m.V + w] = lp;
+}
+
+extern "C" int otflm_all_word_logprobs_batch(const OtflmModel *m, int64_t n, const int32_t *ctx,
+                                             const float *h, const int32_t *hist, const int32_t *hist_len,
+                                             double *out, int32_t precision, void *stream) {
+    if (n <= 0) return OTFLM_OK;
+    if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    if (!m->d.NV || !m->d.ME || !m->d.path_off) { g_detail = "model has no output layer"; return OTFLM_ERR_VALUE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    const DevModel &d = m->d;
+    const int64_t NV = d.V - 1;
+    const bool tcm = precision != OTFLM_PREC_FP64;
+    if (tcm && (d.H % 4 != 0)) { g_detail = "tensor-core all_word_logprobs needs H % 4 == 0"; return OTFLM_ERR_VALUE; }
+    if (tcm) {
+        std::lock_guard<std::mutex> lk(m->nv_mu);
+        if (!m->NV_hi) {
+            OtflmModel *mm = const_cast<OtflmModel *>(m);
+            if (mm->mem.alloc(&mm->NV_hi, (size_t)NV * d.H) || mm->mem.alloc(&mm->NV_lo, (size_t)NV * d.H) ||
+                mm->mem.alloc(&mm->NV_bf, (size_t)NV * d.H)) { g_detail = "cudaMalloc NV split"; return OTFLM_ERR_NOMEM; }
+            k_split_nv<<<1184, 256, 0, s>>>(d, mm->NV_hi, mm->NV_lo, mm->NV_bf);
+            CKL();
+        }
+    }
+    // contexts in chunks: activations + node log-sigmoids are [chunk, V-1]
+    const int64_t ld = (NV + 3) / 4 * 4;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)(512ll << 20) / (ld * 20)));
+    void *act = nullptr; double2 *ls = nullptr;
+    CK(cudaMallocAsync(&act, (size_t)chunk * ld * (tcm ? 4 : 8), s));
+    CK(cudaMallocAsync(&ls, (size_t)chunk * NV * sizeof(double2), s));
+    int rc = OTFLM_OK;
+    for (int64_t q0 = 0; q0 < n && rc == OTFLM_OK; q0 += chunk) {
+        const int64_t nq = std::min(chunk, n - q0);
+        if (tcm) {
+            tc::TcB B{m->NV_hi, m->NV_lo, m->NV_bf, (int)NV, (int)((NV + 31) / 32 * 32), (float *)act, ld};
+            const RowSpec rs{nullptr, nullptr, nullptr, nullptr, nullptr, 0xFFFFFFFFu};
+            if (tc_gemm_launch(d, precision, (uint32_t)nq, rs, ctx + q0, nullptr, h, nullptr, &B, s)) {
+                g_detail = "tcgen05 all_word GEMM launch failed"; rc = OTFLM_ERR_CUDA; break;
+            }
+            g_launches++;
+            k_all_node_lsig<float><<<dim3(cdiv(NV, 256 * 4), (unsigned)nq), 256, 0, s>>>(
+                d, nq, ctx + q0, hist, hist_len, (const float *)act, ld, ls);
+        } else {
+            const size_t sm = (size_t)AW_QT * d.H * sizeof(float);
+            const dim3 grid((unsigned)std::min<int64_t>(cdiv(NV, 8), 1184), cdiv(nq, AW_QT));
+            if (d.H % 4 == 0) {
+                CK(cudaFuncSetAttribute(k_all_acts_f64<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                k_all_acts_f64<4><<<grid, 256, sm, s>>>(d, nq, ctx + q0, h, (double *)act, ld);
+            } else {
+                CK(cudaFuncSetAttribute(k_all_acts_f64<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                k_all_acts_f64<1><<<grid, 256, sm, s>>>(d, nq, ctx + q0, h, (double *)act, ld);
+            }
+            g_launches++;
+            k_all_node_lsig<double><<<dim3(cdiv(NV, 256 * 4), (unsigned)nq), 256, 0, s>>>(
+                d, nq, ctx + q0, hist, hist_len, (const double *)act, ld, ls);
+        }
+        g_launches++;
+        k_all_word_paths<<<dim3(cdiv(d.V, 256), (unsigned)nq), 256, 0, s>>>(d, nq, ls, out + q0 * d.V);
+        CKL();
+    }
+    CK(cudaFreeAsync(act, s));
+    CK(cudaFreeAsync(ls, s));
+    return rc;
 }
 
 // ==========================================================================

@@ -177,11 +177,22 @@ __device__ __forceinline__ uint32_t tile_off(int row, int c) {
 //               while tile i+1 is still in the MMA pipe.
 // Grid: persistent CTAs over tiles = (row tile of 128) x (N tile of bn).
 constexpr int WS_THREADS = 288;
-template <int MODE, int KC_B>
+// The B operand and the epilogue.  EPI 0 (recurrent update): B = W (n_rows =
+// H output units), h' = sigmoid(acc + U[w]) into arena rows.  EPI 1 (raw
+// product, all_word_logprobs): B = the node vectors (n_rows = V - 1), the fp32
+// accumulator goes to out[q * ld + j] as is.
+struct TcB {
+    const float *hi, *lo;           // tf32-rounded split (TF32X3 / TF32), [n_rows, H]
+    const __nv_bfloat16 *bf;        // bf16 copy (BF16)
+    int n_rows, n_pad;              // N extent, rounded up to the N granule
+    float *out;                     // EPI 1
+    int64_t ld;
+};
+template <int MODE, int KC_B, int EPI>
 __global__ void __launch_bounds__(WS_THREADS, 1)
 k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__ in_row,
              const int32_t *__restrict__ words, const float *__restrict__ h_base,
-             float *__restrict__ out_base, uint32_t row_limit_unused, int bn_max, int stages,
+             float *__restrict__ out_base, TcB B, int bn_max, int stages,
              uint32_t tmem_cols) {
     constexpr bool BF = MODE == 2;
     constexpr bool X3 = MODE == 1;
@@ -196,7 +207,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     if (rs.cur && blockIdx.x == 0 && threadIdx.x == 0) rs.cur->base = out0;
     if ((uint64_t)out0 + n > row_limit) return;     // arena overflow (flagged by the HS stage)
     const int H = m.H;
-    const int n_pad = H > 256 ? (H + 31) / 32 * 32 : (H + 15) / 16 * 16;
+    const int n_pad = B.n_pad, NR = B.n_rows;
     const uint32_t m_tiles = (n + BM - 1) / BM;
     // the row count is only known on the device: narrow the N tile while the
     // tiles still fit one per CTA (smem ring and TMEM are sized for bn_max)
@@ -245,6 +256,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     const int NK = (H + KE - 1) / KE;
     const uint32_t sbo = CH * 128, lbo = 128;
     const bool vec_ok = (H & 3) == 0;
+    const bool vec_ok_b = BF ? (H & 7) == 0 : vec_ok;   // 16-byte B chunks = 8 bf16
     const uint32_t my_tiles = (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const uint32_t total_chunks = my_tiles * (uint32_t)NK;
 
@@ -323,22 +335,22 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                 const int row = g8 * 8 + r8;
                 const int wrow = n0 + row;
                 const int kk = k0 + c * (16 / ELT);
-                const bool ok = wrow < H && kk < H && vec_ok;
+                const bool ok = wrow < NR && kk < H && vec_ok_b;
                 const uint32_t off = tile_off<KC_B>(row, c);
                 if (BF) {
-                    cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_bf + (size_t)wrow * H + kk) : (const void *)m.W_bf, ok);
+                    cp_async16(smem_u32(sB + off), ok ? (const void *)(B.bf + (size_t)wrow * H + kk) : (const void *)B.bf, ok);
                 } else {
-                    cp_async16(smem_u32(sB + off), ok ? (const void *)(m.W_hi + (size_t)wrow * H + kk) : (const void *)m.W_hi, ok);
+                    cp_async16(smem_u32(sB + off), ok ? (const void *)(B.hi + (size_t)wrow * H + kk) : (const void *)B.hi, ok);
                     if (X3)
-                        cp_async16(smem_u32(sB + b_bytes + off), ok ? (const void *)(m.W_lo + (size_t)wrow * H + kk) : (const void *)m.W_lo, ok);
+                        cp_async16(smem_u32(sB + b_bytes + off), ok ? (const void *)(B.lo + (size_t)wrow * H + kk) : (const void *)B.lo, ok);
                 }
-                if (!vec_ok && wrow < H) {
+                if (!vec_ok_b && wrow < NR) {
                     for (int e = 0; e < 16 / ELT; e++) {
                         const bool in = kk + e < H;
-                        if (BF) reinterpret_cast<__nv_bfloat16 *>(sB + off)[e] = in ? m.W_bf[(size_t)wrow * H + kk + e] : __float2bfloat16(0.f);
+                        if (BF) reinterpret_cast<__nv_bfloat16 *>(sB + off)[e] = in ? B.bf[(size_t)wrow * H + kk + e] : __float2bfloat16(0.f);
                         else {
-                            reinterpret_cast<float *>(sB + off)[e] = in ? m.W_hi[(size_t)wrow * H + kk + e] : 0.f;
-                            if (X3) reinterpret_cast<float *>(sB + b_bytes + off)[e] = in ? m.W_lo[(size_t)wrow * H + kk + e] : 0.f;
+                            reinterpret_cast<float *>(sB + off)[e] = in ? B.hi[(size_t)wrow * H + kk + e] : 0.f;
+                            if (X3) reinterpret_cast<float *>(sB + b_bytes + off)[e] = in ? B.lo[(size_t)wrow * H + kk + e] : 0.f;
                         }
                     }
                 }
@@ -404,6 +416,28 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t q = q0 + row;
             const bool valid = q < n;
+            if (EPI == 1) {           // raw product rows (all_word_logprobs activations)
+                float *orow = B.out + (int64_t)q * B.ld;
+                for (int c0 = 0; c0 < bn; c0 += 32) {
+                    float v[32];
+                    tmem_ld32(tmem + buf * (uint32_t)bn + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, v);
+                    const int gc = n0 + c0;
+                    if (valid) {
+                        if (gc + 32 <= NR && (B.ld & 3) == 0) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4)
+                                *reinterpret_cast<float4 *>(orow + gc + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                        } else {
+                            for (int j = 0; j < 32; j++) if (gc + j < NR) orow[gc + j] = v[j];
+                        }
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(&tempty[buf])) : "memory");
+                continue;
+            }
             const int wq = valid ? (words ? __ldg(words + q) : (int32_t)q) : 0;
             unsigned long long dig = 0ull;
             const float *urow = m.U + (size_t)wq * H;
@@ -455,17 +489,27 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
 
 }  // namespace tc
 
-static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const RowSpec &rs,
-                             const int32_t *in_row, const int32_t *words, const float *h_base,
-                             float *out_base, uint32_t row_limit, cudaStream_t s) {
+// EPI 0 with B = W (the recurrent update) unless b is given (EPI 1).
+static int tc_gemm_launch(const DevModel &m, int prec, uint32_t n_cap, const RowSpec &rs,
+                          const int32_t *in_row, const int32_t *words, const float *h_base,
+                          float *out_base, const tc::TcB *b, cudaStream_t s) {
     const int H = m.H;
-    const int n_pad = H > 256 ? (H + 31) / 32 * 32 : (H + 15) / 16 * 16;
-    if (n_pad > 512) return -1;
+    tc::TcB B{};
+    const int epi = b ? 1 : 0;
+    if (b) {
+        B = *b;
+    } else {
+        B.hi = m.W_hi; B.lo = m.W_lo; B.bf = m.W_bf;
+        B.n_rows = H;
+        B.n_pad = H > 256 ? (H + 31) / 32 * 32 : (H + 15) / 16 * 16;
+        if (B.n_pad > 512) return -1;
+    }
+    const int n_pad = B.n_pad;
     const uint32_t m_tiles = (n_cap + tc::BM - 1) / tc::BM;
     // Small problems (one decode level) are latency-bound: one tile per CTA,
     // 128-byte K chunks (half the pipeline steps).  Large ones stream tiles
     // through persistent CTAs with 64-byte chunks and deeper rings.
-    const bool small = m_tiles < 148;
+    const bool small = epi ? m_tiles * (uint64_t)((n_pad + 255) / 256) < 148 : m_tiles < 148;
     int bn = std::min(std::min(n_pad, 256), prec == 1 ? 128 : 256);   // bn_max; the kernel narrows it
     bn = (bn + 15) / 16 * 16;
     uint32_t cols = 32;
@@ -484,23 +528,33 @@ static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const 
     const uint64_t tiles = small ? (uint64_t)m_tiles * ((n_pad + 31) / 32)      // finest split
                                  : (uint64_t)m_tiles * ((n_pad + bn - 1) / bn);
     cudaError_t e;
-#define TC_LAUNCH(MODE, KCB)                                                                    \
+#define TC_LAUNCH(MODE, KCB, EPI)                                                               \
     do {                                                                                        \
-        e = cudaFuncSetAttribute(tc::k_advance_tc<MODE, KCB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        e = cudaFuncSetAttribute(tc::k_advance_tc<MODE, KCB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (e != cudaSuccess) return -9;                                                        \
         int per_sm = 1;                                                                         \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc::k_advance_tc<MODE, KCB>, tc::WS_THREADS, smem); \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc::k_advance_tc<MODE, KCB, EPI>, tc::WS_THREADS, smem); \
         per_sm = std::max(1, std::min(per_sm, (int)(512 / cols)));                              \
         const dim3 grid((unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, (uint64_t)148 * per_sm))); \
-        tc::k_advance_tc<MODE, KCB><<<grid, tc::WS_THREADS, smem, s>>>(m, n_cap, rs, in_row, words, h_base, \
-                                                                        out_base, row_limit, bn, stages, cols); \
+        tc::k_advance_tc<MODE, KCB, EPI><<<grid, tc::WS_THREADS, smem, s>>>(m, n_cap, rs, in_row, words, h_base, \
+                                                                             out_base, B, bn, stages, cols); \
     } while (0)
-    if (kcb == 128) {
-        if (prec == 1) TC_LAUNCH(1, 128); else if (prec == 2) TC_LAUNCH(2, 128); else if (prec == 3) TC_LAUNCH(3, 128); else return -1;
-    } else {
-        if (prec == 1) TC_LAUNCH(1, 64); else if (prec == 2) TC_LAUNCH(2, 64); else if (prec == 3) TC_LAUNCH(3, 64); else return -1;
-    }
+#define TC_PREC(KCB, EPI)                                                                       \
+    do {                                                                                        \
+        if (prec == 1) TC_LAUNCH(1, KCB, EPI); else if (prec == 2) TC_LAUNCH(2, KCB, EPI);      \
+        else if (prec == 3) TC_LAUNCH(3, KCB, EPI); else return -1;                             \
+    } while (0)
+    if (kcb == 128) { if (epi) TC_PREC(128, 1); else TC_PREC(128, 0); }
+    else { if (epi) TC_PREC(64, 1); else TC_PREC(64, 0); }
+#undef TC_PREC
 #undef TC_LAUNCH
     e = cudaGetLastError();
     return e == cudaSuccess ? 0 : -9;
+}
+
+static int tc_advance_launch(const DevModel &m, int prec, uint32_t n_cap, const RowSpec &rs,
+                             const int32_t *in_row, const int32_t *words, const float *h_base,
+                             float *out_base, uint32_t row_limit, cudaStream_t s) {
+    (void)row_limit;
+    return tc_gemm_launch(m, prec, n_cap, rs, in_row, words, h_base, out_base, nullptr, s);
 }

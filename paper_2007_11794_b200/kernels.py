@@ -188,3 +188,21 @@ def advance_hidden_batch(dmodel: DeviceModel, ctx, h, words, precision: str = "f
                                                       _lib.PREC[precision], current_stream_ptr()),
                "advance_hidden_batch")
     return out
+
+
+def all_word_logprobs_batch(dmodel: DeviceModel, ctx, h, hist, hist_len, precision: str = "fp64",
+                            out=None):
+    """all_word_logprobs (_kernels_nb.py:89-104) for n contexts: device
+    tensors in, float64 [n, V] out.  precision "fp64": float64 CUDA-core dot
+    products; a tensor-core mode: the [n x (V-1)] node activations are one
+    tcgen05 GEMM against the node vectors."""
+    torch = cuda()
+    n = int(ctx.shape[0])
+    if out is None:
+        out = torch.empty((n, dmodel.V), dtype=torch.float64, device=ctx.device)
+    _lib.check(_lib.load().otflm_all_word_logprobs_batch(dmodel.handle, n, ctx.data_ptr(), h.data_ptr(),
+                                                         hist.data_ptr(), hist_len.data_ptr(),
+                                                         out.data_ptr(), _lib.PREC[precision],
+                                                         current_stream_ptr()),
+               "all_word_logprobs_batch")
+    return out

@@ -176,3 +176,56 @@ def test_word_logprob_fast_mode_within_spec(V, H, torch):
                                      torch.from_numpy(hl).cuda(), torch.from_numpy(w).cuda(),
                                      exact=False).cpu().numpy()
     assert np.max(np.abs(got - want)) <= 1e-5
+
+
+@pytest.mark.parametrize("precision", ["fp64", "tf32x3", "bf16"])
+def test_all_word_logprobs_batch(golden, precision):
+    """Batched full-vocabulary scoring vs the reference's all_word_logprobs
+    (kernels.npz q_all): fp64 |d| <= 1e-12; tcgen05 TF32X3 |d| <= 1e-5 per
+    word; BF16 |d| <= 5e-2 (bf16 operands, the stated looser bound)."""
+    import torch
+    from conftest import GoldenModel
+    from paper_2007_11794_b200 import kernels
+    from paper_2007_11794_b200.device import DeviceModel
+    d = golden("kernels")
+    gm = GoldenModel(d)
+    dm = DeviceModel(gm.model, gm.tree)
+    k = d["q_all"].shape[0]
+    t = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x, dt)).cuda()
+    hist = np.where(d["q_hist"][:k] < 0, 0, d["q_hist"][:k]).astype(np.int32)
+    ctx = t(np.arange(k)[::-1].copy(), np.int32)     # gathered rows, any order
+    out = kernels.all_word_logprobs_batch(dm, ctx, t(d["q_h"][:k], np.float32), t(hist, np.int32),
+                                          t(d["q_hl"][:k], np.int32), precision).cpu().numpy()
+    want = d["q_all"][::-1]
+    tol = {"fp64": 1e-12, "tf32x3": 1e-5, "bf16": 5e-2}[precision]
+    assert np.abs(out - want).max() <= tol
+    assert np.all(np.abs(np.exp(out).sum(axis=1) - 1.0) <= (1e-9 if precision == "fp64" else 1e-4))
+
+
+@pytest.mark.parametrize("precision", ["fp64", "tf32x3"])
+def test_all_word_logprobs_batch_config_c(precision):
+    """V = 65,536, H = 512 (config c): 6 contexts vs the oracle; every
+    distribution normalised (acceptance crit 1, tests/test_acceptance.py:74-86).
+    TF32X3 bound: fp32 accumulation of 512 products per node activation
+    (~5e-6) summed over paths of up to 20 nodes -> |d| <= 3e-4 per word."""
+    import torch
+    from oracle import oracle as O
+    from paper_2007_11794_b200 import kernels, synth
+    from paper_2007_11794_b200.device import DeviceModel
+    from paper_2007_11794_b200.model import build_huffman_from_counts
+    V, H, bits = 65536, 512, 22
+    model = synth.synth_model(V, H, bits)
+    tree = build_huffman_from_counts(synth.zipf_counts(V))
+    dm = DeviceModel(model, tree)
+    words, hidden, hist, hlen, _ = synth.query_set(model, 16, 6)
+    hlen = np.array([0, 1, 2, 3, 3, 3], np.int32)
+    t = lambda x, dt: torch.from_numpy(np.ascontiguousarray(x, dt)).cuda()
+    out = kernels.all_word_logprobs_batch(dm, t(np.arange(6), np.int32), t(hidden, np.float32),
+                                          t(hist, np.int32), t(hlen, np.int32), precision).cpu().numpy()
+    for i in range(6):
+        want = O.all_word_logprobs(hidden[i], hist[i, :hlen[i]], tree.path_nodes, tree.path_signs,
+                                   tree.path_offsets, model.node_vectors, model.maxent_table,
+                                   model.maxent_order, model.hash_seed, model.maxent_size - 1)
+        tol = 1e-11 if precision == "fp64" else 3e-4
+        assert np.abs(out[i] - want).max() <= tol, (i, np.abs(out[i] - want).max())
+        assert abs(np.exp(out[i]).sum() - 1.0) <= (1e-9 if precision == "fp64" else 1e-4)
