@@ -51,6 +51,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-queries", action="store_true", help="skip the config-d query microbench")
     ap.add_argument("--beam-sweep", action="store_true", help="add the config-c beam sweep extra")
+    ap.add_argument("--config", default="b", choices=["b", "e"],
+                    help="b: the headline config (default); e: 4096 utterances at V=64k sharded over ranks")
+    ap.add_argument("--e-total", type=int, default=4096, help="config e: total utterances")
+    ap.add_argument("--e-batch", type=int, default=74,
+                    help="config e: streams decoded at once per GPU (74 2-CTA clusters = 148 SMs)")
     ap.add_argument("--all-word", action="store_true", help="add the all_word_logprobs extra")
     ap.add_argument("--twopass-n", type=int, default=1000, help="n-best size of the two-pass extra (0: skip)")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
@@ -372,10 +377,156 @@ def run_reference(args):
         Path(args.out).write_text(json.dumps(line) + "\n")
 
 
+_E_BASE = None
+
+
+def _e_lattices(ids):
+    from paper_2007_11794_b200 import synth
+    base, frames = _E_BASE
+    return synth.lattices_for_ids(base, ids, frames)
+
+
+def run_config_e(args):
+    """Config (e): 4,096 utterances (V=65,536, H=512, MaxEnt 2^22, 300
+    frames, breadth 3, beam 8) sharded over the ranks (utterance i of rank r's
+    contiguous shard, parallel.shard); each rank decodes its shard in batches
+    of --n-utt streams through the double-buffered BatchDecoder (host compile
+    + H2D of batch i+1 overlap the decode of batch i), then NCCL all-gathers
+    the per-utterance result records.  One step = the whole shard; strong
+    scaling (total work fixed)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2007_11794_b200 import parallel, synth
+    from paper_2007_11794_b200.rescore import BatchDecoder
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n_total = args.e_total
+    ids = parallel.shard(n_total, world, rank)
+    B = args.e_batch
+    base = synth.build_setup("e", n_utt=1, T=args.frames, seed=31)
+    # lattices of this rank's shard, generated on host worker processes
+    # (forked before CUDA is initialised; each lattice is a function of its id)
+    t0 = time.perf_counter()
+    global _E_BASE
+    _E_BASE = (base, args.frames)
+    import multiprocessing as mp
+    n_proc = max(1, min(len(os.sched_getaffinity(0)) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1"))), 32))
+    parts = [ids[i:i + 16] for i in range(0, len(ids), 16)]
+    with mp.get_context("fork").Pool(n_proc) as pool:
+        lat_parts = pool.map(_e_lattices, parts)
+    lat_all = [l for part in lat_parts for l in part]
+    batches = [(ids[b0:b0 + B], lat_all[b0:b0 + B]) for b0 in range(0, len(ids), B)]
+    t_gen = time.perf_counter() - t0
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    need = max(BatchDecoder.contexts_needed(l, base.beam) for _, l in batches)
+    dec = BatchDecoder(base.model, base.tree, base.small_lm, B, need, precision=args.precision,
+                       schedule=args.schedule, n_buffers=2)
+    stream = torch.cuda.current_stream()
+
+    def one_pass(record: bool):
+        """decode the shard: device time (sum of batch decodes) and e2e."""
+        dev_ms = 0.0
+        recs = []
+        frames = 0
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        s_prev, prev_sel = None, None
+        evs = []
+        for sel, lats in batches:
+            s_cur = dec.prepare(lats, base.beam)          # host compile + H2D (overlaps the previous decode)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dec.run(1.0, slot=s_cur)
+            e1.record(stream)
+            evs.append((e0, e1))
+            if s_prev is not None:
+                hyps, out = dec.fetch(slot=s_prev)
+                frames += int(sum(len(h.arcs) for h in hyps[:len(prev_sel)]))
+                if record:
+                    recs.append(parallel.pack_records(prev_sel, out, args.frames))
+            s_prev, prev_sel = s_cur, sel
+        hyps, out = dec.fetch(slot=s_prev)
+        frames += int(sum(len(h.arcs) for h in hyps[:len(prev_sel)]))
+        if record:
+            recs.append(parallel.pack_records(prev_sel, out, args.frames))
+        b.record(stream)
+        torch.cuda.synchronize()
+        dev_ms = sum(x.elapsed_time(y) for x, y in evs)
+        return dev_ms, a.elapsed_time(b), frames, recs
+
+    for _ in range(args.warmup):
+        one_pass(False)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    dev, e2e, fr = [], [], 0
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            d_ms, e_ms, fr, recs = one_pass(i == args.steps - 1)
+            dev.append(d_ms)
+            e2e.append(e_ms)
+    dev_ms, e2e_ms = float(np.mean(dev)), float(np.mean(e2e))
+    if world > 1:
+        t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, e2e_ms = (float(x) for x in t.cpu())
+        allr = parallel.gather_records(np.concatenate(recs), n_total, device="cuda")
+    else:
+        allr = np.concatenate(recs)
+    total_frames = int(allr[:, 1].sum())
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from types import SimpleNamespace
+        threads = len(os.sched_getaffinity(0))
+        n_sample = max(threads, 16)
+        sample = SimpleNamespace(model=base.model, tree=base.tree, small_lm=base.small_lm,
+                                 beam=base.beam, lattices=batches[0][1][:n_sample])
+        f, r, dt, _ = cpu_baseline(sample, n_sample, threads)
+        cpu = {"value": f / dt, "unit": "frames/s", "cores": threads, "kind": "port",
+               "sample": f"the first {n_sample} utterances of the shard x {args.frames} frames "
+                         "(oracle/otflm_oracle.c, all host threads)"}
+    if rank == 0:
+        line = {
+            "metric": "decode frames/sec (RNNLM on-the-fly rescoring, config e: V=64k H=512, 4096 utt x 300 frames, beam 8)",
+            "value": total_frames / (dev_ms / 1e3), "unit": "frames/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64 scores / f32 weights / " + args.precision + " recurrent update",
+            "data": "synthetic (seeded per utterance id)",
+            "config": {"workload": f"config e: V=65536 H=512 MaxEnt 2^22, {n_total} utterances x {args.frames} "
+                                   f"frames sharded over {world} GPU(s), batches of {B} streams, breadth 3, beam 8",
+                       "n_utt_total": n_total, "batch_streams": B, "precision": args.precision,
+                       "schedule": dec.schedule, "lattice_generation_s": t_gen,
+                       "l2": "inputs (4096 lattices, arenas) far larger than L2"},
+            "rtf": (dev_ms / 1e3) / (total_frames * FRAME_S),
+            "rtf_per_stream": (dev_ms / 1e3) / len(batches) / (args.frames * FRAME_S),
+            "utterances_gathered": int(len(allr)),
+            "e2e": {"value": total_frames / (e2e_ms / 1e3), "unit": "frames/s", "ms_per_step": e2e_ms,
+                    "pipeline": "double-buffered batches: host compile + pinned H2D of batch i+1 overlap the decode of batch i; 1-best D2H per batch"},
+            "clocks": clk.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+        if args.out:
+            Path(args.out).write_text(json.dumps(line) + "\n")
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.config == "e":
+        run_config_e(args)
         return
     import torch
     import torch.distributed as dist

@@ -117,6 +117,19 @@ def more_lattices(setup: Setup, n_utt: int, T: int, seed: int) -> list:
                              index=index) for i in range(n_utt)]
 
 
+def lattices_for_ids(setup: Setup, ids, T: int, seed_base: int = 1000) -> list:
+    """One lattice per utterance id, a function of the id alone (so any
+    sharding of the ids over ranks sees the same utterances)."""
+    V = setup.model.vocab_size
+    index = _BigramIndex(setup.small_lm)
+    out = []
+    for u in ids:
+        ref = reference_sentences(V, 1, T, seed_base + int(u))[0]
+        out.append(generate_lattice(ref, V, setup.small_lm, setup.breadth,
+                                    noise_seed=(seed_base + int(u)) * 100003, index=index))
+    return out
+
+
 def query_set(model: RnnlmModel, n_queries: int, n_ctx: int, seed_w: int = 4, seed_c: int = 5):
     """Config (d): words ~ Zipf(1.05) over V, distinct contexts with
     h ~ U(0.001, 0.999) and 3-word histories ~ U[0, V)."""
