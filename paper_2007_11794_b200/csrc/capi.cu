@@ -119,8 +119,8 @@ __global__ void k_prep_weights(DevModel m, float *WT, float *W_hi, float *W_lo, 
 }
 
 // W_hi / W_lo into the persistent kernel's chunked canonical tiles (see DevModel::W_t)
-__global__ void k_prep_wtiles(DevModel m, float *wt) {
-    const int H = m.H, np = m.wt_npad, kcb = m.wt_kcb, KE = kcb / 4;
+__global__ void k_prep_wtiles(DevModel m, float *wt, int kcb) {
+    const int H = m.H, np = m.wt_npad, KE = kcb / 4;
     const int NK = (H + KE - 1) / KE;
     const int64_t total = (int64_t)NK * 2 * np * KE;
     const int64_t blk = (int64_t)np * KE;                  // floats per [hi] or [lo] block
@@ -193,7 +193,7 @@ extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, Otflm
     dm.U = U; dm.W = W; dm.WT = WT; dm.NV = NV; dm.ME = ME;
     dm.path_off = poff; dm.path_code = pcode;
     dm.W_hi = Whi; dm.W_lo = Wlo; dm.W_bf = Wbf;
-    dm.W_t = nullptr; dm.wt_kcb = 0; dm.wt_npad = 0;
+    dm.W_t = nullptr; dm.wt_kcb = 0; dm.wt_npad = 0; dm.W_t64 = nullptr;
     if (W) {
         k_prep_weights<<<256, 256>>>(dm, WT, Whi, Wlo, Wbf);
         CK(cudaGetLastError());
@@ -204,7 +204,13 @@ extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, Otflm
             const size_t nwt = (size_t)NK * 2 * np * KE;
             if (m->mem.alloc(&Wt, nwt) != cudaSuccess) { m->mem.free_all(); delete m; g_detail = "cudaMalloc model"; return OTFLM_ERR_NOMEM; }
             dm.W_t = Wt; dm.wt_kcb = kcb; dm.wt_npad = np;
-            k_prep_wtiles<<<256, 256>>>(dm, Wt);
+            k_prep_wtiles<<<256, 256>>>(dm, Wt, kcb);
+            CK(cudaGetLastError());
+            float *Wt64 = nullptr;
+            const size_t nwt64 = (size_t)((H + 15) / 16) * 2 * np * 16;
+            if (m->mem.alloc(&Wt64, nwt64) != cudaSuccess) { m->mem.free_all(); delete m; g_detail = "cudaMalloc model"; return OTFLM_ERR_NOMEM; }
+            dm.W_t64 = Wt64;
+            k_prep_wtiles<<<256, 256>>>(dm, Wt64, 64);
             CK(cudaGetLastError());
         }
     }
@@ -640,7 +646,10 @@ extern "C" int otflm_all_word_logprobs_batch(const OtflmModel *m, int64_t n, con
     for (int64_t q0 = 0; q0 < n && rc == OTFLM_OK; q0 += chunk) {
         const int64_t nq = std::min(chunk, n - q0);
         if (tcm) {
-            tc::TcB B{m->NV_hi, m->NV_lo, m->NV_bf, (int)NV, (int)((NV + 31) / 32 * 32), (float *)act, ld};
+            tc::TcB B{};
+            B.hi = m->NV_hi; B.lo = m->NV_lo; B.bf = m->NV_bf;
+            B.n_rows = (int)NV; B.n_pad = (int)((NV + 31) / 32 * 32);
+            B.out = (float *)act; B.ld = ld;
             const RowSpec rs{nullptr, nullptr, nullptr, nullptr, nullptr, 0xFFFFFFFFu};
             if (tc_gemm_launch(d, precision, (uint32_t)nq, rs, ctx + q0, nullptr, h, nullptr, &B, s)) {
                 g_detail = "tcgen05 all_word GEMM launch failed"; rc = OTFLM_ERR_CUDA; break;

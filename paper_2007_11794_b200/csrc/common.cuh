@@ -38,6 +38,9 @@ struct DevModel {
     // layout, so one bulk copy moves a whole chunk
     const float *W_t;
     int wt_kcb, wt_npad;
+    // the same with 64-byte K chunks (SWIZZLE_64B), for the batched update
+    // k_advance_tc's B operand: one bulk copy per (K chunk, N tile, hi/lo)
+    const float *W_t64;
 };
 
 struct DevNgram {

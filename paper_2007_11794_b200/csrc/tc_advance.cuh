@@ -176,7 +176,10 @@ __device__ __forceinline__ uint32_t tile_off(int row, int c) {
 //               release the accumulator (tmem_empty[]) so tile i+2 can start
 //               while tile i+1 is still in the MMA pipe.
 // Grid: persistent CTAs over tiles = (row tile of 128) x (N tile of bn).
-constexpr int WS_THREADS = 288;
+constexpr int LW = 8;                 // loader / converter warps 0..LW-1
+constexpr int LT = LW * 32;
+constexpr int MMA_WARP = LW;          // then 4 epilogue warps
+constexpr int WS_THREADS = (LW + 5) * 32;
 // The B operand and the epilogue.  EPI 0 (recurrent update): B = W (n_rows =
 // H output units), h' = sigmoid(acc + U[w]) into arena rows.  EPI 1 (raw
 // product, all_word_logprobs): B = the node vectors (n_rows = V - 1), the fp32
@@ -184,6 +187,8 @@ constexpr int WS_THREADS = 288;
 struct TcB {
     const float *hi, *lo;           // tf32-rounded split (TF32X3 / TF32), [n_rows, H]
     const __nv_bfloat16 *bf;        // bf16 copy (BF16)
+    const float *tiled;             // optional [K chunk][hi | lo][np rows x 64 B] SWIZZLE_64B tiles
+    int tiled_np;
     int n_rows, n_pad;              // N extent, rounded up to the N granule
     float *out;                     // EPI 1
     int64_t ld;
@@ -208,6 +213,8 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     if ((uint64_t)out0 + n > row_limit) return;     // arena overflow (flagged by the HS stage)
     const int H = m.H;
     const int n_pad = B.n_pad, NR = B.n_rows;
+    // B by bulk copy from the pre-tiled swizzled layout (tf32 modes, 64-byte chunks)
+    const bool bulk_b = !BF && KC_B == 64 && B.tiled != nullptr;
     const uint32_t m_tiles = (n + BM - 1) / BM;
     // the row count is only known on the device: narrow the N tile while the
     // tiles still fit one per CTA (smem ring and TMEM are sized for bn_max)
@@ -233,8 +240,8 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
 
     if (tid == 0) {
         for (int st = 0; st < stages; st++) {
-            mbar_init(smem_u32(&full_raw[st]), 128);
-            mbar_init(smem_u32(&full_op[st]), 4);          // one arrival per converter warp
+            mbar_init(smem_u32(&full_raw[st]), LT + (bulk_b ? 1 : 0));
+            mbar_init(smem_u32(&full_op[st]), LW);         // one arrival per converter warp
             mbar_init(smem_u32(&empty[st]), 1);
         }
         for (int b2 = 0; b2 < 2; b2++) {
@@ -243,7 +250,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 4) {
+    if (warp == MMA_WARP) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      :: "r"(smem_u32(tmem_slot)), "r"(tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -260,7 +267,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     const uint32_t my_tiles = (tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const uint32_t total_chunks = my_tiles * (uint32_t)NK;
 
-    if (warp == 4) {
+    if (warp == MMA_WARP) {
         // ------------------------------ MMA issuer ----------------------------
         const uint32_t idesc = make_idesc(BF ? 1 : 2, bn);
         uint32_t g = 0;
@@ -283,12 +290,14 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
 #pragma unroll
                     for (int ks = 0; ks < KC_B / 32; ks++) {     // 32 bytes of K per MMA
                         const uint64_t a_hi = make_desc(smem_u32(sA) + ks * 2 * lbo, lbo, sbo);
-                        const uint64_t b_hi = make_desc(smem_u32(sB) + ks * 2 * lbo, lbo, sbo);
+                        const uint64_t b_hi = bulk_b ? make_desc_sw<64>(smem_u32(sB) + ks * 32)
+                                                     : make_desc(smem_u32(sB) + ks * 2 * lbo, lbo, sbo);
                         const uint32_t acc = (k > 0 || ks > 0) ? 1u : 0u;
                         mma_elect<BF>(dacc, a_hi, b_hi, idesc, acc);
                         if (X3) {
                             const uint64_t a_lo = make_desc(smem_u32(sA2) + ks * 2 * lbo, lbo, sbo);
-                            const uint64_t b_lo = make_desc(smem_u32(sB2) + ks * 2 * lbo, lbo, sbo);
+                            const uint64_t b_lo = bulk_b ? make_desc_sw<64>(smem_u32(sB2) + ks * 32)
+                                                         : make_desc(smem_u32(sB2) + ks * 2 * lbo, lbo, sbo);
                             mma_elect<false>(dacc, a_hi, b_lo, idesc, 1u);
                             mma_elect<false>(dacc, a_lo, b_hi, idesc, 1u);
                         }
@@ -299,8 +308,12 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                 __syncwarp();
             }
         }
-    } else if (warp < 4) {
+    } else if (warp < LW) {
         // ----------------------- loaders / converters -------------------------
+        // source arena rows of this thread's A items, cached per tile
+        constexpr int AI = (BM * (BF ? (KC_B / 2) / 4 : KC_B / 16) + LT - 1) / LT;
+        int src_c[AI];
+        uint32_t src_tile = 0xFFFFFFFFu;
         auto issue = [&](uint32_t gc) {
             const uint32_t it = gc / NK;
             const int k = (int)(gc - it * NK);
@@ -313,14 +326,26 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
             uint8_t *sAop = base + raw_bytes;
             uint8_t *sB = base + raw_bytes + (X3 ? 2 : 1) * a_bytes;
             const int k0 = k * KE;
-            for (int idx = tid; idx < BM * RAW_CH; idx += 128) {
+            if (tile != src_tile) {
+                src_tile = tile;
+#pragma unroll
+                for (int i = 0; i < AI; i++) {
+                    const int idx = tid + i * LT;
+                    const int row = BF ? idx / RAW_CH : ((idx / (8 * CH)) * 8 + (idx & 7));
+                    const uint32_t q = q0 + row;
+                    src_c[i] = (idx < BM * RAW_CH && q < n) ? __ldg(in_row + q) : -1;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < AI; i++) {
+                const int idx = tid + i * LT;
+                if (idx >= BM * RAW_CH) break;
                 int row, c;
                 uint32_t off;
                 if (BF) { row = idx / RAW_CH; c = idx - row * RAW_CH; off = row * RAW_ROW + c * 16; }
                 else { const int r8 = idx & 7, g8 = idx / (8 * CH); c = (idx >> 3) % CH; row = g8 * 8 + r8; off = tile_off<KC_B>(row, c); }
                 uint8_t *dstb = BF ? raw : sAop;
-                const uint32_t q = q0 + row;
-                const int src = q < n ? __ldg(in_row + q) : -1;
+                const int src = src_c[i];
                 const int kk = k0 + c * 4;
                 const bool ok = src >= 0 && kk < H && vec_ok;
                 cp_async16(smem_u32(dstb + off),
@@ -330,7 +355,28 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
                     for (int e = 0; e < 4; e++) dst[e] = kk + e < H ? h_base[(size_t)src * H + kk + e] : 0.f;
                 }
             }
-            for (int idx = tid; idx < bn * CH; idx += 128) {
+            if (bulk_b) {
+                if (warp == 0) {       // hi (+ lo) slices of the pre-tiled chunk: one bulk copy each
+                    const uint32_t part = (uint32_t)B.tiled_np * KC_B;          // bytes of one [hi] block
+                    const uint8_t *src = reinterpret_cast<const uint8_t *>(B.tiled) + (size_t)k * 2 * part +
+                                         (size_t)n0 * KC_B;
+                    const uint32_t bytes = (uint32_t)bn * KC_B;
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    if (X3)
+                        asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 t;\n\telect.sync t|e, 0xffffffff;\n\t"
+                                     "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %4;\n\t"
+                                     "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %3, [%1];\n\t"
+                                     "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%5], [%6], %3, [%1];\n\t}"
+                                     :: "r"(smem_u32(sB)), "r"(smem_u32(&full_raw[st])), "l"(src), "r"(bytes),
+                                        "r"(2u * bytes), "r"(smem_u32(sB + b_bytes)), "l"(src + part) : "memory");
+                    else
+                        asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 t;\n\telect.sync t|e, 0xffffffff;\n\t"
+                                     "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %3;\n\t"
+                                     "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %3, [%1];\n\t}"
+                                     :: "r"(smem_u32(sB)), "r"(smem_u32(&full_raw[st])), "l"(src), "r"(bytes) : "memory");
+                }
+            } else
+            for (int idx = tid; idx < bn * CH; idx += LT) {
                 const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
                 const int row = g8 * 8 + r8;
                 const int wrow = n0 + row;
@@ -367,7 +413,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
             uint8_t *raw = base;
             uint8_t *sA = base + raw_bytes;
             uint8_t *sA2 = sA + a_bytes;
-            for (int idx = tid; idx < BM * CH; idx += 128) {
+            for (int idx = tid; idx < BM * CH; idx += LT) {
                 const int r8 = idx & 7, c = (idx >> 3) % CH, g8 = idx / (8 * CH);
                 const int row = g8 * 8 + r8;
                 const uint32_t off = tile_off<KC_B>(row, c);
@@ -483,7 +529,7 @@ k_advance_tc(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (warp == 4)
+    if (warp == MMA_WARP)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(tmem_cols));
 }
 
@@ -500,6 +546,7 @@ static int tc_gemm_launch(const DevModel &m, int prec, uint32_t n_cap, const Row
         B = *b;
     } else {
         B.hi = m.W_hi; B.lo = m.W_lo; B.bf = m.W_bf;
+        B.tiled = m.W_t64; B.tiled_np = m.wt_npad;
         B.n_rows = H;
         B.n_pad = H > 256 ? (H + 31) / 32 * 32 : (H + 15) / 16 * 16;
         if (B.n_pad > 512) return -1;
@@ -510,7 +557,7 @@ static int tc_gemm_launch(const DevModel &m, int prec, uint32_t n_cap, const Row
     // 128-byte K chunks (half the pipeline steps).  Large ones stream tiles
     // through persistent CTAs with 64-byte chunks and deeper rings.
     const bool small = epi ? m_tiles * (uint64_t)((n_pad + 255) / 256) < 148 : m_tiles < 148;
-    int bn = std::min(std::min(n_pad, 256), prec == 1 ? 128 : 256);   // bn_max; the kernel narrows it
+    int bn = std::min(n_pad, (small && prec == 1) ? 128 : 256);   // bn_max; the kernel narrows it
     bn = (bn + 15) / 16 * 16;
     uint32_t cols = 32;
     while ((int)cols < 2 * bn) cols <<= 1;             // two accumulators
