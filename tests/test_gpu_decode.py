@@ -333,3 +333,66 @@ def test_double_buffered_pipeline_matches_single_batches():
     for r, g in zip(ref, got):
         assert [h.arcs for h in r] == [h.arcs for h in g]
         assert [h.combined_score for h in r] == [h.combined_score for h in g]
+
+
+def _random_dag(rng, n_nodes, V, lm, max_skip=3, out_deg=(1, 4)):
+    """A non-layered lattice: arcs i -> j > i with skips of up to max_skip
+    nodes, several finals, ids not in time order of a sausage (Kahn order
+    interleaves frames), arc small-LM scores from the bigram on a random
+    predecessor word (any weight is legal for the decoder)."""
+    from paper_2007_11794_b200.lattice import Lattice
+    from paper_2007_11794_b200.model import ngram_logprob
+    src, dst, word, ac, slm = [], [], [], [], []
+    for i in range(n_nodes - 1):
+        for _ in range(int(rng.randint(out_deg[0], out_deg[1] + 1))):
+            j = min(n_nodes - 1, i + int(rng.randint(1, max_skip + 1)))
+            w = int(rng.randint(3, V))
+            src.append(i); dst.append(j); word.append(w)
+            ac.append(-abs(float(rng.normal(1.0, 0.7))))
+            slm.append(ngram_logprob(lm, [int(rng.randint(1, V))], w))
+    finals = sorted({n_nodes - 1, n_nodes - 2})
+    return Lattice(0, finals, src=np.array(src), dst=np.array(dst), word=np.array(word),
+                   acoustic=np.array(ac), smalllm=np.array(slm))
+
+
+@pytest.mark.parametrize("schedule,precision", [("level", "fp64"), ("stream", "tf32x3")])
+def test_ragged_and_non_layered_batch_vs_oracle(schedule, precision):
+    """Edge cases in one batch: utterances of 1, 2, 5, 17 and 40 frames next
+    to random non-layered DAGs (skip arcs, several finals, out-degree up to
+    4).  fp64 level schedule: exact 1-best / counters, scores within 1e-9;
+    TF32X3 stream schedule: same 1-best, scores within 1e-4 per arc."""
+    from paper_2007_11794_b200 import synth
+    base = synth.build_setup("a", n_utt=1, T=5, seed=2)
+    rng = np.random.RandomState(12)
+    lats = []
+    for T in (1, 2, 5, 17, 40):
+        lats += synth.more_lattices(base, 1, T, seed=100 + T)
+    for n in (6, 15, 33):
+        lats.append(_random_dag(rng, n, base.model.vocab_size, base.small_lm))
+    s = synth.Setup("ragged", base.model, base.tree, base.small_lm, lats, 8, 3)
+    for beam in (3, 8):
+        ref = O.decode_many(s.model, s.tree, s.small_lm, lats, beam=beam, n_threads=4)
+        hyps, out, st = _decode(s, precision, schedule, beam)
+        for u, (r, (lk, hi, mi)) in enumerate(ref):
+            assert hyps[u].arcs == r.arcs, (u, beam)
+            tol = TOL if precision == "fp64" else 1e-4 * max(1, len(r.arcs))
+            assert abs(hyps[u].combined_score - r.combined_score) <= tol
+            assert int(out["expansions"][u]) == r.expansions
+            if precision == "fp64":
+                assert hyps[u].end_context == r.end_context
+        assert [int(x) for x in st[:, 0]] == [x[1][0] for x in ref]
+        if precision == "fp64":
+            assert [int(x) for x in st[:, 2]] == [x[1][2] for x in ref]
+
+
+def test_config_c_geometry_stream_decode_vs_oracle():
+    """H = 512, V = 65,536 (config c/e geometry): stream schedule TF32X3 vs
+    the exact oracle on 3 utterances x 25 frames."""
+    from paper_2007_11794_b200 import synth
+    s = synth.build_setup("c", n_utt=3, T=25, seed=9)
+    ref = O.decode_many(s.model, s.tree, s.small_lm, s.lattices, beam=8, n_threads=3)
+    hyps, out, st = _decode(s, "tf32x3", "stream", 8)
+    for u, (r, (lk, hi, mi)) in enumerate(ref):
+        assert hyps[u].arcs == r.arcs
+        assert abs(hyps[u].combined_score - r.combined_score) <= 1e-4 * 25
+        assert int(out["expansions"][u]) == r.expansions
