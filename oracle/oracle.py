@@ -91,6 +91,8 @@ def lib():
         L.orc_decode_many.argtypes = [p, p, p, i32, f64, i64, i32, i32, p, p, p, p, p]
         L.orc_query_batch.restype = None
         L.orc_query_batch.argtypes = [p, i64, p, p, p, p, p, p, i32]
+        L.orc_stack_set_capacity.restype = C.c_int
+        L.orc_stack_set_capacity.argtypes = [p, i64]
         L.orc_nbest.restype = C.c_int
         L.orc_nbest.argtypes = [p, i32, f64, p, p, p, i64, p, p]
         L.orc_twopass.restype = C.c_int
@@ -315,9 +317,16 @@ class OracleStats:
 class OracleStack:
     """Oracle RescoreStack (decoder.py:61-70): table + cache + ledger."""
 
-    def __init__(self, model, tree, enabled: bool = True, max_entries: int = (1 << 64) - 2):
+    def __init__(self, model, tree, enabled: bool = True, max_entries: int = (1 << 64) - 2,
+                 capacity_bytes: int = 0):
         self.om = model if isinstance(model, OracleModel) else OracleModel(model, tree)
         self.handle = lib().orc_stack_create(self.om.ref, int(bool(enabled)), int(max_entries))
+        if capacity_bytes:
+            self.set_capacity(capacity_bytes)
+
+    def set_capacity(self, capacity_bytes: int) -> None:
+        """RescoreCache.set_capacity (cache.py:130-137)."""
+        _check(lib().orc_stack_set_capacity(self.handle, int(capacity_bytes)), "set_capacity")
 
     def rnnlm_prob(self, w: int, c: int):
         p = np.zeros(1, np.float64)

@@ -443,7 +443,15 @@ typedef struct {
     int64_t ledger_requests, ledger_bytes_indexed, ledger_bytes_full;
     float *zero_h, *scratch_h;
     int64_t scratch_hist[8];
+    /* capacity-bounded LFU with LRU tie-break (cache.py:98-134): per slot
+     * residency, use count and last use; lazy min-heap of (freq, seq, slot) */
+    int64_t capacity_bytes;   /* 0 = unbounded */
+    uint8_t *resident; int64_t *freq, *last;
+    int64_t seq, n_resident;
+    int64_t *heap; int64_t heap_n, heap_cap;   /* triples */
 } OrcStack;
+
+#define ORC_ENTRY_BYTES 32   /* cache.py:26 */
 
 OrcStack *orc_stack_create(const OrcModel *model, int32_t enabled, uint64_t max_entries) {
     OrcStack *s = (OrcStack *)calloc(1, sizeof(OrcStack));
@@ -454,6 +462,11 @@ OrcStack *orc_stack_create(const OrcModel *model, int32_t enabled, uint64_t max_
     s->cache_cap = 1024;
     s->cache_p = (double *)malloc(sizeof(double) * s->cache_cap);
     s->cache_c = (uint32_t *)malloc(sizeof(uint32_t) * s->cache_cap);
+    s->resident = (uint8_t *)calloc(s->cache_cap, 1);
+    s->freq = (int64_t *)calloc(s->cache_cap, sizeof(int64_t));
+    s->last = (int64_t *)calloc(s->cache_cap, sizeof(int64_t));
+    s->heap_cap = 1024;
+    s->heap = (int64_t *)malloc(sizeof(int64_t) * 3 * s->heap_cap);
     s->zero_h = (float *)calloc((size_t)model->H, sizeof(float));
     s->scratch_h = (float *)calloc((size_t)model->H, sizeof(float));
     return s;
@@ -464,7 +477,68 @@ void orc_stack_destroy(OrcStack *s) {
     orc_table_free(&s->table);
     orc_map_free(&s->cache);
     free(s->cache_p); free(s->cache_c); free(s->zero_h); free(s->scratch_h);
+    free(s->resident); free(s->freq); free(s->last); free(s->heap);
     free(s);
+}
+
+/* lazy heap of (freq, seq, slot), ordered by (freq, seq) -- heapq tuples
+ * (cache.py:95,110); seq is unique per push so the slot never decides */
+static int orc_heap_less(const int64_t *a, const int64_t *b) {
+    return a[0] < b[0] || (a[0] == b[0] && a[1] < b[1]);
+}
+static void orc_heap_push(OrcStack *s, int64_t f, int64_t q, int64_t slot) {
+    if (s->heap_n == s->heap_cap) {
+        s->heap_cap *= 2;
+        s->heap = (int64_t *)realloc(s->heap, sizeof(int64_t) * 3 * s->heap_cap);
+    }
+    int64_t i = s->heap_n++;
+    int64_t *h = s->heap;
+    h[3 * i] = f; h[3 * i + 1] = q; h[3 * i + 2] = slot;
+    while (i > 0) {
+        int64_t p = (i - 1) / 2;
+        if (!orc_heap_less(h + 3 * i, h + 3 * p)) break;
+        for (int k = 0; k < 3; k++) { int64_t t = h[3 * p + k]; h[3 * p + k] = h[3 * i + k]; h[3 * i + k] = t; }
+        i = p;
+    }
+}
+static void orc_heap_pop(OrcStack *s, int64_t *out) {
+    int64_t *h = s->heap;
+    for (int k = 0; k < 3; k++) out[k] = h[k];
+    s->heap_n--;
+    for (int k = 0; k < 3; k++) h[k] = h[3 * s->heap_n + k];
+    int64_t i = 0, n = s->heap_n;
+    for (;;) {
+        int64_t l = 2 * i + 1, r = l + 1, m = i;
+        if (l < n && orc_heap_less(h + 3 * l, h + 3 * m)) m = l;
+        if (r < n && orc_heap_less(h + 3 * r, h + 3 * m)) m = r;
+        if (m == i) break;
+        for (int k = 0; k < 3; k++) { int64_t t = h[3 * m + k]; h[3 * m + k] = h[3 * i + k]; h[3 * i + k] = t; }
+        i = m;
+    }
+}
+
+/* _evict_one (cache.py:117-128): stale heap items are skipped lazily */
+static void orc_evict_one(OrcStack *s) {
+    int64_t t[3];
+    while (s->heap_n > 0) {
+        orc_heap_pop(s, t);
+        int64_t slot = t[2];
+        if (s->resident[slot] && s->freq[slot] == t[0] && s->last[slot] == t[1]) {
+            s->resident[slot] = 0;
+            s->n_resident--;
+            s->cur.evictions++;
+            return;
+        }
+    }
+}
+
+/* set_capacity (cache.py:130-137): 0 removes the bound; shrinking evicts at once */
+int orc_stack_set_capacity(OrcStack *s, int64_t capacity_bytes) {
+    if (capacity_bytes < 0) return ORC_ERR_VALUE;
+    s->capacity_bytes = capacity_bytes;
+    if (capacity_bytes > 0)
+        while (s->n_resident > 0 && s->n_resident * ORC_ENTRY_BYTES > capacity_bytes) orc_evict_one(s);
+    return ORC_OK;
 }
 
 /* reset_utterance: cache.py:185-191 (roll stats; clear unless retain) */
@@ -475,6 +549,8 @@ void orc_stack_reset(OrcStack *s, int32_t retain) {
     if (!retain) {
         orc_map_clear(&s->cache);
         s->cache_n = 0;
+        s->n_resident = 0;
+        s->heap_n = 0;
         orc_table_clear(&s->table);
     }
 }
@@ -484,7 +560,7 @@ void orc_stack_reset(OrcStack *s, int32_t retain) {
  *             ledger_bytes_indexed, ledger_bytes_full] */
 void orc_stack_stats(const OrcStack *s, int64_t *out) {
     out[0] = s->cur.lookups; out[1] = s->cur.hits; out[2] = s->cur.misses;
-    out[3] = s->cur.evictions; out[4] = (int64_t)s->cache_n; out[5] = (int64_t)s->table.n;
+    out[3] = s->cur.evictions; out[4] = s->n_resident; out[5] = (int64_t)s->table.n;
     out[6] = s->cum.lookups + s->cur.lookups; out[7] = s->cum.hits + s->cur.hits;
     out[8] = s->cum.misses + s->cur.misses;
     out[9] = s->ledger_requests; out[10] = s->ledger_bytes_indexed; out[11] = s->ledger_bytes_full;
@@ -521,8 +597,8 @@ static int orc_compute(OrcStack *s, const float *h, const int64_t *hist, int32_t
     return orc_table_encode(&s->table, s->scratch_h, s->scratch_hist, nl - start, c_next);
 }
 
-/* rnnlm_prob: cache.py:165-182 with RescoreCache.get/put (cache.py:82-109),
- * unbounded capacity (capacity_bytes == 0). */
+/* rnnlm_prob: cache.py:165-182 with RescoreCache.get/put (cache.py:82-109);
+ * capacity_bytes > 0 adds the LFU + LRU eviction of cache.py:98-128. */
 int orc_rnnlm_prob(OrcStack *s, int32_t w, uint64_t c, double *p, uint64_t *c_next,
                    int32_t *hit) {
     const OrcModel *m = s->model;
@@ -532,8 +608,12 @@ int orc_rnnlm_prob(OrcStack *s, int32_t w, uint64_t c, double *p, uint64_t *c_ne
     *hit = 0;
     if (s->enabled) {
         int64_t *slot = orc_map_find(&s->cache, key);
-        if (slot) {
+        if (slot && s->resident[*slot]) {
             s->cur.hits++;
+            s->seq++;                         /* freq / recency bookkeeping (cache.py:91-95) */
+            s->freq[*slot]++;
+            s->last[*slot] = s->seq;
+            orc_heap_push(s, s->freq[*slot], s->seq, *slot);
             *p = s->cache_p[*slot]; *c_next = s->cache_c[*slot]; *hit = 1;
             return ORC_OK;
         }
@@ -544,15 +624,35 @@ int orc_rnnlm_prob(OrcStack *s, int32_t w, uint64_t c, double *p, uint64_t *c_ne
     if (rc) return rc;
     rc = orc_compute(s, h, hist, L, w, p, c_next);
     if (rc) return rc;
-    if (s->enabled) {
-        if (s->cache_n == s->cache_cap) {
-            s->cache_cap *= 2;
-            s->cache_p = (double *)realloc(s->cache_p, sizeof(double) * s->cache_cap);
-            s->cache_c = (uint32_t *)realloc(s->cache_c, sizeof(uint32_t) * s->cache_cap);
+    if (s->enabled) {                        /* put (cache.py:99-109) */
+        if (s->capacity_bytes > 0) {
+            while (s->n_resident > 0 && (s->n_resident + 1) * ORC_ENTRY_BYTES > s->capacity_bytes)
+                orc_evict_one(s);
+            if ((s->n_resident + 1) * ORC_ENTRY_BYTES > s->capacity_bytes) return ORC_OK;
         }
-        s->cache_p[s->cache_n] = *p; s->cache_c[s->cache_n] = (uint32_t)*c_next;
-        if (orc_map_put(&s->cache, key, (int64_t)s->cache_n)) return ORC_ERR_NOMEM;
-        s->cache_n++;
+        int64_t *old = orc_map_find(&s->cache, key);
+        int64_t slot;
+        if (old) {                           /* re-insert of an evicted key: reuse its slot */
+            slot = *old;
+        } else {
+            if (s->cache_n == s->cache_cap) {
+                s->cache_cap *= 2;
+                s->cache_p = (double *)realloc(s->cache_p, sizeof(double) * s->cache_cap);
+                s->cache_c = (uint32_t *)realloc(s->cache_c, sizeof(uint32_t) * s->cache_cap);
+                s->resident = (uint8_t *)realloc(s->resident, s->cache_cap);
+                s->freq = (int64_t *)realloc(s->freq, sizeof(int64_t) * s->cache_cap);
+                s->last = (int64_t *)realloc(s->last, sizeof(int64_t) * s->cache_cap);
+            }
+            slot = (int64_t)s->cache_n++;
+            if (orc_map_put(&s->cache, key, slot)) return ORC_ERR_NOMEM;
+        }
+        s->cache_p[slot] = *p; s->cache_c[slot] = (uint32_t)*c_next;
+        s->resident[slot] = 1;
+        s->n_resident++;
+        s->seq++;
+        s->freq[slot] = 1;
+        s->last[slot] = s->seq;
+        orc_heap_push(s, 1, s->seq, slot);
     }
     return ORC_OK;
 }

@@ -27,6 +27,11 @@ twopass.npz    nbest (decoder.py:180-230) and rescore_twopass (decoder.py:243-27
                against decode_small.npz) and on the config (a) lattice:
                n-best arcs and scores, two-pass winners, per-hypothesis LM
                scores (rnnlm and hybrid modes).
+lfu.npz        capacity-bounded RescoreCache (cache.py:61-134, LFU with LRU
+               tie-break): the acceptance crit-8 recipe (tests/test_acceptance.py:
+               227-282; command corpus, retained cache, beam 6) at several
+               capacities, per-utterance lookups/hits/misses/evictions/entries,
+               plus a bounded 2000-step rnnlm_prob trace replay.
 decode_a.npz   config (a) geometry (V=1000, H=64, MaxEnt 2^20; one 300-step
                breadth-3 lattice, beam 8): model regenerated from seeds at
                test time (sha256-checked), lattice arcs and the bigram
@@ -56,7 +61,8 @@ from otflm.huffman import build_huffman, build_huffman_from_counts  # noqa: E402
 from otflm.lattice import generate_lattice  # noqa: E402
 from otflm.ngram import ngram_logprob, train_ngram  # noqa: E402
 from otflm.rnnlm import RnnlmContext, RnnlmModel  # noqa: E402
-from otflm.synth import zipfian_corpus  # noqa: E402
+from otflm.synth import command_corpus, zipfian_corpus  # noqa: E402
+from otflm.cache import reset_utterance  # noqa: E402
 from otflm.vocab import Vocabulary, build_vocabulary  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
@@ -360,14 +366,87 @@ def make_twopass():
     np.savez_compressed(OUT / "twopass.npz", **d)
 
 
+def make_lfu():
+    lines = zipfian_corpus(400, 60, seed=91)
+    vocab = build_vocabulary(lines)
+    tree = build_huffman(vocab)
+    bigram = train_ngram(lines, vocab, 2, smoothing="kneser-ney")
+    model = RnnlmModel.new(vocab.size, hidden_size=16, maxent_order=3, maxent_table_bits=12, seed=17)
+    rnnlm_mod.train(model, lines[:150], vocab, tree, epochs=1, learn_rate=0.1)
+    small = np.load(OUT / "decode_small.npz")
+    assert np.array_equal(small["U"], model.input_weights), "small setup drifted"
+    templates, utts = command_corpus(n_templates=15, n_utterances=80, seed=31, vocab_size=50)
+    d = {}
+    lat_of = {}
+    order = []
+    for tid, line in utts:
+        if tid not in lat_of:
+            lat = generate_lattice(vocab.tokenize(line), vocab, bigram, 2,
+                                   noise_seed=zlib.crc32(line.encode()))
+            lat_of[tid] = len(lat_of)
+            d.update(lattice_arrays(lat, f"t{lat_of[tid]}_"))
+            lat_of[("lat", tid)] = lat
+        order.append(lat_of[tid])
+    d["utt_template"] = np.array(order, np.int32)
+    d["n_templates"] = np.int32(len([k for k in lat_of if not isinstance(k, tuple)]))
+    caps = [0, 32 * 16, 32 * 64, 32 * 256, 250 * 1024]
+    d["capacities"] = np.array(caps, np.int64)
+    for ci, cap in enumerate(caps):
+        for retain in (True, False):
+            st = RescoreStack(model=model, tree=tree, table=IndexTable(16, 3),
+                              cache=RescoreCache(capacity_bytes=cap), ledger=TransferLedger())
+            rec = []
+            for i, (tid, _) in enumerate(utts):
+                hyp, rep = rescore_onthefly(lat_of[("lat", tid)], bigram, st, beam=6)
+                s_ = st.cache.stats()
+                rec.append((s_.lookups, s_.hits, s_.misses, s_.evictions, len(st.cache),
+                            len(st.table), hyp.combined_score, hyp.end_context))
+                reset_utterance(st.cache, st.table, retain=retain)
+            cum = st.cache.cumulative_stats()
+            d[f"c{ci}_r{int(retain)}"] = np.array(rec, np.float64)
+            d[f"c{ci}_r{int(retain)}_cum"] = np.array([cum.lookups, cum.hits, cum.misses, cum.evictions],
+                                                     np.int64)
+    # bounded trace replay (tests/test_cache.py:60-97 recipe with capacity)
+    rng = np.random.RandomState(13)
+    trace = []
+    for i in range(2000):
+        w = int(rng.randint(0, model.vocab_size))
+        parent = int(rng.randint(-1, i)) if i > 0 else -1
+        if rng.rand() < 0.3:
+            parent = -1
+        trace.append((w, parent))
+    for cap in (32 * 40, 32 * 300):
+        table = IndexTable(16, 3)
+        cache = RescoreCache(capacity_bytes=cap)
+        succ, hits = [], []
+        for w, parent in trace:
+            c = 0 if parent < 0 else succ[parent]
+            h0 = cache.stats().hits
+            v = rnnlm_prob(cache, table, model, tree, w, c)
+            succ.append(v.c_next)
+            hits.append(cache.stats().hits - h0)
+        s_ = cache.stats()
+        d[f"trace_cap{cap}"] = np.array([s_.lookups, s_.hits, s_.misses, s_.evictions, len(cache),
+                                         len(table)], np.int64)
+        d[f"trace_cap{cap}_hits"] = np.array(hits, np.int8)
+        d[f"trace_cap{cap}_succ"] = np.array(succ, np.int64)
+    d["trace"] = np.array(trace, np.int64)
+    d["produced_by"] = np.array("otflm.cache.RescoreCache(capacity_bytes>0) via rescore_onthefly / rnnlm_prob")
+    np.savez_compressed(OUT / "lfu.npz", **d)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["twopass"]:
         make_twopass()
+        sys.exit(0)
+    if sys.argv[1:] == ["lfu"]:
+        make_lfu()
         sys.exit(0)
     make_kernels()
     make_huffman()
     make_decode_small()
     make_decode_a()
     make_twopass()
+    make_lfu()
     for p in sorted(OUT.glob("*.npz")):
         print(p.name, p.stat().st_size)

@@ -121,3 +121,49 @@ def test_oracle_path_score_equals_decode_score(small):
     st = O.OracleStack(gm.model, gm.tree)
     r = st.rescore_onthefly(lats[6], gm.lm, beam=1 << 30)
     assert O.path_score(gm.model, gm.tree, gm.lm, lats[6], r.arcs) == r.combined_score
+
+
+def _lfu_lattices(golden):
+    d = golden("lfu")
+    lats = {int(i): golden_lattice(d, f"t{int(i)}_") for i in set(d["utt_template"].tolist())}
+    return d, lats
+
+
+def test_oracle_lfu_cache_matches_reference(golden, small):
+    """Capacity-bounded RescoreCache (cache.py:61-134): the crit-8 recipe
+    (tests/test_acceptance.py:227-282) -- 80 command utterances, beam 6,
+    retained and reset caches -- per-utterance lookups / hits / misses /
+    evictions / resident entries / table length and the decode itself."""
+    _, gm, _ = small
+    d, lats = _lfu_lattices(golden)
+    og = O.OracleNgram(gm.lm)
+    om = O.OracleModel(gm.model, gm.tree)
+    for ci, cap in enumerate(d["capacities"]):
+        for retain in (True, False):
+            st = O.OracleStack(om, None, capacity_bytes=int(cap))
+            want = d[f"c{ci}_r{int(retain)}"]
+            for i, t in enumerate(d["utt_template"]):
+                r = st.rescore_onthefly(lats[int(t)], og, beam=6)
+                s = st.stats()
+                got = (s.lookups, s.hits, s.misses, s.evictions, s.entries, s.table_len)
+                assert got == tuple(int(x) for x in want[i, :6]), (cap, retain, i, got, want[i])
+                assert r.combined_score == want[i, 6] and r.end_context == int(want[i, 7])
+                st.reset(retain)
+
+
+def test_oracle_lfu_trace_matches_reference(golden, small):
+    _, gm, _ = small
+    d, _ = _lfu_lattices(golden)
+    for cap in (32 * 40, 32 * 300):
+        st = O.OracleStack(gm.model, gm.tree, capacity_bytes=cap)
+        succ, hits = [], []
+        for w, parent in d["trace"]:
+            c = 0 if parent < 0 else succ[parent]
+            _, cn, hit = st.rnnlm_prob(int(w), int(c))
+            succ.append(cn)
+            hits.append(int(hit))
+        s = st.stats()
+        assert [s.lookups, s.hits, s.misses, s.evictions, s.entries, s.table_len] == \
+            list(d[f"trace_cap{cap}"])
+        assert hits == list(d[f"trace_cap{cap}_hits"])
+        assert succ == list(d[f"trace_cap{cap}_succ"])
