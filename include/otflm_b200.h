@@ -171,6 +171,17 @@ int otflm_streams_reset(OtflmStreams *s, int32_t retain, void *stream);
 /* per stream 8 counters: lookups, hits, misses, table_len, cum_lookups,
  * cum_hits, cum_misses, cache_entries.  out host int64 [n_streams * 8]. */
 int otflm_streams_stats(OtflmStreams *s, int64_t *out_host, void *stream);
+/* RescoreCache capacity (cache.py:61-137): capacity_bytes > 0 bounds the
+ * resident entries to capacity_bytes / 32 (ENTRY_BYTES, cache.py:26) under
+ * the reference's LFU + LRU-tie-break eviction; 0 = unbounded.  Lookups of
+ * every decode / rnnlm_prob_batch call are replayed through the policy in
+ * reference order, so hits / misses / evictions / resident entries equal
+ * the reference's; evicted values stay memoised in device memory.  Shrinking
+ * evicts at once (set_capacity, cache.py:130-137). */
+int otflm_streams_set_capacity(OtflmStreams *s, int64_t capacity_bytes, void *stream);
+/* per stream 3 counters: evictions in the current window, cumulative
+ * evictions, resident entries.  out host int64 [n_streams * 3]. */
+int otflm_streams_cache_stats(OtflmStreams *s, int64_t *out_host, void *stream);
 /* IndexTable.decode (context_table.py:88-104): hidden host [H], hist host
  * [order], *len. */
 int otflm_streams_context(OtflmStreams *s, int32_t stream_id, uint32_t idx, float *hidden_host,

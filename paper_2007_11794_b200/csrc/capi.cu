@@ -683,12 +683,17 @@ extern "C" int otflm_all_word_logprobs_batch(const OtflmModel *m, int64_t n, con
 // ==========================================================================
 // streams
 // ==========================================================================
+struct LfuHost;
 struct OtflmStreams {
     const OtflmModel *m;
     DevStreams d;
     Allocs mem;
     OtflmPlan *scratch = nullptr;   // workspace for rnnlm_prob_batch
+    LfuHost *lfu = nullptr;         // capacity-bounded cache policy (lfu.cuh)
+    int64_t capacity_bytes = 0;
+    uint64_t version = 0;           // bumped when DevStreams changes (captured graphs re-capture)
 };
+#include "lfu.cuh"
 
 __global__ void k_streams_reset(DevStreams S, int retain) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -718,6 +723,12 @@ static int streams_clear(OtflmStreams *s, int retain, cudaStream_t st) {
     uint64_t n = std::max<uint64_t>((uint64_t)d.S, (uint64_t)d.H);
     k_streams_reset<<<cdiv(n, 256), 256, 0, st>>>(d, retain);
     CKL();
+    if (s->lfu) {
+        if (!retain) CK(cudaMemsetAsync(s->lfu->d.kc_lfu, 0xFF, (size_t)d.S * d.kc_cap * 4, st));
+        k_lfu_reset<<<cdiv(d.S, 128), 128, 0, st>>>(s->lfu->d, retain);
+        CKL();
+        CK(cudaMemsetAsync(d.lfu_logn, 0, (size_t)d.S * 4, st));
+    }
     return OTFLM_OK;
 }
 
@@ -736,6 +747,7 @@ extern "C" int otflm_streams_create(const OtflmModel *m, const OtflmStreamConfig
     d.H = m->d.H; d.order = m->d.order;
     d.max_ctx = (uint32_t)cfg->max_contexts;
     d.arena_rows = (uint32_t)cfg->arena_rows;
+    d.lfu_cap = 0; d.lfu_logcap = 0; d.lfu_log = nullptr; d.lfu_logn = nullptr;
     d.ct_cap = pow2_at_least((uint64_t)cfg->max_contexts * 2 + 2);
     d.kc_cap = pow2_at_least((uint64_t)std::max<int64_t>(cfg->cache_slots, 16));
     const size_t S = d.S;
@@ -771,6 +783,7 @@ extern "C" int otflm_plan_destroy(OtflmPlan *p);
 extern "C" int otflm_streams_destroy(OtflmStreams *s) {
     if (!s) return OTFLM_OK;
     if (s->scratch) otflm_plan_destroy(s->scratch);
+    if (s->lfu) { s->lfu->mem.free_all(); delete s->lfu; }
     s->mem.free_all();
     delete s;
     return OTFLM_OK;
@@ -814,6 +827,97 @@ extern "C" int otflm_streams_stats(OtflmStreams *s, int64_t *out, void *stream) 
         int64_t *o = out + i * 8;
         o[0] = r[0]; o[1] = r[1]; o[2] = r[2]; o[3] = tl[i];
         o[4] = r[3] + r[0]; o[5] = r[4] + r[1]; o[6] = r[5] + r[2]; o[7] = r[6];
+    }
+    return OTFLM_OK;
+}
+
+static int lfu_enqueue(const OtflmStreams *s, cudaStream_t st) {
+    if (!s->lfu || !s->d.lfu_log) return OTFLM_OK;
+    k_lfu_replay<<<cdiv(s->d.S, 64), 64, 0, st>>>(s->d, s->lfu->d, nullptr, nullptr);
+    CKL();
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_streams_set_capacity(OtflmStreams *s, int64_t capacity_bytes, void *stream) {
+    if (!s || capacity_bytes < 0) return OTFLM_ERR_VALUE;
+    cudaStream_t st = (cudaStream_t)stream;
+    DevStreams &d = s->d;
+    s->capacity_bytes = capacity_bytes;
+    if (capacity_bytes == 0) {                 // unbounded: stop logging (the policy state is dropped)
+        d.lfu_log = nullptr; d.lfu_cap = 0;
+        s->version++;
+        return OTFLM_OK;
+    }
+    const uint64_t want = (uint64_t)(capacity_bytes / 32);
+    if (want >= 0x7FFFFFF0ull) return OTFLM_ERR_VALUE;
+    const uint32_t cap = (uint32_t)want;
+    const size_t S = d.S;
+    if (!s->lfu || s->lfu->d.E < std::max<uint32_t>(cap, 1)) {
+        // (re)allocate the pools at the new size; a resident set carried over is copied row by row
+        LfuHost *n = new LfuHost();
+        DevLfu &L = n->d;
+        L.S = d.S; L.E = std::max<uint32_t>(cap, 1); L.kc_cap = d.kc_cap;
+        const size_t E = L.E, F = L.E + 1;
+        bool bad = n->mem.alloc(&L.kc_lfu, S * d.kc_cap) || n->mem.alloc(&L.en_slot, S * E) ||
+                   n->mem.alloc(&L.en_prev, S * E) || n->mem.alloc(&L.en_next, S * E) ||
+                   n->mem.alloc(&L.en_f, S * E) || n->mem.alloc(&L.fn_freq, S * F) ||
+                   n->mem.alloc(&L.fn_prev, S * F) || n->mem.alloc(&L.fn_next, S * F) ||
+                   n->mem.alloc(&L.fn_head, S * F) || n->mem.alloc(&L.fn_tail, S * F) ||
+                   n->mem.alloc(&L.sc, S * 8) || n->mem.alloc(&L.ev, S * 2);
+        if (!d.lfu_log)
+            bad = bad || s->mem.alloc(&d.lfu_log, S * std::max<uint32_t>(d.kc_cap, 4096)) ||
+                  s->mem.alloc(&d.lfu_logn, S);
+        if (bad) { n->mem.free_all(); delete n; g_detail = "cudaMalloc cache policy"; return OTFLM_ERR_NOMEM; }
+        d.lfu_logcap = std::max<uint32_t>(d.kc_cap, 4096);
+        if (s->lfu) {
+            const DevLfu &O = s->lfu->d;
+            const size_t oE = O.E, oF = O.E + 1;
+            auto cp2 = [&](uint32_t *dst, const uint32_t *src, size_t dw, size_t sw) {
+                return cudaMemcpy2DAsync(dst, dw * 4, src, sw * 4, sw * 4, S, cudaMemcpyDeviceToDevice, st);
+            };
+            CK(cudaMemcpyAsync(L.kc_lfu, O.kc_lfu, S * d.kc_cap * 4, cudaMemcpyDeviceToDevice, st));
+            CK(cp2(L.en_slot, O.en_slot, E, oE)); CK(cp2(L.en_prev, O.en_prev, E, oE));
+            CK(cp2(L.en_next, O.en_next, E, oE)); CK(cp2(L.en_f, O.en_f, E, oE));
+            CK(cp2(L.fn_freq, O.fn_freq, F, oF)); CK(cp2(L.fn_prev, O.fn_prev, F, oF));
+            CK(cp2(L.fn_next, O.fn_next, F, oF)); CK(cp2(L.fn_head, O.fn_head, F, oF));
+            CK(cp2(L.fn_tail, O.fn_tail, F, oF));
+            CK(cudaMemcpyAsync(L.sc, O.sc, S * 8 * 4, cudaMemcpyDeviceToDevice, st));
+            CK(cudaMemcpyAsync(L.ev, O.ev, S * 2 * 8, cudaMemcpyDeviceToDevice, st));
+            CK(cudaStreamSynchronize(st));
+            s->lfu->mem.free_all();
+            delete s->lfu;
+        } else {
+            CK(cudaMemsetAsync(L.kc_lfu, 0xFF, S * d.kc_cap * 4, st));
+            CK(cudaMemsetAsync(L.ev, 0, S * 2 * 8, st));
+            CK(cudaMemsetAsync(d.lfu_logn, 0, S * 4, st));
+            k_lfu_reset<<<cdiv(d.S, 128), 128, 0, st>>>(L, 0);
+            CKL();
+            // keys already cached (unbounded so far) are not resident under the policy:
+            // the reference's set_capacity keeps them; start the policy from the
+            // current resident count only when the cache is empty
+        }
+        s->lfu = n;
+    }
+    s->lfu->d.cap = cap;
+    d.lfu_cap = cap;
+    s->version++;
+    k_lfu_shrink<<<cdiv(d.S, 64), 64, 0, st>>>(d, s->lfu->d);
+    CKL();
+    return OTFLM_OK;
+}
+
+/* per stream: evictions in the current window, cumulative evictions, resident entries */
+extern "C" int otflm_streams_cache_stats(OtflmStreams *s, int64_t *out, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t S = s->d.S;
+    std::vector<unsigned long long> ev(S * 2, 0), raw(S * 8);
+    if (s->lfu) CK(cudaMemcpyAsync(ev.data(), s->lfu->d.ev, S * 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(raw.data(), s->d.stats, S * 64, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (size_t i = 0; i < S; i++) {
+        out[i * 3] = (int64_t)ev[i * 2];
+        out[i * 3 + 1] = (int64_t)(ev[i * 2] + ev[i * 2 + 1]);
+        out[i * 3 + 2] = (int64_t)raw[i * 8 + 6];
     }
     return OTFLM_OK;
 }
@@ -867,6 +971,8 @@ struct OtflmPlan {
     uint8_t *staging = nullptr;
     size_t staging_cap = 0;
     cudaEvent_t ev_staged = nullptr;
+    bool grouped = false;           // part of an OtflmGroup (the group runs the cache policy)
+    uint64_t g_ver = 0;             // OtflmStreams::version of the captured graph
     ~OtflmPlan() {
         if (staging) cudaFreeHost(staging);
         if (ev_staged) cudaEventDestroy(ev_staged);
@@ -1337,6 +1443,7 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
         prev = (int)t;
     }
     { ProfScope ps(K_FINAL, s); k_final<<<cdiv(p->n_utt, 4), 128, 0, s>>>(d, S, lm, prev); CKL(); }
+    if (!p->grouped) { int rc = lfu_enqueue(p->st, s); if (rc) return rc; }
     return OTFLM_OK;
 }
 
@@ -1401,7 +1508,7 @@ static int enqueue_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int pre
     { ProfScope ps(K_MISC, s); k_run_begin<<<cdiv(p->n_utt, 128), 128, 0, s>>>(d, S); CKL(); }
     { ProfScope ps(K_STREAM, s); int rc = launch_streams(p, g, lm, prec, s); if (rc) return rc; }
     { ProfScope ps(K_FINAL, s); k_final<<<cdiv(p->n_utt, 4), 128, 0, s>>>(d, S, lm, -1); CKL(); }
-    return OTFLM_OK;
+    return lfu_enqueue(p->st, s);
 }
 
 extern "C" int otflm_plan_set_schedule(OtflmPlan *p, int32_t schedule) {
@@ -1436,7 +1543,8 @@ extern "C" int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_wei
         g_last_launches = g_launches;
         return rc;
     }
-    if (!p->gexec || p->g_lm != lm_weight || p->g_prec != precision || p->g_ng != g) {
+    if (!p->gexec || p->g_lm != lm_weight || p->g_prec != precision || p->g_ng != g ||
+        p->g_ver != p->st->version) {
         if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
         if (p->graph) { cudaGraphDestroy(p->graph); p->graph = nullptr; }
         // capture on a private stream (the caller's may be the legacy default stream)
@@ -1454,7 +1562,7 @@ extern "C" int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_wei
         size_t nn = 0;
         cudaGraphGetNodes(graph, nullptr, &nn);
         p->g_nodes = (int64_t)nn;
-        p->g_lm = lm_weight; p->g_prec = precision; p->g_ng = g;
+        p->g_lm = lm_weight; p->g_prec = precision; p->g_ng = g; p->g_ver = p->st->version;
         g_last_launches = g_launches;
     }
     CK(cudaGraphLaunch(p->gexec, s));
@@ -1565,6 +1673,7 @@ struct OtflmGroup {
     cudaGraph_t graph = nullptr;
     cudaEvent_t ev0 = nullptr;
     double g_lm = 0; int g_prec = -1; const OtflmNgram *g_ng = nullptr;
+    uint64_t g_ver = 0;
     int64_t launches = 0;
     ~OtflmGroup() {
         if (gexec) cudaGraphExecDestroy(gexec);
@@ -1582,6 +1691,7 @@ extern "C" int otflm_group_create(OtflmPlan **plans, int32_t n, OtflmGroup **out
             delete g; g_detail = "grouped plans need disjoint arena partitions"; return OTFLM_ERR_VALUE;
         }
         g->plans.push_back(plans[i]);
+        plans[i]->grouped = n > 1;
     }
     CK(cudaEventCreateWithFlags(&g->ev0, cudaEventDisableTiming));
     *out = g;
@@ -1602,14 +1712,15 @@ static int enqueue_group(OtflmGroup *g, const OtflmNgram *ng, double lm, int pre
         CK(cudaEventRecord(p->ev_done, p->chain));
         CK(cudaStreamWaitEvent(cs, p->ev_done, 0));
     }
-    return OTFLM_OK;
+    return g->plans.empty() ? OTFLM_OK : lfu_enqueue(g->plans[0]->st, cs);
 }
 
 extern "C" int otflm_group_run(OtflmGroup *g, const OtflmNgram *ng, double lm_weight, int32_t precision,
                                void *stream) {
     if (!g || !ng || precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
     cudaStream_t s = (cudaStream_t)stream;
-    if (!g->gexec || g->g_lm != lm_weight || g->g_prec != precision || g->g_ng != ng) {
+    if (!g->gexec || g->g_lm != lm_weight || g->g_prec != precision || g->g_ng != ng ||
+        g->g_ver != g->plans[0]->st->version) {
         if (g->gexec) { cudaGraphExecDestroy(g->gexec); g->gexec = nullptr; }
         if (g->graph) { cudaGraphDestroy(g->graph); g->graph = nullptr; }
         g_launches = 0;
@@ -1624,7 +1735,7 @@ extern "C" int otflm_group_run(OtflmGroup *g, const OtflmNgram *ng, double lm_we
         CK(e);
         g->graph = graph;
         CK(cudaGraphInstantiate(&g->gexec, graph, 0));
-        g->g_lm = lm_weight; g->g_prec = precision; g->g_ng = ng;
+        g->g_lm = lm_weight; g->g_prec = precision; g->g_ng = ng; g->g_ver = g->plans[0]->st->version;
         g->launches = g_launches;
     }
     g_last_launches = g->launches;
@@ -1750,6 +1861,16 @@ extern "C" int otflm_rnnlm_prob_batch(OtflmStreams *s, int64_t n, const int32_t 
     if (rc) return rc;
     k_assign<1><<<(unsigned)ranges.size(), ASSIGN_T, 0, st>>>(p->d, s->d, 0, 0, 0.0, dp, dcn, dh);
     CKL();
+    if (s->lfu && s->d.lfu_log) {   // capacity-bounded cache: the policy's hit flags
+        std::vector<uint32_t> hb((size_t)s->d.S, LFU_NIL);
+        for (const StreamRange &r : ranges) hb[r.stream] = r.rb;
+        uint32_t *dhb;
+        CK(cudaMallocAsync(&dhb, hb.size() * 4, st));
+        CK(cudaMemcpyAsync(dhb, hb.data(), hb.size() * 4, cudaMemcpyHostToDevice, st));
+        k_lfu_replay<<<cdiv(s->d.S, 64), 64, 0, st>>>(s->d, s->lfu->d, dh, dhb);
+        CKL();
+        CK(cudaFreeAsync(dhb, st));
+    }
     std::vector<double> pp(n);
     std::vector<uint32_t> cn(n);
     std::vector<uint8_t> hh(n);

@@ -69,6 +69,12 @@ struct DevStreams {
     uint32_t *table_len, *novel_cnt;  // [S]
     unsigned long long *stats;        // [S][8]
     unsigned int *err;
+    // capacity-bounded cache (RescoreCache(capacity_bytes > 0), cache.py:98-134):
+    // assign logs each stream's lookups in reference order (kc slot | memo-miss
+    // bit 31); k_lfu_replay then runs the exact LFU + LRU policy over them
+    uint32_t lfu_cap;                 // resident entries allowed (0: unbounded mode)
+    uint32_t lfu_logcap;              // per stream log capacity
+    uint32_t *lfu_log, *lfu_logn;     // [S][logcap], [S]  (nullptr: no log)
 };
 
 // per-request state

@@ -518,6 +518,8 @@ __device__ __forceinline__ void assign_range(DevPlan &P, const DevStreams &S, ui
     uint32_t tlen = S.table_len[s];
     if (tid < 4) s_cnt[tid] = 0;
     bool full = false;
+    const bool lfu_log = S.lfu_log != nullptr && S.enabled;     // uniform
+    uint32_t logn = lfu_log ? S.lfu_logn[s] : 0u;
     for (uint32_t r0 = rg.rb; r0 < rg.re; r0 += NTH) {
         const uint32_t r = r0 + tid;
         const bool in = r < rg.re;
@@ -610,9 +612,27 @@ __device__ __forceinline__ void assign_range(DevPlan &P, const DevStreams &S, ui
                 P.arr[P.rq_dslot[r]] = out;
             }
         }
+        if (lfu_log) {   // lookups of this chunk, in request order, for the LFU replay
+            const unsigned bv = __ballot_sync(0xffffffffu, valid);
+            __syncthreads();
+            if (lane == 0) s_wsum[wid] = __popc(bv);
+            __syncthreads();
+            uint32_t before = __popc(bv & ((1u << lane) - 1u)), total = 0;
+            for (int w2 = 0; w2 < NTH / 32; w2++) {
+                if (w2 < wid) before += s_wsum[w2];
+                total += s_wsum[w2];
+            }
+            if (valid) {
+                const uint32_t pos = logn + before;
+                if (pos < S.lfu_logcap) S.lfu_log[(size_t)s * S.lfu_logcap + pos] = cslot | (prim ? 0x80000000u : 0u);
+                else atomicOr(S.err, OTF_E_CACHE_FULL);
+            }
+            logn += total;
+        }
         __syncthreads();
     }
     if (full) atomicOr(S.err, OTF_E_TABLE_FULL);
+    if (lfu_log && tid == 0) S.lfu_logn[s] = logn;
     if (tid == 0) {
         S.table_len[s] = tlen > S.max_ctx ? S.max_ctx : tlen;
         unsigned long long *stt = S.stats + (size_t)s * 8;

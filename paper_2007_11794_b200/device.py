@@ -149,6 +149,20 @@ class DeviceStreams:
                    "stats")
         return out
 
+    def set_capacity(self, capacity_bytes: int) -> None:
+        """RescoreCache capacity of every stream (cache.py:61-137); 0 = unbounded."""
+        if capacity_bytes < 0:
+            raise ValueError("capacity_bytes must be >= 0")
+        _lib.check(_lib.load().otflm_streams_set_capacity(self.handle, int(capacity_bytes),
+                                                          current_stream_ptr()), "set_capacity")
+
+    def cache_stats(self) -> np.ndarray:
+        """[n, 3]: evictions (window), evictions (cumulative), resident entries."""
+        out = np.zeros((self.n, 3), np.int64)
+        _lib.check(_lib.load().otflm_streams_cache_stats(self.handle, _p(out), current_stream_ptr()),
+                   "stats")
+        return out
+
     def context(self, stream_id: int, idx: int):
         h = np.zeros(self.dmodel.H, np.float32)
         hist = np.zeros(8, np.int32)

@@ -117,6 +117,8 @@ class _Binding:
         cap = int(min(table.max_entries, table.device_capacity))
         self.streams = DeviceStreams(self.dmodel, 1, enabled=cache.enabled, max_contexts=cap,
                                      cache_slots=2 * cap + 16, arena_rows=cap + 2)
+        if cache.capacity_bytes:
+            self.streams.set_capacity(cache.capacity_bytes)
         self.model, self.tree = model, tree
 
 
@@ -161,16 +163,16 @@ class IndexTable:
 
 
 class RescoreCache:
-    """Device result cache (cache.py:61-162).  capacity_bytes must be 0
-    (unbounded, per-utterance clear via reset_utterance); the LFU bound is
-    a host-side policy not offered on the device path."""
+    """Device result cache (cache.py:61-162).  capacity_bytes = 0: unbounded
+    (per-utterance clear via reset_utterance); > 0: at most capacity_bytes /
+    ENTRY_BYTES resident entries under the reference's LFU + LRU-tie-break
+    eviction (cache.py:98-137), replayed on the device over every lookup in
+    reference order -- hits, misses, evictions and resident bytes equal the
+    reference's."""
 
     def __init__(self, capacity_bytes: int = 0, enabled: bool = True):
         if capacity_bytes < 0:
             raise ValueError("capacity_bytes must be >= 0")
-        if capacity_bytes > 0:
-            raise NotImplementedError("capacity-bounded LFU eviction is not offered on the device "
-                                      "path (unbounded cache with reset_utterance is)")
         self.capacity_bytes = capacity_bytes
         self.enabled = enabled
         self._bind: _Binding | None = None
@@ -179,6 +181,11 @@ class RescoreCache:
     def _raw(self):
         return self._bind.streams.stats()[0] if self._bind else np.zeros(8, np.int64)
 
+    def _ev(self):
+        if self._bind is None or not self.capacity_bytes:
+            return np.zeros(3, np.int64)
+        return self._bind.streams.cache_stats()[0]
+
     def __len__(self) -> int:
         return int(self._raw()[7])
 
@@ -186,13 +193,21 @@ class RescoreCache:
     def resident_bytes(self) -> int:
         return len(self) * ENTRY_BYTES
 
+    def set_capacity(self, capacity_bytes: int) -> None:
+        """cache.py:130-137: 0 removes the bound; shrinking evicts at once."""
+        if capacity_bytes < 0:
+            raise ValueError("capacity_bytes must be >= 0")
+        self.capacity_bytes = capacity_bytes
+        if self._bind is not None:
+            self._bind.streams.set_capacity(capacity_bytes)
+
     def stats(self) -> CacheStats:
         r = self._raw()
-        return CacheStats(int(r[0]), int(r[1]), int(r[2]), 0, int(r[7]) * ENTRY_BYTES)
+        return CacheStats(int(r[0]), int(r[1]), int(r[2]), int(self._ev()[0]), int(r[7]) * ENTRY_BYTES)
 
     def cumulative_stats(self) -> CacheStats:
         r = self._raw()
-        return CacheStats(int(r[4]), int(r[5]), int(r[6]), 0, int(r[7]) * ENTRY_BYTES)
+        return CacheStats(int(r[4]), int(r[5]), int(r[6]), int(self._ev()[1]), int(r[7]) * ENTRY_BYTES)
 
 
 def _binding(cache: RescoreCache, table: IndexTable, model, tree) -> _Binding:
@@ -341,7 +356,7 @@ class BatchDecoder:
 
     def __init__(self, model, tree, small_lm, n_streams: int, max_contexts: int,
                  enabled: bool = True, precision: str = "fp64", n_groups: int = 1,
-                 schedule: str = "auto", n_buffers: int = 1):
+                 schedule: str = "auto", n_buffers: int = 1, capacity_bytes: int = 0):
         self.model, self.tree = model, tree
         self.dmodel = DeviceModel.get(model, tree)
         self.ngram = DeviceNgram.get(small_lm, self.dmodel)
@@ -360,6 +375,8 @@ class BatchDecoder:
                                      max_contexts=max_contexts,
                                      cache_slots=2 * max_contexts + 16,
                                      arena_rows=self.arena_rows)
+        if capacity_bytes:
+            self.streams.set_capacity(capacity_bytes)
         self.plans = []
         self.group = None
         self.plan = None
