@@ -261,7 +261,8 @@ int otflm_plan_set_schedule(OtflmPlan *p, int32_t schedule);
  * o[2] MMA drain, o[3] update epilogue, o[4] HS setup + row staging,
  * o[5] HS pair rounds, o[6] whole HS group (small-LM scores + HS; runs
  * concurrently with o[1..3]), o[7] assign, o[8] wait of the update group for
- * the HS group, o[9] MMA-warp wait for operands, o[10] 0, o[11] CTAs. */
+ * the HS group, o[9] MMA-warp wait for operands, o[10] 0, o[11] CTAs,
+ * o[12..16] assign sections (probe, dedup scan, numbering, values, arrivals): 17 entries. */
 int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream);
 int otflm_schedule_supported(const OtflmModel *m, int32_t schedule, int32_t precision);
 int otflm_group_create(OtflmPlan **plans, int32_t n, OtflmGroup **out);

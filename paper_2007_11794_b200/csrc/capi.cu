@@ -1172,7 +1172,7 @@ static int plan_alloc_workspace(OtflmPlan *p, uint32_t R, uint32_t n_lvl_slots) 
     bad |= p->mem.alloc(&d.pr_p, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.pr_dig, R) != cudaSuccess;
     bad |= p->mem.alloc(&d.lvl, n_lvl_slots) != cudaSuccess;
-    bad |= p->mem.alloc(&p->alg_buf, 24) != cudaSuccess;   // [0..3] work counters, [8..19] phase ns
+    bad |= p->mem.alloc(&p->alg_buf, 40) != cudaSuccess;   // [0..3] work counters, [8..19] phase ns, [24..28] assign sections
     bad |= p->mem.alloc(&d.cursor, 1) != cudaSuccess;
     d.alg = nullptr;   // counters are only maintained in profiling runs
     d.phase_ns = nullptr;
@@ -1353,10 +1353,11 @@ extern "C" int otflm_plan_info(const OtflmPlan *p, int64_t *o) {
 
 extern "C" int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream) {
     if (!p || !o) return OTFLM_ERR_VALUE;
-    unsigned long long a[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long a[21] = {0};
     CK(cudaMemcpyAsync(a, p->alg_buf + 8, sizeof(a), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     for (int i = 0; i < 12; i++) o[i] = (int64_t)a[i];
+    for (int i = 0; i < 5; i++) o[12 + i] = (int64_t)a[16 + i];
     return OTFLM_OK;
 }
 
@@ -1464,6 +1465,7 @@ static bool sd_config(const DevModel &m, int prec, SdConfig *c) {
     if (hs_fixed + 8 * 4 * (size_t)m.H > budget) return false;
     c->qb_max = (int)std::min<size_t>(sd::QMAX, (budget - hs_fixed) / (4 * (size_t)m.H));
     c->smem = std::max((size_t)c->stages * stage, hs_fixed + (size_t)c->qb_max * 4 * m.H);
+    c->smem = std::max(c->smem, (size_t)28 * sd::NT);       // assign's chunk dedup hash (rank 0)
     c->tmem_cols = 128;
     while ((int)c->tmem_cols < m.wt_npad) c->tmem_cols <<= 1;
     return true;

@@ -28,6 +28,12 @@
 #include "common.cuh"
 #include "hs.cuh"
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 struct StreamRange {         // requests of one stream inside one level
     uint32_t stream, rb, re, pad;
 };
@@ -501,13 +507,19 @@ constexpr int ASSIGN_T = 128;
 struct AssignSmem {           // per-thread scratch of assign_range (NTH entries)
     unsigned long long *key;
     uint32_t *row, *cn, *wsum, *cnt;
+    unsigned long long *hkey;   // [2 NTH] chunk dedup hash: content key ...
+    uint32_t *htid, *ins;       // [2 NTH] ... -> first request (min thread); [NTH] table slot per first
 };
 // Requests [rg.rb, rg.re) of one stream in one level, NTH threads of the CTA
 // (the reference order is the thread order inside each chunk of NTH).
 template <int MODE, int NTH>
 __device__ __forceinline__ void assign_range(DevPlan &P, const DevStreams &S, uint32_t lvl, const StreamRange &rg,
                                              const LevelCtr &lc, uint32_t limit, double lm_weight, double *out_p,
-                                             uint32_t *out_cn, uint8_t *out_hit, const AssignSmem &sm) {
+                                             uint32_t *out_cn, uint8_t *out_hit, const AssignSmem &sm,
+                                             unsigned long long *tprof = nullptr) {
+    // tprof (profiling runs, thread 0): device ns per section, summed
+    unsigned long long tp0 = (tprof && threadIdx.x == 0) ? globaltimer_ns() : 0ull, tpa[6] = {0, 0, 0, 0, 0, 0};
+#define AS_MARK(i) do { if (tprof && threadIdx.x == 0) { const unsigned long long t_ = globaltimer_ns(); tpa[i] += t_ - tp0; tp0 = t_; } } while (0)
     unsigned long long *s_key = sm.key;
     uint32_t *s_row = sm.row, *s_cn = sm.cn, *s_wsum = sm.wsum, *s_cnt = sm.cnt;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -529,16 +541,31 @@ __device__ __forceinline__ void assign_range(DevPlan &P, const DevStreams &S, ui
         bool prim = st == RQ_NOCACHE;
         if (st == RQ_PENDING) prim = S.kc_claim[kb + cslot] == r;
         const uint32_t m = prim ? P.rq_m[r] : OTF_UNSET;
+        // chunk-local dedup table and slot hand-over, cleared per chunk
+        for (int i = tid; i < 2 * NTH; i += NTH) { sm.hkey[i] = 0ull; sm.htid[i] = 0xFFFFFFFFu; }
+        sm.ins[tid] = OTF_UNSET;
         unsigned long long key = 0;
-        uint32_t row = 0, cn = OTF_UNSET;
+        uint32_t row = 0, cn = OTF_UNSET, ins_slot = OTF_UNSET;
         if (prim) {
             key = otf_hash64(P.pr_dig[m]) | 1ull;
             row = lc.base + m;
-            uint32_t slot = (uint32_t)(key >> 20) & cmask;   // contexts of earlier levels / chunks
+            // contexts of earlier levels / chunks; a new key is inserted right
+            // away (the stream's table has one writer, this CTA) and numbered
+            // below -- an entry whose index is still unset was inserted by this
+            // chunk and is resolved by the chunk dedup
+            uint32_t slot = (uint32_t)(key >> 20) & cmask;
             for (uint32_t probes = 0; probes <= S.ct_cap; probes++) {
-                const unsigned long long k = S.ct_key[cb + slot];
-                if (k == 0ull) break;
-                if (k == key && rows_equal_lane(S, S.ct_row[cb + slot], row)) { cn = S.ct_idx[cb + slot]; break; }
+                unsigned long long k = S.ct_key[cb + slot];
+                if (k == 0ull) {
+                    const unsigned long long prev = atomicCAS(&S.ct_key[cb + slot], 0ull, key);
+                    if (prev == 0ull) { ins_slot = slot; break; }
+                    k = prev;
+                }
+                if (k == key) {
+                    const uint32_t ix = ld_volatile_u32(&S.ct_idx[cb + slot]);
+                    if (ix == OTF_UNSET) break;                                  // in flight (this chunk)
+                    if (rows_equal_lane(S, S.ct_row[cb + slot], row)) { cn = ix; break; }
+                }
                 slot = (slot + 1) & cmask;
             }
         }
@@ -546,19 +573,34 @@ __device__ __forceinline__ void assign_range(DevPlan &P, const DevStreams &S, ui
         s_key[tid] = novel ? key : 0ull;
         s_row[tid] = row;
         __syncthreads();
-        // equal contexts created by earlier requests of this chunk
+        AS_MARK(0);
+        // equal contexts created by earlier requests of this chunk: the first
+        // (lowest thread = request order) of each key through a shared hash
+        uint32_t hslot = 0;
+        if (novel) {
+            hslot = (uint32_t)(key >> 7) & (2 * NTH - 1);
+            for (int probes = 0; probes < 2 * NTH; probes++) {
+                const unsigned long long prev = atomicCAS(&sm.hkey[hslot], 0ull, key);
+                if (prev == 0ull || prev == key) { atomicMin(&sm.htid[hslot], (uint32_t)tid); break; }
+                hslot = (hslot + 1) & (2 * NTH - 1);
+            }
+        }
+        __syncthreads();
         int dup_of = -1;
-        if (novel)
-            for (int t = 0; t < tid; t++)
-                if (s_key[t] == key) {
-                    if (rows_equal_lane(S, s_row[t], row)) { dup_of = t; break; }
-                    atomicOr(S.err, OTF_E_HASH);
-                }
+        if (novel) {
+            const int f = (int)sm.htid[hslot];
+            if (f != tid) {
+                if (rows_equal_lane(S, s_row[f], row)) dup_of = f;
+                else atomicOr(S.err, OTF_E_HASH);
+            }
+            if (ins_slot != OTF_UNSET) sm.ins[dup_of >= 0 ? dup_of : tid] = ins_slot;   // slot to the first
+        }
         const bool first = novel && dup_of < 0;
         // block-wide exclusive scan of `first` in thread (= request) order
         const unsigned fb = __ballot_sync(0xffffffffu, first);
         if (lane == 0) s_wsum[wid] = __popc(fb);
         __syncthreads();
+        AS_MARK(1);
         uint32_t before = __popc(fb & ((1u << lane) - 1u)), total = 0;
         for (int w2 = 0; w2 < NTH / 32; w2++) {
             if (w2 < wid) before += s_wsum[w2];
@@ -566,13 +608,11 @@ __device__ __forceinline__ void assign_range(DevPlan &P, const DevStreams &S, ui
         }
         if (first) {
             const uint32_t idx = tlen + before + 1u;            // len + 1 (context_table.py:83-86)
-            if (idx > S.max_ctx) {
+            const uint32_t slot = sm.ins[tid];
+            if (idx > S.max_ctx || slot == OTF_UNSET) {
                 full = true;
             } else {
                 cn = idx;
-                uint32_t slot = (uint32_t)(key >> 20) & cmask;
-                for (uint32_t probes = 0; probes <= S.ct_cap; probes++, slot = (slot + 1) & cmask)
-                    if (atomicCAS(&S.ct_key[cb + slot], 0ull, key) == 0ull) break;
                 S.ct_idx[cb + slot] = idx;
                 S.ct_row[cb + slot] = row;
                 S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + idx] = row;
@@ -581,6 +621,7 @@ __device__ __forceinline__ void assign_range(DevPlan &P, const DevStreams &S, ui
         tlen += total;
         s_cn[tid] = cn;
         __syncthreads();
+        AS_MARK(2);
         if (dup_of >= 0) cn = s_cn[dup_of];
         double p = 0.0;
         if (prim) {
@@ -588,6 +629,7 @@ __device__ __forceinline__ void assign_range(DevPlan &P, const DevStreams &S, ui
             if (st == RQ_PENDING) { S.kc_p[kb + cslot] = p; S.kc_cnext[kb + cslot] = cn; }
         }
         __syncthreads();
+        AS_MARK(3);
         if (valid && !prim) {   // hit: earlier level, or an earlier request of this level
             p = S.kc_p[kb + cslot];
             cn = ld_volatile_u32(&S.kc_cnext[kb + cslot]);
@@ -630,9 +672,12 @@ __device__ __forceinline__ void assign_range(DevPlan &P, const DevStreams &S, ui
             logn += total;
         }
         __syncthreads();
+        AS_MARK(4);
     }
     if (full) atomicOr(S.err, OTF_E_TABLE_FULL);
     if (lfu_log && tid == 0) S.lfu_logn[s] = logn;
+    if (tprof && tid == 0) for (int i = 0; i < 5; i++) atomicAdd(&tprof[i], tpa[i]);
+#undef AS_MARK
     if (tid == 0) {
         S.table_len[s] = tlen > S.max_ctx ? S.max_ctx : tlen;
         unsigned long long *stt = S.stats + (size_t)s * 8;
@@ -646,15 +691,15 @@ template <int MODE>
 __global__ void __launch_bounds__(ASSIGN_T) k_assign(DevPlan P, DevStreams S, uint32_t lvl, uint32_t range_begin,
                                                      double lm_weight, double *out_p, uint32_t *out_cn,
                                                      uint8_t *out_hit) {
-    __shared__ unsigned long long s_key[ASSIGN_T];
-    __shared__ uint32_t s_row[ASSIGN_T], s_cn[ASSIGN_T], s_wsum[ASSIGN_T / 32];
+    __shared__ unsigned long long s_key[ASSIGN_T], s_hkey[2 * ASSIGN_T];
+    __shared__ uint32_t s_row[ASSIGN_T], s_cn[ASSIGN_T], s_wsum[ASSIGN_T / 32], s_htid[2 * ASSIGN_T], s_ins[ASSIGN_T];
     __shared__ uint32_t s_cnt[4];
     const LevelCtr lc = P.lvl[lvl];
     if (MODE == 1 && blockIdx.x == 0 && threadIdx.x == 0) *S.arena_used = lc.base + lc.n_prim;
     const uint32_t limit = P.arena_start == OTF_UNSET ? S.arena_rows : P.arena_end;
     const StreamRange rg = P.ranges[range_begin + blockIdx.x];
     assign_range<MODE, ASSIGN_T>(P, S, lvl, rg, lc, limit, lm_weight, out_p, out_cn, out_hit,
-                                 AssignSmem{s_key, s_row, s_cn, s_wsum, s_cnt});
+                                 AssignSmem{s_key, s_row, s_cn, s_wsum, s_cnt, s_hkey, s_htid, s_ins});
 }
 
 // --------------------------------------------------------------------------

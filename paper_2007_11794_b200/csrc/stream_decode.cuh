@@ -398,7 +398,10 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
         Q.pr_req += o; Q.pr_inrow += o; Q.pr_w += o; Q.pr_p += o; Q.pr_dig += o;
     }
     const uint32_t sid = u < P.n_utt ? P.utt_stream[u] : 0u;
-    const AssignSmem asmem{a_key, a_row, a_cn, a_wsum, a_cnt};
+    // assign's chunk dedup hash lives in rank 0's dynamic shared memory (the HS
+    // staging area, idle while assign runs): 2 NT keys + 2 NT threads + NT slots
+    const AssignSmem asmem{a_key, a_row, a_cn, a_wsum, a_cnt, reinterpret_cast<unsigned long long *>(smem),
+                           reinterpret_cast<uint32_t *>(smem + 16 * NT), reinterpret_cast<uint32_t *>(smem + 24 * NT)};
     uint32_t gctr = 0;          // K chunks through the ring so far (rank 1, uniform)
     uint32_t tiles_done = 0;
     // node-parallel HS scratch (rank 0): the whole dynamic shared memory
@@ -631,7 +634,8 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
         // ---------------- assign (rank 0) ----------------
         const StreamRange rg{sid, 0u, L.re - L.rb, 0u};
         const LevelCtr lc{n, base, 0u, 0u};
-        assign_range<0, NT>(Q, S, L.t, rg, lc, row_limit, lm_weight, nullptr, nullptr, nullptr, asmem);
+        assign_range<0, NT>(Q, S, L.t, rg, lc, row_limit, lm_weight, nullptr, nullptr, nullptr, asmem,
+                            P.phase_ns ? P.phase_ns + 16 : nullptr);
         __syncthreads();
         SD_MARK(7);
     }

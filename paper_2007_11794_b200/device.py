@@ -268,12 +268,15 @@ class Plan:
     def phase_ns(self) -> dict:
         """Stream schedule, after ``profile``: device ns per phase summed over
         CTAs (utterance streams)."""
-        o = np.zeros(12, np.int64)
+        o = np.zeros(17, np.int64)
         _lib.check(_lib.load().otflm_plan_phase_ns(self.handle, o.ctypes.data, current_stream_ptr()),
                    "phase_ns")
         names = ("expand", "update_kloop", "update_drain", "update_epilogue", "hs_setup", "hs_pairs",
                  "hs_group_total", "assign", "control_waits_for_update", "mma_wait_operands")
         out = {k: int(o[i]) for i, k in enumerate(names)}
+        for i, k in enumerate(("assign_probe", "assign_dedup_scan", "assign_numbering", "assign_values",
+                               "assign_arrivals")):
+            out[k] = int(o[12 + i])
         out["ctas"] = int(o[11])
         return out
 
