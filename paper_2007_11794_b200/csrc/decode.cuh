@@ -140,13 +140,16 @@ __device__ __forceinline__ uint32_t cache_probe(const DevStreams &S, uint32_t s,
     const unsigned long long key = ((((unsigned long long)c) << 32) | (uint32_t)w) + 1ull;
     const uint32_t mask = S.kc_cap - 1;
     uint32_t sl = (uint32_t)otf_hash64(key) & mask;
+    // one atomic per probe: a fresh key is inserted by the CAS itself (no
+    // value can be present yet), an existing one is checked for a value
     for (uint32_t probes = 0;; probes++) {
-        unsigned long long k = S.kc_key[kb + sl];
-        if (k == 0ull) {
-            unsigned long long prev = atomicCAS(&S.kc_key[kb + sl], 0ull, key);
-            k = prev == 0ull ? key : prev;
+        const unsigned long long prev = atomicCAS(&S.kc_key[kb + sl], 0ull, key);
+        if (prev == 0ull) {
+            atomicMin(&S.kc_claim[kb + sl], r);
+            *state = RQ_PENDING;
+            return sl;
         }
-        if (k == key) break;
+        if (prev == key) break;
         sl = (sl + 1) & mask;
         if (probes > S.kc_cap) { atomicOr(S.err, OTF_E_CACHE_FULL); *state = RQ_INVALID; return OTF_UNSET; }
     }
@@ -162,7 +165,8 @@ __device__ __forceinline__ uint32_t cache_probe(const DevStreams &S, uint32_t s,
 // warp-aggregated compaction of the requests that run the model this level
 // (all lanes of the warp call it)
 __device__ __forceinline__ void compact_primary(DevPlan &P, const DevStreams &S, uint32_t *n_prim, bool need,
-                                                uint32_t r, uint32_t c, int32_t w, uint32_t s) {
+                                                uint32_t r, uint32_t c, int32_t w, uint32_t s,
+                                                uint32_t crow = OTF_UNSET) {
     const unsigned bal = __ballot_sync(0xffffffffu, need);
     if (!bal) return;
     const int lane = threadIdx.x & 31;
@@ -175,7 +179,7 @@ __device__ __forceinline__ void compact_primary(DevPlan &P, const DevStreams &S,
         P.rq_m[r] = m;
         P.pr_req[m] = r;
         P.pr_w[m] = w;
-        P.pr_inrow[m] = (int32_t)S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + c];
+        P.pr_inrow[m] = (int32_t)(crow != OTF_UNSET ? crow : S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + c]);
         P.pr_dig[m] = 0ull;
     }
 }
@@ -327,7 +331,7 @@ __device__ __forceinline__ void expand_node(DevPlan &P, const DevStreams &S, con
     for (uint32_t j0 = 0; j0 < n_kept * outdeg; j0 += 32) {
         const uint32_t j = j0 + lane;
         const bool emit = j < n_kept * outdeg;
-        uint32_t r = 0, c = 0, s_tok = 0;
+        uint32_t r = 0, c = 0, s_tok = 0, crow = OTF_UNSET;
         int32_t w = 0;
         double sc = 0.0;
         uint8_t st = RQ_INVALID;
@@ -343,6 +347,7 @@ __device__ __forceinline__ void expand_node(DevPlan &P, const DevStreams &S, con
             const uint32_t a = (outdeg <= 32) ? s_arc[q] : P.out_list[nd.out_b + q];
             r = rq0 + j;
             w = P.arc_word[a];
+            crow = S.ctx_row[(uint64_t)nd.stream * (S.max_ctx + 1) + c];   // in flight during the probe
             st = RQ_NOCACHE;
             uint32_t cslot = OTF_UNSET;
             if (S.enabled) cslot = cache_probe(S, nd.stream, c, w, r, &st);
@@ -366,7 +371,7 @@ __device__ __forceinline__ void expand_node(DevPlan &P, const DevStreams &S, con
             P.rq_cslot[r] = cslot;
             P.rq_state[r] = st;
         }
-        compact_primary(P, S, n_prim, emit && (st == RQ_PENDING || st == RQ_NOCACHE), r, c, w, nd.stream);
+        compact_primary(P, S, n_prim, emit && (st == RQ_PENDING || st == RQ_NOCACHE), r, c, w, nd.stream, crow);
     }
     for (uint32_t r = n_kept * outdeg + lane; r < nd.keep * outdeg; r += 32)
         P.rq_state[rq0 + r] = RQ_INVALID;
