@@ -458,8 +458,15 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
         else { n = *r0_nprim; base = *r0_base; abort = *r0_abort != 0; if (prof) t0 = sd::gtimer(); }
         if (abort) break;
         if (rank == 0) {
-            small_lm_scores(Q, S, g, sid, L.re - L.rb, tid, NT);
-            if (n) hs_level_nodepar<CPL, ORD, NT, 0>(m, Q, S, base, n, hsm, qb_max, tid, wid, lane, prof ? ph : nullptr);
+            // warps 0..13: HS (named barrier 1); warps 14, 15: the small-LM
+            // scores of the level's requests (they only feed assign) alongside
+            constexpr int HS_NT = NT - 64;
+            if (tid < HS_NT) {
+                if (n) hs_level_nodepar<CPL, ORD, HS_NT, 1>(m, Q, S, base, n, hsm, qb_max, tid, wid, lane,
+                                                             prof ? ph : nullptr);
+            } else {
+                small_lm_scores(Q, S, g, sid, L.re - L.rb, tid - HS_NT, NT - HS_NT);
+            }
             SD_MARK(6);
         } else if (n) {
             // ------------- recurrent update (tcgen05) -------------
@@ -583,44 +590,40 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
                 __syncwarp();
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 {
+                    // work items = (M tile, group of 8 rows): the 4 warps of a TMEM
+                    // lane quadrant share a tile's rows 8 at a time.  The 8 U loads
+                    // of a group are in flight together and the group's digest
+                    // terms are reduced with the 9-exchange reduce8 pattern (the
+                    // sum for row g lands on the lanes whose bits 4,3,2 spell g).
                     const int quad = wid & 3;
-                    const int nch = (nr + 31) / 32;
-                    for (int it = wid >> 2; it < nmt * nch; it += NW / 4) {
-                        const int mt = it / nch, ch = it - mt * nch;
+                    const int n8 = (nr + 7) / 8;
+                    for (int it = wid >> 2; it < nmt * n8; it += NW / 4) {
+                        const int mt = it / n8, r0 = (it - mt * n8) * 8;
                         const int unit = mt * BM + quad * 32 + lane;
-                        float v[32];
-                        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(mt * BM + ch * 32), v);
-                        // lane j fetches row j's word once; rows are broadcast below.
-                        // Rows go in groups of 8: the 8 U loads of a group are in
-                        // flight together, and the group's digest terms are reduced
-                        // with the 9-exchange reduce8 pattern (the sum for row g of
-                        // the group lands on the lanes whose bits 4,3,2 spell g).
-                        const int wl = ch * 32 + lane < nr ? Q.pr_w[q0 + ch * 32 + lane] : 0;
+                        float v[8];
+                        tmem_ld8(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(mt * BM + r0), v);
+                        const int wl = lane < 8 && r0 + lane < nr ? Q.pr_w[q0 + r0 + lane] : 0;
                         const float *ucol = m.U + unit;
-                        float *ocol = S.arena_h + (size_t)(base + q0 + ch * 32) * H + unit;
+                        float *ocol = S.arena_h + (size_t)(base + q0 + r0) * H + unit;
+                        float uv[8];
 #pragma unroll
-                        for (int jg = 0; jg < 32; jg += 8) {
-                            float uv[8];
-#pragma unroll
-                            for (int g = 0; g < 8; g++) {
-                                const int wq = __shfl_sync(0xffffffffu, wl, jg + g);
-                                uv[g] = (ch * 32 + jg + g < nr && unit < H) ? __ldg(ucol + (size_t)wq * H) : 0.f;
-                            }
-                            unsigned long long dg[8];
-#pragma unroll
-                            for (int g = 0; g < 8; g++) {
-                                dg[g] = 0ull;
-                                const int j = jg + g;
-                                if (ch * 32 + j < nr && unit < H) {
-                                    const float o = __frcp_rn(1.f + expf(-(v[j] + uv[g])));   // == 1/x, IEEE
-                                    ocol[(size_t)j * H] = o;
-                                    dg[g] = otf_dig_h((uint32_t)unit, o);
-                                }
-                            }
-                            const unsigned long long tot = sd::reduce8_u64(dg, lane);
-                            const int row = ch * 32 + jg + node_of_lane(lane);
-                            if ((lane & 3) == 0 && row < nr) atomicAdd(&Q.pr_dig[q0 + row], tot);
+                        for (int g = 0; g < 8; g++) {
+                            const int wq = __shfl_sync(0xffffffffu, wl, g);
+                            uv[g] = (r0 + g < nr && unit < H) ? __ldg(ucol + (size_t)wq * H) : 0.f;
                         }
+                        unsigned long long dg[8];
+#pragma unroll
+                        for (int g = 0; g < 8; g++) {
+                            dg[g] = 0ull;
+                            if (r0 + g < nr && unit < H) {
+                                const float o = __frcp_rn(1.f + expf(-(v[g] + uv[g])));   // == 1/x, IEEE
+                                ocol[(size_t)g * H] = o;
+                                dg[g] = otf_dig_h((uint32_t)unit, o);
+                            }
+                        }
+                        const unsigned long long tot = sd::reduce8_u64(dg, lane);
+                        const int row = r0 + node_of_lane(lane);
+                        if ((lane & 3) == 0 && row < nr) atomicAdd(&Q.pr_dig[q0 + row], tot);
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
