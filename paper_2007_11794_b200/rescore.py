@@ -317,8 +317,9 @@ class TraversalReport:
 
 def _hyp(out, u, lat, arc_base: int = 0) -> PathHypothesis:
     n = int(out["path_len"][u])
-    arcs = tuple(int(a) - arc_base for a in out["path_arcs"][u, :n])   # batch -> lattice arc ids
-    words = tuple(int(lat.arc_word[a]) for a in arcs)
+    a = out["path_arcs"][u, :n].astype(np.int64) - arc_base            # batch -> lattice arc ids
+    arcs = tuple(a.tolist())
+    words = tuple(np.asarray(lat.arc_word)[a].tolist())
     return PathHypothesis(arcs, words, float(out["acoustic"][u]), float(out["lm"][u]),
                           float(out["combined"][u]), int(out["end_ctx"][u]))
 
