@@ -417,6 +417,13 @@ def run_config_e(args):
         lat_parts = pool.map(_e_lattices, parts)
     lat_all = [l for part in lat_parts for l in part]
     batches = [(ids[b0:b0 + B], lat_all[b0:b0 + B]) for b0 in range(0, len(ids), B)]
+    # a short last batch is padded with repeats of its own utterances (decoded,
+    # not counted) so every batch has the same compiled structure and the
+    # plans are refreshed in place instead of rebuilt
+    sel, lats = batches[-1]
+    if len(lats) < B and len(batches) > 1:
+        pad = [lats[i % len(lats)] for i in range(B - len(lats))]
+        batches[-1] = (sel, lats + pad)
     t_gen = time.perf_counter() - t0
     torch.cuda.set_device(local)
     if world > 1:
@@ -448,12 +455,14 @@ def run_config_e(args):
                 hyps, out = dec.fetch(slot=s_prev)
                 frames += int(sum(len(h.arcs) for h in hyps[:len(prev_sel)]))
                 if record:
-                    recs.append(parallel.pack_records(prev_sel, out, args.frames))
+                    recs.append(parallel.pack_records(prev_sel, {k: v[:len(prev_sel)] for k, v in out.items()},
+                                                      args.frames))
             s_prev, prev_sel = s_cur, sel
         hyps, out = dec.fetch(slot=s_prev)
         frames += int(sum(len(h.arcs) for h in hyps[:len(prev_sel)]))
         if record:
-            recs.append(parallel.pack_records(prev_sel, out, args.frames))
+            recs.append(parallel.pack_records(prev_sel, {k: v[:len(prev_sel)] for k, v in out.items()},
+                                              args.frames))
         b.record(stream)
         torch.cuda.synchronize()
         dev_ms = sum(x.elapsed_time(y) for x, y in evs)
