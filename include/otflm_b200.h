@@ -271,6 +271,18 @@ int otflm_group_run(OtflmGroup *g, const OtflmNgram *ng, double lm_weight, int32
                     void *stream);
 int otflm_group_profile(OtflmGroup *g, const OtflmNgram *ng, double lm_weight, int32_t precision,
                         void *stream, double *ms_out, int64_t *n_out);
+/* Lattice-out: with enable != 0 the decode marks every
+ * kept arrival (a token that was expanded within the beam, or a final
+ * recombination winner); otflm_decode_lattice_fetch then returns, per
+ * utterance, the RNNLM-rescored pruned state lattice as 24-byte records
+ * {double score; uint32 state, parent, arc, pad} in state order: state =
+ * arrival slot relative to the utterance, parent = the state it was expanded
+ * from (0xFFFFFFFF for the start state), arc = batch-global arc id, score =
+ * the path score of decoder.py:144.  count_host [n_utt]; records_host may be
+ * NULL to query the counts (capacity cap records). */
+int otflm_plan_set_lattice_out(OtflmPlan *p, int32_t enable);
+int otflm_decode_lattice_fetch(OtflmPlan *p, int64_t *count_host, void *records_host, int64_t cap,
+                               void *stream);
 /* Copy results of the last run to host (synchronizes). */
 int otflm_decode_fetch(OtflmPlan *p, OtflmDecodeResult *res, void *stream);
 /* End to end: plan_create + decode_run + decode_fetch + plan_destroy. */

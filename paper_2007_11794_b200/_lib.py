@@ -127,6 +127,8 @@ _SIGS = {
     "otflm_plan_counters": (C.c_int, [_P, _P, _P]),
     "otflm_decode_profile": (C.c_int, [_P, _P, C.c_double, C.c_int32, _P, _P, _P]),
     "otflm_plan_set_arena": (C.c_int, [_P, C.c_uint32, C.c_uint32]),
+    "otflm_plan_set_lattice_out": (C.c_int, [_P, C.c_int32]),
+    "otflm_decode_lattice_fetch": (C.c_int, [_P, _P, _P, C.c_int64, _P]),
     "otflm_plan_set_schedule": (C.c_int, [_P, C.c_int32]),
     "otflm_plan_phase_ns": (C.c_int, [_P, _P, _P]),
     "otflm_schedule_supported": (C.c_int, [_P, C.c_int32, C.c_int32]),

@@ -972,6 +972,12 @@ struct OtflmPlan {
     size_t staging_cap = 0;
     cudaEvent_t ev_staged = nullptr;
     bool grouped = false;           // part of an OtflmGroup (the group runs the cache policy)
+    // lattice-out (otflm_plan_set_lattice_out): per-utterance slot ranges and buffers
+    std::vector<uint32_t> utt_slot_off;
+    uint32_t *utt_slot_off_dev = nullptr;
+    LatRecord *lat_rec = nullptr;
+    long long *lat_cnt = nullptr;
+    uint8_t *kept_buf = nullptr;
     uint64_t g_ver = 0;             // OtflmStreams::version of the captured graph
     ~OtflmPlan() {
         if (staging) cudaFreeHost(staging);
@@ -1219,6 +1225,14 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     }
     if (ranges.empty()) ranges.push_back(StreamRange{0, 0, 0, 0});
     p->utt_stream_host = utt_stream;
+    {   // per-utterance arrival-slot ranges (slots are assigned utterance by utterance)
+        p->utt_slot_off.assign(1, 0);
+        uint64_t nb = 0;
+        for (int u = 0; u < L->n_utt; u++) {
+            nb += (uint64_t)L->n_nodes[u];
+            p->utt_slot_off.push_back(u + 1 < L->n_utt ? nodes[nb].slot_base : p->n_slots);
+        }
+    }
     DevPlan &d = p->d;
     NodeInfo *dn; uint32_t *dln, *dol, *das, *dss, *dus, *dfo, *dfi; int32_t *daw; double *dac, *dsl;
     StreamRange *drg;
@@ -1420,6 +1434,7 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
     CK(cudaMemsetAsync(d.arr, 0xFF, (size_t)std::max<uint32_t>(p->n_slots, 1) * sizeof(Arrival), s));
     CK(cudaMemsetAsync(d.lvl, 0, (size_t)(p->n_levels + 1) * sizeof(LevelCtr), s));
     if (d.alg) CK(cudaMemsetAsync(d.alg, 0, 4 * sizeof(unsigned long long), s));
+    if (d.kept) CK(cudaMemsetAsync(d.kept, 0, std::max<uint32_t>(p->n_slots, 1), s));
     { ProfScope ps(K_MISC, s); k_run_begin<<<cdiv(p->n_utt, 128), 128, 0, s>>>(d, S); CKL(); }
     int prev = -1;
     for (uint32_t t = 0; t < p->n_levels; t++) {
@@ -1505,6 +1520,7 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
 static int enqueue_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, cudaStream_t s) {
     DevStreams &S = p->st->d;
     DevPlan &d = p->d;
+    if (d.kept) CK(cudaMemsetAsync(d.kept, 0, std::max<uint32_t>(p->n_slots, 1), s));
     CK(cudaMemsetAsync(d.arr, 0xFF, (size_t)std::max<uint32_t>(p->n_slots, 1) * sizeof(Arrival), s));
     if (d.alg) CK(cudaMemsetAsync(d.alg, 0, 24 * sizeof(unsigned long long), s));
     { ProfScope ps(K_MISC, s); k_run_begin<<<cdiv(p->n_utt, 128), 128, 0, s>>>(d, S); CKL(); }
@@ -1660,6 +1676,51 @@ extern "C" int otflm_decode(OtflmStreams *s, const OtflmNgram *g, const OtflmLat
 // partitions) captured as parallel dependency chains of one CUDA graph, so
 // the latency-bound level stages of different groups overlap on the GPU
 // ==========================================================================
+extern "C" int otflm_plan_set_lattice_out(OtflmPlan *p, int32_t enable) {
+    if (!p) return OTFLM_ERR_VALUE;
+    if (enable && !p->lat_rec) {
+        const size_t n = std::max<uint32_t>(p->n_slots, 1);
+        uint8_t *kept;
+        if (p->mem.alloc(&kept, n) || p->mem.alloc(&p->lat_rec, n) || p->mem.alloc(&p->lat_cnt, p->n_utt) ||
+            p->mem.alloc(&p->utt_slot_off_dev, p->utt_slot_off.size())) {
+            g_detail = "cudaMalloc lattice-out"; return OTFLM_ERR_NOMEM;
+        }
+        CK(cudaMemcpy(p->utt_slot_off_dev, p->utt_slot_off.data(), p->utt_slot_off.size() * 4, cudaMemcpyHostToDevice));
+        CK(cudaMemset(kept, 0, n));
+        p->kept_buf = kept;
+    }
+    uint8_t *want = enable ? p->kept_buf : nullptr;
+    if (p->d.kept != want) {          // captured graphs hold the old plan arguments
+        p->d.kept = want;
+        if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+        if (p->graph) { cudaGraphDestroy(p->graph); p->graph = nullptr; }
+    }
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_decode_lattice_fetch(OtflmPlan *p, int64_t *count_host, void *records_host, int64_t cap,
+                                          void *stream) {
+    if (!p || !p->d.kept) { g_detail = "lattice-out not enabled on this plan"; return OTFLM_ERR_VALUE; }
+    cudaStream_t s = (cudaStream_t)stream;
+    k_lattice_out<<<p->n_utt, 256, 0, s>>>(p->d, p->utt_slot_off_dev, p->lat_rec, p->lat_cnt);
+    CKL();
+    std::vector<long long> cnt(p->n_utt);
+    CK(cudaMemcpyAsync(cnt.data(), p->lat_cnt, p->n_utt * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    int64_t total = 0;
+    for (uint32_t u = 0; u < p->n_utt; u++) { count_host[u] = cnt[u]; total += cnt[u]; }
+    if (!records_host) return OTFLM_OK;              // size query
+    if (total > cap) { g_detail = "record buffer too small"; return OTFLM_ERR_VALUE; }
+    uint8_t *dst = (uint8_t *)records_host;
+    for (uint32_t u = 0; u < p->n_utt; u++) {        // utterance u's records sit at its slot base
+        if (!cnt[u]) continue;
+        CK(cudaMemcpyAsync(dst, p->lat_rec + p->utt_slot_off[u], cnt[u] * sizeof(LatRecord), cudaMemcpyDeviceToHost, s));
+        dst += cnt[u] * sizeof(LatRecord);
+    }
+    CK(cudaStreamSynchronize(s));
+    return OTFLM_OK;
+}
+
 extern "C" int otflm_plan_set_arena(OtflmPlan *p, uint32_t start, uint32_t end) {
     if (!p || end <= start || end > p->st->d.arena_rows || start == 0) return OTFLM_ERR_VALUE;
     p->d.arena_start = start;

@@ -86,6 +86,7 @@ struct DevPlan {
     const UttLevel *ul;
     const uint32_t *ul_off, *rq_off;
     unsigned long long *phase_ns;  // profiling only: [expand, update, hs, assign, CTAs]
+    uint8_t *kept;                // lattice-out only: [n_slots] arrival kept (expanded, or a final winner)
 };
 
 // content digest term of element i of a hidden row / word j of the history
@@ -288,6 +289,7 @@ __device__ __forceinline__ void expand_node(DevPlan &P, const DevStreams &S, con
             s_ctx[rank] = ci;
             s_score[rank] = si;
             s_slot[rank] = nd.slot_base + lane;
+            if (P.kept) P.kept[nd.slot_base + lane] = 1;
         }
     } else {
         // general path: O(cap^2 / 32) sweeps through the slot_win scratch;
@@ -321,6 +323,7 @@ __device__ __forceinline__ void expand_node(DevPlan &P, const DevStreams &S, con
             if (wi && rank < n_kept) {
                 const unsigned long long sb = (unsigned long long)__double_as_longlong(ai.score);
                 P.tok[nd.slot_base + rank] = make_uint4(ai.ctx, nd.slot_base + i, (uint32_t)sb, (uint32_t)(sb >> 32));
+                if (P.kept) P.kept[nd.slot_base + i] = 1;
             }
         }
         __threadfence_block();
@@ -732,6 +735,7 @@ __global__ void k_final(DevPlan P, DevStreams S, double lm_weight, int last_lvl)
             uint32_t i = i0 + lane;
             if (i < nd.cap && P.slot_win[nd.slot_base + i]) {
                 Arrival a = P.arr[nd.slot_base + i];
+                if (P.kept) P.kept[nd.slot_base + i] = 1;     // lattice-out: every final winner
                 if (!bh || a.score > bs || (a.score == bs && a.ctx < bc)) {
                     bh = true; bs = a.score; bc = a.ctx; bslot = nd.slot_base + i;
                 }
@@ -776,4 +780,52 @@ __global__ void k_run_begin(DevPlan P, DevStreams S) {
     }
     if (t < P.n_utt) S.stats[(size_t)P.utt_stream[t] * 8 + 7] = 0;
     if (t == 0 && P.arena_start != OTF_UNSET) *P.cursor = P.arena_start;
+}
+
+
+// --------------------------------------------------------------------------
+// lattice-out: the RNNLM-rescored, beam-pruned state lattice of each
+// utterance -- every kept arrival (a token that was expanded, or a final
+// recombination winner) with its parent arrival, lattice arc and path score.
+// One CTA per utterance compacts its slot range in slot order.
+// --------------------------------------------------------------------------
+struct LatRecord {           // 24 B
+    double score;            // path score of the state (decoder.py:144 sums)
+    uint32_t state, parent;  // slot - utterance slot base; parent state or OTF_UNSET (start)
+    uint32_t arc;            // batch-global arc id (OTF_UNSET for the start state)
+    uint32_t pad;
+};
+
+__global__ void k_lattice_out(DevPlan P, const uint32_t *utt_slot_off, LatRecord *out, long long *count) {
+    const uint32_t u = blockIdx.x;
+    if (u >= P.n_utt) return;
+    const uint32_t lo = utt_slot_off[u], hi = utt_slot_off[u + 1];
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t base;
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (uint32_t s0 = lo; s0 < hi; s0 += blockDim.x) {
+        const uint32_t sl = s0 + threadIdx.x;
+        const bool k = sl < hi && P.kept[sl];
+        const unsigned b = __ballot_sync(0xffffffffu, k);
+        if (lane == 0) wsum[wid] = __popc(b);
+        __syncthreads();
+        uint32_t before = __popc(b & ((1u << lane) - 1u)), total = 0;
+        for (int w = 0; w < nw; w++) { if (w < wid) before += wsum[w]; total += wsum[w]; }
+        if (k) {
+            const Arrival a = P.arr[sl];
+            LatRecord r;
+            r.score = a.score;
+            r.state = sl - lo;
+            r.parent = a.parent == OTF_UNSET ? OTF_UNSET : a.parent - lo;
+            r.arc = a.arc;
+            r.pad = 0;
+            out[lo + base + before] = r;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) base += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) count[u] = base;
 }

@@ -309,6 +309,24 @@ class Plan:
                                                     _p(ms), _p(n)), "profile")
         return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(_lib.PROFILE_CATEGORIES)}
 
+    def set_lattice_out(self, enable: bool = True) -> None:
+        _lib.check(_lib.load().otflm_plan_set_lattice_out(self.handle, int(bool(enable))), "lattice-out")
+
+    def fetch_lattice_records(self, stream: int | None = None):
+        """Per utterance the rescored, pruned state lattice of the last run as
+        a structured array (score, state, parent, arc) -- see
+        otflm_decode_lattice_fetch."""
+        L = _lib.load()
+        st = current_stream_ptr() if stream is None else stream
+        cnt = np.zeros(self.n_utt, np.int64)
+        _lib.check(L.otflm_decode_lattice_fetch(self.handle, _p(cnt), None, 0, st), "lattice-out")
+        dt = np.dtype([("score", "<f8"), ("state", "<u4"), ("parent", "<u4"), ("arc", "<u4"), ("pad", "<u4")])
+        rec = np.zeros(max(int(cnt.sum()), 1), dt)
+        _lib.check(L.otflm_decode_lattice_fetch(self.handle, _p(cnt), rec.ctypes.data_as(C.c_void_p),
+                                                len(rec), st), "lattice-out")
+        off = np.concatenate([[0], np.cumsum(cnt)])
+        return [rec[off[u]:off[u + 1]] for u in range(self.n_utt)]
+
     def fetch(self, stream: int | None = None):
         U, MP = self.n_utt, self.max_path
         out = dict(path_len=np.zeros(U, np.int32), path_arcs=np.zeros((U, MP), np.int32),

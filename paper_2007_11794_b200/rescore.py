@@ -357,7 +357,8 @@ class BatchDecoder:
 
     def __init__(self, model, tree, small_lm, n_streams: int, max_contexts: int,
                  enabled: bool = True, precision: str = "fp64", n_groups: int = 1,
-                 schedule: str = "auto", n_buffers: int = 1, capacity_bytes: int = 0):
+                 schedule: str = "auto", n_buffers: int = 1, capacity_bytes: int = 0,
+                 lattice_out: bool = False):
         self.model, self.tree = model, tree
         self.dmodel = DeviceModel.get(model, tree)
         self.ngram = DeviceNgram.get(small_lm, self.dmodel)
@@ -378,6 +379,7 @@ class BatchDecoder:
                                      arena_rows=self.arena_rows)
         if capacity_bytes:
             self.streams.set_capacity(capacity_bytes)
+        self.lattice_out = bool(lattice_out)
         self.plans = []
         self.group = None
         self.plan = None
@@ -441,6 +443,8 @@ class BatchDecoder:
             ids = np.arange(bounds[g], bounds[g + 1])
             p = Plan(self.streams, [lattices[i] for i in ids], beam, stream_ids=ids)
             p.set_schedule(self.schedule)
+            if self.lattice_out:
+                p.set_lattice_out(True)
             if G > 1:
                 p.set_arena(1 + g * rows, 1 + (g + 1) * rows)
             self.plans.append(p)
@@ -452,6 +456,7 @@ class BatchDecoder:
     def run(self, lm_weight: float = 1.0, use_graph: bool = True, slot: int | None = None) -> None:
         if slot is not None:
             self._activate(slot)
+        self._lm_weight = lm_weight
         self.streams.reset(retain=False)
         if self.group is not None:
             self.group.run(self.ngram, lm_weight, self.precision)
@@ -504,6 +509,50 @@ class BatchDecoder:
             else:
                 merged[k] = np.concatenate([o[k] for o in outs])
         return hyps, merged
+
+
+    def fetch_lattices(self, slot: int | None = None) -> list:
+        """Lattice-out (BatchDecoder(lattice_out=True)): per utterance the
+        RNNLM-rescored, beam-pruned state lattice of the last run as a
+        ``Lattice``.  States are the kept tokens (node, context); an arc
+        carries the original arc's word and acoustic score and, as its
+        small-LM field, the rescored LM term (smalllm + delta), so that
+        acoustic + lm_weight * smalllm is the arc's on-the-fly weight and the
+        best path under first-pass weights is the on-the-fly 1-best."""
+        from .lattice import Lattice
+        if not self.lattice_out:
+            raise ValueError("BatchDecoder(lattice_out=True) is required")
+        if slot is not None:
+            self._activate(slot)
+        lm_w = getattr(self, "_lm_weight", 1.0)
+        out = []
+        for p in self.plans:
+            recs = p.fetch_lattice_records()
+            A = p.arrays
+            for u, r in enumerate(recs):
+                a0 = int(A["arc_off"][u])
+                lat = p.lats[u]
+                st = r["state"].astype(np.int64)
+                score = dict(zip(st.tolist(), r["score"].tolist()))
+                child = r["parent"] != 0xFFFFFFFF
+                start = int(st[~child][0])
+                arc = r["arc"][child].astype(np.int64) - a0
+                par = r["parent"][child].astype(np.int64)
+                sc = r["score"][child]
+                psc = np.array([score[int(x)] for x in par], np.float64)
+                ac = np.asarray(lat.arc_acoustic, np.float64)[arc]
+                lmv = (sc - psc - ac) / lm_w if lm_w != 0 else np.zeros(len(arc))
+                fin_nodes = set(int(x) for x in lat.finals)
+                dst_node = np.asarray(lat.arc_dst)[arc]
+                finals = sorted(int(s_) for s_, d in zip(st[child].tolist(), dst_node.tolist())
+                                if int(d) in fin_nodes)
+                if lat.start in fin_nodes:
+                    finals = sorted(set(finals) | {start})
+                lo = Lattice(start, finals, src=par, dst=st[child],
+                             word=np.asarray(lat.arc_word)[arc], acoustic=ac, smalllm=lmv)
+                lo.arc_ref = arc          # arc id in the input lattice, per output arc
+                out.append(lo)
+        return out
 
 
 def schedule_supported(dmodel, schedule: str, precision: str) -> bool:

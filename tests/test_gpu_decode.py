@@ -396,3 +396,28 @@ def test_config_c_geometry_stream_decode_vs_oracle():
         assert hyps[u].arcs == r.arcs
         assert abs(hyps[u].combined_score - r.combined_score) <= 1e-4 * 25
         assert int(out["expansions"][u]) == r.expansions
+
+
+@pytest.mark.parametrize("schedule,precision", [("level", "fp64"), ("stream", "tf32x3")])
+def test_lattice_out_contains_the_onthefly_best_path(schedule, precision):
+    """Lattice-out: the rescored pruned state lattice is a
+    DAG whose best path under first-pass weights (acoustic + lm_weight *
+    rescored LM) is the on-the-fly 1-best -- same input arcs, same score --
+    and every state's score is its parent's plus the arc weight."""
+    from paper_2007_11794_b200 import nbest, synth
+    from paper_2007_11794_b200.rescore import BatchDecoder
+    s = synth.build_setup("a", n_utt=5, T=30, seed=21)
+    lm_w = 0.8
+    need = BatchDecoder.contexts_needed(s.lattices, s.beam)
+    dec = BatchDecoder(s.model, s.tree, s.small_lm, len(s.lattices), need, precision=precision,
+                       schedule=schedule, lattice_out=True)
+    dec.prepare(s.lattices, s.beam)
+    dec.run(lm_w)
+    hyps, _ = dec.fetch()
+    lats = dec.fetch_lattices()
+    for u, (h, lo) in enumerate(zip(hyps, lats)):
+        assert lo.n_arcs > len(h.arcs)
+        assert lo.n_arcs <= s.beam * s.lattices[u].n_arcs
+        best = nbest(lo, 1, lm_weight=lm_w)[0]
+        assert abs(best.combined_score - h.combined_score) <= 1e-9 * max(1.0, abs(h.combined_score))
+        assert tuple(int(lo.arc_ref[a]) for a in best.arcs) == h.arcs
