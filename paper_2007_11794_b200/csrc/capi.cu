@@ -978,8 +978,16 @@ struct OtflmPlan {
     LatRecord *lat_rec = nullptr;
     long long *lat_cnt = nullptr;
     uint8_t *kept_buf = nullptr;
+    // refresh uploads run on their own stream, after this plan's previous run
+    // (ev_lastrun) and before its next one (ev_up), so the H2D of batch i+1
+    // overlaps the decode of batch i on the compute stream
+    cudaStream_t up = nullptr;
+    cudaEvent_t ev_up = nullptr, ev_lastrun = nullptr;
     uint64_t g_ver = 0;             // OtflmStreams::version of the captured graph
     ~OtflmPlan() {
+        if (up) cudaStreamDestroy(up);
+        if (ev_up) cudaEventDestroy(ev_up);
+        if (ev_lastrun) cudaEventDestroy(ev_lastrun);
         if (staging) cudaFreeHost(staging);
         if (ev_staged) cudaEventDestroy(ev_staged);
         if (side) cudaStreamDestroy(side);
@@ -1322,11 +1330,16 @@ extern "C" int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *L, int3
         p->staging_cap = need;
     }
     if (!p->ev_staged) CK(cudaEventCreateWithFlags(&p->ev_staged, cudaEventDisableTiming));
+    if (!p->up) {
+        CK(cudaStreamCreateWithFlags(&p->up, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&p->ev_up, cudaEventDisableTiming));
+    }
+    if (p->ev_lastrun) CK(cudaStreamWaitEvent(p->up, p->ev_lastrun, 0));   // buffers free again
     size_t pos = 0;
     auto put = [&](const void *dst, const void *src, size_t bytes) -> cudaError_t {
         if (!bytes) return cudaSuccess;
         std::memcpy(p->staging + pos, src, bytes);
-        cudaError_t e = cudaMemcpyAsync((void *)dst, p->staging + pos, bytes, cudaMemcpyHostToDevice, s);
+        cudaError_t e = cudaMemcpyAsync((void *)dst, p->staging + pos, bytes, cudaMemcpyHostToDevice, p->up);
         pos += al(bytes);
         return e;
     };
@@ -1344,7 +1357,9 @@ extern "C" int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *L, int3
     CK(put(d.ul, ul.data(), ul.size() * sizeof(UttLevel)));
     CK(put(d.ul_off, ul_off.data(), ul_off.size() * 4));
     CK(put(d.rq_off, rq_off.data(), rq_off.size() * 4));
-    CK(cudaEventRecord(p->ev_staged, s));
+    CK(cudaEventRecord(p->ev_staged, p->up));
+    CK(cudaEventRecord(p->ev_up, p->up));
+    CK(cudaStreamWaitEvent(s, p->ev_up, 0));          // the next run on s sees the new batch
     *same = 1;
     return OTFLM_OK;
 }
@@ -1548,8 +1563,20 @@ static int enqueue_any(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
 
 static int64_t g_last_launches = 0;
 
+static int decode_run_impl(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
+                           int32_t use_graph, void *stream);
 extern "C" int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
                                 int32_t use_graph, void *stream) {
+    int rc = decode_run_impl(p, g, lm_weight, precision, use_graph, stream);
+    if (rc == OTFLM_OK) {      // the plan's input arrays may be refreshed once this run is done
+        if (!p->ev_lastrun) CK(cudaEventCreateWithFlags(&p->ev_lastrun, cudaEventDisableTiming));
+        CK(cudaEventRecord(p->ev_lastrun, (cudaStream_t)stream));
+    }
+    return rc;
+}
+
+static int decode_run_impl(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
+                           int32_t use_graph, void *stream) {
     if (!p || !g) return OTFLM_ERR_VALUE;
     if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
     if (g->d.order - 1 > p->st->m->d.order) { g_detail = "small LM order exceeds the stored context history"; return OTFLM_ERR_VALUE; }
@@ -1803,6 +1830,10 @@ extern "C" int otflm_group_run(OtflmGroup *g, const OtflmNgram *ng, double lm_we
     }
     g_last_launches = g->launches;
     CK(cudaGraphLaunch(g->gexec, s));
+    for (OtflmPlan *gp : g->plans) {
+        if (!gp->ev_lastrun) CK(cudaEventCreateWithFlags(&gp->ev_lastrun, cudaEventDisableTiming));
+        CK(cudaEventRecord(gp->ev_lastrun, s));
+    }
     return OTFLM_OK;
 }
 
