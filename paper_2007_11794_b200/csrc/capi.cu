@@ -199,7 +199,7 @@ extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, Otflm
         CK(cudaGetLastError());
         const int np = (H + 127) / 128 * 128;             // whole 128-row M tiles
         if (np <= 512) {
-            const int kcb = np <= 256 ? 128 : 32, KE = kcb / 4, NK = (H + KE - 1) / KE;
+            const int kcb = np <= 256 ? 128 : 64, KE = kcb / 4, NK = (H + KE - 1) / KE;   // few, large K chunks
             float *Wt = nullptr;
             const size_t nwt = (size_t)NK * 2 * np * KE;
             if (m->mem.alloc(&Wt, nwt) != cudaSuccess) { m->mem.free_all(); delete m; g_detail = "cudaMalloc model"; return OTFLM_ERR_NOMEM; }
@@ -1521,9 +1521,9 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
     do {                                                                                                        \
         if (m.H <= 128) SD_ORD(MODE, 128, 1);                                                                   \
         else if (m.H <= 256) SD_ORD(MODE, 128, 2);                                                              \
-        else SD_ORD(MODE, 32, 4);                                                                               \
+        else SD_ORD(MODE, 64, 4);                                                                               \
     } while (0)
-    if ((m.wt_npad <= 256 ? 128 : 32) != m.wt_kcb) { g_detail = "W tile layout mismatch"; return OTFLM_ERR_VALUE; }
+    if ((m.wt_npad <= 256 ? 128 : 64) != m.wt_kcb) { g_detail = "W tile layout mismatch"; return OTFLM_ERR_VALUE; }
     if (prec == OTFLM_PREC_TF32X3) SD_H(1); else SD_H(3);
 #undef SD_H
 #undef SD_ORD
