@@ -653,7 +653,7 @@ def main():
     # double-buffered through the public API: each step compiles + uploads
     # (pinned H2D) batch i+1 on the host while the GPU decodes batch i, then
     # reads batch i's 1-best back (D2H).  The pipeline is filled untimed.
-    n_e2e = max(3, min(args.steps, 6))
+    n_e2e = max(3, args.steps)
     s_prev = dec.prepare(batches[0], setup.beam)
     dec.run(1.0, use_graph=True, slot=s_prev)
     for i in range(1, 3):                                 # both buffers built and warm
