@@ -38,9 +38,17 @@ from .rescore import (  # noqa: F401
     IndexTable,
     PathHypothesis,
     RescoreCache,
+    RescoreRequest,
+    RescoreResponse,
+    RescoreServer,
     RescoreStack,
     TransferLedger,
     TraversalReport,
+    edit_distance,
+    first_pass_weight,
+    quantize_delta,
+    rescored_path_score,
+    small_context,
     pack,
     reduction_ratio,
     rescore_batch,

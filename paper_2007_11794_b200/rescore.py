@@ -17,6 +17,7 @@ live on the device (libotflm_b200.so), never on the host.
 
 from __future__ import annotations
 
+import struct
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -292,6 +293,147 @@ class RescoreStack:
     cache: RescoreCache
     ledger: TransferLedger = field(default_factory=TransferLedger)
     rnn_bits: int = 32
+
+
+# --------------------------------------------------------------------------
+# the paper's search <-> rescorer boundary (codec.py:23-92, decoder.py:73-104):
+# 16-byte requests in, 16-byte responses out; the LM work behind serve() is the
+# device Table-1 lookup (rnnlm_prob), the small-LM term is the host n-gram
+_REQUEST = struct.Struct("<QII")     # packed (c, small idx), word, frame
+_RESPONSE = struct.Struct("<fQ4x")   # f32 delta, packed (c', small idx)
+
+
+def quantize_delta(delta: float) -> float:
+    """codec.py:57-60 -- the response carries the delta as an f32."""
+    return float(np.float32(delta))
+
+
+@dataclass(frozen=True)
+class RescoreRequest:
+    """codec.py:63-75"""
+
+    packed: int
+    w: int
+    frame: int
+
+    def to_bytes(self) -> bytes:
+        return _REQUEST.pack(self.packed, self.w, self.frame)
+
+    @classmethod
+    def from_bytes(cls, raw: bytes) -> "RescoreRequest":
+        return cls(*_REQUEST.unpack(raw))
+
+
+@dataclass(frozen=True)
+class RescoreResponse:
+    """codec.py:78-92"""
+
+    delta: float
+    c_next_packed: int
+
+    @classmethod
+    def build(cls, delta: float, c_next_packed: int) -> "RescoreResponse":
+        return cls(quantize_delta(delta), c_next_packed)
+
+    def to_bytes(self) -> bytes:
+        return _RESPONSE.pack(self.delta, self.c_next_packed)
+
+    @classmethod
+    def from_bytes(cls, raw: bytes) -> "RescoreResponse":
+        return cls(*_RESPONSE.unpack(raw))
+
+
+def small_context(history: Sequence[int], small_lm) -> list:
+    """decoder.py:73-80 -- stored history, left-padded with <s>."""
+    hist = list(history)
+    pad = small_lm.order - 1 - len(hist)
+    return [small_lm.bos_id] * pad + hist if pad > 0 else hist
+
+
+class RescoreServer:
+    """decoder.py:83-104: consumes request bytes, returns response bytes.
+
+    ``serve`` answers one request exactly as the reference does; ``serve_batch``
+    answers a concatenation of requests with one device batch (array order =
+    reference order for cache claims and index numbering), for clients that
+    pipeline a frame's requests."""
+
+    def __init__(self, stack: "RescoreStack", small_lm):
+        if small_lm.order - 1 > stack.model.maxent_order:
+            raise ValueError("small LM order exceeds the stored context history; "
+                             f"need maxent_order >= {small_lm.order - 1}")
+        self.stack = stack
+        self.small_lm = small_lm
+        self.precision = "fp64"
+
+    def serve(self, raw: bytes) -> bytes:
+        return self.serve_batch(raw)
+
+    def serve_batch(self, raw: bytes) -> bytes:
+        from .model import ngram_logprob
+        st = self.stack
+        n, rem = divmod(len(raw), REQUEST_BYTES)
+        if rem or n == 0:
+            raise ValueError(f"request buffer of {len(raw)} bytes is not a whole number of "
+                             f"{REQUEST_BYTES}-byte requests")
+        reqs = np.frombuffer(raw, dtype=np.dtype([("packed", "<u8"), ("w", "<u4"), ("frame", "<u4")]))
+        small_bits = 64 - st.rnn_bits
+        if not 1 <= st.rnn_bits <= 63:
+            raise ValueError(f"rnn_bits must be in 1..63, got {st.rnn_bits}")
+        c = (reqs["packed"] >> np.uint64(small_bits)).astype(np.int64)
+        small = reqs["packed"] & np.uint64((1 << small_bits) - 1)
+        w = reqs["w"].astype(np.int64)
+        if np.any(w >= st.model.vocab_size):
+            raise ValueError(f"word id out of range 0..{st.model.vocab_size - 1}")
+        if np.any(c >= (1 << 32)):
+            raise _lib.UnknownIndexError("context index beyond the device table")
+        b = _binding(st.cache, st.table, st.model, st.tree)
+        p, cn, _ = b.streams.rnnlm_prob_batch(np.zeros(n, np.int32), c, w, self.precision)
+        hist = {}
+        out = bytearray()
+        for i in range(n):
+            ci = int(c[i])
+            if ci not in hist:
+                hist[ci] = st.table.decode(ci).history
+            p_small = ngram_logprob(self.small_lm, small_context(hist[ci], self.small_lm), int(w[i]))
+            out += RescoreResponse.build(float(p[i]) - p_small,
+                                         pack(int(cn[i]), int(small[i]), st.rnn_bits)).to_bytes()
+        st.ledger.record(st.table.element_bytes, n)
+        return bytes(out)
+
+
+def first_pass_weight(arc, lm_weight: float) -> float:
+    """decoder.py:176-177"""
+    return arc.acoustic + lm_weight * arc.smalllm
+
+
+def rescored_path_score(lattice, arc_ids: Sequence[int], model, tree, small_lm,
+                        lm_weight: float = 1.0) -> float:
+    """decoder.py:277-292 -- one path under the on-the-fly objective, straight
+    from the model (device word_logprob / advance_context, exact f64 mode)."""
+    from . import advance_context, word_logprob
+    from .model import ngram_logprob
+    ctx = model.zero_context()
+    score = 0.0
+    for a in arc_ids:
+        arc = lattice.arcs[a]
+        p = word_logprob(model, tree, ctx, arc.word)
+        p_small = ngram_logprob(small_lm, small_context(ctx.history, small_lm), arc.word)
+        score = score + arc.acoustic + lm_weight * (arc.smalllm + quantize_delta(p - p_small))
+        ctx = advance_context(model, ctx, arc.word)
+    return score
+
+
+def edit_distance(ref: Sequence, hyp: Sequence) -> int:
+    """decoder.py:295-303 -- Levenshtein distance (word error counts)."""
+    row = np.arange(len(hyp) + 1)
+    for i, r in enumerate(ref, 1):
+        nxt = np.empty_like(row)
+        nxt[0] = i
+        for j, h in enumerate(hyp, 1):
+            nxt[j] = min(row[j] + 1, nxt[j - 1] + 1, row[j - 1] + (r != h))
+        row = nxt
+    return int(row[-1])
 
 
 @dataclass

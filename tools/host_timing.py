@@ -1,3 +1,4 @@
+import sys; sys.path.insert(0, ".")
 import time, json
 import numpy as np
 import torch
