@@ -32,6 +32,7 @@ REQUEST_BYTES = 16        # codec.py:23
 RESPONSE_BYTES = 16
 DEFAULT_RNN_BITS = 32
 DEFAULT_DEVICE_CONTEXTS = 1 << 18
+_HISTORY_SENTINEL = 0xFFFFFFFFFFFFFFFF   # context_table.py: empty history slot
 
 
 @dataclass(frozen=True)
@@ -153,6 +154,25 @@ class IndexTable:
             raise _lib.UnknownIndexError(f"index {idx} not in table (length {len(self)})")
         h, hist = self._bind.streams.context(0, idx)
         return RnnlmContext(h, hist)
+
+    def _key_bytes(self, ctx: RnnlmContext) -> bytes:
+        """context_table.py:64-74: f32 hidden + history slots (u64, sentinel-padded)."""
+        if ctx.hidden.shape != (self.hidden_size,):
+            raise ValueError(f"context hidden size {ctx.hidden.shape} does not match table "
+                             f"H={self.hidden_size}")
+        if len(ctx.history) > self.maxent_order:
+            raise ValueError("context history longer than table maxent order")
+        slots = np.full(self.maxent_order, _HISTORY_SENTINEL, dtype="<u8")
+        slots[:len(ctx.history)] = ctx.history
+        return np.ascontiguousarray(ctx.hidden, dtype="<f4").tobytes() + slots.tobytes()
+
+    def serialized(self, idx: int) -> bytes:
+        """context_table.py:107-111: the stored element bytes of index idx
+        (key bytes + u32 order + u32 index), read back from the device row."""
+        idx = int(idx)
+        if self._bind is None or not 1 <= idx <= len(self):
+            raise _lib.UnknownIndexError(f"index {idx} not in table")
+        return self._key_bytes(self.decode(idx)) + struct.pack("<II", self.maxent_order, idx)
 
     def memory_report(self) -> tuple:
         n = len(self)

@@ -8,7 +8,8 @@ Writes tests/golden/server.npz: on the decode_small model and KN bigram
 (same recipe as make_golden.make_decode_small, checked against
 decode_small.npz), a 1500-request RescoreServer.serve session
 (decoder.py:83-104): request bytes in, response bytes out (codec.py:23-28
-layouts), the ledger after the session, the cache/table counters; plus
+layouts), the ledger after the session, the cache/table counters, IndexTable.serialized
+(context_table.py:107-111) of five indices; plus
 rescored_path_score (decoder.py:277-292) of the beam-8 1-best of the first
 8 decode_small lattices.
 """
@@ -50,7 +51,9 @@ def main():
         resps.append(np.frombuffer(out, np.uint8))
         known.append(int.from_bytes(out[4:12], "little") >> 32)
     s = st.cache.stats()
-    d = dict(requests=np.stack(reqs), responses=np.stack(resps),
+    ser_idx = [1, 2, 10, 100, len(st.table)]
+    ser = np.stack([np.frombuffer(st.table.serialized(i), np.uint8) for i in ser_idx])
+    d = dict(ser_idx=np.array(ser_idx, np.int64), serialized=ser, requests=np.stack(reqs), responses=np.stack(resps),
              ledger=np.array([st.ledger.requests, st.ledger.bytes_indexed, st.ledger.bytes_full_baseline], np.int64),
              stats=np.array([s.lookups, s.hits, s.misses, len(st.table)], np.int64))
     # rescored_path_score of reference 1-best paths

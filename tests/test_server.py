@@ -124,3 +124,25 @@ def test_rescored_path_score_matches_reference(golden, small):
         off += n
         got = rescored_path_score(lats[li], arcs, gm.model, gm.tree, gm.lm, 1.0 if li % 2 else 0.7)
         assert abs(got - float(d["path_scores"][li])) <= 1e-9
+
+
+@pytest.mark.gpu
+def test_index_table_serialized_matches_reference(golden, small):
+    """IndexTable.serialized after the serve session: history slots, order and
+    index bytes identical; hidden f32 within 1 ulp (exact-mode bound)."""
+    from paper_2007_11794_b200 import RescoreServer, UnknownIndexError
+    d = golden("server")
+    _, gm, _ = small
+    st = _stack(gm)
+    srv = RescoreServer(st, gm.lm)
+    for raw in d["requests"]:
+        srv.serve(raw.tobytes())
+    H = gm.model.hidden_size
+    for idx, ref in zip(d["ser_idx"], d["serialized"]):
+        got = np.frombuffer(st.table.serialized(int(idx)), np.uint8)
+        assert got.shape == ref.shape == (st.table.element_bytes,)
+        assert np.array_equal(got[4 * H:], ref[4 * H:])
+        gh, rh = got[:4 * H].view(np.int32), ref[:4 * H].view(np.int32)
+        assert np.all(np.abs(gh.astype(np.int64) - rh) <= 1)
+    with pytest.raises(UnknownIndexError):
+        st.table.serialized(len(st.table) + 1)
