@@ -171,6 +171,25 @@ int otflm_streams_reset(OtflmStreams *s, int32_t retain, void *stream);
 /* per stream 8 counters: lookups, hits, misses, table_len, cum_lookups,
  * cum_hits, cum_misses, cache_entries.  out host int64 [n_streams * 8]. */
 int otflm_streams_stats(OtflmStreams *s, int64_t *out_host, void *stream);
+/* IndexTable.encode (context_table.py:76-89) on stream sid: n host contexts
+ * (hidden f32 [n, H], history u32 [n, order] + lengths) in call order; the
+ * index of each (existing equal content, or len + 1).  OTFLM_ERR_TABLE_FULL
+ * when the table is full (TableFullError, context_table.py:84-85). */
+int otflm_streams_encode(OtflmStreams *s, int32_t sid, int64_t n, const float *hidden_host,
+                         const uint32_t *hist_host, const int32_t *hist_len_host, uint32_t *idx_host,
+                         void *stream);
+/* RescoreCache.get / put (cache.py:80-108) on stream sid, keys (c, w) in call
+ * order.  get counts lookups / hits / misses (cache disabled: every lookup a
+ * miss) and returns found + (p, c').  put stores a value unless the key holds
+ * one (first value wins; disabled cache: no-op).  Unbounded caches only: a
+ * capacity-bounded cache returns OTFLM_ERR_VALUE (its policy replays the
+ * lookups rnnlm_prob logs). */
+int otflm_streams_cache_get(OtflmStreams *s, int32_t sid, int64_t n, const uint32_t *c_host,
+                            const int32_t *w_host, uint8_t *found_host, double *p_host, uint32_t *c_next_host,
+                            void *stream);
+int otflm_streams_cache_put(OtflmStreams *s, int32_t sid, int64_t n, const uint32_t *c_host,
+                            const int32_t *w_host, const double *p_host, const uint32_t *c_next_host,
+                            void *stream);
 /* RescoreCache capacity (cache.py:61-137): capacity_bytes > 0 bounds the
  * resident entries to capacity_bytes / 32 (ENTRY_BYTES, cache.py:26) under
  * the reference's LFU + LRU-tie-break eviction; 0 = unbounded.  Lookups of

@@ -2011,3 +2011,87 @@ extern "C" const char *otflm_last_error_detail(void) { return g_detail.c_str(); 
 // two-pass rescoring (uses the launchers above)
 // ==========================================================================
 #include "twopass.cuh"
+
+// ==========================================================================
+// container-level table operations (tables.cuh)
+// ==========================================================================
+#include "tables.cuh"
+
+template <typename T>
+static int to_dev(T **d, const T *h, int64_t n, cudaStream_t st) {
+    CK(cudaMallocAsync(d, (size_t)std::max<int64_t>(n, 1) * sizeof(T), st));
+    if (h && n) CK(cudaMemcpyAsync(*d, h, (size_t)n * sizeof(T), cudaMemcpyHostToDevice, st));
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_streams_encode(OtflmStreams *s, int32_t sid, int64_t n, const float *hidden_h,
+                                    const uint32_t *hist_h, const int32_t *hist_len_h, uint32_t *idx_h,
+                                    void *stream) {
+    if (!s || sid < 0 || sid >= s->d.S || n < 0) return OTFLM_ERR_VALUE;
+    if (n == 0) return OTFLM_OK;
+    for (int64_t i = 0; i < n; i++)
+        if (hist_len_h[i] < 0 || hist_len_h[i] > s->d.order) { g_detail = "context history longer than table maxent order"; return OTFLM_ERR_VALUE; }
+    cudaStream_t st = (cudaStream_t)stream;
+    float *dh; uint32_t *dhist, *didx; int32_t *dlen;
+    int rc = to_dev(&dh, hidden_h, n * s->d.H, st);
+    if (!rc) rc = to_dev(&dhist, hist_h, n * s->d.order, st);
+    if (!rc) rc = to_dev(&dlen, hist_len_h, n, st);
+    if (!rc) rc = to_dev(&didx, (const uint32_t *)nullptr, n, st);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(didx, 0, (size_t)n * 4, st));
+    k_table_encode<<<1, 1, 0, st>>>(s->d, (uint32_t)sid, (uint32_t)n, dh, dhist, dlen, didx);
+    CKL();
+    CK(cudaMemcpyAsync(idx_h, didx, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(dh, st)); CK(cudaFreeAsync(dhist, st)); CK(cudaFreeAsync(dlen, st)); CK(cudaFreeAsync(didx, st));
+    return check_err(s, st);
+}
+
+static int cache_direct_ok(const OtflmStreams *s, int32_t sid, int64_t n) {
+    if (!s || sid < 0 || sid >= s->d.S || n < 0) return OTFLM_ERR_VALUE;
+    if (s->lfu && s->d.lfu_log) {
+        g_detail = "direct get/put on a capacity-bounded device cache is not supported (use rnnlm_prob)";
+        return OTFLM_ERR_VALUE;
+    }
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_streams_cache_get(OtflmStreams *s, int32_t sid, int64_t n, const uint32_t *c_h,
+                                       const int32_t *w_h, uint8_t *found_h, double *p_h, uint32_t *cn_h,
+                                       void *stream) {
+    int rc = cache_direct_ok(s, sid, n);
+    if (rc || n == 0) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t *dc, *dcn; int32_t *dw; uint8_t *df; double *dp;
+    rc = to_dev(&dc, c_h, n, st);
+    if (!rc) rc = to_dev(&dw, w_h, n, st);
+    if (!rc) rc = to_dev(&df, (const uint8_t *)nullptr, n, st);
+    if (!rc) rc = to_dev(&dp, (const double *)nullptr, n, st);
+    if (!rc) rc = to_dev(&dcn, (const uint32_t *)nullptr, n, st);
+    if (rc) return rc;
+    k_cache_get<<<1, 1, 0, st>>>(s->d, (uint32_t)sid, (uint32_t)n, dc, dw, df, dp, dcn);
+    CKL();
+    CK(cudaMemcpyAsync(found_h, df, (size_t)n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(p_h, dp, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(cn_h, dcn, (size_t)n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(dc, st)); CK(cudaFreeAsync(dw, st)); CK(cudaFreeAsync(df, st));
+    CK(cudaFreeAsync(dp, st)); CK(cudaFreeAsync(dcn, st));
+    return check_err(s, st);
+}
+
+extern "C" int otflm_streams_cache_put(OtflmStreams *s, int32_t sid, int64_t n, const uint32_t *c_h,
+                                       const int32_t *w_h, const double *p_h, const uint32_t *cn_h,
+                                       void *stream) {
+    int rc = cache_direct_ok(s, sid, n);
+    if (rc || n == 0) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t *dc, *dcn; int32_t *dw; double *dp;
+    rc = to_dev(&dc, c_h, n, st);
+    if (!rc) rc = to_dev(&dw, w_h, n, st);
+    if (!rc) rc = to_dev(&dp, p_h, n, st);
+    if (!rc) rc = to_dev(&dcn, cn_h, n, st);
+    if (rc) return rc;
+    k_cache_put<<<1, 1, 0, st>>>(s->d, (uint32_t)sid, (uint32_t)n, dc, dw, dp, dcn);
+    CKL();
+    CK(cudaFreeAsync(dc, st)); CK(cudaFreeAsync(dw, st)); CK(cudaFreeAsync(dp, st)); CK(cudaFreeAsync(dcn, st));
+    return check_err(s, st);
+}

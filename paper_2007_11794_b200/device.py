@@ -172,6 +172,35 @@ class DeviceStreams:
                    "decode")
         return h, tuple(int(x) for x in hist[:n[0]])
 
+    def encode(self, stream_id: int, hidden, hist, hist_len):
+        """IndexTable.encode of n host contexts on one stream (context_table.py:76-89)."""
+        hh = np.ascontiguousarray(hidden, np.float32)
+        hs = np.ascontiguousarray(hist, np.uint32)
+        hl = np.ascontiguousarray(hist_len, np.int32)
+        idx = np.zeros(len(hl), np.uint32)
+        _lib.check(_lib.load().otflm_streams_encode(self.handle, int(stream_id), len(hl), _p(hh), _p(hs),
+                                                    _p(hl), _p(idx), current_stream_ptr()), "encode")
+        return idx
+
+    def cache_get(self, stream_id: int, c, w):
+        cc = np.ascontiguousarray(c, np.uint32)
+        ww = np.ascontiguousarray(w, np.int32)
+        n = len(ww)
+        found = np.zeros(n, np.uint8)
+        p = np.zeros(n, np.float64)
+        cn = np.zeros(n, np.uint32)
+        _lib.check(_lib.load().otflm_streams_cache_get(self.handle, int(stream_id), n, _p(cc), _p(ww), _p(found),
+                                                       _p(p), _p(cn), current_stream_ptr()), "cache get")
+        return found.astype(bool), p, cn
+
+    def cache_put(self, stream_id: int, c, w, p, cn) -> None:
+        cc = np.ascontiguousarray(c, np.uint32)
+        ww = np.ascontiguousarray(w, np.int32)
+        pp = np.ascontiguousarray(p, np.float64)
+        nn = np.ascontiguousarray(cn, np.uint32)
+        _lib.check(_lib.load().otflm_streams_cache_put(self.handle, int(stream_id), len(ww), _p(cc), _p(ww), _p(pp),
+                                                       _p(nn), current_stream_ptr()), "cache put")
+
     def rnnlm_prob_batch(self, stream_ids, c, w, precision: str = "fp64"):
         sid = np.ascontiguousarray(stream_ids, np.int32)
         cc = np.ascontiguousarray(c, np.uint32)

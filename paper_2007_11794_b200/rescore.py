@@ -155,6 +155,23 @@ class IndexTable:
         h, hist = self._bind.streams.context(0, idx)
         return RnnlmContext(h, hist)
 
+    def bind(self, model, tree, cache: "RescoreCache | None" = None) -> "IndexTable":
+        """Attach the table to a model's device stream (rnnlm_prob and
+        RescoreStack do this on first use)."""
+        _binding(cache if cache is not None else RescoreCache(), self, model, tree)
+        return self
+
+    def encode(self, ctx: RnnlmContext) -> int:
+        """context_table.py:76-89 on the device: the index of an equal stored
+        context (bit-exact hidden bytes + history), else len + 1."""
+        self._key_bytes(ctx)                                   # the reference's ValueErrors
+        if self._bind is None:
+            raise ValueError("IndexTable has no device stream yet: call bind(model, tree) "
+                             "or use it through rnnlm_prob / a RescoreStack first")
+        hist = np.zeros((1, self.maxent_order), np.uint32)
+        hist[0, :len(ctx.history)] = ctx.history
+        return int(self._bind.streams.encode(0, ctx.hidden[None, :], hist, [len(ctx.history)])[0])
+
     def _key_bytes(self, ctx: RnnlmContext) -> bytes:
         """context_table.py:64-74: f32 hidden + history slots (u64, sentinel-padded)."""
         if ctx.hidden.shape != (self.hidden_size,):
@@ -213,6 +230,24 @@ class RescoreCache:
     @property
     def resident_bytes(self) -> int:
         return len(self) * ENTRY_BYTES
+
+    def _direct(self):
+        if self._bind is None:
+            raise ValueError("RescoreCache has no device stream yet: use it through rnnlm_prob / "
+                             "a RescoreStack first (or IndexTable.bind(model, tree, cache))")
+        return self._bind.streams
+
+    def get(self, key) -> "CacheValue | None":
+        """cache.py:80-94 on the device: counts the lookup; None on a miss
+        (and always when the cache is disabled)."""
+        c, w = (int(x) for x in key)
+        found, p, cn = self._direct().cache_get(0, [c], [w])
+        return CacheValue(float(p[0]), int(cn[0])) if found[0] else None
+
+    def put(self, key, value: CacheValue) -> None:
+        """cache.py:96-108 on the device: first value wins; no-op when disabled."""
+        c, w = (int(x) for x in key)
+        self._direct().cache_put(0, [c], [w], [float(value.p)], [int(value.c_next)])
 
     def set_capacity(self, capacity_bytes: int) -> None:
         """cache.py:130-137: 0 removes the bound; shrinking evicts at once."""
