@@ -21,7 +21,10 @@ NUMBA_DISABLED = True
 
 def _t(x, dtype):
     torch = cuda()
-    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda")
+    a = np.ascontiguousarray(x)
+    if not a.flags.writeable:            # read-only views (np.frombuffer, np.load): copy, torch needs writable
+        a = a.copy()
+    return torch.as_tensor(a, dtype=dtype, device="cuda")
 
 
 class _ArraysModel:

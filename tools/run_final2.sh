@@ -1,7 +1,7 @@
 # round deliverables after the latency work: default bench line, reference arm,
 # GPU tests, ncu launch list + full capture of the stream kernel and the batched update
 mkdir -p gpurun_out /tmp/rep
-TAG=${1:-r01g}
+TAG=${1:-r01p}
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo pytest=$?
 tail -2 gpurun_out/${TAG}_pytest_gpu.log
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.jsonl 2> gpurun_out/${TAG}_bench.err; echo bench=$?
