@@ -116,6 +116,8 @@ _SIGS = {
     "otflm_streams_encode": (C.c_int, [_P, C.c_int32, C.c_int64, _P, _P, _P, _P, _P]),
     "otflm_streams_cache_get": (C.c_int, [_P, C.c_int32, C.c_int64, _P, _P, _P, _P, _P, _P]),
     "otflm_streams_cache_put": (C.c_int, [_P, C.c_int32, C.c_int64, _P, _P, _P, _P, _P]),
+    "otflm_streams_roll_stats": (C.c_int, [_P, C.c_int32, _P]),
+    "otflm_streams_cache_clear": (C.c_int, [_P, C.c_int32, _P]),
     "otflm_streams_set_capacity": (C.c_int, [_P, C.c_int64, _P]),
     "otflm_streams_cache_stats": (C.c_int, [_P, _P, _P]),
     "otflm_rnnlm_prob_batch": (C.c_int, [_P, C.c_int64, _P, _P, _P, C.c_int32, _P, _P, _P, _P]),

@@ -2095,3 +2095,32 @@ extern "C" int otflm_streams_cache_put(OtflmStreams *s, int32_t sid, int64_t n, 
     CK(cudaFreeAsync(dc, st)); CK(cudaFreeAsync(dw, st)); CK(cudaFreeAsync(dp, st)); CK(cudaFreeAsync(dcn, st));
     return check_err(s, st);
 }
+
+// RescoreCache.roll_stats / clear (cache.py:121-128, :155-157) on one stream
+__global__ void k_stream_stats_op(DevStreams S, uint32_t s, int op) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    unsigned long long *st = S.stats + (size_t)s * 8;
+    if (op == 0) { st[3] += st[0]; st[4] += st[1]; st[5] += st[2]; st[0] = st[1] = st[2] = 0; }
+    else st[6] = 0;                                    // entries after clear
+}
+
+extern "C" int otflm_streams_roll_stats(OtflmStreams *s, int32_t sid, void *stream) {
+    int rc = cache_direct_ok(s, sid, 0);
+    if (rc) return rc;
+    k_stream_stats_op<<<1, 1, 0, (cudaStream_t)stream>>>(s->d, (uint32_t)sid, 0);
+    CKL();
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_streams_cache_clear(OtflmStreams *s, int32_t sid, void *stream) {
+    int rc = cache_direct_ok(s, sid, 0);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t o = (size_t)sid * s->d.kc_cap, n = s->d.kc_cap;
+    CK(cudaMemsetAsync(s->d.kc_key + o, 0, n * 8, st));
+    CK(cudaMemsetAsync(s->d.kc_claim + o, 0xFF, n * 4, st));
+    CK(cudaMemsetAsync(s->d.kc_cnext + o, 0xFF, n * 4, st));
+    k_stream_stats_op<<<1, 1, 0, st>>>(s->d, (uint32_t)sid, 1);
+    CKL();
+    return OTFLM_OK;
+}

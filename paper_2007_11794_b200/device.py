@@ -193,6 +193,14 @@ class DeviceStreams:
                                                        _p(p), _p(cn), current_stream_ptr()), "cache get")
         return found.astype(bool), p, cn
 
+    def roll_stats(self, stream_id: int) -> None:
+        _lib.check(_lib.load().otflm_streams_roll_stats(self.handle, int(stream_id), current_stream_ptr()),
+                   "roll_stats")
+
+    def cache_clear(self, stream_id: int) -> None:
+        _lib.check(_lib.load().otflm_streams_cache_clear(self.handle, int(stream_id), current_stream_ptr()),
+                   "cache clear")
+
     def cache_put(self, stream_id: int, c, w, p, cn) -> None:
         cc = np.ascontiguousarray(c, np.uint32)
         ww = np.ascontiguousarray(w, np.int32)

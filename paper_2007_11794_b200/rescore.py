@@ -244,6 +244,16 @@ class RescoreCache:
         found, p, cn = self._direct().cache_get(0, [c], [w])
         return CacheValue(float(p[0]), int(cn[0])) if found[0] else None
 
+    def clear(self) -> None:
+        """cache.py:121-125: drop every entry; counters are kept."""
+        if self._bind is not None:
+            self._bind.streams.cache_clear(0)
+
+    def roll_stats(self) -> None:
+        """cache.py:155-157: the window counters move into the cumulative ones."""
+        if self._bind is not None:
+            self._bind.streams.roll_stats(0)
+
     def put(self, key, value: CacheValue) -> None:
         """cache.py:96-108 on the device: first value wins; no-op when disabled."""
         c, w = (int(x) for x in key)

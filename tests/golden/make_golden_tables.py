@@ -81,6 +81,15 @@ def main():
         d[f"res_{tag}_p"] = np.array([r[0] for r in res])
         d[f"res_{tag}_c"] = np.array([r[1] for r in res], np.int64)
         d[f"stats_{tag}"] = np.array([s.lookups, s.hits, s.misses, len(c2)], np.int64)
+        if enabled:                                      # roll_stats, clear, then one more get
+            c2.roll_stats()
+            s1, cu = c2.stats(), c2.cumulative_stats()
+            c2.clear()
+            k = keys[0]
+            v = c2.get(k)
+            s2 = c2.stats()
+            d["after_ops"] = np.array([s1.lookups, s1.hits, s1.misses, cu.lookups, cu.hits, cu.misses,
+                                       len(c2), int(v is None), s2.lookups, s2.misses], np.int64)
     d["produced_by"] = np.array("otflm.context_table.IndexTable.encode; otflm.cache.rnnlm_prob; RescoreCache.get/put")
     np.savez_compressed(G.OUT / "tables.npz", **d)
     print("tables.npz", (G.OUT / "tables.npz").stat().st_size, "len", tl1, len(table), d["stats_on"], d["stats_off"])

@@ -75,3 +75,26 @@ def test_direct_get_put_refused_on_bounded_cache(small):
         cache.get((0, 5))
     with pytest.raises(ValueError, match="capacity-bounded"):
         cache.put((0, 5), CacheValue(-1.0, 1))
+
+
+def test_roll_stats_and_clear_match_reference(golden, small):
+    from paper_2007_11794_b200 import CacheValue, IndexTable, RescoreCache
+    d = golden("tables")
+    _, gm, _ = small
+    cache = RescoreCache()
+    IndexTable(16, 3).bind(gm.model, gm.tree, cache)
+    for (op, c, w, cn), p in zip(d["ops_on"], d["ops_on_p"]):
+        if op == 0:
+            cache.get((int(c), int(w)))
+        else:
+            cache.put((int(c), int(w)), CacheValue(float(p), int(cn)))
+    cache.roll_stats()
+    s1, cu = cache.stats(), cache.cumulative_stats()
+    cache.clear()
+    n_after = len(cache)
+    a = d["after_ops"]
+    assert [s1.lookups, s1.hits, s1.misses, cu.lookups, cu.hits, cu.misses, n_after] == [int(x) for x in a[:7]]
+    k = (int(d["ops_on"][0][1]), int(d["ops_on"][0][2]))
+    assert (cache.get(k) is None) == bool(a[7])
+    s2 = cache.stats()
+    assert [s2.lookups, s2.misses] == [int(a[8]), int(a[9])]
