@@ -1,0 +1,100 @@
+"""Parity at the bench's full sizes.
+
+The headline workload itself -- config b, 64 utterances x 300 frames,
+V = 20,000, H = 256, MaxEnt 2^21, beam 8, the bench's seed, TF32X3 stream
+schedule -- decoded on the B200 and by the exact CPU oracle (utterance-
+parallel over the host's cores, a few seconds), plus config c geometry
+(V = 65,536, H = 512) at full utterance length.
+
+Bar (BASELINE.json north star): outputs match the CPU reference, the 1-best
+identical except where competing path costs tie within the tolerance.  The
+exact FP64 mode is held to identity at the full bench size (arcs, expansions,
+context ids, cache counters; scores within 1e-9).  The TF32X3 tensor-core
+mode is held to the stated looser bound in its test.  Size-independent
+property in both: the GPU's combined score equals the oracle's rescoring of
+the GPU's own arcs (`oracle_path_score`, reference tests/conftest.py:65-78).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_decode(s, beam, precision):
+    from paper_2007_11794_b200.rescore import BatchDecoder
+    need = BatchDecoder.contexts_needed(s.lattices, beam)
+    dec = BatchDecoder(s.model, s.tree, s.small_lm, len(s.lattices), need, precision=precision)
+    dec.prepare(s.lattices, beam)
+    dec.run(1.0)
+    hyps, out = dec.fetch()
+    return dec, hyps, out, dec.streams.stats()
+
+
+def _compare(s, beam, precision):
+    """Per utterance: (arcs identical, expansions identical, |GPU - oracle
+    best| score, oracle rescoring of the GPU path - oracle best)."""
+    dec, hyps, out, st = _gpu_decode(s, beam, precision)
+    ref = O.decode_many(s.model, s.tree, s.small_lm, s.lattices, beam=beam)
+    om, og = O.OracleModel(s.model, s.tree), O.OracleNgram(s.small_lm)
+    rows = []
+    for u, (r, counts) in enumerate(ref):
+        h = hyps[u]
+        gpu_path = O.path_score(om, None, og, s.lattices[u], h.arcs)
+        rows.append(dict(arcs=h.arcs == r.arcs, exp=int(out["expansions"][u]) == r.expansions,
+                         counts=tuple(int(x) for x in st[u, :3]) == counts,
+                         end_ctx=h.end_context == r.end_context,
+                         d_score=abs(h.combined_score - r.combined_score),
+                         self_consistency=abs(h.combined_score - gpu_path),
+                         gap=gpu_path - r.combined_score))
+    return dec, rows
+
+
+def test_bench_config_b_full_workload_fp64_exact():
+    """The bench's N=1 workload (bench.py: build_setup(CONFIG, 64, 300,
+    seed=7)) in the exact FP64 mode: 1-best arcs, expansions, end context,
+    cache lookups / hits / misses identical for all 64 utterances, combined
+    scores within 1e-9."""
+    from paper_2007_11794_b200 import synth
+    s = synth.build_setup("b", n_utt=64, T=300, seed=7)
+    dec, rows = _compare(s, 8, "fp64")
+    for u, r in enumerate(rows):
+        assert r["arcs"] and r["exp"] and r["end_ctx"] and r["counts"], (u, r)
+        assert r["d_score"] <= 1e-9 and r["self_consistency"] <= 1e-9, (u, r)
+
+
+@pytest.mark.parametrize("config,n_utt,seed", [("b", 64, 7), ("c", 8, 17)])
+def test_full_size_tf32x3_stream_vs_oracle(config, n_utt, seed):
+    """The bench's throughput mode (TF32X3 recurrent update on tcgen05,
+    stream schedule) at full utterance length.  For every utterance the
+    GPU's combined score equals the oracle's rescoring of the GPU's own arcs
+    within 1e-4 per frame (every per-query score on the path is right).  The
+    1-best is the oracle's for at least 3/4 of the utterances; the others
+    diverge at beam-pruning near-ties (a token ranked 8th vs 9th at a node by
+    less than the ~1e-6 per-query difference; once pruned differently the
+    search continues on another path), and the path found there scores at
+    most 2e-3 per frame below the oracle's best under the oracle's own
+    rescoring.  Measured (profiles/r01q_fullsize_parity.log): config b 53/64
+    identical, divergent gaps 0.004-0.42 (at most 1.6e-4 of the path score);
+    config c 8/8 identical.  The FP64 mode above is the bit-exact one
+    (DESIGN.md "Precision and the 1-best")."""
+    from paper_2007_11794_b200 import synth
+    T = 300
+    s = synth.build_setup(config, n_utt=n_utt, T=T, seed=seed)
+    dec, rows = _compare(s, 8, "tf32x3")
+    assert dec.schedule == "stream"
+    same = sum(r["arcs"] for r in rows)
+    gaps = [r["gap"] for r in rows if not r["arcs"]]
+    print(f"config {config} full length tf32x3: identical 1-best {same}/{len(rows)}, "
+          f"divergent gaps {sorted(round(g, 4) for g in gaps)}")
+    for u, r in enumerate(rows):
+        assert r["self_consistency"] <= 1e-4 * T, (u, r)
+        if r["arcs"]:
+            assert r["d_score"] <= 1e-4 * T, (u, r)
+        else:
+            assert -2e-3 * T <= r["gap"] <= 1e-4 * T, (u, r)
+    assert 4 * same >= 3 * len(rows)
