@@ -80,7 +80,10 @@ def test_full_size_tf32x3_stream_vs_oracle(config, n_utt, seed):
     most 2e-3 per frame below the oracle's best under the oracle's own
     rescoring.  Measured (profiles/r01q_fullsize_parity.log): config b 53/64
     identical, divergent gaps 0.004-0.42 (at most 1.6e-4 of the path score);
-    config c 8/8 identical.  The FP64 mode above is the bit-exact one
+    config c 8/8 identical.  The exact oracle moved by one f32 ulp in W
+    changes 8/64 of the same 1-bests with gaps -0.16..+0.53
+    (tools/perturb_ties.py), so these are beam-search bifurcations at
+    fp32-level ties.  The FP64 mode above is the bit-exact one
     (DESIGN.md "Precision and the 1-best")."""
     from paper_2007_11794_b200 import synth
     T = 300
