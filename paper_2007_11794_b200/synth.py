@@ -27,6 +27,8 @@ from .model import HuffmanTree, NgramModel, RnnlmModel, build_huffman_from_count
 CONFIGS = {
     "a": dict(V=1000, H=64, bits=20, n_utt=1, T=300, breadth=3, beam=8),
     "b": dict(V=20000, H=256, bits=21, n_utt=64, T=300, breadth=3, beam=8),
+    # SURVEY.md §8d config (b) "fat variant": breadth 16, beam 64
+    "b_fat": dict(V=20000, H=256, bits=21, n_utt=64, T=300, breadth=16, beam=64),
     "c": dict(V=65536, H=512, bits=22, n_utt=8, T=300, breadth=3, beam=8),
     "d": dict(V=65536, H=512, bits=22, n_queries=1 << 20, n_ctx=1 << 18),
     "e": dict(V=65536, H=512, bits=22, n_utt=4096, T=300, breadth=3, beam=8),

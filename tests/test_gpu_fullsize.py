@@ -101,3 +101,21 @@ def test_full_size_tf32x3_stream_vs_oracle(config, n_utt, seed):
         else:
             assert -2e-3 * T <= r["gap"] <= 1e-4 * T, (u, r)
     assert 4 * same >= 3 * len(rows)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "tf32x3"])
+def test_fat_variant_vs_oracle(precision):
+    """SURVEY.md §8d config (b) fat variant: breadth 16, beam 64 (about 15k
+    requests per frame per utterance, 256 tokens x 16 arcs per node set)."""
+    from paper_2007_11794_b200 import synth
+    T = 10
+    s = synth.build_setup("b_fat", n_utt=4, T=T, seed=3)
+    dec, rows = _compare(s, 64, precision)
+    for u, r in enumerate(rows):
+        if precision == "fp64":
+            assert r["arcs"] and r["exp"] and r["end_ctx"] and r["counts"], (u, r)
+            assert r["d_score"] <= 1e-9 and r["self_consistency"] <= 1e-9, (u, r)
+        else:
+            assert r["self_consistency"] <= 1e-4 * T, (u, r)
+            assert r["arcs"] or -2e-3 * T <= r["gap"] <= 1e-4 * T, (u, r)
+    print(f"fat {precision}: schedule {dec.schedule}, identical 1-best {sum(r['arcs'] for r in rows)}/{len(rows)}")
