@@ -801,12 +801,14 @@ static int check_err(OtflmStreams *s, cudaStream_t st) {
     if (he) {
         CK(cudaMemsetAsync(s->d.err, 0, 4, st));
         CK(cudaStreamSynchronize(st));
-        if (he & OTF_E_HASH) { g_detail = "content digest collision"; return OTFLM_ERR_HASH; }
+        // a capacity overflow first: the stages after it read rows that were
+        // never written, which can also raise a spurious digest mismatch
         if (he & (OTF_E_TABLE_FULL | OTF_E_ARENA_FULL | OTF_E_CACHE_FULL)) {
             g_detail = (he & OTF_E_ARENA_FULL) ? "hidden-state arena full"
                      : (he & OTF_E_CACHE_FULL) ? "cache table full" : "index table full";
             return OTFLM_ERR_TABLE_FULL;
         }
+        if (he & OTF_E_HASH) { g_detail = "content digest collision"; return OTFLM_ERR_HASH; }
         if (he & OTF_E_KEY) { g_detail = "word missing from unigram table"; return OTFLM_ERR_KEY; }
         if (he & OTF_E_VALUE) return OTFLM_ERR_VALUE;
         return OTFLM_ERR_CUDA;

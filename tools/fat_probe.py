@@ -11,8 +11,8 @@ from paper_2007_11794_b200.rescore import BatchDecoder
 n_utt, T = int(sys.argv[1]), int(sys.argv[2])
 s = synth.build_setup("b_fat", n_utt=n_utt, T=T, seed=7)
 need = BatchDecoder.contexts_needed(s.lattices, 64)
-for prec in ("tf32x3", "fp64"):
-    dec = BatchDecoder(s.model, s.tree, s.small_lm, n_utt, need, precision=prec)
+for prec, sched in (("tf32x3", "level"), ("tf32x3", "stream"), ("fp64", "level")):
+    dec = BatchDecoder(s.model, s.tree, s.small_lm, n_utt, need, precision=prec, schedule=sched)
     dec.prepare(s.lattices, 64)
     dec.run(1.0)
     torch.cuda.synchronize()
