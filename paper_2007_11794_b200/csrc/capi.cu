@@ -806,6 +806,7 @@ static int check_err(OtflmStreams *s, cudaStream_t st) {
         if (he & (OTF_E_TABLE_FULL | OTF_E_ARENA_FULL | OTF_E_CACHE_FULL)) {
             g_detail = (he & OTF_E_ARENA_FULL) ? "hidden-state arena full"
                      : (he & OTF_E_CACHE_FULL) ? "cache table full" : "index table full";
+            g_detail += " [device flags " + std::to_string(he) + "]";
             return OTFLM_ERR_TABLE_FULL;
         }
         if (he & OTF_E_HASH) { g_detail = "content digest collision"; return OTFLM_ERR_HASH; }

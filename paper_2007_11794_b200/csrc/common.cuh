@@ -24,6 +24,7 @@
 #define OTF_E_KEY 16u
 #define OTF_E_VALUE 32u
 #define OTF_E_PATH 64u
+#define OTF_E_NOSLOT 128u   // with OTF_E_TABLE_FULL: a new context found no index-table slot
 
 struct DevModel {
     int H, V, order;

@@ -619,6 +619,7 @@ __device__ __forceinline__ void assign_range(DevPlan &P, const DevStreams &S, ui
             const uint32_t slot = sm.ins[tid];
             if (idx > S.max_ctx || slot == OTF_UNSET) {
                 full = true;
+                if (slot == OTF_UNSET) atomicOr(S.err, OTF_E_NOSLOT);
             } else {
                 cn = idx;
                 S.ct_idx[cb + slot] = idx;
