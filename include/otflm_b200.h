@@ -45,6 +45,10 @@ extern "C" {
 #define OTFLM_PREC_TF32X3 1  /* tcgen05 kind::tf32, 3-pass split (fp32-faithful) */
 #define OTFLM_PREC_BF16 2    /* tcgen05 kind::f16 with bf16 operands */
 #define OTFLM_PREC_TF32 3    /* tcgen05 kind::tf32, single pass */
+#define OTFLM_PREC_EXACT 4   /* tcgen05 kind::i8 digit planes, exact int32 accumulation, certified
+                                f32 rounding + sequential-f64 fallback: every h' equals the
+                                reference's (_kernels_nb.py:51-60); float64 HS.  Persistent stream
+                                schedule; elsewhere it runs the FP64 path */
 
 /* decode schedules (otflm_plan_set_schedule) */
 #define OTFLM_SCHED_LEVEL 0   /* level-synchronous: expand / HS || update / assign kernels per level

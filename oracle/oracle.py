@@ -89,6 +89,8 @@ def lib():
         L.orc_path_score.argtypes = [p, p, p, p, i32, f64, p]
         L.orc_decode_many.restype = C.c_int
         L.orc_decode_many.argtypes = [p, p, p, i32, f64, i64, i32, i32, p, p, p, p, p]
+        L.orc_decode_many_t.restype = C.c_int
+        L.orc_decode_many_t.argtypes = [p, p, p, i32, f64, i64, i32, i32, p, p, p, p, p, p]
         L.orc_query_batch.restype = None
         L.orc_query_batch.argtypes = [p, i64, p, p, p, p, p, p, i32]
         L.orc_stack_set_capacity.restype = C.c_int
@@ -296,6 +298,7 @@ class OraclePath:
     combined_score: float
     end_context: int
     expansions: int
+    table_len: int = -1       # IndexTable length after the decode (decode_many only)
 
 
 @dataclass
@@ -406,16 +409,16 @@ def decode_many(model, tree, ngram, lattices, lm_weight=1.0, beam=8, enabled=Tru
     bufs = [np.zeros(max(l.n_arcs, 1), np.int32) for l in ols]
     res_arr = ResArr(*[_OrcResult(0, _ptr(b).value, len(b), 0.0, 0.0, 0.0, 0, 0) for b in bufs])
     rcs = np.zeros(n, np.int32)
-    lk, hi, mi = (np.zeros(n, np.int64) for _ in range(3))
-    _check(lib().orc_decode_many(om.ref, og.handle, lat_arr, n, float(lm_weight), int(beam),
-                                 int(bool(enabled)), int(n_threads), res_arr, _ptr(rcs),
-                                 _ptr(lk), _ptr(hi), _ptr(mi)), "decode_many")
+    lk, hi, mi, tl = (np.zeros(n, np.int64) for _ in range(4))
+    _check(lib().orc_decode_many_t(om.ref, og.handle, lat_arr, n, float(lm_weight), int(beam),
+                                   int(bool(enabled)), int(n_threads), res_arr, _ptr(rcs),
+                                   _ptr(lk), _ptr(hi), _ptr(mi), _ptr(tl)), "decode_many")
     out = []
     for i, l in enumerate(ols):
         r = res_arr[i]
         arcs = tuple(int(a) for a in bufs[i][:r.n_arcs])
         out.append((OraclePath(arcs, tuple(int(l.arrs[2][a]) for a in arcs), r.acoustic, r.lm,
-                               r.combined, int(r.end_ctx), int(r.expansions)),
+                               r.combined, int(r.end_ctx), int(r.expansions), int(tl[i])),
                     (int(lk[i]), int(hi[i]), int(mi[i]))))
     return out
 

@@ -918,7 +918,7 @@ typedef struct {
     double lm_weight; int64_t beam; int32_t enabled;
     OrcResult *res; int32_t *rcs;
     int32_t next; pthread_mutex_t mu;
-    int64_t *lookups, *hits, *misses;
+    int64_t *lookups, *hits, *misses, *table_len;
 } OrcJob;
 
 static void *orc_worker(void *arg) {
@@ -931,20 +931,23 @@ static void *orc_worker(void *arg) {
         if (i >= j->n_lat) break;
         j->rcs[i] = orc_rescore_onthefly(s, j->g, &j->lats[i], j->lm_weight, j->beam, &j->res[i]);
         j->lookups[i] = s->cur.lookups; j->hits[i] = s->cur.hits; j->misses[i] = s->cur.misses;
+        if (j->table_len) j->table_len[i] = (int64_t)s->table.n;
         orc_stack_reset(s, 0);
     }
     orc_stack_destroy(s);
     return NULL;
 }
 
-int orc_decode_many(const OrcModel *m, const OrcNgram *g, const OrcLattice *lats,
-                    int32_t n_lat, double lm_weight, int64_t beam, int32_t enabled,
-                    int32_t n_threads, OrcResult *res, int32_t *rcs,
-                    int64_t *lookups, int64_t *hits, int64_t *misses) {
+/* table_len (nullable): IndexTable length of each utterance's stream after
+ * its decode (context_table.py:116-119) */
+int orc_decode_many_t(const OrcModel *m, const OrcNgram *g, const OrcLattice *lats,
+                      int32_t n_lat, double lm_weight, int64_t beam, int32_t enabled,
+                      int32_t n_threads, OrcResult *res, int32_t *rcs,
+                      int64_t *lookups, int64_t *hits, int64_t *misses, int64_t *table_len) {
     OrcJob j;
     j.m = m; j.g = g; j.lats = lats; j.n_lat = n_lat; j.lm_weight = lm_weight;
     j.beam = beam; j.enabled = enabled; j.res = res; j.rcs = rcs; j.next = 0;
-    j.lookups = lookups; j.hits = hits; j.misses = misses;
+    j.lookups = lookups; j.hits = hits; j.misses = misses; j.table_len = table_len;
     pthread_mutex_init(&j.mu, NULL);
     if (n_threads < 1) n_threads = 1;
     pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)n_threads);
@@ -954,6 +957,14 @@ int orc_decode_many(const OrcModel *m, const OrcNgram *g, const OrcLattice *lats
     pthread_mutex_destroy(&j.mu);
     for (int32_t i = 0; i < n_lat; i++) if (rcs[i]) return rcs[i];
     return ORC_OK;
+}
+
+int orc_decode_many(const OrcModel *m, const OrcNgram *g, const OrcLattice *lats,
+                    int32_t n_lat, double lm_weight, int64_t beam, int32_t enabled,
+                    int32_t n_threads, OrcResult *res, int32_t *rcs,
+                    int64_t *lookups, int64_t *hits, int64_t *misses) {
+    return orc_decode_many_t(m, g, lats, n_lat, lm_weight, beam, enabled, n_threads, res, rcs,
+                             lookups, hits, misses, NULL);
 }
 
 /* Batched kernel-level helpers (threaded) for the query microbench and

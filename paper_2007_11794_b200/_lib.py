@@ -19,7 +19,7 @@ OK = 0
 ERR_VALUE, ERR_UNKNOWN_INDEX, ERR_TABLE_FULL, ERR_NO_PATH, ERR_KEY = -1, -2, -3, -4, -5
 ERR_NOMEM, ERR_CYCLE, ERR_PACK, ERR_CUDA, ERR_HASH = -6, -7, -8, -9, -10
 
-PREC = {"fp64": 0, "tf32x3": 1, "bf16": 2, "tf32": 3}
+PREC = {"fp64": 0, "tf32x3": 1, "bf16": 2, "tf32": 3, "exact": 4}
 PROFILE_CATEGORIES = ("expand", "hs", "advance", "assign", "final", "misc", "stream")
 SCHED = {"level": 0, "stream": 1}
 

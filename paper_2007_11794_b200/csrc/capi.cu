@@ -86,6 +86,12 @@ struct Allocs {
     }
 };
 
+// OTFLM_PREC_EXACT runs the integer digit-plane update only in the persistent
+// stream kernel; everywhere else it is the FP64 path (both are bit-exact with
+// the reference's float32 results: exact_update.cuh, hs.cuh)
+static inline bool prec_ok(int p) { return p >= 0 && p <= 4; }
+static inline int level_prec(int p) { return p == OTFLM_PREC_EXACT ? OTFLM_PREC_FP64 : p; }
+
 // ==========================================================================
 // model
 // ==========================================================================
@@ -194,6 +200,7 @@ extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, Otflm
     dm.path_off = poff; dm.path_code = pcode;
     dm.W_hi = Whi; dm.W_lo = Wlo; dm.W_bf = Wbf;
     dm.W_t = nullptr; dm.wt_kcb = 0; dm.wt_npad = 0; dm.W_t64 = nullptr;
+    dm.Wd = nullptr; dm.wx = nullptr; dm.wd_nkx = 0;
     if (W) {
         k_prep_weights<<<256, 256>>>(dm, WT, Whi, Wlo, Wbf);
         CK(cudaGetLastError());
@@ -212,6 +219,18 @@ extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, Otflm
             dm.W_t64 = Wt64;
             k_prep_wtiles<<<256, 256>>>(dm, Wt64, 64);
             CK(cudaGetLastError());
+            // exact mode: 8-bit digit planes of W + per-unit bound constants
+            const int nkx = (H + xu::KC - 1) / xu::KC;
+            uint8_t *Wd = nullptr;
+            double4 *wx = nullptr;
+            const size_t nwd = (size_t)(np / tc::BM) * nkx * 4 * xu::PLANE_W;
+            if (m->mem.alloc(&Wd, nwd) != cudaSuccess || m->mem.alloc(&wx, (size_t)H) != cudaSuccess) {
+                m->mem.free_all(); delete m; g_detail = "cudaMalloc model"; return OTFLM_ERR_NOMEM;
+            }
+            CK(cudaMemset(Wd, 0, nwd));
+            k_prep_wdigits<<<H, 256>>>(W, H, nkx, Wd, wx);
+            CK(cudaGetLastError());
+            dm.Wd = Wd; dm.wx = wx; dm.wd_nkx = nkx;
         }
     }
     CK(cudaDeviceSynchronize());
@@ -431,7 +450,8 @@ static int launch_advance(const DevModel &m, int prec, uint32_t n_cap, const Row
 extern "C" int otflm_advance_hidden_batch(const OtflmModel *m, int64_t n, const int32_t *ctx, const float *h_in,
                                           const int32_t *w, float *h_out, int32_t precision, void *stream) {
     if (n <= 0) return OTFLM_OK;
-    if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    if (!prec_ok(precision)) return OTFLM_ERR_VALUE;
+    precision = level_prec(precision);
     if (!m->d.U || !m->d.W) { g_detail = "model has no recurrent weights"; return OTFLM_ERR_VALUE; }
     const RowSpec rs{nullptr, nullptr, nullptr, nullptr, nullptr, 0xFFFFFFFFu};
     return launch_advance(m->d, precision, (uint32_t)n, rs, ctx, w, h_in, h_out, 0xFFFFFFFFu, (cudaStream_t)stream);
@@ -440,7 +460,8 @@ extern "C" int otflm_advance_hidden_batch(const OtflmModel *m, int64_t n, const 
 extern "C" int otflm_advance_hidden_rows(const OtflmModel *m, int64_t n, const float *input_rows, const int32_t *ctx,
                                          const float *h_in, float *h_out, int32_t precision, void *stream) {
     if (n <= 0) return OTFLM_OK;
-    if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    if (!prec_ok(precision)) return OTFLM_ERR_VALUE;
+    precision = level_prec(precision);
     if (!m->d.W) { g_detail = "model has no recurrent weights"; return OTFLM_ERR_VALUE; }
     DevModel dm = m->d;
     dm.U = input_rows;   // row i is the input row of query i
@@ -619,7 +640,8 @@ extern "C" int otflm_all_word_logprobs_batch(const OtflmModel *m, int64_t n, con
                                              const float *h, const int32_t *hist, const int32_t *hist_len,
                                              double *out, int32_t precision, void *stream) {
     if (n <= 0) return OTFLM_OK;
-    if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    if (!prec_ok(precision)) return OTFLM_ERR_VALUE;
+    precision = level_prec(precision);
     if (!m->d.NV || !m->d.ME || !m->d.path_off) { g_detail = "model has no output layer"; return OTFLM_ERR_VALUE; }
     cudaStream_t s = (cudaStream_t)stream;
     const DevModel &d = m->d;
@@ -961,6 +983,8 @@ struct OtflmPlan {
     double g_lm = 0; int g_prec = -1; const OtflmNgram *g_ng = nullptr; int64_t g_nodes = 0;
     uint64_t h2d_bytes = 0;
     unsigned long long *alg_buf = nullptr;
+    uint8_t *xs = nullptr;             // exact stream mode: per-stream digit scratch (Allocs-owned)
+    size_t xs_bytes = 0;
     cudaStream_t side = nullptr;               // second branch of each level (HS)
     cudaStream_t chain = nullptr;              // this plan's chain inside a group graph
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_done = nullptr;
@@ -1484,6 +1508,21 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
 // ---- persistent per-stream schedule (stream_decode.cuh) ----
 struct SdConfig { int stages, qb_max; size_t smem; uint32_t tmem_cols; };
 static bool sd_config(const DevModel &m, int prec, SdConfig *c) {
+    if (prec == OTFLM_PREC_EXACT) {
+        if (!m.Wd || m.H % 4 != 0 || m.H > 512 || !m.U || !m.NV || !m.path_off) return false;
+        const size_t budget = 200u * 1024u;
+        const size_t tail = 2u * xu::FBCAP * 4 + 2u * xu::XR * 8 + 16;
+        c->stages = (int)std::min<size_t>(4, (budget - tail) / xu::STAGE);
+        if (c->stages < 2) return false;
+        const int ord = m.order <= 3 ? 3 : OTF_MAX_ORDER;
+        const size_t hs_fixed = (size_t)sd::PAIRCAP * 13 + (size_t)sd::QMAX * (ord * 8 + 7 * 4) + (sd::NW + 2) * 4 + 64;
+        if (hs_fixed + 8 * 8 * (size_t)m.H > budget) return false;
+        c->qb_max = (int)std::min<size_t>(sd::QMAX, (budget - hs_fixed) / (8 * (size_t)m.H));   // float64 rows
+        c->smem = std::max((size_t)c->stages * xu::STAGE + tail, hs_fixed + (size_t)c->qb_max * 8 * m.H);
+        c->smem = std::max(c->smem, (size_t)28 * sd::NT);
+        c->tmem_cols = 512;
+        return true;
+    }
     if (!(prec == OTFLM_PREC_TF32X3 || prec == OTFLM_PREC_TF32)) return false;
     if (!m.W_t || m.H % 4 != 0 || m.wt_npad > 512 || !m.U || !m.NV || !m.path_off) return false;
     const bool x3 = prec == OTFLM_PREC_TF32X3;
@@ -1509,7 +1548,7 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
     DevStreams &S = p->st->d;
     DevPlan &d = p->d;
     SdConfig c;
-    if (!sd_config(m, prec, &c)) { g_detail = "persistent schedule needs a TF32X3/TF32 precision and H % 4 == 0, H <= 512"; return OTFLM_ERR_VALUE; }
+    if (!sd_config(m, prec, &c)) { g_detail = "persistent schedule needs an EXACT/TF32X3/TF32 precision and H % 4 == 0, H <= 512"; return OTFLM_ERR_VALUE; }
     const bool part = d.arena_start != OTF_UNSET;
     uint32_t *cursor = part ? d.cursor : S.arena_used;
     const uint32_t limit = part ? d.arena_end : S.arena_rows;
@@ -1517,7 +1556,8 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
     do {                                                                                                        \
         CK(cudaFuncSetAttribute(k_decode_streams<MODE, KCB, CPL, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem)); \
         k_decode_streams<MODE, KCB, CPL, ORD><<<2 * p->n_utt, sd::NT, c.smem, s>>>(m, d, S, g->d, (long long)p->beam, lm, \
-                                                                              c.stages, c.qb_max, cursor, limit, c.tmem_cols); \
+                                                                              c.stages, c.qb_max, cursor, limit, c.tmem_cols, \
+                                                                              p->xs, xs_stride); \
     } while (0)
 #define SD_ORD(MODE, KCB, CPL) do { if (m.order <= 3) SD_LAUNCH(MODE, KCB, CPL, 3); else SD_LAUNCH(MODE, KCB, CPL, OTF_MAX_ORDER); } while (0)
 #define SD_H(MODE)                                                                                              \
@@ -1526,8 +1566,23 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
         else if (m.H <= 256) SD_ORD(MODE, 128, 2);                                                              \
         else SD_ORD(MODE, 64, 4);                                                                               \
     } while (0)
-    if ((m.wt_npad <= 256 ? 128 : 64) != m.wt_kcb) { g_detail = "W tile layout mismatch"; return OTFLM_ERR_VALUE; }
-    if (prec == OTFLM_PREC_TF32X3) SD_H(1); else SD_H(3);
+    size_t xs_stride = 0;
+    if (prec == OTFLM_PREC_EXACT) {
+        // one chunk of digit planes per stream: [kc][plane][XR rows x 64 B]
+        xs_stride = (size_t)m.wd_nkx * 4 * xu::XR * xu::KC;
+        const size_t need = xs_stride * std::max<uint32_t>(p->n_utt, 1);
+        if (p->xs_bytes < need) {
+            uint8_t *x = nullptr;
+            if (p->mem.alloc(&x, need) != cudaSuccess) { g_detail = "cudaMalloc exact scratch"; return OTFLM_ERR_NOMEM; }
+            p->xs = x; p->xs_bytes = need;
+        }
+        if (m.H <= 128) SD_ORD(4, 64, 1);
+        else if (m.H <= 256) SD_ORD(4, 64, 2);
+        else SD_ORD(4, 64, 4);
+    } else {
+        if ((m.wt_npad <= 256 ? 128 : 64) != m.wt_kcb) { g_detail = "W tile layout mismatch"; return OTFLM_ERR_VALUE; }
+        if (prec == OTFLM_PREC_TF32X3) SD_H(1); else SD_H(3);
+    }
 #undef SD_H
 #undef SD_ORD
 #undef SD_LAUNCH
@@ -1555,7 +1610,7 @@ extern "C" int otflm_plan_set_schedule(OtflmPlan *p, int32_t schedule) {
 
 extern "C" int otflm_schedule_supported(const OtflmModel *m, int32_t schedule, int32_t precision) {
     if (!m) return 0;
-    if (schedule == OTFLM_SCHED_LEVEL) return precision >= 0 && precision <= 3;
+    if (schedule == OTFLM_SCHED_LEVEL) return prec_ok(precision) ? 1 : 0;
     SdConfig c;
     return schedule == OTFLM_SCHED_STREAM && sd_config(m->d, precision, &c) ? 1 : 0;
 }
@@ -1581,7 +1636,8 @@ extern "C" int otflm_decode_run(OtflmPlan *p, const OtflmNgram *g, double lm_wei
 static int decode_run_impl(OtflmPlan *p, const OtflmNgram *g, double lm_weight, int32_t precision,
                            int32_t use_graph, void *stream) {
     if (!p || !g) return OTFLM_ERR_VALUE;
-    if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    if (!prec_ok(precision)) return OTFLM_ERR_VALUE;
+    if (p->schedule != OTFLM_SCHED_STREAM) precision = level_prec(precision);
     if (g->d.order - 1 > p->st->m->d.order) { g_detail = "small LM order exceeds the stored context history"; return OTFLM_ERR_VALUE; }
     if (g->d.V < p->st->m->d.V) { g_detail = "small LM vocabulary smaller than model"; return OTFLM_ERR_VALUE; }
     cudaStream_t s = (cudaStream_t)stream;
@@ -1810,7 +1866,8 @@ static int enqueue_group(OtflmGroup *g, const OtflmNgram *ng, double lm, int pre
 
 extern "C" int otflm_group_run(OtflmGroup *g, const OtflmNgram *ng, double lm_weight, int32_t precision,
                                void *stream) {
-    if (!g || !ng || precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    if (!g || !ng || !prec_ok(precision)) return OTFLM_ERR_VALUE;
+    precision = level_prec(precision);
     cudaStream_t s = (cudaStream_t)stream;
     if (!g->gexec || g->g_lm != lm_weight || g->g_prec != precision || g->g_ng != ng ||
         g->g_ver != g->plans[0]->st->version) {
@@ -1909,7 +1966,8 @@ extern "C" int otflm_rnnlm_prob_batch(OtflmStreams *s, int64_t n, const int32_t 
                                       uint8_t *hit_h, void *stream) {
     if (!s || n < 0) return OTFLM_ERR_VALUE;
     if (n == 0) return OTFLM_OK;
-    if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    if (!prec_ok(precision)) return OTFLM_ERR_VALUE;
+    precision = level_prec(precision);
     cudaStream_t st = (cudaStream_t)stream;
     const DevModel &m = s->m->d;
     for (int64_t i = 0; i < n; i++) {

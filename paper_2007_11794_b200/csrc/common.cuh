@@ -42,6 +42,12 @@ struct DevModel {
     // the same with 64-byte K chunks (SWIZZLE_64B), for the batched update
     // k_advance_tc's B operand: one bulk copy per (K chunk, N tile, hi/lo)
     const float *W_t64;
+    // exact mode (exact_update.cuh): W as 8-bit digit planes pre-tiled per
+    // (M tile, 64-byte K chunk) -- [mt][kc][plane][128 rows x 64 B] -- and per
+    // output unit {sW 2^-47, A_i, B_i, sW} for the combine and the error bound
+    const uint8_t *Wd;
+    const double4 *wx;
+    int wd_nkx;                        // 64-byte K chunks (H rounded up to 64)
 };
 
 struct DevNgram {

@@ -130,6 +130,7 @@ __device__ __forceinline__ unsigned long long transpose_sum32(unsigned long long
     return v[0];
 }
 }  // namespace sd
+#include "exact_update.cuh"
 
 // --------------------------------------------------------------------------
 // Node-parallel HS + MaxEnt for one level of one stream (fast mode: f32 lane
@@ -147,6 +148,7 @@ constexpr int PAIRCAP = 2048;      // (query, node) pairs per batch
 constexpr int QMAX = 128;          // queries per batch (upper bound)
 struct HsLevelSmem {
     float *h;                      // [qb][H] context rows
+    double *hd;                    // [qb][H] context rows widened (EXACT)
     double *lsig;                  // [PAIRCAP] activation, then log-sigmoid, per pair
     uint32_t *pcode;               // [PAIRCAP] path code of each pair
     uint8_t *pq;                   // [PAIRCAP] batch query of each pair
@@ -159,7 +161,7 @@ struct HsLevelSmem {
 
 // Run by a group of NT threads (NW warps) synchronising on named barrier
 // BAR; tid / wid are group-relative.
-template <int CPL, int ORD, int NT, int BAR>
+template <int CPL, int ORD, int NT, int BAR, bool EXACT>
 __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, DevStreams &S, uint32_t base,
                                                  uint32_t n, const sd::HsLevelSmem &hs, int qb_max, int tid,
                                                  int wid, int lane, unsigned long long *ph) {
@@ -231,8 +233,14 @@ __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, 
         }
         for (int i = tid; i < nb * NCH; i += NT) {
             const int t = i / NCH, c = i - t * NCH;
-            reinterpret_cast<float4 *>(hs.h)[(size_t)t * NCH + c] =
-                __ldcg(reinterpret_cast<const float4 *>(S.arena_h + (size_t)hs.row[t] * H) + c);
+            const float4 x = __ldcg(reinterpret_cast<const float4 *>(S.arena_h + (size_t)hs.row[t] * H) + c);
+            if (EXACT) {
+                double2 *d2 = reinterpret_cast<double2 *>(hs.hd + (size_t)t * H + 4 * c);
+                d2[0] = make_double2(widen(x.x), widen(x.y));
+                d2[1] = make_double2(widen(x.z), widen(x.w));
+            } else {
+                reinterpret_cast<float4 *>(hs.h)[(size_t)t * NCH + c] = x;
+            }
         }
         HS_SYNC();
         HS_MARK(4);
@@ -250,21 +258,43 @@ __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, 
                 double me = 0.0;
                 if (live && sub < kmax)
                     me = (double)__ldg(m.ME + (otf_mix(hs.pre[t * ORD + sub], (uint64_t)(code & 0x7FFFFFFFu)) & m.mask));
-                float f0 = 0.f, f1 = 0.f, f2 = 0.f, f3 = 0.f;
-                if (live) {
-                    const float4 *row = reinterpret_cast<const float4 *>(m.NV + (size_t)(code & 0x7FFFFFFFu) * H);
-                    const float4 *hv = reinterpret_cast<const float4 *>(hs.h + (size_t)t * H);
-#pragma unroll 8
-                    for (int k = sub; k < NCH; k += 4) {
-                        const float4 x = __ldg(row + k);
-                        const float4 h4 = hv[k];
-                        f0 = fmaf(x.x, h4.x, f0);
-                        f1 = fmaf(x.y, h4.y, f1);
-                        f2 = fmaf(x.z, h4.z, f2);
-                        f3 = fmaf(x.w, h4.w, f3);
+                double a;
+                if (EXACT) {
+                    // float64 accumulation of the exact f32 x f32 products
+                    // (_kernels_nb.py:66-68); the node-vector element is
+                    // widened half by the conversion unit, half by integer ops
+                    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                    if (live) {
+                        const float4 *row = reinterpret_cast<const float4 *>(m.NV + (size_t)(code & 0x7FFFFFFFu) * H);
+                        const double2 *hv = reinterpret_cast<const double2 *>(hs.hd + (size_t)t * H);
+#pragma unroll 4
+                        for (int k = sub; k < NCH; k += 4) {
+                            const float4 x = __ldg(row + k);
+                            const double2 h01 = hv[2 * k], h23 = hv[2 * k + 1];
+                            a0 = fma((double)x.x, h01.x, a0);
+                            a1 = fma(widen(x.y), h01.y, a1);
+                            a2 = fma((double)x.z, h23.x, a2);
+                            a3 = fma(widen(x.w), h23.y, a3);
+                        }
                     }
+                    a = (a0 + a1) + (a2 + a3);
+                } else {
+                    float f0 = 0.f, f1 = 0.f, f2 = 0.f, f3 = 0.f;
+                    if (live) {
+                        const float4 *row = reinterpret_cast<const float4 *>(m.NV + (size_t)(code & 0x7FFFFFFFu) * H);
+                        const float4 *hv = reinterpret_cast<const float4 *>(hs.h + (size_t)t * H);
+#pragma unroll 8
+                        for (int k = sub; k < NCH; k += 4) {
+                            const float4 x = __ldg(row + k);
+                            const float4 h4 = hv[k];
+                            f0 = fmaf(x.x, h4.x, f0);
+                            f1 = fmaf(x.y, h4.y, f1);
+                            f2 = fmaf(x.z, h4.z, f2);
+                            f3 = fmaf(x.w, h4.w, f3);
+                        }
+                    }
+                    a = ((double)f0 + (double)f1) + ((double)f2 + (double)f3);
                 }
-                double a = ((double)f0 + (double)f1) + ((double)f2 + (double)f3);
                 a += __shfl_xor_sync(0xffffffffu, a, 1);
                 a += __shfl_xor_sync(0xffffffffu, a, 2);
                 // MaxEnt orders added in reference order (k = 1, 2, ...)
@@ -338,10 +368,12 @@ __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, 
 template <int MODE, int KC_B, int CPL, int ORD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sd::NT, 1)
 k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, double lm_weight, int stages,
-                 int qb_max, uint32_t *cursor, uint32_t row_limit, uint32_t tmem_cols) {
+                 int qb_max, uint32_t *cursor, uint32_t row_limit, uint32_t tmem_cols, uint8_t *xscratch,
+                 size_t xs_stride) {
     using namespace tc;
     namespace cg = cooperative_groups;
     constexpr bool X3 = MODE == 1;
+    constexpr bool EXACT = MODE == 4;       // integer digit-plane update + float64 HS (bit-exact)
     constexpr int NT = sd::NT, NW = sd::NW;
     constexpr int KE = KC_B / 4;            // tf32 elements of K per chunk
     constexpr int CH = KC_B / 16;           // 16-byte pieces per row per chunk
@@ -367,11 +399,16 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
 
     if (tid == 0) {
         for (int st = 0; st < stages; st++) {
-            mbar_init(smem_u32(&bar_full[st]), NW);           // one per loader warp + the W copy
+            mbar_init(smem_u32(&bar_full[st]), EXACT ? 1 : NW);   // loader warps (+ W copy) / one bulk producer
             mbar_init(smem_u32(&bar_empty[st]), 1);
         }
         mbar_init(smem_u32(&bar_done), 1);
         s_abort = 0;
+        if (EXACT && rank == 1) {                          // deferred-fallback counters (xu::Ring::fb_n)
+            uint32_t *fbn = reinterpret_cast<uint32_t *>(smem + (size_t)stages * xu::STAGE + 2 * xu::FBCAP * 4 +
+                                                         2 * xu::XR * 8);
+            fbn[0] = 0u; fbn[1] = 0u;
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     uint32_t tmem = 0;
@@ -407,8 +444,9 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     // node-parallel HS scratch (rank 0): the whole dynamic shared memory
     sd::HsLevelSmem hsm;
     {
-        uint8_t *p = smem + (size_t)qb_max * 4 * H;
+        uint8_t *p = smem + (size_t)qb_max * (EXACT ? 8 : 4) * H;
         hsm.h = reinterpret_cast<float *>(smem);
+        hsm.hd = reinterpret_cast<double *>(smem);
         hsm.lsig = reinterpret_cast<double *>(p); p += sd::PAIRCAP * 8;
         hsm.pcode = reinterpret_cast<uint32_t *>(p); p += sd::PAIRCAP * 4;
         hsm.pre = reinterpret_cast<unsigned long long *>(p); p += sd::QMAX * ORD * 8;
@@ -462,12 +500,26 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
             // scores of the level's requests (they only feed assign) alongside
             constexpr int HS_NT = NT - 64;
             if (tid < HS_NT) {
-                if (n) hs_level_nodepar<CPL, ORD, HS_NT, 1>(m, Q, S, base, n, hsm, qb_max, tid, wid, lane,
+                if (n) hs_level_nodepar<CPL, ORD, HS_NT, 1, EXACT>(m, Q, S, base, n, hsm, qb_max, tid, wid, lane,
                                                              prof ? ph : nullptr);
             } else {
                 small_lm_scores(Q, S, g, sid, L.re - L.rb, tid - HS_NT, NT - HS_NT);
             }
             SD_MARK(6);
+        } else if (n && EXACT) {
+            // ------------- exact recurrent update (tcgen05 kind::i8) -------------
+            xu::Ring rg;
+            rg.smem = smem; rg.stages = stages; rg.tmem = tmem;
+            rg.full = bar_full; rg.empty = bar_empty; rg.done = &bar_done;
+            uint8_t *tail = smem + (size_t)stages * xu::STAGE;
+            rg.fb = reinterpret_cast<uint32_t *>(tail);
+            rg.sh = reinterpret_cast<double *>(tail + 2 * xu::FBCAP * 4);
+            rg.eh = rg.sh + xu::XR;
+            rg.fb_n = reinterpret_cast<uint32_t *>(rg.eh + xu::XR);
+            rg.xs = xscratch + (size_t)u * xs_stride;
+            xu::update_level<NT>(m, Q, S, n, base, rg, gctr, tiles_done, tid, wid, lane,
+                                 [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); },
+                                 prof ? ph : nullptr, t0);
         } else if (n) {
             // ------------- recurrent update (tcgen05) -------------
             for (uint32_t q0 = 0; q0 < n; q0 += BM) {

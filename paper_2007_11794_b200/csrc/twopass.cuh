@@ -568,7 +568,8 @@ extern "C" int otflm_twopass_run(OtflmTwopass *p, int32_t mode, double interp_we
                                  int32_t precision, int32_t use_graph, void *stream) {
     if (mode != 0 && mode != 1) { g_detail = "unknown two-pass mode"; return OTFLM_ERR_VALUE; }
     if (mode == 1 && !p->g) { g_detail = "hybrid mode needs the small LM"; return OTFLM_ERR_VALUE; }
-    if (precision < 0 || precision > 3) return OTFLM_ERR_VALUE;
+    if (!prec_ok(precision)) return OTFLM_ERR_VALUE;
+    precision = level_prec(precision);
     if (precision != OTFLM_PREC_FP64 && p->m->d.H > 512) { g_detail = "tensor-core update needs H <= 512"; return OTFLM_ERR_VALUE; }
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t l0 = g_launches;
