@@ -2,15 +2,21 @@
 """On-the-fly RNNLM rescoring benchmark (BASELINE.json metric: decode frames/s
 & RTF; RNNLM (history, word) queries/s per GPU).
 
-Workload at N=1: configs[1] = config (b): synthetic HS+MaxEnt RNNLM
-(V=20,000, H=256, MaxEnt 2^21), 64 utterances x 300 frames (one lattice
-step = one 10 ms frame), breadth 3, beam 8, bigram small LM; one step =
-decoding the whole batch (every frame of every utterance, fresh
-per-utterance streams).  Under torchrun each rank decodes its own 64
-utterances (weak scaling) and NCCL gathers the per-utterance results.
+Default workload (the largest single-GPU configuration, BASELINE.json
+configs[4] / SURVEY.md §8d config e): synthetic HS+MaxEnt RNNLM with
+V=65,536, H=512, MaxEnt 2^22, 4,096 utterances x 300 frames (one lattice
+step = one 10 ms frame), breadth 3, beam 8, bigram small LM, fresh streams
+per utterance.  The utterances are sharded over the ranks (strong scaling:
+the total is fixed); each rank decodes its shard in batches of 74 streams
+(74 two-CTA clusters = 148 SMs) through the double-buffered BatchDecoder, in
+the EXACT precision (integer digit-plane tcgen05 update with certified
+rounding + float64 HS: every hidden state and 1-best bit-identical to the
+reference).  NCCL only all-gathers the per-utterance result records.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--precision P]
-  python bench.py --impl reference      # CPU arm (oracle port, all host cores)
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--precision P] [--config e|b]
+  python bench.py --impl reference      # CPU arm: the reference algorithm on host cores
+
+--gpus N without torchrun re-launches itself under torch.distributed.run.
 """
 
 from __future__ import annotations
@@ -33,6 +39,8 @@ FRAME_S = 0.01          # one lattice step = one 10 ms frame
 CONFIG = "b"
 METRIC = "decode frames/sec (RNNLM on-the-fly rescoring, config b: V=20k H=256 HS+MaxEnt 2^21, " \
          "64 utt x 300 frames, beam 8)"
+METRIC_E = "decode frames/sec (RNNLM on-the-fly rescoring, config e: V=64k H=512 HS+MaxEnt 2^22, " \
+           "4096 utt x 300 frames, beam 8)"
 
 
 def parse():
@@ -41,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--precision", default="tf32x3", choices=["fp64", "tf32x3", "tf32", "bf16"])
+    ap.add_argument("--precision", default="exact", choices=["exact", "fp64", "tf32x3", "tf32", "bf16"])
     ap.add_argument("--n-utt", type=int, default=64)
     ap.add_argument("--frames", type=int, default=300)
     ap.add_argument("--no-graph", action="store_true")
@@ -51,7 +59,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-queries", action="store_true", help="skip the config-d query microbench")
     ap.add_argument("--beam-sweep", action="store_true", help="add the config-c beam sweep extra")
-    ap.add_argument("--config", default="b", choices=["b", "e"],
+    ap.add_argument("--config", default="e", choices=["b", "e"],
                     help="b: the headline config (default); e: 4096 utterances at V=64k sharded over ranks")
     ap.add_argument("--e-total", type=int, default=4096, help="config e: total utterances")
     ap.add_argument("--e-batch", type=int, default=74,
@@ -339,37 +347,101 @@ def cpu_baseline(setup, n_sample: int, threads: int):
     return frames, reqs, dt, res
 
 
+def _ref_lattices(args, threads):
+    """The reference arm's bounded sample of the benchmarked workload."""
+    from paper_2007_11794_b200 import synth
+    if args.config == "e":
+        base = synth.build_setup("e", n_utt=1, T=args.frames, seed=31)
+        n_sample = max(threads, 16)
+        lats = synth.lattices_for_ids(base, range(n_sample), args.frames)
+        base.lattices = lats
+        return base, n_sample, (f"config e: V=65536 H=512 MaxEnt 2^22, utterances 0..{n_sample - 1} of the "
+                                f"{args.e_total}-utterance workload x {args.frames} frames, breadth 3, beam 8")
+    n_sample = min(args.n_utt, max(threads, 16))
+    setup = synth.build_setup(CONFIG, n_utt=n_sample, T=args.frames, seed=7)
+    return setup, n_sample, (f"config {CONFIG}: V=20000 H=256 MaxEnt 2^21, {n_sample} utt x "
+                             f"{args.frames} frames sample of the 64-utt batch, breadth 3, beam 8")
+
+
+def numba_reference_sample(setup, n_frames_cap: int = 300):
+    """The unmodified reference (otflm, numba kernels) from baseline/_ref on
+    one utterance of the workload: rescore_onthefly (decoder.py:114-173) with
+    a fresh RescoreStack, built from the same synthetic arrays.  Returns None
+    when baseline/_ref is absent."""
+    ref_root = ROOT / "baseline" / "_ref"
+    if not (ref_root / "otflm").exists():
+        return None
+    sys.path.insert(0, str(ref_root))
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_otflm")
+    try:
+        from otflm import cache as rc, codec as rcod, context_table as rct, decoder as rdec
+        from otflm import huffman as rh, lattice as rl, ngram as rng_, rnnlm as rr
+        from paper_2007_11794_b200 import synth
+    except Exception as e:                                   # pragma: no cover
+        return {"unavailable": f"import failed: {e}"}
+    m = setup.model
+    model = rr.RnnlmModel(m.hidden_size, m.vocab_size, m.maxent_order, m.maxent_size, m.hash_seed,
+                          m.input_weights, m.recurrent_weights, m.node_vectors, m.maxent_table)
+    tree = rh.build_huffman_from_counts([int(c) for c in synth.zipf_counts(m.vocab_size)])
+    lm = rng_.NgramModel(setup.small_lm.order, setup.small_lm.vocab_size, setup.small_lm.bos_id,
+                         setup.small_lm.eos_id, setup.small_lm.probs, setup.small_lm.backoffs)
+    lat = setup.lattices[0]
+    arcs = [rl.Arc(i, int(lat.arc_src[i]), int(lat.arc_dst[i]), int(lat.arc_word[i]),
+                   float(lat.arc_acoustic[i]), float(lat.arc_smalllm[i])) for i in range(len(lat.arc_word))]
+    rlat = rl.Lattice(lat.start, set(lat.finals), arcs)
+
+    def stack():
+        return rdec.RescoreStack(model=model, tree=tree, table=rct.IndexTable(m.hidden_size, m.maxent_order),
+                                 cache=rc.RescoreCache(), ledger=rcod.TransferLedger())
+    # JIT warm-up (numba compiles or loads its cache) on a short prefix
+    short = [a for a in arcs if rlat.times.get(a.dst, 0) <= 3]
+    ends = {a.dst for a in short if rlat.times.get(a.dst, 0) == 3}
+    if short and ends:
+        rdec.rescore_onthefly(rl.Lattice(lat.start, ends, short), lm, stack(), beam=setup.beam)
+    t0 = time.perf_counter()
+    hyp, rep = rdec.rescore_onthefly(rlat, lm, stack(), beam=setup.beam)
+    dt = time.perf_counter() - t0
+    frames = len(hyp.arcs)
+    return {"value": frames / dt, "unit": "frames/s", "cores": 1, "kind": "reference",
+            "sample": f"utterance 0 ({frames} frames, {rep.expansions} requests) through the unmodified "
+                      "reference otflm.decoder.rescore_onthefly (numba kernels, one thread), baseline/_ref",
+            "seconds": dt, "requests_per_s": rep.expansions / dt,
+            "one_best": list(hyp.arcs)}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2007_11794_b200 import synth
     threads = len(os.sched_getaffinity(0))
-    n_sample = min(args.n_utt, max(threads, 16))
-    setup = synth.build_setup(CONFIG, n_utt=n_sample, T=args.frames, seed=7)
+    setup, n_sample, workload = _ref_lattices(args, threads)
     times = []
     frames = reqs = 0
+    res = None
     for i in range(args.warmup + args.steps):
-        f, r, dt, _ = cpu_baseline(setup, n_sample, threads)
+        f, r, dt, res = cpu_baseline(setup, n_sample, threads)
         if i >= args.warmup:
             times.append(dt)
             frames, reqs = f, r
     t = float(np.mean(times))
     v = frames / t
+    numba = numba_reference_sample(setup)
+    if numba and "one_best" in numba:
+        numba["one_best_equals_port"] = numba.pop("one_best") == list(res[0][0].arcs)
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "frames/s",
+        "impl": "reference", "metric": METRIC_E if args.config == "e" else METRIC, "value": v, "unit": "frames/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong" if args.config == "e" else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config {CONFIG}: V=20000 H=256 MaxEnt 2^21, {n_sample} utt x "
-                               f"{args.frames} frames sample of the 64-utt batch, breadth 3, beam 8",
-                   "n_utt": n_sample, "frames": args.frames},
+        "config": {"workload": workload, "n_utt": n_sample, "frames": args.frames},
         "rtf": (t / (frames * FRAME_S)),
         "queries_per_s": reqs / t,
         "cpu_baseline": {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
-                         "sample": f"{n_sample} utterances x {args.frames} frames per step, "
-                                   "oracle/otflm_oracle.c (C restatement of the reference "
-                                   "decoder; numba/Python reference is not shipped)"},
+                         "sample": f"{n_sample} utterances x {args.frames} frames per step through "
+                                   "oracle/otflm_oracle.c (the reference decoder restated in C, bit-exact with "
+                                   "the reference's golden vectors), fresh stream per utterance, "
+                                   f"{threads} threads"},
+        "numba_reference": numba,
         "e2e": {"value": v, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -386,17 +458,26 @@ def _e_lattices(ids):
     return synth.lattices_for_ids(base, ids, frames)
 
 
+def _alg_bytes(H: int, cnt: dict, misses: int, requests: int) -> float:
+    """SURVEY.md §8d algorithmic bytes of one decode: HS per query
+    P(4H + 4k + 8) + 4H + 16, the recurrent update 3 x 4H per computed
+    context (h_c and U[w] read, h' written), ~96 B of request / arrival /
+    cache state per request."""
+    hs = cnt["sum_path"] * (4 * H + 8) + 4 * cnt["sum_path_k"] + cnt["hs_queries"] * (4 * H + 16)
+    return float(hs + 12.0 * H * misses + 96.0 * requests)
+
+
 def run_config_e(args):
     """Config (e): 4,096 utterances (V=65,536, H=512, MaxEnt 2^22, 300
-    frames, breadth 3, beam 8) sharded over the ranks (utterance i of rank r's
-    contiguous shard, parallel.shard); each rank decodes its shard in batches
-    of --n-utt streams through the double-buffered BatchDecoder (host compile
-    + H2D of batch i+1 overlap the decode of batch i), then NCCL all-gathers
-    the per-utterance result records.  One step = the whole shard; strong
-    scaling (total work fixed)."""
+    frames, breadth 3, beam 8) sharded over the ranks (parallel.shard); each
+    rank decodes its shard in batches of --e-batch streams through the
+    double-buffered BatchDecoder (host compile + H2D of batch i+1 overlap the
+    decode of batch i), then NCCL all-gathers the per-utterance result
+    records.  One step = the whole shard; strong scaling (total work fixed)."""
     import torch
     import torch.distributed as dist
     from paper_2007_11794_b200 import parallel, synth
+    from paper_2007_11794_b200.device import last_launch_count
     from paper_2007_11794_b200.rescore import BatchDecoder
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -405,6 +486,7 @@ def run_config_e(args):
     ids = parallel.shard(n_total, world, rank)
     B = args.e_batch
     base = synth.build_setup("e", n_utt=1, T=args.frames, seed=31)
+    H = base.model.hidden_size
     # lattices of this rank's shard, generated on host worker processes
     # (forked before CUDA is initialised; each lattice is a function of its id)
     t0 = time.perf_counter()
@@ -432,51 +514,56 @@ def run_config_e(args):
     dec = BatchDecoder(base.model, base.tree, base.small_lm, B, need, precision=args.precision,
                        schedule=args.schedule, n_buffers=2)
     stream = torch.cuda.current_stream()
+    launches = [0]
 
     def one_pass(record: bool):
-        """decode the shard: device time (sum of batch decodes) and e2e."""
-        dev_ms = 0.0
+        """decode the shard: device time (sum of the batch decodes) and e2e."""
         recs = []
-        frames = 0
+        frames = requests = misses = 0
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
         s_prev, prev_sel = None, None
         evs = []
-        for sel, lats in batches:
-            s_cur = dec.prepare(lats, base.beam)          # host compile + H2D (overlaps the previous decode)
+        h2d = d2h = 0
+
+        def take(slot, sel_):
+            nonlocal frames, requests, misses, d2h
+            hyps, out = dec.fetch(slot=slot)
+            n = len(sel_)
+            frames += int(sum(len(h.arcs) for h in hyps[:n]))
+            requests += int(out["expansions"][:n].sum())
+            d2h += int(sum(v.nbytes for v in out.values()))
+            if record:
+                recs.append(parallel.pack_records(sel_, {k: v[:n] for k, v in out.items()}, args.frames))
+        for sel_, lats_ in batches:
+            s_cur = dec.prepare(lats_, base.beam)         # host compile + pinned H2D (overlaps the previous decode)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             dec.run(1.0, slot=s_cur)
             e1.record(stream)
+            launches[0] += last_launch_count()
             evs.append((e0, e1))
             if s_prev is not None:
-                hyps, out = dec.fetch(slot=s_prev)
-                frames += int(sum(len(h.arcs) for h in hyps[:len(prev_sel)]))
-                if record:
-                    recs.append(parallel.pack_records(prev_sel, {k: v[:len(prev_sel)] for k, v in out.items()},
-                                                      args.frames))
-            s_prev, prev_sel = s_cur, sel
-        hyps, out = dec.fetch(slot=s_prev)
-        frames += int(sum(len(h.arcs) for h in hyps[:len(prev_sel)]))
-        if record:
-            recs.append(parallel.pack_records(prev_sel, {k: v[:len(prev_sel)] for k, v in out.items()},
-                                              args.frames))
+                take(s_prev, prev_sel)
+            s_prev, prev_sel = s_cur, sel_
+        take(s_prev, prev_sel)
         b.record(stream)
         torch.cuda.synchronize()
         dev_ms = sum(x.elapsed_time(y) for x, y in evs)
-        return dev_ms, a.elapsed_time(b), frames, recs
+        return dev_ms, a.elapsed_time(b), frames, requests, d2h, recs
 
     for _ in range(args.warmup):
         one_pass(False)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    dev, e2e, fr = [], [], 0
+    launches[0] = 0
+    dev, e2e = [], []
     with Clocks(local) as clk:
         for i in range(args.steps):
-            d_ms, e_ms, fr, recs = one_pass(i == args.steps - 1)
+            d_ms, e_ms, fr, rq, d2h, recs = one_pass(i == args.steps - 1)
             dev.append(d_ms)
             e2e.append(e_ms)
     dev_ms, e2e_ms = float(np.mean(dev)), float(np.mean(e2e))
@@ -488,6 +575,43 @@ def run_config_e(args):
     else:
         allr = np.concatenate(recs)
     total_frames = int(allr[:, 1].sum())
+    total_requests = int(allr[:, 6].sum())
+    # ---- roofline of the persistent decode kernel: one profiled batch
+    # (event-record nodes around every kernel) gives the algorithmic-work
+    # counters and the kernel's share of a decode run ----
+    s_last = dec.prepare(batches[0][1], base.beam)
+    prof = dec.profile(1.0)
+    cnt = dec.counters()
+    phases = dec.plan.phase_ns()
+    hyps0, out0 = dec.fetch(slot=s_last)
+    st0 = dec.streams.stats()
+    req0, miss0 = int(out0["expansions"].sum()), int(st0[:, 2].sum())
+    byt0 = _alg_bytes(H, cnt, miss0, req0)
+    run_ms = sum(v[0] for v in prof.values())
+    share = prof["stream"][0] / run_ms if "stream" in prof and run_ms > 0 else 1.0
+    n_batches = len(batches)
+    kern_ms = dev_ms / n_batches * share                  # avg k_decode_streams launch, timed region
+    byt = byt0 * (total_requests / world / n_batches) / max(req0, 1)   # per launch, scaled to the timed batches
+    hbm, tc_peak, peak_src = peaks()
+    roof = {"kernel": "k_decode_streams (persistent: expand + tcgen05 digit-plane update + f64 HS + assign)",
+            "bound": "hbm", "achieved": byt / (kern_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "traffic": None, "peak_source": peak_src, "avg_launch_us": kern_ms * 1e3,
+            "algorithmic_bytes_per_launch": byt, "launches_per_step": n_batches,
+            "kernel_share_of_decode_run": share,
+            "tensor_int8_tops": 17 * 2.0 * H * H * miss0 / (prof.get("stream", (run_ms, 1))[0] / 1e3) / 1e12}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    tfile = ROOT / "profiles" / "traffic.json"
+    key = f"k_decode_streams_e_{args.precision}"
+    if tfile.exists():
+        try:
+            tj = json.loads(tfile.read_text()).get(key)
+            if tj:
+                roof["traffic"] = tj["dram_bytes_per_launch"] * (byt / tj["algorithmic_bytes_per_launch"])
+                roof["traffic_source"] = tj["source"]
+        except (KeyError, ValueError, ZeroDivisionError):
+            pass
+    nl = max(1, args.frames)
+    ph = {k: round(v / max(phases["ctas"], 1) / nl / 1e3, 3) for k, v in phases.items() if k != "ctas"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from types import SimpleNamespace
@@ -495,29 +619,44 @@ def run_config_e(args):
         n_sample = max(threads, 16)
         sample = SimpleNamespace(model=base.model, tree=base.tree, small_lm=base.small_lm,
                                  beam=base.beam, lattices=batches[0][1][:n_sample])
-        f, r, dt, _ = cpu_baseline(sample, n_sample, threads)
+        f, r, dt, ref = cpu_baseline(sample, n_sample, threads)
+        agree = sum(1 for u in range(n_sample) if tuple(hyps0[u].arcs) == tuple(ref[u][0].arcs))
         cpu = {"value": f / dt, "unit": "frames/s", "cores": threads, "kind": "port",
                "sample": f"the first {n_sample} utterances of the shard x {args.frames} frames "
-                         "(oracle/otflm_oracle.c, all host threads)"}
+                         "(oracle/otflm_oracle.c, all host threads)",
+               "one_best_agreement": f"{agree}/{n_sample}"}
+    extras = {}
+    if rank == 0 and not args.no_queries:
+        extras["config_d_queries"] = query_microbench("exact" if args.precision == "exact" else args.precision)
     if rank == 0:
         line = {
-            "metric": "decode frames/sec (RNNLM on-the-fly rescoring, config e: V=64k H=512, 4096 utt x 300 frames, beam 8)",
+            "metric": METRIC_E,
             "value": total_frames / (dev_ms / 1e3), "unit": "frames/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64 scores / f32 weights / " + args.precision + " recurrent update",
-            "data": "synthetic (seeded per utterance id)",
+            "dtype": "u8 digit planes / s32 accumulation / f64 scores (exact)" if args.precision == "exact"
+                     else "f64 scores / f32 weights / " + args.precision + " recurrent update",
+            "data": "synthetic (seeded per utterance id; RnnlmModel.new recipe + Zipf Huffman + synthetic bigram)",
             "config": {"workload": f"config e: V=65536 H=512 MaxEnt 2^22, {n_total} utterances x {args.frames} "
                                    f"frames sharded over {world} GPU(s), batches of {B} streams, breadth 3, beam 8",
                        "n_utt_total": n_total, "batch_streams": B, "precision": args.precision,
-                       "schedule": dec.schedule, "lattice_generation_s": t_gen,
-                       "l2": "inputs (4096 lattices, arenas) far larger than L2"},
+                       "schedule": dec.schedule, "lattice_generation_s": round(t_gen, 2),
+                       "l2": "inputs (4096 lattices, arenas, 280 MB of weights) far larger than L2; not flushed"},
             "rtf": (dev_ms / 1e3) / (total_frames * FRAME_S),
-            "rtf_per_stream": (dev_ms / 1e3) / len(batches) / (args.frames * FRAME_S),
+            "rtf_per_stream": (dev_ms / 1e3) / n_batches / (args.frames * FRAME_S),
+            "requests_per_s": total_requests / (dev_ms / 1e3),
             "utterances_gathered": int(len(allr)),
+            "roofline": roof,
+            "stream_phase_us_per_level": ph,
+            "exact_uncertified_elements_per_batch": cnt.get("exact_fallbacks"),
             "e2e": {"value": total_frames / (e2e_ms / 1e3), "unit": "frames/s", "ms_per_step": e2e_ms,
-                    "pipeline": "double-buffered batches: host compile + pinned H2D of batch i+1 overlap the decode of batch i; 1-best D2H per batch"},
+                    "h2d_bytes_per_step": int(cnt["h2d_bytes"] * n_batches),
+                    "d2h_bytes_per_step": int(d2h),
+                    "pipeline": "double-buffered batches through the public BatchDecoder API: host compile + "
+                                "pinned H2D of batch i+1 overlap the decode of batch i; 1-best D2H per batch"},
+            "gpu_launches": int(launches[0]),
             "clocks": clk.summary(),
+            "extras": extras,
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
@@ -529,14 +668,38 @@ def run_config_e(args):
         dist.destroy_process_group()
 
 
+def _self_launch(args) -> bool:
+    """--gpus N outside torchrun: re-run this command under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous)."""
+    world = os.environ.get("WORLD_SIZE")
+    if world is not None:
+        if int(world) != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return False
+    if args.gpus <= 1:
+        return False
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    sys.exit(subprocess.run(cmd).returncode)
+
+
 def main():
     args = parse()
+    _self_launch(args)
     if args.impl == "reference":
         run_reference(args)
         return
     if args.config == "e":
         run_config_e(args)
         return
+    run_config_b(args)
+
+
+def run_config_b(args):
     import torch
     import torch.distributed as dist
 
@@ -728,6 +891,7 @@ def main():
         "queries_per_s": misses * world / (ms / 1e3),
         "requests_per_s": requests * world / (ms / 1e3),
         "kernel_ms_per_step": kernel_ms,
+        "exact_uncertified_elements_per_step": cnt.get("exact_fallbacks"),
         "stream_phase_us_per_level": phases,
         "roofline": roof,
         "e2e": {"value": frames_per_step * world / (e2e / 1e3), "unit": "frames/s",

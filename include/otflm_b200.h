@@ -259,10 +259,12 @@ int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *lats, int32_t *sam
 /* plan stats: levels, nodes, arcs, slots, max requests per level, total
  * request slots, graph nodes (int64 [8]) */
 int otflm_plan_info(const OtflmPlan *p, int64_t *out8);
-/* Algorithmic-work counters of the last run + upload size (int64 [4]):
+/* Algorithmic-work counters of the last profiled run + upload size (int64 [5]):
  * sum of Huffman path lengths over HS queries, sum of path length x MaxEnt
- * orders, HS queries, bytes uploaded by plan_create. */
-int otflm_plan_counters(const OtflmPlan *p, int64_t *out4, void *stream);
+ * orders, HS queries, bytes uploaded by plan_create, and (OTFLM_PREC_EXACT)
+ * hidden-state elements whose rounding could not be certified and ran the
+ * reference's sequential loop. */
+int otflm_plan_counters(const OtflmPlan *p, int64_t *out5, void *stream);
 /* One decode run captured as a CUDA graph with an event-record node around
  * every kernel; writes device-side total ms / launch counts per category
  * (7 entries: expand, hs, advance, assign, final, misc, stream).  HS and the
@@ -289,8 +291,11 @@ int otflm_plan_set_schedule(OtflmPlan *p, int32_t schedule);
  * o[2] MMA drain, o[3] update epilogue, o[4] HS setup + row staging,
  * o[5] HS pair rounds, o[6] whole HS group (small-LM scores + HS; runs
  * concurrently with o[1..3]), o[7] assign, o[8] wait of the update group for
- * the HS group, o[9] MMA-warp wait for operands, o[10] 0, o[11] CTAs,
- * o[12..16] assign sections (probe, dedup scan, numbering, values, arrivals): 17 entries. */
+ * the HS group, o[9] MMA-warp wait for operands, o[10] uncertified-element
+ * loop (OTFLM_PREC_EXACT), o[11] CTAs, o[12..16] assign sections (probe, dedup
+ * scan, numbering, values, arrivals), o[17..20] EXACT update: row table,
+ * digitize, 2 spare: 21 entries.  (EXACT: o[1] is the digitize barrier,
+ * o[2] the digit-pair K loops.) */
 int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream);
 int otflm_schedule_supported(const OtflmModel *m, int32_t schedule, int32_t precision);
 int otflm_group_create(OtflmPlan **plans, int32_t n, OtflmGroup **out);

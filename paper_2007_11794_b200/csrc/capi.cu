@@ -223,12 +223,12 @@ extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, Otflm
             const int nkx = (H + xu::KC - 1) / xu::KC;
             uint8_t *Wd = nullptr;
             double4 *wx = nullptr;
-            const size_t nwd = (size_t)(np / tc::BM) * nkx * 4 * xu::PLANE_W;
+            const size_t nwd = (size_t)(np / tc::BM) * nkx * xu::NPW * xu::PLANE_W;
             if (m->mem.alloc(&Wd, nwd) != cudaSuccess || m->mem.alloc(&wx, (size_t)H) != cudaSuccess) {
                 m->mem.free_all(); delete m; g_detail = "cudaMalloc model"; return OTFLM_ERR_NOMEM;
             }
             CK(cudaMemset(Wd, 0, nwd));
-            k_prep_wdigits<<<H, 256>>>(W, H, nkx, Wd, wx);
+            k_prep_wdigits<<<H, 256>>>(W, U, V, H, nkx, Wd, wx);
             CK(cudaGetLastError());
             dm.Wd = Wd; dm.wx = wx; dm.wd_nkx = nkx;
         }
@@ -1414,6 +1414,7 @@ extern "C" int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream)
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     for (int i = 0; i < 12; i++) o[i] = (int64_t)a[i];
     for (int i = 0; i < 5; i++) o[12 + i] = (int64_t)a[16 + i];
+    for (int i = 0; i < 4; i++) o[17 + i] = (int64_t)a[12 + i];   // EXACT update: row table, digitize, spare
     return OTFLM_OK;
 }
 
@@ -1424,6 +1425,7 @@ extern "C" int otflm_plan_counters(const OtflmPlan *p, int64_t *o, void *stream)
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     o[0] = (int64_t)a[0]; o[1] = (int64_t)a[1]; o[2] = (int64_t)a[2];
     o[3] = (int64_t)p->h2d_bytes;
+    o[4] = (int64_t)a[3];
     return OTFLM_OK;
 }
 
@@ -1511,7 +1513,7 @@ static bool sd_config(const DevModel &m, int prec, SdConfig *c) {
     if (prec == OTFLM_PREC_EXACT) {
         if (!m.Wd || m.H % 4 != 0 || m.H > 512 || !m.U || !m.NV || !m.path_off) return false;
         const size_t budget = 200u * 1024u;
-        const size_t tail = 2u * xu::FBCAP * 4 + 2u * xu::XR * 8 + 16;
+        const size_t tail = 2u * xu::FBCAP * 4 + 2u * xu::XR * 8 + 8 + 2u * xu::XR * 4 + 32 * 8 + 16;
         c->stages = (int)std::min<size_t>(4, (budget - tail) / xu::STAGE);
         if (c->stages < 2) return false;
         const int ord = m.order <= 3 ? 3 : OTF_MAX_ORDER;

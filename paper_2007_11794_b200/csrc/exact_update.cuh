@@ -3,14 +3,17 @@
 // on tcgen05 integer tensor cores.
 //
 // Digit planes.  Every W row i gets a power-of-two scale sW_i > max_j |W_ij|
-// and X_ij = rint(W_ij / sW_i * 2^31) in four 8-bit planes (top plane signed,
-// lower planes unsigned): W_ij ~ sW_i (d0 2^-7 + u1 2^-15 + u2 2^-23 + u3 2^-31).
-// Every context row r gets sH_r = 2^e > max_j h_rj and Y_rj = rint(h_rj / sH_r
-// * 2^32) in four unsigned planes.  A digit pair (a, b) carries the weight
-// sW sH 2^-(15 + 8(a + b)); the 13 pairs with a + b <= 4 are accumulated by
-// `tcgen05.mma.kind::i8` into five int32 anti-diagonal accumulators D_s
-// (s = a + b) -- exactly, |D_s| < 2^28 -- and combined once in float64:
-//   x~ = U + sW sH 2^-47 (D0 2^32 + D1 2^24 + D2 2^16 + D3 2^8 + D4).
+// and X_ij = rint(W_ij / sW_i * 2^39) in five 8-bit planes (top plane signed,
+// lower planes unsigned): W_ij ~ sW_i (d0 2^-7 + u1 2^-15 + ... + u4 2^-39),
+// exact for |W_ij| >= 2^-15 sW_i.
+// Every context row r (a sigmoid output in [0, 1), or the zero context) has
+// Y_rj = rint(h_rj 2^32) in four unsigned planes (sH_r = 1; exact for
+// h >= 2^-9, the rest is carried by the error bound).  A digit pair (a, b) carries the weight
+// sW sH 2^-(15 + 8(a + b)); the 17 pairs with a + b <= 5 are accumulated by
+// `tcgen05.mma.kind::i8` into six int32 anti-diagonal accumulators D_s
+// (s = a + b) -- exactly, |D_s| < 2^28 -- and combined once:
+//   x~ = U + sW sH (T_hi 2^-31 + T_lo 2^-55),
+//   T_hi = D0 2^16 + D1 2^8 + D2,  T_lo = D3 2^16 + D4 2^8 + D5  (int64, exact).
 // One MMA serves several pairs: the h planes sit in shared memory as
 // consecutive row blocks [e0 | e1 | e2 | e3], so the MMA of W plane a over the
 // row blocks b = 0..nb-1 writes TMEM column blocks s = a..a+nb-1 -- the
@@ -23,8 +26,8 @@
 // candidate y = rcp(1 + exp(-x~)) is accepted only if sigmoid over
 // [x~ - eps, x~ + eps] provably stays strictly between the two f32 rounding
 // midpoints around y (checked as z m - 1 against the margin, z = 1 + e^-x).
-// Elements that cannot be certified (~0.2-0.4 %) are recomputed by the
-// reference's own sequential float64 loop and sigmoid.  So every h' equals
+// Elements that cannot be certified (~1e-5 of them) are recomputed by the
+// reference's own sequential float64 loop and sigmoid (a warp per element).  So every h' equals
 // the reference's float32 result; the content dedup (context_table.py:74-86)
 // then merges exactly the contexts the reference merges.
 #pragma once
@@ -32,7 +35,9 @@
 
 namespace xu {
 constexpr int KC = 64;                 // bytes (= int8 elements) of K per ring stage
-constexpr int XR = 96;                 // context rows per chunk: 5 accumulators x 96 columns <= 512
+constexpr int NDIAG = 6;               // anti-diagonals s = a + b <= 5 (17 digit pairs)
+constexpr int NPW = 5;                 // W digit planes (h: 4)
+constexpr int XR = 80;                 // context rows per chunk: 6 accumulators x 80 columns <= 512
 constexpr int PLANE_W = tc::BM * KC;   // one W plane block (128 rows x 64 B)
 constexpr int FBCAP = 1024;            // deferred fallback elements per M tile
 
@@ -91,27 +96,56 @@ __device__ __noinline__ float ref_element(const float *__restrict__ wrow, const 
     return (float)otf_sigmoid(acc);
 }
 
-// Certified float32 rounding of sigmoid(x) for |x - x_ref| <= eps.  Returns
-// false when the interval may straddle a rounding midpoint.
-__device__ __forceinline__ bool certify(double x, double eps, float &out) {
-    const double z = 1.0 + exp(-x);
-    if (!(z < 1e300) || !(eps < 1e-3)) return false;        // non-finite / no useful bound
-    const double dl = eps * 1.0001 + 2.0e-15;               // + exp, sigmoid and fma roundings
-    float y = __frcp_rn(__double2float_rn(z));
-#pragma unroll 1
-    for (int it = 0; it < 3; it++) {
-        const uint32_t yb = __float_as_uint(y);
-        if (yb < 0x00800000u || yb >= 0x3F800000u) return false;   // keep to normal (0, 1)
-        const double yd = (double)y;
-        const double m_lo = 0.5 * (yd + (double)__uint_as_float(yb - 1));
-        const double m_hi = 0.5 * (yd + (double)__uint_as_float(yb + 1));
-        const double t_lo = fma(z, m_lo, -1.0), t_hi = fma(z, m_hi, -1.0);
-        if (t_lo < -dl && t_hi > dl) { out = y; return true; }
-        if (t_lo > dl) { y = __uint_as_float(yb - 1); continue; }   // sigmoid below the lower midpoint
-        if (t_hi < -dl) { y = __uint_as_float(yb + 1); continue; }  // above the upper midpoint
-        return false;                                            // within the margin of a midpoint
-    }
-    return false;
+// e^-x for |x| <= 700: k = rint(-32 x log2 e), r = -x - k ln2/32 (Cody-Waite,
+// ln2_hi has 11 trailing zero bits so k ln2_hi/32 is exact), e^-x =
+// 2^(k>>5) * tab[k & 31] * e^r with tab[j] = 2^(j/32) and e^r by its degree-6
+// Taylor polynomial (|r| <= ln2/64: truncation < 4e-18).  Relative error
+// ~1e-16, well inside the certification margin, in 12 float64 operations.
+__device__ __forceinline__ double exp_neg(double x, const double *__restrict__ tab) {
+    const double t = x * -46.166241308446828;                 // -32 log2(e) x
+    const double sh = t + 6755399441055744.0;
+    const int k = __double2loint(sh);
+    const double kd = sh - 6755399441055744.0;
+    double r = fma(kd, -0.021660849386535119265, -x);         // ln2_hi / 32
+    r = fma(kd, -5.9631716539705865626e-12, r);               // ln2_lo / 32
+    double p = 1.0 / 720.0;
+    p = fma(p, r, 1.0 / 120.0);
+    p = fma(p, r, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r, 1.0);
+    p = fma(p, r, 1.0);
+    p *= tab[k & 31];
+    return __hiloint2double(__double2hiint(p) + ((k >> 5) << 20), __double2loint(p));
+}
+
+// Certified float32 rounding of sigmoid(x) (branch free, so the elements of
+// a row group interleave).  epsm = the x error bound (|x - x_ref| <= eps) x
+// 1.0001 + 2e-15 for the exp, Newton and the reference's own float64
+// sigmoid roundings, all relative to sigmoid.  h = 1/(1 + e^-x) to ~1 f64 ulp
+// (hardware reciprocal seed + two Newton steps); y = the float nearest h;
+// d = h - y is exact.  sigmoid(x_ref), and the reference's float64 sigmoid
+// of x_ref, round to y if |d| + epsm h stays inside the half gap to the
+// neighbouring float on d's side (a quarter gap below a power of two).
+// Returns false otherwise, or for |x| >= 60 / y outside the normal (0, 1).
+__device__ __forceinline__ bool certify(double x, double epsm, const double *__restrict__ tab, float &out) {
+    const double z = 1.0 + exp_neg(x, tab);
+    double h;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(h) : "d"(z));
+    h = fma(h, fma(-z, h, 1.0), h);
+    h = fma(h, fma(-z, h, 1.0), h);
+    const float y = __double2float_rn(h);
+    const uint32_t yb = __float_as_uint(y);
+    const double d = h - (double)y;
+    // half gap above y: 2^(E_y - 24); below: the same, halved at a power of two
+    const uint32_t ey = (yb >> 23) & 255u;
+    const int hw = (int)((ey + 1023u - 127u - 24u) << 20);
+    const double half_up = __hiloint2double(hw, 0);
+    const double half_dn = __hiloint2double((yb & 0x7FFFFFu) ? hw : hw - (1 << 20), 0);
+    const double margin = epsm * h;
+    out = y;
+    const bool ok = d >= 0.0 ? d + margin < half_up : margin - d < half_dn;
+    return ok && fabs(x) < 60.0 && ey >= 1u && yb < 0x3F800000u;
 }
 }  // namespace xu
 
@@ -119,15 +153,18 @@ __device__ __forceinline__ bool certify(double x, double eps, float &out) {
 // model preparation (once per model upload)
 // --------------------------------------------------------------------------
 // per unit i (block per row): planes into the pre-tiled layout
-// Wd[mt][kc][a][128 rows x 64 B] and the float64 constants
-// wx[i] = {sW 2^-47, A_i, B_i, sW}.
-__global__ void k_prep_wdigits(const float *__restrict__ W, int H, int nkx, uint8_t *__restrict__ Wd,
-                               double4 *__restrict__ wx) {
+// Wd[mt][kc][a < 5][128 rows x 64 B] and the float64 constants
+// wx[i] = {sW 2^-31, epsm_i, B_i, sW 2^-55}: the certification margin of
+// unit i is epsm_i + B_i eH_r (relative to sigmoid).
+__global__ void k_prep_wdigits(const float *__restrict__ W, const float *__restrict__ U, int V, int H, int nkx,
+                               uint8_t *__restrict__ Wd, double4 *__restrict__ wx) {
     const int i = blockIdx.x;
     if (i >= H) return;
     const float *row = W + (size_t)i * H;
     __shared__ float s_max[32];
     __shared__ double s_sum[4][32];
+    // (the h-representation term of the bound is B_i * sum_j |dh_j| with
+    // B_i = max_j |W_ij| -- only the few elements below 2^-9 carry dh)
     float mx = 0.f;
     for (int j = threadIdx.x; j < H; j += blockDim.x) mx = fmaxf(mx, fabsf(row[j]));
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -140,32 +177,44 @@ __global__ void k_prep_wdigits(const float *__restrict__ W, int H, int nkx, uint
     }
     __syncthreads();
     mx = s_max[0];
+    // max_w |U[w, i]| (the reference's sum starts from U: rounding bound)
+    float mu = 0.f;
+    if (U) for (int w = threadIdx.x; w < V; w += blockDim.x) mu = fmaxf(mu, fabsf(U[(size_t)w * H + i]));
+    for (int o = 16; o; o >>= 1) mu = fmaxf(mu, __shfl_xor_sync(0xffffffffu, mu, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) s_max[2 + (threadIdx.x >> 5)] = mu;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float v = 0.f;
+        for (int wv = 0; wv < (int)(blockDim.x >> 5); wv++) v = fmaxf(v, s_max[2 + wv]);
+        s_max[1] = v;
+    }
+    __syncthreads();
     int e = 0;                                   // sW = 2^e > max |W_ij|
     if (mx > 0.f) { frexpf(mx, &e); }             // mx = f * 2^e, f in [0.5, 1)
     const double sW = ldexp(1.0, e);
     const int mt = i / tc::BM, r = i % tc::BM;
-    double sum_w = 0.0, err_w = 0.0, s2 = 0.0, s3 = 0.0;
+    double sum_w = 0.0, err_w = 0.0, s3 = 0.0, s4 = 0.0;
     for (int j = threadIdx.x; j < nkx * xu::KC; j += blockDim.x) {
-        int d0 = 0, u1 = 0, u2 = 0, u3 = 0;
+        int dg[xu::NPW] = {0, 0, 0, 0, 0};
         if (j < H) {
             const double w = (double)row[j];
-            const long long X = llrint(ldexp(w, 31 - e));           // |X| < 2^31
-            d0 = (int)(X >> 24);
-            const long long R = X - ((long long)d0 << 24);
-            u1 = (int)(R >> 16); u2 = (int)((R >> 8) & 255); u3 = (int)(R & 255);
+            const long long X = llrint(ldexp(w, 39 - e));           // |X| < 2^39
+            const long long d0 = X >> 32;
+            const long long R = X - (d0 << 32);                      // [0, 2^32)
+            dg[0] = (int)d0; dg[1] = (int)(R >> 24); dg[2] = (int)((R >> 16) & 255);
+            dg[3] = (int)((R >> 8) & 255); dg[4] = (int)(R & 255);
             sum_w += fabs(w);
-            err_w += fabs(ldexp((double)X, e - 31) - w);
-            s2 += u2; s3 += u3;
+            err_w += fabs(ldexp((double)X, e - 39) - w);
+            s3 += dg[3]; s4 += dg[4];
         }
         const int kc = j / xu::KC, kk = j % xu::KC;
-        const size_t blk = ((size_t)mt * nkx + kc) * 4;
+        const size_t blk = ((size_t)mt * nkx + kc) * xu::NPW;
         const uint32_t o = xu::toff(r, kk >> 4) + (kk & 15);
-        Wd[(blk + 0) * xu::PLANE_W + o] = (uint8_t)(int8_t)d0;
-        Wd[(blk + 1) * xu::PLANE_W + o] = (uint8_t)u1;
-        Wd[(blk + 2) * xu::PLANE_W + o] = (uint8_t)u2;
-        Wd[(blk + 3) * xu::PLANE_W + o] = (uint8_t)u3;
+#pragma unroll
+        for (int a = 0; a < xu::NPW; a++) Wd[(blk + a) * xu::PLANE_W + o] = (uint8_t)dg[a];
     }
-    double v4[4] = {sum_w, err_w, s2, s3};
+    double v4[4] = {sum_w, err_w, s3, s4};
 #pragma unroll
     for (int k = 0; k < 4; k++)
         for (int o = 16; o; o >>= 1) v4[k] += __shfl_xor_sync(0xffffffffu, v4[k], o);
@@ -176,14 +225,16 @@ __global__ void k_prep_wdigits(const float *__restrict__ W, int H, int nkx, uint
         double t[4] = {0, 0, 0, 0};
         for (int wv = 0; wv < (int)(blockDim.x >> 5); wv++)
             for (int k = 0; k < 4; k++) t[k] += s_sum[k][wv];
-        // dropped pairs (2,3), (3,2), (3,3): |D_ab| <= (sum_j |w_a|) * 255
-        const double drop = 255.0 * (t[2] * ldexp(1.0, -55) + t[3] * ldexp(1.0, -55) + t[3] * ldexp(1.0, -63));
+        // dropped pairs (3,3), (4,2), (4,3): |D_ab| <= (sum_j |w_a|) * 255
+        const double drop = 255.0 * (t[2] * ldexp(1.0, -63) + t[3] * ldexp(1.0, -63) + t[3] * ldexp(1.0, -71));
         const double c1 = (double)(H + 8) * ldexp(1.0, -53) * 1.01;   // sequential-sum rounding
+        // (context rows are scaled by sH = 1: sum_j |W_ij h_j| <= sum_j |W_ij|)
+        const double eps = (drop * sW + t[1]) * 1.01 + c1 * (t[0] + (double)s_max[1]) * 1.01;
         double4 o;
-        o.x = ldexp(sW, -47);
-        o.y = (drop * sW + t[1]) * 1.01 + c1 * t[0] * 1.01;         // coefficient of sH_r
-        o.z = t[0] * 1.01;                                           // coefficient of eH_r (max |dh|)
-        o.w = sW;
+        o.x = ldexp(sW, -31);
+        o.y = eps * 1.0001 + 2.0e-15;                               // epsm without the h term
+        o.z = (double)mx * 1.01 * 1.0001;                            // coefficient of eH_r (sum |dh|)
+        o.w = ldexp(sW, -55);
         wx[i] = o;
     }
 }
@@ -197,7 +248,7 @@ __global__ void k_prep_wdigits(const float *__restrict__ W, int H, int nkx, uint
 // (warp 1 bulk-copies the W and h plane blocks of each 64-byte K chunk into
 // the ring, warp 0 issues the digit-pair MMAs) and the epilogue of all warps
 // (combine, certify, store, digest); uncertified elements are recomputed by
-// the reference loop after the tile.
+// the reference loop after the tile, a warp per element.
 // --------------------------------------------------------------------------
 namespace xu {
 struct Ring {
@@ -207,11 +258,63 @@ struct Ring {
     uint64_t *full, *empty, *done;
     uint32_t *fb;                  // [2][FBCAP] deferred fallback elements (row << 16 | unit)
     uint32_t *fb_n;                // [2]
-    double *sh, *eh;               // [XR] per chunk row: scale sH, max |dh|
+    double *sh, *eh;               // [XR] per chunk row: scale sH, sum_j |dh_j|
+    int32_t *src;                  // [XR] per chunk row: its source context's arena row
+    int32_t *wrd;                  // [XR] per chunk row: its word x H (U row offset)
+    const double *tab;             // [32] 2^(j/32) for exp_neg
     uint8_t *xs;                   // this stream's global digit scratch
 };
-constexpr uint32_t STAGE = 4u * PLANE_W + 4u * XR * KC;
-constexpr uint32_t HOFF = 4u * PLANE_W;
+constexpr uint32_t STAGE = (uint32_t)NPW * PLANE_W + 4u * XR * KC;
+constexpr uint32_t HOFF = (uint32_t)NPW * PLANE_W;
+
+// Y = rint(h 2^32) of one h element and the representation error
+// |h - Y 2^-32| (every context row uses the scale sH = 1: hidden states are
+// sigmoid outputs in [0, 1), and the zero context is 0).  h >= 2^-9 is exact;
+// smaller, non-finite, negative or >= 1 values are still bounded by err.
+__device__ __forceinline__ uint32_t digit_word(float h, float &err) {
+    const uint32_t u = __float_as_uint(h);
+    const uint32_t E = u >> 23;                          // biased exponent (sign bit -> >= 256)
+    if (E >= 118u && E < 127u) {                          // [2^-9, 1): 24-bit significand << (E - 118)
+        err = 0.f;
+        return ((u & 0x7FFFFFu) | 0x800000u) << (E - 118u);
+    }
+    if (E < 118u) {                                      // tiny (or zero / subnormal): Y < 2^24
+        const uint32_t Y = __float2uint_rn(h * 4294967296.f);
+        err = fabsf(h - (float)Y * 2.3283064365386963e-10f);
+        return Y;
+    }
+    err = (u >> 31) ? fabsf(h) : fabsf(h - 1.0f) + 2.3283064365386963e-10f;   // negative / >= 1 / NaN
+    return (u >> 31) ? 0u : 0xFFFFFFFFu;
+}
+
+// The reference's element (_kernels_nb.py:54-58) by one warp: lane l holds
+// elements [l P, (l + 1) P) of the W row and the context row; the exact
+// float64 products are formed in parallel, then the sum runs in the
+// reference's order, lane after lane (acc = U; acc += p_j for j = 0..H-1).
+template <int P>
+__device__ __forceinline__ float ref_element_warp(const float *__restrict__ wrow, const float *__restrict__ h,
+                                                 float u, int H, int lane) {
+    double p[P];
+#pragma unroll
+    for (int k = 0; k < P; k += 4) {
+        const int j = lane * P + k;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (j < H) { a = __ldg(reinterpret_cast<const float4 *>(wrow + j)); b = __ldcg(reinterpret_cast<const float4 *>(h + j)); }
+        p[k] = (double)a.x * (double)b.x; p[k + 1] = (double)a.y * (double)b.y;
+        p[k + 2] = (double)a.z * (double)b.z; p[k + 3] = (double)a.w * (double)b.w;
+    }
+    double acc = (double)u;
+    const int nl = (H + P - 1) / P;
+    for (int l = 0; l < nl; l++) {
+        if (lane == l) {
+#pragma unroll
+            for (int k = 0; k < P; k++)
+                if (l * P + k < H) acc += p[k];
+        }
+        acc = __shfl_sync(0xffffffffu, acc, l);
+    }
+    return (float)otf_sigmoid(acc);
+}
 
 template <int NT, typename WaitFn>
 __device__ __forceinline__ void update_level(const DevModel &m, const DevPlan &Q, DevStreams &S, uint32_t n,
@@ -220,104 +323,105 @@ __device__ __forceinline__ void update_level(const DevModel &m, const DevPlan &Q
                                              unsigned long long &t0) {
     constexpr int NW = NT / 32;
     const int H = m.H, NK = m.wd_nkx, nmt = (H + tc::BM - 1) / tc::BM;
-    const double c1 = (double)(H + 8) * 1.1102230246251565e-16 * 1.01;
     auto mark = [&](int i) {
         if (ph) { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); ph[i] += t - t0; t0 = t; }
     };
+    // digitize geometry: NG 16-element groups per row, a power-of-two lane
+    // group per row (NGP lanes), 32 / NGP rows per warp
+    const int NG = NK * 4;
+    int NGP = 4;
+    while (NGP < NG) NGP <<= 1;
+    const int RPW = 32 / NGP;
     for (uint32_t q0 = 0; q0 < n; q0 += XR) {
         const int R = (int)min((uint32_t)XR, n - q0);
         const int Rp = (R + 15) & ~15;
-        // ---- digitize the chunk's context rows (warp per row) ----
-        for (int r = wid; r < R; r += NW) {
-            const float *hrow = S.arena_h + (size_t)Q.pr_inrow[q0 + r] * H;
-            float mx = 0.f;
-            for (int g = lane; g < NK * 4; g += 32)
+        // ---- digitize the chunk's context rows: thread = (row, 16-element group) ----
+        for (int r = tid; r < R; r += NT) { rg.src[r] = Q.pr_inrow[q0 + r]; rg.wrd[r] = Q.pr_w[q0 + r] * H; }
+        __syncthreads();
+        mark(12);
+        auto load = [&](int rb, float (&x)[16]) {
+            const int r = rb + lane / NGP, g = lane % NGP;
+            const bool live = r < R && g < NG;
+            const float *hrow = S.arena_h + (size_t)(live ? rg.src[r] : 0) * H;
 #pragma unroll
-                for (int v = 0; v < 4; v++) {
-                    const int j = g * 16 + v * 4;
-                    if (j < H) {
-                        const float4 x = __ldcg(reinterpret_cast<const float4 *>(hrow + j));
-                        mx = fmaxf(mx, fmaxf(fmaxf(x.x, x.y), fmaxf(x.z, x.w)));
-                    }
+            for (int v = 0; v < 4; v++) {
+                const int j = g * 16 + v * 4;
+                float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (live && j < H) t = __ldcg(reinterpret_cast<const float4 *>(hrow + j));
+                x[4 * v] = t.x; x[4 * v + 1] = t.y; x[4 * v + 2] = t.z; x[4 * v + 3] = t.w;
+            }
+        };
+        auto emit = [&](int rb, const float (&x)[16]) {
+            const int r = rb + lane / NGP, g = lane % NGP;
+            const bool live = r < R && g < NG;
+            float esum = 0.f;          // errors are exact multiples of tiny powers of two; f32 sum + 1% slack
+            uint32_t pl[4][4];
+#pragma unroll
+            for (int v = 0; v < 4; v++) {
+                uint32_t Y[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    float err;
+                    Y[k] = digit_word(x[4 * v + k], err);
+                    esum += err;
                 }
-            for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            int e = 0;
-            if (mx > 0.f) frexpf(mx, &e);                    // sH = 2^e > max h
-            float emax = 0.f;
-            for (int g = lane; g < NK * 4; g += 32) {
-                uint32_t pl[4][4];
+                // plane b = byte 3 - b of the four words (byte permutes)
 #pragma unroll
-                for (int v = 0; v < 4; v++) {
-                    const int j = g * 16 + v * 4;
-                    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (j < H) x = __ldcg(reinterpret_cast<const float4 *>(hrow + j));
-                    const float xs4[4] = {x.x, x.y, x.z, x.w};
-                    uint32_t b0 = 0, b1 = 0, b2 = 0, b3 = 0;
-#pragma unroll
-                    for (int k = 0; k < 4; k++) {
-                        // Y = rint(h 2^(32-e)) by integer shifts of the f32 significand
-                        const uint32_t u = __float_as_uint(xs4[k]);
-                        const int E = (int)((u >> 23) & 255);
-                        uint32_t Y = 0;
-                        float err = 0.f;
-                        if ((u >> 31) == 0 && E > 0) {
-                            const uint32_t mnt = (u & 0x7FFFFFu) | 0x800000u;
-                            const int sh = E - 118 - e;             // <= 8 because h < 2^e
-                            if (sh >= 0) Y = mnt << sh;
-                            else if (sh > -25) {
-                                Y = (mnt + (1u << (-sh - 1))) >> (-sh);
-                                const int d = (int)mnt - (int)(Y << (-sh));
-                                err = ldexpf((float)abs(d), E - 150);
-                            } else err = xs4[k];
-                        } else if (u != 0u && u != 0x80000000u) {
-                            err = fabsf(xs4[k]);                    // subnormal / negative: not represented
-                        }
-                        emax = fmaxf(emax, err);
-                        b0 |= (Y >> 24) << (8 * k);
-                        b1 |= ((Y >> 16) & 255u) << (8 * k);
-                        b2 |= ((Y >> 8) & 255u) << (8 * k);
-                        b3 |= (Y & 255u) << (8 * k);
-                    }
-                    pl[0][v] = b0; pl[1][v] = b1; pl[2][v] = b2; pl[3][v] = b3;
+                for (int b = 0; b < 4; b++) {
+                    const uint32_t sel = (uint32_t)(3 - b) | ((uint32_t)(7 - b) << 4);
+                    pl[b][v] = __byte_perm(__byte_perm(Y[0], Y[1], sel), __byte_perm(Y[2], Y[3], sel), 0x5410);
                 }
-                const int kc = g >> 2, c = g & 3;
-                uint8_t *blk = rg.xs + (size_t)kc * 4 * Rp * KC;
+            }
+            for (int o = NGP >> 1; o; o >>= 1) esum += __shfl_xor_sync(0xffffffffu, esum, o);
+            if (live) {
+                uint8_t *blk = rg.xs + (size_t)(g >> 2) * 4 * Rp * KC + toff(r, g & 3);
 #pragma unroll
                 for (int b = 0; b < 4; b++)
-                    *reinterpret_cast<uint4 *>(blk + (size_t)b * Rp * KC + toff(r, c)) =
-                        make_uint4(pl[b][0], pl[b][1], pl[b][2], pl[b][3]);
+                    *reinterpret_cast<uint4 *>(blk + (size_t)b * Rp * KC) = make_uint4(pl[b][0], pl[b][1], pl[b][2], pl[b][3]);
+                if (g == 0) { rg.sh[r] = 1.0; rg.eh[r] = (double)esum * 1.01; }
             }
-            for (int o = 16; o; o >>= 1) emax = fmaxf(emax, __shfl_xor_sync(0xffffffffu, emax, o));
-            if (lane == 0) { rg.sh[r] = ldexp(1.0, e); rg.eh[r] = (double)emax; }
+        };
+        // two row blocks per trip: both blocks' loads are in flight together
+        for (int rb = wid * RPW; rb < R; rb += 2 * NW * RPW) {
+            float xa[16], xb[16];
+            load(rb, xa);
+            load(rb + NW * RPW, xb);
+            emit(rb, xa);
+            emit(rb + NW * RPW, xb);
         }
         // rows R..Rp-1 of the h blocks are never read back from TMEM (their
         // columns are skipped by the epilogue), whatever the scratch holds
+        mark(13);
         asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncthreads();
         mark(1);
+        const uint32_t hbytes = 4u * (uint32_t)Rp * KC;
+        // warp 1: the W plane block (mt, kc) + h plane block kc of stage gctr + kc
+        auto produce = [&](int mt, int kc0, int kc1) {
+            for (int kc = kc0; kc < kc1; kc++) {
+                const uint32_t gc = gctr + kc;
+                const int st = (int)(gc % (uint32_t)rg.stages);
+                const uint32_t use = gc / (uint32_t)rg.stages;
+                if (use >= 1) wait(tc::smem_u32(&rg.empty[st]), (use - 1) & 1, 11);
+                __syncwarp();
+                uint8_t *sW = rg.smem + (size_t)st * STAGE;
+                const uint8_t *srcW = m.Wd + ((size_t)mt * NK + kc) * NPW * PLANE_W;
+                const uint8_t *srcH = rg.xs + (size_t)kc * hbytes;
+                asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 t;\n\telect.sync t|e, 0xffffffff;\n\t"
+                             "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %6;\n\t"
+                             "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %3, [%1];\n\t"
+                             "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%4], [%5], %7, [%1];\n\t}"
+                             :: "r"(tc::smem_u32(sW)), "r"(tc::smem_u32(&rg.full[st])), "l"(srcW),
+                                "r"(HOFF), "r"(tc::smem_u32(sW + HOFF)), "l"(srcH),
+                                "r"(HOFF + hbytes), "r"(hbytes) : "memory");
+            }
+        };
+        const int npre = min(rg.stages, NK);        // stages of a tile issued ahead (during the previous epilogue)
         for (int mt = 0; mt < nmt; mt++) {
             if (wid == 1) {
-                // ---- producer: W plane block (mt, kc) + h plane block kc per stage ----
-                const uint32_t hbytes = 4u * (uint32_t)Rp * KC;
-                for (int kc = 0; kc < NK; kc++) {
-                    const uint32_t gc = gctr + kc;
-                    const int st = (int)(gc % (uint32_t)rg.stages);
-                    const uint32_t use = gc / (uint32_t)rg.stages;
-                    if (use >= 1) wait(tc::smem_u32(&rg.empty[st]), (use - 1) & 1, 11);
-                    __syncwarp();
-                    uint8_t *sW = rg.smem + (size_t)st * STAGE;
-                    const uint8_t *srcW = m.Wd + ((size_t)mt * NK + kc) * 4 * PLANE_W;
-                    const uint8_t *srcH = rg.xs + (size_t)kc * hbytes;
-                    asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 t;\n\telect.sync t|e, 0xffffffff;\n\t"
-                                 "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %6;\n\t"
-                                 "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%2], %3, [%1];\n\t"
-                                 "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%4], [%5], %7, [%1];\n\t}"
-                                 :: "r"(tc::smem_u32(sW)), "r"(tc::smem_u32(&rg.full[st])), "l"(srcW),
-                                    "r"(4u * PLANE_W), "r"(tc::smem_u32(sW + HOFF)), "l"(srcH),
-                                    "r"(4u * PLANE_W + hbytes), "r"(hbytes) : "memory");
-                }
+                produce(mt, mt == 0 ? 0 : npre, NK);
             } else if (wid == 0) {
-                // ---- MMA issuer: 13 digit pairs per 32-byte K step ----
+                // ---- MMA issuer: 17 digit pairs per 32-byte K step ----
                 for (int kc = 0; kc < NK; kc++) {
                     const uint32_t gc = gctr + kc;
                     const int st = (int)(gc % (uint32_t)rg.stages);
@@ -340,11 +444,13 @@ __device__ __forceinline__ void update_level(const DevModel &m, const DevPlan &Q
                                 mma_i8(rg.tmem + (uint32_t)((a + b0) * Rp + off), da, db, idesc(a == 0, nn), acc);
                             }
                         };
-                        range(0, 0, 4, acc0);      // (0,0) (0,1) (0,2) (0,3)
+                        range(0, 0, 4, acc0);      // (0,0) (0,1) (0,2) (0,3): blocks 0-3 first written
                         range(1, 0, 3, 1u);        // (1,0) (1,1) (1,2)
-                        range(1, 3, 1, acc0);      // (1,3): first write of block 4
+                        range(1, 3, 1, acc0);      // (1,3): block 4 first written
                         range(2, 0, 3, 1u);        // (2,0) (2,1) (2,2)
-                        range(3, 0, 2, 1u);        // (3,0) (3,1)
+                        range(2, 3, 1, acc0);      // (2,3): block 5 first written
+                        range(3, 0, 3, 1u);        // (3,0) (3,1) (3,2)
+                        range(4, 0, 2, 1u);        // (4,0) (4,1)
                     }
                     tc::commit_elect(tc::smem_u32(&rg.empty[st]));
                     if (kc == NK - 1) tc::commit_elect(tc::smem_u32(rg.done));
@@ -352,12 +458,18 @@ __device__ __forceinline__ void update_level(const DevModel &m, const DevPlan &Q
                 }
             }
             gctr += NK;
-            wait(tc::smem_u32(rg.done), tiles_done & 1, 13);
+            // one warp polls the tile's completion; the others block in the
+            // hardware barrier instead of spinning on the mbarrier
+            if (wid == 0) wait(tc::smem_u32(rg.done), tiles_done & 1, 13);
             tiles_done++;
-            __syncwarp();
+            __syncthreads();
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            // the ring is drained: issue the next tile's first stages now, so
+            // they load while this tile's epilogue runs
+            if (wid == 1 && mt + 1 < nmt) produce(mt + 1, 0, npre);
             mark(2);
-            // ---- epilogue: TMEM lane = output unit, columns s * Rp + row ----
+            // ---- epilogue: TMEM lane = output unit, columns s * Rp + row;
+            // the 4 warps of a lane quadrant take groups of 4 rows in turn ----
             const int quad = wid & 3;
             const int unit = mt * tc::BM + quad * 32 + lane;
             const bool uok = unit < H;
@@ -365,70 +477,99 @@ __device__ __forceinline__ void update_level(const DevModel &m, const DevPlan &Q
             if (uok) k4 = m.wx[unit];
             uint32_t *fbl = rg.fb + (mt & 1) * FBCAP;
             uint32_t *fbn = rg.fb_n + (mt & 1);
-            const int n8 = (R + 7) >> 3;
-            for (int it = wid >> 2; it < n8; it += NW / 4) {
-                const int r0 = it * 8;
-                int D[5][8];
-                const uint32_t ta = rg.tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)r0;
+            const float *ucol = m.U + (uok ? unit : 0);
+            const int n4 = (R + 3) >> 2;
+            for (int it = wid >> 2; it < n4; it += NW / 4) {
+                const int r0 = it * 4;
+                mark(17);
+                float uv[4];          // U[w, unit] of the group's rows (V H < 2^31: 32-bit offsets)
 #pragma unroll
-                for (int s = 0; s < 5; s++) tmem_ld8i(ta + (uint32_t)(s * Rp), D[s]);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                const int wl = lane < 8 && r0 + lane < R ? Q.pr_w[q0 + r0 + lane] : 0;
-                float uv[8];
+                for (int g = 0; g < 4; g++) uv[g] = __ldg(ucol + rg.wrd[min(r0 + g, R - 1)]);
+                long long th[4], tl[4];
+                {
+                    uint32_t D[NDIAG][4];
+                    const uint32_t ta = rg.tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)r0;
 #pragma unroll
-                for (int g = 0; g < 8; g++) {
-                    const int wq = __shfl_sync(0xffffffffu, wl, g);
-                    uv[g] = (uok && r0 + g < R) ? __ldg(m.U + (size_t)wq * H + unit) : 0.f;
+                    for (int s2 = 0; s2 < NDIAG; s2++)
+                        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                                     : "=r"(D[s2][0]), "=r"(D[s2][1]), "=r"(D[s2][2]), "=r"(D[s2][3])
+                                     : "r"(ta + (uint32_t)(s2 * Rp)));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    mark(14);
+#pragma unroll
+                    for (int g = 0; g < 4; g++) {
+                        th[g] = ((long long)(int)D[0][g] << 16) + ((long long)(int)D[1][g] << 8) + (long long)(int)D[2][g];
+                        tl[g] = ((long long)(int)D[3][g] << 16) + ((long long)(int)D[4][g] << 8) + (long long)(int)D[5][g];
+                    }
                 }
-                unsigned long long dg[8];
+                bool okv[4];
+                float yv[4];
 #pragma unroll
-                for (int g = 0; g < 8; g++) {
+                for (int g = 0; g < 4; g++) {
+                    const double x = fma((double)th[g], k4.x, fma((double)tl[g], k4.w, (double)uv[g]));
+                    const double epsm = fma(k4.z, rg.eh[min(r0 + g, R - 1)], k4.y);
+                    okv[g] = certify(x, epsm, rg.tab, yv[g]);
+                }
+                if (ph) { const float y0 = yv[0] + yv[1] + yv[2] + yv[3]; asm volatile("" :: "f"(y0)); }
+                mark(15);
+                unsigned long long dg[4];
+#pragma unroll
+                for (int g = 0; g < 4; g++) {
                     dg[g] = 0ull;
                     const int row = r0 + g;
                     if (uok && row < R) {
-                        const double sHr = rg.sh[row], eHr = rg.eh[row];
-                        double T = i2d(D[0][g]);
-                        T = fma(T, 256.0, i2d(D[1][g]));
-                        T = fma(T, 256.0, i2d(D[2][g]));
-                        T = fma(T, 256.0, i2d(D[3][g]));
-                        T = fma(T, 256.0, i2d(D[4][g]));
-                        const double u = (double)uv[g];
-                        const double x = fma(T, k4.x * sHr, u);
-                        const double eps = fma(k4.y, sHr, fma(k4.z, eHr, c1 * fabs(u)));
-                        float y;
-                        bool ok = certify(x, eps, y);
-                        if (!ok) {
+                        if (okv[g]) {
+                            S.arena_h[(size_t)(base + q0 + row) * H + unit] = yv[g];
+                            dg[g] = otf_dig_h((uint32_t)unit, yv[g]);
+                        } else {
                             const uint32_t k = atomicAdd(fbn, 1u);
                             if (k < (uint32_t)FBCAP) fbl[k] = ((uint32_t)row << 16) | (uint32_t)unit;
                             else {                                   // list full: recompute here
-                                y = ref_element(m.W + (size_t)unit * H, S.arena_h + (size_t)Q.pr_inrow[q0 + row] * H,
-                                                uv[g], H);
-                                ok = true;
+                                const float y = ref_element(m.W + (size_t)unit * H,
+                                                            S.arena_h + (size_t)rg.src[row] * H, uv[g], H);
+                                S.arena_h[(size_t)(base + q0 + row) * H + unit] = y;
+                                dg[g] = otf_dig_h((uint32_t)unit, y);
                             }
-                        }
-                        if (ok) {
-                            S.arena_h[(size_t)(base + q0 + row) * H + unit] = y;
-                            dg[g] = otf_dig_h((uint32_t)unit, y);
                         }
                     }
                 }
-                const unsigned long long tot = sd::reduce8_u64(dg, lane);
-                const int row = r0 + node_of_lane(lane);
-                if ((lane & 3) == 0 && row < R) atomicAdd(&Q.pr_dig[q0 + row], tot);
+                // digest terms of the 4 rows summed over the warp's 32 units:
+                // the sum for row g lands on the lanes whose bits (4,3) spell g
+                {
+                    const bool u16 = lane & 16, u8 = lane & 8;
+#pragma unroll
+                    for (int i2 = 0; i2 < 2; i2++) {
+                        const unsigned long long send = u16 ? dg[i2] : dg[i2 + 2], keep = u16 ? dg[i2 + 2] : dg[i2];
+                        dg[i2] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+                    }
+                    const unsigned long long send = u8 ? dg[0] : dg[1], keep = u8 ? dg[1] : dg[0];
+                    unsigned long long x2 = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+                    x2 += __shfl_xor_sync(0xffffffffu, x2, 4);
+                    x2 += __shfl_xor_sync(0xffffffffu, x2, 2);
+                    x2 += __shfl_xor_sync(0xffffffffu, x2, 1);
+                    const int row = r0 + ((lane >> 3) & 3);
+                    if ((lane & 7) == 0 && row < R) atomicAdd(&Q.pr_dig[q0 + row], x2);
+                }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncthreads();
             mark(3);
-            // ---- the reference loop for the uncertified elements ----
+            // ---- the reference loop for the uncertified elements (warp each) ----
             const uint32_t nf = min(*fbn, (uint32_t)FBCAP);
-            for (uint32_t k = (uint32_t)tid; k < nf; k += NT) {
+            for (uint32_t k = (uint32_t)wid; k < nf; k += NW) {
                 const uint32_t e = fbl[k];
                 const int row = (int)(e >> 16), un = (int)(e & 0xFFFFu);
                 const int wq = Q.pr_w[q0 + row];
-                const float y = ref_element(m.W + (size_t)un * H, S.arena_h + (size_t)Q.pr_inrow[q0 + row] * H,
-                                            __ldg(m.U + (size_t)wq * H + un), H);
-                S.arena_h[(size_t)(base + q0 + row) * H + un] = y;
-                atomicAdd(&Q.pr_dig[q0 + row], otf_dig_h((uint32_t)un, y));
+                const float *wr = m.W + (size_t)un * H, *hr = S.arena_h + (size_t)Q.pr_inrow[q0 + row] * H;
+                const float uu = __ldg(m.U + (size_t)wq * H + un);
+                float y;
+                if (H <= 128) y = ref_element_warp<4>(wr, hr, uu, H, lane);
+                else if (H <= 256) y = ref_element_warp<8>(wr, hr, uu, H, lane);
+                else y = ref_element_warp<16>(wr, hr, uu, H, lane);
+                if (lane == 0) {
+                    S.arena_h[(size_t)(base + q0 + row) * H + un] = y;
+                    atomicAdd(&Q.pr_dig[q0 + row], otf_dig_h((uint32_t)un, y));
+                }
             }
             if (Q.alg && tid == 0) atomicAdd(&Q.alg[3], (unsigned long long)*fbn);
             __syncthreads();

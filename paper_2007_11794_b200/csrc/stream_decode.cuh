@@ -236,8 +236,8 @@ __device__ __forceinline__ void hs_level_nodepar(const DevModel &m, DevPlan &Q, 
             const float4 x = __ldcg(reinterpret_cast<const float4 *>(S.arena_h + (size_t)hs.row[t] * H) + c);
             if (EXACT) {
                 double2 *d2 = reinterpret_cast<double2 *>(hs.hd + (size_t)t * H + 4 * c);
-                d2[0] = make_double2(widen(x.x), widen(x.y));
-                d2[1] = make_double2(widen(x.z), widen(x.w));
+                d2[0] = make_double2((double)x.x, (double)x.y);   // conversion unit (exact)
+                d2[1] = make_double2((double)x.z, (double)x.w);
             } else {
                 reinterpret_cast<float4 *>(hs.h)[(size_t)t * NCH + c] = x;
             }
@@ -411,6 +411,11 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (EXACT && rank == 1 && tid < 32) {                  // exp_neg's 2^(j/32) table (xu::Ring::tab)
+        double *tab = reinterpret_cast<double *>(smem + (size_t)stages * xu::STAGE + 2 * xu::FBCAP * 4 +
+                                                 2 * xu::XR * 8 + 8 + 2 * xu::XR * 4);
+        tab[tid] = exp2((double)tid / 32.0);
+    }
     uint32_t tmem = 0;
     if (rank == 1 && wid == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
@@ -463,7 +468,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
 
     // profiling runs only: per-phase device time (ns), summed over streams
     // (thread 0 of each rank marks its own phases)
-    unsigned long long ph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
+    unsigned long long ph[18] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
     const bool prof = P.phase_ns != nullptr && tid == 0;
 #define SD_MARK(i) do { if (prof) { t1 = sd::gtimer(); ph[i] += t1 - t0; t0 = t1; } } while (0)
     if (prof) t0 = sd::gtimer();
@@ -516,6 +521,9 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
             rg.sh = reinterpret_cast<double *>(tail + 2 * xu::FBCAP * 4);
             rg.eh = rg.sh + xu::XR;
             rg.fb_n = reinterpret_cast<uint32_t *>(rg.eh + xu::XR);
+            rg.src = reinterpret_cast<int32_t *>(rg.fb_n + 2);
+            rg.wrd = rg.src + xu::XR;
+            rg.tab = reinterpret_cast<const double *>(rg.wrd + xu::XR);
             rg.xs = xscratch + (size_t)u * xs_stride;
             xu::update_level<NT>(m, Q, S, n, base, rg, gctr, tiles_done, tid, wid, lane,
                                  [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); },
@@ -696,7 +704,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     }
     if (prof) {
         ph[11] = rank == 0 ? 1 : 0;
-        for (int i = 0; i < 12; i++) atomicAdd(&P.phase_ns[i], ph[i]);
+        for (int i = 0; i < 16; i++) atomicAdd(&P.phase_ns[i], ph[i]);
     }
 #undef SD_MARK
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

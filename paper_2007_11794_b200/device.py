@@ -305,16 +305,25 @@ class Plan:
     def phase_ns(self) -> dict:
         """Stream schedule, after ``profile``: device ns per phase summed over
         CTAs (utterance streams)."""
-        o = np.zeros(17, np.int64)
+        o = np.zeros(21, np.int64)
         _lib.check(_lib.load().otflm_plan_phase_ns(self.handle, o.ctypes.data, current_stream_ptr()),
                    "phase_ns")
         names = ("expand", "update_kloop", "update_drain", "update_epilogue", "hs_setup", "hs_pairs",
-                 "hs_group_total", "assign", "control_waits_for_update", "mma_wait_operands")
+                 "hs_group_total", "assign", "control_waits_for_update", "mma_wait_operands",
+                 "update_fallback")
+        # (EXACT profiling: index 5 on rank 1 is also used for the digitize
+        # row table and 6 for the digitize body -- see exact_update.cuh)
+        # (EXACT: update_kloop = digitize the context rows, update_drain = the
+        # digit-pair K loops, update_fallback = the uncertified elements' loop)
         out = {k: int(o[i]) for i, k in enumerate(names)}
         for i, k in enumerate(("assign_probe", "assign_dedup_scan", "assign_numbering", "assign_values",
                                "assign_arrivals")):
             out[k] = int(o[12 + i])
         out["ctas"] = int(o[11])
+        out["x_row_table"] = int(o[17])
+        out["x_digitize"] = int(o[18])
+        out["x_epi_tmem"] = int(o[19])
+        out["x_epi_certify"] = int(o[20])
         return out
 
     def set_schedule(self, schedule: str) -> None:
@@ -324,11 +333,11 @@ class Plan:
         self.schedule = schedule
 
     def counters(self) -> dict:
-        out = np.zeros(4, np.int64)
+        out = np.zeros(5, np.int64)
         _lib.check(_lib.load().otflm_plan_counters(self.handle, _p(out), current_stream_ptr()),
                    "plan counters")
         return dict(sum_path=int(out[0]), sum_path_k=int(out[1]), hs_queries=int(out[2]),
-                    h2d_bytes=int(out[3]))
+                    h2d_bytes=int(out[3]), exact_fallbacks=int(out[4]))
 
     def run(self, ngram: DeviceNgram, lm_weight: float = 1.0, precision: str = "fp64",
             use_graph: bool = True, stream: int | None = None) -> None:
