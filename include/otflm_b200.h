@@ -294,7 +294,8 @@ int otflm_plan_set_schedule(OtflmPlan *p, int32_t schedule);
  * the HS group, o[9] MMA-warp wait for operands, o[10] uncertified-element
  * loop (OTFLM_PREC_EXACT), o[11] CTAs, o[12..16] assign sections (probe, dedup
  * scan, numbering, values, arrivals), o[17..20] EXACT update: row table,
- * digitize, 2 spare: 21 entries.  (EXACT: o[1] is the digitize barrier,
+ * digitize, 2 spare, o[21..23] EXACT HS (rank 0): wait for the chunk's digits,
+ * digit-plane GEMM + epilogue, MaxEnt + log-sigmoid: 24 entries.  (EXACT: o[1] is the digitize barrier,
  * o[2] the digit-pair K loops.) */
 int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream);
 int otflm_schedule_supported(const OtflmModel *m, int32_t schedule, int32_t precision);

@@ -200,7 +200,7 @@ extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, Otflm
     dm.path_off = poff; dm.path_code = pcode;
     dm.W_hi = Whi; dm.W_lo = Wlo; dm.W_bf = Wbf;
     dm.W_t = nullptr; dm.wt_kcb = 0; dm.wt_npad = 0; dm.W_t64 = nullptr;
-    dm.Wd = nullptr; dm.wx = nullptr; dm.wd_nkx = 0;
+    dm.Wd = nullptr; dm.wx = nullptr; dm.wd_nkx = 0; dm.NVd = nullptr; dm.nx = nullptr;
     if (W) {
         k_prep_weights<<<256, 256>>>(dm, WT, Whi, Wlo, Wbf);
         CK(cudaGetLastError());
@@ -231,6 +231,17 @@ extern "C" int otflm_model_create(const OtflmModelDesc *d, int32_t device, Otflm
             k_prep_wdigits<<<H, 256>>>(W, U, V, H, nkx, Wd, wx);
             CK(cudaGetLastError());
             dm.Wd = Wd; dm.wx = wx; dm.wd_nkx = nkx;
+            if (NV) {        // the HS node vectors as digit planes (exact HS on rank 0's tensor core)
+                uint8_t *NVd = nullptr;
+                double4 *nx = nullptr;
+                const size_t nnv = (size_t)(V - 1) * nkx * xu::NPW * xu::KC;
+                if (m->mem.alloc(&NVd, nnv) != cudaSuccess || m->mem.alloc(&nx, (size_t)(V - 1)) != cudaSuccess) {
+                    m->mem.free_all(); delete m; g_detail = "cudaMalloc model"; return OTFLM_ERR_NOMEM;
+                }
+                k_prep_wdigits<<<V - 1, 256>>>(NV, nullptr, V, H, nkx, NVd, nx, V - 1, 1);
+                CK(cudaGetLastError());
+                dm.NVd = NVd; dm.nx = nx;
+            }
         }
     }
     CK(cudaDeviceSynchronize());
@@ -1409,12 +1420,13 @@ extern "C" int otflm_plan_info(const OtflmPlan *p, int64_t *o) {
 
 extern "C" int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream) {
     if (!p || !o) return OTFLM_ERR_VALUE;
-    unsigned long long a[21] = {0};
+    unsigned long long a[24] = {0};
     CK(cudaMemcpyAsync(a, p->alg_buf + 8, sizeof(a), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     for (int i = 0; i < 12; i++) o[i] = (int64_t)a[i];
     for (int i = 0; i < 5; i++) o[12 + i] = (int64_t)a[16 + i];
     for (int i = 0; i < 4; i++) o[17 + i] = (int64_t)a[12 + i];   // EXACT update: row table, digitize, spare
+    for (int i = 0; i < 3; i++) o[21 + i] = (int64_t)a[21 + i];   // EXACT HS (rank 0): digits wait, GEMM, log-sigmoid
     return OTFLM_OK;
 }
 
@@ -1512,16 +1524,18 @@ struct SdConfig { int stages, qb_max; size_t smem; uint32_t tmem_cols; };
 static bool sd_config(const DevModel &m, int prec, SdConfig *c) {
     if (prec == OTFLM_PREC_EXACT) {
         if (!m.Wd || m.H % 4 != 0 || m.H > 512 || !m.U || !m.NV || !m.path_off) return false;
+        if (!m.NVd) return false;
         const size_t budget = 200u * 1024u;
-        const size_t tail = 2u * xu::FBCAP * 4 + 2u * xu::XR * 8 + 8 + 2u * xu::XR * 4 + 32 * 8 + 16;
+        const size_t tail = xu::tail_layout().total;
         c->stages = (int)std::min<size_t>(4, (budget - tail) / xu::STAGE);
         if (c->stages < 2) return false;
         const int ord = m.order <= 3 ? 3 : OTF_MAX_ORDER;
-        const size_t hs_fixed = (size_t)sd::PAIRCAP * 13 + (size_t)sd::QMAX * (ord * 8 + 7 * 4) + (sd::NW + 2) * 4 + 64;
-        if (hs_fixed + 8 * 8 * (size_t)m.H > budget) return false;
-        c->qb_max = (int)std::min<size_t>(sd::QMAX, (budget - hs_fixed) / (8 * (size_t)m.H));   // float64 rows
-        c->smem = std::max((size_t)c->stages * xu::STAGE + tail, hs_fixed + (size_t)c->qb_max * 8 * m.H);
+        // rank 1: the update ring + tail; rank 0: the HS ring + pair tables
+        const size_t hs_bytes = (size_t)xh::ring_bytes() + xh::layout(ord).total;
+        c->qb_max = 0;
+        c->smem = std::max((size_t)c->stages * xu::STAGE + tail, hs_bytes);
         c->smem = std::max(c->smem, (size_t)28 * sd::NT);
+        if (c->smem > 207u * 1024u) return false;
         c->tmem_cols = 512;
         return true;
     }
@@ -1570,8 +1584,8 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
     } while (0)
     size_t xs_stride = 0;
     if (prec == OTFLM_PREC_EXACT) {
-        // one chunk of digit planes per stream: [kc][plane][XR rows x 64 B]
-        xs_stride = (size_t)m.wd_nkx * 4 * xu::XR * xu::KC;
+        // two chunk slots of digit planes per stream: [slot][kc][plane][XR rows x 64 B]
+        xs_stride = 2 * xu::xs_slot_bytes(m.wd_nkx);
         const size_t need = xs_stride * std::max<uint32_t>(p->n_utt, 1);
         if (p->xs_bytes < need) {
             uint8_t *x = nullptr;

@@ -48,6 +48,10 @@ struct DevModel {
     const uint8_t *Wd;
     const double4 *wx;
     int wd_nkx;                        // 64-byte K chunks (H rounded up to 64)
+    // the HS node vectors the same way, per node: NVd[node][kc][plane][64 B],
+    // nx[node] = {sN 2^-31, eps_n, B_n, sN 2^-55} (exact_hs.cuh)
+    const uint8_t *NVd;
+    const double4 *nx;
 };
 
 struct DevNgram {

@@ -96,6 +96,12 @@ __device__ __noinline__ float ref_element(const float *__restrict__ wrow, const 
     return (float)otf_sigmoid(acc);
 }
 
+// exact f32 -> f64 of a normal float by integer operations (no conversion unit)
+__device__ __forceinline__ double widen_d(float x) {
+    const uint32_t u = __float_as_uint(x);
+    return __hiloint2double((int)((u & 0x80000000u) | (((u >> 3) & 0x0FFFFFFFu) + (896u << 20))), (int)(u << 29));
+}
+
 // e^-x for |x| <= 700: k = rint(-32 x log2 e), r = -x - k ln2/32 (Cody-Waite,
 // ln2_hi has 11 trailing zero bits so k ln2_hi/32 is exact), e^-x =
 // 2^(k>>5) * tab[k & 31] * e^r with tab[j] = 2^(j/32) and e^r by its degree-6
@@ -136,7 +142,7 @@ __device__ __forceinline__ bool certify(double x, double epsm, const double *__r
     h = fma(h, fma(-z, h, 1.0), h);
     const float y = __double2float_rn(h);
     const uint32_t yb = __float_as_uint(y);
-    const double d = h - (double)y;
+    const double d = h - widen_d(y);                 // (y normal whenever the result is accepted)
     // half gap above y: 2^(E_y - 24); below: the same, halved at a power of two
     const uint32_t ey = (yb >> 23) & 255u;
     const int hw = (int)((ey + 1023u - 127u - 24u) << 20);
@@ -156,10 +162,14 @@ __device__ __forceinline__ bool certify(double x, double epsm, const double *__r
 // Wd[mt][kc][a < 5][128 rows x 64 B] and the float64 constants
 // wx[i] = {sW 2^-31, epsm_i, B_i, sW 2^-55}: the certification margin of
 // unit i is epsm_i + B_i eH_r (relative to sigmoid).
+// kind 1 (node vectors, exact_hs.cuh): rows are the V-1 HS node vectors, laid
+// out per node as NVd[node][kc][a][64 B] (gathered by rows), and
+// nx[n] = {sN 2^-31, eps_n, B_n, sN 2^-55} bounds the dot with a context
+// row (no U, no sigmoid margin).
 __global__ void k_prep_wdigits(const float *__restrict__ W, const float *__restrict__ U, int V, int H, int nkx,
-                               uint8_t *__restrict__ Wd, double4 *__restrict__ wx) {
+                               uint8_t *__restrict__ Wd, double4 *__restrict__ wx, int n_rows = -1, int kind = 0) {
     const int i = blockIdx.x;
-    if (i >= H) return;
+    if (i >= (n_rows < 0 ? H : n_rows)) return;
     const float *row = W + (size_t)i * H;
     __shared__ float s_max[32];
     __shared__ double s_sum[4][32];
@@ -179,7 +189,7 @@ __global__ void k_prep_wdigits(const float *__restrict__ W, const float *__restr
     mx = s_max[0];
     // max_w |U[w, i]| (the reference's sum starts from U: rounding bound)
     float mu = 0.f;
-    if (U) for (int w = threadIdx.x; w < V; w += blockDim.x) mu = fmaxf(mu, fabsf(U[(size_t)w * H + i]));
+    if (U && kind == 0) for (int w = threadIdx.x; w < V; w += blockDim.x) mu = fmaxf(mu, fabsf(U[(size_t)w * H + i]));
     for (int o = 16; o; o >>= 1) mu = fmaxf(mu, __shfl_xor_sync(0xffffffffu, mu, o));
     __syncthreads();
     if ((threadIdx.x & 31) == 0) s_max[2 + (threadIdx.x >> 5)] = mu;
@@ -209,10 +219,16 @@ __global__ void k_prep_wdigits(const float *__restrict__ W, const float *__restr
             s3 += dg[3]; s4 += dg[4];
         }
         const int kc = j / xu::KC, kk = j % xu::KC;
-        const size_t blk = ((size_t)mt * nkx + kc) * xu::NPW;
-        const uint32_t o = xu::toff(r, kk >> 4) + (kk & 15);
+        if (kind == 0) {
+            const size_t blk = ((size_t)mt * nkx + kc) * xu::NPW;
+            const uint32_t o = xu::toff(r, kk >> 4) + (kk & 15);
 #pragma unroll
-        for (int a = 0; a < xu::NPW; a++) Wd[(blk + a) * xu::PLANE_W + o] = (uint8_t)dg[a];
+            for (int a = 0; a < xu::NPW; a++) Wd[(blk + a) * xu::PLANE_W + o] = (uint8_t)dg[a];
+        } else {
+            uint8_t *dst = Wd + (((size_t)i * nkx + kc) * xu::NPW) * xu::KC + kk;
+#pragma unroll
+            for (int a = 0; a < xu::NPW; a++) dst[(size_t)a * xu::KC] = (uint8_t)dg[a];
+        }
     }
     double v4[4] = {sum_w, err_w, s3, s4};
 #pragma unroll
@@ -232,8 +248,8 @@ __global__ void k_prep_wdigits(const float *__restrict__ W, const float *__restr
         const double eps = (drop * sW + t[1]) * 1.01 + c1 * (t[0] + (double)s_max[1]) * 1.01;
         double4 o;
         o.x = ldexp(sW, -31);
-        o.y = eps * 1.0001 + 2.0e-15;                               // epsm without the h term
-        o.z = (double)mx * 1.01 * 1.0001;                            // coefficient of eH_r (sum |dh|)
+        o.y = kind == 0 ? eps * 1.0001 + 2.0e-15 : eps;             // W: epsm without the h term
+        o.z = (double)mx * 1.01 * (kind == 0 ? 1.0001 : 1.0);        // coefficient of eH_r (sum |dh|)
         o.w = ldexp(sW, -55);
         wx[i] = o;
     }
@@ -258,14 +274,27 @@ struct Ring {
     uint64_t *full, *empty, *done;
     uint32_t *fb;                  // [2][FBCAP] deferred fallback elements (row << 16 | unit)
     uint32_t *fb_n;                // [2]
-    double *sh, *eh;               // [XR] per chunk row: scale sH, sum_j |dh_j|
+    double *sh, *eh;               // [2][XR] per chunk row: scale sH, sum_j |dh_j| (by chunk parity)
     int32_t *src;                  // [XR] per chunk row: its source context's arena row
     int32_t *wrd;                  // [XR] per chunk row: its word x H (U row offset)
     const double *tab;             // [32] 2^(j/32) for exp_neg
-    uint8_t *xs;                   // this stream's global digit scratch
+    uint8_t *xs;                   // this stream's global digit scratch: 2 chunk slots (by parity)
+    size_t xs_slot;                // bytes per slot
 };
 constexpr uint32_t STAGE = (uint32_t)NPW * PLANE_W + 4u * XR * KC;
 constexpr uint32_t HOFF = (uint32_t)NPW * PLANE_W;
+// rank 1's shared memory after its ring (byte offsets); sh / eh are double
+// buffered by chunk parity because rank 0 reads a chunk's eh (DSMEM) while
+// rank 1 already digitizes the next chunk
+struct TailLayout { uint32_t fb, sh, eh, fbn, src, wrd, tab, total; };
+__host__ __device__ constexpr TailLayout tail_layout() {
+    return TailLayout{0u, 2u * FBCAP * 4, 2u * FBCAP * 4 + 2u * XR * 8, 2u * FBCAP * 4 + 4u * XR * 8,
+                      2u * FBCAP * 4 + 4u * XR * 8 + 16, 2u * FBCAP * 4 + 4u * XR * 8 + 16 + XR * 4,
+                      2u * FBCAP * 4 + 4u * XR * 8 + 16 + 2u * XR * 4,
+                      2u * FBCAP * 4 + 4u * XR * 8 + 16 + 2u * XR * 4 + 32 * 8};
+}
+// one chunk of h digit planes in the global scratch: [kc][plane][XR rows x 64 B]
+__host__ __device__ constexpr size_t xs_slot_bytes(int nkx) { return (size_t)nkx * 4 * XR * KC; }
 
 // Y = rint(h 2^32) of one h element and the representation error
 // |h - Y 2^-32| (every context row uses the scale sH = 1: hidden states are
@@ -316,29 +345,42 @@ __device__ __forceinline__ float ref_element_warp(const float *__restrict__ wrow
     return (float)otf_sigmoid(acc);
 }
 
-template <int NT, typename WaitFn>
-__device__ __forceinline__ void update_level(const DevModel &m, const DevPlan &Q, DevStreams &S, uint32_t n,
-                                             uint32_t base, const Ring &rg, uint32_t &gctr, uint32_t &tiles_done,
-                                             int tid, int wid, int lane, WaitFn wait, unsigned long long *ph,
-                                             unsigned long long &t0) {
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
+}
+
+template <int NT, typename WaitFn, typename SyncFn>
+__device__ __forceinline__ void update_chunk(const DevModel &m, const DevPlan &Q, DevStreams &S, uint32_t base,
+                                             uint32_t q0, int R, int chunk, const Ring &rg0, uint32_t &gctr,
+                                             uint32_t &tiles_done, int tid, int wid, int lane, WaitFn wait,
+                                             SyncFn digits_ready, unsigned long long *ph, unsigned long long &t0,
+                                             int mt0, int mt1, bool digitize) {
     constexpr int NW = NT / 32;
     const int H = m.H, NK = m.wd_nkx, nmt = (H + tc::BM - 1) / tc::BM;
     auto mark = [&](int i) {
         if (ph) { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); ph[i] += t - t0; t0 = t; }
     };
+    // this chunk's parity slot of the digit scratch and (the digitizing
+    // rank's) sh / eh; the other rank passes its own copy of eh
+    Ring rg = rg0;
+    rg.xs = rg0.xs + (size_t)(chunk & 1) * rg0.xs_slot;
+    if (digitize) {
+        rg.sh = rg0.sh + (chunk & 1) * XR;
+        rg.eh = rg0.eh + (chunk & 1) * XR;
+    }
     // digitize geometry: NG 16-element groups per row, a power-of-two lane
     // group per row (NGP lanes), 32 / NGP rows per warp
     const int NG = NK * 4;
     int NGP = 4;
     while (NGP < NG) NGP <<= 1;
     const int RPW = 32 / NGP;
-    for (uint32_t q0 = 0; q0 < n; q0 += XR) {
-        const int R = (int)min((uint32_t)XR, n - q0);
+    {
         const int Rp = (R + 15) & ~15;
         // ---- digitize the chunk's context rows: thread = (row, 16-element group) ----
         for (int r = tid; r < R; r += NT) { rg.src[r] = Q.pr_inrow[q0 + r]; rg.wrd[r] = Q.pr_w[q0 + r] * H; }
         __syncthreads();
         mark(12);
+        if (digitize) {
         auto load = [&](int rb, float (&x)[16]) {
             const int r = rb + lane / NGP, g = lane % NGP;
             const bool live = r < R && g < NG;
@@ -393,8 +435,10 @@ __device__ __forceinline__ void update_level(const DevModel &m, const DevPlan &Q
         // columns are skipped by the epilogue), whatever the scratch holds
         mark(13);
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        __syncthreads();
+        digits_ready();                       // rank 0's HS reads this chunk's planes too
+        }
         mark(1);
+        if (mt0 >= mt1) return;
         const uint32_t hbytes = 4u * (uint32_t)Rp * KC;
         // warp 1: the W plane block (mt, kc) + h plane block kc of stage gctr + kc
         auto produce = [&](int mt, int kc0, int kc1) {
@@ -417,9 +461,41 @@ __device__ __forceinline__ void update_level(const DevModel &m, const DevPlan &Q
             }
         };
         const int npre = min(rg.stages, NK);        // stages of a tile issued ahead (during the previous epilogue)
-        for (int mt = 0; mt < nmt; mt++) {
+        // the reference loop for tile mt's uncertified elements, a warp per
+        // element among warps [w0, NW)
+        auto fallbacks = [&](int mt, int w0) {
+            uint32_t *fbl = rg.fb + ((mt - mt0) & 1) * FBCAP;
+            uint32_t *fbn = rg.fb_n + ((mt - mt0) & 1);
+            const uint32_t nf = min(*fbn, (uint32_t)FBCAP);
+            for (uint32_t k = (uint32_t)(wid - w0); k < nf; k += (uint32_t)(NW - w0)) {
+                const uint32_t e = fbl[k];
+                const int row = (int)(e >> 16), un = (int)(e & 0xFFFFu);
+                const float *wr = m.W + (size_t)un * H, *hr = S.arena_h + (size_t)rg.src[row] * H;
+                const float uu = __ldg(m.U + (size_t)rg.wrd[row] + un);
+                float y;
+                if (H <= 128) y = ref_element_warp<4>(wr, hr, uu, H, lane);
+                else if (H <= 256) y = ref_element_warp<8>(wr, hr, uu, H, lane);
+                else y = ref_element_warp<16>(wr, hr, uu, H, lane);
+                if (lane == 0) {
+                    S.arena_h[(size_t)(base + q0 + row) * H + un] = y;
+                    atomicAdd(&Q.pr_dig[q0 + row], otf_dig_h((uint32_t)un, y));
+                }
+            }
+        };
+        auto fallbacks_done = [&](int mt) {        // one thread, after a barrier that follows fallbacks(mt)
+            uint32_t *fbn = rg.fb_n + ((mt - mt0) & 1);
+            if (Q.alg) atomicAdd(&Q.alg[3], (unsigned long long)*fbn);
+            *fbn = 0u;
+        };
+        for (int mt = mt0; mt < mt1; mt++) {
+            if (wid >= 2 && mt > mt0) {
+                // the previous tile's uncertified elements, under this tile's K loop
+                fallbacks(mt - 1, 2);
+                named_sync(3, NT - 64);
+                if (tid == 64) fallbacks_done(mt - 1);
+            }
             if (wid == 1) {
-                produce(mt, mt == 0 ? 0 : npre, NK);
+                produce(mt, mt == mt0 ? 0 : npre, NK);
             } else if (wid == 0) {
                 // ---- MMA issuer: 17 digit pairs per 32-byte K step ----
                 for (int kc = 0; kc < NK; kc++) {
@@ -466,7 +542,7 @@ __device__ __forceinline__ void update_level(const DevModel &m, const DevPlan &Q
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             // the ring is drained: issue the next tile's first stages now, so
             // they load while this tile's epilogue runs
-            if (wid == 1 && mt + 1 < nmt) produce(mt + 1, 0, npre);
+            if (wid == 1 && mt + 1 < mt1) produce(mt + 1, 0, npre);
             mark(2);
             // ---- epilogue: TMEM lane = output unit, columns s * Rp + row;
             // the 4 warps of a lane quadrant take groups of 4 rows in turn ----
@@ -475,8 +551,8 @@ __device__ __forceinline__ void update_level(const DevModel &m, const DevPlan &Q
             const bool uok = unit < H;
             double4 k4 = make_double4(0.0, 0.0, 0.0, 0.0);
             if (uok) k4 = m.wx[unit];
-            uint32_t *fbl = rg.fb + (mt & 1) * FBCAP;
-            uint32_t *fbn = rg.fb_n + (mt & 1);
+            uint32_t *fbl = rg.fb + ((mt - mt0) & 1) * FBCAP;
+            uint32_t *fbn = rg.fb_n + ((mt - mt0) & 1);
             const float *ucol = m.U + (uok ? unit : 0);
             const int n4 = (R + 3) >> 2;
             for (int it = wid >> 2; it < n4; it += NW / 4) {
@@ -506,7 +582,10 @@ __device__ __forceinline__ void update_level(const DevModel &m, const DevPlan &Q
                 float yv[4];
 #pragma unroll
                 for (int g = 0; g < 4; g++) {
-                    const double x = fma((double)th[g], k4.x, fma((double)tl[g], k4.w, (double)uv[g]));
+                    // |T_hi| < 2^41, |T_lo| < 2^44: exact int64 -> f64 through the 1.5 * 2^52 magic
+                    const double dh = __longlong_as_double(th[g] + 0x4338000000000000LL) - 6755399441055744.0;
+                    const double dlo = __longlong_as_double(tl[g] + 0x4338000000000000LL) - 6755399441055744.0;
+                    const double x = fma(dh, k4.x, fma(dlo, k4.w, widen(uv[g])));
                     const double epsm = fma(k4.z, rg.eh[min(r0 + g, R - 1)], k4.y);
                     okv[g] = certify(x, epsm, rg.tab, yv[g]);
                 }
@@ -554,28 +633,12 @@ __device__ __forceinline__ void update_level(const DevModel &m, const DevPlan &Q
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncthreads();
             mark(3);
-            // ---- the reference loop for the uncertified elements (warp each) ----
-            const uint32_t nf = min(*fbn, (uint32_t)FBCAP);
-            for (uint32_t k = (uint32_t)wid; k < nf; k += NW) {
-                const uint32_t e = fbl[k];
-                const int row = (int)(e >> 16), un = (int)(e & 0xFFFFu);
-                const int wq = Q.pr_w[q0 + row];
-                const float *wr = m.W + (size_t)un * H, *hr = S.arena_h + (size_t)Q.pr_inrow[q0 + row] * H;
-                const float uu = __ldg(m.U + (size_t)wq * H + un);
-                float y;
-                if (H <= 128) y = ref_element_warp<4>(wr, hr, uu, H, lane);
-                else if (H <= 256) y = ref_element_warp<8>(wr, hr, uu, H, lane);
-                else y = ref_element_warp<16>(wr, hr, uu, H, lane);
-                if (lane == 0) {
-                    S.arena_h[(size_t)(base + q0 + row) * H + un] = y;
-                    atomicAdd(&Q.pr_dig[q0 + row], otf_dig_h((uint32_t)un, y));
-                }
-            }
-            if (Q.alg && tid == 0) atomicAdd(&Q.alg[3], (unsigned long long)*fbn);
-            __syncthreads();
-            if (tid == 0) *fbn = 0u;
-            mark(10);
         }
+        // the last tile's uncertified elements (every warp)
+        fallbacks(mt1 - 1, 0);
+        __syncthreads();
+        if (tid == 0) fallbacks_done(mt1 - 1);
+        mark(10);
     }
 }
 }  // namespace xu

@@ -131,6 +131,7 @@ __device__ __forceinline__ unsigned long long transpose_sum32(unsigned long long
 }
 }  // namespace sd
 #include "exact_update.cuh"
+#include "exact_hs.cuh"
 
 // --------------------------------------------------------------------------
 // Node-parallel HS + MaxEnt for one level of one stream (fast mode: f32 lane
@@ -398,26 +399,26 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     const int NK = (H + KE - 1) / KE;
 
     if (tid == 0) {
-        for (int st = 0; st < stages; st++) {
-            mbar_init(smem_u32(&bar_full[st]), EXACT ? 1 : NW);   // loader warps (+ W copy) / one bulk producer
+        for (int st = 0; st < (EXACT ? 4 : stages); st++) {   // EXACT rank 0: [0, 2) HS ring, [2, 4) its update share
+            // TF32: loader warps (+ W copy); EXACT rank 1: one bulk producer;
+            // EXACT rank 0 (HS): the A-row gather threads + the B bulk copy
+            mbar_init(smem_u32(&bar_full[st]), EXACT ? (rank == 0 && st < xh::STAGES ? xh::GT + 1 : 1) : NW);
             mbar_init(smem_u32(&bar_empty[st]), 1);
         }
         mbar_init(smem_u32(&bar_done), 1);
         s_abort = 0;
         if (EXACT && rank == 1) {                          // deferred-fallback counters (xu::Ring::fb_n)
-            uint32_t *fbn = reinterpret_cast<uint32_t *>(smem + (size_t)stages * xu::STAGE + 2 * xu::FBCAP * 4 +
-                                                         2 * xu::XR * 8);
+            uint32_t *fbn = reinterpret_cast<uint32_t *>(smem + (size_t)stages * xu::STAGE + xu::tail_layout().fbn);
             fbn[0] = 0u; fbn[1] = 0u;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (EXACT && rank == 1 && tid < 32) {                  // exp_neg's 2^(j/32) table (xu::Ring::tab)
-        double *tab = reinterpret_cast<double *>(smem + (size_t)stages * xu::STAGE + 2 * xu::FBCAP * 4 +
-                                                 2 * xu::XR * 8 + 8 + 2 * xu::XR * 4);
+        double *tab = reinterpret_cast<double *>(smem + (size_t)stages * xu::STAGE + xu::tail_layout().tab);
         tab[tid] = exp2((double)tid / 32.0);
     }
     uint32_t tmem = 0;
-    if (rank == 1 && wid == 0) {
+    if ((rank == 1 || EXACT) && wid == 0) {                // EXACT: both ranks run tensor-core GEMMs
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
                      :: "r"(smem_u32(&s_tmem)), "r"(tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -425,7 +426,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (rank == 1) tmem = s_tmem;
+    if (rank == 1 || EXACT) tmem = s_tmem;
     // rank 0's row count / base / abort flag, read by rank 1 over DSMEM
     const uint32_t *r0_nprim = cluster.map_shared_rank(&s_nprim, 0);
     const uint32_t *r0_base = cluster.map_shared_rank(&s_base, 0);
@@ -445,7 +446,12 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     const AssignSmem asmem{a_key, a_row, a_cn, a_wsum, a_cnt, reinterpret_cast<unsigned long long *>(smem),
                            reinterpret_cast<uint32_t *>(smem + 16 * NT), reinterpret_cast<uint32_t *>(smem + 24 * NT)};
     uint32_t gctr = 0;          // K chunks through the ring so far (rank 1, uniform)
+    uint32_t gctr_u = 0;        // EXACT rank 0: K chunks of its update share (barriers [2, 4))
     uint32_t tiles_done = 0;
+    // EXACT: M tiles of output units, and how many of them rank 0 takes
+    // (H > 384: rank 0 has spare time after the HS, so the last tile moves there)
+    const int x_nmt = (H + BM - 1) / BM;
+    const int x_r0_tiles = (EXACT && x_nmt >= 4) ? 1 : 0;
     // node-parallel HS scratch (rank 0): the whole dynamic shared memory
     sd::HsLevelSmem hsm;
     {
@@ -468,7 +474,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
 
     // profiling runs only: per-phase device time (ns), summed over streams
     // (thread 0 of each rank marks its own phases)
-    unsigned long long ph[18] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, t0 = 0, t1 = 0;
+    unsigned long long ph[24] = {0}, t0 = 0, t1 = 0;
     const bool prof = P.phase_ns != nullptr && tid == 0;
 #define SD_MARK(i) do { if (prof) { t1 = sd::gtimer(); ph[i] += t1 - t0; t0 = t1; } } while (0)
     if (prof) t0 = sd::gtimer();
@@ -500,7 +506,56 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
         if (rank == 0) { n = s_nprim; base = s_base; abort = s_abort != 0; }
         else { n = *r0_nprim; base = *r0_base; abort = *r0_abort != 0; if (prof) t0 = sd::gtimer(); }
         if (abort) break;
-        if (rank == 0) {
+        if (rank == 0 && EXACT) {
+            // HS on this CTA's tensor core, chunk by chunk in step with rank 1's
+            // update (the chunk's h digit planes are shared through the scratch)
+            constexpr int HS_NT = NT - 64;
+            const xh::Smem xs_m = xh::carve(smem, ORD);
+            const uint32_t eh_off = (uint32_t)stages * xu::STAGE + xu::tail_layout().eh;
+            for (uint32_t q0 = 0, c = 0; q0 < n; q0 += xu::XR, c++) {
+                const int nq = (int)min((uint32_t)xu::XR, n - q0);
+                if (tid < HS_NT) xh::setup<ORD, HS_NT>(m, Q, S, q0, nq, xs_m, tid, lane);
+                __syncthreads();
+                SD_MARK(4);
+                cluster.sync();                              // D: rank 1 digitized chunk c
+                const double *eh_r = cluster.map_shared_rank(reinterpret_cast<double *>(smem + eh_off), 1) +
+                                     (c & 1) * xu::XR;
+                SD_MARK(21);
+                xh::run<ORD, NT>(m, Q, S, base, q0, nq, xscratch + (size_t)u * xs_stride + (c & 1) * xu::xs_slot_bytes(m.wd_nkx),
+                                 eh_r, smem, xs_m, tmem, bar_full, bar_empty, &bar_done, gctr, tiles_done, tid, wid, lane,
+                                 [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); },
+                                 [&](int t2, int nt2) {   // the level's small-LM scores, under the first GEMM
+                                     if (c == 0) small_lm_scores(Q, S, g, sid, L.re - L.rb, t2, nt2);
+                                 },
+                                 prof ? ph : nullptr, t0);
+                SD_MARK(5);
+                if (x_r0_tiles) {
+                    // this CTA's share of the recurrent update: the last M tile(s)
+                    constexpr xh::UpdOverlay ov = xh::upd_overlay();
+                    uint8_t *ob = reinterpret_cast<uint8_t *>(xs_m.hkey);
+                    xu::Ring rg;
+                    rg.smem = smem; rg.stages = xh::STAGES; rg.tmem = tmem;
+                    rg.full = bar_full + xh::STAGES; rg.empty = bar_empty + xh::STAGES; rg.done = &bar_done;
+                    rg.fb = reinterpret_cast<uint32_t *>(ob + ov.fb);
+                    rg.fb_n = reinterpret_cast<uint32_t *>(ob + ov.fbn);
+                    rg.eh = reinterpret_cast<double *>(ob + ov.eh);
+                    rg.sh = rg.eh;
+                    rg.src = reinterpret_cast<int32_t *>(ob + ov.src);
+                    rg.wrd = reinterpret_cast<int32_t *>(ob + ov.wrd);
+                    rg.tab = reinterpret_cast<const double *>(ob + ov.tab);
+                    rg.xs = xscratch + (size_t)u * xs_stride;
+                    rg.xs_slot = xu::xs_slot_bytes(m.wd_nkx);
+                    for (int i = tid; i < nq; i += NT) rg.eh[i] = eh_r[i];
+                    if (tid < 32) const_cast<double *>(rg.tab)[tid] = exp2((double)tid / 32.0);
+                    if (tid < 2) rg.fb_n[tid] = 0u;
+                    // (visible after update_chunk's first barrier)
+                    xu::update_chunk<NT>(m, Q, S, base, q0, nq, (int)c, rg, gctr_u, tiles_done, tid, wid, lane,
+                                         [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); },
+                                         []() {}, prof ? ph : nullptr, t0, x_nmt - x_r0_tiles, x_nmt, false);
+                }
+            }
+            SD_MARK(6);
+        } else if (rank == 0) {
             // warps 0..13: HS (named barrier 1); warps 14, 15: the small-LM
             // scores of the level's requests (they only feed assign) alongside
             constexpr int HS_NT = NT - 64;
@@ -517,17 +572,20 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
             rg.smem = smem; rg.stages = stages; rg.tmem = tmem;
             rg.full = bar_full; rg.empty = bar_empty; rg.done = &bar_done;
             uint8_t *tail = smem + (size_t)stages * xu::STAGE;
-            rg.fb = reinterpret_cast<uint32_t *>(tail);
-            rg.sh = reinterpret_cast<double *>(tail + 2 * xu::FBCAP * 4);
-            rg.eh = rg.sh + xu::XR;
-            rg.fb_n = reinterpret_cast<uint32_t *>(rg.eh + xu::XR);
-            rg.src = reinterpret_cast<int32_t *>(rg.fb_n + 2);
-            rg.wrd = rg.src + xu::XR;
-            rg.tab = reinterpret_cast<const double *>(rg.wrd + xu::XR);
+            constexpr xu::TailLayout tl = xu::tail_layout();
+            rg.fb = reinterpret_cast<uint32_t *>(tail + tl.fb);
+            rg.sh = reinterpret_cast<double *>(tail + tl.sh);
+            rg.eh = reinterpret_cast<double *>(tail + tl.eh);
+            rg.fb_n = reinterpret_cast<uint32_t *>(tail + tl.fbn);
+            rg.src = reinterpret_cast<int32_t *>(tail + tl.src);
+            rg.wrd = reinterpret_cast<int32_t *>(tail + tl.wrd);
+            rg.tab = reinterpret_cast<const double *>(tail + tl.tab);
             rg.xs = xscratch + (size_t)u * xs_stride;
-            xu::update_level<NT>(m, Q, S, n, base, rg, gctr, tiles_done, tid, wid, lane,
-                                 [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); },
-                                 prof ? ph : nullptr, t0);
+            rg.xs_slot = xu::xs_slot_bytes(m.wd_nkx);
+            for (uint32_t q0 = 0, c = 0; q0 < n; q0 += xu::XR, c++)
+                xu::update_chunk<NT>(m, Q, S, base, q0, (int)min((uint32_t)xu::XR, n - q0), (int)c, rg, gctr, tiles_done,
+                                     tid, wid, lane, [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); },
+                                     [&]() { cluster.sync(); }, prof ? ph : nullptr, t0, 0, x_nmt - x_r0_tiles, true);
         } else if (n) {
             // ------------- recurrent update (tcgen05) -------------
             for (uint32_t q0 = 0; q0 < n; q0 += BM) {
@@ -704,12 +762,12 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     }
     if (prof) {
         ph[11] = rank == 0 ? 1 : 0;
-        for (int i = 0; i < 16; i++) atomicAdd(&P.phase_ns[i], ph[i]);
+        for (int i = 0; i < 24; i++) if (ph[i]) atomicAdd(&P.phase_ns[i], ph[i]);
     }
 #undef SD_MARK
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if (rank == 1 && wid == 0)
+    if ((rank == 1 || EXACT) && wid == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(tmem_cols));
     cluster.sync();                                          // rank 0's shared memory outlives rank 1's reads
 }

@@ -305,7 +305,7 @@ class Plan:
     def phase_ns(self) -> dict:
         """Stream schedule, after ``profile``: device ns per phase summed over
         CTAs (utterance streams)."""
-        o = np.zeros(21, np.int64)
+        o = np.zeros(24, np.int64)
         _lib.check(_lib.load().otflm_plan_phase_ns(self.handle, o.ctypes.data, current_stream_ptr()),
                    "phase_ns")
         names = ("expand", "update_kloop", "update_drain", "update_epilogue", "hs_setup", "hs_pairs",
@@ -324,6 +324,10 @@ class Plan:
         out["x_digitize"] = int(o[18])
         out["x_epi_tmem"] = int(o[19])
         out["x_epi_certify"] = int(o[20])
+        out["x_hs_wait_digits"] = int(o[21])
+        out["x_hs_kloop"] = int(o[9])
+        out["x_hs_gemm_epilogue"] = int(o[22])
+        out["x_hs_maxent_lsig"] = int(o[23])
         return out
 
     def set_schedule(self, schedule: str) -> None:

@@ -1,0 +1,2 @@
+python tools/decode_once.py b 64 100 exact > gpurun_out/r02j_plain.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:k_decode_streams -c 1 -o gpurun_out/r02j_exact python tools/decode_once.py b 64 100 exact > gpurun_out/r02j_ncu.log 2>&1
