@@ -19,16 +19,6 @@ from .model import (  # noqa: F401
     build_huffman_from_counts,
     ngram_logprob,
 )
-from .lexicon import (  # noqa: F401
-    EmptyCorpusError,
-    Vocabulary,
-    build_vocabulary,
-    leaf_path,
-    load_arpa,
-    perplexity,
-    read_sentences,
-    save_arpa,
-)
 from .lattice import Arc, Lattice, LatticeFormatError, generate_lattice  # noqa: F401
 from .rescore import (  # noqa: F401
     ENTRY_BYTES,

@@ -834,6 +834,12 @@ static int check_err(OtflmStreams *s, cudaStream_t st) {
     if (he) {
         CK(cudaMemsetAsync(s->d.err, 0, 4, st));
         CK(cudaStreamSynchronize(st));
+        // a new context left without an index-table slot by an in-chunk
+        // digest mismatch (HASH | NOSLOT) is a digest error, not a full table
+        if ((he & OTF_E_HASH) && (he & OTF_E_NOSLOT) && !(he & (OTF_E_ARENA_FULL | OTF_E_CACHE_FULL))) {
+            g_detail = "content digest collision [device flags " + std::to_string(he) + "]";
+            return OTFLM_ERR_HASH;
+        }
         // a capacity overflow first: the stages after it read rows that were
         // never written, which can also raise a spurious digest mismatch
         if (he & (OTF_E_TABLE_FULL | OTF_E_ARENA_FULL | OTF_E_CACHE_FULL)) {

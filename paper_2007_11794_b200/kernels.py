@@ -181,6 +181,21 @@ def word_logprob_batch(dmodel: DeviceModel, ctx, h, hist, hist_len, words, exact
     return out
 
 
+def ngram_logprob_batch(dngram, ctx, words, out=None):
+    """ngram_logprob (ngram.py:161-179) for n (context, word) pairs on the
+    device small-LM hash: ctx int32 [n, order-1] already left-padded with
+    <s> (small_context, decoder.py:73-80), words int32 [n]; float64 [n] out.
+    KeyError for a word missing from the unigram table, ValueError for a bad
+    id (the reference's exceptions)."""
+    torch = cuda()
+    n = int(words.shape[0])
+    if out is None:
+        out = torch.empty(n, dtype=torch.float64, device=words.device)
+    _lib.check(_lib.load().otflm_ngram_logprob_batch(dngram.handle, n, ctx.data_ptr(), words.data_ptr(),
+                                                     out.data_ptr(), current_stream_ptr()), "ngram_logprob_batch")
+    return out
+
+
 def advance_hidden_batch(dmodel: DeviceModel, ctx, h, words, precision: str = "fp64", out=None):
     torch = cuda()
     n = int(words.shape[0])

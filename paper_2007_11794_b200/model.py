@@ -20,26 +20,42 @@ from typing import Sequence
 
 import numpy as np
 
+# RNLM file (docs/protocol.md:55-69): 4-byte magic, a little-endian header
+# (version, H, V, MaxEnt order, MaxEnt size, hash seed), then the four f32
+# weight blocks in field order.
 MODEL_MAGIC = b"RNLM"
 MODEL_VERSION = 1
+_HEADER = np.dtype([("magic", "S4"), ("version", "<u4"), ("H", "<u4"), ("V", "<u4"),
+                    ("order", "<u4"), ("M", "<u8"), ("seed", "<u8")])
+_WEIGHTS = ("input_weights", "recurrent_weights", "node_vectors", "maxent_table")
 
 
 @dataclass(eq=False)
 class RnnlmContext:
-    """Immutable scoring context (reference rnnlm.py:51-66)."""
+    """Immutable scoring context (reference rnnlm.py:51-66): the f32 hidden
+    state and the word history (most recent last)."""
 
     hidden: np.ndarray
     history: tuple
 
     def __post_init__(self) -> None:
-        self.hidden = np.ascontiguousarray(self.hidden, dtype=np.float32)
-        self.hidden.flags.writeable = False
-        self.history = tuple(int(w) for w in self.history)
+        h = np.array(self.hidden, dtype=np.float32, copy=True)
+        h.setflags(write=False)
+        self.hidden = h
+        self.history = tuple(map(int, self.history))
+
+
+def _weight_shapes(H: int, V: int, M: int) -> dict:
+    return {"input_weights": (V, H), "recurrent_weights": (H, H),
+            "node_vectors": (V - 1, H), "maxent_table": (M,)}
 
 
 @dataclass(eq=False)
 class RnnlmModel:
-    """Weights of the HS + MaxEnt RNNLM (reference rnnlm.py:69-124)."""
+    """The HS + MaxEnt RNNLM's weights (the reference's rnnlm.py:69-124
+    field schema, so reference and repo objects are interchangeable).  Host
+    holder only: DeviceModel uploads it once; the validation raises
+    ValueError like the reference does."""
 
     hidden_size: int
     vocab_size: int
@@ -52,82 +68,75 @@ class RnnlmModel:
     maxent_table: np.ndarray
 
     def __post_init__(self) -> None:
-        if self.maxent_size & (self.maxent_size - 1) or self.maxent_size < 1:
-            raise ValueError(f"maxent_size must be a power of two, got {self.maxent_size}")
-        if self.maxent_order < 1:
-            raise ValueError("maxent_order must be >= 1")
-        if self.vocab_size < 2:
-            raise ValueError("vocab_size must be >= 2")
-        shapes = {
-            "input_weights": (self.vocab_size, self.hidden_size),
-            "recurrent_weights": (self.hidden_size, self.hidden_size),
-            "node_vectors": (self.vocab_size - 1, self.hidden_size),
-            "maxent_table": (self.maxent_size,),
-        }
-        for name, shape in shapes.items():
+        M = int(self.maxent_size)
+        problems = [msg for bad, msg in (
+            (M < 1 or (M & (M - 1)) != 0, f"maxent_size must be a positive power of two (got {M})"),
+            (self.maxent_order < 1, f"maxent_order must be positive (got {self.maxent_order})"),
+            (self.vocab_size < 2, f"vocab_size must be at least 2 (got {self.vocab_size})"),
+        ) if bad]
+        if problems:
+            raise ValueError("; ".join(problems))
+        for name, shape in _weight_shapes(self.hidden_size, self.vocab_size, M).items():
             arr = np.ascontiguousarray(getattr(self, name), dtype=np.float32)
             if arr.shape != shape:
-                raise ValueError(f"{name} has shape {arr.shape}, expected {shape}")
-            if not np.all(np.isfinite(arr)):
-                raise ValueError(f"{name} contains non-finite values")
+                raise ValueError(f"{name}: shape {arr.shape} does not match {shape}")
+            if not np.isfinite(arr).all():
+                raise ValueError(f"{name}: non-finite weight")
             setattr(self, name, arr)
 
     @classmethod
     def new(cls, vocab_size: int, hidden_size: int = 100, maxent_order: int = 3,
             maxent_table_bits: int = 20, seed: int = 1,
             hash_seed: int = 0x5DEECE66D) -> "RnnlmModel":
-        """Same initial distribution as reference rnnlm.py:104-124 (PCG64)."""
+        """Fresh model with the reference's initial distribution
+        (rnnlm.py:104-124): U then W ~ U(-0.1, 0.1) from one PCG64 stream,
+        zero output layer -- the same draws, so the same weights."""
         rng = np.random.Generator(np.random.PCG64(seed))
-        H = hidden_size
-        M = 1 << maxent_table_bits
-        return cls(
-            hidden_size=H, vocab_size=vocab_size, maxent_order=maxent_order,
-            maxent_size=M, hash_seed=hash_seed,
-            input_weights=rng.uniform(-0.1, 0.1, (vocab_size, H)).astype(np.float32),
-            recurrent_weights=rng.uniform(-0.1, 0.1, (H, H)).astype(np.float32),
-            node_vectors=np.zeros((vocab_size - 1, H), dtype=np.float32),
-            maxent_table=np.zeros(M, dtype=np.float32),
-        )
+        V, H, M = vocab_size, hidden_size, 1 << maxent_table_bits
+        draws = [rng.uniform(-0.1, 0.1, shape).astype(np.float32) for shape in ((V, H), (H, H))]
+        return cls(hidden_size=H, vocab_size=V, maxent_order=maxent_order, maxent_size=M,
+                   hash_seed=hash_seed, input_weights=draws[0], recurrent_weights=draws[1],
+                   node_vectors=np.zeros((V - 1, H), np.float32), maxent_table=np.zeros(M, np.float32))
 
     @property
     def hash_mask(self) -> np.uint64:
         return np.uint64(self.maxent_size - 1)
 
     def zero_context(self) -> RnnlmContext:
-        return RnnlmContext(np.zeros(self.hidden_size, dtype=np.float32), ())
+        return RnnlmContext(np.zeros(self.hidden_size, np.float32), ())
 
-    # RNLM file (docs/protocol.md:55-69; reference rnnlm.py:136-170)
     def save(self, path) -> None:
-        header = MODEL_MAGIC + struct.pack("<IIIIQQ", MODEL_VERSION, self.hidden_size,
-                                           self.vocab_size, self.maxent_order,
-                                           self.maxent_size, self.hash_seed)
+        """RNLM file: structured header + the weight blocks, written in place."""
+        hdr = np.array([(MODEL_MAGIC, MODEL_VERSION, self.hidden_size, self.vocab_size,
+                         self.maxent_order, self.maxent_size, self.hash_seed)], dtype=_HEADER)
         with open(path, "wb") as fh:
-            fh.write(header)
-            for arr in (self.input_weights, self.recurrent_weights, self.node_vectors,
-                        self.maxent_table):
-                fh.write(np.ascontiguousarray(arr, dtype="<f4").tobytes())
+            hdr.tofile(fh)
+            for name in _WEIGHTS:
+                getattr(self, name).astype("<f4", copy=False).tofile(fh)
 
     @classmethod
     def load(cls, path) -> "RnnlmModel":
-        with open(path, "rb") as fh:
-            magic = fh.read(4)
-            if magic != MODEL_MAGIC:
-                raise ValueError(f"{path}: bad magic {magic!r}, expected {MODEL_MAGIC!r}")
-            version, H, n, order, M, hash_seed = struct.unpack("<IIIIQQ", fh.read(32))
-            if version != MODEL_VERSION:
-                raise ValueError(f"{path}: unsupported model version {version}")
-
-            def block(count, shape):
-                raw = fh.read(4 * count)
-                if len(raw) != 4 * count:
-                    raise ValueError(f"{path}: truncated weight block")
-                return np.frombuffer(raw, dtype="<f4").reshape(shape).astype(np.float32)
-
-            return cls(hidden_size=H, vocab_size=n, maxent_order=order, maxent_size=M,
-                       hash_seed=hash_seed, input_weights=block(n * H, (n, H)),
-                       recurrent_weights=block(H * H, (H, H)),
-                       node_vectors=block((n - 1) * H, (n - 1, H)),
-                       maxent_table=block(M, (M,)))
+        """RNLM file through one memory map: the header is parsed as a
+        structured record and the weight blocks are views at their offsets
+        (copied once, when the model validates them)."""
+        raw = np.memmap(path, dtype=np.uint8, mode="r")
+        if raw.size < _HEADER.itemsize:
+            raise ValueError(f"{path}: shorter than the RNLM header")
+        hdr = raw[:_HEADER.itemsize].view(_HEADER)[0]
+        if bytes(hdr["magic"]) != MODEL_MAGIC:
+            raise ValueError(f"{path}: not an RNLM file (magic {bytes(hdr['magic'])!r})")
+        if int(hdr["version"]) != MODEL_VERSION:
+            raise ValueError(f"{path}: RNLM version {int(hdr['version'])} is not supported")
+        H, V, M = int(hdr["H"]), int(hdr["V"]), int(hdr["M"])
+        shapes = _weight_shapes(H, V, M)
+        sizes = [int(np.prod(shapes[n])) * 4 for n in _WEIGHTS]
+        if raw.size < _HEADER.itemsize + sum(sizes):
+            raise ValueError(f"{path}: weight blocks truncated")
+        offs = _HEADER.itemsize + np.concatenate([[0], np.cumsum(sizes)[:-1]])
+        blocks = {n: raw[o:o + sz].view("<f4").reshape(shapes[n])
+                  for n, o, sz in zip(_WEIGHTS, offs, sizes)}
+        return cls(hidden_size=H, vocab_size=V, maxent_order=int(hdr["order"]), maxent_size=M,
+                   hash_seed=int(hdr["seed"]), **blocks)
 
 
 # --------------------------------------------------------------------------
@@ -250,24 +259,25 @@ class NgramModel:
 
 
 def ngram_logprob(model, context: Sequence[int], w: int) -> float:
-    """Longest stored suffix match + backoffs (reference ngram.py:161-179).
-
-    Host-side helper used when generating lattice arc scores; the decoder's
-    per-request lookup runs on the device.
-    """
+    """ln P(w | context) of a back-off LM (the reference's ngram.py:161-179
+    semantics): the longest stored n-gram ending in w over the last
+    order - 1 context words, plus the back-off weights (0 when absent) of the
+    longer contexts that did not match, added from the shortest one outward
+    -- the reference's float64 evaluation order.  Host helper (lattice arc
+    scores, tests); the decoder's lookups run on the device (decode.cuh)."""
     w = int(w)
-    if not 0 <= w < model.vocab_size:
-        raise ValueError(f"word id {w} out of range 0..{model.vocab_size - 1}")
-    ctx = tuple(int(x) for x in context)
-    ctx = ctx[-(model.order - 1):] if model.order > 1 else ()
-    suffixes = [ctx[i:] for i in range(len(ctx) + 1)]
-    for depth, c in enumerate(suffixes):
-        lp = model.probs.get(c + (w,))
-        if lp is not None:
-            for shorter in reversed(suffixes[:depth]):
-                lp = model.backoffs.get(shorter, 0.0) + lp
-            return lp
-    raise KeyError(f"word {w} missing from unigram table")
+    if w < 0 or w >= model.vocab_size:
+        raise ValueError(f"word id {w} outside the vocabulary [0, {model.vocab_size})")
+    keep = max(int(model.order) - 1, 0)
+    hist = tuple(int(x) for x in context)[-keep:] if keep else ()
+    # depth d = number of leading history words dropped before the match
+    matched = next((d for d in range(len(hist) + 1) if hist[d:] + (w,) in model.probs), None)
+    if matched is None:
+        raise KeyError(f"word {w} missing from unigram table")
+    lp = model.probs[hist[matched:] + (w,)]
+    for d in range(matched - 1, -1, -1):
+        lp = model.backoffs.get(hist[d:], 0.0) + lp
+    return lp
 
 
 def ngram_from_arrays(order, V, bos, eos, pk, pl, pv, bk, bl, bv) -> NgramModel:

@@ -67,6 +67,36 @@ def test_bench_config_b_full_workload_fp64_exact():
         assert r["d_score"] <= 1e-9 and r["self_consistency"] <= 1e-9, (u, r)
 
 
+def _assert_exact(rows, table_len_ok=True):
+    for u, r in enumerate(rows):
+        assert r["arcs"] and r["exp"] and r["end_ctx"] and r["counts"], (u, r)
+        assert r["d_score"] <= 1e-9 and r["self_consistency"] <= 1e-9, (u, r)
+
+
+def test_bench_config_b_full_workload_exact_stream():
+    """The EXACT precision of the persistent stream kernel (integer
+    digit-plane tcgen05 update and HS with certified rounding) on the bench's
+    config-b workload: identical to the oracle for all 64 utterances x 300
+    frames (arcs, expansions, end context, cache counters; scores 1e-9)."""
+    from paper_2007_11794_b200 import synth
+    s = synth.build_setup("b", n_utt=64, T=300, seed=7)
+    dec, rows = _compare(s, 8, "exact")
+    assert dec.schedule == "stream"
+    _assert_exact(rows)
+
+
+def test_bench_config_e_batch_exact_stream():
+    """One full batch of the bench's default workload (config e: V=65,536,
+    H=512, MaxEnt 2^22; utterance ids 0..73 of the 4,096, 300 frames; the
+    bench's per-id lattices): EXACT stream decode identical to the oracle."""
+    from paper_2007_11794_b200 import synth
+    base = synth.build_setup("e", n_utt=1, T=300, seed=31)
+    base.lattices = synth.lattices_for_ids(base, range(74), 300)
+    dec, rows = _compare(base, 8, "exact")
+    assert dec.schedule == "stream"
+    _assert_exact(rows)
+
+
 @pytest.mark.parametrize("config,n_utt,seed", [("b", 64, 7), ("c", 8, 17)])
 def test_full_size_tf32x3_stream_vs_oracle(config, n_utt, seed):
     """The bench's throughput mode (TF32X3 recurrent update on tcgen05,
@@ -100,10 +130,12 @@ def test_full_size_tf32x3_stream_vs_oracle(config, n_utt, seed):
             assert r["d_score"] <= 1e-4 * T, (u, r)
         else:
             assert -2e-3 * T <= r["gap"] <= 1e-4 * T, (u, r)
-    assert 4 * same >= 3 * len(rows)
+    # pinned to the measured result for these fixed seeds (config b 53/64,
+    # config c 8/8): any further divergence is a regression
+    assert same >= {"b": 53, "c": 8}[config], same
 
 
-@pytest.mark.parametrize("precision", ["fp64", "tf32x3"])
+@pytest.mark.parametrize("precision", ["fp64", "tf32x3", "exact"])
 def test_fat_variant_vs_oracle(precision):
     """SURVEY.md §8d config (b) fat variant: breadth 16, beam 64 (about 15k
     requests per frame per utterance, 256 tokens x 16 arcs per node set)."""
@@ -112,7 +144,7 @@ def test_fat_variant_vs_oracle(precision):
     s = synth.build_setup("b_fat", n_utt=4, T=T, seed=3)
     dec, rows = _compare(s, 64, precision)
     for u, r in enumerate(rows):
-        if precision == "fp64":
+        if precision in ("fp64", "exact"):
             assert r["arcs"] and r["exp"] and r["end_ctx"] and r["counts"], (u, r)
             assert r["d_score"] <= 1e-9 and r["self_consistency"] <= 1e-9, (u, r)
         else:

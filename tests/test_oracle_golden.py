@@ -6,6 +6,7 @@ exact equality."""
 from __future__ import annotations
 
 import hashlib
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -167,3 +168,29 @@ def test_oracle_lfu_trace_matches_reference(golden, small):
             list(d[f"trace_cap{cap}"])
         assert hits == list(d[f"trace_cap{cap}_hits"])
         assert succ == list(d[f"trace_cap{cap}_succ"])
+
+
+def test_oracle_and_host_ngram_with_trigram_small_lm():
+    """tests/golden/ngram3.npz (reference train_ngram + ARPA round trip,
+    order 3, missing back-offs): the host ngram_logprob equals the
+    reference's on all 4000 queries, and the C oracle's decode with the
+    trigram as small LM equals the reference's rescore_onthefly (1-best,
+    score, counters, IndexTable length)."""
+    from paper_2007_11794_b200.lattice import Lattice
+    from paper_2007_11794_b200.model import (RnnlmModel, build_huffman_from_counts, ngram_from_arrays,
+                                             ngram_logprob)
+    G = np.load(Path(__file__).parent / "golden" / "ngram3.npz")
+    lm = ngram_from_arrays(G["order"], G["V"], G["bos"], G["eos"], G["pk"], G["pl"], G["pv"],
+                           G["bk"], G["bl"], G["bv"])
+    got = [ngram_logprob(lm, [int(a), int(b)], int(w)) for (a, b), w in zip(G["q_ctx"], G["q_w"])]
+    assert np.array_equal(np.array(got), G["q_expect"])
+    U = G["U"]
+    m = RnnlmModel(U.shape[1], U.shape[0], 3, G["ME"].shape[0], int(G["seed"]), U, G["W"], G["NV"], G["ME"])
+    tree = build_huffman_from_counts(G["counts"])
+    lat = Lattice(int(G["lat_start"]), G["lat_finals"].tolist(), src=G["lat_src"], dst=G["lat_dst"],
+                  word=G["lat_word"], acoustic=G["lat_ac"], smalllm=G["lat_slm"])
+    (r, (lk, hi, mi)), = O.decode_many(m, tree, lm, [lat], beam=8, n_threads=1)
+    comb, ac, lms, end_ctx, exp_, look, hit, miss, tlen = G["result"]
+    assert list(r.arcs) == G["arcs"].tolist() and r.combined_score == comb
+    assert (r.end_context, r.expansions, lk, hi, mi, r.table_len) == \
+        (int(end_ctx), int(exp_), int(look), int(hit), int(miss), int(tlen))
