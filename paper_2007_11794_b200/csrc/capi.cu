@@ -443,7 +443,35 @@ static int launch_advance(const DevModel &m, int prec, uint32_t n_cap, const Row
                           const int32_t *in_row, const int32_t *words, const float *h_base, float *out_base,
                           uint32_t row_limit, cudaStream_t s) {
     if (n_cap == 0) return OTFLM_OK;
-    if (prec == OTFLM_PREC_FP64) {
+    if (prec == OTFLM_PREC_EXACT && m.Wd && m.H % 4 == 0) {
+        // persistent digit-plane update: a two-slot scratch per CTA (per device, grown on demand)
+        static std::mutex mu;
+        static uint8_t *xs[16] = {nullptr};
+        static size_t xs_bytes[16] = {0};
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        const size_t stride = 2 * xu::xs_slot_bytes(m.wd_nkx);
+        const size_t stages = std::min<size_t>(4, (200u * 1024u - xu::tail_layout().total) / xu::STAGE);
+        const size_t smem = stages * xu::STAGE + xu::tail_layout().total;
+        const unsigned grid = (unsigned)std::max<uint32_t>(1, std::min<uint32_t>(148, (n_cap + xu::XR - 1) / xu::XR));
+        uint8_t *scratch = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (xs_bytes[dev & 15] < stride * grid) {
+                if (xs[dev & 15]) cudaFree(xs[dev & 15]);
+                xs[dev & 15] = nullptr; xs_bytes[dev & 15] = 0;
+                if (cudaMalloc(&xs[dev & 15], stride * 148) != cudaSuccess) { g_detail = "cudaMalloc exact scratch"; return OTFLM_ERR_NOMEM; }
+                xs_bytes[dev & 15] = stride * 148;
+            }
+            scratch = xs[dev & 15];
+        }
+        CK(cudaFuncSetAttribute(k_advance_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_advance_exact<<<grid, sd::NT, smem, s>>>(m, n_cap, rs, in_row, words, h_base, out_base, scratch, stride,
+                                                   (int)stages, nullptr);
+        CKL();
+        return OTFLM_OK;
+    }
+    if (prec == OTFLM_PREC_FP64 || prec == OTFLM_PREC_EXACT) {
         constexpr int QT = 16;
         const size_t smem = (size_t)QT * m.H * sizeof(float);
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_advance_f64<QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -462,7 +490,7 @@ extern "C" int otflm_advance_hidden_batch(const OtflmModel *m, int64_t n, const 
                                           const int32_t *w, float *h_out, int32_t precision, void *stream) {
     if (n <= 0) return OTFLM_OK;
     if (!prec_ok(precision)) return OTFLM_ERR_VALUE;
-    precision = level_prec(precision);
+    /* EXACT: k_advance_exact */
     if (!m->d.U || !m->d.W) { g_detail = "model has no recurrent weights"; return OTFLM_ERR_VALUE; }
     const RowSpec rs{nullptr, nullptr, nullptr, nullptr, nullptr, 0xFFFFFFFFu};
     return launch_advance(m->d, precision, (uint32_t)n, rs, ctx, w, h_in, h_out, 0xFFFFFFFFu, (cudaStream_t)stream);
@@ -472,7 +500,7 @@ extern "C" int otflm_advance_hidden_rows(const OtflmModel *m, int64_t n, const f
                                          const float *h_in, float *h_out, int32_t precision, void *stream) {
     if (n <= 0) return OTFLM_OK;
     if (!prec_ok(precision)) return OTFLM_ERR_VALUE;
-    precision = level_prec(precision);
+    /* EXACT: k_advance_exact */
     if (!m->d.W) { g_detail = "model has no recurrent weights"; return OTFLM_ERR_VALUE; }
     DevModel dm = m->d;
     dm.U = input_rows;   // row i is the input row of query i
@@ -1459,7 +1487,7 @@ static int enqueue_stage2(OtflmPlan *p, const DevModel &m, DevStreams &S, uint32
             // persistent TMA-ring warps: enough CTAs for the level, at most the
             // resident capacity of the GPU
             const size_t smem = 4 * ring_bytes_per_warp(m.H);
-            const bool exact = prec == OTFLM_PREC_FP64;
+            const bool exact = prec == OTFLM_PREC_FP64 || prec == OTFLM_PREC_EXACT;
 #define CALLR(CPL, EX, ORD)                                                                                        \
             do {                                                                                                   \
                 CK(cudaFuncSetAttribute(k_hs_prim_ring<CPL, EX, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
@@ -1659,7 +1687,7 @@ static int decode_run_impl(OtflmPlan *p, const OtflmNgram *g, double lm_weight, 
                            int32_t use_graph, void *stream) {
     if (!p || !g) return OTFLM_ERR_VALUE;
     if (!prec_ok(precision)) return OTFLM_ERR_VALUE;
-    if (p->schedule != OTFLM_SCHED_STREAM) precision = level_prec(precision);
+    // (EXACT in the level schedule: k_advance_exact + the float64 HS kernels)
     if (g->d.order - 1 > p->st->m->d.order) { g_detail = "small LM order exceeds the stored context history"; return OTFLM_ERR_VALUE; }
     if (g->d.V < p->st->m->d.V) { g_detail = "small LM vocabulary smaller than model"; return OTFLM_ERR_VALUE; }
     cudaStream_t s = (cudaStream_t)stream;
@@ -1889,7 +1917,7 @@ static int enqueue_group(OtflmGroup *g, const OtflmNgram *ng, double lm, int pre
 extern "C" int otflm_group_run(OtflmGroup *g, const OtflmNgram *ng, double lm_weight, int32_t precision,
                                void *stream) {
     if (!g || !ng || !prec_ok(precision)) return OTFLM_ERR_VALUE;
-    precision = level_prec(precision);
+    /* EXACT: k_advance_exact + float64 HS */
     cudaStream_t s = (cudaStream_t)stream;
     if (!g->gexec || g->g_lm != lm_weight || g->g_prec != precision || g->g_ng != ng ||
         g->g_ver != g->plans[0]->st->version) {
@@ -1989,7 +2017,7 @@ extern "C" int otflm_rnnlm_prob_batch(OtflmStreams *s, int64_t n, const int32_t 
     if (!s || n < 0) return OTFLM_ERR_VALUE;
     if (n == 0) return OTFLM_OK;
     if (!prec_ok(precision)) return OTFLM_ERR_VALUE;
-    precision = level_prec(precision);
+    /* EXACT: k_advance_exact + float64 HS */
     cudaStream_t st = (cudaStream_t)stream;
     const DevModel &m = s->m->d;
     for (int64_t i = 0; i < n; i++) {

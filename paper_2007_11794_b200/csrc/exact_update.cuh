@@ -278,6 +278,12 @@ struct Ring {
     int32_t *src;                  // [XR] per chunk row: its source context's arena row
     int32_t *wrd;                  // [XR] per chunk row: its word x H (U row offset)
     const double *tab;             // [32] 2^(j/32) for exp_neg
+    // rows: source context rows hin[in_row[q]], words (nullptr: word = q), results
+    // hout[q], content-digest terms dig[q] (nullptr: none), work counters alg
+    const float *hin;
+    float *hout;
+    const int32_t *in_row, *words;
+    unsigned long long *dig, *alg;
     uint8_t *xs;                   // this stream's global digit scratch: 2 chunk slots (by parity)
     size_t xs_slot;                // bytes per slot
 };
@@ -350,8 +356,7 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 }
 
 template <int NT, typename WaitFn, typename SyncFn>
-__device__ __forceinline__ void update_chunk(const DevModel &m, const DevPlan &Q, DevStreams &S, uint32_t base,
-                                             uint32_t q0, int R, int chunk, const Ring &rg0, uint32_t &gctr,
+__device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int R, int chunk, const Ring &rg0, uint32_t &gctr,
                                              uint32_t &tiles_done, int tid, int wid, int lane, WaitFn wait,
                                              SyncFn digits_ready, unsigned long long *ph, unsigned long long &t0,
                                              int mt0, int mt1, bool digitize) {
@@ -377,14 +382,17 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, const DevPlan &Q
     {
         const int Rp = (R + 15) & ~15;
         // ---- digitize the chunk's context rows: thread = (row, 16-element group) ----
-        for (int r = tid; r < R; r += NT) { rg.src[r] = Q.pr_inrow[q0 + r]; rg.wrd[r] = Q.pr_w[q0 + r] * H; }
+        for (int r = tid; r < R; r += NT) {
+            rg.src[r] = rg.in_row[q0 + r];
+            rg.wrd[r] = (rg.words ? rg.words[q0 + r] : (int32_t)(q0 + r)) * H;
+        }
         __syncthreads();
         mark(12);
         if (digitize) {
         auto load = [&](int rb, float (&x)[16]) {
             const int r = rb + lane / NGP, g = lane % NGP;
             const bool live = r < R && g < NG;
-            const float *hrow = S.arena_h + (size_t)(live ? rg.src[r] : 0) * H;
+            const float *hrow = rg.hin + (size_t)(live ? rg.src[r] : 0) * H;
 #pragma unroll
             for (int v = 0; v < 4; v++) {
                 const int j = g * 16 + v * 4;
@@ -470,21 +478,21 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, const DevPlan &Q
             for (uint32_t k = (uint32_t)(wid - w0); k < nf; k += (uint32_t)(NW - w0)) {
                 const uint32_t e = fbl[k];
                 const int row = (int)(e >> 16), un = (int)(e & 0xFFFFu);
-                const float *wr = m.W + (size_t)un * H, *hr = S.arena_h + (size_t)rg.src[row] * H;
+                const float *wr = m.W + (size_t)un * H, *hr = rg.hin + (size_t)rg.src[row] * H;
                 const float uu = __ldg(m.U + (size_t)rg.wrd[row] + un);
                 float y;
                 if (H <= 128) y = ref_element_warp<4>(wr, hr, uu, H, lane);
                 else if (H <= 256) y = ref_element_warp<8>(wr, hr, uu, H, lane);
                 else y = ref_element_warp<16>(wr, hr, uu, H, lane);
                 if (lane == 0) {
-                    S.arena_h[(size_t)(base + q0 + row) * H + un] = y;
-                    atomicAdd(&Q.pr_dig[q0 + row], otf_dig_h((uint32_t)un, y));
+                    rg.hout[(size_t)(q0 + row) * H + un] = y;
+                    if (rg.dig) atomicAdd(&rg.dig[q0 + row], otf_dig_h((uint32_t)un, y));
                 }
             }
         };
         auto fallbacks_done = [&](int mt) {        // one thread, after a barrier that follows fallbacks(mt)
             uint32_t *fbn = rg.fb_n + ((mt - mt0) & 1);
-            if (Q.alg) atomicAdd(&Q.alg[3], (unsigned long long)*fbn);
+            if (rg.alg) atomicAdd(&rg.alg[3], (unsigned long long)*fbn);
             *fbn = 0u;
         };
         for (int mt = mt0; mt < mt1; mt++) {
@@ -598,15 +606,15 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, const DevPlan &Q
                     const int row = r0 + g;
                     if (uok && row < R) {
                         if (okv[g]) {
-                            S.arena_h[(size_t)(base + q0 + row) * H + unit] = yv[g];
+                            rg.hout[(size_t)(q0 + row) * H + unit] = yv[g];
                             dg[g] = otf_dig_h((uint32_t)unit, yv[g]);
                         } else {
                             const uint32_t k = atomicAdd(fbn, 1u);
                             if (k < (uint32_t)FBCAP) fbl[k] = ((uint32_t)row << 16) | (uint32_t)unit;
                             else {                                   // list full: recompute here
                                 const float y = ref_element(m.W + (size_t)unit * H,
-                                                            S.arena_h + (size_t)rg.src[row] * H, uv[g], H);
-                                S.arena_h[(size_t)(base + q0 + row) * H + unit] = y;
+                                                            rg.hin + (size_t)rg.src[row] * H, uv[g], H);
+                                rg.hout[(size_t)(q0 + row) * H + unit] = y;
                                 dg[g] = otf_dig_h((uint32_t)unit, y);
                             }
                         }
@@ -627,7 +635,7 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, const DevPlan &Q
                     x2 += __shfl_xor_sync(0xffffffffu, x2, 2);
                     x2 += __shfl_xor_sync(0xffffffffu, x2, 1);
                     const int row = r0 + ((lane >> 3) & 3);
-                    if ((lane & 7) == 0 && row < R) atomicAdd(&Q.pr_dig[q0 + row], x2);
+                    if ((lane & 7) == 0 && row < R && rg.dig) atomicAdd(&rg.dig[q0 + row], x2);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

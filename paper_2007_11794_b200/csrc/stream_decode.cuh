@@ -549,7 +549,9 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
                     if (tid < 32) const_cast<double *>(rg.tab)[tid] = exp2((double)tid / 32.0);
                     if (tid < 2) rg.fb_n[tid] = 0u;
                     // (visible after update_chunk's first barrier)
-                    xu::update_chunk<NT>(m, Q, S, base, q0, nq, (int)c, rg, gctr_u, tiles_done, tid, wid, lane,
+                    rg.hin = S.arena_h; rg.hout = S.arena_h + (size_t)base * H; rg.in_row = Q.pr_inrow;
+                    rg.words = Q.pr_w; rg.dig = Q.pr_dig; rg.alg = Q.alg;
+                    xu::update_chunk<NT>(m, q0, nq, (int)c, rg, gctr_u, tiles_done, tid, wid, lane,
                                          [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); },
                                          []() {}, prof ? ph : nullptr, t0, x_nmt - x_r0_tiles, x_nmt, false);
                 }
@@ -582,8 +584,10 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
             rg.tab = reinterpret_cast<const double *>(tail + tl.tab);
             rg.xs = xscratch + (size_t)u * xs_stride;
             rg.xs_slot = xu::xs_slot_bytes(m.wd_nkx);
+            rg.hin = S.arena_h; rg.hout = S.arena_h + (size_t)base * H; rg.in_row = Q.pr_inrow;
+            rg.words = Q.pr_w; rg.dig = Q.pr_dig; rg.alg = Q.alg;
             for (uint32_t q0 = 0, c = 0; q0 < n; q0 += xu::XR, c++)
-                xu::update_chunk<NT>(m, Q, S, base, q0, (int)min((uint32_t)xu::XR, n - q0), (int)c, rg, gctr, tiles_done,
+                xu::update_chunk<NT>(m, q0, (int)min((uint32_t)xu::XR, n - q0), (int)c, rg, gctr, tiles_done,
                                      tid, wid, lane, [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); },
                                      [&]() { cluster.sync(); }, prof ? ph : nullptr, t0, 0, x_nmt - x_r0_tiles, true);
         } else if (n) {
@@ -770,4 +774,76 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     if ((rank == 1 || EXACT) && wid == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(tmem_cols));
     cluster.sync();                                          // rank 0's shared memory outlives rank 1's reads
+}
+
+// --------------------------------------------------------------------------
+// The EXACT recurrent update as a batch (level schedule, two-pass, Table-1
+// batch and the kernel-table API): persistent CTAs over 80-row chunks of the
+// n rows, each with its own two-slot digit scratch, running the same
+// xu::update_chunk as the stream kernel (digitize, digit-pair K loops over
+// every M tile, certifying epilogue, reference-loop fallbacks).
+// Row q: source hin[in_row[q]], word words[q] (nullptr: q), result
+// out_base[row_base(rs) + q]; digest terms into rs.dig[q] when set.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(sd::NT, 1)
+k_advance_exact(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restrict__ in_row,
+                const int32_t *__restrict__ words, const float *__restrict__ h_base, float *__restrict__ out_base,
+                uint8_t *xscratch, size_t xs_stride, int stages, unsigned long long *alg) {
+    using namespace tc;
+    constexpr int NT = sd::NT;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bar_full[4], bar_empty[4], bar_done;
+    __shared__ uint32_t s_tmem;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int wid = __shfl_sync(0xffffffffu, tid >> 5, 0);
+    const uint32_t n = rs.n_dev ? *rs.n_dev : n_cap;
+    const uint32_t out0 = row_base(rs);
+    if (rs.cur && blockIdx.x == 0 && tid == 0) rs.cur->base = out0;
+    if ((uint64_t)out0 + n > rs.row_limit) return;      // arena overflow (flagged by the HS stage)
+    const uint32_t nch = (n + xu::XR - 1) / xu::XR;
+    if (blockIdx.x >= nch) return;
+    constexpr xu::TailLayout tl = xu::tail_layout();
+    uint8_t *tail = smem + (size_t)stages * xu::STAGE;
+    if (tid == 0) {
+        for (int st = 0; st < stages; st++) { mbar_init(smem_u32(&bar_full[st]), 1); mbar_init(smem_u32(&bar_empty[st]), 1); }
+        mbar_init(smem_u32(&bar_done), 1);
+        reinterpret_cast<uint32_t *>(tail + tl.fbn)[0] = 0u;
+        reinterpret_cast<uint32_t *>(tail + tl.fbn)[1] = 0u;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < 32) reinterpret_cast<double *>(tail + tl.tab)[tid] = exp2((double)tid / 32.0);
+    if (wid == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(smem_u32(&s_tmem)), "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    xu::Ring rg;
+    rg.smem = smem; rg.stages = stages; rg.tmem = s_tmem;
+    rg.full = bar_full; rg.empty = bar_empty; rg.done = &bar_done;
+    rg.fb = reinterpret_cast<uint32_t *>(tail + tl.fb);
+    rg.sh = reinterpret_cast<double *>(tail + tl.sh);
+    rg.eh = reinterpret_cast<double *>(tail + tl.eh);
+    rg.fb_n = reinterpret_cast<uint32_t *>(tail + tl.fbn);
+    rg.src = reinterpret_cast<int32_t *>(tail + tl.src);
+    rg.wrd = reinterpret_cast<int32_t *>(tail + tl.wrd);
+    rg.tab = reinterpret_cast<const double *>(tail + tl.tab);
+    rg.xs = xscratch + (size_t)blockIdx.x * xs_stride;
+    rg.xs_slot = xu::xs_slot_bytes(m.wd_nkx);
+    rg.hin = h_base; rg.hout = out_base + (size_t)out0 * m.H; rg.in_row = in_row; rg.words = words;
+    rg.dig = rs.dig; rg.alg = alg;
+    const int nmt = (m.H + BM - 1) / BM;
+    uint32_t gctr = 0, tiles_done = 0;
+    unsigned long long t0 = 0;
+    int local = 0;
+    for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x, local++) {
+        const uint32_t q0 = c * xu::XR;
+        xu::update_chunk<NT>(m, q0, (int)min((uint32_t)xu::XR, n - q0), local, rg, gctr, tiles_done, tid, wid, lane,
+                             [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); },
+                             []() { __syncthreads(); }, nullptr, t0, 0, nmt, true);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (wid == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(rg.tmem), "r"(512));
 }

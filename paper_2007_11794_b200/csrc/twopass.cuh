@@ -526,7 +526,7 @@ static int twopass_enqueue(OtflmTwopass *p, int mode, double lam, double lmw, in
     const bool fork = s2 != s;
     auto event = [&]() { cudaEvent_t e; cudaEventCreateWithFlags(&e, cudaEventDisableTiming); evs->push_back(e); return e; };
     if (fork) { cudaEvent_t e = event(); CK(cudaEventRecord(e, s)); CK(cudaStreamWaitEvent(s2, e, 0)); }
-    const bool exact = prec == OTFLM_PREC_FP64;
+    const bool exact = prec == OTFLM_PREC_FP64 || prec == OTFLM_PREC_EXACT;
     const RowSpec rs{nullptr, nullptr, nullptr, nullptr, nullptr, 0xFFFFFFFFu};
     for (size_t lv = 0; lv < p->level_int.size(); lv++) {
         const uint32_t lo = p->level_off[lv], hi = p->level_off[lv + 1], ni = p->level_int[lv];
@@ -569,8 +569,7 @@ extern "C" int otflm_twopass_run(OtflmTwopass *p, int32_t mode, double interp_we
     if (mode != 0 && mode != 1) { g_detail = "unknown two-pass mode"; return OTFLM_ERR_VALUE; }
     if (mode == 1 && !p->g) { g_detail = "hybrid mode needs the small LM"; return OTFLM_ERR_VALUE; }
     if (!prec_ok(precision)) return OTFLM_ERR_VALUE;
-    precision = level_prec(precision);
-    if (precision != OTFLM_PREC_FP64 && p->m->d.H > 512) { g_detail = "tensor-core update needs H <= 512"; return OTFLM_ERR_VALUE; }
+    if (precision != OTFLM_PREC_FP64 && precision != OTFLM_PREC_EXACT && p->m->d.H > 512) { g_detail = "tensor-core update needs H <= 512"; return OTFLM_ERR_VALUE; }
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t l0 = g_launches;
     if (!use_graph) {

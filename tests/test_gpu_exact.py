@@ -72,3 +72,15 @@ def test_exact_is_the_auto_stream_choice_and_matches_fp64_level():
     for a, b in zip(hs, hl):
         assert a.arcs == b.arcs and a.end_context == b.end_context
         assert abs(a.combined_score - b.combined_score) <= 1e-9
+
+
+@pytest.mark.parametrize("case", [("b", 6, 60, 8, True), ("c", 3, 30, 8, True)])
+def test_exact_level_schedule_identical_to_oracle(case):
+    """EXACT in the level-synchronous schedule (k_advance_exact + the float64
+    HS kernels): the same identity with the oracle."""
+    from paper_2007_11794_b200 import synth
+    name, n_utt, T, beam, enabled = case
+    s = synth.build_setup(name, n_utt=n_utt, T=T, seed=5)
+    ref = O.decode_many(s.model, s.tree, s.small_lm, s.lattices, beam=beam, enabled=enabled, n_threads=4)
+    hyps, out, st = _decode(s, "exact", "level", beam, enabled)
+    _assert_identical(hyps, out, st, ref)

@@ -151,6 +151,30 @@ def test_advance_tensor_core_modes(prec, tol, H, torch):
     assert np.max(np.abs(got.astype(np.float64) - want.astype(np.float64))) <= tol
 
 
+@pytest.mark.parametrize("H", [64, 256, 512])
+def test_advance_exact_bit_identical(H, torch):
+    """EXACT (k_advance_exact: digit planes on tcgen05 kind::i8, certified
+    rounding, the reference loop for the rest): every output float equals
+    the reference's bit for bit -- including zero contexts and context rows
+    with elements far below the 2^-9 digit resolution."""
+    from paper_2007_11794_b200 import kernels, synth
+    from paper_2007_11794_b200.device import DeviceModel
+    V = 4000
+    model = synth.synth_model(V, H, 12)
+    dm = DeviceModel(model, None, output=False)
+    n = 3000
+    h, hist, hl, w = _queries(model, n, seed=11)
+    h[5] = 0.0                                   # the zero context
+    h[7, ::3] = 1e-7                             # tiny elements: not representable in 32 fixed-point bits
+    h[9, :4] = 3.0e-39                           # subnormals
+    perm = np.random.RandomState(2).permutation(n).astype(np.int32)
+    got = kernels.advance_hidden_batch(dm, torch.from_numpy(perm).cuda(), torch.from_numpy(h).cuda(),
+                                       torch.from_numpy(w).cuda(), "exact").cpu().numpy()
+    want = _oracle_perm(model, h, w, perm)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), \
+        int(np.count_nonzero(got.view(np.uint32) != want.view(np.uint32)))
+
+
 def _oracle_perm(model, h, w, perm):
     _, out = O.query_batch(model, _NoTree(model.vocab_size), h[perm],
                            np.zeros((len(perm), model.maxent_order), np.int64),
