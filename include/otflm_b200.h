@@ -259,12 +259,13 @@ int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *lats, int32_t *sam
 /* plan stats: levels, nodes, arcs, slots, max requests per level, total
  * request slots, graph nodes (int64 [8]) */
 int otflm_plan_info(const OtflmPlan *p, int64_t *out8);
-/* Algorithmic-work counters of the last profiled run + upload size (int64 [5]):
+/* Algorithmic-work counters of the last profiled run + upload size (int64 [6]):
  * sum of Huffman path lengths over HS queries, sum of path length x MaxEnt
  * orders, HS queries, bytes uploaded by plan_create, and (OTFLM_PREC_EXACT)
  * hidden-state elements whose rounding could not be certified and ran the
- * reference's sequential loop. */
-int otflm_plan_counters(const OtflmPlan *p, int64_t *out5, void *stream);
+ * reference's sequential loop, and (EXACT stream) context rows whose digit
+ * planes were not made at their creation in this launch (digitized late). */
+int otflm_plan_counters(const OtflmPlan *p, int64_t *out6, void *stream);
 /* One decode run captured as a CUDA graph with an event-record node around
  * every kernel; writes device-side total ms / launch counts per category
  * (7 entries: expand, hs, advance, assign, final, misc, stream).  HS and the

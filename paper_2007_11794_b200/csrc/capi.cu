@@ -444,31 +444,19 @@ static int launch_advance(const DevModel &m, int prec, uint32_t n_cap, const Row
                           uint32_t row_limit, cudaStream_t s) {
     if (n_cap == 0) return OTFLM_OK;
     if (prec == OTFLM_PREC_EXACT && m.Wd && m.H % 4 == 0) {
-        // persistent digit-plane update: a two-slot scratch per CTA (per device, grown on demand)
-        static std::mutex mu;
-        static uint8_t *xs[16] = {nullptr};
-        static size_t xs_bytes[16] = {0};
-        int dev = 0;
-        CK(cudaGetDevice(&dev));
+        // persistent digit-plane update: a two-slot digit scratch per CTA,
+        // stream-ordered (pooled; also valid inside a graph capture)
         const size_t stride = 2 * xu::xs_slot_bytes(m.wd_nkx);
         const size_t stages = std::min<size_t>(4, (200u * 1024u - xu::tail_layout().total) / xu::STAGE);
         const size_t smem = stages * xu::STAGE + xu::tail_layout().total;
         const unsigned grid = (unsigned)std::max<uint32_t>(1, std::min<uint32_t>(148, (n_cap + xu::XR - 1) / xu::XR));
         uint8_t *scratch = nullptr;
-        {
-            std::lock_guard<std::mutex> lk(mu);
-            if (xs_bytes[dev & 15] < stride * grid) {
-                if (xs[dev & 15]) cudaFree(xs[dev & 15]);
-                xs[dev & 15] = nullptr; xs_bytes[dev & 15] = 0;
-                if (cudaMalloc(&xs[dev & 15], stride * 148) != cudaSuccess) { g_detail = "cudaMalloc exact scratch"; return OTFLM_ERR_NOMEM; }
-                xs_bytes[dev & 15] = stride * 148;
-            }
-            scratch = xs[dev & 15];
-        }
+        if (cudaMallocAsync(&scratch, stride * grid, s) != cudaSuccess) { g_detail = "cudaMallocAsync exact scratch"; return OTFLM_ERR_NOMEM; }
         CK(cudaFuncSetAttribute(k_advance_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_advance_exact<<<grid, sd::NT, smem, s>>>(m, n_cap, rs, in_row, words, h_base, out_base, scratch, stride,
                                                    (int)stages, nullptr);
         CKL();
+        CK(cudaFreeAsync(scratch, s));
         return OTFLM_OK;
     }
     if (prec == OTFLM_PREC_FP64 || prec == OTFLM_PREC_EXACT) {
@@ -753,6 +741,7 @@ struct OtflmStreams {
     LfuHost *lfu = nullptr;         // capacity-bounded cache policy (lfu.cuh)
     int64_t capacity_bytes = 0;
     uint64_t version = 0;           // bumped when DevStreams changes (captured graphs re-capture)
+    uint32_t dig_epoch = 0;         // EXACT stream launches so far (arena_dep tags)
 };
 #include "lfu.cuh"
 
@@ -809,6 +798,7 @@ extern "C" int otflm_streams_create(const OtflmModel *m, const OtflmStreamConfig
     d.max_ctx = (uint32_t)cfg->max_contexts;
     d.arena_rows = (uint32_t)cfg->arena_rows;
     d.lfu_cap = 0; d.lfu_logcap = 0; d.lfu_log = nullptr; d.lfu_logn = nullptr;
+    d.arena_dig = nullptr; d.arena_deh = nullptr; d.arena_dep = nullptr;
     d.ct_cap = pow2_at_least((uint64_t)cfg->max_contexts * 2 + 2);
     d.kc_cap = pow2_at_least((uint64_t)std::max<int64_t>(cfg->cache_slots, 16));
     const size_t S = d.S;
@@ -1454,24 +1444,26 @@ extern "C" int otflm_plan_info(const OtflmPlan *p, int64_t *o) {
 
 extern "C" int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream) {
     if (!p || !o) return OTFLM_ERR_VALUE;
-    unsigned long long a[24] = {0};
+    unsigned long long a[26] = {0};
     CK(cudaMemcpyAsync(a, p->alg_buf + 8, sizeof(a), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     for (int i = 0; i < 12; i++) o[i] = (int64_t)a[i];
     for (int i = 0; i < 5; i++) o[12 + i] = (int64_t)a[16 + i];
     for (int i = 0; i < 4; i++) o[17 + i] = (int64_t)a[12 + i];   // EXACT update: row table, digitize, spare
     for (int i = 0; i < 3; i++) o[21 + i] = (int64_t)a[21 + i];   // EXACT HS (rank 0): digits wait, GEMM, log-sigmoid
+    o[24] = (int64_t)a[24]; o[25] = (int64_t)a[25];                 // EXACT update: plane-copy row pass, copy
     return OTFLM_OK;
 }
 
 extern "C" int otflm_plan_counters(const OtflmPlan *p, int64_t *o, void *stream) {
     if (!p || !o) return OTFLM_ERR_VALUE;
-    unsigned long long a[4] = {0, 0, 0, 0};
+    unsigned long long a[6] = {0, 0, 0, 0, 0, 0};
     CK(cudaMemcpyAsync(a, p->alg_buf, sizeof(a), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     o[0] = (int64_t)a[0]; o[1] = (int64_t)a[1]; o[2] = (int64_t)a[2];
     o[3] = (int64_t)p->h2d_bytes;
     o[4] = (int64_t)a[3];
+    o[5] = (int64_t)a[5];
     return OTFLM_OK;
 }
 
@@ -1607,7 +1599,7 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
         CK(cudaFuncSetAttribute(k_decode_streams<MODE, KCB, CPL, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem)); \
         k_decode_streams<MODE, KCB, CPL, ORD><<<2 * p->n_utt, sd::NT, c.smem, s>>>(m, d, S, g->d, (long long)p->beam, lm, \
                                                                               c.stages, c.qb_max, cursor, limit, c.tmem_cols, \
-                                                                              p->xs, xs_stride); \
+                                                                              p->xs, xs_stride, x_epoch); \
     } while (0)
 #define SD_ORD(MODE, KCB, CPL) do { if (m.order <= 3) SD_LAUNCH(MODE, KCB, CPL, 3); else SD_LAUNCH(MODE, KCB, CPL, OTF_MAX_ORDER); } while (0)
 #define SD_H(MODE)                                                                                              \
@@ -1617,7 +1609,22 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
         else SD_ORD(MODE, 64, 4);                                                                               \
     } while (0)
     size_t xs_stride = 0;
+    uint32_t x_epoch = 0;
     if (prec == OTFLM_PREC_EXACT) {
+        // per-arena-row digit planes (made at row creation), allocated on first use
+        OtflmStreams *st = p->st;
+        if (!st->d.arena_dig) {
+            uint8_t *dg = nullptr; float *deh = nullptr; uint32_t *dep = nullptr;
+            const size_t rows = std::max<uint32_t>(st->d.arena_rows, 1);
+            if (st->mem.alloc(&dg, rows * (size_t)m.wd_nkx * 4 * xu::KC) != cudaSuccess ||
+                st->mem.alloc(&deh, rows) != cudaSuccess || st->mem.alloc(&dep, rows) != cudaSuccess) {
+                g_detail = "cudaMalloc digit store"; return OTFLM_ERR_NOMEM;
+            }
+            CK(cudaMemsetAsync(dep, 0, rows * 4, s));
+            st->d.arena_dig = dg; st->d.arena_deh = deh; st->d.arena_dep = dep;
+        }
+        x_epoch = ++st->dig_epoch;
+        S.arena_dig = st->d.arena_dig; S.arena_deh = st->d.arena_deh; S.arena_dep = st->d.arena_dep;
         // two chunk slots of digit planes per stream: [slot][kc][plane][XR rows x 64 B]
         xs_stride = 2 * xu::xs_slot_bytes(m.wd_nkx);
         const size_t need = xs_stride * std::max<uint32_t>(p->n_utt, 1);

@@ -86,6 +86,12 @@ struct DevStreams {
     uint32_t lfu_cap;                 // resident entries allowed (0: unbounded mode)
     uint32_t lfu_logcap;              // per stream log capacity
     uint32_t *lfu_log, *lfu_logn;     // [S][logcap], [S]  (nullptr: no log)
+    // EXACT stream kernel: the digit planes of every arena row, made when the
+    // row is created ([row][kc][plane][64 B]), its representation-error sum
+    // and the launch (epoch) that made them (exact_update.cuh)
+    uint8_t *arena_dig;
+    float *arena_deh;
+    uint32_t *arena_dep;
 };
 
 // per-request state

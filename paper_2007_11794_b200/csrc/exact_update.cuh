@@ -284,6 +284,11 @@ struct Ring {
     float *hout;
     const int32_t *in_row, *words;
     unsigned long long *dig, *alg;
+    // per-arena-row planes made at row creation (nullptr: digitize every chunk)
+    uint8_t *dig_store;
+    float *deh_store;
+    uint32_t *dep_store;
+    uint32_t epoch;
     uint8_t *xs;                   // this stream's global digit scratch: 2 chunk slots (by parity)
     size_t xs_slot;                // bytes per slot
 };
@@ -355,6 +360,75 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" :: "r"(id), "r"(nthreads) : "memory");
 }
 
+// 16 consecutive elements of a context row -> their four digit-plane
+// words per plane (pl[plane][4 x 4 bytes]) and the representation-error sum
+__device__ __forceinline__ void planes16(const float (&x)[16], uint32_t (&pl)[4][4], float &esum) {
+    esum = 0.f;                  // errors are exact multiples of tiny powers of two; f32 sum + 1% slack
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+        uint32_t Y[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            float err;
+            Y[k] = digit_word(x[4 * v + k], err);
+            esum += err;
+        }
+        // plane b = byte 3 - b of the four words (byte permutes)
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const uint32_t sel = (uint32_t)(3 - b) | ((uint32_t)(7 - b) << 4);
+            pl[b][v] = __byte_perm(__byte_perm(Y[0], Y[1], sel), __byte_perm(Y[2], Y[3], sel), 0x5410);
+        }
+    }
+}
+__device__ __forceinline__ void load16(const float *hrow, int g, int H, bool live, float (&x)[16]) {
+#pragma unroll
+    for (int v = 0; v < 4; v++) {
+        const int j = g * 16 + v * 4;
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (live && j < H) t = __ldcg(reinterpret_cast<const float4 *>(hrow + j));
+        x[4 * v] = t.x; x[4 * v + 1] = t.y; x[4 * v + 2] = t.z; x[4 * v + 3] = t.w;
+    }
+}
+
+// The digit planes of arena rows [row0, row0 + n) into the per-row store
+// (right after the rows are created), tagged with this launch's epoch.
+// Thread = (row, 16-element group); the row's lanes reduce its error sum.
+template <int NT>
+__device__ __forceinline__ void digitize_to_store(const DevModel &m, const float *__restrict__ hin, uint32_t row0,
+                                                  uint32_t n, uint8_t *store, float *deh, uint32_t *dep,
+                                                  uint32_t epoch, int tid, int wid, int lane) {
+    constexpr int NW = NT / 32;
+    const int H = m.H, NK = m.wd_nkx, NG = NK * 4;
+    int NGP = 4;
+    while (NGP < NG) NGP <<= 1;
+    const int RPW = 32 / NGP;
+    for (uint32_t rb = (uint32_t)(wid * RPW); rb < n; rb += (uint32_t)(2 * NW * RPW)) {
+        float xa[16], xb[16];
+        const uint32_t ra = rb + lane / NGP, rbb = ra + NW * RPW;
+        const int g = lane % NGP;
+        const bool la = ra < n && g < NG, lb = rbb < n && g < NG;
+        load16(hin + (size_t)(row0 + (la ? ra : 0)) * H, g, H, la, xa);
+        load16(hin + (size_t)(row0 + (lb ? rbb : 0)) * H, g, H, lb, xb);
+#pragma unroll
+        for (int half = 0; half < 2; half++) {
+            uint32_t pl[4][4];
+            float esum;
+            planes16(half ? xb : xa, pl, esum);
+            if (__any_sync(0xffffffffu, esum != 0.f))
+                for (int o = NGP >> 1; o; o >>= 1) esum += __shfl_xor_sync(0xffffffffu, esum, o);
+            const uint32_t r = half ? rbb : ra;
+            if (half ? lb : la) {
+                uint8_t *dst = store + ((size_t)(row0 + r) * NK + (g >> 2)) * 4 * KC + (g & 3) * 16;
+#pragma unroll
+                for (int b = 0; b < 4; b++)
+                    *reinterpret_cast<uint4 *>(dst + b * KC) = make_uint4(pl[b][0], pl[b][1], pl[b][2], pl[b][3]);
+                if (g == 0) { deh[row0 + r] = esum * 1.01f; dep[row0 + r] = epoch; }
+            }
+        }
+    }
+}
+
 template <int NT, typename WaitFn, typename SyncFn>
 __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int R, int chunk, const Ring &rg0, uint32_t &gctr,
                                              uint32_t &tiles_done, int tid, int wid, int lane, WaitFn wait,
@@ -388,7 +462,70 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
         }
         __syncthreads();
         mark(12);
-        if (digitize) {
+        if (digitize && rg.dig_store) {
+            // planes made when the rows were created (this launch): a flat
+            // copy into the chunk layout, six 16-byte pieces in flight per
+            // thread; other rows (the zero context, rows of an earlier launch
+            // or another schedule) are digitized here.  sh[r] = 1 marks fresh.
+            for (int r = tid; r < R; r += NT) {
+                const int src = rg.src[r];
+                const bool fresh = rg.dep_store[src] == rg.epoch;
+                rg.sh[r] = fresh ? 1.0 : 0.0;
+                if (!fresh && rg.alg) atomicAdd(&rg.alg[5], 1ull);
+                if (fresh) rg.eh[r] = (double)rg.deh_store[src];
+            }
+            __syncthreads();
+            mark(24);
+            // warp per (kc, plane) block: lane = c * 8 + (row & 7), so each of the
+            // block's 8-row groups is one contiguous 512-byte write of the
+            // canonical layout; all groups' loads are in flight together.  Rows
+            // not made in this launch are copied too and overwritten below.
+            {
+                const int KP = NK * 4, g8n = Rp >> 3;
+                const size_t row_bytes = (size_t)KP * KC;
+                for (int kp = wid; kp < KP; kp += NW) {
+                    uint4 v[XR / 8];
+#pragma unroll
+                    for (int g8 = 0; g8 < XR / 8; g8++) {
+                        const int r = g8 * 8 + (lane & 7);
+                        v[g8] = make_uint4(0u, 0u, 0u, 0u);
+                        if (g8 < g8n && r < R)
+                            v[g8] = __ldcg(reinterpret_cast<const uint4 *>(rg.dig_store + (size_t)rg.src[r] * row_bytes +
+                                                                           (size_t)kp * KC) + (lane >> 3));
+                    }
+#pragma unroll
+                    for (int g8 = 0; g8 < XR / 8; g8++)
+                        if (g8 < g8n)
+                            *reinterpret_cast<uint4 *>(rg.xs + (size_t)kp * Rp * KC + (size_t)g8 * 512 + lane * 16) = v[g8];
+                }
+            }
+            __syncthreads();
+            mark(25);
+            for (int rb = wid * RPW; rb < R; rb += NW * RPW) {
+                const int r = rb + lane / NGP, g = lane % NGP;
+                const bool live = r < R && g < NG;
+                const bool todo = live && rg.sh[r] == 0.0;
+                if (__any_sync(0xffffffffu, todo)) {
+                    float x[16];
+                    load16(rg.hin + (size_t)(live ? rg.src[r] : 0) * H, g, H, todo, x);
+                    uint32_t pl[4][4];
+                    float esum;
+                    planes16(x, pl, esum);
+                    if (__any_sync(0xffffffffu, esum != 0.f))
+                        for (int o = NGP >> 1; o; o >>= 1) esum += __shfl_xor_sync(0xffffffffu, esum, o);
+                    if (todo) {
+                        uint8_t *blk = rg.xs + (size_t)(g >> 2) * 4 * Rp * KC + toff(r, g & 3);
+#pragma unroll
+                        for (int b = 0; b < 4; b++)
+                            *reinterpret_cast<uint4 *>(blk + (size_t)b * Rp * KC) = make_uint4(pl[b][0], pl[b][1], pl[b][2], pl[b][3]);
+                        if (g == 0) rg.eh[r] = (double)esum * 1.01;
+                    }
+                }
+            }
+            mark(13);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            digits_ready();
+        } else if (digitize) {
         auto load = [&](int rb, float (&x)[16]) {
             const int r = rb + lane / NGP, g = lane % NGP;
             const bool live = r < R && g < NG;
@@ -422,7 +559,9 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                     pl[b][v] = __byte_perm(__byte_perm(Y[0], Y[1], sel), __byte_perm(Y[2], Y[3], sel), 0x5410);
                 }
             }
-            for (int o = NGP >> 1; o; o >>= 1) esum += __shfl_xor_sync(0xffffffffu, esum, o);
+            // (rare) representation errors: reduce only when some lane has one
+            if (__any_sync(0xffffffffu, esum != 0.f))
+                for (int o = NGP >> 1; o; o >>= 1) esum += __shfl_xor_sync(0xffffffffu, esum, o);
             if (live) {
                 uint8_t *blk = rg.xs + (size_t)(g >> 2) * 4 * Rp * KC + toff(r, g & 3);
 #pragma unroll
@@ -431,13 +570,15 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                 if (g == 0) { rg.sh[r] = 1.0; rg.eh[r] = (double)esum * 1.01; }
             }
         };
-        // two row blocks per trip: both blocks' loads are in flight together
-        for (int rb = wid * RPW; rb < R; rb += 2 * NW * RPW) {
-            float xa[16], xb[16];
+        // three row blocks per trip: their loads are in flight together
+        for (int rb = wid * RPW; rb < R; rb += 3 * NW * RPW) {
+            float xa[16], xb[16], xc[16];
             load(rb, xa);
             load(rb + NW * RPW, xb);
+            load(rb + 2 * NW * RPW, xc);
             emit(rb, xa);
             emit(rb + NW * RPW, xb);
+            emit(rb + 2 * NW * RPW, xc);
         }
         // rows R..Rp-1 of the h blocks are never read back from TMEM (their
         // columns are skipped by the epilogue), whatever the scratch holds

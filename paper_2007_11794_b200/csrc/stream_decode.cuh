@@ -370,7 +370,7 @@ template <int MODE, int KC_B, int CPL, int ORD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sd::NT, 1)
 k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, double lm_weight, int stages,
                  int qb_max, uint32_t *cursor, uint32_t row_limit, uint32_t tmem_cols, uint8_t *xscratch,
-                 size_t xs_stride) {
+                 size_t xs_stride, uint32_t x_epoch) {
     using namespace tc;
     namespace cg = cooperative_groups;
     constexpr bool X3 = MODE == 1;
@@ -474,7 +474,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
 
     // profiling runs only: per-phase device time (ns), summed over streams
     // (thread 0 of each rank marks its own phases)
-    unsigned long long ph[24] = {0}, t0 = 0, t1 = 0;
+    unsigned long long ph[26] = {0}, t0 = 0, t1 = 0;
     const bool prof = P.phase_ns != nullptr && tid == 0;
 #define SD_MARK(i) do { if (prof) { t1 = sd::gtimer(); ph[i] += t1 - t0; t0 = t1; } } while (0)
     if (prof) t0 = sd::gtimer();
@@ -551,6 +551,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
                     // (visible after update_chunk's first barrier)
                     rg.hin = S.arena_h; rg.hout = S.arena_h + (size_t)base * H; rg.in_row = Q.pr_inrow;
                     rg.words = Q.pr_w; rg.dig = Q.pr_dig; rg.alg = Q.alg;
+                    rg.dig_store = nullptr; rg.deh_store = nullptr; rg.dep_store = nullptr; rg.epoch = 0;
                     xu::update_chunk<NT>(m, q0, nq, (int)c, rg, gctr_u, tiles_done, tid, wid, lane,
                                          [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); },
                                          []() {}, prof ? ph : nullptr, t0, x_nmt - x_r0_tiles, x_nmt, false);
@@ -586,6 +587,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
             rg.xs_slot = xu::xs_slot_bytes(m.wd_nkx);
             rg.hin = S.arena_h; rg.hout = S.arena_h + (size_t)base * H; rg.in_row = Q.pr_inrow;
             rg.words = Q.pr_w; rg.dig = Q.pr_dig; rg.alg = Q.alg;
+            rg.dig_store = S.arena_dig; rg.deh_store = S.arena_deh; rg.dep_store = S.arena_dep; rg.epoch = x_epoch;
             for (uint32_t q0 = 0, c = 0; q0 < n; q0 += xu::XR, c++)
                 xu::update_chunk<NT>(m, q0, (int)min((uint32_t)xu::XR, n - q0), (int)c, rg, gctr, tiles_done,
                                      tid, wid, lane, [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); },
@@ -754,7 +756,14 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
             }
         }
         cluster.sync();                                      // B: h', p and digests complete
-        if (rank == 1) continue;
+        if (rank == 1) {
+            // EXACT: the digit planes of the level's new rows, while rank 0
+            // runs assign and the next expand (off the per-level critical path)
+            if (EXACT && n && S.arena_dig)
+                xu::digitize_to_store<NT>(m, S.arena_h, base, n, S.arena_dig, S.arena_deh, S.arena_dep, x_epoch,
+                                          tid, wid, lane);
+            continue;
+        }
         SD_MARK(8);                                          // control waits for the update
         // ---------------- assign (rank 0) ----------------
         const StreamRange rg{sid, 0u, L.re - L.rb, 0u};
@@ -766,7 +775,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     }
     if (prof) {
         ph[11] = rank == 0 ? 1 : 0;
-        for (int i = 0; i < 24; i++) if (ph[i]) atomicAdd(&P.phase_ns[i], ph[i]);
+        for (int i = 0; i < 26; i++) if (ph[i]) atomicAdd(&P.phase_ns[i], ph[i]);
     }
 #undef SD_MARK
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -833,6 +842,7 @@ k_advance_exact(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restric
     rg.xs_slot = xu::xs_slot_bytes(m.wd_nkx);
     rg.hin = h_base; rg.hout = out_base + (size_t)out0 * m.H; rg.in_row = in_row; rg.words = words;
     rg.dig = rs.dig; rg.alg = alg;
+    rg.dig_store = nullptr; rg.deh_store = nullptr; rg.dep_store = nullptr; rg.epoch = 0;
     const int nmt = (m.H + BM - 1) / BM;
     uint32_t gctr = 0, tiles_done = 0;
     unsigned long long t0 = 0;

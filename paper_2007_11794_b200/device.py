@@ -305,7 +305,7 @@ class Plan:
     def phase_ns(self) -> dict:
         """Stream schedule, after ``profile``: device ns per phase summed over
         CTAs (utterance streams)."""
-        o = np.zeros(24, np.int64)
+        o = np.zeros(26, np.int64)
         _lib.check(_lib.load().otflm_plan_phase_ns(self.handle, o.ctypes.data, current_stream_ptr()),
                    "phase_ns")
         names = ("expand", "update_kloop", "update_drain", "update_epilogue", "hs_setup", "hs_pairs",
@@ -328,6 +328,8 @@ class Plan:
         out["x_hs_kloop"] = int(o[9])
         out["x_hs_gemm_epilogue"] = int(o[22])
         out["x_hs_maxent_lsig"] = int(o[23])
+        out["x_plane_rows"] = int(o[24])
+        out["x_plane_copy"] = int(o[25])
         return out
 
     def set_schedule(self, schedule: str) -> None:
@@ -337,11 +339,11 @@ class Plan:
         self.schedule = schedule
 
     def counters(self) -> dict:
-        out = np.zeros(5, np.int64)
+        out = np.zeros(6, np.int64)
         _lib.check(_lib.load().otflm_plan_counters(self.handle, _p(out), current_stream_ptr()),
                    "plan counters")
         return dict(sum_path=int(out[0]), sum_path_k=int(out[1]), hs_queries=int(out[2]),
-                    h2d_bytes=int(out[3]), exact_fallbacks=int(out[4]))
+                    h2d_bytes=int(out[3]), exact_fallbacks=int(out[4]), exact_rows_digitized_late=int(out[5]))
 
     def run(self, ngram: DeviceNgram, lm_weight: float = 1.0, precision: str = "fp64",
             use_graph: bool = True, stream: int | None = None) -> None:
