@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-queries", action="store_true", help="skip the config-d query microbench")
     ap.add_argument("--beam-sweep", action="store_true", help="add the config-c beam sweep extra")
+    ap.add_argument("--table4", action="store_true", help="add the Table-4 cache-capacity sweep extra")
     ap.add_argument("--config", default="e", choices=["b", "e"],
                     help="b: the headline config (default); e: 4096 utterances at V=64k sharded over ranks")
     ap.add_argument("--e-total", type=int, default=4096, help="config e: total utterances")
@@ -328,6 +329,67 @@ def beam_sweep(precision: str, beams=(1, 2, 4, 8, 16, 32, 64), n_utt: int = 8, f
         torch.cuda.empty_cache()
     return {"workload": f"config c: V=65536 H=512 MaxEnt 2^22, {n_utt} utterances x {frames} frames, "
                         f"breadth 3, {precision} update; L2 flushed before each run", "sweep": rows}
+
+
+def table4_sweep(precision: str, capacities_kb=(0, 16, 64, 256, 1024, -1), n_streams: int = 74,
+                 n_rounds: int = 12, n_templates: int = 40, frames: int = 100, seed: int = 23):
+    """The paper's Table-4 experiment (reference cli.py:195-228, :287-298):
+    decode throughput and cache behaviour versus RescoreCache capacity.
+    Repeated-command traffic (the acceptance crit-8 recipe, scaled up): each
+    of n_streams streams decodes n_rounds utterances drawn Zipf-wise from a
+    pool of n_templates config-b lattices; capacity 0 = unbounded cache reset
+    per utterance, positive capacities retain the bounded LFU cache (and the
+    IndexTable) across a stream's utterances; -1 = unbounded and retained.
+    Device time per round (lattices resident), summed over rounds.  The
+    device memoises every (c, w) value of a retained stream in HBM, so a
+    bounded capacity changes the reported cache counters (replayed by the
+    exact LFU policy after each decode, lfu.cuh) but not the work; the
+    unbounded retained row shows the compute saved by retention itself."""
+    import torch
+    from paper_2007_11794_b200 import synth
+    from paper_2007_11794_b200.rescore import BatchDecoder
+    base = synth.build_setup("b", n_utt=n_templates, T=frames, seed=seed)
+    rng = np.random.default_rng(seed)
+    p = 1.0 / np.arange(1, n_templates + 1) ** 1.0
+    p /= p.sum()
+    picks = rng.choice(n_templates, size=(n_rounds, n_streams), p=p)
+    rows = []
+    for cap in capacities_kb:
+        retain = cap != 0
+        cap = max(cap, 0)
+        need = max(BatchDecoder.contexts_needed(base.lattices, base.beam), 1) * (n_rounds if retain else 1)
+        dec = BatchDecoder(base.model, base.tree, base.small_lm, n_streams, need, precision=precision,
+                           capacity_bytes=cap * 1024)
+        ms = 0.0
+        fr = 0
+        for k in range(n_rounds):
+            dec.prepare([base.lattices[int(t)] for t in picks[k]], base.beam)
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record()
+            dec.run(1.0, retain=retain and k > 0)
+            b.record()
+            torch.cuda.synchronize()
+            ms += a.elapsed_time(b)
+            hyps, _ = dec.fetch()
+            fr += sum(len(h.arcs) for h in hyps)
+        st = dec.streams.stats()                 # cumulative columns 4..6 after the last round
+        look, hit, miss = (int(st[:, 4].sum() + st[:, 0].sum()), int(st[:, 5].sum() + st[:, 1].sum()),
+                           int(st[:, 6].sum() + st[:, 2].sum()))
+        cs = dec.streams.cache_stats()
+        rows.append({"capacity_kb": cap, "retain": retain, "frames_per_s": fr / (ms / 1e3),
+                     "rtf_per_stream": (ms / 1e3) / n_rounds / (frames * FRAME_S),
+                     "lookups": look, "hits": hit, "computes": miss,
+                     "hit_ratio": hit / look if look else 0.0,
+                     "evictions_cumulative": int(cs[:, 1].sum()), "evictions_last_round": int(cs[:, 0].sum()),
+                     "resident_entries": int(cs[:, 2].sum())})
+        del dec
+        torch.cuda.empty_cache()
+    return {"workload": f"Table 4 (cli.py:195-228): {n_streams} streams x {n_rounds} utterances each, drawn "
+                        f"Zipf(1) from {n_templates} config-b lattices x {frames} frames; {precision}; "
+                        "capacity 0 = unbounded cache reset per utterance, else retained LFU cache",
+            "sweep": rows}
 
 
 def cpu_baseline(setup, n_sample: int, threads: int):
@@ -628,6 +690,8 @@ def run_config_e(args):
     extras = {}
     if rank == 0 and not args.no_queries:
         extras["config_d_queries"] = query_microbench("exact" if args.precision == "exact" else args.precision)
+    if rank == 0 and args.table4:
+        extras["table4_capacity_sweep"] = table4_sweep(args.precision)
     if rank == 0:
         line = {
             "metric": METRIC_E,
@@ -870,6 +934,8 @@ def run_config_b(args):
         extras["all_word_logprobs"] = all_word_microbench(args.precision)
     if rank == 0 and args.beam_sweep:
         extras["config_c_beam_sweep"] = beam_sweep(args.precision)
+    if rank == 0 and args.table4:
+        extras["table4_capacity_sweep"] = table4_sweep(args.precision)
     if rank == 0 and args.twopass_n > 0:
         extras["twopass"] = twopass_microbench(setup, args.precision, args.twopass_n)
     line = {

@@ -660,11 +660,16 @@ class BatchDecoder:
         self.plan = self.plans[0]
         return self.plans
 
-    def run(self, lm_weight: float = 1.0, use_graph: bool = True, slot: int | None = None) -> None:
+    def run(self, lm_weight: float = 1.0, use_graph: bool = True, slot: int | None = None,
+            retain: bool = False) -> None:
+        """Decode the current batch (one utterance per stream).  retain=True
+        keeps every stream's IndexTable and (bounded) cache from its previous
+        utterance (reset_utterance(retain=True), cache.py:185-191) -- the
+        paper's Table-4 setting; False starts fresh streams."""
         if slot is not None:
             self._activate(slot)
         self._lm_weight = lm_weight
-        self.streams.reset(retain=False)
+        self.streams.reset(retain=bool(retain))
         if self.group is not None:
             self.group.run(self.ngram, lm_weight, self.precision)
         else:
