@@ -185,6 +185,11 @@ __device__ __forceinline__ void setup(const DevModel &m, const DevPlan &Q, const
                     r = atomicAdd(&hs.misc[0], 1u);
                     if (r < (uint32_t)RCAP) hs.nrow[r] = node;
                     else { atomicOr(S.err, OTF_E_VALUE); r = RCAP - 1; }
+                    // its digit planes ([kc][plane][64 B], contiguous) into L2 now,
+                    // so the GEMM's row gathers hit L2
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                                 :: "l"(m.NVd + (size_t)node * m.wd_nkx * xu::NPW * xu::KC),
+                                    "r"((uint32_t)(m.wd_nkx * xu::NPW * xu::KC)) : "memory");
                     *reinterpret_cast<volatile uint16_t *>(&hs.hval[h]) = (uint16_t)r;
                     break;
                 }
