@@ -1552,9 +1552,11 @@ static bool sd_config(const DevModel &m, int prec, SdConfig *c) {
         if (!m.Wd || m.H % 4 != 0 || m.H > 512 || !m.U || !m.NV || !m.path_off) return false;
         if (!m.NVd) return false;
         const size_t budget = 200u * 1024u;
-        const size_t tail = xu::tail_layout().total;
-        c->stages = (int)std::min<size_t>(4, (budget - tail) / xu::STAGE);
-        if (c->stages < 2) return false;
+        // 2 ring stages + the staged U block of a tile (the epilogue reads U
+        // from shared memory); the K loop is MMA-bound with W planes in L2
+        const size_t tail = xu::tail_layout().total + xu::US_BYTES;
+        c->stages = 2;
+        if ((size_t)c->stages * xu::STAGE + tail > budget) return false;
         const int ord = m.order <= 3 ? 3 : OTF_MAX_ORDER;
         // rank 1: the update ring + tail; rank 0: the HS ring + pair tables
         const size_t hs_bytes = (size_t)xh::ring_bytes() + xh::layout(ord).total;
@@ -1599,7 +1601,7 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
         CK(cudaFuncSetAttribute(k_decode_streams<MODE, KCB, CPL, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem)); \
         k_decode_streams<MODE, KCB, CPL, ORD><<<2 * p->n_utt, sd::NT, c.smem, s>>>(m, d, S, g->d, (long long)p->beam, lm, \
                                                                               c.stages, c.qb_max, cursor, limit, c.tmem_cols, \
-                                                                              p->xs, xs_stride, x_epoch); \
+                                                                              p->xs, xs_stride, x_epoch, 1); \
     } while (0)
 #define SD_ORD(MODE, KCB, CPL) do { if (m.order <= 3) SD_LAUNCH(MODE, KCB, CPL, 3); else SD_LAUNCH(MODE, KCB, CPL, OTF_MAX_ORDER); } while (0)
 #define SD_H(MODE)                                                                                              \

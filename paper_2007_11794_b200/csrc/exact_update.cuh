@@ -291,7 +291,10 @@ struct Ring {
     uint32_t epoch;
     uint8_t *xs;                   // this stream's global digit scratch: 2 chunk slots (by parity)
     size_t xs_slot;                // bytes per slot
+    float *us;                     // [XR][128] U[w_r, tile units], staged during the tile's K loop
+                                   // (nullptr: the epilogue reads U from global memory)
 };
+constexpr uint32_t US_BYTES = (uint32_t)XR * 128 * 4;
 constexpr uint32_t STAGE = (uint32_t)NPW * PLANE_W + 4u * XR * KC;
 constexpr uint32_t HOFF = (uint32_t)NPW * PLANE_W;
 // rank 1's shared memory after its ring (byte offsets); sh / eh are double
@@ -643,6 +646,17 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                 named_sync(3, NT - 64);
                 if (tid == 64) fallbacks_done(mt - 1);
             }
+            if (wid >= 2 && rg.us) {
+                // this tile's U block U[w_r, mt*128 + (0..127)] into shared memory,
+                // under the K loop (the previous epilogue is done with it)
+                const int u0 = mt * tc::BM;
+                for (int i = tid - 64; i < R * 32; i += NT - 64) {
+                    const int r = i >> 5, c4 = (i & 31) * 4;
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (u0 + c4 < H) v = __ldg(reinterpret_cast<const float4 *>(m.U + (size_t)rg.wrd[r] + u0 + c4));
+                    *reinterpret_cast<float4 *>(rg.us + r * 128 + c4) = v;
+                }
+            }
             if (wid == 1) {
                 produce(mt, mt == mt0 ? 0 : npre, NK);
             } else if (wid == 0) {
@@ -708,8 +722,13 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                 const int r0 = it * 4;
                 mark(17);
                 float uv[4];          // U[w, unit] of the group's rows (V H < 2^31: 32-bit offsets)
+                if (rg.us) {
 #pragma unroll
-                for (int g = 0; g < 4; g++) uv[g] = __ldg(ucol + rg.wrd[min(r0 + g, R - 1)]);
+                    for (int g = 0; g < 4; g++) uv[g] = rg.us[min(r0 + g, R - 1) * 128 + quad * 32 + lane];
+                } else {
+#pragma unroll
+                    for (int g = 0; g < 4; g++) uv[g] = __ldg(ucol + rg.wrd[min(r0 + g, R - 1)]);
+                }
                 long long th[4], tl[4];
                 {
                     uint32_t D[NDIAG][4];

@@ -370,7 +370,7 @@ template <int MODE, int KC_B, int CPL, int ORD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sd::NT, 1)
 k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, double lm_weight, int stages,
                  int qb_max, uint32_t *cursor, uint32_t row_limit, uint32_t tmem_cols, uint8_t *xscratch,
-                 size_t xs_stride, uint32_t x_epoch) {
+                 size_t xs_stride, uint32_t x_epoch, int x_stage_u) {
     using namespace tc;
     namespace cg = cooperative_groups;
     constexpr bool X3 = MODE == 1;
@@ -552,6 +552,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
                     rg.hin = S.arena_h; rg.hout = S.arena_h + (size_t)base * H; rg.in_row = Q.pr_inrow;
                     rg.words = Q.pr_w; rg.dig = Q.pr_dig; rg.alg = Q.alg;
                     rg.dig_store = nullptr; rg.deh_store = nullptr; rg.dep_store = nullptr; rg.epoch = 0;
+                    rg.us = nullptr;
                     xu::update_chunk<NT>(m, q0, nq, (int)c, rg, gctr_u, tiles_done, tid, wid, lane,
                                          [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); },
                                          []() {}, prof ? ph : nullptr, t0, x_nmt - x_r0_tiles, x_nmt, false);
@@ -585,6 +586,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
             rg.tab = reinterpret_cast<const double *>(tail + tl.tab);
             rg.xs = xscratch + (size_t)u * xs_stride;
             rg.xs_slot = xu::xs_slot_bytes(m.wd_nkx);
+            rg.us = x_stage_u ? reinterpret_cast<float *>(tail + tl.total) : nullptr;
             rg.hin = S.arena_h; rg.hout = S.arena_h + (size_t)base * H; rg.in_row = Q.pr_inrow;
             rg.words = Q.pr_w; rg.dig = Q.pr_dig; rg.alg = Q.alg;
             rg.dig_store = S.arena_dig; rg.deh_store = S.arena_deh; rg.dep_store = S.arena_dep; rg.epoch = x_epoch;
@@ -843,6 +845,7 @@ k_advance_exact(DevModel m, uint32_t n_cap, RowSpec rs, const int32_t *__restric
     rg.hin = h_base; rg.hout = out_base + (size_t)out0 * m.H; rg.in_row = in_row; rg.words = words;
     rg.dig = rs.dig; rg.alg = alg;
     rg.dig_store = nullptr; rg.deh_store = nullptr; rg.dep_store = nullptr; rg.epoch = 0;
+    rg.us = nullptr;
     const int nmt = (m.H + BM - 1) / BM;
     uint32_t gctr = 0, tiles_done = 0;
     unsigned long long t0 = 0;
