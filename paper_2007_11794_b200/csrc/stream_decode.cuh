@@ -512,6 +512,9 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
             constexpr int HS_NT = NT - 64;
             const xh::Smem xs_m = xh::carve(smem, ORD);
             const uint32_t eh_off = (uint32_t)stages * xu::STAGE + xu::tail_layout().eh;
+            // a level whose requests all hit the cache (retained streams) computes
+            // nothing, but assign still needs every request's small-LM score
+            if (n == 0) small_lm_scores(Q, S, g, sid, L.re - L.rb, tid, NT);
             for (uint32_t q0 = 0, c = 0; q0 < n; q0 += xu::XR, c++) {
                 const int nq = (int)min((uint32_t)xu::XR, n - q0);
                 if (tid < HS_NT) xh::setup<ORD, HS_NT>(m, Q, S, q0, nq, xs_m, tid, lane);

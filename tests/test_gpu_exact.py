@@ -84,3 +84,37 @@ def test_exact_level_schedule_identical_to_oracle(case):
     ref = O.decode_many(s.model, s.tree, s.small_lm, s.lattices, beam=beam, enabled=enabled, n_threads=4)
     hyps, out, st = _decode(s, "exact", "level", beam, enabled)
     _assert_identical(hyps, out, st, ref)
+
+
+@pytest.mark.parametrize("capacity", [0, 32 * 4000])
+def test_exact_stream_retained_streams_vs_oracle(capacity):
+    """Retained streams (BatchDecoder.run(retain=True), reset_utterance(retain=True),
+    cache.py:185-191): each stream decodes a sequence of utterances with
+    repeats, so whole levels hit the cache (nothing computed) -- their
+    requests still need the small-LM term.  Per round: 1-best, score, end
+    context and cache counters equal an oracle stack with the same history;
+    unbounded and capacity-bounded (LFU) caches."""
+    from paper_2007_11794_b200 import synth
+    from paper_2007_11794_b200.rescore import BatchDecoder
+    s = synth.build_setup("a", n_utt=3, T=30, seed=13)
+    seqs = [[0, 1, 0, 0], [2, 2, 1, 2]]          # stream -> lattice per round
+    need = BatchDecoder.contexts_needed(s.lattices, 8) * 4
+    dec = BatchDecoder(s.model, s.tree, s.small_lm, len(seqs), need, precision="exact", capacity_bytes=capacity)
+    assert dec.schedule == "stream"
+    om, og = O.OracleModel(s.model, s.tree), O.OracleNgram(s.small_lm)
+    stacks = [O.OracleStack(om, None, capacity_bytes=capacity) for _ in seqs]
+    for k in range(4):
+        dec.prepare([s.lattices[q[k]] for q in seqs], 8)
+        dec.run(1.0, retain=k > 0)
+        hyps, out = dec.fetch()
+        st = dec.streams.stats()
+        for u, q in enumerate(seqs):
+            if k > 0:
+                stacks[u].reset(True)
+            r = stacks[u].rescore_onthefly(s.lattices[q[k]], og, beam=8)
+            o = stacks[u].stats()
+            assert hyps[u].arcs == r.arcs, (k, u)
+            assert abs(hyps[u].combined_score - r.combined_score) <= 1e-9, (k, u)
+            assert hyps[u].end_context == r.end_context, (k, u)
+            assert (int(st[u, 0]), int(st[u, 1]), int(st[u, 2])) == (o.lookups, o.hits, o.misses), (k, u)
+    assert int(st[:, 1].sum()) > 0          # the repeats really hit
