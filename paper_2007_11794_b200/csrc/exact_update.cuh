@@ -459,25 +459,25 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
     {
         const int Rp = (R + 15) & ~15;
         // ---- digitize the chunk's context rows: thread = (row, 16-element group) ----
+        // row table; with the per-row plane store also each row's freshness
+        // (planes made when the row was created in this launch: sh[r] = 1)
         for (int r = tid; r < R; r += NT) {
-            rg.src[r] = rg.in_row[q0 + r];
+            const int src = rg.in_row[q0 + r];
+            rg.src[r] = src;
             rg.wrd[r] = (rg.words ? rg.words[q0 + r] : (int32_t)(q0 + r)) * H;
-        }
-        __syncthreads();
-        mark(12);
-        if (digitize && rg.dig_store) {
-            // planes made when the rows were created (this launch): a flat
-            // copy into the chunk layout, six 16-byte pieces in flight per
-            // thread; other rows (the zero context, rows of an earlier launch
-            // or another schedule) are digitized here.  sh[r] = 1 marks fresh.
-            for (int r = tid; r < R; r += NT) {
-                const int src = rg.src[r];
+            if (digitize && rg.dig_store) {
                 const bool fresh = rg.dep_store[src] == rg.epoch;
                 rg.sh[r] = fresh ? 1.0 : 0.0;
                 if (!fresh && rg.alg) atomicAdd(&rg.alg[5], 1ull);
                 if (fresh) rg.eh[r] = (double)rg.deh_store[src];
             }
-            __syncthreads();
+        }
+        __syncthreads();
+        mark(12);
+        if (digitize && rg.dig_store) {
+            // fresh rows: a copy of their planes into the chunk layout; other
+            // rows (the zero context, rows of an earlier launch or another
+            // schedule) are digitized here
             mark(24);
             // warp per (kc, plane) block: lane = c * 8 + (row & 7), so each of the
             // block's 8-row groups is one contiguous 512-byte write of the
