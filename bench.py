@@ -7,11 +7,11 @@ configs[4] / SURVEY.md §8d config e): synthetic HS+MaxEnt RNNLM with
 V=65,536, H=512, MaxEnt 2^22, 4,096 utterances x 300 frames (one lattice
 step = one 10 ms frame), breadth 3, beam 8, bigram small LM, fresh streams
 per utterance.  The utterances are sharded over the ranks (strong scaling:
-the total is fixed); each rank decodes its shard in batches of 74 streams
-(74 two-CTA clusters = 148 SMs) through the double-buffered BatchDecoder, in
-the EXACT precision (integer digit-plane tcgen05 update with certified
-rounding + float64 HS: every hidden state and 1-best bit-identical to the
-reference).  NCCL only all-gathers the per-utterance result records.
+the total is fixed); each rank decodes its shard in batches of 148 streams
+(one CTA per stream on each of the 148 SMs, k_decode_solo) through the
+double-buffered BatchDecoder, in the EXACT precision (integer digit-plane
+tcgen05 update with certified rounding + digit-plane HS: every hidden state
+and 1-best identical to the reference).  NCCL only all-gathers the per-utterance result records.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--precision P] [--config e|b]
   python bench.py --impl reference      # CPU arm: the reference algorithm on host cores
@@ -54,7 +54,7 @@ def parse():
     ap.add_argument("--frames", type=int, default=300)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--groups", type=int, default=4, help="concurrent level chains per GPU (level schedule)")
-    ap.add_argument("--schedule", default="auto", choices=["auto", "level", "stream"],
+    ap.add_argument("--schedule", default="auto", choices=["auto", "level", "stream", "stream1"],
                     help="decode schedule: persistent per-stream kernel or level-synchronous graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-queries", action="store_true", help="skip the config-d query microbench")
@@ -63,8 +63,9 @@ def parse():
     ap.add_argument("--config", default="e", choices=["b", "e"],
                     help="b: the headline config (default); e: 4096 utterances at V=64k sharded over ranks")
     ap.add_argument("--e-total", type=int, default=4096, help="config e: total utterances")
-    ap.add_argument("--e-batch", type=int, default=74,
-                    help="config e: streams decoded at once per GPU (74 2-CTA clusters = 148 SMs)")
+    ap.add_argument("--e-batch", type=int, default=148,
+                    help="config e: streams decoded at once per GPU (148: one CTA per stream per SM; "
+                         "<= 74 selects the 2-CTA cluster kernel)")
     ap.add_argument("--all-word", action="store_true", help="add the all_word_logprobs extra")
     ap.add_argument("--twopass-n", type=int, default=1000, help="n-best size of the two-pass extra (0: skip)")
     ap.add_argument("--out", default=None, help="also write the JSON line here")
@@ -652,10 +653,11 @@ def run_config_e(args):
     run_ms = sum(v[0] for v in prof.values())
     share = prof["stream"][0] / run_ms if "stream" in prof and run_ms > 0 else 1.0
     n_batches = len(batches)
-    kern_ms = dev_ms / n_batches * share                  # avg k_decode_streams launch, timed region
+    kern_ms = dev_ms / n_batches * share                  # avg persistent-kernel launch, timed region
     byt = byt0 * (total_requests / world / n_batches) / max(req0, 1)   # per launch, scaled to the timed batches
     hbm, tc_peak, peak_src = peaks()
-    roof = {"kernel": "k_decode_streams (persistent: expand + tcgen05 digit-plane update + f64 HS + assign)",
+    kname = "k_decode_solo" if dec.schedule == "stream1" else "k_decode_streams"
+    roof = {"kernel": kname + " (persistent: expand + tcgen05 digit-plane update + digit-plane HS + assign)",
             "bound": "hbm", "achieved": byt / (kern_ms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
             "traffic": None, "peak_source": peak_src, "avg_launch_us": kern_ms * 1e3,
             "algorithmic_bytes_per_launch": byt, "launches_per_step": n_batches,
@@ -663,7 +665,7 @@ def run_config_e(args):
             "tensor_int8_tops": 17 * 2.0 * H * H * miss0 / (prof.get("stream", (run_ms, 1))[0] / 1e3) / 1e12}
     roof["frac"] = roof["achieved"] / roof["peak"]
     tfile = ROOT / "profiles" / "traffic.json"
-    key = f"k_decode_streams_e_{args.precision}"
+    key = f"{kname}_e_{args.precision}"
     if tfile.exists():
         try:
             tj = json.loads(tfile.read_text()).get(key)
@@ -867,7 +869,7 @@ def run_config_b(args):
     roof["avg_launch_us"] = dom_ms * 1e3 / max(dom_n, 1)
     kernel_ms = {k: round(v[0], 4) for k, v in prof.items() if v[1]}
     phases = None
-    if dec.schedule == "stream":
+    if dec.schedule != "level":
         ph = dec.plan.phase_ns()
         n_lv = max(1, args.frames)
         phases = {k: round(ph[k] / max(ph["ctas"], 1) / n_lv / 1e3, 3)

@@ -55,6 +55,9 @@ extern "C" {
                                  for the whole batch (CUDA graph); every precision */
 #define OTFLM_SCHED_STREAM 1  /* persistent: one CTA per utterance stream runs all of its levels in
                                  one launch (TF32X3 / TF32, H % 4 == 0, H <= 512) */
+#define OTFLM_SCHED_STREAM1 2  /* OTFLM_PREC_EXACT only: one CTA per utterance stream runs the whole
+                                 level chain (HS and update GEMMs in turn on its own tensor core);
+                                 for batches with at least one stream per SM (exact_solo.cuh) */
 
 typedef struct OtflmModel OtflmModel;
 typedef struct OtflmNgram OtflmNgram;

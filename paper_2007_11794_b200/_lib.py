@@ -21,7 +21,7 @@ ERR_NOMEM, ERR_CYCLE, ERR_PACK, ERR_CUDA, ERR_HASH = -6, -7, -8, -9, -10
 
 PREC = {"fp64": 0, "tf32x3": 1, "bf16": 2, "tf32": 3, "exact": 4}
 PROFILE_CATEGORIES = ("expand", "hs", "advance", "assign", "final", "misc", "stream")
-SCHED = {"level": 0, "stream": 1}
+SCHED = {"level": 0, "stream": 1, "stream1": 2}
 
 
 class UnknownIndexError(KeyError):

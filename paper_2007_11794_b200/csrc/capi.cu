@@ -16,6 +16,7 @@
 #include "hs.cuh"
 #include "tc_advance.cuh"
 #include "stream_decode.cuh"
+#include "exact_solo.cuh"
 
 // --------------------------------------------------------------------------
 static thread_local std::string g_detail;
@@ -1635,7 +1636,19 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
             if (p->mem.alloc(&x, need) != cudaSuccess) { g_detail = "cudaMalloc exact scratch"; return OTFLM_ERR_NOMEM; }
             p->xs = x; p->xs_bytes = need;
         }
-        if (m.H <= 128) SD_ORD(4, 64, 1);
+        if (p->schedule == OTFLM_SCHED_STREAM1) {
+            // one CTA per stream (exact_solo.cuh)
+            const int ord = m.order <= 3 ? 3 : OTF_MAX_ORDER;
+            const size_t smem = xs1::smem_bytes(ord);
+#define SO_LAUNCH(ORD)                                                                                          \
+            do {                                                                                                \
+                CK(cudaFuncSetAttribute(k_decode_solo<ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+                k_decode_solo<ORD><<<p->n_utt, sd::NT, smem, s>>>(m, d, S, g->d, (long long)p->beam, lm, cursor, limit, \
+                                                                  p->xs, xs_stride, x_epoch);                     \
+            } while (0)
+            if (ord == 3) SO_LAUNCH(3); else SO_LAUNCH(OTF_MAX_ORDER);
+#undef SO_LAUNCH
+        } else if (m.H <= 128) SD_ORD(4, 64, 1);
         else if (m.H <= 256) SD_ORD(4, 64, 2);
         else SD_ORD(4, 64, 4);
     } else {
@@ -1662,7 +1675,8 @@ static int enqueue_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int pre
 }
 
 extern "C" int otflm_plan_set_schedule(OtflmPlan *p, int32_t schedule) {
-    if (!p || (schedule != OTFLM_SCHED_LEVEL && schedule != OTFLM_SCHED_STREAM)) return OTFLM_ERR_VALUE;
+    if (!p || (schedule != OTFLM_SCHED_LEVEL && schedule != OTFLM_SCHED_STREAM && schedule != OTFLM_SCHED_STREAM1))
+        return OTFLM_ERR_VALUE;
     p->schedule = schedule;
     return OTFLM_OK;
 }
@@ -1671,11 +1685,14 @@ extern "C" int otflm_schedule_supported(const OtflmModel *m, int32_t schedule, i
     if (!m) return 0;
     if (schedule == OTFLM_SCHED_LEVEL) return prec_ok(precision) ? 1 : 0;
     SdConfig c;
+    if (schedule == OTFLM_SCHED_STREAM1)
+        return precision == OTFLM_PREC_EXACT && sd_config(m->d, precision, &c) &&
+               xs1::smem_bytes(m->d.order <= 3 ? 3 : OTF_MAX_ORDER) <= 207u * 1024u ? 1 : 0;
     return schedule == OTFLM_SCHED_STREAM && sd_config(m->d, precision, &c) ? 1 : 0;
 }
 
 static int enqueue_any(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, cudaStream_t s) {
-    return p->schedule == OTFLM_SCHED_STREAM ? enqueue_streams(p, g, lm, prec, s) : enqueue_run(p, g, lm, prec, s);
+    return p->schedule != OTFLM_SCHED_LEVEL ? enqueue_streams(p, g, lm, prec, s) : enqueue_run(p, g, lm, prec, s);
 }
 
 static int64_t g_last_launches = 0;
@@ -1701,7 +1718,7 @@ static int decode_run_impl(OtflmPlan *p, const OtflmNgram *g, double lm_weight, 
     if (g->d.V < p->st->m->d.V) { g_detail = "small LM vocabulary smaller than model"; return OTFLM_ERR_VALUE; }
     cudaStream_t s = (cudaStream_t)stream;
     g_launches = 0;
-    if (!use_graph || p->schedule == OTFLM_SCHED_STREAM) {   // the persistent schedule is 3 launches
+    if (!use_graph || p->schedule != OTFLM_SCHED_LEVEL) {   // the persistent schedules are 3 launches
         int rc = enqueue_any(p, g, lm_weight, precision, s);
         g_last_launches = g_launches;
         return rc;

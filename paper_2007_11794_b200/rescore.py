@@ -571,14 +571,14 @@ class BatchDecoder:
         self.ngram = DeviceNgram.get(small_lm, self.dmodel)
         self.precision = precision
         if schedule == "auto":
-            schedule = "stream" if schedule_supported(self.dmodel, "stream", precision) else "level"
+            schedule = auto_schedule(self.dmodel, precision, n_streams)
         if schedule not in _lib.SCHED:
             raise ValueError(f"unknown schedule {schedule!r}")
-        if schedule == "stream" and not schedule_supported(self.dmodel, "stream", precision):
-            raise ValueError(f"the stream schedule does not support precision {precision!r} / this model")
+        if schedule != "level" and not schedule_supported(self.dmodel, schedule, precision):
+            raise ValueError(f"the {schedule} schedule does not support precision {precision!r} / this model")
         self.schedule = schedule
         # concurrent groups only help the level-synchronous schedule
-        self.n_groups = 1 if schedule == "stream" else max(1, min(int(n_groups), n_streams))
+        self.n_groups = 1 if schedule != "level" else max(1, min(int(n_groups), n_streams))
         self.arena_rows = n_streams * max_contexts + 2
         self.streams = DeviceStreams(self.dmodel, n_streams, enabled=enabled,
                                      max_contexts=max_contexts,
@@ -765,6 +765,21 @@ class BatchDecoder:
                 lo.arc_ref = arc          # arc id in the input lattice, per output arc
                 out.append(lo)
         return out
+
+
+def auto_schedule(dmodel, precision: str, n_streams: int) -> str:
+    """The persistent per-stream kernel where the precision has one: in
+    EXACT, one CTA per stream ("stream1") once the batch has more streams
+    than half the SMs (a 2-CTA cluster per stream would need a second wave),
+    else the 2-CTA cluster ("stream"); otherwise the level schedule."""
+    if schedule_supported(dmodel, "stream", precision):
+        if schedule_supported(dmodel, "stream1", precision):
+            torch = cuda()
+            n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+            if 2 * n_streams > n_sm:
+                return "stream1"
+        return "stream"
+    return "level"
 
 
 def schedule_supported(dmodel, schedule: str, precision: str) -> bool:

@@ -46,13 +46,16 @@ def _assert_identical(hyps, out, st, ref):
 CASES = [("a", 12, 60, 8, True), ("a", 6, 30, 32, False), ("b", 6, 60, 8, True), ("c", 3, 30, 8, True)]
 
 
+@pytest.mark.parametrize("schedule", ["stream", "stream1"])
 @pytest.mark.parametrize("case", CASES)
-def test_exact_stream_identical_to_oracle(case):
+def test_exact_stream_identical_to_oracle(case, schedule):
+    """Both persistent schedules: the 2-CTA cluster per stream and the
+    one-CTA-per-stream kernel (exact_solo.cuh)."""
     from paper_2007_11794_b200 import synth
     name, n_utt, T, beam, enabled = case
     s = synth.build_setup(name, n_utt=n_utt, T=T, seed=5)
     ref = O.decode_many(s.model, s.tree, s.small_lm, s.lattices, beam=beam, enabled=enabled, n_threads=4)
-    hyps, out, st = _decode(s, "exact", "stream", beam, enabled)
+    hyps, out, st = _decode(s, "exact", schedule, beam, enabled)
     _assert_identical(hyps, out, st, ref)
 
 
@@ -86,8 +89,9 @@ def test_exact_level_schedule_identical_to_oracle(case):
     _assert_identical(hyps, out, st, ref)
 
 
+@pytest.mark.parametrize("schedule", ["stream", "stream1"])
 @pytest.mark.parametrize("capacity", [0, 32 * 4000])
-def test_exact_stream_retained_streams_vs_oracle(capacity):
+def test_exact_stream_retained_streams_vs_oracle(capacity, schedule):
     """Retained streams (BatchDecoder.run(retain=True), reset_utterance(retain=True),
     cache.py:185-191): each stream decodes a sequence of utterances with
     repeats, so whole levels hit the cache (nothing computed) -- their
@@ -99,8 +103,8 @@ def test_exact_stream_retained_streams_vs_oracle(capacity):
     s = synth.build_setup("a", n_utt=3, T=30, seed=13)
     seqs = [[0, 1, 0, 0], [2, 2, 1, 2]]          # stream -> lattice per round
     need = BatchDecoder.contexts_needed(s.lattices, 8) * 4
-    dec = BatchDecoder(s.model, s.tree, s.small_lm, len(seqs), need, precision="exact", capacity_bytes=capacity)
-    assert dec.schedule == "stream"
+    dec = BatchDecoder(s.model, s.tree, s.small_lm, len(seqs), need, precision="exact", capacity_bytes=capacity,
+                       schedule=schedule)
     om, og = O.OracleModel(s.model, s.tree), O.OracleNgram(s.small_lm)
     stacks = [O.OracleStack(om, None, capacity_bytes=capacity) for _ in seqs]
     for k in range(4):
