@@ -1020,6 +1020,7 @@ struct OtflmPlan {
     uint64_t h2d_bytes = 0;
     unsigned long long *alg_buf = nullptr;
     uint8_t *xs = nullptr;             // exact stream mode: per-stream digit scratch (Allocs-owned)
+    uint32_t *work = nullptr;          // stream queue counter of the persistent one-CTA schedule
     size_t xs_bytes = 0;
     cudaStream_t side = nullptr;               // second branch of each level (HS)
     cudaStream_t chain = nullptr;              // this plan's chain inside a group graph
@@ -1637,14 +1638,22 @@ static int launch_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int prec
             p->xs = x; p->xs_bytes = need;
         }
         if (p->schedule == OTFLM_SCHED_STREAM1) {
-            // one CTA per stream (exact_solo.cuh)
+            // persistent CTAs (one per SM at most) taking the streams from a queue (exact_solo.cuh)
             const int ord = m.order <= 3 ? 3 : OTF_MAX_ORDER;
             const size_t smem = xs1::smem_bytes(ord);
+            int dev = 0, n_sm = 148;
+            CK(cudaGetDevice(&dev));
+            CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+            const uint32_t grid = std::max<uint32_t>(1, std::min<uint32_t>(p->n_utt, (uint32_t)n_sm));
+            if (!p->work) {
+                if (p->mem.alloc(&p->work, 1) != cudaSuccess) { g_detail = "cudaMalloc work queue"; return OTFLM_ERR_NOMEM; }
+            }
+            CK(cudaMemsetAsync(p->work, 0, sizeof(uint32_t), s));
 #define SO_LAUNCH(ORD)                                                                                          \
             do {                                                                                                \
                 CK(cudaFuncSetAttribute(k_decode_solo<ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-                k_decode_solo<ORD><<<p->n_utt, sd::NT, smem, s>>>(m, d, S, g->d, (long long)p->beam, lm, cursor, limit, \
-                                                                  p->xs, xs_stride, x_epoch);                     \
+                k_decode_solo<ORD><<<grid, sd::NT, smem, s>>>(m, d, S, g->d, (long long)p->beam, lm, cursor, limit, \
+                                                              p->xs, xs_stride, x_epoch, p->work);                \
             } while (0)
             if (ord == 3) SO_LAUNCH(3); else SO_LAUNCH(OTF_MAX_ORDER);
 #undef SO_LAUNCH

@@ -209,17 +209,22 @@ __device__ __forceinline__ void setup(const DevModel &m, const DevPlan &Q, const
 // ---- part 2 (the chunk's digits are in the scratch slot): the GEMM over
 // M tiles of distinct nodes, the epilogue, MaxEnt + log-sigmoid, path sums,
 // certification, the successor history and its digest.  All NT threads.
+template <int ORD>
+__device__ __forceinline__ void finish(const DevModel &m, DevPlan &Q, DevStreams &S, uint32_t base, uint32_t q0,
+                                       int nq, const Smem &hs, int ft, int FN, int bar);
+
 template <int ORD, int NT, typename WaitFn, typename SideFn>
 __device__ __forceinline__ void run(const DevModel &m, DevPlan &Q, DevStreams &S, uint32_t base, uint32_t q0,
                                     int nq, const uint8_t *xs_slot, const double *eh_remote, uint8_t *smem,
                                     const Smem &hs, uint32_t tmem, uint64_t *full, uint64_t *empty, uint64_t *done,
                                     uint32_t &gctr, uint32_t &tiles_done, int tid, int wid, int lane, WaitFn wait,
-                                    SideFn side, unsigned long long *ph, unsigned long long &t0) {
+                                    SideFn side, unsigned long long *ph, unsigned long long &t0,
+                                    bool defer_finish = false) {
     constexpr int NW = NT / 32;
     auto mark = [&](int i) {
         if (ph) { unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); ph[i] += t - t0; t0 = t; }
     };
-    const int H = m.H, NK = m.wd_nkx;
+    const int NK = m.wd_nkx;
     const int Rp = (nq + 15) & ~15;
     const uint32_t nrows = min(hs.misc[0], (uint32_t)RCAP);
     const uint32_t T = hs.misc[1];
@@ -366,8 +371,23 @@ __device__ __forceinline__ void run(const DevModel &m, DevPlan &Q, DevStreams &S
         __syncthreads();
     }
     mark(22);
+    if (defer_finish) return;
+    finish<ORD>(m, Q, S, base, q0, nq, hs, tid, NT, 5);
+    mark(23);
+}
+
+// The CUDA-core tail of a chunk's HS (after run's TMEM readout): MaxEnt
+// terms, log-sigmoid, per-query path sums with the certified delta, history
+// rows and digests, the float64 recompute of flagged queries.  Threads
+// [0, FN) of the caller's numbering ft take part (named barrier bar): the
+// whole CTA, or the warps that are idle under the next GEMM's K loop.
+template <int ORD>
+__device__ __forceinline__ void finish(const DevModel &m, DevPlan &Q, DevStreams &S, uint32_t base, uint32_t q0,
+                                       int nq, const Smem &hs, int ft, int FN, int bar) {
+    const int H = m.H, fw = ft >> 5, FNW = FN >> 5, lane = ft & 31;
+    const uint32_t T = hs.misc[1];
     // ---- MaxEnt terms in the reference's order, sign, float64 log-sigmoid ----
-    for (uint32_t j = (uint32_t)tid; j < T; j += NT) {
+    for (uint32_t j = (uint32_t)ft; j < T; j += (uint32_t)FN) {
         const int q = hs.pq[j];
         const uint32_t code = hs.pcode[j];
         double a = hs.act[j];
@@ -381,10 +401,10 @@ __device__ __forceinline__ void run(const DevModel &m, DevPlan &Q, DevStreams &S
         hs.errj[j] = __double2float_ru((double)hs.errj[j] + 8.0 * 1.1102230246251565e-16 * (fabs(a) + me_abs));
         hs.act[j] = otf_log_sigmoid((code & 0x80000000u) ? -a : a);
     }
-    __syncthreads();
+    sd::group_sync(bar, FN);
     // ---- per query: path-order sum, certification of delta, history, digest ----
-    if (tid < nq) {
-        const int t = tid;
+    if (ft < nq) {
+        const int t = ft;
         const uint32_t q = q0 + (uint32_t)t;
         const uint32_t o = hs.off[t], p = hs.P[t];
         double lp = 0.0, labs = 0.0, eb = 0.0;
@@ -421,8 +441,7 @@ __device__ __forceinline__ void run(const DevModel &m, DevPlan &Q, DevStreams &S
             atomicAdd(&Q.alg[2], 1ull);
         }
     }
-    __syncthreads();
-    mark(23);
+    sd::group_sync(bar, FN);
     // ---- uncertified queries: float64 CUDA-core activations (warp per pair) ----
     const uint32_t nf = hs.misc[2];
     if (nf) {
@@ -430,7 +449,7 @@ __device__ __forceinline__ void run(const DevModel &m, DevPlan &Q, DevStreams &S
             const int t = (int)hs.flag[f];
             const uint32_t o = hs.off[t], p = hs.P[t];
             const float *hrow = S.arena_h + (size_t)hs.row[t] * H;
-            for (uint32_t i = (uint32_t)wid; i < p; i += NW) {
+            for (uint32_t i = (uint32_t)fw; i < p; i += (uint32_t)FNW) {
                 const uint32_t code = hs.pcode[o + i];
                 const float *v = m.NV + (size_t)(code & 0x7FFFFFFFu) * H;
                 double a = 0.0;
@@ -442,15 +461,15 @@ __device__ __forceinline__ void run(const DevModel &m, DevPlan &Q, DevStreams &S
                 if (lane == 0) hs.act[o + i] = otf_log_sigmoid((code & 0x80000000u) ? -a : a);
             }
         }
-        __syncthreads();
-        if (tid < (int)nf) {
-            const int t = (int)hs.flag[tid];
+        sd::group_sync(bar, FN);
+        if (ft < (int)nf) {
+            const int t = (int)hs.flag[ft];
             double lp = 0.0;
             for (uint32_t i = 0; i < hs.P[t]; i++) lp += hs.act[hs.off[t] + i];
             Q.pr_p[q0 + (uint32_t)t] = lp;
         }
-        if (Q.alg && tid == 0) atomicAdd(&Q.alg[4], (unsigned long long)nf);
-        __syncthreads();
+        if (Q.alg && ft == 0) atomicAdd(&Q.alg[4], (unsigned long long)nf);
+        sd::group_sync(bar, FN);
     }
 }
 }  // namespace xh

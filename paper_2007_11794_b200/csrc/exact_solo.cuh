@@ -27,7 +27,12 @@ __host__ __device__ constexpr Small small_layout() {
     return Small{0u, 2u * xu::XR * 8, 4u * xu::XR * 8, 4u * xu::XR * 8 + 16, 4u * xu::XR * 8 + 16 + xu::XR * 4,
                  4u * xu::XR * 8 + 16 + 2u * xu::XR * 4, 4u * xu::XR * 8 + 16 + 2u * xu::XR * 4 + 32 * 8};
 }
-__host__ __device__ constexpr uint32_t overlay_bytes() { return 2u * xu::FBCAP * 4 + xu::US_BYTES; }
+// the update's fallback lists live on the HS node-dedup hash (idle after
+// xh::setup); its U staging block on the HS pair tables from the second M
+// tile on (the HS tail runs under the first tile's K loop)
+static_assert(2u * xu::FBCAP * 4 <= (uint32_t)xh::HCAP * 6, "fallback lists exceed the dedup hash");
+static_assert(xu::US_BYTES <= xh::layout(3).hkey, "U staging block overlaps the dedup hash");
+__host__ __device__ constexpr uint32_t overlay_bytes() { return xu::US_BYTES; }
 __host__ __device__ constexpr uint32_t tables_bytes(int ord) {
     return xh::layout(ord).total > overlay_bytes() ? xh::layout(ord).total : overlay_bytes();
 }
@@ -39,7 +44,7 @@ __host__ __device__ constexpr uint32_t smem_bytes(int ord) {
 template <int ORD>
 __global__ void __launch_bounds__(sd::NT, 1)
 k_decode_solo(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, double lm_weight, uint32_t *cursor,
-              uint32_t row_limit, uint8_t *xscratch, size_t xs_stride, uint32_t x_epoch) {
+              uint32_t row_limit, uint8_t *xscratch, size_t xs_stride, uint32_t x_epoch, uint32_t *work) {
     using namespace tc;
     constexpr int NT = sd::NT, NW = sd::NW;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -48,10 +53,9 @@ k_decode_solo(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, d
     __shared__ unsigned long long a_key[NT];
     __shared__ uint32_t a_row[NT], a_cn[NT], a_wsum[NW], a_cnt[4];
     __shared__ __align__(8) uint64_t bar_full[4], bar_empty[4], bar_done;
-    __shared__ uint32_t s_tmem, s_nprim, s_base, s_abort;
+    __shared__ uint32_t s_tmem, s_nprim, s_base, s_abort, s_u;
     const int tid = threadIdx.x, lane = tid & 31;
     const int wid = __shfl_sync(0xffffffffu, tid >> 5, 0);
-    const uint32_t u = blockIdx.x;
     const int H = m.H;
     const int nmt = (H + BM - 1) / BM;
     uint8_t *tables = smem + xh::ring_bytes();
@@ -78,14 +82,6 @@ k_decode_solo(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, d
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = s_tmem;
 
-    DevPlan Q = P;
-    if (u < P.n_utt) {
-        const uint32_t o = P.rq_off[u];
-        Q.rq_c += o; Q.rq_arc += o; Q.rq_parent += o; Q.rq_cslot += o; Q.rq_m += o; Q.rq_dslot += o;
-        Q.rq_w += o; Q.rq_state += o; Q.rq_score += o; Q.rq_slm += o; Q.rq_ps += o;
-        Q.pr_req += o; Q.pr_inrow += o; Q.pr_w += o; Q.pr_p += o; Q.pr_dig += o;
-    }
-    const uint32_t sid = u < P.n_utt ? P.utt_stream[u] : 0u;
     const AssignSmem asmem{a_key, a_row, a_cn, a_wsum, a_cnt, reinterpret_cast<unsigned long long *>(smem),
                            reinterpret_cast<uint32_t *>(smem + 16 * NT), reinterpret_cast<uint32_t *>(smem + 24 * NT)};
     const xh::Smem hs = xh::carve(smem, ORD);
@@ -93,17 +89,17 @@ k_decode_solo(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, d
     xu::Ring rg;
     rg.smem = smem; rg.stages = xh::STAGES; rg.tmem = tmem;
     rg.full = bar_full + xh::STAGES; rg.empty = bar_empty + xh::STAGES; rg.done = &bar_done;
-    rg.fb = reinterpret_cast<uint32_t *>(tables);                              // overlay (after the HS)
-    rg.us = reinterpret_cast<float *>(tables + 2 * xu::FBCAP * 4);             // overlay (after the HS)
+    rg.fb = reinterpret_cast<uint32_t *>(tables + xh::layout(ORD).hkey);
+    rg.us = reinterpret_cast<float *>(tables);      // overlay, from the second M tile (the HS tail is done)
     rg.sh = reinterpret_cast<double *>(small + sl.sh);
     rg.eh = reinterpret_cast<double *>(small + sl.eh);
     rg.fb_n = reinterpret_cast<uint32_t *>(small + sl.fbn);
     rg.src = reinterpret_cast<int32_t *>(small + sl.src);
     rg.wrd = reinterpret_cast<int32_t *>(small + sl.wrd);
     rg.tab = reinterpret_cast<const double *>(small + sl.tab);
-    rg.xs = xscratch + (size_t)u * xs_stride;
+    rg.xs = xscratch + (size_t)blockIdx.x * xs_stride;
     rg.xs_slot = xu::xs_slot_bytes(m.wd_nkx);
-    rg.hin = S.arena_h; rg.in_row = Q.pr_inrow; rg.words = Q.pr_w; rg.dig = Q.pr_dig; rg.alg = Q.alg;
+    rg.hin = S.arena_h;
     rg.dig_store = S.arena_dig; rg.deh_store = S.arena_deh; rg.dep_store = S.arena_dep; rg.epoch = x_epoch;
     uint32_t gctr_h = 0, gctr_u = 0, tiles_done = 0;
     auto wait = [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); };
@@ -112,7 +108,24 @@ k_decode_solo(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, d
     const bool prof = P.phase_ns != nullptr && tid == 0;
 #define SO_MARK(i) do { if (prof) { t1 = sd::gtimer(); ph[i] += t1 - t0; t0 = t1; } } while (0)
     if (prof) t0 = sd::gtimer();
-    const uint32_t l_begin = u < P.n_utt ? P.ul_off[u] : 0u, l_end = u < P.n_utt ? P.ul_off[u + 1] : 0u;
+    // persistent: each CTA takes the batch's streams from a queue, so a long
+    // utterance does not hold the launch while the other SMs idle
+    for (;;) {
+    if (tid == 0) s_u = atomicAdd(work, 1u);
+    __syncthreads();
+    const uint32_t u = s_u;
+    if (u >= P.n_utt) break;
+    DevPlan Q = P;
+    {
+        const uint32_t o = P.rq_off[u];
+        Q.rq_c += o; Q.rq_arc += o; Q.rq_parent += o; Q.rq_cslot += o; Q.rq_m += o; Q.rq_dslot += o;
+        Q.rq_w += o; Q.rq_state += o; Q.rq_score += o; Q.rq_slm += o; Q.rq_ps += o;
+        Q.pr_req += o; Q.pr_inrow += o; Q.pr_w += o; Q.pr_p += o; Q.pr_dig += o;
+    }
+    const uint32_t sid = P.utt_stream[u];
+    rg.in_row = Q.pr_inrow; rg.words = Q.pr_w; rg.dig = Q.pr_dig; rg.alg = Q.alg;
+    if (prof) ph[11]++;
+    const uint32_t l_begin = P.ul_off[u], l_end = P.ul_off[u + 1];
     for (uint32_t li = l_begin; li < l_end; li++) {
         const UttLevel L = P.ul[li];
         if (tid == 0) s_nprim = 0;
@@ -133,7 +146,7 @@ k_decode_solo(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, d
         }
         __syncthreads();
         SO_MARK(0);
-        if (s_abort) break;
+        if (s_abort) break;                          // (every later stream aborts at once too)
         const uint32_t base = s_base;
         rg.hout = S.arena_h + (size_t)base * H;
         if (n == 0) small_lm_scores(Q, S, g, sid, L.re - L.rb, tid, NT);
@@ -149,19 +162,22 @@ k_decode_solo(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, d
             xh::run<ORD, NT>(m, Q, S, base, q0, nq, rg.xs + (size_t)(c & 1) * rg.xs_slot, rg.eh + (c & 1) * xu::XR,
                              smem, hs, tmem, bar_full, bar_empty, &bar_done, gctr_h, tiles_done, tid, wid, lane, wait,
                              [&](int t2, int nt2) { if (c == 0) small_lm_scores(Q, S, g, sid, L.re - L.rb, t2, nt2); },
-                             prof ? ph : nullptr, t0);
+                             prof ? ph : nullptr, t0, /*defer_finish=*/true);
             SO_MARK(5);
-            // the recurrent update of the chunk over every M tile (planes already in the slot)
+            // the recurrent update of the chunk over every M tile (planes already
+            // in the slot); the HS tail (MaxEnt, log-sigmoid, path sums, flagged
+            // queries) runs on warps 2.. under the first tile's K loop
             xu::Ring rgc = rg;
             rgc.eh = rg.eh + (c & 1) * xu::XR;
+            rgc.fuse_store = S.arena_dig;          // the new rows' planes straight from the epilogue
+            rgc.out_row0 = base;
             xu::update_chunk<NT>(m, q0, nq, (int)c, rgc, gctr_u, tiles_done, tid, wid, lane, wait,
-                                 []() {}, prof ? ph : nullptr, t0, 0, nmt, false);
+                                 []() {}, prof ? ph : nullptr, t0, 0, nmt, false,
+                                 [&](int ft, int fn) { xh::finish<ORD>(m, Q, S, base, q0, nq, hs, ft, fn, 5); },
+                                 /*side_uses_us=*/true);
             __syncthreads();
         }
-        // the digit planes of the level's new rows, then the ordered resolution
-        if (n && S.arena_dig)
-            xu::digitize_to_store<NT>(m, S.arena_h, base, n, S.arena_dig, S.arena_deh, S.arena_dep, x_epoch,
-                                      tid, wid, lane);
+        // (the level's new rows got their digit planes in the update epilogue)
         __syncthreads();
         SO_MARK(6);
         const StreamRange rgs{sid, 0u, L.re - L.rb, 0u};
@@ -171,10 +187,10 @@ k_decode_solo(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, d
         __syncthreads();
         SO_MARK(7);
     }
-    if (prof) {
-        ph[11] = 1;
-        for (int i = 0; i < 26; i++) if (ph[i]) atomicAdd(&P.phase_ns[i], ph[i]);
+    __syncthreads();                               // s_u / s_abort reused by the next stream
     }
+    if (prof)
+        for (int i = 0; i < 26; i++) if (ph[i]) atomicAdd(&P.phase_ns[i], ph[i]);
 #undef SO_MARK
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();

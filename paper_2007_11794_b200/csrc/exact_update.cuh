@@ -293,6 +293,11 @@ struct Ring {
     size_t xs_slot;                // bytes per slot
     float *us;                     // [XR][128] U[w_r, tile units], staged during the tile's K loop
                                    // (nullptr: the epilogue reads U from global memory)
+    // non-null: the epilogue also writes each result's digit planes into
+    // this per-row store (row out_row0 + q; deh_store / dep_store as
+    // digitize_to_store), so no separate digitize pass follows the update
+    uint8_t *fuse_store = nullptr;
+    uint32_t out_row0 = 0;
 };
 constexpr uint32_t US_BYTES = (uint32_t)XR * 128 * 4;
 constexpr uint32_t STAGE = (uint32_t)NPW * PLANE_W + 4u * XR * KC;
@@ -432,11 +437,19 @@ __device__ __forceinline__ void digitize_to_store(const DevModel &m, const float
     }
 }
 
-template <int NT, typename WaitFn, typename SyncFn>
+struct NoSide {
+    __device__ void operator()(int, int) const {}
+};
+
+// side(t, n): work for warps 2.. (thread t of n) under the first tile's K
+// loop; when it uses the U staging area, side_uses_us makes the first tile's
+// epilogue read U from global memory instead
+template <int NT, typename WaitFn, typename SyncFn, typename SideFn = NoSide>
 __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int R, int chunk, const Ring &rg0, uint32_t &gctr,
                                              uint32_t &tiles_done, int tid, int wid, int lane, WaitFn wait,
                                              SyncFn digits_ready, unsigned long long *ph, unsigned long long &t0,
-                                             int mt0, int mt1, bool digitize) {
+                                             int mt0, int mt1, bool digitize, SideFn side = SideFn(),
+                                             bool side_uses_us = false) {
     constexpr int NW = NT / 32;
     const int H = m.H, NK = m.wd_nkx, nmt = (H + tc::BM - 1) / tc::BM;
     auto mark = [&](int i) {
@@ -464,6 +477,10 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
         for (int r = tid; r < R; r += NT) {
             const int src = rg.in_row[q0 + r];
             rg.src[r] = src;
+            if (rg.fuse_store && mt0 < mt1) {
+                rg.deh_store[rg.out_row0 + q0 + r] = 0.f;
+                rg.dep_store[rg.out_row0 + q0 + r] = rg.epoch;
+            }
             rg.wrd[r] = (rg.words ? rg.words[q0 + r] : (int32_t)(q0 + r)) * H;
             if (digitize && rg.dig_store) {
                 const bool fresh = rg.dep_store[src] == rg.epoch;
@@ -613,6 +630,19 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
             }
         };
         const int npre = min(rg.stages, NK);        // stages of a tile issued ahead (during the previous epilogue)
+        // result element (row, unit) = y into the per-row plane store (fused digitize):
+        // plane b is byte 3 - b of Y = rint(y 2^32) at byte offset (unit mod 64) of K chunk unit / 64
+        auto put_planes = [&](int row, int unit, float y) {
+            float err;
+            const uint32_t Y = digit_word(y, err);
+            const uint32_t orow = rg.out_row0 + q0 + (uint32_t)row;
+            uint8_t *dst = rg.fuse_store + ((size_t)orow * NK + (unit >> 6)) * 4 * KC + (unit & 63);
+            dst[0] = (uint8_t)(Y >> 24);
+            dst[KC] = (uint8_t)(Y >> 16);
+            dst[2 * KC] = (uint8_t)(Y >> 8);
+            dst[3 * KC] = (uint8_t)Y;
+            if (err != 0.f) atomicAdd(&rg.deh_store[orow], err * 1.01f);
+        };
         // the reference loop for tile mt's uncertified elements, a warp per
         // element among warps [w0, NW)
         auto fallbacks = [&](int mt, int w0) {
@@ -631,6 +661,7 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                 if (lane == 0) {
                     rg.hout[(size_t)(q0 + row) * H + un] = y;
                     if (rg.dig) atomicAdd(&rg.dig[q0 + row], otf_dig_h((uint32_t)un, y));
+                    if (rg.fuse_store) put_planes(row, un, y);
                 }
             }
         };
@@ -646,7 +677,9 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                 named_sync(3, NT - 64);
                 if (tid == 64) fallbacks_done(mt - 1);
             }
-            if (wid >= 2 && rg.us) {
+            const bool us_t = rg.us && !(side_uses_us && mt == mt0);
+            if (wid >= 2 && mt == mt0) side(tid - 64, NT - 64);
+            if (wid >= 2 && us_t) {
                 // this tile's U block U[w_r, mt*128 + (0..127)] into shared memory,
                 // under the K loop (the previous epilogue is done with it)
                 const int u0 = mt * tc::BM;
@@ -722,7 +755,7 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                 const int r0 = it * 4;
                 mark(17);
                 float uv[4];          // U[w, unit] of the group's rows (V H < 2^31: 32-bit offsets)
-                if (rg.us) {
+                if (us_t) {
 #pragma unroll
                     for (int g = 0; g < 4; g++) uv[g] = rg.us[min(r0 + g, R - 1) * 128 + quad * 32 + lane];
                 } else {
@@ -768,6 +801,7 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                         if (okv[g]) {
                             rg.hout[(size_t)(q0 + row) * H + unit] = yv[g];
                             dg[g] = otf_dig_h((uint32_t)unit, yv[g]);
+                            if (rg.fuse_store) put_planes(row, unit, yv[g]);
                         } else {
                             const uint32_t k = atomicAdd(fbn, 1u);
                             if (k < (uint32_t)FBCAP) fbl[k] = ((uint32_t)row << 16) | (uint32_t)unit;
@@ -776,6 +810,7 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                                                             rg.hin + (size_t)rg.src[row] * H, uv[g], H);
                                 rg.hout[(size_t)(q0 + row) * H + unit] = y;
                                 dg[g] = otf_dig_h((uint32_t)unit, y);
+                                if (rg.fuse_store) put_planes(row, unit, y);
                             }
                         }
                     }

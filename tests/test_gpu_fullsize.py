@@ -151,3 +151,35 @@ def test_fat_variant_vs_oracle(precision):
             assert r["self_consistency"] <= 1e-4 * T, (u, r)
             assert r["arcs"] or -2e-3 * T <= r["gap"] <= 1e-4 * T, (u, r)
     print(f"fat {precision}: schedule {dec.schedule}, identical 1-best {sum(r['arcs'] for r in rows)}/{len(rows)}")
+
+
+def test_fat_variant_full_length_exact_modes_agree():
+    """The fat variant at full length (4 x 300, breadth 16, beam 64: 19.5M
+    requests, 19.2M IndexTable rows) -- the shape where round 1's FP64 level
+    schedule stopped with a digest error.  FP64 (level schedule, CUDA-core
+    float64), EXACT level (k_advance_exact) and EXACT stream (digit-plane
+    tensor-core kernels) are three different code paths computing the
+    reference's arithmetic: every observable must agree between them, and
+    the table lengths are pinned to the measured FP64 result."""
+    from paper_2007_11794_b200 import synth
+    from paper_2007_11794_b200.rescore import BatchDecoder
+    s = synth.build_setup("b_fat", n_utt=4, T=300, seed=3)
+    need = BatchDecoder.contexts_needed(s.lattices, 64)
+    runs = {}
+    for prec, sched in (("fp64", "level"), ("exact", "level"), ("exact", "stream")):
+        dec = BatchDecoder(s.model, s.tree, s.small_lm, 4, need, precision=prec, schedule=sched)
+        dec.prepare(s.lattices, 64)
+        dec.run(1.0)
+        hyps, out = dec.fetch()
+        st = dec.streams.stats()
+        runs[(prec, sched)] = (hyps, out["expansions"].copy(), st[:, :4].copy())
+        del dec
+    h0, e0, s0 = runs[("fp64", "level")]
+    assert [int(x) for x in s0[:, 3]] == [4791301, 4792910, 4790610, 4790214]
+    assert int(e0.sum()) == 19481664
+    for key, (h, e, st) in runs.items():
+        assert np.array_equal(e, e0), key
+        assert np.array_equal(st, s0), key
+        for a, b in zip(h, h0):
+            assert a.arcs == b.arcs and a.end_context == b.end_context, key
+            assert abs(a.combined_score - b.combined_score) <= 1e-9, key
