@@ -1446,7 +1446,7 @@ extern "C" int otflm_plan_info(const OtflmPlan *p, int64_t *o) {
 
 extern "C" int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream) {
     if (!p || !o) return OTFLM_ERR_VALUE;
-    unsigned long long a[26] = {0};
+    unsigned long long a[28] = {0};
     CK(cudaMemcpyAsync(a, p->alg_buf + 8, sizeof(a), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     for (int i = 0; i < 12; i++) o[i] = (int64_t)a[i];
@@ -1454,6 +1454,7 @@ extern "C" int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream)
     for (int i = 0; i < 4; i++) o[17 + i] = (int64_t)a[12 + i];   // EXACT update: row table, digitize, spare
     for (int i = 0; i < 3; i++) o[21 + i] = (int64_t)a[21 + i];   // EXACT HS (rank 0): digits wait, GEMM, log-sigmoid
     o[24] = (int64_t)a[24]; o[25] = (int64_t)a[25];                 // EXACT update: plane-copy row pass, copy
+    o[26] = (int64_t)a[26]; o[27] = (int64_t)a[27];                 // EXACT update: MMA warp's K loop, epilogue stores
     return OTFLM_OK;
 }
 
@@ -1676,7 +1677,7 @@ static int enqueue_streams(OtflmPlan *p, const OtflmNgram *g, double lm, int pre
     DevPlan &d = p->d;
     if (d.kept) CK(cudaMemsetAsync(d.kept, 0, std::max<uint32_t>(p->n_slots, 1), s));
     CK(cudaMemsetAsync(d.arr, 0xFF, (size_t)std::max<uint32_t>(p->n_slots, 1) * sizeof(Arrival), s));
-    if (d.alg) CK(cudaMemsetAsync(d.alg, 0, 24 * sizeof(unsigned long long), s));
+    if (d.alg) CK(cudaMemsetAsync(d.alg, 0, 40 * sizeof(unsigned long long), s));   // counters + all phase slots
     { ProfScope ps(K_MISC, s); k_run_begin<<<cdiv(p->n_utt, 128), 128, 0, s>>>(d, S); CKL(); }
     { ProfScope ps(K_STREAM, s); int rc = launch_streams(p, g, lm, prec, s); if (rc) return rc; }
     { ProfScope ps(K_FINAL, s); k_final<<<cdiv(p->n_utt, 4), 128, 0, s>>>(d, S, lm, -1); CKL(); }

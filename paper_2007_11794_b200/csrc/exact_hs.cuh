@@ -296,28 +296,7 @@ __device__ __forceinline__ void run(const DevModel &m, DevPlan &Q, DevStreams &S
                 __syncwarp();
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 const uint32_t sW = tc::smem_u32(smem + (size_t)st * xu::STAGE);
-                const uint32_t sH = sW + xu::HOFF;
-#pragma unroll
-                for (int ks = 0; ks < xu::KC / 32; ks++) {
-                    const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
-                    auto range = [&](int a, int b0, int nb, uint32_t acc) {
-                        const int tot = nb * Rp;
-                        for (int off = 0; off < tot; off += 256) {
-                            const int nn = min(256, tot - off);
-                            const int brow = b0 * Rp + off;
-                            const uint64_t da = xu::desc(sW + (uint32_t)a * xu::PLANE_W + (uint32_t)ks * 256u);
-                            const uint64_t db = xu::desc(sH + (uint32_t)(brow >> 3) * 512u + (uint32_t)ks * 256u);
-                            xu::mma_i8(tmem + (uint32_t)((a + b0) * Rp + off), da, db, xu::idesc(a == 0, nn), acc);
-                        }
-                    };
-                    range(0, 0, 4, acc0);
-                    range(1, 0, 3, 1u);
-                    range(1, 3, 1, acc0);
-                    range(2, 0, 3, 1u);
-                    range(2, 3, 1, acc0);
-                    range(3, 0, 3, 1u);
-                    range(4, 0, 2, 1u);
-                }
+                xu::kc_pairs(Rp, kc == 0, tmem, xu::desc(sW), xu::desc(sW + xu::HOFF));
                 tc::commit_elect(tc::smem_u32(&empty[st]));
                 if (kc == NK - 1) tc::commit_elect(tc::smem_u32(done));
                 __syncwarp();

@@ -104,7 +104,7 @@ k_decode_solo(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, d
     uint32_t gctr_h = 0, gctr_u = 0, tiles_done = 0;
     auto wait = [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); };
 
-    unsigned long long ph[26] = {0}, t0 = 0, t1 = 0;
+    unsigned long long ph[28] = {0}, t0 = 0, t1 = 0;
     const bool prof = P.phase_ns != nullptr && tid == 0;
 #define SO_MARK(i) do { if (prof) { t1 = sd::gtimer(); ph[i] += t1 - t0; t0 = t1; } } while (0)
     if (prof) t0 = sd::gtimer();
@@ -190,7 +190,7 @@ k_decode_solo(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, d
     __syncthreads();                               // s_u / s_abort reused by the next stream
     }
     if (prof)
-        for (int i = 0; i < 26; i++) if (ph[i]) atomicAdd(&P.phase_ns[i], ph[i]);
+        for (int i = 0; i < 28; i++) if (ph[i] && (i < 16 || i > 20)) atomicAdd(&P.phase_ns[i], ph[i]);
 #undef SO_MARK
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();

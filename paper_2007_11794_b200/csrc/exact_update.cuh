@@ -55,9 +55,67 @@ __device__ __forceinline__ uint64_t desc(uint32_t saddr) {
     return d;
 }
 // D s32, A s8 (plane 0) or u8, B u8, K-major, M = 128
-__device__ __forceinline__ uint32_t idesc(bool a_signed, int n) {
-    return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(tc::BM >> 4) << 24);
+__host__ __device__ constexpr uint32_t idesc(bool a_signed, int n) {
+    return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
+// One MMA whose TMEM column, A / B descriptor offsets, instruction
+// descriptor and accumulate flag are immediates: only the three bases
+// (stage descriptors, TMEM base) go through the uniform datapath.  With
+// run-time offsets every MMA paid ~7 R2UR moves and ran at ~170 cycles
+// whatever its N (tools/kloop_micro.cu); with immediates the 17 digit pairs
+// of a K step run at the int8 tensor peak.
+template <uint32_t TOFF, uint32_t AOFF, uint32_t BOFF, uint32_t IDESC, int ACC>
+__device__ __forceinline__ void mma_imm(uint32_t tm, uint64_t da, uint64_t db) {
+    asm volatile("{\n\t.reg .pred e;\n\t.reg .b32 t;\n\t.reg .b64 a, b;\n\t"
+                 "elect.sync _|e, 0xffffffff;\n\t"
+                 "add.u32 t, %0, %3;\n\tadd.s64 a, %1, %4;\n\tadd.s64 b, %2, %5;\n\t"
+                 "@e tcgen05.mma.cta_group::1.kind::i8 [t], a, b, %6, %7;\n\t}"
+                 :: "r"(tm), "l"(da), "l"(db), "n"(TOFF), "n"(AOFF >> 4), "n"(BOFF >> 4), "n"(IDESC), "n"(ACC));
+}
+// W plane a x h planes [b0, b0 + nb) into TMEM column blocks a + b (Rp
+// columns each), split at N = 256
+template <int RP, int A, int B0, int NB, int ACC>
+__device__ __forceinline__ void range_imm(uint32_t tm, uint64_t da, uint64_t db) {
+    constexpr int TOT = NB * RP, N1 = TOT < 256 ? TOT : 256, N2 = TOT - N1;
+    mma_imm<(uint32_t)((A + B0) * RP), (uint32_t)(A * 128 * 64), (uint32_t)(((B0 * RP) >> 3) * 512),
+            idesc(A == 0, N1), ACC>(tm, da, db);
+    if constexpr (N2 > 0)
+        mma_imm<(uint32_t)((A + B0) * RP + 256), (uint32_t)(A * 128 * 64), (uint32_t)(((B0 * RP + 256) >> 3) * 512),
+                idesc(A == 0, N2), ACC>(tm, da, db);
+}
+// the 17 digit pairs (a + b <= 5) of one 32-byte K step into the six
+// anti-diagonal accumulators; FIRST: the chunk's first K step, where each
+// diagonal block is written before it accumulates
+template <int RP, bool FIRST>
+__device__ __forceinline__ void ks_pairs(uint32_t tm, uint64_t da, uint64_t db) {
+    if constexpr (FIRST) {
+        range_imm<RP, 0, 0, 4, 0>(tm, da, db);      // (0,0) (0,1) (0,2) (0,3): blocks 0-3 first written
+        range_imm<RP, 1, 0, 3, 1>(tm, da, db);      // (1,0) (1,1) (1,2)
+        range_imm<RP, 1, 3, 1, 0>(tm, da, db);      // (1,3): block 4 first written
+        range_imm<RP, 2, 0, 3, 1>(tm, da, db);      // (2,0) (2,1) (2,2)
+        range_imm<RP, 2, 3, 1, 0>(tm, da, db);      // (2,3): block 5 first written
+        range_imm<RP, 3, 0, 3, 1>(tm, da, db);      // (3,0) (3,1) (3,2)
+        range_imm<RP, 4, 0, 2, 1>(tm, da, db);      // (4,0) (4,1)
+    } else {
+        range_imm<RP, 0, 0, 4, 1>(tm, da, db);
+        range_imm<RP, 1, 0, 4, 1>(tm, da, db);
+        range_imm<RP, 2, 0, 4, 1>(tm, da, db);
+        range_imm<RP, 3, 0, 3, 1>(tm, da, db);
+        range_imm<RP, 4, 0, 2, 1>(tm, da, db);
+    }
+}
+// one staged K chunk (KC = 64 bytes: two K steps) at a run-time Rp in {16, ..., 80}
+__device__ __forceinline__ void kc_pairs(int Rp, bool first, uint32_t tm, uint64_t da, uint64_t db) {
+#define XU_KS(RP)                                                                          \
+    case RP:                                                                               \
+        if (first) ks_pairs<RP, true>(tm, da, db); else ks_pairs<RP, false>(tm, da, db);  \
+        ks_pairs<RP, false>(tm, da + 16, db + 16);                                         \
+        break;
+    switch (Rp) { XU_KS(16) XU_KS(32) XU_KS(48) XU_KS(64) XU_KS(80) default: break; }
+#undef XU_KS
+}
+static_assert(KC == 64, "kc_pairs issues two 32-byte K steps per chunk");
+
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
     asm volatile("{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t"
                  "setp.ne.b32 p, %4, 0;\n\t"
@@ -670,9 +728,65 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
             if (rg.alg) atomicAdd(&rg.alg[3], (unsigned long long)*fbn);
             *fbn = 0u;
         };
+        // With a U staging block the epilogue only certifies: it leaves tile
+        // mt's results y[row][unit] in that block (NaN: uncertified, left to
+        // the fallbacks), and this pass -- a warp per row among warps
+        // [w0, NW), under the next tile's K loop -- stores them: 512-byte
+        // hidden-row segments, the digit planes (4-byte words of the per-row
+        // store), one digest atomic and one error sum per row and tile.
+        auto rows_out = [&](int mt, int w0) {
+            const int c4 = lane * 4, u = mt * tc::BM + c4;
+            for (int r = wid - w0; r < R; r += NW - w0) {
+                unsigned long long dgs = 0ull;
+                float es = 0.f;
+                if (u < H) {                          // (H % 4 == 0: whole float4s)
+                    const float4 y4 = *reinterpret_cast<const float4 *>(rg.us + r * 128 + c4);
+                    const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
+                    bool ok[4];
+#pragma unroll
+                    for (int k = 0; k < 4; k++) ok[k] = !isnan(yv[k]);
+                    float *ho = rg.hout + (size_t)(q0 + r) * H + u;
+                    if (ok[0] && ok[1] && ok[2] && ok[3]) *reinterpret_cast<float4 *>(ho) = y4;
+                    else {
+#pragma unroll
+                        for (int k = 0; k < 4; k++) if (ok[k]) ho[k] = yv[k];
+                    }
+                    uint32_t Y[4];
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        float err = 0.f;
+                        Y[k] = ok[k] ? digit_word(yv[k], err) : 0u;
+                        es += err;
+                        if (ok[k]) dgs += otf_dig_h((uint32_t)(u + k), yv[k]);
+                    }
+                    if (rg.fuse_store) {
+                        uint8_t *dst = rg.fuse_store + ((size_t)(rg.out_row0 + q0 + r) * NK + (u >> 6)) * 4 * KC + (u & 63);
+#pragma unroll
+                        for (int b = 0; b < 4; b++) {
+                            const uint32_t sel = (uint32_t)(3 - b) | ((uint32_t)(7 - b) << 4);
+                            *reinterpret_cast<uint32_t *>(dst + b * KC) =
+                                __byte_perm(__byte_perm(Y[0], Y[1], sel), __byte_perm(Y[2], Y[3], sel), 0x5410);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) dgs += __shfl_xor_sync(0xffffffffu, dgs, o);
+                if (lane == 0 && rg.dig) atomicAdd(&rg.dig[q0 + r], dgs);
+                if (rg.fuse_store && __any_sync(0xffffffffu, es != 0.f)) {
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+                    if (lane == 0) atomicAdd(&rg.deh_store[rg.out_row0 + q0 + r], es * 1.01f);
+                }
+            }
+        };
+        const bool ystage = rg.us != nullptr;
         for (int mt = mt0; mt < mt1; mt++) {
             if (wid >= 2 && mt > mt0) {
-                // the previous tile's uncertified elements, under this tile's K loop
+                // the previous tile's results and uncertified elements, under this tile's K loop
+                if (ystage) {
+                    rows_out(mt - 1, 2);
+                    named_sync(3, NT - 64);
+                }
                 fallbacks(mt - 1, 2);
                 named_sync(3, NT - 64);
                 if (tid == 64) fallbacks_done(mt - 1);
@@ -701,29 +815,8 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                     __syncwarp();
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const uint32_t sW = tc::smem_u32(rg.smem + (size_t)st * STAGE);
-                    const uint32_t sH = sW + HOFF;
-#pragma unroll
-                    for (int ks = 0; ks < KC / 32; ks++) {
-                        const uint32_t acc0 = (kc > 0 || ks > 0) ? 1u : 0u;
-                        // W plane a over h blocks [b0, b0 + nb): TMEM column blocks a + b
-                        auto range = [&](int a, int b0, int nb, uint32_t acc) {
-                            const int tot = nb * Rp;
-                            for (int off = 0; off < tot; off += 256) {
-                                const int nn = min(256, tot - off);
-                                const int brow = b0 * Rp + off;
-                                const uint64_t da = desc(sW + (uint32_t)a * PLANE_W + (uint32_t)ks * 256u);
-                                const uint64_t db = desc(sH + (uint32_t)(brow >> 3) * 512u + (uint32_t)ks * 256u);
-                                mma_i8(rg.tmem + (uint32_t)((a + b0) * Rp + off), da, db, idesc(a == 0, nn), acc);
-                            }
-                        };
-                        range(0, 0, 4, acc0);      // (0,0) (0,1) (0,2) (0,3): blocks 0-3 first written
-                        range(1, 0, 3, 1u);        // (1,0) (1,1) (1,2)
-                        range(1, 3, 1, acc0);      // (1,3): block 4 first written
-                        range(2, 0, 3, 1u);        // (2,0) (2,1) (2,2)
-                        range(2, 3, 1, acc0);      // (2,3): block 5 first written
-                        range(3, 0, 3, 1u);        // (3,0) (3,1) (3,2)
-                        range(4, 0, 2, 1u);        // (4,0) (4,1)
-                    }
+                    // 17 digit pairs per 32-byte K step (ks_pairs), immediates off two stage descriptors
+                    kc_pairs(Rp, kc == 0, rg.tmem, desc(sW), desc(sW + HOFF));
                     tc::commit_elect(tc::smem_u32(&rg.empty[st]));
                     if (kc == NK - 1) tc::commit_elect(tc::smem_u32(rg.done));
                     __syncwarp();
@@ -733,6 +826,7 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
             // one warp polls the tile's completion; the others block in the
             // hardware barrier instead of spinning on the mbarrier
             if (wid == 0) wait(tc::smem_u32(rg.done), tiles_done & 1, 13);
+            mark(26);
             tiles_done++;
             __syncthreads();
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -753,7 +847,7 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
             const int n4 = (R + 3) >> 2;
             for (int it = wid >> 2; it < n4; it += NW / 4) {
                 const int r0 = it * 4;
-                mark(17);
+                mark(27);
                 float uv[4];          // U[w, unit] of the group's rows (V H < 2^31: 32-bit offsets)
                 if (us_t) {
 #pragma unroll
@@ -792,6 +886,25 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                 }
                 if (ph) { const float y0 = yv[0] + yv[1] + yv[2] + yv[3]; asm volatile("" :: "f"(y0)); }
                 mark(15);
+                if (ystage) {
+                    // results into the staging block (rows_out stores them); uncertified -> NaN + list
+#pragma unroll
+                    for (int g = 0; g < 4; g++) {
+                        const int row = r0 + g;
+                        if (uok && row < R) {
+                            float y = yv[g];
+                            if (!okv[g]) {
+                                y = __int_as_float(0x7fffffff);
+                                const uint32_t k = atomicAdd(fbn, 1u);
+                                if (k < (uint32_t)FBCAP) fbl[k] = ((uint32_t)row << 16) | (uint32_t)unit;
+                                else                                  // list full: recompute here
+                                    y = ref_element(m.W + (size_t)unit * H, rg.hin + (size_t)rg.src[row] * H, uv[g], H);
+                            }
+                            rg.us[row * 128 + quad * 32 + lane] = y;
+                        }
+                    }
+                    continue;
+                }
                 unsigned long long dg[4];
 #pragma unroll
                 for (int g = 0; g < 4; g++) {
@@ -837,7 +950,11 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
             __syncthreads();
             mark(3);
         }
-        // the last tile's uncertified elements (every warp)
+        // the last tile's results and uncertified elements (every warp)
+        if (ystage) {
+            rows_out(mt1 - 1, 0);
+            __syncthreads();
+        }
         fallbacks(mt1 - 1, 0);
         __syncthreads();
         if (tid == 0) fallbacks_done(mt1 - 1);

@@ -474,7 +474,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
 
     // profiling runs only: per-phase device time (ns), summed over streams
     // (thread 0 of each rank marks its own phases)
-    unsigned long long ph[26] = {0}, t0 = 0, t1 = 0;
+    unsigned long long ph[28] = {0}, t0 = 0, t1 = 0;
     const bool prof = P.phase_ns != nullptr && tid == 0;
 #define SD_MARK(i) do { if (prof) { t1 = sd::gtimer(); ph[i] += t1 - t0; t0 = t1; } } while (0)
     if (prof) t0 = sd::gtimer();
@@ -780,7 +780,7 @@ k_decode_streams(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam
     }
     if (prof) {
         ph[11] = rank == 0 ? 1 : 0;
-        for (int i = 0; i < 26; i++) if (ph[i]) atomicAdd(&P.phase_ns[i], ph[i]);
+        for (int i = 0; i < 28; i++) if (ph[i] && (i < 16 || i > 20)) atomicAdd(&P.phase_ns[i], ph[i]);
     }
 #undef SD_MARK
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -17,7 +17,7 @@ if cfg == "e":
 else:
     s = synth.build_setup(cfg, n_utt=n, T=T, seed=7)
 need = BatchDecoder.contexts_needed(s.lattices, s.beam)
-dec = BatchDecoder(s.model, s.tree, s.small_lm, n, need, precision=prec, schedule="stream")
+dec = BatchDecoder(s.model, s.tree, s.small_lm, n, need, precision=prec, schedule="auto")
 dec.prepare(s.lattices, s.beam)
 for _ in range(reps):
     dec.run(1.0)
@@ -28,4 +28,4 @@ cnt = dec.counters()
 st = dec.streams.stats()
 print(json.dumps({"frames": int(sum(len(h.arcs) for h in hyps)), "requests": int(out["expansions"].sum()),
                   "misses": int(st[:, 2].sum()), "H": s.model.hidden_size, "counters": cnt,
-                  "kernel_ms": {k: v[0] for k, v in prof.items()}}))
+                  "kernel_ms": {k: v[0] for k, v in prof.items()}, "schedule": dec.schedule}))

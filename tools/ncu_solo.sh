@@ -1,0 +1,5 @@
+# ncu of the one-CTA-per-stream EXACT kernel at config e (148 utterances x 300 frames)
+set -u
+python tools/decode_once.py e 148 300 exact > gpurun_out/solo_once.json 2>&1 || exit 1
+ncu --set full --import-source on --clock-control none -k regex:k_decode_solo -c 1 -o gpurun_out/solo_full -f \
+    python tools/decode_once.py e 148 300 exact > gpurun_out/solo_ncu_full.log 2>&1
