@@ -299,8 +299,12 @@ int otflm_plan_set_schedule(OtflmPlan *p, int32_t schedule);
  * loop (OTFLM_PREC_EXACT), o[11] CTAs, o[12..16] assign sections (probe, dedup
  * scan, numbering, values, arrivals), o[17..20] EXACT update: row table,
  * digitize, 2 spare, o[21..23] EXACT HS (rank 0): wait for the chunk's digits,
- * digit-plane GEMM + epilogue, MaxEnt + log-sigmoid: 24 entries.  (EXACT: o[1] is the digitize barrier,
- * o[2] the digit-pair K loops.) */
+ * digit-plane GEMM + epilogue, MaxEnt + log-sigmoid, o[24..25] EXACT plane
+ * copy (row pass, copy), o[26] the MMA warp's update K loops, o[27] update
+ * epilogue stores, o[28..31] (one-CTA schedule) warp 2 under the K loops: HS
+ * tail, row stores, fallbacks, U staging: 32 entries (o must hold 32).
+ * (EXACT: o[1] is the digitize barrier, o[2] the wait of the MMA warp for the
+ * other warps after its K loops; o[11] counts streams in the one-CTA schedule.) */
 int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream);
 int otflm_schedule_supported(const OtflmModel *m, int32_t schedule, int32_t precision);
 int otflm_group_create(OtflmPlan **plans, int32_t n, OtflmGroup **out);

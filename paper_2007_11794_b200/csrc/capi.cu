@@ -1446,7 +1446,7 @@ extern "C" int otflm_plan_info(const OtflmPlan *p, int64_t *o) {
 
 extern "C" int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream) {
     if (!p || !o) return OTFLM_ERR_VALUE;
-    unsigned long long a[28] = {0};
+    unsigned long long a[32] = {0};
     CK(cudaMemcpyAsync(a, p->alg_buf + 8, sizeof(a), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
     CK(cudaStreamSynchronize((cudaStream_t)stream));
     for (int i = 0; i < 12; i++) o[i] = (int64_t)a[i];
@@ -1455,6 +1455,7 @@ extern "C" int otflm_plan_phase_ns(const OtflmPlan *p, int64_t *o, void *stream)
     for (int i = 0; i < 3; i++) o[21 + i] = (int64_t)a[21 + i];   // EXACT HS (rank 0): digits wait, GEMM, log-sigmoid
     o[24] = (int64_t)a[24]; o[25] = (int64_t)a[25];                 // EXACT update: plane-copy row pass, copy
     o[26] = (int64_t)a[26]; o[27] = (int64_t)a[27];                 // EXACT update: MMA warp's K loop, epilogue stores
+    for (int i = 28; i < 32; i++) o[i] = (int64_t)a[i];            // warp 2 under the K loops: HS tail, rows, fallbacks, U
     return OTFLM_OK;
 }
 

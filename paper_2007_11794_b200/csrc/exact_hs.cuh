@@ -366,19 +366,45 @@ __device__ __forceinline__ void finish(const DevModel &m, DevPlan &Q, DevStreams
     const int H = m.H, fw = ft >> 5, FNW = FN >> 5, lane = ft & 31;
     const uint32_t T = hs.misc[1];
     // ---- MaxEnt terms in the reference's order, sign, float64 log-sigmoid ----
-    for (uint32_t j = (uint32_t)ft; j < T; j += (uint32_t)FN) {
-        const int q = hs.pq[j];
-        const uint32_t code = hs.pcode[j];
-        double a = hs.act[j];
-        double me_abs = 0.0;
-        for (int k = 0; k < hs.kmax[q]; k++) {
-            const double me = (double)__ldg(m.ME + (otf_mix(hs.pre[q * ORD + k], (uint64_t)(code & 0x7FFFFFFFu)) & m.mask));
-            a += me;
-            me_abs += fabs(me);
+    // two pairs per thread and trip, every MaxEnt weight of both loaded before
+    // any is summed (independent L2 reads in flight instead of a chain)
+    for (uint32_t j0 = (uint32_t)ft; j0 < T; j0 += 2u * (uint32_t)FN) {
+        float mev[2][ORD];
+        int km[2];
+        uint32_t cd[2];
+#pragma unroll
+        for (int p = 0; p < 2; p++) {
+            const uint32_t j = j0 + (uint32_t)p * (uint32_t)FN;
+            km[p] = 0;
+            cd[p] = 0u;
+            if (j < T) {
+                const int q = hs.pq[j];
+                cd[p] = hs.pcode[j];
+                km[p] = hs.kmax[q];
+#pragma unroll
+                for (int k = 0; k < ORD; k++)
+                    mev[p][k] = k < km[p] ? __ldg(m.ME + (otf_mix(hs.pre[q * ORD + k], (uint64_t)(cd[p] & 0x7FFFFFFFu)) & m.mask))
+                                          : 0.f;
+            }
         }
-        // + the additions' rounding relative to the reference's (different a~)
-        hs.errj[j] = __double2float_ru((double)hs.errj[j] + 8.0 * 1.1102230246251565e-16 * (fabs(a) + me_abs));
-        hs.act[j] = otf_log_sigmoid((code & 0x80000000u) ? -a : a);
+#pragma unroll
+        for (int p = 0; p < 2; p++) {
+            const uint32_t j = j0 + (uint32_t)p * (uint32_t)FN;
+            if (j < T) {
+                double a = hs.act[j];
+                double me_abs = 0.0;
+#pragma unroll
+                for (int k = 0; k < ORD; k++)
+                    if (k < km[p]) {
+                        const double me = (double)mev[p][k];
+                        a += me;
+                        me_abs += fabs(me);
+                    }
+                // + the additions' rounding relative to the reference's (different a~)
+                hs.errj[j] = __double2float_ru((double)hs.errj[j] + 8.0 * 1.1102230246251565e-16 * (fabs(a) + me_abs));
+                hs.act[j] = otf_log_sigmoid((cd[p] & 0x80000000u) ? -a : a);
+            }
+        }
     }
     sd::group_sync(bar, FN);
     // ---- per query: path-order sum, certification of delta, history, digest ----

@@ -169,6 +169,7 @@ k_decode_solo(DevModel m, DevPlan P, DevStreams S, DevNgram g, long long beam, d
             // queries) runs on warps 2.. under the first tile's K loop
             xu::Ring rgc = rg;
             rgc.eh = rg.eh + (c & 1) * xu::XR;
+            rgc.phase_g = P.phase_ns;
             rgc.fuse_store = S.arena_dig;          // the new rows' planes straight from the epilogue
             rgc.out_row0 = base;
             xu::update_chunk<NT>(m, q0, nq, (int)c, rgc, gctr_u, tiles_done, tid, wid, lane, wait,

@@ -356,6 +356,7 @@ struct Ring {
     // digitize_to_store), so no separate digitize pass follows the update
     uint8_t *fuse_store = nullptr;
     uint32_t out_row0 = 0;
+    unsigned long long *phase_g = nullptr;   // profiling: warp 2's sections under the K loops -> [28, 32)
 };
 constexpr uint32_t US_BYTES = (uint32_t)XR * 128 * 4;
 constexpr uint32_t STAGE = (uint32_t)NPW * PLANE_W + 4u * XR * KC;
@@ -736,16 +737,23 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
         // store), one digest atomic and one error sum per row and tile.
         auto rows_out = [&](int mt, int w0) {
             const int c4 = lane * 4, u = mt * tc::BM + c4;
+            // the ring's fields in registers (the struct itself may live in local memory)
+            const float *__restrict__ us = rg.us;
+            float *__restrict__ hout = rg.hout;
+            uint8_t *__restrict__ fuse = rg.fuse_store;
+            unsigned long long *__restrict__ dig = rg.dig;
+            float *__restrict__ deh = rg.deh_store;
+            const uint32_t orow0 = rg.out_row0 + q0;
             for (int r = wid - w0; r < R; r += NW - w0) {
                 unsigned long long dgs = 0ull;
                 float es = 0.f;
                 if (u < H) {                          // (H % 4 == 0: whole float4s)
-                    const float4 y4 = *reinterpret_cast<const float4 *>(rg.us + r * 128 + c4);
+                    const float4 y4 = *reinterpret_cast<const float4 *>(us + r * 128 + c4);
                     const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
                     bool ok[4];
 #pragma unroll
                     for (int k = 0; k < 4; k++) ok[k] = !isnan(yv[k]);
-                    float *ho = rg.hout + (size_t)(q0 + r) * H + u;
+                    float *ho = hout + (size_t)(q0 + r) * H + u;
                     if (ok[0] && ok[1] && ok[2] && ok[3]) *reinterpret_cast<float4 *>(ho) = y4;
                     else {
 #pragma unroll
@@ -759,8 +767,8 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                         es += err;
                         if (ok[k]) dgs += otf_dig_h((uint32_t)(u + k), yv[k]);
                     }
-                    if (rg.fuse_store) {
-                        uint8_t *dst = rg.fuse_store + ((size_t)(rg.out_row0 + q0 + r) * NK + (u >> 6)) * 4 * KC + (u & 63);
+                    if (fuse) {
+                        uint8_t *dst = fuse + ((size_t)(orow0 + r) * NK + (u >> 6)) * 4 * KC + (u & 63);
 #pragma unroll
                         for (int b = 0; b < 4; b++) {
                             const uint32_t sel = (uint32_t)(3 - b) | ((uint32_t)(7 - b) << 4);
@@ -771,28 +779,40 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                 }
 #pragma unroll
                 for (int o = 16; o; o >>= 1) dgs += __shfl_xor_sync(0xffffffffu, dgs, o);
-                if (lane == 0 && rg.dig) atomicAdd(&rg.dig[q0 + r], dgs);
-                if (rg.fuse_store && __any_sync(0xffffffffu, es != 0.f)) {
+                if (lane == 0 && dig) atomicAdd(&dig[q0 + r], dgs);
+                if (fuse && __any_sync(0xffffffffu, es != 0.f)) {
 #pragma unroll
                     for (int o = 16; o; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
-                    if (lane == 0) atomicAdd(&rg.deh_store[rg.out_row0 + q0 + r], es * 1.01f);
+                    if (lane == 0) atomicAdd(&deh[orow0 + r], es * 1.01f);
                 }
             }
         };
         const bool ystage = rg.us != nullptr;
         for (int mt = mt0; mt < mt1; mt++) {
+            unsigned long long g0 = 0;
+            auto gmark = [&](int i) {
+                if (rg.phase_g && tid == 64) {
+                    unsigned long long t;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                    if (i >= 0) atomicAdd(&rg.phase_g[i], t - g0);
+                    g0 = t;
+                }
+            };
+            gmark(-1);
             if (wid >= 2 && mt > mt0) {
                 // the previous tile's results and uncertified elements, under this tile's K loop
                 if (ystage) {
                     rows_out(mt - 1, 2);
+                    gmark(29);
                     named_sync(3, NT - 64);
                 }
                 fallbacks(mt - 1, 2);
                 named_sync(3, NT - 64);
                 if (tid == 64) fallbacks_done(mt - 1);
+                gmark(30);
             }
             const bool us_t = rg.us && !(side_uses_us && mt == mt0);
-            if (wid >= 2 && mt == mt0) side(tid - 64, NT - 64);
+            if (wid >= 2 && mt == mt0) { side(tid - 64, NT - 64); gmark(28); }
             if (wid >= 2 && us_t) {
                 // this tile's U block U[w_r, mt*128 + (0..127)] into shared memory,
                 // under the K loop (the previous epilogue is done with it)
@@ -803,6 +823,7 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                     if (u0 + c4 < H) v = __ldg(reinterpret_cast<const float4 *>(m.U + (size_t)rg.wrd[r] + u0 + c4));
                     *reinterpret_cast<float4 *>(rg.us + r * 128 + c4) = v;
                 }
+                gmark(31);
             }
             if (wid == 1) {
                 produce(mt, mt == mt0 ? 0 : npre, NK);
@@ -838,6 +859,11 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
             // the 4 warps of a lane quadrant take groups of 4 rows in turn ----
             const int quad = wid & 3;
             const int unit = mt * tc::BM + quad * 32 + lane;
+            float *__restrict__ us_e = rg.us;               // ring fields in registers
+            const double *__restrict__ eh_e = rg.eh;
+            const double *__restrict__ tab_e = rg.tab;
+            const int32_t *__restrict__ wrd_e = rg.wrd;
+            const uint32_t tmem_e = rg.tmem;
             const bool uok = unit < H;
             double4 k4 = make_double4(0.0, 0.0, 0.0, 0.0);
             if (uok) k4 = m.wx[unit];
@@ -851,15 +877,15 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                 float uv[4];          // U[w, unit] of the group's rows (V H < 2^31: 32-bit offsets)
                 if (us_t) {
 #pragma unroll
-                    for (int g = 0; g < 4; g++) uv[g] = rg.us[min(r0 + g, R - 1) * 128 + quad * 32 + lane];
+                    for (int g = 0; g < 4; g++) uv[g] = us_e[min(r0 + g, R - 1) * 128 + quad * 32 + lane];
                 } else {
 #pragma unroll
-                    for (int g = 0; g < 4; g++) uv[g] = __ldg(ucol + rg.wrd[min(r0 + g, R - 1)]);
+                    for (int g = 0; g < 4; g++) uv[g] = __ldg(ucol + wrd_e[min(r0 + g, R - 1)]);
                 }
                 long long th[4], tl[4];
                 {
                     uint32_t D[NDIAG][4];
-                    const uint32_t ta = rg.tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)r0;
+                    const uint32_t ta = tmem_e + ((uint32_t)(quad * 32) << 16) + (uint32_t)r0;
 #pragma unroll
                     for (int s2 = 0; s2 < NDIAG; s2++)
                         asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
@@ -881,8 +907,8 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                     const double dh = __longlong_as_double(th[g] + 0x4338000000000000LL) - 6755399441055744.0;
                     const double dlo = __longlong_as_double(tl[g] + 0x4338000000000000LL) - 6755399441055744.0;
                     const double x = fma(dh, k4.x, fma(dlo, k4.w, widen(uv[g])));
-                    const double epsm = fma(k4.z, rg.eh[min(r0 + g, R - 1)], k4.y);
-                    okv[g] = certify(x, epsm, rg.tab, yv[g]);
+                    const double epsm = fma(k4.z, eh_e[min(r0 + g, R - 1)], k4.y);
+                    okv[g] = certify(x, epsm, tab_e, yv[g]);
                 }
                 if (ph) { const float y0 = yv[0] + yv[1] + yv[2] + yv[3]; asm volatile("" :: "f"(y0)); }
                 mark(15);
@@ -900,7 +926,7 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                                 else                                  // list full: recompute here
                                     y = ref_element(m.W + (size_t)unit * H, rg.hin + (size_t)rg.src[row] * H, uv[g], H);
                             }
-                            rg.us[row * 128 + quad * 32 + lane] = y;
+                            us_e[row * 128 + quad * 32 + lane] = y;
                         }
                     }
                     continue;

@@ -305,7 +305,7 @@ class Plan:
     def phase_ns(self) -> dict:
         """Stream schedule, after ``profile``: device ns per phase summed over
         CTAs (utterance streams)."""
-        o = np.zeros(28, np.int64)
+        o = np.zeros(32, np.int64)
         _lib.check(_lib.load().otflm_plan_phase_ns(self.handle, o.ctypes.data, current_stream_ptr()),
                    "phase_ns")
         names = ("expand", "update_kloop", "update_drain", "update_epilogue", "hs_setup", "hs_pairs",
@@ -332,6 +332,9 @@ class Plan:
         out["x_plane_copy"] = int(o[25])
         out["x_update_mma"] = int(o[26])       # the MMA warp's K loops (issue to completion)
         out["x_epi_rest"] = int(o[27])         # epilogue stores / digests / U loads between row groups
+        # warp 2 under the update K loops (solo kernel): HS tail, row stores, fallbacks, U staging
+        for i, k in enumerate(("w2_hs_tail", "w2_rows_out", "w2_fallbacks", "w2_u_stage")):
+            out[k] = int(o[28 + i])
         return out
 
     def set_schedule(self, schedule: str) -> None:
