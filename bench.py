@@ -292,7 +292,7 @@ def all_word_microbench(precision: str, n_ctx: int = 256, reps: int = 5):
 
 
 def beam_sweep(precision: str, beams=(1, 2, 4, 8, 16, 32, 64), n_utt: int = 8, frames: int = 300,
-               reps: int = 3):
+               reps: int = 3, schedule: str = "auto"):
     """Config (c): V=65,536 H=512 MaxEnt 2^22, 8 utterances x 300 frames,
     decode throughput and RTF per beam (device time, lattices resident, L2
     flushed before each run)."""
@@ -304,7 +304,8 @@ def beam_sweep(precision: str, beams=(1, 2, 4, 8, 16, 32, 64), n_utt: int = 8, f
     rows = []
     for beam in beams:
         need = BatchDecoder.contexts_needed(setup.lattices, beam)
-        dec = BatchDecoder(setup.model, setup.tree, setup.small_lm, n_utt, need, precision=precision)
+        dec = BatchDecoder(setup.model, setup.tree, setup.small_lm, n_utt, need, precision=precision,
+                           schedule=schedule)
         dec.prepare(setup.lattices, beam)
         dec.run(1.0)
         torch.cuda.synchronize()

@@ -262,6 +262,12 @@ int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *lats, int32_t *sam
 /* plan stats: levels, nodes, arcs, slots, max requests per level, total
  * request slots, graph nodes (int64 [8]) */
 int otflm_plan_info(const OtflmPlan *p, int64_t *out8);
+/* wide-level flags of a compiled batch: bit 0 = nodes with more than 64
+ * arrival slots (big beams: expanded by a CTA per node, decode.cuh
+ * k_expand_big), bit 1 = (level, stream) request ranges above 4096 (the
+ * multi-CTA ordered assign, k_asg_*).  Both run on the level schedule, which
+ * BatchDecoder(schedule="auto") then picks (decoder.py:131-149 per node). */
+int otflm_plan_wide(const OtflmPlan *p, int32_t *flags);
 /* Algorithmic-work counters of the last profiled run + upload size (int64 [6]):
  * sum of Huffman path lengths over HS queries, sum of path length x MaxEnt
  * orders, HS queries, bytes uploaded by plan_create, and (OTFLM_PREC_EXACT)

@@ -76,6 +76,8 @@ def lib():
         L.orc_stack_create.argtypes = [p, i32, u64]
         L.orc_stack_destroy.argtypes = [p]
         L.orc_stack_reset.argtypes = [p, i32]
+        L.orc_stack_cache_clear.argtypes = [p]
+        L.orc_stack_roll_stats.argtypes = [p]
         L.orc_stack_stats.argtypes = [p, p]
         L.orc_stack_context.restype = C.c_int
         L.orc_stack_context.argtypes = [p, u64, p, p, p]
@@ -356,6 +358,14 @@ class OracleStack:
 
     def reset(self, retain: bool) -> None:
         lib().orc_stack_reset(self.handle, int(bool(retain)))
+
+    def cache_clear(self) -> None:
+        """RescoreCache.clear (cache.py:136-140): entries only."""
+        lib().orc_stack_cache_clear(self.handle)
+
+    def roll_stats(self) -> None:
+        """RescoreCache.roll_stats (cache.py:156-158)."""
+        lib().orc_stack_roll_stats(self.handle)
 
     def stats(self) -> OracleStats:
         out = np.zeros(12, np.int64)

@@ -555,6 +555,22 @@ void orc_stack_reset(OrcStack *s, int32_t retain) {
     }
 }
 
+/* RescoreCache.clear (cache.py:136-140): drop every entry and the policy
+ * state; counters and the index table stay */
+void orc_stack_cache_clear(OrcStack *s) {
+    orc_map_clear(&s->cache);
+    s->cache_n = 0;
+    s->n_resident = 0;
+    s->heap_n = 0;
+}
+
+/* RescoreCache.roll_stats (cache.py:156-158) alone */
+void orc_stack_roll_stats(OrcStack *s) {
+    s->cum.lookups += s->cur.lookups; s->cum.hits += s->cur.hits;
+    s->cum.misses += s->cur.misses; s->cum.evictions += s->cur.evictions;
+    memset(&s->cur, 0, sizeof(s->cur));
+}
+
 /* stats out: [lookups, hits, misses, evictions, entries, table_len,
  *             cum_lookups, cum_hits, cum_misses, ledger_requests,
  *             ledger_bytes_indexed, ledger_bytes_full] */

@@ -136,6 +136,7 @@ _SIGS = {
     "otflm_decode_lattice_fetch": (C.c_int, [_P, _P, _P, C.c_int64, _P]),
     "otflm_plan_set_schedule": (C.c_int, [_P, C.c_int32]),
     "otflm_plan_phase_ns": (C.c_int, [_P, _P, _P]),
+    "otflm_plan_wide": (C.c_int, [_P, C.POINTER(C.c_int32)]),
     "otflm_schedule_supported": (C.c_int, [_P, C.c_int32, C.c_int32]),
     "otflm_group_create": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_void_p)]),
     "otflm_group_destroy": (C.c_int, [_P]),

@@ -3,6 +3,7 @@
 // compiler (topological levels, per-node beam capacities, arrival slots) and
 // the level loop (captured once into a CUDA graph and replayed).
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -800,6 +801,7 @@ extern "C" int otflm_streams_create(const OtflmModel *m, const OtflmStreamConfig
     d.arena_rows = (uint32_t)cfg->arena_rows;
     d.lfu_cap = 0; d.lfu_logcap = 0; d.lfu_log = nullptr; d.lfu_logn = nullptr;
     d.arena_dig = nullptr; d.arena_deh = nullptr; d.arena_dep = nullptr;
+    d.ct_first = nullptr;
     d.ct_cap = pow2_at_least((uint64_t)cfg->max_contexts * 2 + 2);
     d.kc_cap = pow2_at_least((uint64_t)std::max<int64_t>(cfg->cache_slots, 16));
     const size_t S = d.S;
@@ -1010,6 +1012,11 @@ struct OtflmPlan {
     OtflmStreams *st = nullptr;
     int64_t beam = 0;
     uint32_t n_utt = 0, n_levels = 0, n_nodes = 0, n_arcs = 0, n_slots = 0, R_max = 0;
+    bool has_big = false;              // nodes for k_expand_big (expb_min < cap <= EXPB_MAX)
+    uint32_t expb_min = EXPB_MIN;      // (OTFLM_EXPAND_BIG_MIN / OTFLM_ASSIGN_BIG: test overrides of the thresholds)
+    uint32_t asg_big = ASSIGN_BIG;
+    bool big_asg = false;              // a (level, stream) range above ASSIGN_BIG requests: k_asg_* assign
+    uint32_t ch_cap = 0;               // chunk entries of the multi-CTA assign (max over levels)
     uint64_t total_req = 0;
     std::vector<uint32_t> lvl_node_off, lvl_req, lvl_range_off;   // host copies
     DevPlan d{};
@@ -1156,6 +1163,7 @@ static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam,
             ni.req_base = 0;
             ni.stream = sid;
             ni.pad = 0;
+            if (ni.cap > p->expb_min && ni.cap <= EXPB_MAX && ni.out_e > ni.out_b) p->has_big = true;
             nodes.push_back(ni);
         }
         lv[u].assign(cur + 1, {});
@@ -1190,6 +1198,7 @@ static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam,
                 level_nodes.push_back(g);
             }
             if (run > rb) {
+                if (run - rb > p->asg_big) p->big_asg = true;
                 ranges.push_back(StreamRange{utt_stream[u], (uint32_t)rb, (uint32_t)run, 0});
                 ulv[u].push_back(UttLevel{(uint32_t)t, nb, (uint32_t)level_nodes.size(), (uint32_t)rb, (uint32_t)run, 0, 0, 0});
             }
@@ -1198,6 +1207,10 @@ static int compile_batch(OtflmPlan *p, const OtflmLatticeBatch *L, int64_t beam,
         p->lvl_node_off.push_back((uint32_t)level_nodes.size());
         p->lvl_range_off.push_back((uint32_t)ranges.size());
         p->lvl_req.push_back((uint32_t)run);
+        {
+            const uint64_t nr = p->lvl_range_off.back() - p->lvl_range_off[p->lvl_range_off.size() - 2];
+            p->ch_cap = (uint32_t)std::max<uint64_t>(p->ch_cap, nr * ((run + ASG_CH - 1) / ASG_CH));
+        }
         rmax = std::max(rmax, run);
         total += run;
     }
@@ -1275,6 +1288,8 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     if (L->n_utt < 1) return OTFLM_ERR_VALUE;
     cudaStream_t s = (cudaStream_t)stream;
     OtflmPlan *p = new OtflmPlan();
+    if (const char *e = getenv("OTFLM_EXPAND_BIG_MIN")) p->expb_min = (uint32_t)strtoul(e, nullptr, 10);
+    if (const char *e = getenv("OTFLM_ASSIGN_BIG")) p->asg_big = (uint32_t)strtoul(e, nullptr, 10);
     p->st = st;
     p->beam = beam;
     p->n_utt = L->n_utt;
@@ -1343,6 +1358,19 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     bad |= p->mem.alloc(&d.out_expansions, p->n_utt) != cudaSuccess;
     if (bad) { p->mem.free_all(); delete p; g_detail = "cudaMalloc plan buffers"; return OTFLM_ERR_NOMEM; }
     if ((rc = plan_alloc_workspace(p, std::max<uint32_t>(p->ws_cap, 1), p->n_levels + 1))) { p->mem.free_all(); delete p; return rc; }
+    if (p->big_asg) {
+        // multi-CTA assign scratch; the streams' first-request table once (all unset)
+        const uint32_t W = std::max<uint32_t>(p->ws_cap, 1), C = std::max<uint32_t>(p->ch_cap, 1);
+        bool bad2 = p->mem.alloc(&d.as_kind, W) != cudaSuccess || p->mem.alloc(&d.as_slot, W) != cudaSuccess ||
+                    p->mem.alloc(&d.as_aux, W) != cudaSuccess || p->mem.alloc(&d.ch_cnt, C) != cudaSuccess ||
+                    p->mem.alloc(&d.ch_pre, C) != cudaSuccess;
+        if (!bad2 && !st->d.ct_first) {
+            const size_t n = (size_t)st->d.S * st->d.ct_cap;
+            bad2 = st->mem.alloc(&st->d.ct_first, n) != cudaSuccess;
+            if (!bad2) CK(cudaMemsetAsync(st->d.ct_first, 0xFF, n * 4, s));
+        }
+        if (bad2) { p->mem.free_all(); delete p; g_detail = "cudaMalloc assign scratch"; return OTFLM_ERR_NOMEM; }
+    }
     *out = p;
     return OTFLM_OK;
 }
@@ -1359,6 +1387,7 @@ extern "C" int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *L, int3
     if ((uint32_t)L->n_utt != p->n_utt) return OTFLM_ERR_VALUE;
     cudaStream_t s = (cudaStream_t)stream;
     OtflmPlan tmp;
+    tmp.expb_min = p->expb_min; tmp.asg_big = p->asg_big;
     std::vector<NodeInfo> nodes;
     std::vector<uint32_t> level_nodes, out_list, arc_slot, start_slot, final_off, finals, utt_stream;
     std::vector<int32_t> arc_word;
@@ -1373,7 +1402,7 @@ extern "C" int otflm_plan_refresh(OtflmPlan *p, const OtflmLatticeBatch *L, int3
     if (ul.empty()) ul.push_back(UttLevel{0, 0, 0, 0, 0, 0, 0, 0});
     if (ul.size() > p->ul_cap || rq_off.back() > p->ws_cap) return OTFLM_ERR_VALUE;
     if (tmp.n_levels != p->n_levels || tmp.n_nodes != p->n_nodes || tmp.n_arcs != p->n_arcs ||
-        tmp.n_slots != p->n_slots || tmp.R_max != p->R_max || tmp.lvl_node_off != p->lvl_node_off ||
+        tmp.n_slots != p->n_slots || tmp.R_max != p->R_max || tmp.has_big != p->has_big || tmp.lvl_node_off != p->lvl_node_off ||
         tmp.lvl_req != p->lvl_req || tmp.lvl_range_off != p->lvl_range_off || utt_stream != p->utt_stream_host)
         return OTFLM_ERR_VALUE;
     DevPlan &d = p->d;
@@ -1441,6 +1470,12 @@ extern "C" int otflm_plan_info(const OtflmPlan *p, int64_t *o) {
     if (!p || !o) return OTFLM_ERR_VALUE;
     o[0] = p->n_levels; o[1] = p->n_nodes; o[2] = p->n_arcs; o[3] = p->n_slots;
     o[4] = p->R_max; o[5] = (int64_t)p->total_req; o[6] = p->g_nodes; o[7] = p->n_utt;
+    return OTFLM_OK;
+}
+
+extern "C" int otflm_plan_wide(const OtflmPlan *p, int32_t *flags) {
+    if (!p || !flags) return OTFLM_ERR_VALUE;
+    *flags = (p->has_big ? 1 : 0) | (p->big_asg ? 2 : 0);
     return OTFLM_OK;
 }
 
@@ -1522,22 +1557,48 @@ static int enqueue_run(OtflmPlan *p, const OtflmNgram *g, double lm, int prec, c
     if (d.alg) CK(cudaMemsetAsync(d.alg, 0, 4 * sizeof(unsigned long long), s));
     if (d.kept) CK(cudaMemsetAsync(d.kept, 0, std::max<uint32_t>(p->n_slots, 1), s));
     { ProfScope ps(K_MISC, s); k_run_begin<<<cdiv(p->n_utt, 128), 128, 0, s>>>(d, S); CKL(); }
+    if (p->has_big)
+        CK(cudaFuncSetAttribute(k_expand_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)expb_smem(EXPB_MAX)));
     int prev = -1;
     for (uint32_t t = 0; t < p->n_levels; t++) {
         const uint32_t nb0 = p->lvl_node_off[t], nn = p->lvl_node_off[t + 1] - nb0;
         const uint32_t R = p->lvl_req[t];
+        auto expand = [&]() -> int {
+            ProfScope ps(K_EXPAND, s);
+            k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, g->d, nb0, nn, (long long)p->beam, t,
+                                                 p->has_big ? p->expb_min : 0xFFFFFFFFu);
+            CKL();
+            if (p->has_big) {             // a CTA per node with many arrival slots
+                k_expand_big<<<nn, EXPB_T, expb_smem(EXPB_MAX), s>>>(d, S, g->d, nb0, (long long)p->beam, t, EXPB_MAX,
+                                                                     p->expb_min);
+                CKL();
+            }
+            return OTFLM_OK;
+        };
         if (nn == 0 || R == 0) {
-            if (nn) { ProfScope ps(K_EXPAND, s); k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, g->d, nb0, nn, (long long)p->beam, t); CKL(); }
+            if (nn) { int rc = expand(); if (rc) return rc; }
             continue;
         }
-        { ProfScope ps(K_EXPAND, s); k_expand<<<cdiv(nn, 8), 256, 0, s>>>(d, S, g->d, nb0, nn, (long long)p->beam, t); CKL(); }
+        { int rc = expand(); if (rc) return rc; }
         const bool part = d.arena_start != OTF_UNSET;
         const RowSpec rs{&d.lvl[t].n_prim, &d.lvl[t], prev >= 0 ? &d.lvl[prev] : nullptr,
                          part ? d.cursor : S.arena_used, d.pr_dig, part ? d.arena_end : S.arena_rows};
         int rc = enqueue_stage2(p, m, S, R, prec, rs, s);
         if (rc) return rc;
         const uint32_t r0 = p->lvl_range_off[t], nr = p->lvl_range_off[t + 1] - r0;
-        {
+        if (p->big_asg && !S.lfu_log && S.ct_first) {
+            // many requests per stream: the ordered resolution over chunks (decode.cuh k_asg_*)
+            ProfScope ps(K_ASSIGN, s);
+            const uint32_t nch = (R + ASG_CH - 1) / ASG_CH;
+            const dim3 grid(nch, nr);
+            const uint32_t limit = d.arena_start == OTF_UNSET ? S.arena_rows : d.arena_end;
+            k_asg_probe<<<grid, ASG_CH, 0, s>>>(d, S, t, r0, limit); CKL();
+            k_asg_dedup<<<grid, ASG_CH, 0, s>>>(d, S, t, r0, limit); CKL();
+            k_asg_scan<<<nr, 32, 0, s>>>(d, S, t, r0, nch, limit); CKL();
+            k_asg_number<<<grid, ASG_CH, 0, s>>>(d, S, t, r0, limit); CKL();
+            k_asg_values<<<grid, ASG_CH, 0, s>>>(d, S, t, r0, limit); CKL();
+            k_asg_arrive<<<grid, ASG_CH, 0, s>>>(d, S, t, r0, limit, lm); CKL();
+        } else {
             ProfScope ps(K_ASSIGN, s);
             k_assign<0><<<nr, ASSIGN_T, 0, s>>>(d, S, t, r0, lm, nullptr, nullptr, nullptr);
             CKL();
@@ -2244,31 +2305,51 @@ extern "C" int otflm_streams_cache_put(OtflmStreams *s, int32_t sid, int64_t n, 
     return check_err(s, st);
 }
 
-// RescoreCache.roll_stats / clear (cache.py:121-128, :155-157) on one stream
-__global__ void k_stream_stats_op(DevStreams S, uint32_t s, int op) {
+// RescoreCache.roll_stats / clear (cache.py:156-158, :136-140) on one stream;
+// with a capacity bound also the policy: roll moves the window's evictions
+// into the cumulative count, clear empties the LFU structure (the window's
+// counters stay, as in the reference)
+__global__ void k_stream_stats_op(DevStreams S, uint32_t s, int op, DevLfu L, int bounded) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     unsigned long long *st = S.stats + (size_t)s * 8;
-    if (op == 0) { st[3] += st[0]; st[4] += st[1]; st[5] += st[2]; st[0] = st[1] = st[2] = 0; }
-    else st[6] = 0;                                    // entries after clear
+    if (op == 0) {
+        st[3] += st[0]; st[4] += st[1]; st[5] += st[2]; st[0] = st[1] = st[2] = 0;
+        if (bounded) { unsigned long long *ev = L.ev + (size_t)s * 2; ev[1] += ev[0]; ev[0] = 0; }
+    } else {
+        st[6] = 0;                                     // entries after clear
+        if (bounded) {
+            uint32_t *sc = L.sc + (size_t)s * 8;
+            sc[0] = LFU_NIL; sc[1] = 0; sc[2] = 0; sc[3] = LFU_NIL; sc[4] = 0; sc[5] = LFU_NIL;
+        }
+    }
+}
+
+static int stats_op_ok(const OtflmStreams *s, int32_t sid) {
+    if (!s || sid < 0 || sid >= s->d.S) return OTFLM_ERR_VALUE;
+    return OTFLM_OK;
 }
 
 extern "C" int otflm_streams_roll_stats(OtflmStreams *s, int32_t sid, void *stream) {
-    int rc = cache_direct_ok(s, sid, 0);
+    int rc = stats_op_ok(s, sid);
     if (rc) return rc;
-    k_stream_stats_op<<<1, 1, 0, (cudaStream_t)stream>>>(s->d, (uint32_t)sid, 0);
+    const bool bounded = s->lfu && s->d.lfu_log;
+    k_stream_stats_op<<<1, 1, 0, (cudaStream_t)stream>>>(s->d, (uint32_t)sid, 0, bounded ? s->lfu->d : DevLfu{},
+                                                         bounded ? 1 : 0);
     CKL();
     return OTFLM_OK;
 }
 
 extern "C" int otflm_streams_cache_clear(OtflmStreams *s, int32_t sid, void *stream) {
-    int rc = cache_direct_ok(s, sid, 0);
+    int rc = stats_op_ok(s, sid);
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
     const size_t o = (size_t)sid * s->d.kc_cap, n = s->d.kc_cap;
     CK(cudaMemsetAsync(s->d.kc_key + o, 0, n * 8, st));
     CK(cudaMemsetAsync(s->d.kc_claim + o, 0xFF, n * 4, st));
     CK(cudaMemsetAsync(s->d.kc_cnext + o, 0xFF, n * 4, st));
-    k_stream_stats_op<<<1, 1, 0, st>>>(s->d, (uint32_t)sid, 1);
+    const bool bounded = s->lfu && s->d.lfu_log;
+    if (bounded) CK(cudaMemsetAsync(s->lfu->d.kc_lfu + o, 0xFF, n * 4, st));
+    k_stream_stats_op<<<1, 1, 0, st>>>(s->d, (uint32_t)sid, 1, bounded ? s->lfu->d : DevLfu{}, bounded ? 1 : 0);
     CKL();
     return OTFLM_OK;
 }

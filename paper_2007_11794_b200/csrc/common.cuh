@@ -92,6 +92,10 @@ struct DevStreams {
     uint8_t *arena_dig;
     float *arena_deh;
     uint32_t *arena_dep;
+    // multi-CTA assign (decode.cuh k_asg_*): per content-table slot the first
+    // request of the level that created the key ([S][ct_cap], all OTF_UNSET
+    // between levels; allocated on first use)
+    uint32_t *ct_first;
 };
 
 // per-request state

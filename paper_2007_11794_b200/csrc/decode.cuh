@@ -87,6 +87,9 @@ struct DevPlan {
     const uint32_t *ul_off, *rq_off;
     unsigned long long *phase_ns;  // profiling only: [expand, update, hs, assign, CTAs]
     uint8_t *kept;                // lattice-out only: [n_slots] arrival kept (expanded, or a final winner)
+    // multi-CTA assign (k_asg_*): per request kind / table slot / aux, per chunk counts and offsets
+    uint8_t *as_kind;
+    uint32_t *as_slot, *as_aux, *ch_cnt, *ch_pre;
 };
 
 // content digest term of element i of a hidden row / word j of the history
@@ -399,8 +402,16 @@ __device__ __forceinline__ void small_lm_scores(DevPlan &P, const DevStreams &S,
 }
 
 constexpr int EXP_WARPS = 8;
+// Nodes with big_min < cap <= EXPB_MAX arrival slots (big beams / wide
+// lattices; big_min = EXPB_MIN unless a test lowers it) are expanded by
+// k_expand_big, a CTA per node; k_expand skips them when it runs beside it
+// and takes every node otherwise.
+constexpr uint32_t EXPB_MIN = 64, EXPB_MAX = 2048;
+constexpr int EXPB_T = 512;
+
 __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, DevNgram g, uint32_t node_begin,
-                                                uint32_t n_nodes, long long beam, uint32_t lvl) {
+                                                uint32_t n_nodes, long long beam, uint32_t lvl,
+                                                uint32_t big_min = 0xFFFFFFFFu) {
     __shared__ uint32_t s_ctx[EXP_WARPS][32], s_slot[EXP_WARPS][32];
     __shared__ double s_score[EXP_WARPS][32];
     __shared__ uint32_t s_arc[EXP_WARPS][32];
@@ -408,8 +419,141 @@ __global__ void __launch_bounds__(256) k_expand(DevPlan P, DevStreams S, DevNgra
     const uint32_t gw = blockIdx.x * EXP_WARPS + wib;
     if (gw >= n_nodes) return;
     const NodeInfo nd = P.nodes[P.level_nodes[node_begin + gw]];
+    if (nd.cap > big_min && nd.cap <= EXPB_MAX) return;           // k_expand_big's node
     expand_node(P, S, g, nd, beam, lvl, 0, &P.lvl[lvl].n_prim, s_ctx[wib], s_slot[wib], s_score[wib], s_arc[wib],
                 threadIdx.x & 31);
+}
+
+// One node with many arrival slots per CTA (decoder.py:131-149): the same
+// recombination (per context the best score, ties to the earliest arrival),
+// the same beam ranking (score desc, ctx asc) and the same request emission as
+// expand_node, but O(cap) for the recombination (a shared-memory hash of the
+// contexts: atomicMax of the order-preserving score bits, then atomicMin of
+// the arrival key among the tied) and the ranking spread over the CTA.
+// Dynamic shared memory: expb_smem(cap_max).
+__host__ __device__ constexpr uint32_t expb_hash_slots(uint32_t cap) {
+    uint32_t h = 64;
+    while (h < 2 * cap) h <<= 1;
+    return h;
+}
+__host__ __device__ constexpr size_t expb_smem(uint32_t cap) {
+    return (size_t)cap * 56 + (size_t)expb_hash_slots(cap) * 20 + 64;
+}
+__device__ __forceinline__ unsigned long long ord_score(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x == 0.0 ? 0.0 : x);   // -0 == +0
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__global__ void __launch_bounds__(EXPB_T) k_expand_big(DevPlan P, DevStreams S, DevNgram g, uint32_t node_begin,
+                                                       long long beam, uint32_t lvl, uint32_t cap_max, uint32_t big_min) {
+    extern __shared__ __align__(16) uint8_t smem_eb[];
+    __shared__ uint32_t s_arc[32], s_nwin;
+    const NodeInfo nd = P.nodes[P.level_nodes[node_begin + blockIdx.x]];
+    if (nd.cap <= big_min || nd.cap > EXPB_MAX) return;           // k_expand's node
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t C = cap_max, HB = expb_hash_slots(cap_max), cap = nd.cap;
+    double *a_sc = reinterpret_cast<double *>(smem_eb);
+    unsigned long long *a_key = reinterpret_cast<unsigned long long *>(a_sc + C);
+    double *w_sc = reinterpret_cast<double *>(a_key + C);
+    double *t_sc = w_sc + C;
+    unsigned long long *h_best = reinterpret_cast<unsigned long long *>(t_sc + C);
+    unsigned long long *h_kmin = h_best + HB;
+    uint32_t *a_ct = reinterpret_cast<uint32_t *>(h_kmin + HB);
+    uint32_t *a_hs = a_ct + C;
+    uint32_t *w_ct = a_hs + C, *w_i = w_ct + C, *t_ct = w_i + C, *t_slot = t_ct + C;
+    uint32_t *h_ctx = t_slot + C;
+    const uint32_t outdeg = nd.out_e - nd.out_b;
+    const uint32_t rq0 = nd.req_base;
+    if (outdeg == 0) return;
+    for (uint32_t i = tid; i < HB; i += EXPB_T) { h_ctx[i] = OTF_UNSET; h_best[i] = 0ull; h_kmin[i] = ~0ull; }
+    if (tid < 32 && (uint32_t)tid < outdeg) s_arc[tid] = P.out_list[nd.out_b + tid];
+    if (tid == 0) s_nwin = 0;
+    __syncthreads();
+    // arrivals -> shared memory; per context the best (score, then key) through the hash
+    for (uint32_t i = tid; i < cap; i += EXPB_T) {
+        const Arrival a = P.arr[nd.slot_base + i];
+        a_sc[i] = a.score; a_ct[i] = a.ctx; a_key[i] = arr_key(a);
+        uint32_t hs = OTF_UNSET;
+        if (a.ctx != OTF_UNSET) {
+            hs = (a.ctx * 0x9E3779B1u) & (HB - 1);
+            for (;;) {
+                const uint32_t prev = atomicCAS(&h_ctx[hs], OTF_UNSET, a.ctx);
+                if (prev == OTF_UNSET || prev == a.ctx) break;
+                hs = (hs + 1) & (HB - 1);
+            }
+            atomicMax(&h_best[hs], ord_score(a.score));
+        }
+        a_hs[i] = hs;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < cap; i += EXPB_T)
+        if (a_hs[i] != OTF_UNSET && ord_score(a_sc[i]) == h_best[a_hs[i]]) atomicMin(&h_kmin[a_hs[i]], a_key[i]);
+    __syncthreads();
+    // winners (one per context) into a list; their order there is irrelevant
+    for (uint32_t i = tid; i < cap; i += EXPB_T) {
+        const uint32_t hs = a_hs[i];
+        if (hs != OTF_UNSET && ord_score(a_sc[i]) == h_best[hs] && a_key[i] == h_kmin[hs]) {
+            const uint32_t k = atomicAdd(&s_nwin, 1u);
+            w_sc[k] = a_sc[i]; w_ct[k] = a_ct[i]; w_i[k] = i;
+        }
+    }
+    __syncthreads();
+    const uint32_t n_win = s_nwin;
+    const uint32_t n_kept = (uint32_t)min((long long)n_win, beam);
+    // rank = winners ahead in (score desc, ctx asc) -- contexts are distinct among winners
+    for (uint32_t k = tid; k < n_win; k += EXPB_T) {
+        const double sk = w_sc[k];
+        const uint32_t ck = w_ct[k];
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < n_win; j++) {
+            const double sj = w_sc[j];
+            rank += (sj > sk || (sj == sk && w_ct[j] < ck)) ? 1u : 0u;
+        }
+        if (rank < n_kept) {
+            t_sc[rank] = sk; t_ct[rank] = ck; t_slot[rank] = nd.slot_base + w_i[k];
+            if (P.kept) P.kept[nd.slot_base + w_i[k]] = 1;
+        }
+    }
+    __syncthreads();
+    // one thread per (rank, arc) request, as expand_node
+    const uint32_t nreq = n_kept * outdeg;
+    for (uint32_t j0 = 0; j0 < nreq; j0 += EXPB_T) {
+        const uint32_t j = j0 + tid;
+        const bool emit = j < nreq;
+        uint32_t r = 0, c = 0, crow = OTF_UNSET;
+        int32_t w = 0;
+        uint8_t st = RQ_INVALID;
+        if (emit) {
+            const uint32_t rank = j / outdeg, q = j - rank * outdeg;
+            c = t_ct[rank];
+            const uint32_t a = (outdeg <= 32) ? s_arc[q] : P.out_list[nd.out_b + q];
+            r = rq0 + j;
+            w = P.arc_word[a];
+            crow = S.ctx_row[(uint64_t)nd.stream * (S.max_ctx + 1) + c];
+            st = RQ_NOCACHE;
+            uint32_t cslot = OTF_UNSET;
+            if (S.enabled) cslot = cache_probe(S, nd.stream, c, w, r, &st);
+            double ps = 0.0;
+            {
+                const uint32_t *meta = S.arena_meta + (size_t)crow * OTF_META;
+                if (!ngram_logprob_dev(g, meta + 1, (int)meta[0], w, &ps)) { atomicOr(S.err, OTF_E_KEY); ps = 0.0; }
+            }
+            P.rq_c[r] = c;
+            P.rq_w[r] = w;
+            P.rq_arc[r] = a;
+            P.rq_parent[r] = t_slot[rank];
+            P.rq_score[r] = __dadd_rn(t_sc[rank], P.arc_ac[a]);
+            P.rq_slm[r] = P.arc_slm[a];
+            P.rq_ps[r] = ps;
+            P.rq_dslot[r] = P.arc_slot[a] + rank;
+            P.rq_m[r] = OTF_UNSET;
+            P.rq_cslot[r] = cslot;
+            P.rq_state[r] = st;
+        }
+        compact_primary(P, S, &P.lvl[lvl].n_prim, emit && (st == RQ_PENDING || st == RQ_NOCACHE), r, c, w,
+                        nd.stream, crow);
+    }
+    for (uint32_t r = nreq + tid; r < nd.keep * outdeg; r += EXPB_T) P.rq_state[rq0 + r] = RQ_INVALID;
 }
 
 // --------------------------------------------------------------------------
@@ -712,6 +856,225 @@ __global__ void __launch_bounds__(ASSIGN_T) k_assign(DevPlan P, DevStreams S, ui
 }
 
 // --------------------------------------------------------------------------
+// multi-CTA assign: the same ordered resolution as assign_range for streams
+// whose level has many requests (big beams, wide lattices), spread over
+// chunks of ASG_CH requests in six grid steps (grid = chunks x stream ranges):
+//   probe   content-table probe / insert per computed request; a new key's
+//           first request (lowest index = reference order) by atomicMin on
+//           the key's slot (ct_first)
+//   dedup   equal contexts created later in the level -> duplicates of that
+//           first (full-row check); per-chunk count of new contexts
+//   scan    per stream: chunk offsets = len + earlier chunks' new contexts
+//   number  len + 1 numbering of the new contexts in request order
+//           (context_table.py:83-86)
+//   values  duplicates take their first's index; computed values into the
+//           cache (cache.py:99-109); ct_first back to unset
+//   arrive  hits read the cache (earlier level or an earlier claim of this
+//           level), arrivals and counters as assign_range (MODE 0)
+// Used when no capacity-bounded cache logs lookups (that log is ordered).
+// --------------------------------------------------------------------------
+constexpr int ASG_CH = 256;
+constexpr uint32_t ASSIGN_BIG = 4096;      // a plan whose largest range exceeds this uses k_asg_*
+enum : uint8_t { AK_NONE = 0, AK_OLD = 1, AK_FIRST = 2, AK_DUP = 3 };
+
+struct AsgIdx {
+    StreamRange rg;
+    uint32_t r, ci;
+    bool block_live, in;
+};
+__device__ __forceinline__ AsgIdx asg_idx(const DevPlan &P, uint32_t range_begin) {
+    AsgIdx a;
+    a.rg = P.ranges[range_begin + blockIdx.y];
+    const uint32_t c0 = a.rg.rb + blockIdx.x * ASG_CH;
+    a.block_live = c0 < a.rg.re;
+    a.r = c0 + threadIdx.x;
+    a.in = a.block_live && a.r < a.rg.re;
+    a.ci = blockIdx.y * gridDim.x + blockIdx.x;
+    return a;
+}
+__device__ __forceinline__ bool asg_prim(const DevPlan &P, const DevStreams &S, uint32_t s, uint32_t r,
+                                         uint8_t *st_out, uint32_t *cslot_out) {
+    const uint8_t st = P.rq_state[r];
+    const uint32_t cslot = (st == RQ_HIT || st == RQ_PENDING) ? P.rq_cslot[r] : OTF_UNSET;
+    bool prim = st == RQ_NOCACHE;
+    if (st == RQ_PENDING) prim = S.kc_claim[(uint64_t)s * S.kc_cap + cslot] == r;
+    *st_out = st; *cslot_out = cslot;
+    return prim;
+}
+
+__global__ void __launch_bounds__(ASG_CH) k_asg_probe(DevPlan P, DevStreams S, uint32_t lvl, uint32_t range_begin,
+                                                      uint32_t limit) {
+    const AsgIdx a = asg_idx(P, range_begin);
+    const LevelCtr lc = P.lvl[lvl];
+    if (!a.in || (uint64_t)lc.base + lc.n_prim > limit) return;
+    const uint32_t s = a.rg.stream, r = a.r;
+    const uint64_t cb = (uint64_t)s * S.ct_cap;
+    const uint32_t cmask = S.ct_cap - 1;
+    uint8_t st;
+    uint32_t cslot;
+    uint8_t kind = AK_NONE;
+    uint32_t slot_out = OTF_UNSET, aux = OTF_UNSET;
+    if (asg_prim(P, S, s, r, &st, &cslot)) {
+        const uint32_t m = P.rq_m[r];
+        const unsigned long long key = otf_hash64(P.pr_dig[m]) | 1ull;
+        const uint32_t row = lc.base + m;
+        kind = AK_FIRST;                                   // new unless found below
+        uint32_t slot = (uint32_t)(key >> 20) & cmask;
+        for (uint32_t probes = 0; probes <= S.ct_cap; probes++) {
+            unsigned long long k = S.ct_key[cb + slot];
+            if (k == 0ull) {
+                const unsigned long long prev = atomicCAS(&S.ct_key[cb + slot], 0ull, key);
+                if (prev == 0ull) { slot_out = slot; break; }
+                k = prev;
+            }
+            if (k == key) {
+                const uint32_t ix = ld_volatile_u32(&S.ct_idx[cb + slot]);
+                if (ix == OTF_UNSET) { slot_out = slot; break; }         // created in this level
+                if (rows_equal_lane(S, S.ct_row[cb + slot], row)) { kind = AK_OLD; aux = ix; break; }
+            }
+            slot = (slot + 1) & cmask;
+        }
+        if (kind == AK_FIRST && slot_out != OTF_UNSET) atomicMin(&S.ct_first[cb + slot_out], r);
+    }
+    P.as_kind[r] = kind;
+    P.as_slot[r] = slot_out;
+    P.as_aux[r] = aux;
+}
+
+__global__ void __launch_bounds__(ASG_CH) k_asg_dedup(DevPlan P, DevStreams S, uint32_t lvl, uint32_t range_begin,
+                                                      uint32_t limit) {
+    const AsgIdx a = asg_idx(P, range_begin);
+    const LevelCtr lc = P.lvl[lvl];
+    if (!a.block_live || (uint64_t)lc.base + lc.n_prim > limit) return;
+    bool first = false;
+    if (a.in && P.as_kind[a.r] == AK_FIRST) {
+        const uint32_t r = a.r, slot = P.as_slot[r];
+        first = true;
+        if (slot != OTF_UNSET) {
+            const uint32_t f = S.ct_first[(uint64_t)a.rg.stream * S.ct_cap + slot];
+            if (f != r) {
+                if (rows_equal_lane(S, lc.base + P.rq_m[f], lc.base + P.rq_m[r])) {
+                    P.as_kind[r] = AK_DUP; P.as_aux[r] = f; first = false;
+                } else {
+                    atomicOr(S.err, OTF_E_HASH);
+                    P.as_slot[r] = OTF_UNSET;               // numbered without a slot -> NOSLOT below
+                }
+            }
+        }
+    }
+    const int n = __syncthreads_count(first);
+    if (threadIdx.x == 0) P.ch_cnt[a.ci] = (uint32_t)n;
+}
+
+__global__ void __launch_bounds__(32) k_asg_scan(DevPlan P, DevStreams S, uint32_t lvl, uint32_t range_begin,
+                                                 uint32_t nch, uint32_t limit) {
+    const LevelCtr lc = P.lvl[lvl];
+    if ((uint64_t)lc.base + lc.n_prim > limit) return;
+    const StreamRange rg = P.ranges[range_begin + blockIdx.x];
+    const uint32_t s = rg.stream, lane = threadIdx.x;
+    const uint32_t n = (rg.re - rg.rb + ASG_CH - 1) / ASG_CH;
+    uint32_t run = S.table_len[s];
+    for (uint32_t c0 = 0; c0 < n; c0 += 32) {
+        const uint32_t c = c0 + lane;
+        uint32_t v = c < n ? P.ch_cnt[blockIdx.x * nch + c] : 0u, x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if ((int)lane >= o) x += y;
+        }
+        if (c < n) P.ch_pre[blockIdx.x * nch + c] = run + x - v;
+        run += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) S.table_len[s] = run > S.max_ctx ? S.max_ctx : run;
+}
+
+__global__ void __launch_bounds__(ASG_CH) k_asg_number(DevPlan P, DevStreams S, uint32_t lvl, uint32_t range_begin,
+                                                       uint32_t limit) {
+    __shared__ uint32_t s_w[ASG_CH / 32];
+    const AsgIdx a = asg_idx(P, range_begin);
+    const LevelCtr lc = P.lvl[lvl];
+    if (!a.block_live || (uint64_t)lc.base + lc.n_prim > limit) return;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const bool first = a.in && P.as_kind[a.r] == AK_FIRST;
+    const unsigned b = __ballot_sync(0xffffffffu, first);
+    if (lane == 0) s_w[wid] = __popc(b);
+    __syncthreads();
+    if (!first) return;
+    uint32_t before = __popc(b & ((1u << lane) - 1u));
+    for (int w2 = 0; w2 < wid; w2++) before += s_w[w2];
+    const uint32_t idx = P.ch_pre[a.ci] + before + 1u;           // len + 1 (context_table.py:83-86)
+    const uint32_t r = a.r, s = a.rg.stream, slot = P.as_slot[r], row = lc.base + P.rq_m[r];
+    if (idx > S.max_ctx || slot == OTF_UNSET) {
+        atomicOr(S.err, OTF_E_TABLE_FULL | (slot == OTF_UNSET ? OTF_E_NOSLOT : 0u));
+        return;
+    }
+    const uint64_t cb = (uint64_t)s * S.ct_cap;
+    S.ct_idx[cb + slot] = idx;
+    S.ct_row[cb + slot] = row;
+    S.ctx_row[(uint64_t)s * (S.max_ctx + 1) + idx] = row;
+    P.as_aux[r] = idx;
+}
+
+__global__ void __launch_bounds__(ASG_CH) k_asg_values(DevPlan P, DevStreams S, uint32_t lvl, uint32_t range_begin,
+                                                       uint32_t limit) {
+    const AsgIdx a = asg_idx(P, range_begin);
+    const LevelCtr lc = P.lvl[lvl];
+    if (!a.in || (uint64_t)lc.base + lc.n_prim > limit) return;
+    const uint32_t r = a.r, s = a.rg.stream;
+    const uint8_t kind = P.as_kind[r];
+    if (kind == AK_NONE) return;
+    uint32_t cn = P.as_aux[r];
+    if (kind == AK_DUP) { cn = P.as_aux[cn]; P.as_aux[r] = cn; }   // the first's index (OTF_UNSET if it failed)
+    const uint32_t slot = P.as_slot[r];
+    if (slot != OTF_UNSET) S.ct_first[(uint64_t)s * S.ct_cap + slot] = OTF_UNSET;
+    if (P.rq_state[r] == RQ_PENDING) {
+        const uint64_t k = (uint64_t)s * S.kc_cap + P.rq_cslot[r];
+        S.kc_p[k] = P.pr_p[P.rq_m[r]];
+        S.kc_cnext[k] = cn;
+    }
+}
+
+__global__ void __launch_bounds__(ASG_CH) k_asg_arrive(DevPlan P, DevStreams S, uint32_t lvl, uint32_t range_begin,
+                                                       uint32_t limit, double lm_weight) {
+    const AsgIdx a = asg_idx(P, range_begin);
+    const LevelCtr lc = P.lvl[lvl];
+    if (!a.block_live || (uint64_t)lc.base + lc.n_prim > limit) return;
+    const uint32_t r = a.r, s = a.rg.stream;
+    bool valid = false, prim = false;
+    if (a.in) {
+        const uint8_t st = P.rq_state[r];
+        valid = st != RQ_INVALID;
+        prim = P.as_kind[r] != AK_NONE;
+        if (valid) {
+            double p;
+            uint32_t cn;
+            if (prim) { p = P.pr_p[P.rq_m[r]]; cn = P.as_aux[r]; }
+            else {
+                const uint64_t k = (uint64_t)s * S.kc_cap + P.rq_cslot[r];
+                p = S.kc_p[k];
+                cn = ld_volatile_u32(&S.kc_cnext[k]);
+            }
+            // delta rounded to f32 (codec.py:57-59); score (decoder.py:144)
+            const float delta = __double2float_rn(__dsub_rn(p, P.rq_ps[r]));
+            const double ns = __dadd_rn(P.rq_score[r], __dmul_rn(lm_weight, __dadd_rn(P.rq_slm[r], (double)delta)));
+            Arrival out;
+            out.score = ns; out.ctx = cn; out.parent = P.rq_parent[r]; out.arc = P.rq_arc[r];
+            out.lvl = lvl; out.ridx = r; out.pad = 0;
+            P.arr[P.rq_dslot[r]] = out;
+        }
+    }
+    const int look = __syncthreads_count(valid), miss = __syncthreads_count(prim);
+    if (threadIdx.x == 0 && look) {
+        unsigned long long *stt = S.stats + (size_t)s * 8;
+        atomicAdd(&stt[0], (unsigned long long)look);
+        atomicAdd(&stt[1], (unsigned long long)(look - miss));
+        atomicAdd(&stt[2], (unsigned long long)miss);
+        atomicAdd(&stt[7], (unsigned long long)look);
+        if (S.enabled) atomicAdd(&stt[6], (unsigned long long)miss);
+    }
+}
+
+// --------------------------------------------------------------------------
 // final: best token over sorted finals x sorted ctx (decoder.py:150-156),
 // backtrace (decoder.py:157-162), score breakdown (decoder.py:163-169)
 // --------------------------------------------------------------------------
@@ -730,8 +1093,35 @@ __global__ void k_final(DevPlan P, DevStreams S, double lm_weight, int last_lvl)
     for (uint32_t f = P.final_off[u]; f < P.final_off[u + 1]; f++) {
         const NodeInfo nd = P.nodes[P.finals[f]];
         if (nd.cap == 0) continue;
-        recombine_node(P.arr, P.slot_win, nd.slot_base, nd.cap, lane);
         double bs = 0.0; uint32_t bc = OTF_UNSET, bslot = OTF_UNSET; bool bh = false;
+        if (!P.kept) {
+            // the node's best recombination winner is the lexicographic best
+            // arrival by (score desc, ctx asc, arrival key asc): no O(cap^2)
+            // recombination unless lattice-out wants every winner
+            uint64_t bk = 0;
+            for (uint32_t i = lane; i < nd.cap; i += 32) {
+                const Arrival a = P.arr[nd.slot_base + i];
+                if (a.ctx == OTF_UNSET) continue;
+                const uint64_t k = arr_key(a);
+                if (!bh || a.score > bs || (a.score == bs && (a.ctx < bc || (a.ctx == bc && k < bk)))) {
+                    bh = true; bs = a.score; bc = a.ctx; bk = k; bslot = nd.slot_base + i;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) {
+                const double os = __shfl_xor_sync(0xffffffffu, bs, o);
+                const uint32_t oc = __shfl_xor_sync(0xffffffffu, bc, o);
+                const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
+                const uint32_t osl = __shfl_xor_sync(0xffffffffu, bslot, o);
+                const bool oh = __shfl_xor_sync(0xffffffffu, (int)bh, o);
+                if (oh && (!bh || os > bs || (os == bs && (oc < bc || (oc == bc && ok < bk))))) {
+                    bh = true; bs = os; bc = oc; bk = ok; bslot = osl;
+                }
+            }
+            if (bh && (!have || bs > best)) { have = true; best = bs; best_ctx = bc; best_slot = bslot; }
+            continue;
+        }
+        recombine_node(P.arr, P.slot_win, nd.slot_base, nd.cap, lane);
         for (uint32_t i0 = 0; i0 < nd.cap; i0 += 32) {
             uint32_t i = i0 + lane;
             if (i < nd.cap && P.slot_win[nd.slot_base + i]) {

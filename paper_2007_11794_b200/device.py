@@ -286,6 +286,14 @@ class Plan:
         _lib.check(_lib.load().otflm_plan_info(self.handle, _p(out)), "plan info")
         return out
 
+    def wide(self) -> int:
+        """Bit 0: nodes with more than 64 arrival slots (CTA-per-node expand);
+        bit 1: request ranges above 4096 per (level, stream) (multi-CTA
+        assign).  Both are level-schedule kernels."""
+        f = C.c_int32(0)
+        _lib.check(_lib.load().otflm_plan_wide(self.handle, C.byref(f)), "plan wide")
+        return int(f.value)
+
     def refresh(self, lattices, stream_ids=None) -> bool:
         """Load another batch with the same compiled structure into this plan
         (same buffers, captured graphs stay valid).  False: structure differs."""

@@ -570,6 +570,10 @@ class BatchDecoder:
         self.dmodel = DeviceModel.get(model, tree)
         self.ngram = DeviceNgram.get(small_lm, self.dmodel)
         self.precision = precision
+        # "auto": the persistent kernels for ordinary beams; a batch with wide
+        # levels (big beams: nodes of more than 64 arrival slots) is moved to
+        # the level schedule when it is prepared (k_expand_big / k_asg_*)
+        self._auto = schedule == "auto"
         if schedule == "auto":
             schedule = auto_schedule(self.dmodel, precision, n_streams)
         if schedule not in _lib.SCHED:
@@ -649,6 +653,8 @@ class BatchDecoder:
         for g in range(G):
             ids = np.arange(bounds[g], bounds[g + 1])
             p = Plan(self.streams, [lattices[i] for i in ids], beam, stream_ids=ids)
+            if self._auto and self.schedule != "level" and p.wide():
+                self.schedule = "level"
             p.set_schedule(self.schedule)
             if self.lattice_out:
                 p.set_lattice_out(True)

@@ -110,3 +110,34 @@ def test_bounded_cache_batch_decoder_vs_oracle(schedule, precision):
             assert hyps[u].arcs == r.arcs
             assert (int(st[u, 0]), int(st[u, 1]), int(st[u, 2]), int(cs[u, 0]), int(cs[u, 2])) == \
                 (o.lookups, o.hits, o.misses, o.evictions, o.entries), u
+
+
+def test_bounded_cache_roll_and_clear_match_oracle(small):
+    """roll_stats and clear on a capacity-bounded cache (cache.py:156-158,
+    :136-140): decode, roll, decode (table and cache retained), clear the
+    cache only, decode -- window / cumulative counters, evictions, resident
+    entries and table length after every step equal the oracle's."""
+    from paper_2007_11794_b200 import rescore_onthefly
+    s, gm, lats = small
+    for cap in (32 * 40, 32 * 400):
+        st = _stack(gm, cap)
+        ref = O.OracleStack(gm.model, gm.tree, capacity_bytes=cap)
+        og = O.OracleNgram(gm.lm)
+        for step, lat in enumerate([lats[0], lats[0], lats[0]]):
+            hyp, _ = rescore_onthefly(lat, gm.lm, st, beam=6)
+            r = ref.rescore_onthefly(lat, og, beam=6)
+            assert hyp.arcs == r.arcs and abs(hyp.combined_score - r.combined_score) <= 1e-9
+            a, c, o = st.cache.stats(), st.cache.cumulative_stats(), ref.stats()
+            got = (a.lookups, a.hits, a.misses, len(st.cache), len(st.table), c.lookups, c.hits, c.misses)
+            assert got == (o.lookups, o.hits, o.misses, o.entries, o.table_len,
+                           o.cum_lookups, o.cum_hits, o.cum_misses), (cap, step, got, o)
+            assert a.evictions == o.evictions, (cap, step)
+            if step == 0:
+                st.cache.roll_stats()
+                ref.roll_stats()
+                assert st.cache.stats().lookups == 0 and st.cache.stats().evictions == 0
+            elif step == 1:
+                ev_before = st.cache.cumulative_stats().evictions
+                st.cache.clear()
+                ref.cache_clear()
+                assert len(st.cache) == 0 and st.cache.cumulative_stats().evictions == ev_before
