@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-queries", action="store_true", help="skip the config-d query microbench")
     ap.add_argument("--beam-sweep", action="store_true", help="add the config-c beam sweep extra")
+    ap.add_argument("--no-wide", action="store_true",
+                    help="config e: skip the config-c beam sweep and fat-variant extras")
     ap.add_argument("--table4", action="store_true", help="add the Table-4 cache-capacity sweep extra")
     ap.add_argument("--config", default="e", choices=["b", "e"],
                     help="b: the headline config (default); e: 4096 utterances at V=64k sharded over ranks")
@@ -331,6 +333,46 @@ def beam_sweep(precision: str, beams=(1, 2, 4, 8, 16, 32, 64), n_utt: int = 8, f
         torch.cuda.empty_cache()
     return {"workload": f"config c: V=65536 H=512 MaxEnt 2^22, {n_utt} utterances x {frames} frames, "
                         f"breadth 3, {precision} update; L2 flushed before each run", "sweep": rows}
+
+
+def fat_variant(precision: str, n_utt: int = 4, frames: int = 300, reps: int = 2):
+    """SURVEY.md §8d config (b) fat variant: breadth 16, beam 64 (16 nodes x
+    64 tokens x 16 arcs = 16k requests per frame and utterance, ~1k arrival
+    slots per node), decoded with the automatic schedule (level: the
+    CTA-per-node expand and the multi-CTA assign).  Device time, lattices
+    resident, L2 flushed before each run."""
+    import torch
+    from paper_2007_11794_b200 import synth
+    from paper_2007_11794_b200.rescore import BatchDecoder
+    s = synth.build_setup("b_fat", n_utt=n_utt, T=frames, seed=3)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    need = BatchDecoder.contexts_needed(s.lattices, 64)
+    dec = BatchDecoder(s.model, s.tree, s.small_lm, n_utt, need, precision=precision)
+    dec.prepare(s.lattices, 64)
+    dec.run(1.0)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        dec.run(1.0)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = float(np.median(ts))
+    hyps, out = dec.fetch()
+    fr = sum(len(h.arcs) for h in hyps)
+    st = dec.streams.stats()
+    res = {"workload": f"config b fat variant: V=20000 H=256 MaxEnt 2^21, {n_utt} utterances x {frames} frames, "
+                       f"breadth 16, beam 64, {precision}", "schedule": dec.schedule, "ms": ms,
+           "frames_per_s": fr / (ms / 1e3), "rtf_per_stream": (ms / 1e3) / (frames * FRAME_S),
+           "requests_per_s": int(out["expansions"].sum()) / (ms / 1e3),
+           "contexts_created": int(st[:, 3].sum())}
+    del dec
+    torch.cuda.empty_cache()
+    return res
 
 
 def table4_sweep(precision: str, capacities_kb=(0, 16, 64, 256, 1024, -1), n_streams: int = 74,
@@ -693,6 +735,10 @@ def run_config_e(args):
     extras = {}
     if rank == 0 and not args.no_queries:
         extras["config_d_queries"] = query_microbench("exact" if args.precision == "exact" else args.precision)
+    if rank == 0 and not args.no_wide:
+        # big beams / wide lattices (the level schedule's CTA-per-node expand and multi-CTA assign)
+        extras["config_c_beam_sweep"] = beam_sweep(args.precision, beams=(8, 16, 32, 64), reps=2)
+        extras["fat_variant"] = fat_variant(args.precision)
     if rank == 0 and args.table4:
         extras["table4_capacity_sweep"] = table4_sweep(args.precision)
     if rank == 0:

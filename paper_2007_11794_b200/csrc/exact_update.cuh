@@ -806,9 +806,10 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
                     gmark(29);
                     named_sync(3, NT - 64);
                 }
+                // (no barrier after the fallbacks: the U staging below does not
+                // touch what they read, and their list is reset after the
+                // tile's completion barrier)
                 fallbacks(mt - 1, 2);
-                named_sync(3, NT - 64);
-                if (tid == 64) fallbacks_done(mt - 1);
                 gmark(30);
             }
             const bool us_t = rg.us && !(side_uses_us && mt == mt0);
@@ -851,6 +852,7 @@ __device__ __forceinline__ void update_chunk(const DevModel &m, uint32_t q0, int
             tiles_done++;
             __syncthreads();
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (tid == 64 && mt > mt0) fallbacks_done(mt - 1);   // every warp is past fallbacks(mt - 1)
             // the ring is drained: issue the next tile's first stages now, so
             // they load while this tile's epilogue runs
             if (wid == 1 && mt + 1 < mt1) produce(mt + 1, 0, npre);
