@@ -618,7 +618,7 @@ def run_config_e(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     need = max(BatchDecoder.contexts_needed(l, base.beam) for _, l in batches)
     dec = BatchDecoder(base.model, base.tree, base.small_lm, B, need, precision=args.precision,
-                       schedule=args.schedule, n_buffers=2)
+                       schedule=args.schedule, n_buffers=2, n_groups=args.groups)
     stream = torch.cuda.current_stream()
     launches = [0]
 

@@ -1015,6 +1015,7 @@ struct OtflmPlan {
     bool has_big = false;              // nodes for k_expand_big (expb_min < cap <= EXPB_MAX)
     uint32_t expb_min = EXPB_MIN;      // (OTFLM_EXPAND_BIG_MIN / OTFLM_ASSIGN_BIG: test overrides of the thresholds)
     uint32_t asg_big = ASSIGN_BIG;
+    bool hs_tc = true;                 // EXACT level schedule: digit-plane HS (OTFLM_HS_TC=0: float64 CUDA cores)
     bool big_asg = false;              // a (level, stream) range above ASSIGN_BIG requests: k_asg_* assign
     uint32_t ch_cap = 0;               // chunk entries of the multi-CTA assign (max over levels)
     uint64_t total_req = 0;
@@ -1290,6 +1291,7 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     OtflmPlan *p = new OtflmPlan();
     if (const char *e = getenv("OTFLM_EXPAND_BIG_MIN")) p->expb_min = (uint32_t)strtoul(e, nullptr, 10);
     if (const char *e = getenv("OTFLM_ASSIGN_BIG")) p->asg_big = (uint32_t)strtoul(e, nullptr, 10);
+    if (const char *e = getenv("OTFLM_HS_TC")) p->hs_tc = atoi(e) != 0;
     p->st = st;
     p->beam = beam;
     p->n_utt = L->n_utt;
@@ -1514,7 +1516,27 @@ static int enqueue_stage2(OtflmPlan *p, const DevModel &m, DevStreams &S, uint32
     CK(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
     {
         ProfScope ps(K_HS, p->side);
-        if (m.H % 4 == 0 && m.H <= 1024) {
+        // EXACT: the digit-plane HS on the tensor cores (exact_solo.cuh k_hs_exact)
+        const bool hs_tc = prec == OTFLM_PREC_EXACT && m.Wd && m.NVd && m.H % 64 == 0 && m.H <= 512 && p->hs_tc;
+        if (hs_tc) {
+            const int ord = m.order <= 3 ? 3 : OTF_MAX_ORDER;
+            const size_t smem = xs1::smem_bytes(ord);
+            const size_t stride = 2 * xu::xs_slot_bytes(m.wd_nkx);
+            const unsigned grid = (unsigned)std::max<uint32_t>(1, std::min<uint32_t>(148, (R + xu::XR - 1) / xu::XR));
+            uint8_t *scratch = nullptr;
+            if (cudaMallocAsync(&scratch, stride * grid, p->side) != cudaSuccess) {
+                g_detail = "cudaMallocAsync exact HS scratch"; return OTFLM_ERR_NOMEM;
+            }
+#define HX_LAUNCH(ORD)                                                                                          \
+            do {                                                                                                \
+                CK(cudaFuncSetAttribute(k_hs_exact<ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+                k_hs_exact<ORD><<<grid, sd::NT, smem, p->side>>>(m, d, S, rs, scratch, stride);                \
+            } while (0)
+            if (ord == 3) HX_LAUNCH(3); else HX_LAUNCH(OTF_MAX_ORDER);
+#undef HX_LAUNCH
+            CKL();
+            CK(cudaFreeAsync(scratch, p->side));
+        } else if (m.H % 4 == 0 && m.H <= 1024) {
             // persistent TMA-ring warps: enough CTAs for the level, at most the
             // resident capacity of the GPU
             const size_t smem = 4 * ring_bytes_per_warp(m.H);
