@@ -641,7 +641,12 @@ def run_config_e(args):
             requests += int(out["expansions"][:n].sum())
             d2h += int(sum(v.nbytes for v in out.values()))
             if record:
-                recs.append(parallel.pack_records(sel_, {k: v[:n] for k, v in out.items()}, args.frames))
+                o = {k: v[:n] for k, v in out.items()}
+                arcs = np.full((n, args.frames), -1)       # per-utterance arc ids (out holds batch-global ids)
+                for i, h in enumerate(hyps[:n]):
+                    arcs[i, :min(len(h.arcs), args.frames)] = h.arcs[:args.frames]
+                o["path_arcs"] = arcs
+                recs.append(parallel.pack_records(sel_, o, args.frames))
         for sel_, lats_ in batches:
             s_cur = dec.prepare(lats_, base.beam)         # host compile + pinned H2D (overlaps the previous decode)
             e0 = torch.cuda.Event(enable_timing=True)

@@ -1,3 +1,2 @@
 set -u
-timeout 900 python tools/sched_e.py > gpurun_out/sched_e.jsonl 2> gpurun_out/sched_e.err
-OTFLM_HS_TC=0 timeout 900 python tools/sched_e.py > gpurun_out/sched_e_f64.jsonl 2>> gpurun_out/sched_e.err
+timeout 900 python -m pytest tests/test_gpu_multirank.py -x -q 2>&1 | tail -15 > gpurun_out/mr_tests.log
