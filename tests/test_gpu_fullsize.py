@@ -97,6 +97,19 @@ def test_bench_config_e_batch_exact_stream():
     _assert_exact(rows)
 
 
+def test_bench_config_e_full_batch_exact_solo():
+    """Exactly one batch of the benched path: utterance ids 0..147 of the
+    bench's config-e workload (its per-id lattices, 300 frames), decoded by
+    k_decode_solo (the automatic choice for a 148-stream EXACT batch, as in
+    bench.py) -- every observable identical to the oracle for all 148."""
+    from paper_2007_11794_b200 import synth
+    base = synth.build_setup("e", n_utt=1, T=300, seed=31)
+    base.lattices = synth.lattices_for_ids(base, range(148), 300)
+    dec, rows = _compare(base, 8, "exact")
+    assert dec.schedule == "stream1"
+    _assert_exact(rows)
+
+
 @pytest.mark.parametrize("config,n_utt,seed", [("b", 64, 7), ("c", 8, 17)])
 def test_full_size_tf32x3_stream_vs_oracle(config, n_utt, seed):
     """The bench's throughput mode (TF32X3 recurrent update on tcgen05,
