@@ -197,9 +197,10 @@ int otflm_streams_cache_get(OtflmStreams *s, int32_t sid, int64_t n, const uint3
 int otflm_streams_cache_put(OtflmStreams *s, int32_t sid, int64_t n, const uint32_t *c_host,
                             const int32_t *w_host, const double *p_host, const uint32_t *c_next_host,
                             void *stream);
-/* RescoreCache.roll_stats (cache.py:155-157): window counters into the
- * cumulative ones; RescoreCache.clear (cache.py:121-125): drop every entry of
- * the stream's cache, counters kept.  Unbounded caches only (as get / put). */
+/* RescoreCache.roll_stats (cache.py:156-158): window counters into the
+ * cumulative ones; RescoreCache.clear (cache.py:136-140): drop every entry of
+ * the stream's cache, counters kept.  Also on a capacity-bounded cache: roll moves
+ * the window's evictions too, clear also empties the LFU policy state. */
 int otflm_streams_roll_stats(OtflmStreams *s, int32_t sid, void *stream);
 int otflm_streams_cache_clear(OtflmStreams *s, int32_t sid, void *stream);
 /* RescoreCache capacity (cache.py:61-137): capacity_bytes > 0 bounds the

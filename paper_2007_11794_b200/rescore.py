@@ -245,12 +245,12 @@ class RescoreCache:
         return CacheValue(float(p[0]), int(cn[0])) if found[0] else None
 
     def clear(self) -> None:
-        """cache.py:121-125: drop every entry; counters are kept."""
+        """cache.py:136-140: drop every entry (and, when bounded, the LFU state); counters are kept."""
         if self._bind is not None:
             self._bind.streams.cache_clear(0)
 
     def roll_stats(self) -> None:
-        """cache.py:155-157: the window counters move into the cumulative ones."""
+        """cache.py:156-158: the window counters (and evictions) move into the cumulative ones."""
         if self._bind is not None:
             self._bind.streams.roll_stats(0)
 
