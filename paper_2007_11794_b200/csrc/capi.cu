@@ -1016,6 +1016,7 @@ struct OtflmPlan {
     uint32_t expb_min = EXPB_MIN;      // (OTFLM_EXPAND_BIG_MIN / OTFLM_ASSIGN_BIG: test overrides of the thresholds)
     uint32_t asg_big = ASSIGN_BIG;
     bool hs_tc = true;                 // EXACT level schedule: digit-plane HS (OTFLM_HS_TC=0: float64 CUDA cores)
+    bool lvl_fused = true;             // ... fused with the update in one kernel (OTFLM_LEVEL_FUSED=0: two kernels)
     bool big_asg = false;              // a (level, stream) range above ASSIGN_BIG requests: k_asg_* assign
     uint32_t ch_cap = 0;               // chunk entries of the multi-CTA assign (max over levels)
     uint64_t total_req = 0;
@@ -1292,6 +1293,7 @@ extern "C" int otflm_plan_create(OtflmStreams *st, const OtflmLatticeBatch *L, i
     if (const char *e = getenv("OTFLM_EXPAND_BIG_MIN")) p->expb_min = (uint32_t)strtoul(e, nullptr, 10);
     if (const char *e = getenv("OTFLM_ASSIGN_BIG")) p->asg_big = (uint32_t)strtoul(e, nullptr, 10);
     if (const char *e = getenv("OTFLM_HS_TC")) p->hs_tc = atoi(e) != 0;
+    if (const char *e = getenv("OTFLM_LEVEL_FUSED")) p->lvl_fused = atoi(e) != 0;
     p->st = st;
     p->beam = beam;
     p->n_utt = L->n_utt;
@@ -1512,6 +1514,33 @@ extern "C" int otflm_plan_counters(const OtflmPlan *p, int64_t *o, void *stream)
 static int enqueue_stage2(OtflmPlan *p, const DevModel &m, DevStreams &S, uint32_t R, int prec,
                           const RowSpec &rs, cudaStream_t s) {
     DevPlan &d = p->d;
+    if (prec == OTFLM_PREC_EXACT && m.Wd && m.NVd && m.H % 64 == 0 && m.H <= 512 && p->hs_tc && p->lvl_fused &&
+        (R + xu::XR - 1) / xu::XR > 148) {
+        // EXACT, a level of more 80-request chunks than SMs: HS + recurrent
+        // update in one persistent kernel (exact_solo.cuh k_level_exact,
+        // k_decode_solo's chunk body: one digitize, no second kernel holding
+        // SMs).  Smaller levels keep the two kernels side by side, which
+        // halves the level's latency (HS and update of a chunk on two SMs).
+        ProfScope ps(K_ADVANCE, s);
+        const int ord = m.order <= 3 ? 3 : OTF_MAX_ORDER;
+        const size_t smem = xs1::smem_bytes(ord);
+        const size_t stride = 2 * xu::xs_slot_bytes(m.wd_nkx);
+        const unsigned grid = (unsigned)std::max<uint32_t>(1, std::min<uint32_t>(148, (R + xu::XR - 1) / xu::XR));
+        uint8_t *scratch = nullptr;
+        if (cudaMallocAsync(&scratch, stride * grid, s) != cudaSuccess) {
+            g_detail = "cudaMallocAsync exact level scratch"; return OTFLM_ERR_NOMEM;
+        }
+#define LX_LAUNCH(ORD)                                                                                          \
+        do {                                                                                                    \
+            CK(cudaFuncSetAttribute(k_level_exact<ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+            k_level_exact<ORD><<<grid, sd::NT, smem, s>>>(m, d, S, rs, scratch, stride);                     \
+        } while (0)
+        if (ord == 3) LX_LAUNCH(3); else LX_LAUNCH(OTF_MAX_ORDER);
+#undef LX_LAUNCH
+        CKL();
+        CK(cudaFreeAsync(scratch, s));
+        return OTFLM_OK;
+    }
     CK(cudaEventRecord(p->ev_fork, s));
     CK(cudaStreamWaitEvent(p->side, p->ev_fork, 0));
     {

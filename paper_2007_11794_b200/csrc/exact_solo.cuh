@@ -284,3 +284,100 @@ k_hs_exact(DevModel m, DevPlan P, DevStreams S, RowSpec rs, uint8_t *xscratch, s
     __syncthreads();
     if (wid == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
 }
+
+// --------------------------------------------------------------------------
+// The whole computed-request stage of an EXACT level in one persistent kernel
+// (level schedule): per 80-request chunk of the level, k_decode_solo's chunk
+// body -- digitize the chunk's context rows once, the digit-plane HS GEMM,
+// then the certified recurrent update over every M tile with the HS tail
+// (MaxEnt, log-sigmoid, path sums, successor history + digest) on warps 2..
+// under the first tile's K loop and each tile's row stores under the next.
+// Replaces k_hs_exact + k_advance_exact (one digitize instead of two, no
+// second kernel holding SMs).
+// --------------------------------------------------------------------------
+template <int ORD>
+__global__ void __launch_bounds__(sd::NT, 1)
+k_level_exact(DevModel m, DevPlan P, DevStreams S, RowSpec rs, uint8_t *xscratch, size_t xs_stride) {
+    using namespace tc;
+    constexpr int NT = sd::NT;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bar_full[4], bar_empty[4], bar_done;
+    __shared__ uint32_t s_tmem;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int wid = __shfl_sync(0xffffffffu, tid >> 5, 0);
+    const uint32_t n = rs.n_dev ? *rs.n_dev : 0u;
+    const uint32_t base = row_base(rs);
+    if (rs.cur && blockIdx.x == 0 && tid == 0) rs.cur->base = base;
+    if ((uint64_t)base + n > rs.row_limit) {
+        if (blockIdx.x == 0 && tid == 0) atomicOr(S.err, OTF_E_ARENA_FULL);
+        return;
+    }
+    const uint32_t nch = (n + xu::XR - 1) / xu::XR;
+    if (blockIdx.x >= nch) return;
+    const int nmt = (m.H + BM - 1) / BM;
+    uint8_t *tables = smem + xh::ring_bytes();
+    uint8_t *small = tables + ((xs1::tables_bytes(ORD) + 127u) & ~127u);
+    constexpr xs1::Small sl = xs1::small_layout();
+    if (tid == 0) {
+        for (int st = 0; st < 4; st++) {           // [0, 2): HS ring, [2, 4): update ring
+            mbar_init(smem_u32(&bar_full[st]), st < xh::STAGES ? xh::GT + 1 : 1);
+            mbar_init(smem_u32(&bar_empty[st]), 1);
+        }
+        mbar_init(smem_u32(&bar_done), 1);
+        reinterpret_cast<uint32_t *>(small + sl.fbn)[0] = 0u;
+        reinterpret_cast<uint32_t *>(small + sl.fbn)[1] = 0u;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < 32) reinterpret_cast<double *>(small + sl.tab)[tid] = exp2((double)tid / 32.0);
+    if (wid == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" :: "r"(smem_u32(&s_tmem)), "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = s_tmem;
+    const xh::Smem hs = xh::carve(smem, ORD);
+    DevPlan Q = P;
+    xu::Ring rg;
+    rg.smem = smem; rg.stages = xh::STAGES; rg.tmem = tmem;
+    rg.full = bar_full + xh::STAGES; rg.empty = bar_empty + xh::STAGES; rg.done = &bar_done;
+    rg.fb = reinterpret_cast<uint32_t *>(tables + xh::layout(ORD).hkey);
+    rg.us = reinterpret_cast<float *>(tables);
+    rg.sh = reinterpret_cast<double *>(small + sl.sh);
+    rg.eh = reinterpret_cast<double *>(small + sl.eh);
+    rg.fb_n = reinterpret_cast<uint32_t *>(small + sl.fbn);
+    rg.src = reinterpret_cast<int32_t *>(small + sl.src);
+    rg.wrd = reinterpret_cast<int32_t *>(small + sl.wrd);
+    rg.tab = reinterpret_cast<const double *>(small + sl.tab);
+    rg.xs = xscratch + (size_t)blockIdx.x * xs_stride;
+    rg.xs_slot = xu::xs_slot_bytes(m.wd_nkx);
+    rg.hin = S.arena_h; rg.hout = S.arena_h + (size_t)base * m.H;
+    rg.in_row = Q.pr_inrow; rg.words = Q.pr_w; rg.dig = Q.pr_dig; rg.alg = Q.alg;
+    rg.dig_store = nullptr; rg.deh_store = nullptr; rg.dep_store = nullptr; rg.epoch = 0;
+    uint32_t gctr_h = 0, gctr_u = 0, tiles_done = 0;
+    unsigned long long t0 = 0;
+    auto wait = [](uint32_t b, uint32_t par, int tag) { sd::wait_bounded(b, par, tag); };
+    int local = 0;
+    for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x, local++) {
+        const uint32_t q0 = c * xu::XR;
+        const int nq = (int)min((uint32_t)xu::XR, n - q0);
+        xu::update_chunk<NT>(m, q0, nq, local, rg, gctr_u, tiles_done, tid, wid, lane, wait,
+                             []() { __syncthreads(); }, nullptr, t0, 0, 0, true);
+        if (tid < NT - 64) xh::setup<ORD, NT - 64>(m, Q, S, q0, nq, hs, tid, lane);
+        __syncthreads();
+        xh::run<ORD, NT>(m, Q, S, base, q0, nq, rg.xs + (size_t)(local & 1) * rg.xs_slot,
+                         rg.eh + (local & 1) * xu::XR, smem, hs, tmem, bar_full, bar_empty, &bar_done, gctr_h,
+                         tiles_done, tid, wid, lane, wait, [](int, int) {}, nullptr, t0, /*defer_finish=*/true);
+        xu::Ring rgc = rg;
+        rgc.eh = rg.eh + (local & 1) * xu::XR;
+        xu::update_chunk<NT>(m, q0, nq, local, rgc, gctr_u, tiles_done, tid, wid, lane, wait,
+                             []() {}, nullptr, t0, 0, nmt, false,
+                             [&](int ft, int fn) { xh::finish<ORD>(m, Q, S, base, q0, nq, hs, ft, fn, 5); },
+                             /*side_uses_us=*/true);
+        __syncthreads();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (wid == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(512));
+}
