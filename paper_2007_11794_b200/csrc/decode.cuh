@@ -500,19 +500,33 @@ __global__ void __launch_bounds__(EXPB_T) k_expand_big(DevPlan P, DevStreams S, 
     __syncthreads();
     const uint32_t n_win = s_nwin;
     const uint32_t n_kept = (uint32_t)min((long long)n_win, beam);
-    // rank = winners ahead in (score desc, ctx asc) -- contexts are distinct among winners
-    for (uint32_t k = tid; k < n_win; k += EXPB_T) {
-        const double sk = w_sc[k];
-        const uint32_t ck = w_ct[k];
-        uint32_t rank = 0;
-        for (uint32_t j = 0; j < n_win; j++) {
-            const double sj = w_sc[j];
-            rank += (sj > sk || (sj == sk && w_ct[j] < ck)) ? 1u : 0u;
+    // rank = winners ahead in (score desc, ctx asc) -- contexts are distinct
+    // among winners, so the order is total: a bitonic sort of the winner list
+    // (padded to a power of two with -inf) puts winner of rank r at position r
+    uint32_t N = 2;
+    while (N < n_win) N <<= 1;
+    for (uint32_t i = n_win + tid; i < N; i += EXPB_T) { w_sc[i] = -__longlong_as_double(0x7FF0000000000000LL); w_ct[i] = OTF_UNSET; w_i[i] = 0u; }
+    __syncthreads();
+    for (uint32_t k = 2; k <= N; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = tid; i < N; i += EXPB_T) {
+                const uint32_t l = i ^ j;
+                if (l <= i) continue;
+                const double si = w_sc[i], sl = w_sc[l];
+                const uint32_t ci = w_ct[i], cl = w_ct[l];
+                const bool l_first = sl > si || (sl == si && cl < ci);      // l ranks ahead of i
+                const bool i_first = si > sl || (si == sl && ci < cl);
+                if ((i & k) == 0 ? l_first : i_first) {
+                    w_sc[i] = sl; w_sc[l] = si; w_ct[i] = cl; w_ct[l] = ci;
+                    const uint32_t t2 = w_i[i]; w_i[i] = w_i[l]; w_i[l] = t2;
+                }
+            }
+            __syncthreads();
         }
-        if (rank < n_kept) {
-            t_sc[rank] = sk; t_ct[rank] = ck; t_slot[rank] = nd.slot_base + w_i[k];
-            if (P.kept) P.kept[nd.slot_base + w_i[k]] = 1;
-        }
+    }
+    for (uint32_t r = tid; r < n_kept; r += EXPB_T) {
+        t_sc[r] = w_sc[r]; t_ct[r] = w_ct[r]; t_slot[r] = nd.slot_base + w_i[r];
+        if (P.kept) P.kept[nd.slot_base + w_i[r]] = 1;
     }
     __syncthreads();
     // one thread per (rank, arc) request, as expand_node
