@@ -654,13 +654,35 @@ __global__ void __launch_bounds__(128) k_hs_prim_ring(DevModel m, DevPlan P, Dev
 // --------------------------------------------------------------------------
 // stage 3: per-stream ordered resolution + finish
 // --------------------------------------------------------------------------
+// full-content comparison of two arena rows (bit patterns of h, history
+// meta) by one thread; 16-byte loads, 8 of them in flight per trip, from L2
+// (rows written earlier in the same kernel by other warps or CTAs)
 __device__ __forceinline__ bool rows_equal_lane(const DevStreams &S, uint32_t ra, uint32_t rb) {
     const float *a = S.arena_h + (size_t)ra * S.H, *b = S.arena_h + (size_t)rb * S.H;
-    for (int i = 0; i < S.H; i++)
-        if (__float_as_uint(a[i]) != __float_as_uint(b[i])) return false;
-    for (int i = 0; i < OTF_META; i++)
-        if (S.arena_meta[(size_t)ra * OTF_META + i] != S.arena_meta[(size_t)rb * OTF_META + i]) return false;
-    return true;
+    if ((S.H & 3) == 0) {
+        const uint4 *a4 = reinterpret_cast<const uint4 *>(a), *b4 = reinterpret_cast<const uint4 *>(b);
+        const int n4 = S.H >> 2;
+        for (int i = 0; i < n4; i += 4) {
+            uint4 x[4], y[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                x[k] = make_uint4(0u, 0u, 0u, 0u); y[k] = x[k];
+                if (i + k < n4) { x[k] = __ldcg(a4 + i + k); y[k] = __ldcg(b4 + i + k); }
+            }
+            bool eq = true;
+#pragma unroll
+            for (int k = 0; k < 4; k++) eq &= x[k].x == y[k].x && x[k].y == y[k].y && x[k].z == y[k].z && x[k].w == y[k].w;
+            if (!eq) return false;
+        }
+    } else {
+        for (int i = 0; i < S.H; i++)
+            if (__float_as_uint(__ldcg(a + i)) != __float_as_uint(__ldcg(b + i))) return false;
+    }
+    const uint4 *ma = reinterpret_cast<const uint4 *>(S.arena_meta + (size_t)ra * OTF_META);
+    const uint4 *mb = reinterpret_cast<const uint4 *>(S.arena_meta + (size_t)rb * OTF_META);
+    const uint4 p0 = __ldcg(ma), p1 = __ldcg(ma + 1), q0 = __ldcg(mb), q1 = __ldcg(mb + 1);
+    return p0.x == q0.x && p0.y == q0.y && p0.z == q0.z && p0.w == q0.w &&
+           p1.x == q1.x && p1.y == q1.y && p1.z == q1.z && p1.w == q1.w;
 }
 
 // MODE 0: decode (finish requests into arrival slots)
