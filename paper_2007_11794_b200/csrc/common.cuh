@@ -166,9 +166,14 @@ __device__ __forceinline__ double otf_sigmoid(double x) {
 // comparison, so the term only needs to spread well): one 64-bit multiply of
 // a 32-bit mix of (i, bits).
 __device__ __forceinline__ unsigned long long otf_dig_h(uint32_t i, float x) {
-    const uint32_t k = (__float_as_uint(x) ^ (i * 0x9E3779B9u)) * 0x85EBCA6Bu;
-    const uint64_t v = ((uint64_t)k << 32 | (uint64_t)(i + 0x27D4EB2Fu)) * 0xff51afd7ed558ccdull;
-    return v ^ (v >> 29);
+    // one full 64-bit mix (fmix64) of (element index, float bits): whenever an
+    // element changes -- even by one ulp -- the digest sum moves by an
+    // unrelated 64-bit value.  (A cheaper multiply + xorshift term let the
+    // +-1 ulp changes of two elements cancel exactly: a real collision on the
+    // fat variant between two rows 1 ulp apart in 2 of 256 elements.)  Element
+    // indices stay below 0x10000, so these terms never coincide with the
+    // history terms (dig_meta).
+    return otf_hash64(((uint64_t)i << 32) | (uint64_t)__float_as_uint(x));
 }
 
 __device__ __forceinline__ double shfl_xor_d(double v, int m) {

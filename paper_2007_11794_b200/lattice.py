@@ -252,14 +252,21 @@ def generate_lattice(reference: Sequence[int], vocab_size: int, small_lm, confus
     pool = np.nonzero(~special)[0]
     n_alt = min(b - 1, n_pool - 1)
     for t in range(T):
-        chosen = []
-        while len(chosen) < n_alt:
-            x = int(pool[rng.integers(0, len(pool))])
-            if x != reference[t] and x not in chosen:
-                chosen.append(x)
-        cand[t, 1:1 + n_alt] = chosen
-        if n_alt:
-            cac[t, 1:1 + n_alt] = -np.abs(rng.normal(1.0, 0.5, size=n_alt))
+        # the reference's draw (lattice.py:147-156): rng.choice over the pool
+        # without the reference word, then one N(1, 0.5) per chosen word --
+        # the same generator calls on index arithmetic instead of an O(V)
+        # list per position, so the lattices are byte-identical to the
+        # reference's generate_lattice for the same seed
+        p_ref = int(np.searchsorted(pool, reference[t]))
+        in_pool = p_ref < len(pool) and int(pool[p_ref]) == reference[t]
+        n_alts = len(pool) - (1 if in_pool else 0)
+        k_alt = min(b - 1, n_alts)
+        if k_alt:
+            i = rng.choice(n_alts, size=k_alt, replace=False)
+            if in_pool:
+                i = i + (i >= p_ref)
+            cand[t, 1:1 + k_alt] = pool[i]
+            cac[t, 1:1 + k_alt] = -np.abs(rng.normal(1.0, 0.5, size=k_alt))
     bb = 1 + n_alt
     cand, cac = cand[:, :bb], cac[:, :bb]
     k = max(small_lm.order - 1, 0)

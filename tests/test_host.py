@@ -100,3 +100,30 @@ def test_product_has_no_oracle_dependency():
     for p in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu*")):
         text = p.read_text()
         assert "oracle" not in text.lower().replace("no cpu fallback", ""), p
+
+
+def test_lattice_generator_matches_reference_generator(golden):
+    """The vectorised synthetic-lattice generator (the bench's input builder)
+    is the reference's generate_lattice (lattice.py:130-183) draw for draw:
+    same arcs (src, dst, word, acoustic, small-LM score), start and finals for
+    bigram and trigram small LMs and breadths 1-8 (tests/golden/lattices.npz,
+    made by tests/golden/make_golden_lattices.py from the reference)."""
+    from paper_2007_11794_b200.lattice import generate_lattice
+    from paper_2007_11794_b200.model import ngram_from_arrays
+    d = golden("lattices")
+    V = int(d["V"])
+    for p in d["cases"]:
+        p = str(p)
+        o = p[:3]
+        lm = ngram_from_arrays(*(d[f"{o}ng_{k}"] for k in ("order", "V", "bos", "eos", "pk", "pl", "pv",
+                                                            "bk", "bl", "bv")))
+        lat = generate_lattice([int(w) for w in d[p + "ref"]], V, lm, int(d[p + "breadth"]),
+                               int(d[p + "seed"]))
+        arcs = sorted(lat.arcs, key=lambda a: a.id)
+        assert lat.start == int(d[p + "start"]), p
+        assert sorted(lat.finals) == [int(x) for x in d[p + "finals"]], p
+        assert [a.src for a in arcs] == [int(x) for x in d[p + "src"]], p
+        assert [a.dst for a in arcs] == [int(x) for x in d[p + "dst"]], p
+        assert [a.word for a in arcs] == [int(x) for x in d[p + "word"]], p
+        assert np.array_equal(np.array([a.acoustic for a in arcs]), d[p + "ac"]), p
+        assert np.allclose(np.array([a.smalllm for a in arcs]), d[p + "slm"], rtol=0, atol=1e-12), p
