@@ -605,18 +605,27 @@ def run_config_e(args):
         lat_parts = pool.map(_e_lattices, parts)
     lat_all = [l for part in lat_parts for l in part]
     batches = [(ids[b0:b0 + B], lat_all[b0:b0 + B]) for b0 in range(0, len(ids), B)]
-    # a short last batch is padded with repeats of its own utterances (decoded,
-    # not counted) so every batch has the same compiled structure and the
-    # plans are refreshed in place instead of rebuilt
-    sel, lats = batches[-1]
-    if len(lats) < B and len(batches) > 1:
-        pad = [lats[i % len(lats)] for i in range(B - len(lats))]
-        batches[-1] = (sel, lats + pad)
     t_gen = time.perf_counter() - t0
     torch.cuda.set_device(local)
+    n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+    # a short last batch: with at most half an SM per stream short of a full
+    # wave it gets its own decoder (the automatic schedule then gives each of
+    # its streams a 2-CTA cluster, ~1.5x faster per stream than one CTA);
+    # otherwise it is padded with repeats of its own utterances (decoded, not
+    # counted) so every batch has the same compiled structure and the plans
+    # are refreshed in place instead of rebuilt
+    sel, lats = batches[-1]
+    tail_dec = None
+    if len(lats) < B and len(batches) > 1:
+        if args.schedule == "auto" and 2 * len(lats) <= n_sm:
+            tail_dec = BatchDecoder(base.model, base.tree, base.small_lm, len(lats),
+                                    BatchDecoder.contexts_needed(lats, base.beam), precision=args.precision)
+        else:
+            pad = [lats[i % len(lats)] for i in range(B - len(lats))]
+            batches[-1] = (sel, lats + pad)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    need = max(BatchDecoder.contexts_needed(l, base.beam) for _, l in batches)
+    need = max(BatchDecoder.contexts_needed(l, base.beam) for _, l in (batches[:-1] if tail_dec else batches))
     dec = BatchDecoder(base.model, base.tree, base.small_lm, B, need, precision=args.precision,
                        schedule=args.schedule, n_buffers=2, n_groups=args.groups)
     stream = torch.cuda.current_stream()
@@ -633,9 +642,9 @@ def run_config_e(args):
         evs = []
         h2d = d2h = 0
 
-        def take(slot, sel_):
+        def take(d_, slot, sel_):
             nonlocal frames, requests, misses, d2h
-            hyps, out = dec.fetch(slot=slot)
+            hyps, out = d_.fetch(slot=slot)
             n = len(sel_)
             frames += int(sum(len(h.arcs) for h in hyps[:n]))
             requests += int(out["expansions"][:n].sum())
@@ -647,19 +656,21 @@ def run_config_e(args):
                     arcs[i, :min(len(h.arcs), args.frames)] = h.arcs[:args.frames]
                 o["path_arcs"] = arcs
                 recs.append(parallel.pack_records(sel_, o, args.frames))
-        for sel_, lats_ in batches:
-            s_cur = dec.prepare(lats_, base.beam)         # host compile + pinned H2D (overlaps the previous decode)
+        d_prev = None
+        for bi, (sel_, lats_) in enumerate(batches):
+            d_cur = tail_dec if (tail_dec is not None and bi == len(batches) - 1) else dec
+            s_cur = d_cur.prepare(lats_, base.beam)       # host compile + pinned H2D (overlaps the previous decode)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            dec.run(1.0, slot=s_cur)
+            d_cur.run(1.0, slot=s_cur)
             e1.record(stream)
             launches[0] += last_launch_count()
             evs.append((e0, e1))
             if s_prev is not None:
-                take(s_prev, prev_sel)
-            s_prev, prev_sel = s_cur, sel_
-        take(s_prev, prev_sel)
+                take(d_prev, s_prev, prev_sel)
+            s_prev, prev_sel, d_prev = s_cur, sel_, d_cur
+        take(d_prev, s_prev, prev_sel)
         b.record(stream)
         torch.cuda.synchronize()
         dev_ms = sum(x.elapsed_time(y) for x, y in evs)
@@ -759,6 +770,8 @@ def run_config_e(args):
                                    f"frames sharded over {world} GPU(s), batches of {B} streams, breadth 3, beam 8",
                        "n_utt_total": n_total, "batch_streams": B, "precision": args.precision,
                        "schedule": dec.schedule, "lattice_generation_s": round(t_gen, 2),
+                       "tail_batch": (f"{len(batches[-1][0])} streams, own decoder, schedule {tail_dec.schedule}"
+                                      if tail_dec is not None else "padded to the batch size"),
                        "l2": "inputs (4096 lattices, arenas, 280 MB of weights) far larger than L2; not flushed"},
             "rtf": (dev_ms / 1e3) / (total_frames * FRAME_S),
             "rtf_per_stream": (dev_ms / 1e3) / n_batches / (args.frames * FRAME_S),
